@@ -1,0 +1,169 @@
+// ORACLE HARNESS — test infrastructure only.
+//
+// extern "C" entry points over the reference library (corosim, compiled
+// unmodified from /root/reference/proj/src by oracle/Makefile into
+// oracle/_ref/libcorosim_ref.so).  Used by tests/test_oracle_ref.py to pin the
+// restatements (oracle/numlab.py, oracle/cnumlab.c) and by bench.py's
+// reference arm / cpu_baseline leg to time the reference simulator.
+#include "corosim/engine/engine.hpp"
+#include "corosim/io/metrics.hpp"
+#include "corosim/io/scenario.hpp"
+#include "corosim/numlab/equivalence.hpp"
+#include "corosim/numlab/float_format.hpp"
+#include "corosim/numlab/reduction.hpp"
+#include "corosim/rational.hpp"
+
+#include <json.hpp>
+
+#include <chrono>
+#include <cstring>
+#include <string>
+
+using namespace corosim;
+
+namespace {
+
+std::string fv_str(const FloatValue& v) {
+    switch (v.cls) {
+        case FloatValue::Cls::Finite:
+            return numerator(v.value).str() + "/" + denominator(v.value).str();
+        case FloatValue::Cls::PosInf: return "inf";
+        case FloatValue::Cls::NegInf: return "-inf";
+        case FloatValue::Cls::NaN: return "nan";
+    }
+    return "?";
+}
+
+int put(const std::string& s, char* out, long cap) {
+    if (!out || cap <= 0) return -1;
+    if (static_cast<long>(s.size()) + 1 > cap) return -2;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+FloatFormatKind kind_of(int fmt) {
+    return fmt == 0 ? FloatFormatKind::FP16 : fmt == 1 ? FloatFormatKind::BF16 : FloatFormatKind::FP32;
+}
+
+}  // namespace
+
+extern "C" {
+
+// reduction_result (equivalence.cpp:19-25) as "num/den" | "inf" | "-inf" | "nan"
+int ref_reduction_result(unsigned long long seed, long long n, int fmt, long long grid, char* out,
+                         long cap) {
+    try {
+        ReductionSpec spec{n, seed, kind_of(fmt)};
+        return put(fv_str(reduction_result(spec, grid)), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+// seeded_values (equivalence.cpp:7-17): value i as "num/den"
+int ref_seeded_value(unsigned long long seed, long long n, int fmt, long long i, char* out, long cap) {
+    auto v = seeded_values(seed, n, kind_of(fmt));
+    if (i < 0 || i >= n) return 1;
+    return put(fv_str(v[static_cast<std::size_t>(i)]), out, cap);
+}
+
+// round_to (float_format.cpp:43-67) on an exact rational num/den
+int ref_round_to(int fmt, const char* num, const char* den, char* out, long cap) {
+    try {
+        BigInt bn{std::string(num)};
+        BigInt bd{std::string(den)};
+        Rational r(bn, bd);
+        return put(fv_str(round_to(FloatFormat::of(kind_of(fmt)), r)), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+// reduce_with_plan over explicit values given as exact decimal lines with
+// balanced(n, g) bounds; tree != 0 selects combine_tree.
+int ref_reduce_values(int fmt, const char* values_nl, long long n, long long g, int tree, char* out,
+                      long cap) {
+    try {
+        std::vector<FloatValue> vals;
+        const char* p = values_nl;
+        for (long long i = 0; i < n; ++i) {
+            const char* e = std::strchr(p, '\n');
+            std::string tok = e ? std::string(p, e - p) : std::string(p);
+            vals.push_back(FloatValue::finite(rational_from_decimal(tok)));
+            p = e ? e + 1 : p + tok.size();
+        }
+        ReductionPlan plan = ReductionPlan::balanced(n, g);
+        plan.tree_combine = tree != 0;
+        return put(fv_str(reduce_with_plan(vals, FloatFormat::of(kind_of(fmt)), plan)), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+// Runs scenario_from_json + SimEngine::simulate + compute_metrics and returns
+// a JSON document {metrics, wall_ns, events, transcripts, logical_progress}.
+int ref_simulate_json(const char* scenario_json, char* out, long cap) {
+    try {
+        auto cfg = nlohmann::json::parse(scenario_json);
+        Scenario s = scenario_from_json(cfg, ".");
+        auto t0 = std::chrono::steady_clock::now();
+        SimulationReport rep = SimEngine::simulate(s);
+        auto t1 = std::chrono::steady_clock::now();
+        MetricsReport m = compute_metrics(rep);
+        nlohmann::ordered_json j;
+        j["metrics"] = metrics_to_json(m);
+        j["wall_ns"] = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+        j["events"] = rep.events_processed;
+        j["kernels_completed"] = rep.kernels_completed;
+        nlohmann::ordered_json tr;
+        for (const auto& [vid, sigs] : rep.vctx_transcripts) {
+            nlohmann::ordered_json arr = nlohmann::ordered_json::array();
+            for (const auto& sig : sigs) arr.push_back({sig.semantic_id, sig.grid_size});
+            tr[std::to_string(vid.value)] = arr;
+        }
+        j["transcripts"] = tr;
+        nlohmann::ordered_json lp;
+        for (const auto& [vid, p] : rep.logical_progress) lp[std::to_string(vid.value)] = p;
+        j["logical_progress"] = lp;
+        nlohmann::ordered_json pre = nlohmann::ordered_json::array();
+        for (const auto& pr : rep.preemptions) {
+            pre.push_back({{"vctx", pr.vctx.value},
+                           {"pctx", pr.pctx.value},
+                           {"signal", to_decimal_string(pr.signal_time)},
+                           {"boundary_wait", to_decimal_string(pr.boundary_wait)},
+                           {"overhead", to_decimal_string(pr.overhead)}});
+        }
+        j["preemptions"] = pre;
+        j["policy_errors"] = rep.policy_errors;
+        return put(j.dump(), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+// check_immutable_equivalence (equivalence.cpp:56-95)
+int ref_equivalence_json(const char* scenario_json, char* out, long cap) {
+    try {
+        auto cfg = nlohmann::json::parse(scenario_json);
+        Scenario s = scenario_from_json(cfg, ".");
+        auto t0 = std::chrono::steady_clock::now();
+        EquivalenceResult r = check_immutable_equivalence(s);
+        auto t1 = std::chrono::steady_clock::now();
+        nlohmann::ordered_json j;
+        j["equivalent"] = r.equivalent;
+        j["transcripts_match"] = r.transcripts_match;
+        j["reductions_match"] = r.reductions_match;
+        j["max_delta"] = numerator(r.max_delta).str() + "/" + denominator(r.max_delta).str();
+        j["wall_ns"] = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+        return put(j.dump(), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+}  // extern "C"
