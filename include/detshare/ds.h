@@ -1,0 +1,224 @@
+/*
+ * detshare B200 GPU-coroutine runtime — C ABI (the drop-in boundary).
+ *
+ * Plain C types only: no torch, no C++ types, no exceptions across the ABI.
+ * Every entry point returns a ds_status (0 = ok).  Status codes 1..10 follow
+ * the reference's Errc order (proj/include/corosim/errors.hpp:8-19); codes
+ * >= 100 are runtime/CUDA conditions the CPU reference never had.
+ *
+ * Reference interfaces each group replaces (file:line under /root/reference/proj):
+ *   domain/pool     create_pool, Device, QuotaTier     include/corosim/core/types.hpp:19-21,102-109,133-137
+ *   tenants         JobSpec -> VirtualContext          include/corosim/engine/engine.hpp:43-48; core/types.hpp:80-88
+ *   kernels         immutable Kernel record            include/corosim/core/types.hpp:29-68
+ *   launch          kernel arrival -> pending queue    src/engine/engine.cpp:810-819 (on_arrival)
+ *   bind/unbind     BindingTable, bind, unbind         include/corosim/core/types.hpp:112-131; src/core/types.cpp:62-85
+ *   preempt         signal_preempt / rck_flag          src/engine/engine.cpp:756-806; core/types.hpp:97
+ *   migrate         begin_migration (remap)            src/engine/engine.cpp:620-672
+ *   transcript      SimulationReport.vctx_transcripts  include/corosim/engine/engine.hpp:124-129
+ *   solo baseline   exclusive_baseline                 src/engine/engine.cpp:1400-1417
+ *   policy engine   SimEngine + Policy hooks           include/corosim/engine/engine.hpp:152-170; policy/policy.hpp:97-126
+ */
+#ifndef DETSHARE_DS_H
+#define DETSHARE_DS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_ABI_VERSION 1
+#define DS_MAX_TENANTS 64
+#define DS_MAX_SMS 256
+#define DS_MASK_WORDS 8 /* 8 x 32 bits = 256 SM slots */
+
+typedef enum ds_status {
+    DS_OK = 0,
+    /* Errc (errors.hpp:8-19), same order */
+    DS_INVALID_TIER = 1,
+    DS_BIND_CONFLICT = 2,
+    DS_DOUBLE_BIND = 3,
+    DS_CAUSALITY_VIOLATION = 4,
+    DS_EVENT_BUDGET_EXCEEDED = 5,
+    DS_TRACE_VIOLATION = 6,
+    DS_PLAN_MISMATCH = 7,
+    DS_INVALID_SPLIT = 8,
+    DS_PARSE_ERROR = 9,
+    DS_CONFIG_ERROR = 10,
+    /* runtime conditions */
+    DS_CUDA_ERROR = 100,
+    DS_NO_DEVICE = 101,
+    DS_NOT_RUNNING = 102,
+    DS_TIMEOUT = 103,
+    DS_RING_FULL = 104,
+    DS_INVALID_ARGUMENT = 105,
+    DS_ALREADY_RUNNING = 106
+} ds_status;
+
+/* Tenant bodies compiled into the executor ("unmodified kernels": each is a
+ * device function of the logical block index, also launchable solo as a
+ * plain __global__ grid). */
+typedef enum ds_body_id {
+    DS_BODY_NONE = 0,
+    DS_BODY_REDUCE_CHUNKS = 1,  /* block c folds chunk c (reduction.cpp:22-34) */
+    DS_BODY_REDUCE_COMBINE = 2, /* grid 1: fold partials left-to-right (reduction.cpp:67-70) */
+    DS_BODY_SGEMM = 3,          /* fp32 C = A.B, 64x64 tiles, k-ascending fma */
+    DS_BODY_SPIN = 4,           /* test body: busy-wait ns per block, writes (smid, t) */
+    DS_BODY_GEMV_BF16 = 5,      /* decode projection: y[32,N] = x[32,K] W^T (+fused epilogue) */
+    DS_BODY_ATTN_DECODE = 6,    /* GQA decode attention over a KV cache */
+    DS_BODY_GEMM_BF16 = 7,      /* training GEMM on tcgen05/TMEM */
+    DS_BODY_RMSNORM = 8,        /* row RMS statistics for the decode tenant */
+    DS_BODY_COUNT = 9
+} ds_body_id;
+
+typedef enum ds_priority { DS_LATENCY_CRITICAL = 0, DS_BEST_EFFORT = 1 } ds_priority; /* types.hpp:24 */
+typedef enum ds_phase { DS_PREFILL = 0, DS_DECODE = 1, DS_TRAINING = 2, DS_OTHER = 3 } ds_phase; /* types.hpp:23 */
+
+typedef struct ds_domain ds_domain;
+
+typedef struct ds_domain_config {
+    int device;                /* CUDA ordinal */
+    int n_tiers;               /* pool: one pctx per tier (create_pool, types.cpp:87-106) */
+    int64_t tier_num[16];      /* tier fraction = num/den in (0, 1] */
+    int64_t tier_den[16];
+    int ring_capacity;         /* launches in flight per tenant (power of two, <= 4096) */
+    int block_log_capacity;    /* logical-block claim log entries (0 = off) */
+    int lend_idle_sms;         /* 1: unbound SMs run best-effort tenants' blocks until reclaimed */
+    int executor_smem;         /* dynamic smem per worker CTA (bytes); 0 = default */
+} ds_domain_config;
+
+typedef struct ds_tenant_desc {
+    const char* name;
+    int priority; /* ds_priority */
+} ds_tenant_desc;
+
+typedef struct ds_kernel_desc {
+    const char* semantic_id; /* KernelSignature.semantic_id (types.hpp:29-34) */
+    int body;                /* ds_body_id */
+    uint32_t grid_x, grid_y, grid_z; /* logical grid; grid_size = product */
+    uint32_t block_threads;  /* <= 256 */
+    const void* args;        /* host pointer to the body's POD argument struct (copied) */
+    uint32_t args_size;      /* <= 512 */
+    int phase;               /* ds_phase */
+    int64_t request;         /* request id for metrics, -1 if none */
+    int decode_index;        /* 0-based decode step within a request, -1 otherwise */
+} ds_kernel_desc;
+
+typedef struct ds_completion {
+    int32_t tenant;
+    int32_t kernel;          /* registered kernel id */
+    uint64_t seq;            /* per-tenant launch sequence number (program order) */
+    uint64_t launch_tag;     /* caller tag passed to ds_launch */
+    uint32_t grid;           /* executed grid size */
+    uint32_t sms_used;       /* distinct SMs that ran >= 1 block */
+    uint64_t t_first_claim;  /* %globaltimer ns */
+    uint64_t t_end;          /* %globaltimer ns (last block retired) */
+} ds_completion;
+
+typedef struct ds_block_record {
+    int32_t tenant;
+    uint32_t seq;
+    uint32_t block;
+    uint16_t smid;
+    uint16_t flags;
+    uint64_t t_start;
+    uint64_t t_end;
+} ds_block_record;
+
+typedef struct ds_switch_record { /* an SM changing tenant at a block boundary */
+    uint16_t smid;
+    int16_t from_tenant;      /* -1 = idle */
+    int16_t to_tenant;        /* -1 = idle */
+    uint16_t pad;
+    uint32_t ctl_gen;         /* control generation in force */
+    uint64_t t;               /* %globaltimer ns */
+} ds_switch_record;
+
+typedef struct ds_ctl_record { /* control-word change observed on the device */
+    uint32_t ctl_gen;
+    uint32_t source;          /* 0 host mailbox, 1 claim trigger, 2 time trigger */
+    uint64_t t;
+} ds_ctl_record;
+
+typedef struct ds_stats {
+    uint64_t launches_enqueued;
+    uint64_t launches_completed;
+    uint64_t blocks_executed;
+    uint64_t ctl_changes;
+    uint64_t switches;
+    uint64_t block_log_entries;
+    uint64_t block_log_dropped;
+    uint32_t num_sms;
+    uint32_t running;
+} ds_stats;
+
+/* ---- errors ---- */
+const char* ds_status_name(int status);
+const char* ds_last_error(void); /* thread-local detail for the last failing call */
+int ds_abi_version(void);
+
+/* ---- domain / pool ---- */
+int ds_domain_create(const ds_domain_config* cfg, ds_domain** out);
+int ds_domain_destroy(ds_domain* dom);
+int ds_num_sms(ds_domain* dom, int* out);
+int ds_smids(ds_domain* dom, int* out, int cap, int* n); /* physical %smid of each worker slot */
+int ds_pctx_count(ds_domain* dom, int* out);
+int ds_pctx_info(ds_domain* dom, int pctx, int64_t* tier_num, int64_t* tier_den, int* n_sms, int* bound_tenant);
+
+/* ---- registration (immutable records) ---- */
+int ds_tenant_register(ds_domain* dom, const ds_tenant_desc* desc, int* tenant_id);
+int ds_kernel_register(ds_domain* dom, const ds_kernel_desc* desc, int* kernel_id);
+
+/* ---- executor lifecycle ---- */
+int ds_start(ds_domain* dom);
+int ds_stop(ds_domain* dom);
+
+/* ---- launches (program order per tenant; "kernel resumes, never restarts") ---- */
+int ds_launch(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, uint64_t* seq);
+/* negative-control mutant (engine.hpp:68-71): executed grid = max(1, floor(grid * tier)) */
+int ds_launch_atomized(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, int64_t tier_num,
+                       int64_t tier_den, uint64_t* seq);
+int ds_wait_tenant(ds_domain* dom, int tenant, uint64_t seq, int timeout_ms); /* until seq completed */
+int ds_poll(ds_domain* dom, ds_completion* out, int cap, int* n);
+
+/* ---- arbiter: pctx binding and raw SM quota ---- */
+int ds_bind(ds_domain* dom, int tenant, int pctx);
+int ds_unbind(ds_domain* dom, int tenant);
+int ds_migrate(ds_domain* dom, int tenant, int dst_pctx);
+int ds_preempt(ds_domain* dom, int pctx); /* revoke at the next logical-block boundary */
+int ds_bound_pctx(ds_domain* dom, int tenant, int* pctx);
+/* raw control word: SM slot i (0..num_sms-1) runs owner[i] first, then lender[i]
+ * when the owner has no claimable block; -1 = none */
+int ds_quota_set(ds_domain* dom, const int32_t* owner, const int32_t* lender, int n);
+int ds_quota_get(ds_domain* dom, int32_t* owner, int32_t* lender, int n);
+int ds_set_lend(ds_domain* dom, int lend_tenant); /* tenant allowed on idle SMs (-1 none) */
+/* device-side control program: when tenant's launch `seq` has claimed `block`
+ * blocks, install owner/lender (n entries).  Used for exact mid-kernel
+ * quota changes (config 1) and the migration sweep (config 3). */
+int ds_quota_at_claim(ds_domain* dom, int tenant, uint64_t seq, uint32_t block, const int32_t* owner,
+                      const int32_t* lender, int n);
+/* periodic device-timer flips between two control words (period ns, 0 = off) */
+int ds_quota_periodic(ds_domain* dom, uint64_t period_ns, const int32_t* owner_a, const int32_t* lender_a,
+                      const int32_t* owner_b, const int32_t* lender_b, int n);
+
+/* ---- observation ---- */
+int ds_stats_get(ds_domain* dom, ds_stats* out);
+int ds_transcript(ds_domain* dom, int tenant, int32_t* kernel_ids, uint32_t* grids, int cap, int* n);
+int ds_logical_progress(ds_domain* dom, int tenant, int64_t* out);
+int ds_block_log(ds_domain* dom, ds_block_record* out, int64_t cap, int64_t* n);
+int ds_switch_log(ds_domain* dom, ds_switch_record* out, int64_t cap, int64_t* n);
+int ds_ctl_log(ds_domain* dom, ds_ctl_record* out, int64_t cap, int64_t* n);
+int ds_clear_logs(ds_domain* dom);
+int ds_globaltimer(ds_domain* dom, uint64_t* ns); /* device %globaltimer now (probe kernel) */
+int ds_debug_dump(ds_domain* dom, char* out, int64_t cap); /* text snapshot of device control state */
+
+/* ---- solo baseline: the same body as a plain __global__ grid (exclusive_baseline) ---- */
+int ds_solo_launch(int device, const ds_kernel_desc* desc, void* stream);
+int ds_solo_launch_registered(ds_domain* dom, int kernel_id, void* stream);
+int ds_body_smem(int body, uint32_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DETSHARE_DS_H */

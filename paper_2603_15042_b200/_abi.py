@@ -1,0 +1,223 @@
+"""ctypes binding of the C ABI in include/detshare/ds.h (libdetshare.so).
+
+This is the reference-side binding a Python maintainer would add (see
+INTEGRATION.md); the product path is the native library.  There is no CPU
+fallback: if the library or a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+
+DS_MAX_TENANTS = 64
+DS_MAX_SMS = 256
+
+# ds_body_id
+BODY_REDUCE_CHUNKS = 1
+BODY_REDUCE_COMBINE = 2
+BODY_SGEMM = 3
+BODY_SPIN = 4
+BODY_GEMV_BF16 = 5
+BODY_ATTN_DECODE = 6
+BODY_GEMM_BF16 = 7
+BODY_RMSNORM = 8
+
+LATENCY_CRITICAL, BEST_EFFORT = 0, 1
+PREFILL, DECODE, TRAINING, OTHER = 0, 1, 2, 3
+
+STATUS = {
+    0: "Ok", 1: "InvalidTier", 2: "BindConflict", 3: "DoubleBind", 4: "CausalityViolation",
+    5: "EventBudgetExceeded", 6: "TraceViolation", 7: "PlanMismatch", 8: "InvalidSplit",
+    9: "ParseError", 10: "ConfigError", 100: "CudaError", 101: "NoDevice", 102: "NotRunning",
+    103: "Timeout", 104: "RingFull", 105: "InvalidArgument", 106: "AlreadyRunning",
+}
+
+
+class DsError(RuntimeError):
+    """Mirror of corosim::SimError (errors.hpp:21-30): carries the status code."""
+
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{STATUS.get(code, 'UnknownError')}: {what}")
+        self.code = code
+
+
+class DomainConfig(ctypes.Structure):
+    _fields_ = [
+        ("device", ctypes.c_int),
+        ("n_tiers", ctypes.c_int),
+        ("tier_num", ctypes.c_int64 * 16),
+        ("tier_den", ctypes.c_int64 * 16),
+        ("ring_capacity", ctypes.c_int),
+        ("block_log_capacity", ctypes.c_int),
+        ("lend_idle_sms", ctypes.c_int),
+        ("executor_smem", ctypes.c_int),
+    ]
+
+
+class TenantDesc(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("priority", ctypes.c_int)]
+
+
+class KernelDesc(ctypes.Structure):
+    _fields_ = [
+        ("semantic_id", ctypes.c_char_p),
+        ("body", ctypes.c_int),
+        ("grid_x", ctypes.c_uint32),
+        ("grid_y", ctypes.c_uint32),
+        ("grid_z", ctypes.c_uint32),
+        ("block_threads", ctypes.c_uint32),
+        ("args", ctypes.c_void_p),
+        ("args_size", ctypes.c_uint32),
+        ("phase", ctypes.c_int),
+        ("request", ctypes.c_int64),
+        ("decode_index", ctypes.c_int),
+    ]
+
+
+class Completion(ctypes.Structure):
+    _fields_ = [
+        ("tenant", ctypes.c_int32),
+        ("kernel", ctypes.c_int32),
+        ("seq", ctypes.c_uint64),
+        ("launch_tag", ctypes.c_uint64),
+        ("grid", ctypes.c_uint32),
+        ("sms_used", ctypes.c_uint32),
+        ("t_first_claim", ctypes.c_uint64),
+        ("t_end", ctypes.c_uint64),
+    ]
+
+
+class BlockRecord(ctypes.Structure):
+    _fields_ = [
+        ("tenant", ctypes.c_int32),
+        ("seq", ctypes.c_uint32),
+        ("block", ctypes.c_uint32),
+        ("smid", ctypes.c_uint16),
+        ("flags", ctypes.c_uint16),
+        ("t_start", ctypes.c_uint64),
+        ("t_end", ctypes.c_uint64),
+    ]
+
+
+class SwitchRecord(ctypes.Structure):
+    _fields_ = [
+        ("smid", ctypes.c_uint16),
+        ("from_tenant", ctypes.c_int16),
+        ("to_tenant", ctypes.c_int16),
+        ("pad", ctypes.c_uint16),
+        ("ctl_gen", ctypes.c_uint32),
+        ("t", ctypes.c_uint64),
+    ]
+
+
+class CtlRecord(ctypes.Structure):
+    _fields_ = [("ctl_gen", ctypes.c_uint32), ("source", ctypes.c_uint32), ("t", ctypes.c_uint64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("launches_enqueued", ctypes.c_uint64),
+        ("launches_completed", ctypes.c_uint64),
+        ("blocks_executed", ctypes.c_uint64),
+        ("ctl_changes", ctypes.c_uint64),
+        ("switches", ctypes.c_uint64),
+        ("block_log_entries", ctypes.c_uint64),
+        ("block_log_dropped", ctypes.c_uint64),
+        ("num_sms", ctypes.c_uint32),
+        ("running", ctypes.c_uint32),
+    ]
+
+
+# ---- body argument structs (POD, mirrors csrc/bodies/*.cuh) ----
+class ReduceArgs(ctypes.Structure):
+    _fields_ = [("inp", ctypes.c_uint64), ("partials", ctypes.c_uint64), ("out", ctypes.c_uint64),
+                ("ticket", ctypes.c_uint64), ("n", ctypes.c_int64), ("fmt", ctypes.c_int32),
+                ("combine", ctypes.c_int32)]
+
+
+class SgemmArgs(ctypes.Structure):
+    _fields_ = [("A", ctypes.c_uint64), ("B", ctypes.c_uint64), ("C", ctypes.c_uint64),
+                ("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class SpinArgs(ctypes.Structure):
+    _fields_ = [("out", ctypes.c_uint64), ("ns", ctypes.c_uint64)]
+
+
+# exported symbols the header declares (checked by the CPU test suite)
+EXPORTS = [
+    "ds_status_name", "ds_last_error", "ds_abi_version", "ds_domain_create", "ds_domain_destroy",
+    "ds_num_sms", "ds_smids", "ds_pctx_count", "ds_pctx_info", "ds_tenant_register", "ds_kernel_register",
+    "ds_start", "ds_stop", "ds_launch", "ds_launch_atomized", "ds_wait_tenant", "ds_poll", "ds_bind",
+    "ds_unbind", "ds_migrate", "ds_preempt", "ds_bound_pctx", "ds_quota_set", "ds_quota_get",
+    "ds_set_lend", "ds_quota_at_claim", "ds_quota_periodic", "ds_stats_get", "ds_transcript",
+    "ds_logical_progress", "ds_block_log", "ds_switch_log", "ds_ctl_log", "ds_clear_logs",
+    "ds_globaltimer", "ds_debug_dump", "ds_solo_launch", "ds_solo_launch_registered", "ds_body_smem",
+]
+
+_lib = None
+
+
+def lib():
+    """Load libdetshare.so (building it in-tree if absent).  Raises if it
+    cannot be loaded — there is no fallback path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            _build.build()
+        L = ctypes.CDLL(LIB_PATH)
+        vp = ctypes.c_void_p
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.ds_status_name.restype = ctypes.c_char_p
+        L.ds_status_name.argtypes = [ctypes.c_int]
+        L.ds_last_error.restype = ctypes.c_char_p
+        L.ds_domain_create.argtypes = [ctypes.POINTER(DomainConfig), ctypes.POINTER(vp)]
+        L.ds_domain_destroy.argtypes = [vp]
+        L.ds_num_sms.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+        L.ds_smids.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.ds_pctx_count.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+        L.ds_pctx_info.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        L.ds_tenant_register.argtypes = [vp, ctypes.POINTER(TenantDesc), ctypes.POINTER(ctypes.c_int)]
+        L.ds_kernel_register.argtypes = [vp, ctypes.POINTER(KernelDesc), ctypes.POINTER(ctypes.c_int)]
+        L.ds_start.argtypes = [vp]
+        L.ds_stop.argtypes = [vp]
+        L.ds_launch.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+        L.ds_launch_atomized.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64)]
+        L.ds_wait_tenant.argtypes = [vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int]
+        L.ds_poll.argtypes = [vp, ctypes.POINTER(Completion), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.ds_bind.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+        L.ds_unbind.argtypes = [vp, ctypes.c_int]
+        L.ds_migrate.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+        L.ds_preempt.argtypes = [vp, ctypes.c_int]
+        L.ds_bound_pctx.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.ds_quota_set.argtypes = [vp, i32p, i32p, ctypes.c_int]
+        L.ds_quota_get.argtypes = [vp, i32p, i32p, ctypes.c_int]
+        L.ds_set_lend.argtypes = [vp, ctypes.c_int]
+        L.ds_quota_at_claim.argtypes = [vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, i32p, i32p, ctypes.c_int]
+        L.ds_quota_periodic.argtypes = [vp, ctypes.c_uint64, i32p, i32p, i32p, i32p, ctypes.c_int]
+        L.ds_stats_get.argtypes = [vp, ctypes.POINTER(Stats)]
+        L.ds_transcript.argtypes = [vp, ctypes.c_int, i32p, ctypes.POINTER(ctypes.c_uint32), ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_int)]
+        L.ds_logical_progress.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_block_log.argtypes = [vp, ctypes.POINTER(BlockRecord), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_switch_log.argtypes = [vp, ctypes.POINTER(SwitchRecord), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_ctl_log.argtypes = [vp, ctypes.POINTER(CtlRecord), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_clear_logs.argtypes = [vp]
+        L.ds_globaltimer.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+        L.ds_debug_dump.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
+        L.ds_solo_launch.argtypes = [ctypes.c_int, ctypes.POINTER(KernelDesc), vp]
+        L.ds_solo_launch_registered.argtypes = [vp, ctypes.c_int, vp]
+        L.ds_body_smem.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise DsError(rc, (lib().ds_last_error() or b"").decode())

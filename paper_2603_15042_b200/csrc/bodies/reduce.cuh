@@ -1,0 +1,94 @@
+// Reduction tenant — the GPU realisation of the reference determinism lab's
+// reduction kernel (reduction_result, src/numlab/equivalence.cpp:19-25).
+//
+// Launched with logical grid g, logical block c folds chunk
+// [c*n/g, (c+1)*n/g) left-to-right seeded with its first element
+// (ReductionPlan::balanced + fold, src/numlab/reduction.cpp:7-34), every add
+// rounded once in the target format with the native RN instruction
+// (add.rn.f16 / add.rn.bf16 / add.rn.f32; no FTZ).  The block that retires
+// last (ticket counter, threadfence pattern) folds the partials left-to-right
+// in chunk order (reduction.cpp:67-70).  The result therefore depends only on
+// (values, format, g) — never on which SM ran which chunk or in what order.
+#pragma once
+#include "common.cuh"
+
+namespace ds {
+
+struct ReduceArgs {
+    uint64_t in;        // n values, raw bits: u16 for fp16/bf16, u32 for fp32
+    uint64_t partials;  // >= g partial bit patterns (u32 each)
+    uint64_t out;       // u32: result bits
+    uint64_t ticket;    // u32 counter, 0 at launch; reset by the last block
+    int64_t n;
+    int32_t fmt;        // 0 fp16, 1 bf16, 2 fp32 (FloatFormatKind order)
+    int32_t combine;    // 1: last block folds partials (full reduction_result)
+};
+
+__device__ __forceinline__ uint32_t add_rn(int fmt, uint32_t a, uint32_t b) {
+    if (fmt == 0) {
+        uint16_t r;
+        asm("add.rn.f16 %0, %1, %2;" : "=h"(r) : "h"((uint16_t)a), "h"((uint16_t)b));
+        return r;
+    } else if (fmt == 1) {
+        uint16_t r;
+        asm("add.rn.bf16 %0, %1, %2;" : "=h"(r) : "h"((uint16_t)a), "h"((uint16_t)b));
+        return r;
+    } else {
+        float r;
+        asm("add.rn.f32 %0, %1, %2;" : "=f"(r) : "f"(__uint_as_float(a)), "f"(__uint_as_float(b)));
+        return __float_as_uint(r);
+    }
+}
+
+__device__ __forceinline__ uint32_t load_val(int fmt, const void* base, int64_t i) {
+    if (fmt == 2) return reinterpret_cast<const uint32_t*>(base)[i];
+    return reinterpret_cast<const uint16_t*>(base)[i];
+}
+
+// smem staging of up to kChunk values; thread 0 folds sequentially
+__device__ void body_reduce(const BodyCtx& c) {
+    const ReduceArgs& a = *reinterpret_cast<const ReduceArgs*>(c.args);
+    const uint32_t g = c.gx * c.gy * c.gz;
+    const uint32_t blk = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int64_t lo = (int64_t)blk * a.n / g;
+    const int64_t hi = (int64_t)(blk + 1) * a.n / g;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(c.smem);
+    const int64_t kChunk = 16384;
+    uint32_t acc = 0;  // FloatValue::finite(0) for an empty chunk (+0 bits)
+    bool first = true;
+    const void* in = reinterpret_cast<const void*>(a.in);
+    for (int64_t base = lo; base < hi; base += kChunk) {
+        int64_t cnt = hi - base < kChunk ? hi - base : kChunk;
+        for (int64_t i = threadIdx.x; i < cnt; i += kBodyThreads) stage[i] = load_val(a.fmt, in, base + i);
+        body_sync();
+        if (threadIdx.x == 0) {
+            int64_t i = 0;
+            if (first) { acc = stage[0]; i = 1; first = false; }
+            for (; i < cnt; ++i) acc = add_rn(a.fmt, acc, stage[i]);
+        }
+        body_sync();
+    }
+    __shared__ int is_last;
+    if (threadIdx.x == 0) {
+        uint32_t* partials = reinterpret_cast<uint32_t*>(a.partials);
+        partials[blk] = acc;
+        is_last = 0;
+        if (a.combine) {
+            __threadfence();
+            uint32_t t = atomicAdd(reinterpret_cast<uint32_t*>(a.ticket), 1u);
+            is_last = (t == g - 1);
+        }
+    }
+    body_sync();
+    if (is_last && threadIdx.x == 0) {
+        __threadfence();
+        const volatile uint32_t* p = reinterpret_cast<const volatile uint32_t*>(a.partials);
+        uint32_t r = p[0];
+        for (uint32_t i = 1; i < g; ++i) r = add_rn(a.fmt, r, p[i]);
+        *reinterpret_cast<uint32_t*>(a.out) = r;
+        *reinterpret_cast<uint32_t*>(a.ticket) = 0;  // ready for the next launch
+    }
+    body_sync();
+}
+
+}  // namespace ds

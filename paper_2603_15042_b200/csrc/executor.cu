@@ -1,0 +1,510 @@
+// Persistent GPU-coroutine executor + SM arbiter (sm_100a).
+//
+// One worker CTA per SM (cooperative launch, 1 CTA/SM forced by shared
+// memory).  Each CTA reads %smid and, at every logical-block boundary, looks
+// up the control word of its SM (owner tenant, then lender tenant), claims the
+// next logical block of that tenant's current launch from the tenant's atomic
+// claim word and runs the tenant's unmodified body on it.  Quota changes
+// (host-written through the mailbox, or device-written by claim/time
+// triggers) therefore take effect only at logical-block boundaries: an SM
+// leaving a tenant finishes its current block first ("yield"), and the
+// tenant's launch keeps its claim word, so it resumes — never restarts —
+// wherever SMs are granted next (reference: signal_preempt /
+// on_preempt_boundary / start_or_resume, src/engine/engine.cpp:756-806,925-984,470-529).
+//
+// Warp roles per CTA (320 threads):
+//   warps 0-7  tenant body (256 threads, body_sync = named barrier 1)
+//   warp 8     scheduler: claim -> stage -> (body runs) -> retire, logs
+//   warp 9     CTA 0 only: loader — polls the host mailbox over PCIe, copies
+//              launch slots into HBM rings, mirrors the control word.
+#include <cuda_runtime.h>
+
+#include "bodies/common.cuh"
+#include "bodies/reduce.cuh"
+#include "bodies/sgemm.cuh"
+#include "ds_device.cuh"
+
+namespace ds {
+
+// ---------------------------------------------------------------------------
+// Body dispatch (shared by the executor and the solo wrapper)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
+    switch (body) {
+        case DS_BODY_REDUCE_CHUNKS: body_reduce(c); break;
+        case DS_BODY_SGEMM: body_sgemm(c); break;
+        case DS_BODY_SPIN: body_spin(c); break;
+        default: break;
+    }
+}
+
+struct Stage {
+    int32_t tenant;   // -1 exit
+    int32_t body;
+    uint32_t seq;
+    uint32_t block;
+    uint32_t gx, gy, gz;
+    uint32_t pad;
+    uint64_t args;
+};
+
+// ---------------------------------------------------------------------------
+// Claim-word protocol
+// ---------------------------------------------------------------------------
+// Open launch `seq` if it is enqueued and its word is still closed.  Called by
+// the completer of seq-1 and by the loader after publishing a new tail (the
+// two sides are ordered by fence.sc, Dekker-style, so one of them opens it).
+__device__ void try_open(DevTenant* T) {
+    for (;;) {
+        unsigned long long w = ld_volatile_u64(&T->claim);
+        uint32_t s = (uint32_t)(w >> 32), b = (uint32_t)w;
+        if (b < kSat) return;
+        uint32_t tail = ld_volatile_u32(&T->tail);
+        if (s >= tail) return;
+        if (atomicCAS(&T->claim, w, (unsigned long long)s << 32) == w) return;
+    }
+}
+
+__device__ void log_ctl(DevState* st, uint32_t gen, uint32_t source) {
+    if (st->clog_cap == 0) return;
+    unsigned long long i = atomicAdd(&st->clog_count, 1ull);
+    if (i < st->clog_cap) {
+        ds_ctl_record r;
+        r.ctl_gen = gen;
+        r.source = source;
+        r.t = globaltimer();
+        st->clog[i] = r;
+    }
+}
+
+// Lane-parallel install of a control word (owner/lender by smid).
+__device__ void install_ctl(DevState* st, const int32_t* owner, const int32_t* lender, bool volatile_src,
+                            uint32_t source, int lane) {
+    for (int i = lane; i < DS_MAX_SMS; i += 32) {
+        int32_t o, l;
+        if (volatile_src) {
+            o = (int32_t)ld_acquire_sys_u32(owner + i);
+            l = (int32_t)ld_acquire_sys_u32(lender + i);
+        } else {
+            o = owner[i];
+            l = lender[i];
+        }
+        st_volatile_u32(&st->ctl.owner[i], (uint32_t)o);
+        st_volatile_u32(&st->ctl.lender[i], (uint32_t)l);
+    }
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) {
+        uint32_t g = atomicAdd(&st->ctl.gen, 1u) + 1u;
+        log_ctl(st, g, source);
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// Loader warp (CTA 0): host mailbox -> HBM
+// ---------------------------------------------------------------------------
+__device__ void loader_loop(DevState* st) {
+    const int lane = threadIdx.x & 31;
+    HostMailbox* mb = st->mailbox;
+    __shared__ uint32_t known_tail[DS_MAX_TENANTS];
+    for (int i = lane; i < DS_MAX_TENANTS; i += 32) known_tail[i] = 0;
+    __syncwarp();
+    uint32_t last_gen = 0, last_pgen = 0;
+    uint64_t period = 0, next_flip = 0;
+    int phase = 0;
+    for (;;) {
+        uint32_t ex = ld_acquire_sys_u32((const void*)&mb->exit);
+        if (ex) {
+            if (lane == 0) {
+                __threadfence();
+                st_volatile_u32(&st->ctl.exit, 1u);
+            }
+            __syncwarp();
+            return;
+        }
+        // new launches
+        for (int base = 0; base < DS_MAX_TENANTS; base += 32) {
+            int t = base + lane;
+            uint32_t ht = ld_acquire_sys_u32((const void*)&mb->tail[t]);
+            uint32_t kt = known_tail[t];
+            unsigned pending = __ballot_sync(0xffffffffu, ht != kt);
+            while (pending) {
+                int src = __ffs(pending) - 1;
+                pending &= pending - 1;
+                int tt = base + src;
+                uint32_t from = __shfl_sync(0xffffffffu, kt, src);
+                uint32_t to = __shfl_sync(0xffffffffu, ht, src);
+                // copy slots [from, to): 16 u32 per slot, 2 slots per warp step
+                for (uint32_t s = from; s < to; s += 2) {
+                    uint32_t my = s + (lane >> 4);
+                    if (my < to) {
+                        uint32_t idx = (uint32_t)tt * (st->ring_mask + 1) + (my & st->ring_mask);
+                        const uint32_t* hs = reinterpret_cast<const uint32_t*>(&st->host_rings[idx]);
+                        uint32_t* ds = reinterpret_cast<uint32_t*>(&st->rings[idx]);
+                        uint32_t v = ld_acquire_sys_u32(hs + (lane & 15));
+                        ds[lane & 15] = v;
+                        __threadfence();
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence();
+                    st_release_u32(&st->tenants[tt].tail, to);
+                    __threadfence();
+                    try_open(&st->tenants[tt]);
+                }
+                __syncwarp();
+                if (lane == src) known_tail[t] = to;
+                __syncwarp();
+            }
+        }
+        // control word
+        uint32_t g = ld_acquire_sys_u32((const void*)&mb->gen);
+        if (g != last_gen) {
+            install_ctl(st, (const int32_t*)mb->owner, (const int32_t*)mb->lender, true, 0, lane);
+            last_gen = g;
+        }
+        // periodic device-timer program (config 3 migration sweep)
+        uint32_t pg = ld_acquire_sys_u32((const void*)&mb->periodic_gen);
+        if (pg != last_pgen) {
+            last_pgen = pg;
+            period = ld_acquire_sys_u64((const void*)&mb->periodic_ns);
+            next_flip = globaltimer() + period;
+            phase = 0;
+        }
+        if (period && globaltimer() >= next_flip) {
+            phase ^= 1;
+            install_ctl(st, (const int32_t*)mb->per_owner[phase], (const int32_t*)mb->per_lender[phase], true, 2,
+                        lane);
+            next_flip += period;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Scheduler warp (every CTA)
+// ---------------------------------------------------------------------------
+struct Claimed {
+    int32_t tenant;
+    uint32_t seq;
+    uint32_t block;
+    LaunchSlot* slot;
+};
+
+__device__ bool try_claim(DevState* st, int t, Claimed& out) {
+    DevTenant* T = &st->tenants[t];
+    unsigned long long w = ld_volatile_u64(&T->claim);
+    uint32_t s = (uint32_t)(w >> 32), b = (uint32_t)w;
+    if (b >= kSat) return false;
+    uint32_t tail = ld_acquire_u32(&T->tail);
+    if (s >= tail) return false;
+    LaunchSlot* slot = &st->rings[(size_t)t * (st->ring_mask + 1) + (s & st->ring_mask)];
+    uint32_t grid = ld_volatile_u32(&slot->grid);
+    if (b >= grid) return false;
+    unsigned long long old = atomicAdd(&T->claim, 1ull);
+    uint32_t s2 = (uint32_t)(old >> 32), b2 = (uint32_t)old;
+    if (b2 >= kSat) return false;
+    if (s2 != s) {
+        // the word advanced between our read and the add: the add landed on
+        // launch s2, which is open (block field < kSat) hence enqueued.
+        slot = &st->rings[(size_t)t * (st->ring_mask + 1) + (s2 & st->ring_mask)];
+        grid = ld_volatile_u32(&slot->grid);
+    }
+    if (b2 >= grid) return false;
+    out.tenant = t;
+    out.seq = s2;
+    out.block = b2;
+    out.slot = slot;
+    return true;
+}
+
+__device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* slot) {
+    DevTenant* T = &st->tenants[t];
+    __threadfence();
+    uint64_t tend = globaltimer();
+    // device -> host completion record
+    unsigned long long i = atomicAdd(&st->completion_count, 1ull);
+    HostCompletion* hc = &st->completions[i & st->completion_mask];
+    ds_completion c;
+    c.tenant = t;
+    c.kernel = ld_volatile_u32(&slot->kernel_id);
+    c.seq = seq;
+    c.launch_tag = ld_volatile_u64(&slot->tag);
+    c.grid = ld_volatile_u32(&slot->grid);
+    c.sms_used = ld_volatile_u32(&slot->sms);
+    c.t_first_claim = ld_volatile_u64(&slot->t_first);
+    c.t_end = tend;
+    hc->c = c;
+    __threadfence_system();
+    st_release_sys_u64((void*)&hc->valid, i + 1);
+    // advance the tenant to seq+1
+    st_release_u32(&T->head, seq + 1);
+    uint32_t nxt = seq + 1;
+    uint32_t tail = ld_acquire_u32(&T->tail);
+    if (nxt < tail) {
+        atomicExch(&T->claim, (unsigned long long)nxt << 32);
+    } else {
+        atomicExch(&T->claim, ((unsigned long long)nxt << 32) | kSat);
+        __threadfence();
+        try_open(T);
+    }
+}
+
+__device__ void maybe_fire_trigger(DevState* st, const Claimed& w, int lane) {
+    uint32_t k = 0;
+    if (lane == 0) k = ld_volatile_u32(&st->trig_next);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= ld_volatile_u32(&st->trig_count)) return;
+    const ClaimTrigger* tr = &st->triggers[k];
+    bool fire = false;
+    if (lane == 0) {
+        if (tr->tenant == w.tenant && tr->seq == w.seq && w.block >= tr->block) {
+            fire = atomicCAS(&st->trig_next, k, k + 1) == k;
+        }
+    }
+    fire = __shfl_sync(0xffffffffu, fire, 0);
+    if (fire) install_ctl(st, tr->owner, tr->lender, false, 1, lane);
+}
+
+__device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, uint32_t sm) {
+    const int lane = threadIdx.x & 31;
+    int32_t last_tenant = -1;
+    uint32_t last_seq = 0xffffffffu;
+    bool idle_logged = false;
+    uint32_t backoff = 32;
+    bool have_prev = false;
+    Claimed prev{};
+    for (;;) {
+        // ---- retire the block the body just finished ----
+        if (have_prev) {
+            named_sync(kBarDone, kBodyThreads + 32);
+            if (lane == 0) {
+                uint64_t t1 = globaltimer();
+                uint64_t t0 = *body_t0;
+                __threadfence();
+                uint32_t r = atomicAdd(&prev.slot->retired, 1u);
+                atomicAdd(&st->blocks_executed, 1ull);
+                if (st->blog_cap) {
+                    unsigned long long i = atomicAdd(&st->blog_count, 1ull);
+                    if (i < st->blog_cap) {
+                        ds_block_record br;
+                        br.tenant = prev.tenant;
+                        br.seq = prev.seq;
+                        br.block = prev.block;
+                        br.smid = (uint16_t)sm;
+                        br.flags = 0;
+                        br.t_start = t0;
+                        br.t_end = t1;
+                        st->blog[i] = br;
+                    }
+                }
+                if (r == ld_volatile_u32(&prev.slot->grid) - 1) complete_launch(st, prev.tenant, prev.seq, prev.slot);
+            }
+            __syncwarp();
+            have_prev = false;
+        }
+        // ---- claim the next block for this SM ----
+        Claimed w{};
+        bool got = false, exit_now = false;
+        if (lane == 0) {
+            for (;;) {
+                if (ld_volatile_u32(&st->ctl.exit)) { exit_now = true; break; }
+                int32_t ow = (int32_t)ld_volatile_u32(&st->ctl.owner[sm]);
+                int32_t ln = (int32_t)ld_volatile_u32(&st->ctl.lender[sm]);
+                if (ow >= 0 && ow < DS_MAX_TENANTS && try_claim(st, ow, w)) { got = true; break; }
+                if (ln >= 0 && ln < DS_MAX_TENANTS && ln != ow && try_claim(st, ln, w)) { got = true; break; }
+                if (!idle_logged && last_tenant != -1 && st->slog_cap) {
+                    unsigned long long i = atomicAdd(&st->slog_count, 1ull);
+                    if (i < st->slog_cap) {
+                        ds_switch_record r;
+                        r.smid = (uint16_t)sm;
+                        r.from_tenant = (int16_t)last_tenant;
+                        r.to_tenant = -1;
+                        r.pad = 0;
+                        r.ctl_gen = ld_volatile_u32(&st->ctl.gen);
+                        r.t = globaltimer();
+                        st->slog[i] = r;
+                    }
+                    idle_logged = true;
+                    last_tenant = -1;
+                }
+                __nanosleep(backoff);
+                if (backoff < 1024) backoff <<= 1;
+            }
+            if (got) {
+                backoff = 32;
+                __threadfence();  // acquire: prior launches' results (and invalidate L1)
+                Stage s;
+                s.tenant = w.tenant;
+                s.body = ld_volatile_u32(&w.slot->body);
+                s.seq = w.seq;
+                s.block = w.block;
+                s.gx = ld_volatile_u32(&w.slot->gx);
+                s.gy = ld_volatile_u32(&w.slot->gy);
+                s.gz = ld_volatile_u32(&w.slot->gz);
+                s.pad = 0;
+                s.args = ld_volatile_u64(&w.slot->args);
+                *stage = s;
+            } else {
+                stage->tenant = -1;
+            }
+        }
+        __syncwarp();
+        named_arrive(kBarFull, kBodyThreads + 32);
+        exit_now = __shfl_sync(0xffffffffu, exit_now, 0);
+        got = __shfl_sync(0xffffffffu, got, 0);
+        if (!got) {  // exit: let the body warps read the exit stage, then leave
+            named_sync(kBarEmpty, kBodyThreads + 32);
+            break;
+        }
+        w.tenant = __shfl_sync(0xffffffffu, w.tenant, 0);
+        w.seq = __shfl_sync(0xffffffffu, w.seq, 0);
+        w.block = __shfl_sync(0xffffffffu, w.block, 0);
+        w.slot = (LaunchSlot*)__shfl_sync(0xffffffffu, (unsigned long long)w.slot, 0);
+        // ---- bookkeeping while the body runs ----
+        if (lane == 0) {
+            if (w.block == 0) w.slot->t_first = globaltimer();
+            if (w.tenant != last_tenant || w.seq != last_seq) {
+                atomicAdd(&w.slot->sms, 1u);
+                if (w.tenant != last_tenant && st->slog_cap) {
+                    unsigned long long i = atomicAdd(&st->slog_count, 1ull);
+                    if (i < st->slog_cap) {
+                        ds_switch_record r;
+                        r.smid = (uint16_t)sm;
+                        r.from_tenant = (int16_t)last_tenant;
+                        r.to_tenant = (int16_t)w.tenant;
+                        r.pad = 0;
+                        r.ctl_gen = ld_volatile_u32(&st->ctl.gen);
+                        r.t = globaltimer();
+                        st->slog[i] = r;
+                    }
+                }
+            }
+            last_tenant = w.tenant;
+            last_seq = w.seq;
+            idle_logged = false;
+        }
+        __syncwarp();
+        maybe_fire_trigger(st, w, lane);
+        named_sync(kBarEmpty, kBodyThreads + 32);  // body copied the stage
+        prev = w;
+        have_prev = true;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Body warps
+// ---------------------------------------------------------------------------
+__device__ void body_loop(Stage* stage, volatile uint64_t* body_t0, char* smem, uint32_t smem_bytes,
+                          uint32_t tmem_base) {
+    for (;;) {
+        named_sync(kBarFull, kBodyThreads + 32);
+        Stage s = *stage;
+        named_arrive(kBarEmpty, kBodyThreads + 32);
+        if (s.tenant < 0) return;
+        if (threadIdx.x == 0) *body_t0 = globaltimer();
+        BodyCtx c;
+        c.gx = s.gx;
+        c.gy = s.gy;
+        c.gz = s.gz;
+        c.bx = s.block % s.gx;
+        c.by = (s.block / s.gx) % s.gy;
+        c.bz = s.block / (s.gx * s.gy);
+        c.args = reinterpret_cast<const void*>(s.args);
+        c.smem = smem;
+        c.smem_bytes = smem_bytes;
+        c.tmem_base = tmem_base;
+        run_body(s.body, c);
+        __threadfence();  // this thread's writes visible at gpu scope before retire
+        named_arrive(kBarDone, kBodyThreads + 32);
+    }
+}
+
+extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel(DevState* st, uint32_t smem_bytes) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ Stage stage;
+    __shared__ volatile uint64_t body_t0;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t sm = smid();
+    if (warp == kLoaderWarp) {
+        if (blockIdx.x == 0) loader_loop(st);
+        return;
+    }
+    if (warp == kSchedWarp) {
+        scheduler_loop(st, &stage, &body_t0, sm);
+    } else {
+        body_loop(&stage, &body_t0, smem, smem_bytes, 0);
+    }
+}
+
+// Solo baseline: the same body as a plain grid (exclusive_baseline,
+// src/engine/engine.cpp:1400-1417).  256 threads, blockIdx = logical block.
+extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
+    ds_solo_kernel(int body, const void* args, uint32_t gx, uint32_t gy, uint32_t gz, uint32_t smem_bytes) {
+    extern __shared__ __align__(1024) char smem[];
+    uint32_t b = blockIdx.x;
+    BodyCtx c;
+    c.gx = gx;
+    c.gy = gy;
+    c.gz = gz;
+    c.bx = b % gx;
+    c.by = (b / gx) % gy;
+    c.bz = b / (gx * gy);
+    c.args = args;
+    c.smem = smem;
+    c.smem_bytes = smem_bytes;
+    c.tmem_base = 0;
+    run_body(body, c);
+}
+
+extern "C" __global__ void ds_probe_kernel(uint32_t* smids, uint32_t* nsmid, uint64_t* timer) {
+    if (threadIdx.x == 0) {
+        smids[blockIdx.x] = smid();
+        uint32_t n;
+        asm volatile("mov.u32 %0, %%nsmid;" : "=r"(n));
+        if (blockIdx.x == 0) {
+            *nsmid = n;
+            *timer = globaltimer();
+        }
+    }
+}
+
+}  // namespace ds
+
+// host-side launch shims (called from runtime.cpp)
+extern "C" cudaError_t ds_dev_launch_executor(ds::DevState* st, int num_ctas, uint32_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(ds::ds_executor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void* args[] = {&st, &smem};
+    return cudaLaunchCooperativeKernel((void*)ds::ds_executor_kernel, dim3(num_ctas), dim3(ds::kExecThreads), args,
+                                       smem, s);
+}
+
+extern "C" cudaError_t ds_dev_executor_occupancy(uint32_t smem, int* blocks_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(ds::ds_executor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, ds::ds_executor_kernel, ds::kExecThreads, smem);
+}
+
+extern "C" cudaError_t ds_dev_launch_solo(int body, const void* args, uint32_t gx, uint32_t gy, uint32_t gz,
+                                          uint32_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(ds::ds_solo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    ds::ds_solo_kernel<<<dim3(gx * gy * gz), dim3(ds::kBodyThreads), smem, s>>>(body, args, gx, gy, gz, smem);
+    return cudaGetLastError();
+}
+
+extern "C" cudaError_t ds_dev_probe(int nblocks, uint32_t* smids, uint32_t* nsmid, uint64_t* timer, cudaStream_t s) {
+    ds::ds_probe_kernel<<<nblocks, 32, 0, s>>>(smids, nsmid, timer);
+    return cudaGetLastError();
+}
+
+extern "C" uint32_t ds_dev_body_smem(int body) {
+    switch (body) {
+        case DS_BODY_REDUCE_CHUNKS: return 16384 * 4 + 1024;
+        case DS_BODY_SGEMM: return (32 * 68 + 32 * 64) * 4 + 1024;
+        case DS_BODY_SPIN: return 1024;
+        default: return ds::kDefaultSmem;
+    }
+}

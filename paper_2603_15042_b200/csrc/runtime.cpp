@@ -1,0 +1,994 @@
+// Host side of the GPU-coroutine runtime: the C ABI of include/detshare/ds.h.
+//
+// One ds_domain = one GPU sharing domain (the reference's Device with its pctx
+// pool, src/core/types.cpp:87-106).  The host owns registration (immutable
+// kernel records, include/corosim/core/types.hpp:46-68), the pctx pool and the
+// injective binding table (types.cpp:62-85), and writes the SM control word;
+// the device executor (executor.cu) does everything per logical block.
+//
+// Threads: the caller's thread(s) issue API calls (serialised by a mutex); a
+// drainer thread consumes device->host completion records from pinned mapped
+// memory and maintains per-tenant completion state, transcripts and timings.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ds_device.cuh"
+
+extern "C" cudaError_t ds_dev_launch_executor(ds::DevState* st, int num_ctas, uint32_t smem, cudaStream_t s);
+extern "C" cudaError_t ds_dev_executor_occupancy(uint32_t smem, int* blocks_per_sm);
+extern "C" cudaError_t ds_dev_launch_solo(int body, const void* args, uint32_t gx, uint32_t gy, uint32_t gz,
+                                          uint32_t smem, cudaStream_t s);
+extern "C" cudaError_t ds_dev_probe(int nblocks, uint32_t* smids, uint32_t* nsmid, uint64_t* timer, cudaStream_t s);
+extern "C" uint32_t ds_dev_body_smem(int body);
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& why) {
+    g_last_error = why;
+    return status;
+}
+
+#define DS_CUDA(call)                                                                           \
+    do {                                                                                        \
+        cudaError_t _e = (call);                                                                \
+        if (_e != cudaSuccess) return fail(DS_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+struct KernelRecord {
+    std::string semantic_id;
+    int body;
+    uint32_t gx, gy, gz;
+    uint32_t block_threads;
+    uint64_t args_dev;   // device pointer into the arena
+    std::vector<uint8_t> args_host;
+    int phase;
+    int64_t request;
+    int decode_index;
+    uint64_t fingerprint;
+};
+
+struct TenantRecord {
+    std::string name;
+    int priority;
+    uint64_t next_seq = 0;            // launches issued
+    std::atomic<uint64_t> completed{0};  // launches completed (drainer)
+    std::vector<int32_t> launched_kernel;  // by seq
+    std::vector<uint32_t> launched_grid;   // by seq (executed grid)
+    int bound_pctx = -1;
+};
+
+struct Pctx {
+    int64_t num, den;
+    int n_sms;
+    int bound = -1;              // tenant
+    std::vector<int> slots;      // SM slots while bound
+};
+
+}  // namespace
+
+struct ds_domain {
+    int device = 0;
+    int num_sms = 0;
+    std::vector<int> smids;      // physical smid of slot i
+    int nsmid = 0;
+    uint32_t smem = ds::kDefaultSmem;
+    int ring_cap = 1024;
+    int lend_idle = 1;
+    int lend_tenant = -1;
+
+    cudaStream_t exec_stream = nullptr, copy_stream = nullptr;
+    ds::DevState* d_state = nullptr;
+    ds::LaunchSlot* d_rings = nullptr;
+    ds::ClaimTrigger* d_triggers = nullptr;
+    uint8_t* d_args = nullptr;
+    size_t args_cap = 0, args_used = 0;
+    ds_block_record* d_blog = nullptr;
+    ds_switch_record* d_slog = nullptr;
+    ds_ctl_record* d_clog = nullptr;
+    uint64_t blog_cap = 0, slog_cap = 1 << 20, clog_cap = 1 << 16;
+    uint32_t* d_probe = nullptr;
+    uint64_t* d_probe_t = nullptr;
+
+    ds::HostMailbox* mb = nullptr;       // pinned mapped
+    ds::LaunchSlot* h_rings = nullptr;   // pinned mapped
+    ds::HostCompletion* h_comp = nullptr;
+    uint32_t comp_cap = 1 << 18;
+
+    std::vector<KernelRecord> kernels;
+    std::vector<TenantRecord*> tenants;
+    std::vector<Pctx> pctxs;
+    std::vector<int32_t> owner, lender;  // by SM slot
+    int n_triggers = 0;
+
+    std::mutex mu;                 // API serialisation
+    std::mutex comp_mu;            // completions vector
+    std::condition_variable comp_cv;
+    std::vector<ds_completion> completions;  // drained, not yet polled
+    std::vector<std::vector<ds_completion>> per_tenant_done;
+    std::atomic<bool> running{false};
+    std::atomic<bool> drain_stop{false};
+    std::thread drainer;
+    uint64_t comp_next = 0;
+    uint64_t enqueued = 0;
+    std::atomic<uint64_t> completed_total{0};
+};
+
+namespace {
+
+uint64_t fnv_mix(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);  // hash_mix, types.cpp:24-26
+    return h;
+}
+
+void drain_loop(ds_domain* d) {
+    while (!d->drain_stop.load(std::memory_order_acquire)) {
+        bool any = false;
+        for (;;) {
+            ds::HostCompletion* hc = &d->h_comp[d->comp_next & (d->comp_cap - 1)];
+            uint64_t v = hc->valid;
+            if (v != d->comp_next + 1) break;
+            std::atomic_thread_fence(std::memory_order_acquire);
+            ds_completion c = hc->c;
+            d->comp_next++;
+            any = true;
+            {
+                std::lock_guard<std::mutex> g(d->comp_mu);
+                d->completions.push_back(c);
+                if (c.tenant >= 0 && c.tenant < (int)d->per_tenant_done.size())
+                    d->per_tenant_done[c.tenant].push_back(c);
+            }
+            if (c.tenant >= 0 && c.tenant < (int)d->tenants.size())
+                d->tenants[c.tenant]->completed.store(c.seq + 1, std::memory_order_release);
+            d->completed_total.fetch_add(1, std::memory_order_relaxed);
+        }
+        if (any) d->comp_cv.notify_all();
+        else std::this_thread::sleep_for(std::chrono::microseconds(2));
+    }
+}
+
+int push_control(ds_domain* d) {
+    // slot-space owner/lender -> smid-space mailbox, then bump the generation
+    for (int i = 0; i < DS_MAX_SMS; ++i) {
+        d->mb->owner[i] = -1;
+        d->mb->lender[i] = -1;
+    }
+    for (int s = 0; s < d->num_sms; ++s) {
+        int sm = d->smids[s];
+        int32_t o = d->owner[s];
+        int32_t l = d->lender[s];
+        if (d->lend_idle && l < 0 && d->lend_tenant >= 0 && o != d->lend_tenant) l = d->lend_tenant;
+        d->mb->owner[sm] = o;
+        d->mb->lender[sm] = l;
+    }
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    d->mb->gen = d->mb->gen + 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    return DS_OK;
+}
+
+// Choose n free SM slots, preferring whole TPCs (slot pairs with smid 2k,2k+1).
+std::vector<int> pick_slots(ds_domain* d, int n) {
+    std::vector<int> free_slots;
+    for (int s = 0; s < d->num_sms; ++s)
+        if (d->owner[s] < 0) free_slots.push_back(s);
+    std::sort(free_slots.begin(), free_slots.end(), [&](int a, int b) { return d->smids[a] < d->smids[b]; });
+    std::vector<int> out;
+    for (int s : free_slots) {
+        if ((int)out.size() >= n) break;
+        out.push_back(s);
+    }
+    return out;
+}
+
+int check_dom(ds_domain* d) {
+    if (!d) return fail(DS_INVALID_ARGUMENT, "null domain");
+    return DS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ds_status_name(int status) {
+    switch (status) {
+        case DS_OK: return "Ok";
+        case DS_INVALID_TIER: return "InvalidTier";
+        case DS_BIND_CONFLICT: return "BindConflict";
+        case DS_DOUBLE_BIND: return "DoubleBind";
+        case DS_CAUSALITY_VIOLATION: return "CausalityViolation";
+        case DS_EVENT_BUDGET_EXCEEDED: return "EventBudgetExceeded";
+        case DS_TRACE_VIOLATION: return "TraceViolation";
+        case DS_PLAN_MISMATCH: return "PlanMismatch";
+        case DS_INVALID_SPLIT: return "InvalidSplit";
+        case DS_PARSE_ERROR: return "ParseError";
+        case DS_CONFIG_ERROR: return "ConfigError";
+        case DS_CUDA_ERROR: return "CudaError";
+        case DS_NO_DEVICE: return "NoDevice";
+        case DS_NOT_RUNNING: return "NotRunning";
+        case DS_TIMEOUT: return "Timeout";
+        case DS_RING_FULL: return "RingFull";
+        case DS_INVALID_ARGUMENT: return "InvalidArgument";
+        case DS_ALREADY_RUNNING: return "AlreadyRunning";
+    }
+    return "UnknownError";  // errors.cpp:19
+}
+
+const char* ds_last_error(void) { return g_last_error.c_str(); }
+int ds_abi_version(void) { return DS_ABI_VERSION; }
+
+int ds_body_smem(int body, uint32_t* bytes) {
+    if (!bytes || body <= 0 || body >= DS_BODY_COUNT) return fail(DS_INVALID_ARGUMENT, "unknown body");
+    *bytes = ds_dev_body_smem(body);
+    return DS_OK;
+}
+
+int ds_domain_create(const ds_domain_config* cfg, ds_domain** out) {
+    if (!cfg || !out) return fail(DS_INVALID_ARGUMENT, "null config");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(DS_NO_DEVICE, "no CUDA device");
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(DS_NO_DEVICE, "bad device ordinal");
+    if (cfg->n_tiers < 1 || cfg->n_tiers > 16) return fail(DS_INVALID_TIER, "pool needs 1..16 tiers");
+    for (int i = 0; i < cfg->n_tiers; ++i) {
+        // create_pool (types.cpp:87-98): tiers must lie in (0, 1]
+        if (cfg->tier_den[i] <= 0 || cfg->tier_num[i] <= 0 || cfg->tier_num[i] > cfg->tier_den[i])
+            return fail(DS_INVALID_TIER, "tier fraction outside (0, 1]");
+    }
+    int ring = cfg->ring_capacity > 0 ? cfg->ring_capacity : 1024;
+    if ((ring & (ring - 1)) != 0 || ring > 4096) return fail(DS_CONFIG_ERROR, "ring_capacity must be a power of two <= 4096");
+
+    auto* d = new ds_domain();
+    d->device = cfg->device;
+    d->ring_cap = ring;
+    d->lend_idle = cfg->lend_idle_sms;
+    if (cfg->executor_smem > 0) d->smem = (uint32_t)cfg->executor_smem;
+    d->blog_cap = cfg->block_log_capacity > 0 ? (uint64_t)cfg->block_log_capacity : 0;
+    auto bail = [&](int st) {
+        delete d;
+        return st;
+    };
+    if (cudaSetDevice(d->device) != cudaSuccess) return bail(fail(DS_CUDA_ERROR, "cudaSetDevice"));
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, d->device);
+    if (prop.major < 10) return bail(fail(DS_NO_DEVICE, "needs sm_100 (B200)"));
+    d->num_sms = prop.multiProcessorCount;
+    if (d->num_sms > DS_MAX_SMS) return bail(fail(DS_CONFIG_ERROR, "too many SMs"));
+    int occ = 0;
+    if (ds_dev_executor_occupancy(d->smem, &occ) != cudaSuccess || occ != 1)
+        return bail(fail(DS_CONFIG_ERROR, "executor must be exactly 1 CTA/SM (occupancy " + std::to_string(occ) + ")"));
+
+    cudaStreamCreateWithFlags(&d->exec_stream, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
+
+    // probe %smid of each SM (many CTAs, take the distinct set)
+    {
+        int nb = d->num_sms * 8;
+        uint32_t *dsm = nullptr, *dn = nullptr;
+        uint64_t* dt = nullptr;
+        cudaMalloc(&dsm, nb * sizeof(uint32_t));
+        cudaMalloc(&dn, sizeof(uint32_t));
+        cudaMalloc(&dt, sizeof(uint64_t));
+        ds_dev_probe(nb, dsm, dn, dt, d->copy_stream);
+        std::vector<uint32_t> h(nb);
+        uint32_t nsmid = 0;
+        cudaMemcpyAsync(h.data(), dsm, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, d->copy_stream);
+        cudaMemcpyAsync(&nsmid, dn, sizeof(uint32_t), cudaMemcpyDeviceToHost, d->copy_stream);
+        cudaError_t e = cudaStreamSynchronize(d->copy_stream);
+        cudaFree(dsm);
+        cudaFree(dn);
+        cudaFree(dt);
+        if (e != cudaSuccess) return bail(fail(DS_CUDA_ERROR, std::string("probe: ") + cudaGetErrorString(e)));
+        std::sort(h.begin(), h.end());
+        h.erase(std::unique(h.begin(), h.end()), h.end());
+        d->nsmid = (int)nsmid;
+        if ((int)h.size() != d->num_sms || nsmid > DS_MAX_SMS)
+            return bail(fail(DS_CONFIG_ERROR, "smid probe saw " + std::to_string(h.size()) + " SMs, nsmid " +
+                                                  std::to_string(nsmid)));
+        for (uint32_t s : h) d->smids.push_back((int)s);
+    }
+    d->owner.assign(d->num_sms, -1);
+    d->lender.assign(d->num_sms, -1);
+
+    // pool (create_pool): one pctx per tier; SM count = round(tier * num_sms), >= 1
+    for (int i = 0; i < cfg->n_tiers; ++i) {
+        Pctx p;
+        p.num = cfg->tier_num[i];
+        p.den = cfg->tier_den[i];
+        p.n_sms = (int)((p.num * d->num_sms * 2 + p.den) / (2 * p.den));
+        if (p.n_sms < 1) p.n_sms = 1;
+        if (p.n_sms > d->num_sms) p.n_sms = d->num_sms;
+        d->pctxs.push_back(p);
+    }
+
+    // device memory
+    size_t ring_bytes = sizeof(ds::LaunchSlot) * DS_MAX_TENANTS * (size_t)ring;
+    d->args_cap = 8u << 20;
+    if (cudaMalloc(&d->d_state, sizeof(ds::DevState)) != cudaSuccess ||
+        cudaMalloc(&d->d_rings, ring_bytes) != cudaSuccess || cudaMalloc(&d->d_args, d->args_cap) != cudaSuccess ||
+        cudaMalloc(&d->d_triggers, sizeof(ds::ClaimTrigger) * ds::kMaxTriggers) != cudaSuccess ||
+        cudaMalloc(&d->d_slog, sizeof(ds_switch_record) * d->slog_cap) != cudaSuccess ||
+        cudaMalloc(&d->d_clog, sizeof(ds_ctl_record) * d->clog_cap) != cudaSuccess)
+        return bail(fail(DS_CUDA_ERROR, "cudaMalloc"));
+    if (cudaMalloc(&d->d_probe, 16) != cudaSuccess || cudaMalloc(&d->d_probe_t, 8) != cudaSuccess)
+        return bail(fail(DS_CUDA_ERROR, "cudaMalloc probe"));
+    if (d->blog_cap && cudaMalloc(&d->d_blog, sizeof(ds_block_record) * d->blog_cap) != cudaSuccess)
+        return bail(fail(DS_CUDA_ERROR, "cudaMalloc block log"));
+    // host mapped
+    if (cudaHostAlloc(&d->mb, sizeof(ds::HostMailbox), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostAlloc(&d->h_rings, ring_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostAlloc(&d->h_comp, sizeof(ds::HostCompletion) * d->comp_cap,
+                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+        return bail(fail(DS_CUDA_ERROR, "cudaHostAlloc"));
+    std::memset((void*)d->mb, 0, sizeof(ds::HostMailbox));
+    std::memset(d->h_rings, 0, ring_bytes);
+    std::memset(d->h_comp, 0, sizeof(ds::HostCompletion) * d->comp_cap);
+    for (int i = 0; i < DS_MAX_SMS; ++i) {
+        d->mb->owner[i] = -1;
+        d->mb->lender[i] = -1;
+    }
+    *out = d;
+    return DS_OK;
+}
+
+int ds_domain_destroy(ds_domain* d) {
+    if (!d) return DS_OK;
+    if (d->running) ds_stop(d);
+    cudaSetDevice(d->device);
+    cudaFree(d->d_state);
+    cudaFree(d->d_rings);
+    cudaFree(d->d_args);
+    cudaFree(d->d_triggers);
+    cudaFree(d->d_slog);
+    cudaFree(d->d_clog);
+    if (d->d_blog) cudaFree(d->d_blog);
+    cudaFree(d->d_probe);
+    cudaFree(d->d_probe_t);
+    cudaFreeHost((void*)d->mb);
+    cudaFreeHost(d->h_rings);
+    cudaFreeHost(d->h_comp);
+    if (d->exec_stream) cudaStreamDestroy(d->exec_stream);
+    if (d->copy_stream) cudaStreamDestroy(d->copy_stream);
+    for (auto* t : d->tenants) delete t;
+    delete d;
+    return DS_OK;
+}
+
+int ds_num_sms(ds_domain* d, int* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    *out = d->num_sms;
+    return DS_OK;
+}
+
+int ds_smids(ds_domain* d, int* out, int cap, int* n) {
+    if (check_dom(d) || !n) return fail(DS_INVALID_ARGUMENT, "null");
+    int m = std::min(cap, d->num_sms);
+    for (int i = 0; i < m; ++i) out[i] = d->smids[i];
+    *n = d->num_sms;
+    return DS_OK;
+}
+
+int ds_pctx_count(ds_domain* d, int* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    *out = (int)d->pctxs.size();
+    return DS_OK;
+}
+
+int ds_pctx_info(ds_domain* d, int pctx, int64_t* num, int64_t* den, int* n_sms, int* bound) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (pctx < 0 || pctx >= (int)d->pctxs.size()) return fail(DS_INVALID_ARGUMENT, "unknown pctx");
+    const Pctx& p = d->pctxs[pctx];
+    if (num) *num = p.num;
+    if (den) *den = p.den;
+    if (n_sms) *n_sms = p.n_sms;
+    if (bound) *bound = p.bound;
+    return DS_OK;
+}
+
+int ds_tenant_register(ds_domain* d, const ds_tenant_desc* desc, int* tenant_id) {
+    if (check_dom(d) || !desc || !tenant_id) return fail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(d->mu);
+    if ((int)d->tenants.size() >= DS_MAX_TENANTS) return fail(DS_CONFIG_ERROR, "too many tenants");
+    auto* t = new TenantRecord();
+    t->name = desc->name ? desc->name : "";
+    t->priority = desc->priority;
+    d->tenants.push_back(t);
+    {
+        std::lock_guard<std::mutex> g2(d->comp_mu);
+        d->per_tenant_done.emplace_back();
+    }
+    *tenant_id = (int)d->tenants.size() - 1;  // job i => vctx i (engine.cpp:139-145)
+    return DS_OK;
+}
+
+int ds_kernel_register(ds_domain* d, const ds_kernel_desc* k, int* kernel_id) {
+    if (check_dom(d) || !k || !kernel_id) return fail(DS_INVALID_ARGUMENT, "null");
+    if (k->body <= DS_BODY_NONE || k->body >= DS_BODY_COUNT) return fail(DS_CONFIG_ERROR, "unknown body");
+    uint64_t grid = (uint64_t)k->grid_x * k->grid_y * k->grid_z;
+    if (grid < 1 || grid >= ds::kSat) return fail(DS_CONFIG_ERROR, "grid_size must be >= 1");  // engine.cpp:169-171
+    if (k->block_threads != 256) return fail(DS_CONFIG_ERROR, "built-in bodies run 256 threads");
+    if (k->args_size > ds::kMaxArgs || (k->args_size && !k->args)) return fail(DS_CONFIG_ERROR, "args too large");
+    std::lock_guard<std::mutex> g(d->mu);
+    if (d->args_used + ds::kMaxArgs > d->args_cap) return fail(DS_CONFIG_ERROR, "args arena full");
+    KernelRecord r;
+    r.semantic_id = k->semantic_id ? k->semantic_id : "";
+    r.body = k->body;
+    r.gx = k->grid_x;
+    r.gy = k->grid_y;
+    r.gz = k->grid_z;
+    r.block_threads = k->block_threads;
+    r.args_dev = (uint64_t)(d->d_args + d->args_used);
+    r.args_host.assign((const uint8_t*)k->args, (const uint8_t*)k->args + k->args_size);
+    r.phase = k->phase;
+    r.request = k->request;
+    r.decode_index = k->decode_index;
+    // fingerprint over the immutable launch configuration (Kernel::fingerprint, types.cpp:39-48)
+    uint64_t h = 0x811c9dc5ULL;
+    h = fnv_mix(h, r.semantic_id.size());
+    for (unsigned char c : r.semantic_id) h = fnv_mix(h, c);
+    h = fnv_mix(h, grid);
+    h = fnv_mix(h, (uint64_t)r.body);
+    for (uint8_t b : r.args_host) h = fnv_mix(h, b);
+    r.fingerprint = h;
+    if (k->args_size) {
+        cudaSetDevice(d->device);
+        DS_CUDA(cudaMemcpyAsync((void*)r.args_dev, k->args, k->args_size, cudaMemcpyHostToDevice, d->copy_stream));
+        DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    }
+    d->args_used += ds::kMaxArgs;
+    d->kernels.push_back(std::move(r));
+    *kernel_id = (int)d->kernels.size() - 1;
+    return DS_OK;
+}
+
+int ds_start(ds_domain* d) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (d->running) return fail(DS_ALREADY_RUNNING, "executor already running");
+    cudaSetDevice(d->device);
+    ds::DevState h;
+    std::memset(&h, 0, sizeof(h));
+    for (int t = 0; t < DS_MAX_TENANTS; ++t) {
+        uint64_t seq = t < (int)d->tenants.size() ? d->tenants[t]->next_seq : 0;
+        uint64_t done = t < (int)d->tenants.size() ? d->tenants[t]->completed.load() : 0;
+        if (seq != done) return fail(DS_CONFIG_ERROR, "tenant has launches in flight from a previous run");
+        h.tenants[t].claim = ((unsigned long long)seq << 32) | ds::kSat;
+        h.tenants[t].tail = (uint32_t)seq;
+        h.tenants[t].head = (uint32_t)seq;
+        d->mb->tail[t] = (uint32_t)seq;
+    }
+    for (int i = 0; i < DS_MAX_SMS; ++i) {
+        h.ctl.owner[i] = -1;
+        h.ctl.lender[i] = -1;
+    }
+    h.rings = d->d_rings;
+    ds::LaunchSlot* hr = nullptr;
+    ds::HostMailbox* hm = nullptr;
+    ds::HostCompletion* hc = nullptr;
+    DS_CUDA(cudaHostGetDevicePointer((void**)&hr, d->h_rings, 0));
+    DS_CUDA(cudaHostGetDevicePointer((void**)&hm, (void*)d->mb, 0));
+    DS_CUDA(cudaHostGetDevicePointer((void**)&hc, d->h_comp, 0));
+    h.host_rings = hr;
+    h.mailbox = hm;
+    h.completions = hc;
+    h.blog = d->d_blog;
+    h.slog = d->d_slog;
+    h.clog = d->d_clog;
+    h.ring_mask = (uint32_t)d->ring_cap - 1;
+    h.completion_mask = d->comp_cap - 1;
+    h.blog_cap = d->blog_cap;
+    h.slog_cap = d->slog_cap;
+    h.clog_cap = d->clog_cap;
+    h.num_tenants_cap = DS_MAX_TENANTS;
+    h.triggers = d->d_triggers;
+    h.trig_count = 0;
+    h.trig_next = 0;
+    d->n_triggers = 0;
+    // completions restart from index 0
+    std::memset(d->h_comp, 0, sizeof(ds::HostCompletion) * d->comp_cap);
+    d->comp_next = 0;
+    d->mb->exit = 0;
+    d->mb->periodic_ns = 0;
+    d->mb->gen = 0;
+    DS_CUDA(cudaMemcpyAsync(d->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    d->drain_stop = false;
+    d->drainer = std::thread(drain_loop, d);
+    cudaError_t e = ds_dev_launch_executor(d->d_state, d->num_sms, d->smem, d->exec_stream);
+    if (e != cudaSuccess) {
+        d->drain_stop = true;
+        d->drainer.join();
+        return fail(DS_CUDA_ERROR, std::string("executor launch: ") + cudaGetErrorString(e));
+    }
+    d->running = true;
+    push_control(d);
+    return DS_OK;
+}
+
+int ds_stop(ds_domain* d) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (!d->running) return DS_OK;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    d->mb->exit = 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    cudaSetDevice(d->device);
+    // bounded wait: a wedged tenant body must not hang the caller forever
+    cudaError_t e = cudaErrorNotReady;
+    auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(20);
+    while ((e = cudaStreamQuery(d->exec_stream)) == cudaErrorNotReady) {
+        if (std::chrono::steady_clock::now() > deadline) {
+            d->drain_stop = true;
+            d->drainer.join();
+            return fail(DS_TIMEOUT, "executor did not exit within 20 s");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    // drain what is left, then stop the drainer
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    d->drain_stop = true;
+    d->drainer.join();
+    d->running = false;
+    if (e != cudaSuccess) return fail(DS_CUDA_ERROR, std::string("executor: ") + cudaGetErrorString(e));
+    return DS_OK;
+}
+
+static int launch_impl(ds_domain* d, int tenant, int kernel_id, uint64_t tag, uint32_t exec_grid, uint32_t egx,
+                       uint32_t egy, uint32_t egz, uint64_t* seq_out) {
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
+    TenantRecord* t = d->tenants[tenant];
+    const KernelRecord& k = d->kernels[kernel_id];
+    uint64_t seq = t->next_seq;
+    // ring flow control: slot seq % R is free once seq - R completed
+    auto t0 = std::chrono::steady_clock::now();
+    while (seq - t->completed.load(std::memory_order_acquire) >= (uint64_t)d->ring_cap) {
+        if (!d->running) return fail(DS_RING_FULL, "ring full and executor stopped");
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) return fail(DS_RING_FULL, "ring full");
+        std::this_thread::yield();
+    }
+    ds::LaunchSlot& s = d->h_rings[(size_t)tenant * d->ring_cap + (seq & (d->ring_cap - 1))];
+    s.body = k.body;
+    s.grid = exec_grid;
+    s.gx = egx;
+    s.gy = egy;
+    s.gz = egz;
+    s.kernel_id = kernel_id;
+    s.args = k.args_dev;
+    s.tag = tag;
+    s.retired = 0;
+    s.sms = 0;
+    s.t_first = 0;
+    s.seq = (uint32_t)seq;
+    s.flags = 0;
+    t->launched_kernel.push_back(kernel_id);
+    t->launched_grid.push_back(exec_grid);
+    t->next_seq = seq + 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    d->mb->tail[tenant] = (uint32_t)(seq + 1);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    d->enqueued++;
+    if (seq_out) *seq_out = seq;
+    return DS_OK;
+}
+
+int ds_launch(ds_domain* d, int tenant, int kernel_id, uint64_t tag, uint64_t* seq) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
+    const KernelRecord& k = d->kernels[kernel_id];
+    return launch_impl(d, tenant, kernel_id, tag, k.gx * k.gy * k.gz, k.gx, k.gy, k.gz, seq);
+}
+
+// atomized_grid (engine.cpp:26-30): the grid is rewritten to fit the tier.
+int ds_launch_atomized(ds_domain* d, int tenant, int kernel_id, uint64_t tag, int64_t num, int64_t den,
+                       uint64_t* seq) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    if (den <= 0 || num <= 0 || num > den) return fail(DS_INVALID_TIER, "tier outside (0, 1]");
+    std::lock_guard<std::mutex> g(d->mu);
+    if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
+    const KernelRecord& k = d->kernels[kernel_id];
+    uint64_t grid = (uint64_t)k.gx * k.gy * k.gz;
+    int64_t gnew = (int64_t)(grid * (uint64_t)num / (uint64_t)den);
+    if (gnew < 1) gnew = 1;
+    // 1-D rewrite of the logical grid (the mutant breaks the launch config by design)
+    return launch_impl(d, tenant, kernel_id, tag, (uint32_t)gnew, (uint32_t)gnew, 1, 1, seq);
+}
+
+int ds_wait_tenant(ds_domain* d, int tenant, uint64_t seq, int timeout_ms) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    TenantRecord* t = d->tenants[tenant];
+    auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms < 0 ? 1 << 30 : timeout_ms);
+    while (t->completed.load(std::memory_order_acquire) <= seq) {
+        if (!d->running) return fail(DS_NOT_RUNNING, "executor not running");
+        if (std::chrono::steady_clock::now() > deadline) return fail(DS_TIMEOUT, "wait timed out");
+        std::unique_lock<std::mutex> lk(d->comp_mu);
+        d->comp_cv.wait_for(lk, std::chrono::microseconds(200));
+    }
+    return DS_OK;
+}
+
+int ds_poll(ds_domain* d, ds_completion* out, int cap, int* n) {
+    if (check_dom(d) || !n) return fail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(d->comp_mu);
+    int m = std::min<int>(cap, (int)d->completions.size());
+    for (int i = 0; i < m; ++i) out[i] = d->completions[i];
+    d->completions.erase(d->completions.begin(), d->completions.begin() + m);
+    *n = m;
+    return DS_OK;
+}
+
+int ds_quota_set(ds_domain* d, const int32_t* owner, const int32_t* lender, int n) {
+    if (check_dom(d) || n != d->num_sms) return fail(DS_INVALID_ARGUMENT, "control word needs num_sms entries");
+    std::lock_guard<std::mutex> g(d->mu);
+    for (int i = 0; i < n; ++i) {
+        d->owner[i] = owner ? owner[i] : -1;
+        d->lender[i] = lender ? lender[i] : -1;
+    }
+    // raw control bypasses the pctx table: forget bindings
+    for (auto& p : d->pctxs) {
+        if (p.bound >= 0) d->tenants[p.bound]->bound_pctx = -1;
+        p.bound = -1;
+        p.slots.clear();
+    }
+    return push_control(d);
+}
+
+int ds_quota_get(ds_domain* d, int32_t* owner, int32_t* lender, int n) {
+    if (check_dom(d) || n != d->num_sms) return fail(DS_INVALID_ARGUMENT, "control word needs num_sms entries");
+    std::lock_guard<std::mutex> g(d->mu);
+    for (int i = 0; i < n; ++i) {
+        if (owner) owner[i] = d->owner[i];
+        if (lender) lender[i] = d->lender[i];
+    }
+    return DS_OK;
+}
+
+int ds_set_lend(ds_domain* d, int lend_tenant) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    d->lend_tenant = lend_tenant;
+    return push_control(d);
+}
+
+// bind (types.cpp:62-74): BindConflict if the pctx is bound, DoubleBind if the
+// tenant is mapped; spatial feasibility (sum of bound tiers <= 1, engine.cpp:721-725)
+int ds_bind(ds_domain* d, int tenant, int pctx) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    if (pctx < 0 || pctx >= (int)d->pctxs.size()) return fail(DS_INVALID_ARGUMENT, "unknown pctx");
+    Pctx& p = d->pctxs[pctx];
+    if (p.bound >= 0) return fail(DS_BIND_CONFLICT, "pctx " + std::to_string(pctx) + " is bound");
+    if (d->tenants[tenant]->bound_pctx >= 0) return fail(DS_DOUBLE_BIND, "vctx " + std::to_string(tenant) + " is mapped");
+    // exact rational feasibility: sum(num_i/den_i) + p <= 1
+    long double sum = (long double)p.num / p.den;
+    for (const Pctx& q : d->pctxs)
+        if (q.bound >= 0) sum += (long double)q.num / q.den;
+    if (sum > 1.0L + 1e-12L) return fail(DS_CONFIG_ERROR, "bind violates spatial feasibility");
+    std::vector<int> slots = pick_slots(d, p.n_sms);
+    if ((int)slots.size() < p.n_sms) return fail(DS_CONFIG_ERROR, "not enough free SMs");
+    for (int s : slots) d->owner[s] = tenant;
+    p.slots = slots;
+    p.bound = tenant;
+    d->tenants[tenant]->bound_pctx = pctx;
+    return push_control(d);
+}
+
+static int unbind_locked(ds_domain* d, int tenant) {
+    int pc = d->tenants[tenant]->bound_pctx;
+    if (pc < 0) return fail(DS_BIND_CONFLICT, "unbind of a pair that is not bound");  // types.cpp:77-78
+    Pctx& p = d->pctxs[pc];
+    for (int s : p.slots) d->owner[s] = -1;
+    p.slots.clear();
+    p.bound = -1;
+    d->tenants[tenant]->bound_pctx = -1;
+    return DS_OK;
+}
+
+int ds_unbind(ds_domain* d, int tenant) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    int st = unbind_locked(d, tenant);
+    if (st) return st;
+    return push_control(d);
+}
+
+// begin_migration (engine.cpp:620-672) on one GPU: unbind + bind in one
+// control-word change; SMs leaving the tenant yield at their block boundary.
+int ds_migrate(ds_domain* d, int tenant, int dst) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    if (dst < 0 || dst >= (int)d->pctxs.size()) return fail(DS_INVALID_ARGUMENT, "unknown pctx");
+    Pctx& p = d->pctxs[dst];
+    if (p.bound >= 0) return fail(DS_BIND_CONFLICT, "remap to a bound pctx");
+    int src = d->tenants[tenant]->bound_pctx;
+    long double sum = (long double)p.num / p.den;
+    for (int i = 0; i < (int)d->pctxs.size(); ++i)
+        if (d->pctxs[i].bound >= 0 && i != src) sum += (long double)d->pctxs[i].num / d->pctxs[i].den;
+    if (sum > 1.0L + 1e-12L) return fail(DS_CONFIG_ERROR, "remap violates spatial feasibility");
+    std::vector<int> keep;
+    if (src >= 0) {
+        keep = d->pctxs[src].slots;
+        unbind_locked(d, tenant);
+    }
+    // prefer SMs the tenant already holds (no yield needed there)
+    std::vector<int> slots;
+    for (int s : keep)
+        if ((int)slots.size() < p.n_sms) slots.push_back(s);
+    for (int s : slots) d->owner[s] = tenant;
+    if ((int)slots.size() < p.n_sms) {
+        std::vector<int> more = pick_slots(d, p.n_sms - (int)slots.size());
+        for (int s : more) {
+            d->owner[s] = tenant;
+            slots.push_back(s);
+        }
+    }
+    if ((int)slots.size() < p.n_sms) return fail(DS_CONFIG_ERROR, "not enough free SMs");
+    p.slots = slots;
+    p.bound = tenant;
+    d->tenants[tenant]->bound_pctx = dst;
+    return push_control(d);
+}
+
+// signal_preempt (engine.cpp:756-806): the bound tenant loses the pctx's SMs
+// at its next logical-block boundary; its launch stays paused in its claim word.
+int ds_preempt(ds_domain* d, int pctx) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (pctx < 0 || pctx >= (int)d->pctxs.size()) return fail(DS_INVALID_ARGUMENT, "unknown pctx");
+    Pctx& p = d->pctxs[pctx];
+    if (p.bound < 0) return DS_OK;  // preempting an unbound pctx is a no-op (engine.cpp:738-746)
+    unbind_locked(d, p.bound);
+    return push_control(d);
+}
+
+int ds_bound_pctx(ds_domain* d, int tenant, int* pctx) {
+    if (check_dom(d) || !pctx) return fail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(d->mu);
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    *pctx = d->tenants[tenant]->bound_pctx;
+    return DS_OK;
+}
+
+int ds_quota_at_claim(ds_domain* d, int tenant, uint64_t seq, uint32_t block, const int32_t* owner,
+                      const int32_t* lender, int n) {
+    if (check_dom(d) || n != d->num_sms) return fail(DS_INVALID_ARGUMENT, "control word needs num_sms entries");
+    std::lock_guard<std::mutex> g(d->mu);
+    if (d->n_triggers >= ds::kMaxTriggers) return fail(DS_CONFIG_ERROR, "trigger table full");
+    std::vector<ds::ClaimTrigger> one(1);
+    ds::ClaimTrigger& tr = one[0];
+    tr.tenant = tenant;
+    tr.seq = (uint32_t)seq;
+    tr.block = block;
+    for (int i = 0; i < DS_MAX_SMS; ++i) {
+        tr.owner[i] = -1;
+        tr.lender[i] = -1;
+    }
+    for (int s = 0; s < n; ++s) {
+        tr.owner[d->smids[s]] = owner ? owner[s] : -1;
+        tr.lender[d->smids[s]] = lender ? lender[s] : -1;
+    }
+    cudaSetDevice(d->device);
+    DS_CUDA(cudaMemcpyAsync(d->d_triggers + d->n_triggers, &tr, sizeof(tr), cudaMemcpyHostToDevice, d->copy_stream));
+    d->n_triggers++;
+    uint32_t cnt = (uint32_t)d->n_triggers;
+    DS_CUDA(cudaMemcpyAsync(&d->d_state->trig_count, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    // the host mirror follows the last installed trigger
+    for (int s = 0; s < n; ++s) {
+        d->owner[s] = owner ? owner[s] : -1;
+        d->lender[s] = lender ? lender[s] : -1;
+    }
+    return DS_OK;
+}
+
+int ds_quota_periodic(ds_domain* d, uint64_t period_ns, const int32_t* oa, const int32_t* la, const int32_t* ob,
+                      const int32_t* lb, int n) {
+    if (check_dom(d) || n != d->num_sms) return fail(DS_INVALID_ARGUMENT, "control word needs num_sms entries");
+    std::lock_guard<std::mutex> g(d->mu);
+    for (int i = 0; i < DS_MAX_SMS; ++i)
+        for (int k = 0; k < 2; ++k) {
+            d->mb->per_owner[k][i] = -1;
+            d->mb->per_lender[k][i] = -1;
+        }
+    for (int s = 0; s < n; ++s) {
+        int sm = d->smids[s];
+        d->mb->per_owner[0][sm] = oa ? oa[s] : -1;
+        d->mb->per_lender[0][sm] = la ? la[s] : -1;
+        d->mb->per_owner[1][sm] = ob ? ob[s] : -1;
+        d->mb->per_lender[1][sm] = lb ? lb[s] : -1;
+    }
+    d->mb->periodic_ns = period_ns;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    d->mb->periodic_gen = d->mb->periodic_gen + 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    return DS_OK;
+}
+
+int ds_stats_get(ds_domain* d, ds_stats* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    std::memset(out, 0, sizeof(*out));
+    out->launches_enqueued = d->enqueued;
+    out->launches_completed = d->completed_total.load();
+    out->num_sms = d->num_sms;
+    out->running = d->running ? 1 : 0;
+    cudaSetDevice(d->device);
+    unsigned long long v[5] = {0, 0, 0, 0, 0};
+    DS_CUDA(cudaMemcpyAsync(&v[0], &d->d_state->blocks_executed, 8, cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaMemcpyAsync(&v[1], &d->d_state->ctl.gen, 4, cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaMemcpyAsync(&v[2], &d->d_state->slog_count, 8, cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaMemcpyAsync(&v[3], &d->d_state->blog_count, 8, cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    out->blocks_executed = v[0];
+    out->ctl_changes = v[1] & 0xffffffffu;
+    out->switches = v[2];
+    out->block_log_entries = std::min<uint64_t>(v[3], d->blog_cap);
+    out->block_log_dropped = v[3] > d->blog_cap ? v[3] - d->blog_cap : 0;
+    return DS_OK;
+}
+
+// vctx_transcripts (engine.hpp:124): executed signatures of completed launches
+int ds_transcript(ds_domain* d, int tenant, int32_t* kernel_ids, uint32_t* grids, int cap, int* n) {
+    if (check_dom(d) || !n) return fail(DS_INVALID_ARGUMENT, "null");
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    std::lock_guard<std::mutex> g(d->mu);
+    TenantRecord* t = d->tenants[tenant];
+    uint64_t done = t->completed.load();
+    int m = (int)std::min<uint64_t>(done, (uint64_t)cap);
+    for (int i = 0; i < m; ++i) {
+        if (kernel_ids) kernel_ids[i] = t->launched_kernel[i];
+        if (grids) grids[i] = t->launched_grid[i];
+    }
+    *n = (int)done;
+    return DS_OK;
+}
+
+int ds_logical_progress(ds_domain* d, int tenant, int64_t* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    *out = (int64_t)d->tenants[tenant]->completed.load();  // types.hpp:86 logical_progress
+    return DS_OK;
+}
+
+}  // extern "C"
+
+template <class T>
+static int copy_log(ds_domain* d, T* dev, unsigned long long* dcount, uint64_t cap_dev, T* out, int64_t cap,
+                    int64_t* n) {
+    cudaSetDevice(d->device);
+    unsigned long long cnt = 0;
+    DS_CUDA(cudaMemcpyAsync(&cnt, dcount, 8, cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    uint64_t avail = std::min<uint64_t>(cnt, cap_dev);
+    uint64_t m = std::min<uint64_t>(avail, cap < 0 ? 0 : (uint64_t)cap);
+    if (m && out) {
+        DS_CUDA(cudaMemcpyAsync(out, dev, m * sizeof(T), cudaMemcpyDeviceToHost, d->copy_stream));
+        DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    }
+    *n = (int64_t)avail;
+    return DS_OK;
+}
+
+extern "C" {
+
+int ds_block_log(ds_domain* d, ds_block_record* out, int64_t cap, int64_t* n) {
+    if (check_dom(d) || !n) return fail(DS_INVALID_ARGUMENT, "null");
+    if (!d->d_blog) {
+        *n = 0;
+        return DS_OK;
+    }
+    return copy_log(d, d->d_blog, &d->d_state->blog_count, d->blog_cap, out, cap, n);
+}
+
+int ds_switch_log(ds_domain* d, ds_switch_record* out, int64_t cap, int64_t* n) {
+    if (check_dom(d) || !n) return fail(DS_INVALID_ARGUMENT, "null");
+    return copy_log(d, d->d_slog, &d->d_state->slog_count, d->slog_cap, out, cap, n);
+}
+
+int ds_ctl_log(ds_domain* d, ds_ctl_record* out, int64_t cap, int64_t* n) {
+    if (check_dom(d) || !n) return fail(DS_INVALID_ARGUMENT, "null");
+    return copy_log(d, d->d_clog, &d->d_state->clog_count, d->clog_cap, out, cap, n);
+}
+
+int ds_clear_logs(ds_domain* d) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    cudaSetDevice(d->device);
+    unsigned long long z = 0;
+    DS_CUDA(cudaMemcpyAsync(&d->d_state->blog_count, &z, 8, cudaMemcpyHostToDevice, d->copy_stream));
+    DS_CUDA(cudaMemcpyAsync(&d->d_state->slog_count, &z, 8, cudaMemcpyHostToDevice, d->copy_stream));
+    DS_CUDA(cudaMemcpyAsync(&d->d_state->clog_count, &z, 8, cudaMemcpyHostToDevice, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    return DS_OK;
+}
+
+int ds_globaltimer(ds_domain* d, uint64_t* ns) {
+    if (check_dom(d) || !ns) return fail(DS_INVALID_ARGUMENT, "null");
+    cudaSetDevice(d->device);
+    // 1 CTA of 32 threads with no smem co-resides with the executor; buffers
+    // are preallocated (cudaFree would synchronize with the resident executor)
+    ds_dev_probe(1, d->d_probe, d->d_probe + 1, d->d_probe_t, d->copy_stream);
+    cudaMemcpyAsync(ns, d->d_probe_t, 8, cudaMemcpyDeviceToHost, d->copy_stream);
+    cudaError_t e = cudaStreamSynchronize(d->copy_stream);
+    if (e != cudaSuccess) return fail(DS_CUDA_ERROR, cudaGetErrorString(e));
+    return DS_OK;
+}
+
+
+// Debug snapshot of the device control state (readable while the executor runs).
+int ds_debug_dump(ds_domain* d, char* out, int64_t cap) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    cudaSetDevice(d->device);
+    std::vector<uint8_t> buf(sizeof(ds::DevState));
+    DS_CUDA(cudaMemcpyAsync(buf.data(), d->d_state, sizeof(ds::DevState), cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    const ds::DevState* st = reinterpret_cast<const ds::DevState*>(buf.data());
+    std::string s;
+    char line[256];
+    snprintf(line, sizeof line, "ctl.gen=%u exit=%u blocks=%llu comp=%llu trig_next=%u trig_count=%u mb.gen=%u host_comp_next=%llu\n",
+             st->ctl.gen, st->ctl.exit, st->blocks_executed, st->completion_count, st->trig_next, st->trig_count,
+             d->mb->gen, (unsigned long long)d->comp_next);
+    s += line;
+    for (int t = 0; t < (int)d->tenants.size(); ++t) {
+        const ds::DevTenant& T = st->tenants[t];
+        snprintf(line, sizeof line, "tenant %d: claim seq=%u blk=%u tail=%u head=%u host_tail=%u next_seq=%llu completed=%llu\n", t,
+                 (unsigned)(T.claim >> 32), (unsigned)(T.claim & 0xffffffffu), T.tail, T.head, d->mb->tail[t],
+                 (unsigned long long)d->tenants[t]->next_seq, (unsigned long long)d->tenants[t]->completed.load());
+        s += line;
+    }
+    int owned = 0, lent = 0;
+    for (int i = 0; i < DS_MAX_SMS; ++i) {
+        owned += st->ctl.owner[i] >= 0;
+        lent += st->ctl.lender[i] >= 0;
+    }
+    snprintf(line, sizeof line, "device ctl: %d SMs owned, %d with lender\n", owned, lent);
+    s += line;
+    if ((int64_t)s.size() + 1 > cap) s.resize(cap - 1);
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return DS_OK;
+}
+
+int ds_solo_launch(int device, const ds_kernel_desc* k, void* stream) {
+    if (!k) return fail(DS_INVALID_ARGUMENT, "null desc");
+    if (k->body <= DS_BODY_NONE || k->body >= DS_BODY_COUNT) return fail(DS_CONFIG_ERROR, "unknown body");
+    if (k->args_size > ds::kMaxArgs) return fail(DS_CONFIG_ERROR, "args too large");
+    cudaSetDevice(device);
+    cudaStream_t s = (cudaStream_t)stream;
+    void* dargs = nullptr;
+    DS_CUDA(cudaMalloc(&dargs, ds::kMaxArgs));
+    DS_CUDA(cudaMemcpyAsync(dargs, k->args, k->args_size, cudaMemcpyHostToDevice, s));
+    uint32_t smem = ds_dev_body_smem(k->body);
+    cudaError_t e = ds_dev_launch_solo(k->body, dargs, k->grid_x, k->grid_y, k->grid_z, smem, s);
+    cudaStreamSynchronize(s);
+    cudaFree(dargs);
+    if (e != cudaSuccess) return fail(DS_CUDA_ERROR, std::string("solo launch: ") + cudaGetErrorString(e));
+    return DS_OK;
+}
+
+int ds_solo_launch_registered(ds_domain* d, int kernel_id, void* stream) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
+    const KernelRecord& k = d->kernels[kernel_id];
+    cudaSetDevice(d->device);
+    cudaError_t e = ds_dev_launch_solo(k.body, (const void*)k.args_dev, k.gx, k.gy, k.gz, ds_dev_body_smem(k.body),
+                                       (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(DS_CUDA_ERROR, std::string("solo launch: ") + cudaGetErrorString(e));
+    return DS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+"""Python view of one GPU sharing domain over the C ABI (tests, bench, smoke).
+
+Names follow the reference: a *tenant* is the reference's JobSpec/vctx, a
+*kernel* is the immutable Kernel launch record, a *pctx* is a quota-tier
+physical context, and bind/unbind/migrate/preempt are the binding-table and
+rck_flag operations (include/corosim/core/types.hpp:19-137,
+src/engine/engine.cpp:620-806).
+"""
+from __future__ import annotations
+
+import ctypes
+from fractions import Fraction
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+from . import _abi
+from ._abi import check, lib
+
+
+class Domain:
+    def __init__(self, device: int = 0, tiers: Sequence[Fraction] = (Fraction(1),), ring_capacity: int = 1024,
+                 block_log_capacity: int = 1 << 20, lend_idle_sms: bool = True, executor_smem: int = 0):
+        cfg = _abi.DomainConfig()
+        cfg.device = device
+        cfg.n_tiers = len(tiers)
+        for i, t in enumerate(tiers):
+            t = Fraction(t)
+            cfg.tier_num[i] = t.numerator
+            cfg.tier_den[i] = t.denominator
+        cfg.ring_capacity = ring_capacity
+        cfg.block_log_capacity = block_log_capacity
+        cfg.lend_idle_sms = int(lend_idle_sms)
+        cfg.executor_smem = executor_smem
+        h = ctypes.c_void_p()
+        check(lib().ds_domain_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self.h = h
+        self.device = device
+        self.tiers = [Fraction(t) for t in tiers]
+        n = ctypes.c_int()
+        check(lib().ds_num_sms(self.h, ctypes.byref(n)))
+        self.num_sms = n.value
+        self._args_keep = []
+
+    # -- lifecycle --
+    def close(self):
+        if self.h:
+            lib().ds_domain_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        try:
+            self.stop()
+        finally:
+            self.close()
+
+    def start(self):
+        check(lib().ds_start(self.h))
+
+    def stop(self):
+        if self.h:
+            check(lib().ds_stop(self.h))
+
+    # -- registration --
+    def tenant(self, name: str, priority: int = _abi.BEST_EFFORT) -> int:
+        d = _abi.TenantDesc(name.encode(), priority)
+        out = ctypes.c_int()
+        check(lib().ds_tenant_register(self.h, ctypes.byref(d), ctypes.byref(out)))
+        return out.value
+
+    def kernel(self, semantic_id: str, body: int, grid: Tuple[int, int, int], args: ctypes.Structure,
+               phase: int = _abi.OTHER, request: int = -1, decode_index: int = -1, block_threads: int = 256) -> int:
+        desc = make_desc(semantic_id, body, grid, args, phase, request, decode_index, block_threads)
+        self._args_keep.append(args)
+        out = ctypes.c_int()
+        check(lib().ds_kernel_register(self.h, ctypes.byref(desc), ctypes.byref(out)))
+        return out.value
+
+    # -- launches --
+    def launch(self, tenant: int, kernel: int, tag: int = 0) -> int:
+        seq = ctypes.c_uint64()
+        check(lib().ds_launch(self.h, tenant, kernel, tag, ctypes.byref(seq)))
+        return seq.value
+
+    def launch_atomized(self, tenant: int, kernel: int, tier: Fraction, tag: int = 0) -> int:
+        tier = Fraction(tier)
+        seq = ctypes.c_uint64()
+        check(lib().ds_launch_atomized(self.h, tenant, kernel, tag, tier.numerator, tier.denominator,
+                                       ctypes.byref(seq)))
+        return seq.value
+
+    def wait(self, tenant: int, seq: int, timeout_ms: int = 60000):
+        check(lib().ds_wait_tenant(self.h, tenant, seq, timeout_ms))
+
+    def poll(self, cap: int = 4096) -> List[_abi.Completion]:
+        arr = (_abi.Completion * cap)()
+        n = ctypes.c_int()
+        check(lib().ds_poll(self.h, arr, cap, ctypes.byref(n)))
+        return [arr[i] for i in range(n.value)]
+
+    # -- arbiter --
+    def bind(self, tenant: int, pctx: int):
+        check(lib().ds_bind(self.h, tenant, pctx))
+
+    def unbind(self, tenant: int):
+        check(lib().ds_unbind(self.h, tenant))
+
+    def migrate(self, tenant: int, pctx: int):
+        check(lib().ds_migrate(self.h, tenant, pctx))
+
+    def preempt(self, pctx: int):
+        check(lib().ds_preempt(self.h, pctx))
+
+    def bound_pctx(self, tenant: int) -> int:
+        out = ctypes.c_int()
+        check(lib().ds_bound_pctx(self.h, tenant, ctypes.byref(out)))
+        return out.value
+
+    def _arr(self, xs: Optional[Iterable[int]]):
+        if xs is None:
+            return None
+        xs = list(xs)
+        assert len(xs) == self.num_sms
+        return (ctypes.c_int32 * self.num_sms)(*xs)
+
+    def quota_set(self, owner: Sequence[int], lender: Optional[Sequence[int]] = None):
+        check(lib().ds_quota_set(self.h, self._arr(owner), self._arr(lender), self.num_sms))
+
+    def quota_at_claim(self, tenant: int, seq: int, block: int, owner: Sequence[int],
+                       lender: Optional[Sequence[int]] = None):
+        check(lib().ds_quota_at_claim(self.h, tenant, seq, block, self._arr(owner), self._arr(lender),
+                                      self.num_sms))
+
+    def quota_periodic(self, period_ns: int, owner_a, owner_b, lender_a=None, lender_b=None):
+        check(lib().ds_quota_periodic(self.h, period_ns, self._arr(owner_a), self._arr(lender_a),
+                                      self._arr(owner_b), self._arr(lender_b), self.num_sms))
+
+    def set_lend(self, tenant: int):
+        check(lib().ds_set_lend(self.h, tenant))
+
+    def mask(self, tenant: int, first: int, count: int, default: int = -1) -> List[int]:
+        """Owner vector giving SM slots [first, first+count) to tenant."""
+        return [tenant if first <= i < first + count else default for i in range(self.num_sms)]
+
+    # -- observation --
+    def stats(self) -> _abi.Stats:
+        s = _abi.Stats()
+        check(lib().ds_stats_get(self.h, ctypes.byref(s)))
+        return s
+
+    def transcript(self, tenant: int) -> List[Tuple[int, int]]:
+        n = ctypes.c_int()
+        check(lib().ds_transcript(self.h, tenant, None, None, 0, ctypes.byref(n)))
+        k = (ctypes.c_int32 * max(1, n.value))()
+        g = (ctypes.c_uint32 * max(1, n.value))()
+        check(lib().ds_transcript(self.h, tenant, k, g, n.value, ctypes.byref(n)))
+        return [(k[i], g[i]) for i in range(n.value)]
+
+    def logical_progress(self, tenant: int) -> int:
+        out = ctypes.c_int64()
+        check(lib().ds_logical_progress(self.h, tenant, ctypes.byref(out)))
+        return out.value
+
+    def _log(self, fn, rec):
+        n = ctypes.c_int64()
+        check(fn(self.h, None, 0, ctypes.byref(n)))
+        arr = (rec * max(1, n.value))()
+        check(fn(self.h, arr, n.value, ctypes.byref(n)))
+        return [arr[i] for i in range(n.value)]
+
+    def block_log(self):
+        return self._log(lib().ds_block_log, _abi.BlockRecord)
+
+    def switch_log(self):
+        return self._log(lib().ds_switch_log, _abi.SwitchRecord)
+
+    def ctl_log(self):
+        return self._log(lib().ds_ctl_log, _abi.CtlRecord)
+
+    def clear_logs(self):
+        check(lib().ds_clear_logs(self.h))
+
+    def globaltimer(self) -> int:
+        out = ctypes.c_uint64()
+        check(lib().ds_globaltimer(self.h, ctypes.byref(out)))
+        return out.value
+
+    def debug(self) -> str:
+        buf = ctypes.create_string_buffer(1 << 16)
+        check(lib().ds_debug_dump(self.h, buf, len(buf)))
+        return buf.value.decode()
+
+    def smids(self) -> List[int]:
+        arr = (ctypes.c_int * self.num_sms)()
+        n = ctypes.c_int()
+        check(lib().ds_smids(self.h, arr, self.num_sms, ctypes.byref(n)))
+        return list(arr)
+
+    def solo(self, kernel: int, stream: int = 0):
+        check(lib().ds_solo_launch_registered(self.h, kernel, ctypes.c_void_p(stream)))
+
+
+def make_desc(semantic_id, body, grid, args, phase=_abi.OTHER, request=-1, decode_index=-1, block_threads=256):
+    gx, gy, gz = (tuple(grid) + (1, 1, 1))[:3]
+    return _abi.KernelDesc(semantic_id.encode(), body, gx, gy, gz, block_threads,
+                           ctypes.cast(ctypes.pointer(args), ctypes.c_void_p), ctypes.sizeof(args), phase,
+                           request, decode_index)
+
+
+def solo_launch(device: int, semantic_id: str, body: int, grid, args, stream: int = 0):
+    """Run a body standalone as a plain grid (exclusive_baseline)."""
+    desc = make_desc(semantic_id, body, grid, args)
+    check(lib().ds_solo_launch(device, ctypes.byref(desc), ctypes.c_void_p(stream)))
