@@ -218,6 +218,12 @@ int ds_solo_launch(int device, const ds_kernel_desc* desc, void* stream);
 int ds_solo_launch_registered(ds_domain* dom, int kernel_id, void* stream);
 int ds_body_smem(int body, uint32_t* bytes);
 
+/* ---- body argument helpers ---- */
+/* encode a TMA descriptor (CUtensorMap, 128 B) for a row-major bf16 [rows][cols]
+ * matrix, SWIZZLE_128B boxes of box_rows x box_cols (box_cols*2 must be 128) */
+int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                          uint32_t box_cols);
+
 #ifdef __cplusplus
 }
 #endif

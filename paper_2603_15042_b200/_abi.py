@@ -144,6 +144,35 @@ class SgemmArgs(ctypes.Structure):
                 ("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
+class TmaDesc(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_uint64 * 16)]
+
+
+class GemmArgs(ctypes.Structure):
+    """C[M,N] bf16 = A[M,K] . B[N,K]^T (csrc/bodies/gemm_tc.cuh)."""
+    _fields_ = [("tmA", TmaDesc), ("tmB", TmaDesc), ("C", ctypes.c_uint64), ("M", ctypes.c_int32),
+                ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32)]
+
+
+def tensor_map_bf16(ptr: int, rows: int, cols: int, box_rows: int, box_cols: int = 64) -> TmaDesc:
+    d = TmaDesc()
+    check(lib().ds_tensor_map_bf16_2d(ctypes.byref(d), ctypes.c_void_p(ptr), rows, cols, box_rows, box_cols))
+    return d
+
+
+GEMM_BM, GEMM_BN = 128, 256
+
+
+def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16) -> "GemmArgs":
+    if M % GEMM_BM or N % GEMM_BN or K % 64:
+        raise DsError(10, f"gemm shape {M}x{N}x{K} must tile by 128x256x64")
+    return GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM), tensor_map_bf16(B, N, K, GEMM_BN), C, M, N, K, group_m)
+
+
+def gemm_grid(M: int, N: int):
+    return ((M // GEMM_BM) * (N // GEMM_BN), 1, 1)
+
+
 class SpinArgs(ctypes.Structure):
     _fields_ = [("out", ctypes.c_uint64), ("ns", ctypes.c_uint64)]
 
@@ -157,6 +186,7 @@ EXPORTS = [
     "ds_set_lend", "ds_quota_at_claim", "ds_quota_periodic", "ds_stats_get", "ds_transcript",
     "ds_logical_progress", "ds_block_log", "ds_switch_log", "ds_ctl_log", "ds_clear_logs",
     "ds_globaltimer", "ds_debug_dump", "ds_solo_launch", "ds_solo_launch_registered", "ds_body_smem",
+    "ds_tensor_map_bf16_2d",
 ]
 
 _lib = None
@@ -214,6 +244,7 @@ def lib():
         L.ds_solo_launch.argtypes = [ctypes.c_int, ctypes.POINTER(KernelDesc), vp]
         L.ds_solo_launch_registered.argtypes = [vp, ctypes.c_int, vp]
         L.ds_body_smem.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
+        L.ds_tensor_map_bf16_2d.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
         _lib = L
     return _lib
 

@@ -3,6 +3,7 @@
 // the executor the CTA also holds a scheduler warp and a loader warp that
 // never enter tenant code.
 #pragma once
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 #include "../ds_device.cuh"

@@ -1,0 +1,174 @@
+// tcgen05/TMEM/TMA tile engine and the two contraction tenants built on it.
+//
+//   D[BM x BN] (fp32, TMEM) = sum_k A[BM rows][k] . B[BN rows][k]   (both K-major, bf16)
+//
+// One logical block = one output tile (training GEMM) or one (row-slab,
+// K-split) piece (decode GEMV).  Per block: warp 0 is the TMA producer
+// (SWIZZLE_128B tiles into a STAGES-deep smem ring, mbarrier complete_tx),
+// warp 1 issues tcgen05.mma (one elected thread, accumulator in TMEM,
+// tcgen05.commit frees ring slots), warps 4-7 drain TMEM with tcgen05.ld in
+// the epilogue.  The K loop order and the split-K combine order are fixed
+// functions of the logical block index, so results are bit-identical wherever
+// and whenever the block runs (solo or as a coroutine).
+#pragma once
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace ds {
+
+struct alignas(64) TmaDesc {
+    uint64_t w[16];  // CUtensorMap (128 B), encoded on the host
+};
+
+constexpr int kTcBM = 128;
+constexpr int kTcBK = 64;  // 64 bf16 = one 128-B swizzle row
+
+template <int BN, int STAGES>
+struct TcSmem {
+    static constexpr uint32_t kABytes = kTcBM * kTcBK * 2;  // 16 KB
+    static constexpr uint32_t kBBytes = BN * kTcBK * 2;
+    static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+    static constexpr uint32_t kBarOff = STAGES * kStageBytes;
+    static constexpr uint32_t kBytes = kBarOff + 1024;  // barriers + epilogue scratch follow
+};
+
+__device__ __forceinline__ char* align1024(char* p) {
+    return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Runs the mainloop for one logical block; on return (all 256 threads) the
+// accumulator is in TMEM columns [tmem_base, tmem_base + BN) and the epilogue
+// warps (4-7) have passed the tmem_full barrier.  Returns the smem base.
+template <int BN, int STAGES>
+__device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
+                                            int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first) {
+    using L = TcSmem<BN, STAGES>;
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tmem_full, 1);
+        tc::fence_mbar_init();
+    }
+    body_sync();
+    const int nkb = kb_end - kb_begin;
+    if (warp == 0 && lane == 0) {
+        tc::tma_fence_desc(tmA);
+        tc::tma_fence_desc(tmB);
+        const uint64_t pol = a_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = (i / STAGES) & 1;
+            if (i >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
+            char* sa = base + s * L::kStageBytes;
+            char* sb = sa + L::kABytes;
+            tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+            const int k0 = (kb_begin + i) * kTcBK;
+            tc::tma_load_2d_hint(sa, tmA, &full[s], k0, a_row, pol);
+            tc::tma_load_2d(sb, tmB, &full[s], k0, b_row);
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(kTcBM, BN);
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = (i / STAGES) & 1;
+            tc::mbar_wait(&full[s], ph);
+            tc::tc_fence_after();
+            char* sa = base + s * L::kStageBytes;
+            char* sb = sa + L::kABytes;
+            const uint64_t ad = tc::smem_desc_k_sw128(sa);
+            const uint64_t bd = tc::smem_desc_k_sw128(sb);
+#pragma unroll
+            for (int k = 0; k < kTcBK / 16; ++k) {
+                // +32 B per K=16 step inside the 128-B swizzle row
+                tc::mma_bf16(tmem_base, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
+            }
+            tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(tmem_full);
+    }
+    if (warp >= 4) {
+        tc::mbar_wait(tmem_full, 0);
+        tc::tc_fence_after();
+    }
+}
+
+template <int BN, int STAGES>
+__device__ __forceinline__ void tc_teardown(char* base) {
+    using L = TcSmem<BN, STAGES>;
+    tc::tc_fence_before();
+    body_sync();
+    if (threadIdx.x == 0) {
+        uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
+        for (int s = 0; s < 2 * STAGES + 1; ++s) tc::mbar_inval(&full[s]);
+    }
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Training GEMM tenant: C[M,N] (bf16) = A[M,K] . B[N,K]^T, fp32 accumulate.
+// Logical block t -> output tile (m_blk, n_blk), grouped raster so ~148
+// concurrent tiles share A/B panels in L2.
+// ---------------------------------------------------------------------------
+struct GemmArgs {
+    TmaDesc tmA;  // A [M][K] bf16, box {64, 128}
+    TmaDesc tmB;  // B [N][K] bf16, box {64, 256}
+    uint64_t C;   // bf16 [M][N]
+    int32_t M, N, K;
+    int32_t group_m;
+};
+
+constexpr int kGemmBN = 256;
+constexpr int kGemmStages = 4;
+
+__device__ void body_gemm_bf16(const BodyCtx& c) {
+    const GemmArgs& a = *reinterpret_cast<const GemmArgs*>(c.args);
+    char* base = align1024(c.smem);
+    const int m_blocks = a.M / kTcBM, n_blocks = a.N / kGemmBN;
+    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int gm = a.group_m > 0 ? a.group_m : 16;
+    const int group_size = gm * n_blocks;
+    const int g = t / group_size;
+    const int first_m = g * gm;
+    const int rows = min(gm, m_blocks - first_m);
+    const int r = t % group_size;
+    const int m_blk = first_m + r % rows;
+    const int n_blk = r / rows;
+    tc_mainloop<kGemmBN, kGemmStages>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * kGemmBN, 0, a.K / kTcBK, c.tmem_base,
+                                      false);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= 4) {
+        const int q = warp & 3;
+        const int row = m_blk * kTcBM + q * 32 + lane;
+        __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(a.C);
+        uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * a.N + n_blk * kGemmBN);
+#pragma unroll 1
+        for (int ch = 0; ch < kGemmBN / 32; ++ch) {
+            uint32_t v[32];
+            tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, v);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint4 o;
+                o.x = pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                o.y = pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                o.z = pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                o.w = pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                dst[ch * 4 + j] = o;
+            }
+        }
+    }
+    tc_teardown<kGemmBN, kGemmStages>(base);
+}
+
+}  // namespace ds

@@ -22,9 +22,12 @@
 #include "bodies/common.cuh"
 #include "bodies/reduce.cuh"
 #include "bodies/sgemm.cuh"
+#include "bodies/gemm_tc.cuh"
 #include "ds_device.cuh"
 
 namespace ds {
+
+constexpr uint32_t kTmemCols = 256;
 
 // ---------------------------------------------------------------------------
 // Body dispatch (shared by the executor and the solo wrapper)
@@ -34,6 +37,7 @@ __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
         case DS_BODY_REDUCE_CHUNKS: body_reduce(c); break;
         case DS_BODY_SGEMM: body_sgemm(c); break;
         case DS_BODY_SPIN: body_spin(c); break;
+        case DS_BODY_GEMM_BF16: body_gemm_bf16(c); break;
         default: break;
     }
 }
@@ -431,11 +435,22 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
         if (blockIdx.x == 0) loader_loop(st);
         return;
     }
+    // TMEM: one allocation for the CTA's lifetime, shared by all bodies
+    __shared__ uint32_t tmem_base_sh;
+    if (warp == 0) tc::tmem_alloc(&tmem_base_sh, kTmemCols);
+    tc::tc_fence_before();
+    named_sync(kBarExit, kBodyThreads + 32);
+    tc::tc_fence_after();
+    const uint32_t tmem_base = tmem_base_sh;
     if (warp == kSchedWarp) {
         scheduler_loop(st, &stage, &body_t0, sm);
     } else {
-        body_loop(&stage, &body_t0, smem, smem_bytes, 0);
+        body_loop(&stage, &body_t0, smem, smem_bytes, tmem_base);
     }
+    tc::tc_fence_before();
+    named_sync(kBarExit, kBodyThreads + 32);
+    tc::tc_fence_after();
+    if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
 }
 
 // Solo baseline: the same body as a plain grid (exclusive_baseline,
@@ -454,8 +469,24 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     c.args = args;
     c.smem = smem;
     c.smem_bytes = smem_bytes;
-    c.tmem_base = 0;
+    __shared__ uint32_t tmem_base_sh;
+    const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16;
+    if (tc_body) {
+        if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(&tmem_base_sh, kTmemCols);
+        tc::tc_fence_before();
+        __syncthreads();
+        tc::tc_fence_after();
+        c.tmem_base = tmem_base_sh;
+    } else {
+        c.tmem_base = 0;
+    }
     run_body(body, c);
+    if (tc_body) {
+        tc::tc_fence_before();
+        __syncthreads();
+        tc::tc_fence_after();
+        if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(c.tmem_base, kTmemCols);
+    }
 }
 
 extern "C" __global__ void ds_probe_kernel(uint32_t* smids, uint32_t* nsmid, uint64_t* timer) {
@@ -505,6 +536,7 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_REDUCE_CHUNKS: return 16384 * 4 + 1024;
         case DS_BODY_SGEMM: return (32 * 68 + 32 * 64) * 4 + 1024;
         case DS_BODY_SPIN: return 1024;
+        case DS_BODY_GEMM_BF16: return ds::TcSmem<ds::kGemmBN, ds::kGemmStages>::kBytes + 1024;
         default: return ds::kDefaultSmem;
     }
 }

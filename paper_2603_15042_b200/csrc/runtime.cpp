@@ -9,6 +9,7 @@
 // Threads: the caller's thread(s) issue API calls (serialised by a mutex); a
 // drainer thread consumes device->host completion records from pinned mapped
 // memory and maintains per-tenant completion state, transcripts and timings.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -960,6 +961,38 @@ int ds_debug_dump(ds_domain* d, char* out, int64_t cap) {
     s += line;
     if ((int64_t)s.size() + 1 > cap) s.resize(cap - 1);
     std::memcpy(out, s.c_str(), s.size() + 1);
+    return DS_OK;
+}
+
+// ---- TMA tensor maps (host encode through the driver entry point; libcuda is
+// never linked, so the library still loads on a CPU-only host) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                          uint32_t box_cols) {
+    if (!out128 || !base) return fail(DS_INVALID_ARGUMENT, "null");
+    if (box_cols * 2 != 128) return fail(DS_CONFIG_ERROR, "box inner extent must be 128 B (SWIZZLE_128B)");
+    if ((cols * 2) % 16 != 0 || ((uintptr_t)base & 15)) return fail(DS_CONFIG_ERROR, "row pitch / base must be 16-B aligned");
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return fail(DS_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)p;
+    }
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(DS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    std::memcpy(out128, &m, 128);
     return DS_OK;
 }
 
