@@ -173,6 +173,30 @@ def gemm_grid(M: int, N: int):
     return ((M // GEMM_BM) * (N // GEMM_BN), 1, 1)
 
 
+class GemvArgs(ctypes.Structure):
+    """Decode projection on tcgen05 (csrc/bodies/decode.cuh)."""
+    _fields_ = [("tmW", TmaDesc), ("tmX", TmaDesc), ("out", ctypes.c_uint64), ("resid", ctypes.c_uint64),
+                ("ws", ctypes.c_uint64), ("counters", ctypes.c_uint64), ("stats_in", ctypes.c_uint64),
+                ("stats_out", ctypes.c_uint64), ("kcache", ctypes.c_uint64), ("vcache", ctypes.c_uint64),
+                ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("S", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("P_in", ctypes.c_int32), ("eps", ctypes.c_float), ("pos", ctypes.c_int32), ("Lmax", ctypes.c_int32),
+                ("q_dim", ctypes.c_int32), ("kv_dim", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("pad1", ctypes.c_int32)]
+
+
+GEMV_STORE, GEMV_RESID, GEMV_SILU_MUL, GEMV_QKV = 0, 1, 2, 3
+
+
+class RmsArgs(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_uint64), ("stats", ctypes.c_uint64), ("K", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class AttnArgs(ctypes.Structure):
+    _fields_ = [("q", ctypes.c_uint64), ("kcache", ctypes.c_uint64), ("vcache", ctypes.c_uint64),
+                ("out", ctypes.c_uint64), ("ws", ctypes.c_uint64), ("counters", ctypes.c_uint64),
+                ("L", ctypes.c_int32), ("Lmax", ctypes.c_int32), ("S", ctypes.c_int32), ("scale", ctypes.c_float)]
+
+
 class SpinArgs(ctypes.Structure):
     _fields_ = [("out", ctypes.c_uint64), ("ns", ctypes.c_uint64)]
 

@@ -23,6 +23,7 @@
 #include "bodies/reduce.cuh"
 #include "bodies/sgemm.cuh"
 #include "bodies/gemm_tc.cuh"
+#include "bodies/decode.cuh"
 #include "ds_device.cuh"
 
 namespace ds {
@@ -38,6 +39,9 @@ __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
         case DS_BODY_SGEMM: body_sgemm(c); break;
         case DS_BODY_SPIN: body_spin(c); break;
         case DS_BODY_GEMM_BF16: body_gemm_bf16(c); break;
+        case DS_BODY_GEMV_BF16: body_gemv_bf16(c); break;
+        case DS_BODY_ATTN_DECODE: body_attn_decode(c); break;
+        case DS_BODY_RMSNORM: body_rmsnorm(c); break;
         default: break;
     }
 }
@@ -537,6 +541,9 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_SGEMM: return (32 * 68 + 32 * 64) * 4 + 1024;
         case DS_BODY_SPIN: return 1024;
         case DS_BODY_GEMM_BF16: return ds::TcSmem<ds::kGemmBN, ds::kGemmStages>::kBytes + 1024;
+        case DS_BODY_GEMV_BF16: return ds::kGemvScratch + (128 * 33 + 64) * 4 + 1024;
+        case DS_BODY_ATTN_DECODE: return 8 * 4 * 130 * 4 + 1024;
+        case DS_BODY_RMSNORM: return 1024;
         default: return ds::kDefaultSmem;
     }
 }

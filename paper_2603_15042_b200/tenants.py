@@ -1,0 +1,216 @@
+"""Tenant workloads of the benchmark configs, built from the native bodies.
+
+* ``DecodeModel`` — Llama-3-8B-shaped decode step, batch 32 (config 2): per
+  layer RMSNorm-folded QKV projection (+ KV-cache append), GQA attention,
+  O projection (+ residual), gate/up projection (+ SiLU*up), down projection
+  (+ residual); final norm + LM head.  162 launches per decode step.
+* ``TrainGemm`` — bf16 GEMM 8192^3 training step on tcgen05 (config 2).
+
+Weights are random (synthetic data, no checkpoints); shapes are exactly the
+named model's.  Device memory comes from torch (plumbing only).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import List
+
+import torch
+
+from . import _abi
+
+SMS = 148
+
+
+def pick_split(nb: int, kblocks: int, sms: int = SMS, max_s: int = 16, min_kb: int = 4, slack: float = 0.04) -> int:
+    """K-split S for a GEMV with nb row slabs: the smallest S whose wave
+    efficiency nblk / (ceil(nblk/sms)*sms) is within `slack` of the best,
+    keeping >= min_kb k-blocks per block (fewer, larger blocks amortise the
+    per-block pipeline fill)."""
+    effs = {}
+    for s in range(1, max_s + 1):
+        if kblocks // s < min_kb:
+            break
+        n = nb * s
+        effs[s] = n / (math.ceil(n / sms) * sms)
+    best = max(effs.values())
+    return min(s for s, e in effs.items() if e >= best - slack)
+
+
+@dataclass
+class DecodeConfig:
+    layers: int = 32
+    d: int = 4096
+    n_q: int = 32
+    n_kv: int = 8
+    ffn: int = 14336
+    vocab: int = 128256
+    batch: int = 32
+    L: int = 1024          # attended KV length (positions 0..L-1; the new token writes L-1)
+    eps: float = 1e-5
+    attn_splits: int = 2
+
+
+class DecodeModel:
+    def __init__(self, cfg: DecodeConfig = DecodeConfig(), device="cuda", seed: int = 0):
+        assert cfg.batch == 32 and cfg.d == cfg.n_q * 128 and cfg.n_q == 4 * cfg.n_kv
+        self.cfg = cfg
+        c = cfg
+        g = torch.Generator(device=device).manual_seed(seed)
+
+        def w(n, k):
+            return ((torch.rand(n, k, device=device, generator=g) * 2 - 1) / math.sqrt(k)).to(torch.bfloat16)
+
+        self.kv_dim = c.n_kv * 128
+        self.qkv_n = c.d + 2 * self.kv_dim
+        self.Wqkv = [w(self.qkv_n, c.d) for _ in range(c.layers)]
+        self.Wo = [w(c.d, c.d) for _ in range(c.layers)]
+        self.Wgu = [w(2 * c.ffn, c.d) for _ in range(c.layers)]   # slabs of [64 gate | 64 up] rows
+        self.Wd = [w(c.d, c.ffn) for _ in range(c.layers)]
+        self.lm = w(c.vocab, c.d)
+        self.Lmax = c.L
+        self.kc = [((torch.rand(32, c.n_kv, self.Lmax, 128, device=device, generator=g) * 2 - 1)).to(torch.bfloat16)
+                   for _ in range(c.layers)]
+        self.vc = [((torch.rand(32, c.n_kv, self.Lmax, 128, device=device, generator=g) * 2 - 1)).to(torch.bfloat16)
+                   for _ in range(c.layers)]
+        bf = torch.bfloat16
+        self.H = [((torch.rand(32, c.d, device=device, generator=g) * 2 - 1)).to(bf), torch.zeros(32, c.d, device=device, dtype=bf)]
+        self.h_mid = torch.zeros(32, c.d, device=device, dtype=bf)
+        self.q = torch.zeros(32, c.d, device=device, dtype=bf)
+        self.attn = torch.zeros(32, c.d, device=device, dtype=bf)
+        self.act = torch.zeros(32, c.ffn, device=device, dtype=bf)
+        self.logits = torch.zeros(32, c.vocab, device=device, dtype=bf)
+        self.st0 = torch.zeros(1, 32, device=device)
+        self.st_h = torch.zeros(c.d // 128, 32, device=device)
+        self.st_mid = torch.zeros(c.d // 128, 32, device=device)
+        # split-K plans and workspaces
+        self.S = {
+            "qkv": pick_split(self.qkv_n // 128, c.d // 64),
+            "o": pick_split(c.d // 128, c.d // 64),
+            "gu": pick_split(2 * c.ffn // 128, c.d // 64),
+            "down": pick_split(c.d // 128, c.ffn // 64),
+            "lm": pick_split(c.vocab // 128, c.d // 64),
+        }
+        ws_elems = max(self.S["qkv"] * self.qkv_n, self.S["o"] * c.d, self.S["gu"] * 2 * c.ffn,
+                       self.S["down"] * c.d, self.S["lm"] * c.vocab) * 32
+        self.ws = torch.zeros(ws_elems, device=device)
+        self.counters = torch.zeros(max(c.vocab, 2 * c.ffn) // 128 + 1, device=device, dtype=torch.int32)
+        self.attn_ws = torch.zeros(256 * c.attn_splits * 4 * 130, device=device)
+        self.attn_counters = torch.zeros(256, device=device, dtype=torch.int32)
+        self._build_args()
+
+    # ---- launch records ----
+    def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None):
+        tmW = _abi.tensor_map_bf16(W.data_ptr(), N, K, 128)
+        tmX = _abi.tensor_map_bf16(X.data_ptr(), 32, K, 32)
+        a = _abi.GemvArgs()
+        a.tmW, a.tmX = tmW, tmX
+        a.out = out.data_ptr()
+        a.resid = resid.data_ptr() if resid is not None else 0
+        a.ws = self.ws.data_ptr()
+        a.counters = self.counters.data_ptr()
+        a.stats_in = stats_in.data_ptr() if stats_in is not None else 0
+        a.stats_out = stats_out.data_ptr() if stats_out is not None else 0
+        a.kcache = self.kc[l].data_ptr() if l is not None else 0
+        a.vcache = self.vc[l].data_ptr() if l is not None else 0
+        a.N, a.K, a.S, a.mode, a.P_in = N, K, S, mode, P_in
+        a.eps = self.cfg.eps
+        a.pos = self.cfg.L - 1
+        a.Lmax = self.Lmax
+        a.q_dim, a.kv_dim = self.cfg.d, self.kv_dim
+        return a, ((N // 128) * S, 1, 1)
+
+    def _build_args(self):
+        c = self.cfg
+        self.records = []  # (semantic_id, body, grid, args, bytes)
+        ra = _abi.RmsArgs(self.H[0].data_ptr(), self.st0.data_ptr(), c.d, 0)
+        self.records.append(("decode/rms0", _abi.BODY_RMSNORM, (1, 1, 1), ra, 32 * c.d * 2))
+        for l in range(c.layers):
+            hin, hout = self.H[l % 2], self.H[(l + 1) % 2]
+            st_in, p_in = (self.st0, 1) if l == 0 else (self.st_h, c.d // 128)
+            a, g = self._gemv(self.Wqkv[l], hin, self.qkv_n, c.d, self.S["qkv"], _abi.GEMV_QKV, self.q,
+                              stats_in=st_in, P_in=p_in, l=l)
+            self.records.append((f"decode/qkv", _abi.BODY_GEMV_BF16, g, a, self.qkv_n * c.d * 2))
+            at = _abi.AttnArgs(self.q.data_ptr(), self.kc[l].data_ptr(), self.vc[l].data_ptr(), self.attn.data_ptr(),
+                               self.attn_ws.data_ptr(), self.attn_counters.data_ptr(), c.L, self.Lmax, c.attn_splits,
+                               1.0 / math.sqrt(128))
+            self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,
+                                 2 * 32 * c.n_kv * c.L * 128 * 2))
+            a, g = self._gemv(self.Wo[l], self.attn, c.d, c.d, self.S["o"], _abi.GEMV_RESID, self.h_mid, resid=hin,
+                              stats_out=self.st_mid)
+            self.records.append(("decode/o", _abi.BODY_GEMV_BF16, g, a, c.d * c.d * 2))
+            a, g = self._gemv(self.Wgu[l], self.h_mid, 2 * c.ffn, c.d, self.S["gu"], _abi.GEMV_SILU_MUL, self.act,
+                              stats_in=self.st_mid, P_in=c.d // 128)
+            self.records.append(("decode/gate_up", _abi.BODY_GEMV_BF16, g, a, 2 * c.ffn * c.d * 2))
+            a, g = self._gemv(self.Wd[l], self.act, c.d, c.ffn, self.S["down"], _abi.GEMV_RESID, hout,
+                              resid=self.h_mid, stats_out=self.st_h)
+            self.records.append(("decode/down", _abi.BODY_GEMV_BF16, g, a, c.d * c.ffn * 2))
+        hfin = self.H[c.layers % 2]
+        a, g = self._gemv(self.lm, hfin, c.vocab, c.d, self.S["lm"], _abi.GEMV_STORE, self.logits,
+                          stats_in=self.st_h, P_in=c.d // 128)
+        self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
+
+    @property
+    def weight_bytes(self) -> int:
+        return sum(r[4] for r in self.records if r[1] == _abi.BODY_GEMV_BF16)
+
+    @property
+    def step_bytes(self) -> int:
+        """Algorithmic HBM bytes per decode step: weights + KV cache read
+        (activations are O(MB) and L2-resident)."""
+        return sum(r[4] for r in self.records)
+
+    def register(self, dom, phase=_abi.DECODE) -> List[int]:
+        return [dom.kernel(sid, body, grid, args, phase=phase) for sid, body, grid, args, _ in self.records]
+
+    def solo_step(self, device: int = 0):
+        from .runtime import solo_launch
+        for sid, body, grid, args, _ in self.records:
+            solo_launch(device, sid, body, grid, args)
+
+    # ---- plain torch fp32 reference of the same step (numerics tests) ----
+    @torch.no_grad()
+    def reference_step(self, h0: torch.Tensor, kc, vc):
+        c = self.cfg
+        bf = torch.bfloat16
+        h = h0.clone()
+        kc = [k.clone() for k in kc]
+        vc = [v.clone() for v in vc]
+        for l in range(c.layers):
+            r = torch.rsqrt(h.float().pow(2).sum(-1) / c.d + c.eps)
+            qkv = (h.float() @ self.Wqkv[l].float().t()) * r[:, None]
+            q = qkv[:, :c.d].to(bf)
+            kc[l][:, :, c.L - 1] = qkv[:, c.d:c.d + self.kv_dim].to(bf).view(32, c.n_kv, 128)
+            vc[l][:, :, c.L - 1] = qkv[:, c.d + self.kv_dim:].to(bf).view(32, c.n_kv, 128)
+            Q = q.float().view(32, c.n_kv, 4, 128)
+            K = kc[l][:, :, :c.L].float()
+            V = vc[l][:, :, :c.L].float()
+            s = torch.einsum("bhqd,bhpd->bhqp", Q, K) / math.sqrt(128)
+            o = torch.einsum("bhqp,bhpd->bhqd", torch.softmax(s, -1), V)
+            attn = o.reshape(32, c.d).to(bf)
+            hmid = (h.float() + attn.float() @ self.Wo[l].float().t()).to(bf)
+            r2 = torch.rsqrt(hmid.float().pow(2).sum(-1) / c.d + c.eps)
+            gu = (hmid.float() @ self.Wgu[l].float().t()) * r2[:, None]
+            gu = gu.view(32, -1, 2, 64)
+            act = (torch.nn.functional.silu(gu[:, :, 0]) * gu[:, :, 1]).reshape(32, c.ffn).to(bf)
+            h = (hmid.float() + act.float() @ self.Wd[l].float().t()).to(bf)
+        rf = torch.rsqrt(h.float().pow(2).sum(-1) / c.d + c.eps)
+        logits = ((h.float() @ self.lm.float().t()) * rf[:, None]).to(bf)
+        return logits, h
+
+
+class TrainGemm:
+    """One training-step contraction: C = A . B^T, bf16 in, fp32 accumulate."""
+
+    def __init__(self, M=8192, N=8192, K=8192, device="cuda", seed=1):
+        g = torch.Generator(device=device).manual_seed(seed)
+        self.M, self.N, self.K = M, N, K
+        self.A = (torch.rand(M, K, device=device, generator=g) * 2 - 1).to(torch.bfloat16)
+        self.B = (torch.rand(N, K, device=device, generator=g) * 2 - 1).to(torch.bfloat16)
+        self.C = torch.zeros(M, N, device=device, dtype=torch.bfloat16)
+        self.args = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), M, N, K)
+        self.grid = _abi.gemm_grid(M, N)
+        self.flops = 2.0 * M * N * K
+
+    def register(self, dom, phase=_abi.TRAINING) -> int:
+        return dom.kernel("train/gemm_bf16", _abi.BODY_GEMM_BF16, self.grid, self.args, phase=phase)

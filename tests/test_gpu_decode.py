@@ -1,0 +1,74 @@
+"""Decode tenant numerics: one Llama-3-shaped decode step (2 layers, reduced
+vocab/KV for test time) on the native bodies vs a plain torch fp32 reference
+of the same math with the same bf16 rounding points.  Tolerance: bf16
+storage of every intermediate -> |err| <= 0.05 (|ref| + 1), mean <= 5e-3.
+Then: the same step as a coroutine under quota changes is bit-identical to
+the solo step."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2603_15042_b200 import _abi
+from paper_2603_15042_b200.runtime import Domain
+from paper_2603_15042_b200.tenants import DecodeConfig, DecodeModel, pick_split
+
+pytestmark = pytest.mark.gpu
+
+
+def small_model():
+    cfg = DecodeConfig(layers=2, vocab=2048, L=96, attn_splits=2)
+    return DecodeModel(cfg, seed=5)
+
+
+def test_decode_step_matches_torch_reference():
+    m = small_model()
+    h0 = m.H[0].clone()
+    kc0 = [k.clone() for k in m.kc]
+    vc0 = [v.clone() for v in m.vc]
+    m.solo_step()
+    torch.cuda.synchronize()
+    ref_logits, ref_h = m.reference_step(h0, kc0, vc0)
+    got = m.logits.float()
+    ref = ref_logits.float()
+    err = (got - ref).abs() / (ref.abs() + 1)
+    assert float(err.max()) <= 0.05, float(err.max())
+    assert float(err.mean()) <= 5e-3, float(err.mean())
+    herr = (m.H[m.cfg.layers % 2].float() - ref_h.float()).abs() / (ref_h.float().abs() + 1)
+    assert float(herr.max()) <= 0.05
+
+
+def test_decode_step_coroutine_bit_exact_vs_solo():
+    m = small_model()
+    h0 = m.H[0].clone()
+    kc0 = [k.clone() for k in m.kc]
+    vc0 = [v.clone() for v in m.vc]
+    m.solo_step()
+    torch.cuda.synchronize()
+    solo_logits = m.logits.clone()
+    solo_h = m.H[m.cfg.layers % 2].clone()
+    # reset state, then run the same step as a coroutine with quota changes
+    m.H[0].copy_(h0)
+    for l in range(m.cfg.layers):
+        m.kc[l].copy_(kc0[l])
+        m.vc[l].copy_(vc0[l])
+    m.logits.zero_()
+    torch.cuda.synchronize()
+    with Domain(0, tiers=[Fraction(1, 2), Fraction(1)], block_log_capacity=1 << 16) as dom:
+        dom.start()
+        t = dom.tenant("decode", _abi.LATENCY_CRITICAL)
+        dom.quota_set(dom.mask(t, 0, dom.num_sms))
+        kids = m.register(dom)
+        dom.quota_at_claim(t, 3, 10, dom.mask(t, 0, 37))
+        dom.quota_at_claim(t, 6, 5, dom.mask(t, 40, 90))
+        dom.quota_at_claim(t, 9, 0, dom.mask(t, 0, dom.num_sms))
+        last = None
+        for k in kids:
+            last = dom.launch(t, k)
+        dom.wait(t, last)
+        got_logits = m.logits.cpu()
+        got_h = m.H[m.cfg.layers % 2].cpu()
+        assert dom.transcript(t) == [(k, r[2][0]) for k, r in zip(kids, m.records)]
+    assert np.array_equal(got_logits.view(torch.int16).numpy(), solo_logits.cpu().view(torch.int16).numpy())
+    assert np.array_equal(got_h.view(torch.int16).numpy(), solo_h.cpu().view(torch.int16).numpy())
