@@ -69,7 +69,9 @@ typedef enum ds_body_id {
     DS_BODY_ATTN_DECODE = 6,    /* GQA decode attention over a KV cache */
     DS_BODY_GEMM_BF16 = 7,      /* training GEMM on tcgen05/TMEM */
     DS_BODY_RMSNORM = 8,        /* row RMS statistics for the decode tenant */
-    DS_BODY_COUNT = 9
+    DS_BODY_EMBED = 9,          /* token embedding gather (decode step input) */
+    DS_BODY_ARGMAX = 10,        /* greedy sampling (decode step result) */
+    DS_BODY_COUNT = 11
 } ds_body_id;
 
 typedef enum ds_priority { DS_LATENCY_CRITICAL = 0, DS_BEST_EFFORT = 1 } ds_priority; /* types.hpp:24 */
@@ -223,6 +225,69 @@ int ds_body_smem(int body, uint32_t* bytes);
  * matrix, SWIZZLE_128B boxes of box_rows x box_cols (box_cols*2 must be 128) */
 int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                           uint32_t box_cols);
+
+/* ---- policy engine: the SimEngine dispatch loop over the executor ----
+ * (engine.hpp:152-170; Policy hooks policy.hpp:97-126; built-ins
+ * policies.hpp:12-75).  Records are the reference's Kernel launch records;
+ * each runs as >= 1 registered device kernels in program order. */
+typedef struct ds_engine ds_engine;
+
+typedef struct ds_engine_config {
+    const char* policy;        /* "slo-aware" | "tpot-first" | "temporal" | "static" */
+    int64_t quantum_ns;        /* temporal slice (PolicyConfig.quantum) */
+    double alpha;              /* predictor EWMA (PolicyConfig.predictor_alpha) */
+    int64_t cold_start_ns;     /* PolicyConfig.cold_start_prediction */
+    int release_on_idle;       /* EngineConfig.release_on_idle */
+    int fair_handover;         /* temporal: preempt the previous owner at each quantum */
+    int lend_tenant;           /* tenant run on unbound SMs (-1: strict, idle SMs stay idle) */
+    int n_assignments;         /* static partition map */
+    int32_t assign_vctx[64];
+    int32_t assign_pctx[64];
+} ds_engine_config;
+
+typedef struct ds_record_desc {
+    const char* semantic_id;
+    int64_t grid_size;         /* signature grid (predictor key) */
+    const int32_t* kernels;    /* registered kernel ids, program order */
+    int n_kernels;
+    int phase;                 /* ds_phase */
+    int64_t request;
+    int decode_index;
+    int64_t arrival_ns;        /* engine clock; 0 = now */
+    int64_t request_arrival_ns;
+    int64_t ttft_ns, tpot_ns;  /* SLO (0 = none) */
+    int64_t base_hint_ns;      /* predictor cold-start hint */
+    int64_t sat_num, sat_den;  /* compute saturation in (0, 1] */
+} ds_record_desc;
+
+typedef struct ds_record_info {
+    uint64_t id;
+    int32_t job, state;        /* state: 0 queued, 1 dispatched, 2 done */
+    int32_t pctx, preempted;
+    int32_t phase, decode_index;
+    int64_t request;
+    int64_t arrival_host_ns, dispatch_host_ns, finish_host_ns;
+    uint64_t t_first_claim, t_end; /* device %globaltimer */
+} ds_record_info;
+
+typedef struct ds_engine_counters {
+    uint64_t decisions, dispatches, completed, preemptions, migrations, unbinds, policy_errors;
+} ds_engine_counters;
+
+const char* ds_engine_last_error(void);
+int ds_engine_create(ds_domain* dom, const ds_engine_config* cfg, ds_engine** out);
+int ds_engine_destroy(ds_engine* eng);
+int ds_engine_add_job(ds_engine* eng, int tenant, int priority, int* job);
+int ds_engine_submit(ds_engine* eng, int job, const ds_record_desc* rec, uint64_t* rec_id);
+int ds_engine_start(ds_engine* eng);
+int ds_engine_stop(ds_engine* eng);
+int ds_engine_now(ds_engine* eng, int64_t* ns);
+int ds_engine_wait(ds_engine* eng, uint64_t rec_id, int timeout_ms);
+int ds_engine_record(ds_engine* eng, uint64_t rec_id, ds_record_info* out);
+int ds_engine_counters_get(ds_engine* eng, ds_engine_counters* out);
+int ds_engine_transcript(ds_engine* eng, int job, uint64_t* rec_ids, int cap, int* n);
+int ds_engine_predict(ds_engine* eng, const char* semantic_id, int64_t grid, int64_t* ns);
+int ds_policy_names(char* out, int cap);
 
 #ifdef __cplusplus
 }

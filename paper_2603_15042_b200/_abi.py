@@ -25,6 +25,8 @@ BODY_GEMV_BF16 = 5
 BODY_ATTN_DECODE = 6
 BODY_GEMM_BF16 = 7
 BODY_RMSNORM = 8
+BODY_EMBED = 9
+BODY_ARGMAX = 10
 
 LATENCY_CRITICAL, BEST_EFFORT = 0, 1
 PREFILL, DECODE, TRAINING, OTHER = 0, 1, 2, 3
@@ -197,8 +199,46 @@ class AttnArgs(ctypes.Structure):
                 ("L", ctypes.c_int32), ("Lmax", ctypes.c_int32), ("S", ctypes.c_int32), ("scale", ctypes.c_float)]
 
 
+class EmbedArgs(ctypes.Structure):
+    _fields_ = [("table", ctypes.c_uint64), ("tokens", ctypes.c_uint64), ("h", ctypes.c_uint64),
+                ("d", ctypes.c_int32), ("vocab", ctypes.c_int32)]
+
+
+class ArgmaxArgs(ctypes.Structure):
+    _fields_ = [("logits", ctypes.c_uint64), ("tokens", ctypes.c_uint64), ("vocab", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
 class SpinArgs(ctypes.Structure):
     _fields_ = [("out", ctypes.c_uint64), ("ns", ctypes.c_uint64)]
+
+
+class EngineConfig(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_char_p), ("quantum_ns", ctypes.c_int64), ("alpha", ctypes.c_double),
+                ("cold_start_ns", ctypes.c_int64), ("release_on_idle", ctypes.c_int), ("fair_handover", ctypes.c_int),
+                ("lend_tenant", ctypes.c_int), ("n_assignments", ctypes.c_int), ("assign_vctx", ctypes.c_int32 * 64),
+                ("assign_pctx", ctypes.c_int32 * 64)]
+
+
+class RecordDesc(ctypes.Structure):
+    _fields_ = [("semantic_id", ctypes.c_char_p), ("grid_size", ctypes.c_int64),
+                ("kernels", ctypes.POINTER(ctypes.c_int32)), ("n_kernels", ctypes.c_int), ("phase", ctypes.c_int),
+                ("request", ctypes.c_int64), ("decode_index", ctypes.c_int), ("arrival_ns", ctypes.c_int64),
+                ("request_arrival_ns", ctypes.c_int64), ("ttft_ns", ctypes.c_int64), ("tpot_ns", ctypes.c_int64),
+                ("base_hint_ns", ctypes.c_int64), ("sat_num", ctypes.c_int64), ("sat_den", ctypes.c_int64)]
+
+
+class RecordInfo(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_uint64), ("job", ctypes.c_int32), ("state", ctypes.c_int32),
+                ("pctx", ctypes.c_int32), ("preempted", ctypes.c_int32), ("phase", ctypes.c_int32),
+                ("decode_index", ctypes.c_int32), ("request", ctypes.c_int64), ("arrival_host_ns", ctypes.c_int64),
+                ("dispatch_host_ns", ctypes.c_int64), ("finish_host_ns", ctypes.c_int64),
+                ("t_first_claim", ctypes.c_uint64), ("t_end", ctypes.c_uint64)]
+
+
+class EngineCounters(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("decisions", "dispatches", "completed", "preemptions", "migrations",
+                                               "unbinds", "policy_errors")]
 
 
 # exported symbols the header declares (checked by the CPU test suite)
@@ -210,7 +250,9 @@ EXPORTS = [
     "ds_set_lend", "ds_quota_at_claim", "ds_quota_periodic", "ds_stats_get", "ds_transcript",
     "ds_logical_progress", "ds_block_log", "ds_switch_log", "ds_ctl_log", "ds_clear_logs",
     "ds_globaltimer", "ds_debug_dump", "ds_solo_launch", "ds_solo_launch_registered", "ds_body_smem",
-    "ds_tensor_map_bf16_2d",
+    "ds_tensor_map_bf16_2d", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
+    "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
+    "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
 ]
 
 _lib = None
@@ -269,6 +311,21 @@ def lib():
         L.ds_solo_launch_registered.argtypes = [vp, ctypes.c_int, vp]
         L.ds_body_smem.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
         L.ds_tensor_map_bf16_2d.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
+        L.ds_engine_last_error.restype = ctypes.c_char_p
+        L.ds_engine_create.argtypes = [vp, ctypes.POINTER(EngineConfig), ctypes.POINTER(vp)]
+        L.ds_engine_destroy.argtypes = [vp]
+        L.ds_engine_add_job.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.ds_engine_submit.argtypes = [vp, ctypes.c_int, ctypes.POINTER(RecordDesc), ctypes.POINTER(ctypes.c_uint64)]
+        L.ds_engine_start.argtypes = [vp]
+        L.ds_engine_stop.argtypes = [vp]
+        L.ds_engine_now.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_engine_wait.argtypes = [vp, ctypes.c_uint64, ctypes.c_int]
+        L.ds_engine_record.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(RecordInfo)]
+        L.ds_engine_counters_get.argtypes = [vp, ctypes.POINTER(EngineCounters)]
+        L.ds_engine_transcript.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_int)]
+        L.ds_engine_predict.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_policy_names.argtypes = [ctypes.c_char_p, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -276,3 +333,8 @@ def lib():
 def check(rc: int) -> None:
     if rc != 0:
         raise DsError(rc, (lib().ds_last_error() or b"").decode())
+
+
+def check_engine(rc: int) -> None:
+    if rc != 0:
+        raise DsError(rc, (lib().ds_engine_last_error() or b"").decode())

@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUTLASS_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/flashinfer/data/cutlass/include"
 
 CU_SOURCES = ["executor.cu"]
-CPP_SOURCES = ["runtime.cpp"]
+CPP_SOURCES = ["runtime.cpp", "policy.cpp", "engine.cpp"]
 
 
 def sources():
@@ -46,17 +46,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(PKG, "_obj")
     os.makedirs(objdir, exist_ok=True)
-    common = ["-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
+    common = ["-O3", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
               "-I" + CSRC]
     objs = []
     for src in CU_SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC] + common + ARCH + ["-lineinfo", "-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + common + ["-std=c++17"] + ARCH + ["-lineinfo", "-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj]
         _run(cmd, verbose)
         objs.append(obj)
     for src in CPP_SOURCES:
         obj = os.path.join(objdir, src.replace(".cpp", ".o"))
-        cmd = [NVCC] + common + ["-x", "cu"] + ARCH + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + common + ["-std=c++20", "-x", "cu"] + ARCH + ["-c", os.path.join(CSRC, src), "-o", obj]
         _run(cmd, verbose)
         objs.append(obj)
     cmd = [NVCC, "-shared", "-Xcompiler", "-fPIC"] + ARCH + objs + ["-cudart", "static", "-o", LIB,

@@ -360,3 +360,69 @@ __device__ void body_attn_decode(const BodyCtx& c) {
 }
 
 }  // namespace ds
+
+namespace ds {
+
+// ---------------------------------------------------------------------------
+// Token embedding gather (step input): h[b][:] = E[tok[b]][:].  grid 32.
+// ---------------------------------------------------------------------------
+struct EmbedArgs {
+    uint64_t table;   // bf16 [vocab][d]
+    uint64_t tokens;  // int32 [32]
+    uint64_t h;       // bf16 [32][d]
+    int32_t d, vocab;
+};
+
+__device__ void body_embed(const BodyCtx& c) {
+    const EmbedArgs& a = *reinterpret_cast<const EmbedArgs*>(c.args);
+    const int b = c.bx;
+    int tok = __ldcg(reinterpret_cast<const int*>(a.tokens) + b);
+    tok = tok < 0 ? 0 : (tok >= a.vocab ? a.vocab - 1 : tok);
+    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.table) + (size_t)tok * a.d);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.h) + (size_t)b * a.d);
+    for (int i = threadIdx.x; i < a.d / 8; i += kBodyThreads) dst[i] = __ldcs(src + i);
+    body_sync();
+}
+
+// ---------------------------------------------------------------------------
+// Greedy sampling (step result): tok[b] = argmax_v logits[b][v], lowest index
+// on ties.  grid 32, fixed-order tree -> deterministic.
+// ---------------------------------------------------------------------------
+struct ArgmaxArgs {
+    uint64_t logits;  // bf16 [32][vocab]
+    uint64_t tokens;  // int32 [32]
+    int32_t vocab;
+    int32_t pad;
+};
+
+__device__ void body_argmax(const BodyCtx& c) {
+    const ArgmaxArgs& a = *reinterpret_cast<const ArgmaxArgs*>(c.args);
+    const int b = c.bx;
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(a.logits) + (size_t)b * a.vocab;
+    float best = kNegInf;
+    int idx = 0x7fffffff;
+    for (int v = threadIdx.x; v < a.vocab; v += kBodyThreads) {
+        float f = bf16_to_f(__ldcg(row + v));
+        if (f > best) { best = f; idx = v; }
+    }
+    __shared__ float sb[kBodyThreads];
+    __shared__ int si[kBodyThreads];
+    sb[threadIdx.x] = best;
+    si[threadIdx.x] = idx;
+    body_sync();
+    for (int o = kBodyThreads / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            float f2 = sb[threadIdx.x + o];
+            int i2 = si[threadIdx.x + o];
+            if (f2 > sb[threadIdx.x] || (f2 == sb[threadIdx.x] && i2 < si[threadIdx.x])) {
+                sb[threadIdx.x] = f2;
+                si[threadIdx.x] = i2;
+            }
+        }
+        body_sync();
+    }
+    if (threadIdx.x == 0) reinterpret_cast<int*>(a.tokens)[b] = si[0];
+    body_sync();
+}
+
+}  // namespace ds

@@ -42,6 +42,8 @@ __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
         case DS_BODY_GEMV_BF16: body_gemv_bf16(c); break;
         case DS_BODY_ATTN_DECODE: body_attn_decode(c); break;
         case DS_BODY_RMSNORM: body_rmsnorm(c); break;
+        case DS_BODY_EMBED: body_embed(c); break;
+        case DS_BODY_ARGMAX: body_argmax(c); break;
         default: break;
     }
 }
@@ -544,6 +546,8 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_GEMV_BF16: return ds::kGemvScratch + (128 * 33 + 64) * 4 + 1024;
         case DS_BODY_ATTN_DECODE: return 8 * 4 * 130 * 4 + 1024;
         case DS_BODY_RMSNORM: return 1024;
+        case DS_BODY_EMBED: return 1024;
+        case DS_BODY_ARGMAX: return 1024;
         default: return ds::kDefaultSmem;
     }
 }

@@ -13,7 +13,7 @@ from fractions import Fraction
 from typing import Iterable, List, Optional, Sequence, Tuple
 
 from . import _abi
-from ._abi import check, lib
+from ._abi import check, check_engine, lib
 
 
 class Domain:
@@ -212,3 +212,86 @@ def solo_launch(device: int, semantic_id: str, body: int, grid, args, stream: in
     """Run a body standalone as a plain grid (exclusive_baseline)."""
     desc = make_desc(semantic_id, body, grid, args)
     check(lib().ds_solo_launch(device, ctypes.byref(desc), ctypes.c_void_p(stream)))
+
+
+class Engine:
+    """SimEngine-like dispatch loop over one domain (C++ engine thread).
+
+    Jobs map 1:1 to tenants; ``submit`` is the reference's kernel arrival of a
+    launch record that runs as the listed registered kernels."""
+
+    def __init__(self, dom: Domain, policy: str = "tpot-first", quantum_ns: int = 5_000_000, alpha: float = 0.3,
+                 cold_start_ns: int = 1_000_000_000, release_on_idle: bool = True, fair_handover: bool = True,
+                 lend_tenant: int = -1, assignments=None):
+        cfg = _abi.EngineConfig()
+        cfg.policy = policy.encode()
+        cfg.quantum_ns = quantum_ns
+        cfg.alpha = alpha
+        cfg.cold_start_ns = cold_start_ns
+        cfg.release_on_idle = int(release_on_idle)
+        cfg.fair_handover = int(fair_handover)
+        cfg.lend_tenant = lend_tenant
+        assignments = assignments or {}
+        cfg.n_assignments = len(assignments)
+        for i, (v, p) in enumerate(assignments.items()):
+            cfg.assign_vctx[i] = v
+            cfg.assign_pctx[i] = p
+        h = ctypes.c_void_p()
+        check_engine(lib().ds_engine_create(dom.h, ctypes.byref(cfg), ctypes.byref(h)))
+        self.h = h
+        self.dom = dom
+        self._keep = []
+
+    def add_job(self, tenant: int, priority: int) -> int:
+        out = ctypes.c_int()
+        check_engine(lib().ds_engine_add_job(self.h, tenant, priority, ctypes.byref(out)))
+        return out.value
+
+    def submit(self, job: int, kernels: Sequence[int], semantic_id: str, phase: int = _abi.OTHER, grid_size: int = 1,
+               request: int = -1, decode_index: int = -1, arrival_ns: int = 0, request_arrival_ns: int = 0,
+               ttft_ns: int = 0, tpot_ns: int = 0, base_hint_ns: int = 0, saturation: Fraction = Fraction(1)) -> int:
+        arr = (ctypes.c_int32 * len(kernels))(*kernels)
+        sat = Fraction(saturation)
+        d = _abi.RecordDesc(semantic_id.encode(), grid_size, arr, len(kernels), phase, request, decode_index,
+                            arrival_ns, request_arrival_ns, ttft_ns, tpot_ns, base_hint_ns, sat.numerator,
+                            sat.denominator)
+        out = ctypes.c_uint64()
+        check_engine(lib().ds_engine_submit(self.h, job, ctypes.byref(d), ctypes.byref(out)))
+        return out.value
+
+    def start(self):
+        check_engine(lib().ds_engine_start(self.h))
+
+    def stop(self):
+        if self.h:
+            check_engine(lib().ds_engine_stop(self.h))
+
+    def close(self):
+        if self.h:
+            lib().ds_engine_destroy(self.h)
+            self.h = None
+
+    def now(self) -> int:
+        out = ctypes.c_int64()
+        check_engine(lib().ds_engine_now(self.h, ctypes.byref(out)))
+        return out.value
+
+    def wait(self, rec: int, timeout_ms: int = 120000):
+        check_engine(lib().ds_engine_wait(self.h, rec, timeout_ms))
+
+    def record(self, rec: int) -> _abi.RecordInfo:
+        out = _abi.RecordInfo()
+        check_engine(lib().ds_engine_record(self.h, rec, ctypes.byref(out)))
+        return out
+
+    def counters(self) -> dict:
+        c = _abi.EngineCounters()
+        check_engine(lib().ds_engine_counters_get(self.h, ctypes.byref(c)))
+        return {n: getattr(c, n) for n, _ in _abi.EngineCounters._fields_}
+
+    def transcript(self, job: int) -> List[int]:
+        n = ctypes.c_int()
+        check_engine(lib().ds_engine_transcript(self.h, job, None, 0, ctypes.byref(n)))
+        arr = (ctypes.c_uint64 * max(1, n.value))()
+        check_engine(lib().ds_engine_transcript(self.h, job, arr, n.value, ctypes.byref(n)))
+        return list(arr)[:n.value]

@@ -68,6 +68,8 @@ class DecodeModel:
         self.Wgu = [w(2 * c.ffn, c.d) for _ in range(c.layers)]   # slabs of [64 gate | 64 up] rows
         self.Wd = [w(c.d, c.ffn) for _ in range(c.layers)]
         self.lm = w(c.vocab, c.d)
+        self.embed = ((torch.rand(c.vocab, c.d, device=device, generator=g) * 2 - 1)).to(torch.bfloat16)
+        self.tokens = torch.randint(0, c.vocab, (32,), device=device, generator=g, dtype=torch.int32)
         self.Lmax = c.L
         self.kc = [((torch.rand(32, c.n_kv, self.Lmax, 128, device=device, generator=g) * 2 - 1)).to(torch.bfloat16)
                    for _ in range(c.layers)]
@@ -123,6 +125,8 @@ class DecodeModel:
     def _build_args(self):
         c = self.cfg
         self.records = []  # (semantic_id, body, grid, args, bytes)
+        ea = _abi.EmbedArgs(self.embed.data_ptr(), self.tokens.data_ptr(), self.H[0].data_ptr(), c.d, c.vocab)
+        self.records.append(("decode/embed", _abi.BODY_EMBED, (32, 1, 1), ea, 32 * c.d * 2 * 2))
         ra = _abi.RmsArgs(self.H[0].data_ptr(), self.st0.data_ptr(), c.d, 0)
         self.records.append(("decode/rms0", _abi.BODY_RMSNORM, (1, 1, 1), ra, 32 * c.d * 2))
         for l in range(c.layers):
@@ -149,6 +153,8 @@ class DecodeModel:
         a, g = self._gemv(self.lm, hfin, c.vocab, c.d, self.S["lm"], _abi.GEMV_STORE, self.logits,
                           stats_in=self.st_h, P_in=c.d // 128)
         self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
+        am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), c.vocab, 0)
+        self.records.append(("decode/argmax", _abi.BODY_ARGMAX, (32, 1, 1), am, 32 * c.vocab * 2))
 
     @property
     def weight_bytes(self) -> int:
@@ -170,10 +176,11 @@ class DecodeModel:
 
     # ---- plain torch fp32 reference of the same step (numerics tests) ----
     @torch.no_grad()
-    def reference_step(self, h0: torch.Tensor, kc, vc):
+    def reference_step(self, tokens: torch.Tensor, kc, vc):
+        """fp32 torch restatement of one step; returns (logits, h_final, next tokens)."""
         c = self.cfg
         bf = torch.bfloat16
-        h = h0.clone()
+        h = self.embed[tokens.long()].clone()
         kc = [k.clone() for k in kc]
         vc = [v.clone() for v in vc]
         for l in range(c.layers):
@@ -196,7 +203,7 @@ class DecodeModel:
             h = (hmid.float() + act.float() @ self.Wd[l].float().t()).to(bf)
         rf = torch.rsqrt(h.float().pow(2).sum(-1) / c.d + c.eps)
         logits = ((h.float() @ self.lm.float().t()) * rf[:, None]).to(bf)
-        return logits, h
+        return logits, h, logits.float().argmax(-1).to(torch.int32)
 
 
 class TrainGemm:

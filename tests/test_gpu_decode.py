@@ -24,12 +24,12 @@ def small_model():
 
 def test_decode_step_matches_torch_reference():
     m = small_model()
-    h0 = m.H[0].clone()
+    tok0 = m.tokens.clone()
     kc0 = [k.clone() for k in m.kc]
     vc0 = [v.clone() for v in m.vc]
     m.solo_step()
     torch.cuda.synchronize()
-    ref_logits, ref_h = m.reference_step(h0, kc0, vc0)
+    ref_logits, ref_h, ref_tok = m.reference_step(tok0, kc0, vc0)
     got = m.logits.float()
     ref = ref_logits.float()
     err = (got - ref).abs() / (ref.abs() + 1)
@@ -37,11 +37,17 @@ def test_decode_step_matches_torch_reference():
     assert float(err.mean()) <= 5e-3, float(err.mean())
     herr = (m.H[m.cfg.layers % 2].float() - ref_h.float()).abs() / (ref_h.float().abs() + 1)
     assert float(herr.max()) <= 0.05
+    # greedy sampling: the kernel's argmax of its own logits (ties -> lowest index)
+    assert torch.equal(m.tokens.cpu(), m.logits.float().argmax(-1).to(torch.int32).cpu())
+    # and the sampled token agrees with the reference wherever the top-2 margin exceeds the tolerance
+    top2 = ref_logits.float().topk(2, -1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 0.1 * (top2[:, 0].abs() + 1)
+    assert torch.equal(m.tokens.cpu()[clear.cpu()], ref_tok.cpu()[clear.cpu()])
 
 
 def test_decode_step_coroutine_bit_exact_vs_solo():
     m = small_model()
-    h0 = m.H[0].clone()
+    tok0 = m.tokens.clone()
     kc0 = [k.clone() for k in m.kc]
     vc0 = [v.clone() for v in m.vc]
     m.solo_step()
@@ -49,7 +55,7 @@ def test_decode_step_coroutine_bit_exact_vs_solo():
     solo_logits = m.logits.clone()
     solo_h = m.H[m.cfg.layers % 2].clone()
     # reset state, then run the same step as a coroutine with quota changes
-    m.H[0].copy_(h0)
+    m.tokens.copy_(tok0)
     for l in range(m.cfg.layers):
         m.kc[l].copy_(kc0[l])
         m.vc[l].copy_(vc0[l])
