@@ -10,7 +10,18 @@
 
 namespace ds {
 
-__device__ __forceinline__ void body_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// A CTA of the executor hosts kLanes independent worker lanes; lane L owns
+// threads [256 L, 256 L + 256) for bodies.  Bodies see a lane-local thread id
+// and lane-private named barriers, so the same body code runs in either lane
+// and in the solo wrapper (lane 0).
+__device__ __forceinline__ uint32_t body_lane() { return threadIdx.x >> 8; }
+__device__ __forceinline__ uint32_t ltid() { return threadIdx.x & 255; }
+__device__ __forceinline__ void body_sync() {
+    asm volatile("bar.sync %0, 256;" ::"r"(body_lane() ? 8 : 1) : "memory");
+}
+__device__ __forceinline__ void epi_sync() {  // the 4 epilogue warps of a lane
+    asm volatile("bar.sync %0, 128;" ::"r"(body_lane() ? 12 : 7) : "memory");
+}
 
 __device__ __forceinline__ void named_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");

@@ -41,7 +41,7 @@ struct GemvArgs {
 };
 
 constexpr int kGemvBN = 32;
-constexpr int kGemvStages = 8;
+constexpr int kGemvStages = kCtasPerSm == 2 ? 4 : 8;
 constexpr uint32_t kGemvScratch = TcSmem<kGemvBN, kGemvStages>::kBytes;  // epilogue scratch offset
 
 __device__ __forceinline__ float bf16_to_f(uint16_t v) { return __uint_as_float((uint32_t)v << 16); }
@@ -50,7 +50,6 @@ __device__ __forceinline__ uint16_t f_to_bf16(float f) {
     return *reinterpret_cast<uint16_t*>(&h);
 }
 
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 7, 128;" ::: "memory"); }
 
 __device__ void body_gemv_bf16(const BodyCtx& c) {
     const GemvArgs& a = *reinterpret_cast<const GemvArgs*>(c.args);
@@ -61,7 +60,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     const int KB = a.K / kTcBK;
     const int kb0 = (int)((int64_t)s * KB / a.S), kb1 = (int)((int64_t)(s + 1) * KB / a.S);
     tc_mainloop<kGemvBN, kGemvStages>(base, &a.tmW, &a.tmX, n_blk * kTcBM, 0, kb0, kb1, c.tmem_base, true);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = ltid() >> 5, lane = ltid() & 31;
     if (warp >= 4) {
         const int q = warp & 3;
         const int row = q * 32 + lane;  // row within the slab
@@ -190,18 +189,30 @@ struct RmsArgs {
 };
 
 __device__ void body_rmsnorm(const BodyCtx& c) {
+    // grid 32: block b reduces row b in a fixed order (16-B loads, fixed tree)
     const RmsArgs& a = *reinterpret_cast<const RmsArgs*>(c.args);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint16_t* x = reinterpret_cast<const uint16_t*>(a.x);
-    for (int b = warp; b < 32; b += 8) {
-        float ss = 0.f;
-        for (int k = lane; k < a.K; k += 32) {
-            float f = bf16_to_f(__ldcg(x + (size_t)b * a.K + k));
-            ss += f * f;
-        }
+    const int b = c.bx, warp = ltid() >> 5, lane = ltid() & 31;
+    const uint4* x = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.x) + (size_t)b * a.K);
+    float ss = 0.f;
+    for (int i = ltid(); i < a.K / 8; i += kBodyThreads) {
+        uint4 v = __ldcg(x + i);
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) reinterpret_cast<float*>(a.stats)[b] = ss;
+        for (int j = 0; j < 4; ++j) {
+            float lo = __uint_as_float(w[j] << 16), hi = __uint_as_float(w[j] & 0xffff0000u);
+            ss += lo * lo + hi * hi;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    __shared__ float part_l[2][8];
+    float* part = part_l[body_lane()];
+    if (lane == 0) part[warp] = ss;
+    body_sync();
+    if (ltid() == 0) {
+        float t = 0.f;
+        for (int w = 0; w < 8; ++w) t += part[w];
+        reinterpret_cast<float*>(a.stats)[b] = t;
     }
     body_sync();
 }
@@ -228,7 +239,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
     const int bh = t % 256, sp = t / 256;
     const int b = bh >> 3, h = bh & 7;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = ltid() >> 5, lane = ltid() & 31;
     const int p0 = (int)((int64_t)sp * a.L / a.S), p1 = (int)((int64_t)(sp + 1) * a.L / a.S);
     const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q) + (size_t)b * 4096 + (h * 4) * 128;
     float qv[4][4];
@@ -250,7 +261,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
     }
-    constexpr int U = 4;
+    constexpr int U = 8;
     for (int pbase = p0 + warp * U; pbase < p1; pbase += 8 * U) {
         uint2 kr[U], vr[U];
 #pragma unroll
@@ -301,7 +312,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     }
     body_sync();
     // thread -> (head i = tid / 64, dims 2*(tid%64), +1)
-    const int i = threadIdx.x >> 6, d0 = (threadIdx.x & 63) * 2;
+    const int i = ltid() >> 6, d0 = (ltid() & 63) * 2;
     float M = kNegInf;
     for (int w = 0; w < 8; ++w) M = fmaxf(M, sm[(w * 4 + i) * 130 + 128]);
     float Ls = 0.f, A0 = 0.f, A1 = 0.f;
@@ -314,18 +325,19 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         A1 += src[d0 + 1] * f;
     }
     bool write_out = true;
-    __shared__ int last_flag;
+    __shared__ int last_flag_l[2];
+    int& last_flag = last_flag_l[body_lane()];
     if (a.S > 1) {
         float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130 + i * 130;
         ws[d0] = A0;
         ws[d0 + 1] = A1;
-        if ((threadIdx.x & 63) == 0) {
+        if ((ltid() & 63) == 0) {
             ws[128] = M;
             ws[129] = Ls;
         }
         __threadfence();
         body_sync();
-        if (threadIdx.x == 0) {
+        if (ltid() == 0) {
             uint32_t tk = atomicAdd(reinterpret_cast<uint32_t*>(a.counters) + bh, 1u);
             last_flag = tk == (uint32_t)a.S - 1;
         }
@@ -347,7 +359,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
                 A0 += __ldcg(src + d0) * f;
                 A1 += __ldcg(src + d0 + 1) * f;
             }
-            if (threadIdx.x == 0) reinterpret_cast<uint32_t*>(a.counters)[bh] = 0;
+            if (ltid() == 0) reinterpret_cast<uint32_t*>(a.counters)[bh] = 0;
         }
     }
     if (write_out) {
@@ -380,7 +392,7 @@ __device__ void body_embed(const BodyCtx& c) {
     tok = tok < 0 ? 0 : (tok >= a.vocab ? a.vocab - 1 : tok);
     const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.table) + (size_t)tok * a.d);
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.h) + (size_t)b * a.d);
-    for (int i = threadIdx.x; i < a.d / 8; i += kBodyThreads) dst[i] = __ldcs(src + i);
+    for (int i = ltid(); i < a.d / 8; i += kBodyThreads) dst[i] = __ldcs(src + i);
     body_sync();
 }
 
@@ -401,27 +413,29 @@ __device__ void body_argmax(const BodyCtx& c) {
     const uint16_t* row = reinterpret_cast<const uint16_t*>(a.logits) + (size_t)b * a.vocab;
     float best = kNegInf;
     int idx = 0x7fffffff;
-    for (int v = threadIdx.x; v < a.vocab; v += kBodyThreads) {
+    for (int v = ltid(); v < a.vocab; v += kBodyThreads) {
         float f = bf16_to_f(__ldcg(row + v));
         if (f > best) { best = f; idx = v; }
     }
-    __shared__ float sb[kBodyThreads];
-    __shared__ int si[kBodyThreads];
-    sb[threadIdx.x] = best;
-    si[threadIdx.x] = idx;
+    __shared__ float sb_l[2][kBodyThreads];
+    __shared__ int si_l[2][kBodyThreads];
+    float* sb = sb_l[body_lane()];
+    int* si = si_l[body_lane()];
+    sb[ltid()] = best;
+    si[ltid()] = idx;
     body_sync();
     for (int o = kBodyThreads / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            float f2 = sb[threadIdx.x + o];
-            int i2 = si[threadIdx.x + o];
-            if (f2 > sb[threadIdx.x] || (f2 == sb[threadIdx.x] && i2 < si[threadIdx.x])) {
-                sb[threadIdx.x] = f2;
-                si[threadIdx.x] = i2;
+        if (ltid() < o) {
+            float f2 = sb[ltid() + o];
+            int i2 = si[ltid() + o];
+            if (f2 > sb[ltid()] || (f2 == sb[ltid()] && i2 < si[ltid()])) {
+                sb[ltid()] = f2;
+                si[ltid()] = i2;
             }
         }
         body_sync();
     }
-    if (threadIdx.x == 0) reinterpret_cast<int*>(a.tokens)[b] = si[0];
+    if (ltid() == 0) reinterpret_cast<int*>(a.tokens)[b] = si[0];
     body_sync();
 }
 

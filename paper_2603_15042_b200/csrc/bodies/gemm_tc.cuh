@@ -46,8 +46,8 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
+    const int warp = ltid() >> 5, lane = ltid() & 31;
+    if (ltid() == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
@@ -103,7 +103,7 @@ __device__ __forceinline__ void tc_teardown(char* base) {
     using L = TcSmem<BN, STAGES>;
     tc::tc_fence_before();
     body_sync();
-    if (threadIdx.x == 0) {
+    if (ltid() == 0) {
         uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
         for (int s = 0; s < 2 * STAGES + 1; ++s) tc::mbar_inval(&full[s]);
     }
@@ -129,7 +129,7 @@ struct GemmArgs {
 };
 
 constexpr int kGemmBN = 256;
-constexpr int kGemmStages = 4;
+constexpr int kGemmStages = kCtasPerSm == 2 ? 2 : 4;
 
 __device__ void body_gemm_bf16(const BodyCtx& c) {
     const GemmArgs& a = *reinterpret_cast<const GemmArgs*>(c.args);
@@ -146,7 +146,7 @@ __device__ void body_gemm_bf16(const BodyCtx& c) {
     const int n_blk = r / rows;
     tc_mainloop<kGemmBN, kGemmStages>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * kGemmBN, 0, a.K / kTcBK, c.tmem_base,
                                       false);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = ltid() >> 5, lane = ltid() & 31;
     if (warp >= 4) {
         const int q = warp & 3;
         const int row = m_blk * kTcBM + q * 32 + lane;

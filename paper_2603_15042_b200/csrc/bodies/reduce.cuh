@@ -59,17 +59,18 @@ __device__ void body_reduce(const BodyCtx& c) {
     const void* in = reinterpret_cast<const void*>(a.in);
     for (int64_t base = lo; base < hi; base += kChunk) {
         int64_t cnt = hi - base < kChunk ? hi - base : kChunk;
-        for (int64_t i = threadIdx.x; i < cnt; i += kBodyThreads) stage[i] = load_val(a.fmt, in, base + i);
+        for (int64_t i = ltid(); i < cnt; i += kBodyThreads) stage[i] = load_val(a.fmt, in, base + i);
         body_sync();
-        if (threadIdx.x == 0) {
+        if (ltid() == 0) {
             int64_t i = 0;
             if (first) { acc = stage[0]; i = 1; first = false; }
             for (; i < cnt; ++i) acc = add_rn(a.fmt, acc, stage[i]);
         }
         body_sync();
     }
-    __shared__ int is_last;
-    if (threadIdx.x == 0) {
+    __shared__ int is_last_l[2];
+    int& is_last = is_last_l[body_lane()];
+    if (ltid() == 0) {
         uint32_t* partials = reinterpret_cast<uint32_t*>(a.partials);
         partials[blk] = acc;
         is_last = 0;
@@ -80,7 +81,7 @@ __device__ void body_reduce(const BodyCtx& c) {
         }
     }
     body_sync();
-    if (is_last && threadIdx.x == 0) {
+    if (is_last && ltid() == 0) {
         __threadfence();
         const volatile uint32_t* p = reinterpret_cast<const volatile uint32_t*>(a.partials);
         uint32_t r = p[0];

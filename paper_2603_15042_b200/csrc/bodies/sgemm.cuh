@@ -23,7 +23,7 @@ __device__ void body_sgemm(const BodyCtx& c) {
     const int row0 = c.by * 64, col0 = c.bx * 64;
     float (*As)[64 + 4] = reinterpret_cast<float (*)[64 + 4]>(c.smem);              // [32][68], As[k][m]
     float (*Bs)[64] = reinterpret_cast<float (*)[64]>(c.smem + 32 * 68 * sizeof(float));  // [32][64]
-    const int tid = threadIdx.x;
+    const int tid = ltid();
     const int ty = tid / 16, tx = tid % 16;
     float acc[4][4];
 #pragma unroll
@@ -74,7 +74,7 @@ struct SpinArgs {
 
 __device__ void body_spin(const BodyCtx& c) {
     const SpinArgs& a = *reinterpret_cast<const SpinArgs*>(c.args);
-    if (threadIdx.x == 0) {
+    if (ltid() == 0) {
         uint32_t blk = c.bx + c.gx * (c.by + c.gy * c.bz);
         uint64_t t0 = globaltimer();
         uint64_t t = t0;

@@ -17,22 +17,30 @@
 
 namespace ds {
 
+#ifndef DS_LANES
+#define DS_LANES 2
+#endif
+// Worker lanes per executor CTA (one CTA per SM).  Each lane = 8 body warps +
+// 1 scheduler warp with its own barriers, smem half and TMEM columns; two
+// lanes let one stream a block while the other claims / fills its pipeline.
+constexpr int kLanes = DS_LANES;
+constexpr int kCtasPerSm = kLanes;  // tile/pipeline sizing follows the number of concurrent workers per SM
 constexpr uint32_t kSat = 0x40000000u;      // claim-word block field >= kSat: kernel not open
-constexpr int kBodyThreads = 256;           // warps 0..7 run tenant bodies
-constexpr int kSchedWarp = 8;               // per-CTA scheduler warp (claims, retires, control)
-constexpr int kLoaderWarp = 9;              // CTA 0 only: host mailbox poller
-constexpr int kExecThreads = 320;
+constexpr int kBodyThreads = 256;           // warps 8L..8L+7 run lane L's tenant bodies
+constexpr int kSchedWarp0 = 8 * kLanes;     // scheduler warp of lane L = kSchedWarp0 + L
+constexpr int kLoaderWarp = 9 * kLanes;     // CTA 0 only: host mailbox poller
+constexpr int kExecThreads = 32 * (9 * kLanes + 1);
 constexpr int kMaxArgs = 512;
-constexpr uint32_t kDefaultSmem = 200 * 1024;
+constexpr uint32_t kLaneSmem = kLanes == 2 ? 104 * 1024 : 200 * 1024;  // dynamic smem per lane
+constexpr uint32_t kDefaultSmem = kLaneSmem * kLanes;
 constexpr int kMaxTriggers = 64;
 
-// Named barrier ids (0 is reserved for __syncthreads, 1 for body-internal syncs).
-constexpr int kBarBody = 1;   // 256 body threads
-constexpr int kBarFull = 2;   // scheduler staged work -> body
-constexpr int kBarEmpty = 3;  // body copied the stage -> scheduler
-constexpr int kBarDone = 4;   // body finished the block -> scheduler
+// Named barrier ids (0 reserved).  Lane 0: body 1, full 2, empty 3, done 4,
+// epilogue 7; lane 1: body 8, full 9, empty 10, done 11, epilogue 12; 5 = exit.
+__host__ __device__ constexpr int bar_full(int lane) { return lane ? 9 : 2; }
+__host__ __device__ constexpr int bar_empty(int lane) { return lane ? 10 : 3; }
+__host__ __device__ constexpr int bar_done(int lane) { return lane ? 11 : 4; }
 constexpr int kBarExit = 5;
-constexpr int kBarBody2 = 6;  // extra body-internal barrier ids for bodies (6..15)
 
 struct alignas(64) LaunchSlot {
     int32_t body;
@@ -68,8 +76,7 @@ struct ClaimTrigger {
 };
 
 struct alignas(128) DevControl {
-    int32_t owner[DS_MAX_SMS];   // by physical smid
-    int32_t lender[DS_MAX_SMS];
+    unsigned long long word[DS_MAX_SMS];  // by physical smid: (lender << 32) | owner, -1 = none
     uint32_t gen;                // bumped on every control change (any source)
     uint32_t exit;
     uint32_t pad[30];

@@ -28,7 +28,8 @@
 
 namespace ds {
 
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemCols = 512;                  // whole TMEM, split between lanes
+constexpr uint32_t kLaneTmemCols = kTmemCols / kLanes;
 
 // ---------------------------------------------------------------------------
 // Body dispatch (shared by the executor and the solo wrapper)
@@ -99,8 +100,8 @@ __device__ void install_ctl(DevState* st, const int32_t* owner, const int32_t* l
             o = owner[i];
             l = lender[i];
         }
-        st_volatile_u32(&st->ctl.owner[i], (uint32_t)o);
-        st_volatile_u32(&st->ctl.lender[i], (uint32_t)l);
+        unsigned long long w = ((unsigned long long)(uint32_t)l << 32) | (uint32_t)o;
+        asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&st->ctl.word[i]), "l"(w) : "memory");
     }
     __syncwarp();
     __threadfence();
@@ -202,26 +203,72 @@ struct Claimed {
     LaunchSlot* slot;
 };
 
-__device__ bool try_claim(DevState* st, int t, Claimed& out) {
+// Per-scheduler memo of the launch it claimed from last: while that launch
+// still had blocks, the next claim is a single atomicAdd (no pre-read).
+struct ClaimCache {
+    int32_t tenant = -1;
+    uint32_t seq = 0;
+    uint32_t grid = 0;
+    bool more = false;
+    LaunchSlot* slot = nullptr;
+};
+
+__device__ __forceinline__ LaunchSlot* slot_of(DevState* st, int t, uint32_t s) {
+    return &st->rings[(size_t)t * (st->ring_mask + 1) + (s & st->ring_mask)];
+}
+
+__device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
     DevTenant* T = &st->tenants[t];
-    unsigned long long w = ld_volatile_u64(&T->claim);
-    uint32_t s = (uint32_t)(w >> 32), b = (uint32_t)w;
-    if (b >= kSat) return false;
-    uint32_t tail = ld_acquire_u32(&T->tail);
-    if (s >= tail) return false;
-    LaunchSlot* slot = &st->rings[(size_t)t * (st->ring_mask + 1) + (s & st->ring_mask)];
-    uint32_t grid = ld_volatile_u32(&slot->grid);
-    if (b >= grid) return false;
+    uint32_t s, grid;
+    LaunchSlot* slot;
+    if (!(cc.tenant == t && cc.more)) {
+        unsigned long long w = ld_volatile_u64(&T->claim);
+        s = (uint32_t)(w >> 32);
+        uint32_t b = (uint32_t)w;
+        if (b >= kSat) return false;
+        if (cc.tenant == t && cc.seq == s) {
+            slot = cc.slot;
+            grid = cc.grid;
+        } else {
+            uint32_t tail = ld_acquire_u32(&T->tail);
+            if (s >= tail) return false;
+            slot = slot_of(st, t, s);
+            grid = ld_volatile_u32(&slot->grid);
+        }
+        if (b >= grid) {
+            cc.tenant = t;
+            cc.seq = s;
+            cc.grid = grid;
+            cc.slot = slot;
+            cc.more = false;
+            return false;
+        }
+    } else {
+        s = cc.seq;
+        grid = cc.grid;
+        slot = cc.slot;
+    }
     unsigned long long old = atomicAdd(&T->claim, 1ull);
     uint32_t s2 = (uint32_t)(old >> 32), b2 = (uint32_t)old;
-    if (b2 >= kSat) return false;
+    if (b2 >= kSat) {
+        cc.more = false;
+        return false;
+    }
     if (s2 != s) {
-        // the word advanced between our read and the add: the add landed on
-        // launch s2, which is open (block field < kSat) hence enqueued.
-        slot = &st->rings[(size_t)t * (st->ring_mask + 1) + (s2 & st->ring_mask)];
+        // the word advanced since our read: the add landed on launch s2, which
+        // is open (block field < kSat) hence enqueued
+        slot = slot_of(st, t, s2);
         grid = ld_volatile_u32(&slot->grid);
     }
-    if (b2 >= grid) return false;
+    cc.tenant = t;
+    cc.seq = s2;
+    cc.grid = grid;
+    cc.slot = slot;
+    if (b2 >= grid) {
+        cc.more = false;
+        return false;
+    }
+    cc.more = b2 + 1 < grid;
     out.tenant = t;
     out.seq = s2;
     out.block = b2;
@@ -232,8 +279,19 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out) {
 __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* slot) {
     DevTenant* T = &st->tenants[t];
     __threadfence();
-    uint64_t tend = globaltimer();
-    // device -> host completion record
+    const uint64_t tend = globaltimer();
+    // 1. advance the tenant to seq+1 first (critical path of the next kernel)
+    st_release_u32(&T->head, seq + 1);
+    const uint32_t nxt = seq + 1;
+    const uint32_t tail = ld_acquire_u32(&T->tail);
+    if (nxt < tail) {
+        atomicExch(&T->claim, (unsigned long long)nxt << 32);
+    } else {
+        atomicExch(&T->claim, ((unsigned long long)nxt << 32) | kSat);
+        __threadfence();
+        try_open(T);
+    }
+    // 2. device -> host completion record (PCIe, off the critical path)
     unsigned long long i = atomicAdd(&st->completion_count, 1ull);
     HostCompletion* hc = &st->completions[i & st->completion_mask];
     ds_completion c;
@@ -248,17 +306,6 @@ __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* s
     hc->c = c;
     __threadfence_system();
     st_release_sys_u64((void*)&hc->valid, i + 1);
-    // advance the tenant to seq+1
-    st_release_u32(&T->head, seq + 1);
-    uint32_t nxt = seq + 1;
-    uint32_t tail = ld_acquire_u32(&T->tail);
-    if (nxt < tail) {
-        atomicExch(&T->claim, (unsigned long long)nxt << 32);
-    } else {
-        atomicExch(&T->claim, ((unsigned long long)nxt << 32) | kSat);
-        __threadfence();
-        try_open(T);
-    }
 }
 
 __device__ void maybe_fire_trigger(DevState* st, const Claimed& w, int lane) {
@@ -277,7 +324,8 @@ __device__ void maybe_fire_trigger(DevState* st, const Claimed& w, int lane) {
     if (fire) install_ctl(st, tr->owner, tr->lender, false, 1, lane);
 }
 
-__device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, uint32_t sm) {
+__device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, uint32_t sm, int lane_id) {
+    const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
     const int lane = threadIdx.x & 31;
     int32_t last_tenant = -1;
     uint32_t last_seq = 0xffffffffu;
@@ -285,10 +333,11 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
     uint32_t backoff = 32;
     bool have_prev = false;
     Claimed prev{};
+    ClaimCache cc;
     for (;;) {
         // ---- retire the block the body just finished ----
         if (have_prev) {
-            named_sync(kBarDone, kBodyThreads + 32);
+            named_sync(kDone, kBodyThreads + 32);
             if (lane == 0) {
                 uint64_t t1 = globaltimer();
                 uint64_t t0 = *body_t0;
@@ -320,10 +369,11 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
         if (lane == 0) {
             for (;;) {
                 if (ld_volatile_u32(&st->ctl.exit)) { exit_now = true; break; }
-                int32_t ow = (int32_t)ld_volatile_u32(&st->ctl.owner[sm]);
-                int32_t ln = (int32_t)ld_volatile_u32(&st->ctl.lender[sm]);
-                if (ow >= 0 && ow < DS_MAX_TENANTS && try_claim(st, ow, w)) { got = true; break; }
-                if (ln >= 0 && ln < DS_MAX_TENANTS && ln != ow && try_claim(st, ln, w)) { got = true; break; }
+                const unsigned long long cw = ld_volatile_u64(&st->ctl.word[sm]);
+                const int32_t ow = (int32_t)(uint32_t)cw;
+                const int32_t ln = (int32_t)(uint32_t)(cw >> 32);
+                if (ow >= 0 && ow < DS_MAX_TENANTS && try_claim(st, ow, w, cc)) { got = true; break; }
+                if (ln >= 0 && ln < DS_MAX_TENANTS && ln != ow && try_claim(st, ln, w, cc)) { got = true; break; }
                 if (!idle_logged && last_tenant != -1 && st->slog_cap) {
                     unsigned long long i = atomicAdd(&st->slog_count, 1ull);
                     if (i < st->slog_cap) {
@@ -340,7 +390,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                     last_tenant = -1;
                 }
                 __nanosleep(backoff);
-                if (backoff < 1024) backoff <<= 1;
+                if (backoff < 256) backoff <<= 1;
             }
             if (got) {
                 backoff = 32;
@@ -361,11 +411,11 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
             }
         }
         __syncwarp();
-        named_arrive(kBarFull, kBodyThreads + 32);
+        named_arrive(kFull, kBodyThreads + 32);
         exit_now = __shfl_sync(0xffffffffu, exit_now, 0);
         got = __shfl_sync(0xffffffffu, got, 0);
         if (!got) {  // exit: let the body warps read the exit stage, then leave
-            named_sync(kBarEmpty, kBodyThreads + 32);
+            named_sync(kEmpty, kBodyThreads + 32);
             break;
         }
         w.tenant = __shfl_sync(0xffffffffu, w.tenant, 0);
@@ -397,7 +447,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
         }
         __syncwarp();
         maybe_fire_trigger(st, w, lane);
-        named_sync(kBarEmpty, kBodyThreads + 32);  // body copied the stage
+        named_sync(kEmpty, kBodyThreads + 32);  // body copied the stage
         prev = w;
         have_prev = true;
     }
@@ -407,13 +457,14 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
 // Body warps
 // ---------------------------------------------------------------------------
 __device__ void body_loop(Stage* stage, volatile uint64_t* body_t0, char* smem, uint32_t smem_bytes,
-                          uint32_t tmem_base) {
+                          uint32_t tmem_base, int lane_id) {
+    const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
     for (;;) {
-        named_sync(kBarFull, kBodyThreads + 32);
+        named_sync(kFull, kBodyThreads + 32);
         Stage s = *stage;
-        named_arrive(kBarEmpty, kBodyThreads + 32);
+        named_arrive(kEmpty, kBodyThreads + 32);
         if (s.tenant < 0) return;
-        if (threadIdx.x == 0) *body_t0 = globaltimer();
+        if (ltid() == 0) *body_t0 = globaltimer();
         BodyCtx c;
         c.gx = s.gx;
         c.gy = s.gy;
@@ -427,36 +478,38 @@ __device__ void body_loop(Stage* stage, volatile uint64_t* body_t0, char* smem, 
         c.tmem_base = tmem_base;
         run_body(s.body, c);
         __threadfence();  // this thread's writes visible at gpu scope before retire
-        named_arrive(kBarDone, kBodyThreads + 32);
+        named_arrive(kDone, kBodyThreads + 32);
     }
 }
 
 extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel(DevState* st, uint32_t smem_bytes) {
     extern __shared__ __align__(1024) char smem[];
-    __shared__ Stage stage;
-    __shared__ volatile uint64_t body_t0;
+    __shared__ Stage stage[kLanes];
+    __shared__ volatile uint64_t body_t0[kLanes];
     const int warp = threadIdx.x >> 5;
     const uint32_t sm = smid();
     if (warp == kLoaderWarp) {
         if (blockIdx.x == 0) loader_loop(st);
         return;
     }
-    // TMEM: one allocation for the CTA's lifetime, shared by all bodies
+    // TMEM: one allocation for the CTA's lifetime, split between the lanes
     __shared__ uint32_t tmem_base_sh;
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, kTmemCols);
     tc::tc_fence_before();
-    named_sync(kBarExit, kBodyThreads + 32);
+    named_sync(kBarExit, kLanes * (kBodyThreads + 32));
     tc::tc_fence_after();
-    const uint32_t tmem_base = tmem_base_sh;
-    if (warp == kSchedWarp) {
-        scheduler_loop(st, &stage, &body_t0, sm);
+    const uint32_t lane_smem = smem_bytes / kLanes;
+    if (warp >= kSchedWarp0) {
+        const int l = warp - kSchedWarp0;
+        scheduler_loop(st, &stage[l], &body_t0[l], sm, l);
     } else {
-        body_loop(&stage, &body_t0, smem, smem_bytes, tmem_base);
+        const int l = warp >> 3;
+        body_loop(&stage[l], &body_t0[l], smem + l * lane_smem, lane_smem, tmem_base_sh + l * kLaneTmemCols, l);
     }
     tc::tc_fence_before();
-    named_sync(kBarExit, kBodyThreads + 32);
+    named_sync(kBarExit, kLanes * (kBodyThreads + 32));
     tc::tc_fence_after();
-    if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
+    if (warp == 0) tc::tmem_dealloc(tmem_base_sh, kTmemCols);
 }
 
 // Solo baseline: the same body as a plain grid (exclusive_baseline,
@@ -478,7 +531,7 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     __shared__ uint32_t tmem_base_sh;
     const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16;
     if (tc_body) {
-        if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(&tmem_base_sh, kTmemCols);
+        if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(&tmem_base_sh, kLaneTmemCols);
         tc::tc_fence_before();
         __syncthreads();
         tc::tc_fence_after();
@@ -491,7 +544,7 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
         tc::tc_fence_before();
         __syncthreads();
         tc::tc_fence_after();
-        if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(c.tmem_base, kTmemCols);
+        if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(c.tmem_base, kLaneTmemCols);
     }
 }
 
@@ -510,8 +563,17 @@ extern "C" __global__ void ds_probe_kernel(uint32_t* smids, uint32_t* nsmid, uin
 }  // namespace ds
 
 // host-side launch shims (called from runtime.cpp)
-extern "C" cudaError_t ds_dev_launch_executor(ds::DevState* st, int num_ctas, uint32_t smem, cudaStream_t s) {
+static cudaError_t exec_attrs(uint32_t smem) {
     cudaError_t e = cudaFuncSetAttribute(ds::ds_executor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // all of the unified L1/shared array as shared memory: the worker CTAs of
+    // one SM must fit side by side
+    return cudaFuncSetAttribute(ds::ds_executor_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared);
+}
+
+extern "C" cudaError_t ds_dev_launch_executor(ds::DevState* st, int num_ctas, uint32_t smem, cudaStream_t s) {
+    cudaError_t e = exec_attrs(smem);
     if (e != cudaSuccess) return e;
     void* args[] = {&st, &smem};
     return cudaLaunchCooperativeKernel((void*)ds::ds_executor_kernel, dim3(num_ctas), dim3(ds::kExecThreads), args,
@@ -519,7 +581,7 @@ extern "C" cudaError_t ds_dev_launch_executor(ds::DevState* st, int num_ctas, ui
 }
 
 extern "C" cudaError_t ds_dev_executor_occupancy(uint32_t smem, int* blocks_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(ds::ds_executor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = exec_attrs(smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, ds::ds_executor_kernel, ds::kExecThreads, smem);
 }
@@ -550,4 +612,16 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_ARGMAX: return 1024;
         default: return ds::kDefaultSmem;
     }
+}
+
+extern "C" int ds_dev_ctas_per_sm(void) { return 1; }  // one CTA per SM (kLanes worker lanes inside)
+
+extern "C" int ds_dev_exec_attrs(int* regs, int* local, int* static_smem, int* max_threads) {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, ds::ds_executor_kernel) != cudaSuccess) return -1;
+    *regs = a.numRegs;
+    *local = (int)a.localSizeBytes;
+    *static_smem = (int)a.sharedSizeBytes;
+    *max_threads = a.maxThreadsPerBlock;
+    return 0;
 }

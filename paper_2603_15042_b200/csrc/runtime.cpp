@@ -32,6 +32,7 @@ extern "C" cudaError_t ds_dev_launch_solo(int body, const void* args, uint32_t g
                                           uint32_t smem, cudaStream_t s);
 extern "C" cudaError_t ds_dev_probe(int nblocks, uint32_t* smids, uint32_t* nsmid, uint64_t* timer, cudaStream_t s);
 extern "C" uint32_t ds_dev_body_smem(int body);
+extern "C" int ds_dev_ctas_per_sm(void);
 
 namespace {
 
@@ -267,8 +268,9 @@ int ds_domain_create(const ds_domain_config* cfg, ds_domain** out) {
     d->num_sms = prop.multiProcessorCount;
     if (d->num_sms > DS_MAX_SMS) return bail(fail(DS_CONFIG_ERROR, "too many SMs"));
     int occ = 0;
-    if (ds_dev_executor_occupancy(d->smem, &occ) != cudaSuccess || occ != 1)
-        return bail(fail(DS_CONFIG_ERROR, "executor must be exactly 1 CTA/SM (occupancy " + std::to_string(occ) + ")"));
+    if (ds_dev_executor_occupancy(d->smem, &occ) != cudaSuccess || occ != ds_dev_ctas_per_sm())
+        return bail(fail(DS_CONFIG_ERROR, "executor must be exactly " + std::to_string(ds_dev_ctas_per_sm()) +
+                                              " CTA(s)/SM (occupancy " + std::to_string(occ) + ")"));
 
     cudaStreamCreateWithFlags(&d->exec_stream, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
@@ -470,10 +472,7 @@ int ds_start(ds_domain* d) {
         h.tenants[t].head = (uint32_t)seq;
         d->mb->tail[t] = (uint32_t)seq;
     }
-    for (int i = 0; i < DS_MAX_SMS; ++i) {
-        h.ctl.owner[i] = -1;
-        h.ctl.lender[i] = -1;
-    }
+    for (int i = 0; i < DS_MAX_SMS; ++i) h.ctl.word[i] = ~0ull;
     h.rings = d->d_rings;
     ds::LaunchSlot* hr = nullptr;
     ds::HostMailbox* hm = nullptr;
@@ -507,7 +506,7 @@ int ds_start(ds_domain* d) {
     DS_CUDA(cudaStreamSynchronize(d->copy_stream));
     d->drain_stop = false;
     d->drainer = std::thread(drain_loop, d);
-    cudaError_t e = ds_dev_launch_executor(d->d_state, d->num_sms, d->smem, d->exec_stream);
+    cudaError_t e = ds_dev_launch_executor(d->d_state, d->num_sms * ds_dev_ctas_per_sm(), d->smem, d->exec_stream);
     if (e != cudaSuccess) {
         d->drain_stop = true;
         d->drainer.join();
@@ -954,8 +953,8 @@ int ds_debug_dump(ds_domain* d, char* out, int64_t cap) {
     }
     int owned = 0, lent = 0;
     for (int i = 0; i < DS_MAX_SMS; ++i) {
-        owned += st->ctl.owner[i] >= 0;
-        lent += st->ctl.lender[i] >= 0;
+        owned += (int32_t)(uint32_t)st->ctl.word[i] >= 0;
+        lent += (int32_t)(uint32_t)(st->ctl.word[i] >> 32) >= 0;
     }
     snprintf(line, sizeof line, "device ctl: %d SMs owned, %d with lender\n", owned, lent);
     s += line;

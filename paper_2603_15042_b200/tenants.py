@@ -128,7 +128,7 @@ class DecodeModel:
         ea = _abi.EmbedArgs(self.embed.data_ptr(), self.tokens.data_ptr(), self.H[0].data_ptr(), c.d, c.vocab)
         self.records.append(("decode/embed", _abi.BODY_EMBED, (32, 1, 1), ea, 32 * c.d * 2 * 2))
         ra = _abi.RmsArgs(self.H[0].data_ptr(), self.st0.data_ptr(), c.d, 0)
-        self.records.append(("decode/rms0", _abi.BODY_RMSNORM, (1, 1, 1), ra, 32 * c.d * 2))
+        self.records.append(("decode/rms0", _abi.BODY_RMSNORM, (32, 1, 1), ra, 32 * c.d * 2))
         for l in range(c.layers):
             hin, hout = self.H[l % 2], self.H[(l + 1) % 2]
             st_in, p_in = (self.st0, 1) if l == 0 else (self.st_h, c.d // 128)
