@@ -182,8 +182,8 @@ class GemvArgs(ctypes.Structure):
                 ("stats_out", ctypes.c_uint64), ("kcache", ctypes.c_uint64), ("vcache", ctypes.c_uint64),
                 ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("S", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("P_in", ctypes.c_int32), ("eps", ctypes.c_float), ("pos", ctypes.c_int32), ("Lmax", ctypes.c_int32),
-                ("q_dim", ctypes.c_int32), ("kv_dim", ctypes.c_int32), ("pad0", ctypes.c_int32),
-                ("pad1", ctypes.c_int32)]
+                ("q_dim", ctypes.c_int32), ("kv_dim", ctypes.c_int32), ("dbg", ctypes.c_uint64),
+                ("w_packed", ctypes.c_uint64)]
 
 
 GEMV_STORE, GEMV_RESID, GEMV_SILU_MUL, GEMV_QKV = 0, 1, 2, 3
@@ -205,8 +205,8 @@ class EmbedArgs(ctypes.Structure):
 
 
 class ArgmaxArgs(ctypes.Structure):
-    _fields_ = [("logits", ctypes.c_uint64), ("tokens", ctypes.c_uint64), ("vocab", ctypes.c_int32),
-                ("pad", ctypes.c_int32)]
+    _fields_ = [("logits", ctypes.c_uint64), ("tokens", ctypes.c_uint64), ("ws", ctypes.c_uint64),
+                ("counters", ctypes.c_uint64), ("vocab", ctypes.c_int32), ("chunks", ctypes.c_int32)]
 
 
 class SpinArgs(ctypes.Structure):

@@ -37,12 +37,15 @@ struct GemvArgs {
     int32_t pos;        // kGemvQKV: cache row written this step
     int32_t Lmax;
     int32_t q_dim, kv_dim;
-    int32_t pad0, pad1;
+    uint64_t dbg;       // optional phase timestamps [grid][8] (0 = off)
+    uint64_t w_packed;  // W pre-packed as SWIZZLE_128B [N/128][K/64][128][64] tiles (0 = use tmW)
 };
 
 constexpr int kGemvBN = 32;
-constexpr int kGemvStages = kCtasPerSm == 2 ? 4 : 8;
-constexpr uint32_t kGemvScratch = TcSmem<kGemvBN, kGemvStages>::kBytes;  // epilogue scratch offset
+constexpr int kGemvStages = kCtasPerSm == 2 ? 5 : 8;
+// epilogue scratch [128][33] fp32 + rvec/flag reuses the TMA ring: every
+// stage has been consumed once the accumulator is complete
+constexpr uint32_t kGemvScratch = 0;
 
 __device__ __forceinline__ float bf16_to_f(uint16_t v) { return __uint_as_float((uint32_t)v << 16); }
 __device__ __forceinline__ uint16_t f_to_bf16(float f) {
@@ -59,66 +62,111 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     const int n_blk = t % nb, s = t / nb;
     const int KB = a.K / kTcBK;
     const int kb0 = (int)((int64_t)s * KB / a.S), kb1 = (int)((int64_t)(s + 1) * KB / a.S);
-    tc_mainloop<kGemvBN, kGemvStages>(base, &a.tmW, &a.tmX, n_blk * kTcBM, 0, kb0, kb1, c.tmem_base, true);
+    uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
+    if (dbg && ltid() == 0) dbg[0] = globaltimer();
+    tc_mainloop<kGemvBN, kGemvStages>(base, &a.tmW, &a.tmX, n_blk * kTcBM, 0, kb0, kb1, c.tmem_base, true,
+                                      reinterpret_cast<const char*>(a.w_packed), KB);
+    if (dbg && ltid() == 128) dbg[1] = globaltimer();
     const int warp = ltid() >> 5, lane = ltid() & 31;
+    float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + rvec[32] + flag
+    float* rvec = scratch + 128 * 33;
+    volatile int* flag = reinterpret_cast<volatile int*>(scratch + 128 * 33 + 32 + 16);
+    const int q = warp & 3;
+    const int row = q * 32 + lane;  // epilogue warps: row within the slab
+    const int n = n_blk * kTcBM + row;
+    float v[32];
     if (warp >= 4) {
-        const int q = warp & 3;
-        const int row = q * 32 + lane;  // row within the slab
-        const int n = n_blk * kTcBM + row;
-        float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + flags
-        volatile int* flag = reinterpret_cast<volatile int*>(scratch + 128 * 33 + 32);
-        float* rvec = scratch + 128 * 33;
         uint32_t raw[32];
         tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16), raw);
         tc::tmem_ld_wait();
-        float v[32];
 #pragma unroll
         for (int b = 0; b < 32; ++b) v[b] = __uint_as_float(raw[b]);
-        bool proceed = true;
-        if (a.S > 1) {
+    }
+    bool proceed = true;
+    if (a.S > 1) {
+        if (warp >= 4) {
             float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.ws) + ((size_t)s * a.N + n) * 32);
 #pragma unroll
             for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            __threadfence();
-            epi_sync();
-            if (warp == 4 && lane == 0) {
-                uint32_t tk = atomicAdd(reinterpret_cast<uint32_t*>(a.counters) + n_blk, 1u);
-                *flag = (tk == (uint32_t)a.S - 1);
-            }
-            epi_sync();
-            proceed = *flag != 0;
-            if (proceed) {
-                __threadfence();
-                const float* wsr = reinterpret_cast<const float*>(a.ws);
-#pragma unroll
-                for (int b = 0; b < 32; ++b) v[b] = 0.f;
-                for (int sp = 0; sp < a.S; ++sp) {  // fixed order
-                    const float4* p = reinterpret_cast<const float4*>(wsr + ((size_t)sp * a.N + n) * 32);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        float4 x = __ldcg(p + j);
-                        v[4 * j] += x.x;
-                        v[4 * j + 1] += x.y;
-                        v[4 * j + 2] += x.z;
-                        v[4 * j + 3] += x.w;
-                    }
-                }
-                if (warp == 4 && lane == 0) reinterpret_cast<uint32_t*>(a.counters)[n_blk] = 0;
-            }
         }
+        body_sync();
+        if (ltid() == 0) {
+            // one release/acquire RMW publishes the whole CTA's partial (the
+            // bar.sync above orders the other threads' stores before it)
+            uint32_t tk;
+            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                         : "=r"(tk) : "l"(reinterpret_cast<uint32_t*>(a.counters) + n_blk) : "memory");
+            *flag = (tk == (uint32_t)a.S - 1);
+        }
+        body_sync();
+        proceed = *flag != 0;
+        if (dbg && ltid() == 0) dbg[2] = globaltimer() | ((uint64_t)proceed << 63);
+        if (proceed) {
+            // all 256 threads, coalesced: thread owns float4 f = ltid() + 256 j
+            // of the slab's [128 rows][32] block; partials summed in the fixed
+            // order s = 0..S-1
+            __threadfence();
+            const float4* wsb = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.ws) +
+                                                                (size_t)n_blk * kTcBM * 32);
+            const size_t sstride4 = (size_t)a.N * 8;
+            float4 acc[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 3
+            for (int sp = 0; sp < a.S; ++sp) {
+                float4 x[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[j] = __ldcg(wsb + sp * sstride4 + ltid() + 256 * j);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[j].x += x[j].x;
+                    acc[j].y += x[j].y;
+                    acc[j].z += x[j].z;
+                    acc[j].w += x[j].w;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int f = ltid() + 256 * j;
+                float* dst = scratch + (f >> 3) * 33 + (f & 7) * 4;
+                dst[0] = acc[j].x;
+                dst[1] = acc[j].y;
+                dst[2] = acc[j].z;
+                dst[3] = acc[j].w;
+            }
+            if (ltid() == 0) reinterpret_cast<uint32_t*>(a.counters)[n_blk] = 0;
+            body_sync();
+            if (warp >= 4) {
+#pragma unroll
+                for (int b = 0; b < 32; ++b) v[b] = scratch[row * 33 + b];
+            }
+            body_sync();  // scratch rows are rewritten by the mode epilogues below
+            if (dbg && ltid() == 0) dbg[3] = globaltimer();
+        }
+    }
+    if (warp >= 4) {
         if (proceed) {
             // RMSNorm of the input rows folded in as a per-row scale
             if (a.stats_in) {
-                if (warp == 4) {
+                float* red = scratch + 128 * 33 + 64;  // [4][32]
+                {
                     const float* st = reinterpret_cast<const float*>(a.stats_in);
+                    const int p0 = q * a.P_in / 4, p1 = (q + 1) * a.P_in / 4;
                     float ss = 0.f;
-                    for (int p = 0; p < a.P_in; ++p) ss += __ldcg(st + p * 32 + lane);
+#pragma unroll 8
+                    for (int p = p0; p < p1; ++p) ss += __ldcg(st + p * 32 + lane);
+                    red[q * 32 + lane] = ss;
+                }
+                epi_sync();
+                if (warp == 4) {
+                    const float ss = ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
                     rvec[lane] = rsqrtf(ss / (float)a.K + a.eps);
                 }
                 epi_sync();
 #pragma unroll
                 for (int b = 0; b < 32; ++b) v[b] *= rvec[b];
             }
+            if (dbg && ltid() == 128) dbg[4] = globaltimer();
             if (a.mode == kGemvStore) {
                 uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
 #pragma unroll
@@ -135,10 +183,16 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
                     scratch[row * 33 + b] = hr * hr;
                 }
                 epi_sync();
-                if (warp == 4) {  // lane = b: fixed-order sum over the 128 rows
+                {  // fixed-order sum over the 128 rows: 4 quarter sums, then in order
+                    float* red = scratch + 128 * 33 + 64;
                     float ss = 0.f;
-                    for (int r = 0; r < 128; ++r) ss += scratch[r * 33 + lane];
-                    reinterpret_cast<float*>(a.stats_out)[n_blk * 32 + lane] = ss;
+#pragma unroll 8
+                    for (int r = q * 32; r < q * 32 + 32; ++r) ss += scratch[r * 33 + lane];
+                    red[q * 32 + lane] = ss;
+                    epi_sync();
+                    if (warp == 4)
+                        reinterpret_cast<float*>(a.stats_out)[n_blk * 32 + lane] =
+                            ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
                 }
             } else if (a.mode == kGemvSiluMul) {
                 // slab rows [0,64) are gate features, [64,128) the matching up features
@@ -174,7 +228,9 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
             }
         }
     }
+    if (dbg && ltid() == 128) dbg[5] = globaltimer();
     tc_teardown<kGemvBN, kGemvStages>(base);
+    if (dbg && ltid() == 0) dbg[6] = globaltimer();
 }
 
 // ---------------------------------------------------------------------------
@@ -234,6 +290,13 @@ struct AttnArgs {
     float scale;        // 1/sqrt(128)
 };
 
+constexpr int kAttnChunk = 32;   // KV positions per staged chunk (8 KB of K + 8 KB of V)
+constexpr int kAttnStages = 4;
+constexpr uint32_t kAttnStageBytes = 2 * kAttnChunk * 128 * 2;
+constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStageBytes;       // 64 KB
+constexpr uint32_t kAttnMergeOff = kAttnBarOff + 1024;               // [8][4][130] fp32
+constexpr uint32_t kAttnSmem = kAttnMergeOff + 8 * 4 * 130 * 4 + 1024;
+
 __device__ void body_attn_decode(const BodyCtx& c) {
     const AttnArgs& a = *reinterpret_cast<const AttnArgs*>(c.args);
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
@@ -241,6 +304,33 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     const int b = bh >> 3, h = bh & 7;
     const int warp = ltid() >> 5, lane = ltid() & 31;
     const int p0 = (int)((int64_t)sp * a.L / a.S), p1 = (int)((int64_t)(sp + 1) * a.L / a.S);
+    const int nch = (p1 - p0 + kAttnChunk - 1) / kAttnChunk;
+    char* base = align1024(c.smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + kAttnBarOff);
+    uint64_t* empty = full + kAttnStages;
+    const uint16_t* kb = reinterpret_cast<const uint16_t*>(a.kcache) + ((size_t)(b * 8 + h) * a.Lmax) * 128;
+    const uint16_t* vb = reinterpret_cast<const uint16_t*>(a.vcache) + ((size_t)(b * 8 + h) * a.Lmax) * 128;
+    // the KV stream is read once per step: TMA bulk copies into a 4-deep smem ring
+    auto issue = [&](int i) {
+        const int s = i % kAttnStages;
+        const int r0 = p0 + i * kAttnChunk;
+        const int rows = min(kAttnChunk, p1 - r0);
+        const uint32_t bytes = rows * 256;
+        char* dst = base + s * kAttnStageBytes;
+        const uint64_t pol = tc::policy_evict_first();
+        tc::mbar_arrive_expect_tx(&full[s], 2 * bytes);
+        tc::bulk_g2s_hint(dst, kb + (size_t)r0 * 128, bytes, &full[s], pol);
+        tc::bulk_g2s_hint(dst + kAttnChunk * 256, vb + (size_t)r0 * 128, bytes, &full[s], pol);
+    };
+    if (ltid() == 0) {
+        for (int s = 0; s < kAttnStages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 8);
+        }
+        tc::fence_mbar_init();
+        for (int i = 0; i < min(kAttnStages, nch); ++i) issue(i);
+    }
+    body_sync();
     const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q) + (size_t)b * 4096 + (h * 4) * 128;
     float qv[4][4];
 #pragma unroll
@@ -251,8 +341,6 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         qv[i][2] = __uint_as_float(raw.y << 16) * a.scale;
         qv[i][3] = __uint_as_float(raw.y & 0xffff0000u) * a.scale;
     }
-    const uint16_t* kb = reinterpret_cast<const uint16_t*>(a.kcache) + ((size_t)(b * 8 + h) * a.Lmax) * 128;
-    const uint16_t* vb = reinterpret_cast<const uint16_t*>(a.vcache) + ((size_t)(b * 8 + h) * a.Lmax) * 128;
     float m[4], l[4], acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -261,28 +349,23 @@ __device__ void body_attn_decode(const BodyCtx& c) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
     }
-    constexpr int U = 8;
-    for (int pbase = p0 + warp * U; pbase < p1; pbase += 8 * U) {
-        uint2 kr[U], vr[U];
+    for (int ci = 0; ci < nch; ++ci) {
+        const int s = ci % kAttnStages;
+        const uint32_t ph = (ci / kAttnStages) & 1;
+        tc::mbar_wait(&full[s], ph);
+        const char* stg = base + s * kAttnStageBytes;
+        const int r0 = p0 + ci * kAttnChunk;
+        const int rows = min(kAttnChunk, p1 - r0);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int p = pbase + u;
-            if (p < p1) {
-                kr[u] = __ldcs(reinterpret_cast<const uint2*>(kb + (size_t)p * 128 + lane * 4));
-                vr[u] = __ldcs(reinterpret_cast<const uint2*>(vb + (size_t)p * 128 + lane * 4));
-            } else {
-                kr[u] = make_uint2(0, 0);
-                vr[u] = make_uint2(0, 0);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int p = pbase + u;
-            if (p >= p1) break;
-            float kf[4] = {__uint_as_float(kr[u].x << 16), __uint_as_float(kr[u].x & 0xffff0000u),
-                           __uint_as_float(kr[u].y << 16), __uint_as_float(kr[u].y & 0xffff0000u)};
-            float vf[4] = {__uint_as_float(vr[u].x << 16), __uint_as_float(vr[u].x & 0xffff0000u),
-                           __uint_as_float(vr[u].y << 16), __uint_as_float(vr[u].y & 0xffff0000u)};
+        for (int u = 0; u < kAttnChunk / 8; ++u) {
+            const int r = warp * (kAttnChunk / 8) + u;
+            if (r >= rows) break;
+            const uint2 kr = *reinterpret_cast<const uint2*>(stg + r * 256 + lane * 8);
+            const uint2 vr = *reinterpret_cast<const uint2*>(stg + kAttnChunk * 256 + r * 256 + lane * 8);
+            float kf[4] = {__uint_as_float(kr.x << 16), __uint_as_float(kr.x & 0xffff0000u),
+                           __uint_as_float(kr.y << 16), __uint_as_float(kr.y & 0xffff0000u)};
+            float vf[4] = {__uint_as_float(vr.x << 16), __uint_as_float(vr.x & 0xffff0000u),
+                           __uint_as_float(vr.y << 16), __uint_as_float(vr.y & 0xffff0000u)};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 float d = qv[i][0] * kf[0] + qv[i][1] * kf[1] + qv[i][2] * kf[2] + qv[i][3] * kf[3];
@@ -297,9 +380,15 @@ __device__ void body_attn_decode(const BodyCtx& c) {
                 m[i] = mn;
             }
         }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        if (ltid() == 0 && ci + kAttnStages < nch) {
+            tc::mbar_wait(&empty[s], ph);  // all 8 warps released this slot
+            issue(ci + kAttnStages);
+        }
     }
     // merge the 8 warps in order (smem: [8][4][130])
-    float* sm = reinterpret_cast<float*>(c.smem);
+    float* sm = reinterpret_cast<float*>(base + kAttnMergeOff);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         float* w = sm + (warp * 4 + i) * 130;
@@ -369,6 +458,8 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         *out = pack_bf16x2(A0 * inv, A1 * inv);
     }
     body_sync();
+    if (ltid() == 0)
+        for (int s = 0; s < 2 * kAttnStages; ++s) tc::mbar_inval(&full[s]);
 }
 
 }  // namespace ds
@@ -398,44 +489,85 @@ __device__ void body_embed(const BodyCtx& c) {
 
 // ---------------------------------------------------------------------------
 // Greedy sampling (step result): tok[b] = argmax_v logits[b][v], lowest index
-// on ties.  grid 32, fixed-order tree -> deterministic.
+// on ties.  Logical block t -> (row b = t % 32, chunk c = t / 32); each chunk
+// writes (max, idx); the row's last chunk (ticket) reduces chunks 0..C-1 in
+// order.  Deterministic under any schedule.
 // ---------------------------------------------------------------------------
 struct ArgmaxArgs {
-    uint64_t logits;  // bf16 [32][vocab]
-    uint64_t tokens;  // int32 [32]
+    uint64_t logits;    // bf16 [32][vocab]
+    uint64_t tokens;    // int32 [32]
+    uint64_t ws;        // {float, int} [32][chunks]
+    uint64_t counters;  // u32 [32]
     int32_t vocab;
-    int32_t pad;
+    int32_t chunks;
 };
+
+__device__ __forceinline__ void amax_merge(float& f, int& i, float f2, int i2) {
+    if (f2 > f || (f2 == f && i2 < i)) {
+        f = f2;
+        i = i2;
+    }
+}
 
 __device__ void body_argmax(const BodyCtx& c) {
     const ArgmaxArgs& a = *reinterpret_cast<const ArgmaxArgs*>(c.args);
-    const int b = c.bx;
+    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int b = t % 32, ch = t / 32;
+    const int v0 = (int)((int64_t)ch * a.vocab / a.chunks), v1 = (int)((int64_t)(ch + 1) * a.vocab / a.chunks);
     const uint16_t* row = reinterpret_cast<const uint16_t*>(a.logits) + (size_t)b * a.vocab;
     float best = kNegInf;
     int idx = 0x7fffffff;
-    for (int v = ltid(); v < a.vocab; v += kBodyThreads) {
-        float f = bf16_to_f(__ldcg(row + v));
-        if (f > best) { best = f; idx = v; }
+    // 16-B vector body over the 8-aligned interior, scalar edges
+    const int va = (v0 + 7) & ~7, vb = v1 & ~7;
+    for (int v = v0 + (int)ltid(); v < min(va, v1); v += kBodyThreads) amax_merge(best, idx, bf16_to_f(row[v]), v);
+    for (int v = va + 8 * (int)ltid(); v < vb; v += 8 * kBodyThreads) {
+        uint4 q = __ldcs(reinterpret_cast<const uint4*>(row + v));
+        uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            amax_merge(best, idx, __uint_as_float(w[j] << 16), v + 2 * j);
+            amax_merge(best, idx, __uint_as_float(w[j] & 0xffff0000u), v + 2 * j + 1);
+        }
     }
-    __shared__ float sb_l[2][kBodyThreads];
-    __shared__ int si_l[2][kBodyThreads];
+    for (int v = max(vb, va) + (int)ltid(); v < v1; v += kBodyThreads) amax_merge(best, idx, bf16_to_f(row[v]), v);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        float f2 = __shfl_xor_sync(0xffffffffu, best, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+        amax_merge(best, idx, f2, i2);
+    }
+    __shared__ float sb_l[2][8];
+    __shared__ int si_l[2][8];
+    __shared__ int last_l[2];
     float* sb = sb_l[body_lane()];
     int* si = si_l[body_lane()];
-    sb[ltid()] = best;
-    si[ltid()] = idx;
-    body_sync();
-    for (int o = kBodyThreads / 2; o > 0; o >>= 1) {
-        if (ltid() < o) {
-            float f2 = sb[ltid() + o];
-            int i2 = si[ltid() + o];
-            if (f2 > sb[ltid()] || (f2 == sb[ltid()] && i2 < si[ltid()])) {
-                sb[ltid()] = f2;
-                si[ltid()] = i2;
-            }
-        }
-        body_sync();
+    const int warp = ltid() >> 5, lane = ltid() & 31;
+    if (lane == 0) {
+        sb[warp] = best;
+        si[warp] = idx;
     }
-    if (ltid() == 0) reinterpret_cast<int*>(a.tokens)[b] = si[0];
+    body_sync();
+    if (ltid() == 0) {
+        float f = sb[0];
+        int i = si[0];
+        for (int w = 1; w < 8; ++w) amax_merge(f, i, sb[w], si[w]);
+        float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)b * a.chunks + ch) * 2;
+        ws[0] = f;
+        reinterpret_cast<int*>(ws)[1] = i;
+        __threadfence();
+        uint32_t tk = atomicAdd(reinterpret_cast<uint32_t*>(a.counters) + b, 1u);
+        last_l[body_lane()] = tk == (uint32_t)a.chunks - 1;
+        if (tk == (uint32_t)a.chunks - 1) {
+            __threadfence();
+            const float* wr = reinterpret_cast<const float*>(a.ws) + (size_t)b * a.chunks * 2;
+            float bf = __ldcg(wr);
+            int bi = __ldcg(reinterpret_cast<const int*>(wr) + 1);
+            for (int k = 1; k < a.chunks; ++k)
+                amax_merge(bf, bi, __ldcg(wr + 2 * k), __ldcg(reinterpret_cast<const int*>(wr + 2 * k) + 1));
+            reinterpret_cast<int*>(a.tokens)[b] = bi;
+            reinterpret_cast<uint32_t*>(a.counters)[b] = 0;
+        }
+    }
     body_sync();
 }
 

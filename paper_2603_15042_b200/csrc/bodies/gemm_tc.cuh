@@ -39,9 +39,14 @@ __device__ __forceinline__ char* align1024(char* p) {
 // Runs the mainloop for one logical block; on return (all 256 threads) the
 // accumulator is in TMEM columns [tmem_base, tmem_base + BN) and the epilogue
 // warps (4-7) have passed the tmem_full barrier.  Returns the smem base.
+// a_packed != nullptr: the A operand is pre-packed in HBM as the SWIZZLE_128B
+// smem image of consecutive [128 x 64] tiles (row slab a_row/128, k-block kb at
+// ((a_row/128) * a_kblocks + kb) * 16 KB), fetched with one contiguous 16-KB
+// bulk copy per stage instead of 128 strided row segments.
 template <int BN, int STAGES>
 __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
-                                            int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first) {
+                                            int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
+                                            const char* a_packed = nullptr, int a_kblocks = 0) {
     using L = TcSmem<BN, STAGES>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -58,7 +63,7 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
     body_sync();
     const int nkb = kb_end - kb_begin;
     if (warp == 0 && lane == 0) {
-        tc::tma_fence_desc(tmA);
+        if (!a_packed) tc::tma_fence_desc(tmA);
         tc::tma_fence_desc(tmB);
         const uint64_t pol = a_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
         for (int i = 0; i < nkb; ++i) {
@@ -69,7 +74,11 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             char* sb = sa + L::kABytes;
             tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
             const int k0 = (kb_begin + i) * kTcBK;
-            tc::tma_load_2d_hint(sa, tmA, &full[s], k0, a_row, pol);
+            if (a_packed)
+                tc::bulk_g2s_hint(sa, a_packed + ((size_t)(a_row / kTcBM) * a_kblocks + kb_begin + i) * L::kABytes,
+                                  L::kABytes, &full[s], pol);
+            else
+                tc::tma_load_2d_hint(sa, tmA, &full[s], k0, a_row, pol);
             tc::tma_load_2d(sb, tmB, &full[s], k0, b_row);
         }
     } else if (warp == 1 && lane == 0) {

@@ -20,9 +20,11 @@ import torch
 from . import _abi
 
 SMS = 148
+LANES = 2
+WORKERS = SMS * LANES  # concurrent logical blocks (2 worker lanes per SM)
 
 
-def pick_split(nb: int, kblocks: int, sms: int = SMS, max_s: int = 16, min_kb: int = 4, slack: float = 0.04) -> int:
+def pick_split(nb: int, kblocks: int, sms: int = WORKERS, max_s: int = 16, min_kb: int = 4, slack: float = 0.04) -> int:
     """K-split S for a GEMV with nb row slabs: the smallest S whose wave
     efficiency nblk / (ceil(nblk/sms)*sms) is within `slack` of the best,
     keeping >= min_kb k-blocks per block (fewer, larger blocks amortise the
@@ -35,6 +37,20 @@ def pick_split(nb: int, kblocks: int, sms: int = SMS, max_s: int = 16, min_kb: i
         effs[s] = n / (math.ceil(n / sms) * sms)
     best = max(effs.values())
     return min(s for s, e in effs.items() if e >= best - slack)
+
+
+def pack_sw128(W: torch.Tensor) -> torch.Tensor:
+    """[N, K] bf16 -> the SWIZZLE_128B shared-memory image of its [128 x 64]
+    tiles, tile (slab, kblock) contiguous at ((slab * K/64) + kblock) * 16 KB:
+    within a tile, row r's 16-B chunk c is stored at chunk c ^ (r % 8)
+    (exactly what a TMA SWIZZLE_128B load would place in smem)."""
+    N, K = W.shape
+    assert N % 128 == 0 and K % 64 == 0
+    t = W.reshape(N // 128, 128, K // 64, 8, 8).permute(0, 2, 1, 3, 4)  # [nb][kb][r][chunk][8]
+    r = torch.arange(128, device=W.device).view(128, 1)
+    c = torch.arange(8, device=W.device).view(1, 8)
+    src = (c ^ (r % 8)).view(1, 1, 128, 8, 1).expand(t.shape[0], t.shape[1], 128, 8, 8)
+    return torch.gather(t, 3, src).contiguous()
 
 
 @dataclass
@@ -99,10 +115,14 @@ class DecodeModel:
         self.counters = torch.zeros(max(c.vocab, 2 * c.ffn) // 128 + 1, device=device, dtype=torch.int32)
         self.attn_ws = torch.zeros(256 * c.attn_splits * 4 * 130, device=device)
         self.attn_counters = torch.zeros(256, device=device, dtype=torch.int32)
+        self.amax_ws = torch.zeros(32 * 16 * 2, device=device)
+        self.amax_counters = torch.zeros(32, device=device, dtype=torch.int32)
         self._build_args()
 
     # ---- launch records ----
     def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None):
+        Wp = pack_sw128(W)
+        self._packed.append(Wp)
         tmW = _abi.tensor_map_bf16(W.data_ptr(), N, K, 128)
         tmX = _abi.tensor_map_bf16(X.data_ptr(), 32, K, 32)
         a = _abi.GemvArgs()
@@ -120,11 +140,13 @@ class DecodeModel:
         a.pos = self.cfg.L - 1
         a.Lmax = self.Lmax
         a.q_dim, a.kv_dim = self.cfg.d, self.kv_dim
+        a.w_packed = Wp.data_ptr()
         return a, ((N // 128) * S, 1, 1)
 
     def _build_args(self):
         c = self.cfg
         self.records = []  # (semantic_id, body, grid, args, bytes)
+        self._packed = []  # pre-packed weights (the copies the GEMV bodies stream)
         ea = _abi.EmbedArgs(self.embed.data_ptr(), self.tokens.data_ptr(), self.H[0].data_ptr(), c.d, c.vocab)
         self.records.append(("decode/embed", _abi.BODY_EMBED, (32, 1, 1), ea, 32 * c.d * 2 * 2))
         ra = _abi.RmsArgs(self.H[0].data_ptr(), self.st0.data_ptr(), c.d, 0)
@@ -153,8 +175,10 @@ class DecodeModel:
         a, g = self._gemv(self.lm, hfin, c.vocab, c.d, self.S["lm"], _abi.GEMV_STORE, self.logits,
                           stats_in=self.st_h, P_in=c.d // 128)
         self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
-        am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), c.vocab, 0)
-        self.records.append(("decode/argmax", _abi.BODY_ARGMAX, (32, 1, 1), am, 32 * c.vocab * 2))
+        chunks = max(1, min(16, c.vocab // 2048))
+        am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), self.amax_ws.data_ptr(),
+                             self.amax_counters.data_ptr(), c.vocab, chunks)
+        self.records.append(("decode/argmax", _abi.BODY_ARGMAX, (32 * chunks, 1, 1), am, 32 * c.vocab * 2))
 
     @property
     def weight_bytes(self) -> int:

@@ -3,9 +3,27 @@ from paper_2603_15042_b200.tenants import pick_split
 
 
 def test_pick_split_wave_efficiency():
-    assert pick_split(48, 64) == 3       # QKV 6144 rows: 144 blocks on 148 SMs
-    assert pick_split(1002, 64) == 1     # LM head: 1002 slabs, 97% wave efficiency already
+    assert pick_split(48, 64, sms=148) == 3   # QKV 6144 rows: 144 blocks on 148 workers
+    assert pick_split(1002, 64, sms=148) == 1  # LM head: 1002 slabs, 97% wave efficiency already
+    assert pick_split(48, 64) == 6            # 288 blocks on 296 worker lanes
     assert pick_split(32, 224) >= 4      # down proj: 32 slabs need K-split
     for nb, kb in ((48, 64), (32, 64), (224, 64), (32, 224), (1002, 64)):
         s = pick_split(nb, kb)
         assert kb // s >= 4
+
+
+def test_pack_sw128_is_the_tma_swizzle_image():
+    """Weights are pre-packed as the SWIZZLE_128B smem image of [128 x 64]
+    tiles: 16-B chunk c of row r sits at chunk c ^ (r % 8)."""
+    import torch
+    from paper_2603_15042_b200.tenants import pack_sw128
+    W = torch.arange(256 * 192, dtype=torch.float32).view(256, 192).to(torch.bfloat16)
+    P = pack_sw128(W)
+    assert P.shape == (2, 3, 128, 8, 8)
+    for slab in range(2):
+        for kb in range(3):
+            t = P[slab, kb].reshape(128, 64)
+            for r in (0, 5, 8, 77, 127):
+                for c in range(8):
+                    p = c ^ (r % 8)
+                    assert torch.equal(t[r, p * 8:(p + 1) * 8], W[slab * 128 + r, kb * 64 + c * 8:kb * 64 + (c + 1) * 8])
