@@ -194,9 +194,9 @@ class RmsArgs(ctypes.Structure):
 
 
 class AttnArgs(ctypes.Structure):
-    _fields_ = [("q", ctypes.c_uint64), ("kcache", ctypes.c_uint64), ("vcache", ctypes.c_uint64),
-                ("out", ctypes.c_uint64), ("ws", ctypes.c_uint64), ("counters", ctypes.c_uint64),
-                ("L", ctypes.c_int32), ("Lmax", ctypes.c_int32), ("S", ctypes.c_int32), ("scale", ctypes.c_float)]
+    _fields_ = [("tmK", TmaDesc), ("tmV", TmaDesc), ("q", ctypes.c_uint64), ("out", ctypes.c_uint64),
+                ("ws", ctypes.c_uint64), ("counters", ctypes.c_uint64), ("L", ctypes.c_int32),
+                ("Lmax", ctypes.c_int32), ("S", ctypes.c_int32), ("scale", ctypes.c_float), ("dbg", ctypes.c_uint64)]
 
 
 class EmbedArgs(ctypes.Structure):

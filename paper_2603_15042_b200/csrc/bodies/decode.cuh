@@ -280,22 +280,32 @@ __device__ void body_rmsnorm(const BodyCtx& c) {
 // warps merge in order 0..7, splits merge in order 0..S-1 (last block).
 // ---------------------------------------------------------------------------
 struct AttnArgs {
+    TmaDesc tmK;        // K cache viewed as [32*8*Lmax][128] bf16, box {64, 32}, SWIZZLE_128B
+    TmaDesc tmV;        // V cache, same view
     uint64_t q;         // bf16 [32][32*128]
-    uint64_t kcache;    // bf16 [32][8][Lmax][128]
-    uint64_t vcache;
     uint64_t out;       // bf16 [32][32*128]
     uint64_t ws;        // fp32 [256][S][4][130]
     uint64_t counters;  // u32 [256]
     int32_t L, Lmax, S;
     float scale;        // 1/sqrt(128)
+    uint64_t dbg;       // optional [grid][8] timestamps
 };
 
-constexpr int kAttnChunk = 32;   // KV positions per staged chunk (8 KB of K + 8 KB of V)
+constexpr int kAttnChunk = 32;   // KV positions per staged chunk
 constexpr int kAttnStages = 4;
-constexpr uint32_t kAttnStageBytes = 2 * kAttnChunk * 128 * 2;
+constexpr uint32_t kAttnHalf = kAttnChunk * 128;                      // [32 rows][64 dims] bf16 = 4 KB
+constexpr uint32_t kAttnStageBytes = 4 * kAttnHalf;                   // K lo/hi + V lo/hi = 16 KB
 constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStageBytes;       // 64 KB
-constexpr uint32_t kAttnMergeOff = kAttnBarOff + 1024;               // [8][4][130] fp32
-constexpr uint32_t kAttnSmem = kAttnMergeOff + 8 * 4 * 130 * 4 + 1024;
+constexpr uint32_t kAttnQOff = kAttnBarOff + 1024;                    // q fp32 [4][128]
+constexpr uint32_t kAttnSOff = kAttnQOff + 4 * 128 * 4;               // scores fp32 [2][4][32]
+constexpr uint32_t kAttnMergeOff = kAttnSOff + (2 * 4 * 32 + 8 * 32) * 4;  // scores + probabilities
+constexpr uint32_t kAttnSmem = kAttnMergeOff + 8 * 130 * 4 + 1024;
+
+// element (row r, dim d in [0,64)) of a SWIZZLE_128B [32][64] bf16 tile
+__device__ __forceinline__ const uint16_t* sw128_at(const char* tile, int r, int d) {
+    const int chunk = (d >> 3) ^ (r & 7);
+    return reinterpret_cast<const uint16_t*>(tile + r * 128 + chunk * 16) + (d & 7);
+}
 
 __device__ void body_attn_decode(const BodyCtx& c) {
     const AttnArgs& a = *reinterpret_cast<const AttnArgs*>(c.args);
@@ -308,19 +318,22 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     char* base = align1024(c.smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(base + kAttnBarOff);
     uint64_t* empty = full + kAttnStages;
-    const uint16_t* kb = reinterpret_cast<const uint16_t*>(a.kcache) + ((size_t)(b * 8 + h) * a.Lmax) * 128;
-    const uint16_t* vb = reinterpret_cast<const uint16_t*>(a.vcache) + ((size_t)(b * 8 + h) * a.Lmax) * 128;
-    // the KV stream is read once per step: TMA bulk copies into a 4-deep smem ring
+    float* qs = reinterpret_cast<float*>(base + kAttnQOff);
+    float* S = reinterpret_cast<float*>(base + kAttnSOff);
+    const int row0 = (b * 8 + h) * a.Lmax + p0;
+    uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
+    uint64_t t_wait = 0, t_a = 0, t_b = 0, t_sync = 0;
+    if (dbg && ltid() == 32) dbg[0] = globaltimer();
     auto issue = [&](int i) {
         const int s = i % kAttnStages;
-        const int r0 = p0 + i * kAttnChunk;
-        const int rows = min(kAttnChunk, p1 - r0);
-        const uint32_t bytes = rows * 256;
         char* dst = base + s * kAttnStageBytes;
+        const int r = row0 + i * kAttnChunk;
         const uint64_t pol = tc::policy_evict_first();
-        tc::mbar_arrive_expect_tx(&full[s], 2 * bytes);
-        tc::bulk_g2s_hint(dst, kb + (size_t)r0 * 128, bytes, &full[s], pol);
-        tc::bulk_g2s_hint(dst + kAttnChunk * 256, vb + (size_t)r0 * 128, bytes, &full[s], pol);
+        tc::mbar_arrive_expect_tx(&full[s], kAttnStageBytes);
+        tc::tma_load_2d_hint(dst, &a.tmK, &full[s], 0, r, pol);
+        tc::tma_load_2d_hint(dst + kAttnHalf, &a.tmK, &full[s], 64, r, pol);
+        tc::tma_load_2d_hint(dst + 2 * kAttnHalf, &a.tmV, &full[s], 0, r, pol);
+        tc::tma_load_2d_hint(dst + 3 * kAttnHalf, &a.tmV, &full[s], 64, r, pol);
     };
     if (ltid() == 0) {
         for (int s = 0; s < kAttnStages; ++s) {
@@ -328,58 +341,103 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             tc::mbar_init(&empty[s], 8);
         }
         tc::fence_mbar_init();
+        tc::tma_fence_desc(&a.tmK);
+        tc::tma_fence_desc(&a.tmV);
         for (int i = 0; i < min(kAttnStages, nch); ++i) issue(i);
     }
+    {  // q (4 heads of this kv group) -> smem fp32, pre-scaled
+        const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q) + (size_t)b * 4096 + (h * 4) * 128;
+        for (int i = ltid(); i < 512; i += kBodyThreads) qs[i] = bf16_to_f(__ldcg(qb + i)) * a.scale;
+    }
     body_sync();
-    const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q) + (size_t)b * 4096 + (h * 4) * 128;
-    float qv[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        uint2 raw = __ldcg(reinterpret_cast<const uint2*>(qb + i * 128 + lane * 4));
-        qv[i][0] = __uint_as_float(raw.x << 16) * a.scale;
-        qv[i][1] = __uint_as_float(raw.x & 0xffff0000u) * a.scale;
-        qv[i][2] = __uint_as_float(raw.y << 16) * a.scale;
-        qv[i][3] = __uint_as_float(raw.y & 0xffff0000u) * a.scale;
-    }
-    float m[4], l[4], acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        m[i] = kNegInf;
-        l[i] = 0.f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-    }
+    // phase A role: head ha = warp & 3, positions pa = (warp >> 2) * 16 + (lane & 15), dims half dha = lane >> 4
+    const int ha = warp & 3, pa = (warp >> 2) * 16 + (lane & 15), dha = lane >> 4;
+    // phase B role: head hb = warp & 3, dims half dhb = warp >> 2, dims dhb*64 + 2*lane, +1
+    const int hb = warp & 3, dhb = warp >> 2;
+    float m = kNegInf, lsum = 0.f, acc0 = 0.f, acc1 = 0.f;
     for (int ci = 0; ci < nch; ++ci) {
         const int s = ci % kAttnStages;
         const uint32_t ph = (ci / kAttnStages) & 1;
+        uint64_t tw0 = dbg ? globaltimer() : 0;
         tc::mbar_wait(&full[s], ph);
+        uint64_t tw1 = dbg ? globaltimer() : 0;
+        t_wait += tw1 - tw0;
         const char* stg = base + s * kAttnStageBytes;
-        const int r0 = p0 + ci * kAttnChunk;
-        const int rows = min(kAttnChunk, p1 - r0);
+        const int valid = min(kAttnChunk, p1 - (p0 + ci * kAttnChunk));
+        float* Sc = S + (ci & 1) * 128;  // double-buffered [4][32]
+        {   // ---- phase A: scores S[ha][pa] = q[ha] . K[pa] ----
+            const char* kt = stg + dha * kAttnHalf;
+            const float* qh = qs + ha * 128 + dha * 64;
+            float part[4] = {0.f, 0.f, 0.f, 0.f};  // independent chains
 #pragma unroll
-        for (int u = 0; u < kAttnChunk / 8; ++u) {
-            const int r = warp * (kAttnChunk / 8) + u;
-            if (r >= rows) break;
-            const uint2 kr = *reinterpret_cast<const uint2*>(stg + r * 256 + lane * 8);
-            const uint2 vr = *reinterpret_cast<const uint2*>(stg + kAttnChunk * 256 + r * 256 + lane * 8);
-            float kf[4] = {__uint_as_float(kr.x << 16), __uint_as_float(kr.x & 0xffff0000u),
-                           __uint_as_float(kr.y << 16), __uint_as_float(kr.y & 0xffff0000u)};
-            float vf[4] = {__uint_as_float(vr.x << 16), __uint_as_float(vr.x & 0xffff0000u),
-                           __uint_as_float(vr.y << 16), __uint_as_float(vr.y & 0xffff0000u)};
+            for (int jh = 0; jh < 8; jh += 4) {
+                uint4 kk[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float d = qv[i][0] * kf[0] + qv[i][1] * kf[1] + qv[i][2] * kf[2] + qv[i][3] * kf[3];
+                for (int j = 0; j < 4; ++j) kk[j] = *reinterpret_cast<const uint4*>(sw128_at(kt, pa, (jh + j) * 8));
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                const float mn = fmaxf(m[i], d);
-                const float alpha = __expf(m[i] - mn);
-                const float pexp = __expf(d - mn);
-                l[i] = l[i] * alpha + pexp;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = acc[i][j] * alpha + pexp * vf[j];
-                m[i] = mn;
+                for (int j = 0; j < 4; ++j) {
+                    const float4 qa = *reinterpret_cast<const float4*>(qh + (jh + j) * 8);
+                    const float4 qb4 = *reinterpret_cast<const float4*>(qh + (jh + j) * 8 + 4);
+                    part[0] = fmaf(qa.x, __uint_as_float(kk[j].x << 16), part[0]);
+                    part[1] = fmaf(qa.y, __uint_as_float(kk[j].x & 0xffff0000u), part[1]);
+                    part[2] = fmaf(qa.z, __uint_as_float(kk[j].y << 16), part[2]);
+                    part[3] = fmaf(qa.w, __uint_as_float(kk[j].y & 0xffff0000u), part[3]);
+                    part[0] = fmaf(qb4.x, __uint_as_float(kk[j].z << 16), part[0]);
+                    part[1] = fmaf(qb4.y, __uint_as_float(kk[j].z & 0xffff0000u), part[1]);
+                    part[2] = fmaf(qb4.z, __uint_as_float(kk[j].w << 16), part[2]);
+                    part[3] = fmaf(qb4.w, __uint_as_float(kk[j].w & 0xffff0000u), part[3]);
+                }
             }
+            float d = (part[0] + part[1]) + (part[2] + part[3]);
+            d += __shfl_xor_sync(0xffffffffu, d, 16);  // the two 64-dim halves
+            if (dha == 0) Sc[ha * 32 + pa] = pa < valid ? d : kNegInf;
         }
+        uint64_t ta1 = dbg ? globaltimer() : 0;
+        t_a += ta1 - tw1;
+        body_sync();
+        uint64_t ts1 = dbg ? globaltimer() : 0;
+        t_sync += ts1 - ta1;
+        {   // ---- softmax for this chunk (one rescale) + phase B: acc += p . V ----
+            const float sl = Sc[hb * 32 + lane];
+            float cm = sl;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+            const float mn = fmaxf(m, cm);
+            const float alpha = __expf(m - mn);
+            const float pl = __expf(sl - mn);  // 0 for masked positions
+            float ps = pl;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            lsum = lsum * alpha + ps;
+            acc0 *= alpha;
+            acc1 *= alpha;
+            m = mn;
+            const char* vt = stg + (2 + dhb) * kAttnHalf;
+            float* Pw = S + 256 + warp * 32;  // this warp's probabilities (smem, broadcast reads)
+            Pw[lane] = pl;
+            __syncwarp();
+            float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ph2 = 0; ph2 < kAttnChunk; ph2 += 16) {
+                uint32_t vv[16];
+#pragma unroll
+                for (int p = 0; p < 16; ++p) vv[p] = *reinterpret_cast<const uint32_t*>(sw128_at(vt, ph2 + p, 2 * lane));
+#pragma unroll
+                for (int p = 0; p < 16; p += 4) {
+                    const float4 p4 = *reinterpret_cast<const float4*>(Pw + ph2 + p);
+                    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        a0[u] = fmaf(pv[u], __uint_as_float(vv[p + u] << 16), a0[u]);
+                        a1[u] = fmaf(pv[u], __uint_as_float(vv[p + u] & 0xffff0000u), a1[u]);
+                    }
+                }
+            }
+            acc0 += (a0[0] + a0[1]) + (a0[2] + a0[3]);
+            acc1 += (a1[0] + a1[1]) + (a1[2] + a1[3]);
+            __syncwarp();
+        }
+        if (dbg) t_b += globaltimer() - ts1;
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&empty[s]);
         if (ltid() == 0 && ci + kAttnStages < nch) {
@@ -387,60 +445,45 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             issue(ci + kAttnStages);
         }
     }
-    // merge the 8 warps in order (smem: [8][4][130])
-    float* sm = reinterpret_cast<float*>(base + kAttnMergeOff);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        float* w = sm + (warp * 4 + i) * 130;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) w[lane * 4 + j] = acc[i][j];
-        if (lane == 0) {
-            w[128] = m[i];
-            w[129] = l[i];
-        }
+    if (dbg && ltid() == 32) {
+        dbg[1] = globaltimer();
+        dbg[2] = t_wait;
+        dbg[3] = t_a;
+        dbg[4] = t_sync;
+        dbg[5] = t_b;
     }
-    body_sync();
-    // thread -> (head i = tid / 64, dims 2*(tid%64), +1)
-    const int i = ltid() >> 6, d0 = (ltid() & 63) * 2;
-    float M = kNegInf;
-    for (int w = 0; w < 8; ++w) M = fmaxf(M, sm[(w * 4 + i) * 130 + 128]);
-    float Ls = 0.f, A0 = 0.f, A1 = 0.f;
-    for (int w = 0; w < 8; ++w) {
-        const float* src = sm + (w * 4 + i) * 130;
-        const float mw = src[128];
-        const float f = (mw == kNegInf) ? 0.f : __expf(mw - M);
-        Ls += src[129] * f;
-        A0 += src[d0] * f;
-        A1 += src[d0 + 1] * f;
-    }
+    // each (head hb, dims half dhb) warp owns final (m, l, acc) for 64 dims
+    const int d0 = dhb * 64 + 2 * lane;
     bool write_out = true;
     __shared__ int last_flag_l[2];
     int& last_flag = last_flag_l[body_lane()];
+    float M = m, Ls = lsum, A0 = acc0, A1 = acc1;
     if (a.S > 1) {
-        float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130 + i * 130;
+        float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130 + hb * 130;
         ws[d0] = A0;
         ws[d0 + 1] = A1;
-        if ((ltid() & 63) == 0) {
+        if (lane == 0 && dhb == 0) {
             ws[128] = M;
             ws[129] = Ls;
         }
-        __threadfence();
         body_sync();
         if (ltid() == 0) {
-            uint32_t tk = atomicAdd(reinterpret_cast<uint32_t*>(a.counters) + bh, 1u);
+            uint32_t tk;
+            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                         : "=r"(tk) : "l"(reinterpret_cast<uint32_t*>(a.counters) + bh) : "memory");
             last_flag = tk == (uint32_t)a.S - 1;
         }
         body_sync();
         write_out = last_flag != 0;
         if (write_out) {
             __threadfence();
-            const float* wsb = reinterpret_cast<const float*>(a.ws) + (size_t)bh * a.S * 4 * 130 + i * 130;
+            const float* wsb = reinterpret_cast<const float*>(a.ws) + (size_t)bh * a.S * 4 * 130 + hb * 130;
             M = kNegInf;
             for (int s2 = 0; s2 < a.S; ++s2) M = fmaxf(M, __ldcg(wsb + s2 * 4 * 130 + 128));
             Ls = 0.f;
             A0 = 0.f;
             A1 = 0.f;
-            for (int s2 = 0; s2 < a.S; ++s2) {
+            for (int s2 = 0; s2 < a.S; ++s2) {  // fixed order
                 const float* src = wsb + s2 * 4 * 130;
                 const float mw = __ldcg(src + 128);
                 const float f = (mw == kNegInf) ? 0.f : __expf(mw - M);
@@ -454,10 +497,11 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     if (write_out) {
         const float inv = 1.f / Ls;
         uint32_t* out = reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(a.out) + (size_t)b * 4096 +
-                                                    (h * 4 + i) * 128 + d0);
+                                                    (h * 4 + hb) * 128 + d0);
         *out = pack_bf16x2(A0 * inv, A1 * inv);
     }
     body_sync();
+    if (dbg && ltid() == 32) dbg[6] = globaltimer();
     if (ltid() == 0)
         for (int s = 0; s < 2 * kAttnStages; ++s) tc::mbar_inval(&full[s]);
 }

@@ -157,9 +157,11 @@ class DecodeModel:
             a, g = self._gemv(self.Wqkv[l], hin, self.qkv_n, c.d, self.S["qkv"], _abi.GEMV_QKV, self.q,
                               stats_in=st_in, P_in=p_in, l=l)
             self.records.append((f"decode/qkv", _abi.BODY_GEMV_BF16, g, a, self.qkv_n * c.d * 2))
-            at = _abi.AttnArgs(self.q.data_ptr(), self.kc[l].data_ptr(), self.vc[l].data_ptr(), self.attn.data_ptr(),
-                               self.attn_ws.data_ptr(), self.attn_counters.data_ptr(), c.L, self.Lmax, c.attn_splits,
-                               1.0 / math.sqrt(128))
+            rows = 32 * c.n_kv * self.Lmax
+            at = _abi.AttnArgs(_abi.tensor_map_bf16(self.kc[l].data_ptr(), rows, 128, 32),
+                               _abi.tensor_map_bf16(self.vc[l].data_ptr(), rows, 128, 32), self.q.data_ptr(),
+                               self.attn.data_ptr(), self.attn_ws.data_ptr(), self.attn_counters.data_ptr(), c.L,
+                               self.Lmax, c.attn_splits, 1.0 / math.sqrt(128))
             self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,
                                  2 * 32 * c.n_kv * c.L * 128 * 2))
             a, g = self._gemv(self.Wo[l], self.attn, c.d, c.d, self.S["o"], _abi.GEMV_RESID, self.h_mid, resid=hin,
