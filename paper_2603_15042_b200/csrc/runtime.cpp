@@ -171,7 +171,11 @@ int push_control(ds_domain* d) {
         int sm = d->smids[s];
         int32_t o = d->owner[s];
         int32_t l = d->lender[s];
-        if (d->lend_idle && l < 0 && d->lend_tenant >= 0 && o != d->lend_tenant) l = d->lend_tenant;
+        // idle-SM lending: only SMs bound to no pctx run the lend tenant; an
+        // SM owned by a tenant never runs another tenant's blocks in its gaps
+        // (a latency-critical owner would wait a whole foreign block on every
+        // kernel boundary)
+        if (d->lend_idle && l < 0 && o < 0 && d->lend_tenant >= 0) l = d->lend_tenant;
         d->mb->owner[sm] = o;
         d->mb->lender[sm] = l;
     }
