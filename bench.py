@@ -48,6 +48,18 @@ def nearest_rank(samples, pct):
     return s[k - 1]
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read+write per launch of this body from the committed ncu
+    capture (profiles/r1_ncu_summary.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_summary.json")))["kernels"]
+        key = {"decode/attn": "attn", "decode/gate_up": "gate_up", "decode/lm_head": "lm_head",
+               "train/gemm_bf16": "gemm"}.get(kernel)
+        return int(d[key]["traffic_bytes"]) if key in d else None
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         p = json.load(open(PEAKS_PATH))
@@ -395,15 +407,42 @@ def gpu_arm(args, rank, world):
         "e2e": {"value": round(p99_e2e, 4), "unit": "ms (P99 TPOT, host token loop)",
                 "h2d_bytes_per_step": 32 * 4 * args.tokens, "d2h_bytes_per_step": 32 * 4 * args.tokens},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": round(gemv_gbs, 1), "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(gemv_gbs / peaks["hbm_gbs"], 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(gemv_gbs / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(top),
+                     "algorithmic_bytes": bytes_by[top],
                      "peak_source": peaks_src},
         "roofline_gemm": {"bound": "tensor", "kernel": "train/gemm_bf16", "achieved": round(gemm_tf, 1),
                           "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                          "frac": round(gemm_tf / peaks["bf16_tflops"], 4), "peak_source": peaks_src},
+                          "frac": round(gemm_tf / peaks["bf16_tflops"], 4), "peak_source": peaks_src,
+                          "traffic": ncu_traffic("train/gemm_bf16"), "algorithmic_bytes": 3 * 8192 * 8192 * 2},
         "clocks": clocks,
         "gpu_launches": len(m.records) * (args.steps + args.warmup) * args.tokens,
     }
     return out, solo
+
+
+def aggregate_ranks(vals):
+    """Whole-job line from per-rank lines (independent domains, weak scaling):
+    latency metrics take the worst rank, throughputs sum, timing is the max
+    over ranks."""
+    out = dict(vals[0])
+    out["value"] = max(v["value"] for v in vals)
+    out["train_tflops"] = round(sum(v["train_tflops"] for v in vals), 1)
+    out["e2e"] = dict(vals[0]["e2e"])
+    out["e2e"]["value"] = max(v["e2e"]["value"] for v in vals)
+    out["ms_per_step"] = max(v["ms_per_step"] for v in vals)
+    out["timeslice"] = {"p99_tpot_ms": max(v["timeslice"]["p99_tpot_ms"] for v in vals),
+                        "train_tflops": round(sum(v["timeslice"]["train_tflops"] for v in vals), 1)}
+    out["bit_exact_vs_solo"] = all(v["bit_exact_vs_solo"] for v in vals)
+    out["gpu_launches"] = sum(v["gpu_launches"] for v in vals)
+    out["n_gpus"] = len(vals)
+    return out
+
+
+def gather_ranks(out, world):
+    import torch.distributed as dist
+    vals = [None] * world
+    dist.all_gather_object(vals, out)
+    return aggregate_ranks(vals)
 
 
 def main():
@@ -453,14 +492,7 @@ def main():
         return
     out, solo = gpu_arm(args, rank, world)
     if world > 1:
-        import torch.distributed as dist
-        vals = [None] * world
-        dist.all_gather_object(vals, out)
-        if rank == 0:
-            out["value"] = max(v["value"] for v in vals)
-            out["train_tflops"] = round(sum(v["train_tflops"] for v in vals), 1)
-            out["e2e"]["value"] = max(v["e2e"]["value"] for v in vals)
-            out["ms_per_step"] = max(v["ms_per_step"] for v in vals)
+        out = gather_ranks(out, world)
     if rank == 0:
         if not args.no_cpu_baseline:
             try:
