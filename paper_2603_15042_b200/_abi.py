@@ -162,6 +162,12 @@ def tensor_map_bf16(ptr: int, rows: int, cols: int, box_rows: int, box_cols: int
     return d
 
 
+def tensor_map_kv(ptr: int, rows: int, box_rows: int = 32) -> TmaDesc:
+    d = TmaDesc()
+    check(lib().ds_tensor_map_bf16_kv(ctypes.byref(d), ctypes.c_void_p(ptr), rows, box_rows))
+    return d
+
+
 GEMM_BM, GEMM_BN = 128, 256
 
 
@@ -250,7 +256,7 @@ EXPORTS = [
     "ds_set_lend", "ds_quota_at_claim", "ds_quota_periodic", "ds_stats_get", "ds_transcript",
     "ds_logical_progress", "ds_block_log", "ds_switch_log", "ds_ctl_log", "ds_clear_logs",
     "ds_globaltimer", "ds_debug_dump", "ds_solo_launch", "ds_solo_launch_registered", "ds_body_smem",
-    "ds_tensor_map_bf16_2d", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
+    "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_kv", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
 ]
@@ -311,6 +317,7 @@ def lib():
         L.ds_solo_launch_registered.argtypes = [vp, ctypes.c_int, vp]
         L.ds_body_smem.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
         L.ds_tensor_map_bf16_2d.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
+        L.ds_tensor_map_bf16_kv.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint32]
         L.ds_engine_last_error.restype = ctypes.c_char_p
         L.ds_engine_create.argtypes = [vp, ctypes.POINTER(EngineConfig), ctypes.POINTER(vp)]
         L.ds_engine_destroy.argtypes = [vp]

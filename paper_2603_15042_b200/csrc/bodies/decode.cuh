@@ -280,7 +280,7 @@ __device__ void body_rmsnorm(const BodyCtx& c) {
 // warps merge in order 0..7, splits merge in order 0..S-1 (last block).
 // ---------------------------------------------------------------------------
 struct AttnArgs {
-    TmaDesc tmK;        // K cache viewed as [32*8*Lmax][128] bf16, box {64, 32}, SWIZZLE_128B
+    TmaDesc tmK;        // K cache rows as a {64, 2, rows} view, box {64, 2, 32}: 8 KB contiguous, SWIZZLE_128B
     TmaDesc tmV;        // V cache, same view
     uint64_t q;         // bf16 [32][32*128]
     uint64_t out;       // bf16 [32][32*128]
@@ -291,21 +291,50 @@ struct AttnArgs {
     uint64_t dbg;       // optional [grid][8] timestamps
 };
 
-constexpr int kAttnChunk = 32;   // KV positions per staged chunk
-constexpr int kAttnStages = 4;
-constexpr uint32_t kAttnHalf = kAttnChunk * 128;                      // [32 rows][64 dims] bf16 = 4 KB
-constexpr uint32_t kAttnStageBytes = 4 * kAttnHalf;                   // K lo/hi + V lo/hi = 16 KB
+constexpr int kAttnChunk = 64;   // KV positions per staged chunk (8 n-tiles: one per warp in QK)
+constexpr int kAttnStages = 3;
+constexpr uint32_t kAttnTile = kAttnChunk * 256;                      // 64 rows x 128 dims bf16 = 16 KB
+constexpr uint32_t kAttnStageBytes = 2 * kAttnTile;                   // K + V = 32 KB
 constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStageBytes;       // 64 KB
-constexpr uint32_t kAttnQOff = kAttnBarOff + 1024;                    // q fp32 [4][128]
-constexpr uint32_t kAttnSOff = kAttnQOff + 4 * 128 * 4;               // scores fp32 [2][4][32]
-constexpr uint32_t kAttnMergeOff = kAttnSOff + (2 * 4 * 32 + 8 * 32) * 4;  // scores + probabilities
-constexpr uint32_t kAttnSmem = kAttnMergeOff + 8 * 130 * 4 + 1024;
+constexpr uint32_t kAttnSOff = kAttnBarOff + 1024;                    // scores fp32 [4][64]
+constexpr uint32_t kAttnSmem = kAttnSOff + 4 * kAttnChunk * 4 + 1024;
 
-// element (row r, dim d in [0,64)) of a SWIZZLE_128B [32][64] bf16 tile
-__device__ __forceinline__ const uint16_t* sw128_at(const char* tile, int r, int d) {
-    const int chunk = (d >> 3) ^ (r & 7);
-    return reinterpret_cast<const uint16_t*>(tile + r * 128 + chunk * 16) + (d & 7);
+// byte address of (position r, dim d (multiple of 8)) in a K/V tile loaded
+// through the {64, 2, rows} view: smem 128-B row R = 2r + d/64, SWIZZLE_128B
+__device__ __forceinline__ uint32_t kv_addr(uint32_t tile, int r, int d) {
+    const int R = 2 * r + (d >> 6);
+    return tile + R * 128 + ((((d & 63) >> 3) ^ (R & 7)) << 4);
 }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+// D = A(16x16 bf16, row) . B(16x8 bf16, col) + D, fp32 accumulate
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// GQA decode attention on tensor cores, warp-specialised.  K/V chunks of 64
+// positions arrive by TMA (SWIZZLE_128B, one contiguous 16-KB box each).
+//   warps 0-3 (QK):  S = Q.K^T for 16 positions each (M = 16 rows, the kv
+//                    group's 4 query heads real; K = 128 dims, 8 mma k-steps)
+//   warps 4-7 (PV):  softmax over the chunk (one rescale per chunk) and
+//                    O += P.V for 32 dims each (P reused from registers as A)
+// S is handed over through smem with a FULL/EMPTY named-barrier pair, so QK
+// of chunk i+1 overlaps softmax/PV of chunk i.  Deterministic: fixed chunk
+// order, fixed reduction trees.
+__device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 256;" ::"r"(id) : "memory"); }
 
 __device__ void body_attn_decode(const BodyCtx& c) {
     const AttnArgs& a = *reinterpret_cast<const AttnArgs*>(c.args);
@@ -313,27 +342,26 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     const int bh = t % 256, sp = t / 256;
     const int b = bh >> 3, h = bh & 7;
     const int warp = ltid() >> 5, lane = ltid() & 31;
+    const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
     const int p0 = (int)((int64_t)sp * a.L / a.S), p1 = (int)((int64_t)(sp + 1) * a.L / a.S);
     const int nch = (p1 - p0 + kAttnChunk - 1) / kAttnChunk;
     char* base = align1024(c.smem);
+    const uint32_t sbase = tc::smem_u32(base);
     uint64_t* full = reinterpret_cast<uint64_t*>(base + kAttnBarOff);
     uint64_t* empty = full + kAttnStages;
-    float* qs = reinterpret_cast<float*>(base + kAttnQOff);
-    float* S = reinterpret_cast<float*>(base + kAttnSOff);
+    const uint32_t Ssm = sbase + kAttnSOff;  // scores fp32 [4][kAttnChunk]
+    const int BAR_SFULL = body_lane() ? 14 : 6, BAR_SEMPTY = body_lane() ? 15 : 13;
     const int row0 = (b * 8 + h) * a.Lmax + p0;
     uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
-    uint64_t t_wait = 0, t_a = 0, t_b = 0, t_sync = 0;
-    if (dbg && ltid() == 32) dbg[0] = globaltimer();
+    if (dbg && ltid() == 128) dbg[0] = globaltimer();
     auto issue = [&](int i) {
         const int s = i % kAttnStages;
         char* dst = base + s * kAttnStageBytes;
         const int r = row0 + i * kAttnChunk;
         const uint64_t pol = tc::policy_evict_first();
         tc::mbar_arrive_expect_tx(&full[s], kAttnStageBytes);
-        tc::tma_load_2d_hint(dst, &a.tmK, &full[s], 0, r, pol);
-        tc::tma_load_2d_hint(dst + kAttnHalf, &a.tmK, &full[s], 64, r, pol);
-        tc::tma_load_2d_hint(dst + 2 * kAttnHalf, &a.tmV, &full[s], 0, r, pol);
-        tc::tma_load_2d_hint(dst + 3 * kAttnHalf, &a.tmV, &full[s], 64, r, pol);
+        tc::tma_load_3d_hint(dst, &a.tmK, &full[s], 0, 0, r, pol);
+        tc::tma_load_3d_hint(dst + kAttnTile, &a.tmV, &full[s], 0, 0, r, pol);
     };
     if (ltid() == 0) {
         for (int s = 0; s < kAttnStages; ++s) {
@@ -345,126 +373,150 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         tc::tma_fence_desc(&a.tmV);
         for (int i = 0; i < min(kAttnStages, nch); ++i) issue(i);
     }
-    {  // q (4 heads of this kv group) -> smem fp32, pre-scaled
-        const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q) + (size_t)b * 4096 + (h * 4) * 128;
-        for (int i = ltid(); i < 512; i += kBodyThreads) qs[i] = bf16_to_f(__ldcg(qb + i)) * a.scale;
-    }
     body_sync();
-    // phase A role: head ha = warp & 3, positions pa = (warp >> 2) * 16 + (lane & 15), dims half dha = lane >> 4
-    const int ha = warp & 3, pa = (warp >> 2) * 16 + (lane & 15), dha = lane >> 4;
-    // phase B role: head hb = warp & 3, dims half dhb = warp >> 2, dims dhb*64 + 2*lane, +1
-    const int hb = warp & 3, dhb = warp >> 2;
-    float m = kNegInf, lsum = 0.f, acc0 = 0.f, acc1 = 0.f;
-    for (int ci = 0; ci < nch; ++ci) {
-        const int s = ci % kAttnStages;
-        const uint32_t ph = (ci / kAttnStages) & 1;
-        uint64_t tw0 = dbg ? globaltimer() : 0;
-        tc::mbar_wait(&full[s], ph);
-        uint64_t tw1 = dbg ? globaltimer() : 0;
-        t_wait += tw1 - tw0;
-        const char* stg = base + s * kAttnStageBytes;
-        const int valid = min(kAttnChunk, p1 - (p0 + ci * kAttnChunk));
-        float* Sc = S + (ci & 1) * 128;  // double-buffered [4][32]
-        {   // ---- phase A: scores S[ha][pa] = q[ha] . K[pa] ----
-            const char* kt = stg + dha * kAttnHalf;
-            const float* qh = qs + ha * 128 + dha * 64;
-            float part[4] = {0.f, 0.f, 0.f, 0.f};  // independent chains
+    const float scale = a.scale;
+    float m = kNegInf, lsum = 0.f;
+    float o[4][4];
 #pragma unroll
-            for (int jh = 0; jh < 8; jh += 4) {
-                uint4 kk[4];
+    for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) kk[j] = *reinterpret_cast<const uint4*>(sw128_at(kt, pa, (jh + j) * 8));
+        for (int j = 0; j < 4; ++j) o[nt][j] = 0.f;
+    if (warp < 4) {
+        // ================= QK warps =================
+        uint32_t qa[8][2];  // Q A-fragments (rows = query heads g < 4, rest zero)
+        {
+            const uint32_t* qb = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(a.q) +
+                                                                    (size_t)b * 4096 + (h * 4 + (g & 3)) * 128);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float4 qa = *reinterpret_cast<const float4*>(qh + (jh + j) * 8);
-                    const float4 qb4 = *reinterpret_cast<const float4*>(qh + (jh + j) * 8 + 4);
-                    part[0] = fmaf(qa.x, __uint_as_float(kk[j].x << 16), part[0]);
-                    part[1] = fmaf(qa.y, __uint_as_float(kk[j].x & 0xffff0000u), part[1]);
-                    part[2] = fmaf(qa.z, __uint_as_float(kk[j].y << 16), part[2]);
-                    part[3] = fmaf(qa.w, __uint_as_float(kk[j].y & 0xffff0000u), part[3]);
-                    part[0] = fmaf(qb4.x, __uint_as_float(kk[j].z << 16), part[0]);
-                    part[1] = fmaf(qb4.y, __uint_as_float(kk[j].z & 0xffff0000u), part[1]);
-                    part[2] = fmaf(qb4.z, __uint_as_float(kk[j].w << 16), part[2]);
-                    part[3] = fmaf(qb4.w, __uint_as_float(kk[j].w & 0xffff0000u), part[3]);
+            for (int kk = 0; kk < 8; ++kk) {
+                qa[kk][0] = g < 4 ? __ldcg(qb + kk * 8 + tq) : 0u;
+                qa[kk][1] = g < 4 ? __ldcg(qb + kk * 8 + 4 + tq) : 0u;
+            }
+        }
+        const int m4 = lane >> 3;
+        for (int ci = 0; ci < nch; ++ci) {
+            const int s = ci % kAttnStages;
+            tc::mbar_wait(&full[s], (ci / kAttnStages) & 1);
+            const uint32_t kt = sbase + s * kAttnStageBytes;
+            const int valid = min(kAttnChunk, p1 - (p0 + ci * kAttnChunk));
+            float sv[2][2];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {  // positions 16w + 8nt .. +7
+                float acc4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+                const int prow = warp * 16 + nt * 8 + (lane & 7);
+#pragma unroll
+                for (int kk = 0; kk < 8; kk += 2) {
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(kv_addr(kt, prow, 16 * (kk + (m4 >> 1)) + 8 * (m4 & 1)), b0, b1, b2, b3);
+                    mma16816(acc4[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
+                    mma16816(acc4[1], qa[kk + 1][0], 0u, qa[kk + 1][1], 0u, b2, b3);
+                }
+                const int pc = warp * 16 + nt * 8 + 2 * tq;
+                sv[nt][0] = pc < valid ? (acc4[0][0] + acc4[1][0]) * scale : kNegInf;
+                sv[nt][1] = pc + 1 < valid ? (acc4[0][1] + acc4[1][1]) * scale : kNegInf;
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[s]);  // K of this slot consumed
+            if (ci > 0) nbar_sync(BAR_SEMPTY);           // PV warps have read the previous S
+            if (g < 4) {
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const uint32_t sa = Ssm + (g * kAttnChunk + warp * 16 + nt * 8 + 2 * tq) * 4;
+                    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(sa), "f"(sv[nt][0]), "f"(sv[nt][1])
+                                 : "memory");
                 }
             }
-            float d = (part[0] + part[1]) + (part[2] + part[3]);
-            d += __shfl_xor_sync(0xffffffffu, d, 16);  // the two 64-dim halves
-            if (dha == 0) Sc[ha * 32 + pa] = pa < valid ? d : kNegInf;
+            nbar_arrive(BAR_SFULL);
+            if (ltid() == 0 && ci + kAttnStages < nch) {
+                tc::mbar_wait(&empty[s], (ci / kAttnStages) & 1);  // K and V of the slot consumed
+                issue(ci + kAttnStages);
+            }
         }
-        uint64_t ta1 = dbg ? globaltimer() : 0;
-        t_a += ta1 - tw1;
-        body_sync();
-        uint64_t ts1 = dbg ? globaltimer() : 0;
-        t_sync += ts1 - ta1;
-        {   // ---- softmax for this chunk (one rescale) + phase B: acc += p . V ----
-            const float sl = Sc[hb * 32 + lane];
-            float cm = sl;
+        if (nch > 0) nbar_sync(BAR_SEMPTY);  // balance the PV warps' last release
+    } else {
+        // ================= PV warps =================
+        const int pw = warp - 4;  // dims 32 pw .. 32 pw + 31
+        constexpr int KS = kAttnChunk / 16;
+        const int m4 = lane >> 3;
+        for (int ci = 0; ci < nch; ++ci) {
+            const int s = ci % kAttnStages;
+            tc::mbar_wait(&full[s], (ci / kAttnStages) & 1);
+            const uint32_t vt = sbase + s * kAttnStageBytes + kAttnTile;
+            nbar_sync(BAR_SFULL);
+            float pv[KS][4];  // [k-step][a0.x, a0.y, a2.x, a2.y]
+            {
+                const uint32_t sr = Ssm + ((g & 3) * kAttnChunk + 2 * tq) * 4;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+                for (int kk = 0; kk < KS; ++kk) {
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(pv[kk][0]), "=f"(pv[kk][1]) : "r"(sr + 64 * kk));
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(pv[kk][2]), "=f"(pv[kk][3])
+                                 : "r"(sr + 64 * kk + 32));
+                }
+            }
+            nbar_arrive(BAR_SEMPTY);  // S copied into registers
+            float cm = kNegInf;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cm = fmaxf(cm, pv[kk][j]);
+            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
             const float mn = fmaxf(m, cm);
             const float alpha = __expf(m - mn);
-            const float pl = __expf(sl - mn);  // 0 for masked positions
-            float ps = pl;
+            float ps = 0.f;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    pv[kk][j] = __expf(pv[kk][j] - mn);
+                    ps += pv[kk][j];
+                }
+            ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+            ps += __shfl_xor_sync(0xffffffffu, ps, 2);
             lsum = lsum * alpha + ps;
-            acc0 *= alpha;
-            acc1 *= alpha;
             m = mn;
-            const char* vt = stg + (2 + dhb) * kAttnHalf;
-            float* Pw = S + 256 + warp * 32;  // this warp's probabilities (smem, broadcast reads)
-            Pw[lane] = pl;
-            __syncwarp();
-            float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int ph2 = 0; ph2 < kAttnChunk; ph2 += 16) {
-                uint32_t vv[16];
+            for (int nt = 0; nt < 4; ++nt) {
+                o[nt][0] *= alpha;
+                o[nt][1] *= alpha;
+            }
 #pragma unroll
-                for (int p = 0; p < 16; ++p) vv[p] = *reinterpret_cast<const uint32_t*>(sw128_at(vt, ph2 + p, 2 * lane));
+            for (int kk = 0; kk < KS; ++kk) {
+                const uint32_t pa0 = g < 4 ? pack_bf16x2(pv[kk][0], pv[kk][1]) : 0u;
+                const uint32_t pa2 = g < 4 ? pack_bf16x2(pv[kk][2], pv[kk][3]) : 0u;
+                const int pos = 16 * kk + 8 * (m4 & 1) + (lane & 7);
 #pragma unroll
-                for (int p = 0; p < 16; p += 4) {
-                    const float4 p4 = *reinterpret_cast<const float4*>(Pw + ph2 + p);
-                    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        a0[u] = fmaf(pv[u], __uint_as_float(vv[p + u] << 16), a0[u]);
-                        a1[u] = fmaf(pv[u], __uint_as_float(vv[p + u] & 0xffff0000u), a1[u]);
-                    }
+                for (int np = 0; np < 2; ++np) {  // n-tile pairs (4 n-tiles of 8 dims)
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(kv_addr(vt, pos, 32 * pw + 16 * np + 8 * (m4 >> 1)), b0, b1, b2, b3);
+                    mma16816(o[2 * np], pa0, 0u, pa2, 0u, b0, b1);
+                    mma16816(o[2 * np + 1], pa0, 0u, pa2, 0u, b2, b3);
                 }
             }
-            acc0 += (a0[0] + a0[1]) + (a0[2] + a0[3]);
-            acc1 += (a1[0] + a1[1]) + (a1[2] + a1[3]);
             __syncwarp();
-        }
-        if (dbg) t_b += globaltimer() - ts1;
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&empty[s]);
-        if (ltid() == 0 && ci + kAttnStages < nch) {
-            tc::mbar_wait(&empty[s], ph);  // all 8 warps released this slot
-            issue(ci + kAttnStages);
+            if (lane == 0) tc::mbar_arrive(&empty[s]);  // V of this slot consumed
         }
     }
-    if (dbg && ltid() == 32) {
-        dbg[1] = globaltimer();
-        dbg[2] = t_wait;
-        dbg[3] = t_a;
-        dbg[4] = t_sync;
-        dbg[5] = t_b;
-    }
-    // each (head hb, dims half dhb) warp owns final (m, l, acc) for 64 dims
-    const int d0 = dhb * 64 + 2 * lane;
+    if (dbg && ltid() == 128) dbg[1] = globaltimer();
+    // PV lanes with g < 4 own O[head g][32 pw + 8 nt + 2 tq, +1], nt = 0..3
+    const int pw = warp - 4;
     bool write_out = true;
     __shared__ int last_flag_l[2];
     int& last_flag = last_flag_l[body_lane()];
-    float M = m, Ls = lsum, A0 = acc0, A1 = acc1;
+    float M = m, Ls = lsum;
+    const int hq = g & 3;
     if (a.S > 1) {
-        float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130 + hb * 130;
-        ws[d0] = A0;
-        ws[d0 + 1] = A1;
-        if (lane == 0 && dhb == 0) {
-            ws[128] = M;
-            ws[129] = Ls;
+        float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130 + hq * 130;
+        if (warp >= 4 && g < 4) {
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                ws[32 * pw + 8 * nt + 2 * tq] = o[nt][0];
+                ws[32 * pw + 8 * nt + 2 * tq + 1] = o[nt][1];
+            }
+            if (warp == 4 && tq == 0) {
+                ws[128] = M;
+                ws[129] = Ls;
+            }
         }
         body_sync();
         if (ltid() == 0) {
@@ -475,33 +527,37 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         }
         body_sync();
         write_out = last_flag != 0;
-        if (write_out) {
+        if (write_out && warp >= 4 && g < 4) {
             __threadfence();
-            const float* wsb = reinterpret_cast<const float*>(a.ws) + (size_t)bh * a.S * 4 * 130 + hb * 130;
+            const float* wsb = reinterpret_cast<const float*>(a.ws) + (size_t)bh * a.S * 4 * 130 + hq * 130;
             M = kNegInf;
             for (int s2 = 0; s2 < a.S; ++s2) M = fmaxf(M, __ldcg(wsb + s2 * 4 * 130 + 128));
             Ls = 0.f;
-            A0 = 0.f;
-            A1 = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) o[nt][0] = o[nt][1] = 0.f;
             for (int s2 = 0; s2 < a.S; ++s2) {  // fixed order
                 const float* src = wsb + s2 * 4 * 130;
                 const float mw = __ldcg(src + 128);
                 const float f = (mw == kNegInf) ? 0.f : __expf(mw - M);
                 Ls += __ldcg(src + 129) * f;
-                A0 += __ldcg(src + d0) * f;
-                A1 += __ldcg(src + d0 + 1) * f;
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    o[nt][0] += __ldcg(src + 32 * pw + 8 * nt + 2 * tq) * f;
+                    o[nt][1] += __ldcg(src + 32 * pw + 8 * nt + 2 * tq + 1) * f;
+                }
             }
-            if (ltid() == 0) reinterpret_cast<uint32_t*>(a.counters)[bh] = 0;
         }
+        if (write_out && ltid() == 0) reinterpret_cast<uint32_t*>(a.counters)[bh] = 0;
     }
-    if (write_out) {
+    if (write_out && warp >= 4 && g < 4) {
         const float inv = 1.f / Ls;
-        uint32_t* out = reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(a.out) + (size_t)b * 4096 +
-                                                    (h * 4 + hb) * 128 + d0);
-        *out = pack_bf16x2(A0 * inv, A1 * inv);
+        uint16_t* orow = reinterpret_cast<uint16_t*>(a.out) + (size_t)b * 4096 + (h * 4 + hq) * 128;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+            *reinterpret_cast<uint32_t*>(orow + 32 * pw + 8 * nt + 2 * tq) = pack_bf16x2(o[nt][0] * inv, o[nt][1] * inv);
     }
     body_sync();
-    if (dbg && ltid() == 32) dbg[6] = globaltimer();
+    if (dbg && ltid() == 128) dbg[6] = globaltimer();
     if (ltid() == 0)
         for (int s = 0; s < 2 * kAttnStages; ++s) tc::mbar_inval(&full[s]);
 }

@@ -999,6 +999,34 @@ int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_
     return DS_OK;
 }
 
+// KV-cache view for the attention body: [rows][128] bf16 as a 3-D tensor
+// {64 dims, 2 halves, rows} so one box {64, 2, 32} is 32 whole rows = 8 KB
+// of contiguous memory, landing in smem as 64 SWIZZLE_128B rows
+// (smem row R = 2*row + half).
+int ds_tensor_map_bf16_kv(void* out128, const void* base, uint64_t rows, uint32_t box_rows) {
+    if (!out128 || !base) return fail(DS_INVALID_ARGUMENT, "null");
+    if (((uintptr_t)base & 15)) return fail(DS_CONFIG_ERROR, "base must be 16-B aligned");
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return fail(DS_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)p;
+    }
+    CUtensorMap m;
+    cuuint64_t dims[3] = {64, 2, rows};
+    cuuint64_t strides[2] = {128, 256};
+    cuuint32_t box[3] = {64, 2, box_rows};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(DS_CUDA_ERROR, "cuTensorMapEncodeTiled(kv) failed (" + std::to_string((int)r) + ")");
+    std::memcpy(out128, &m, 128);
+    return DS_OK;
+}
+
 int ds_solo_launch(int device, const ds_kernel_desc* k, void* stream) {
     if (!k) return fail(DS_INVALID_ARGUMENT, "null desc");
     if (k->body <= DS_BODY_NONE || k->body >= DS_BODY_COUNT) return fail(DS_CONFIG_ERROR, "unknown body");

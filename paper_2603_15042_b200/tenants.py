@@ -20,6 +20,7 @@ import torch
 from . import _abi
 
 SMS = 148
+ATTN_CHUNK = 64  # KV positions per attention TMA box (bodies/decode.cuh kAttnChunk)
 LANES = 2
 WORKERS = SMS * LANES  # concurrent logical blocks (2 worker lanes per SM)
 
@@ -158,8 +159,8 @@ class DecodeModel:
                               stats_in=st_in, P_in=p_in, l=l)
             self.records.append((f"decode/qkv", _abi.BODY_GEMV_BF16, g, a, self.qkv_n * c.d * 2))
             rows = 32 * c.n_kv * self.Lmax
-            at = _abi.AttnArgs(_abi.tensor_map_bf16(self.kc[l].data_ptr(), rows, 128, 32),
-                               _abi.tensor_map_bf16(self.vc[l].data_ptr(), rows, 128, 32), self.q.data_ptr(),
+            at = _abi.AttnArgs(_abi.tensor_map_kv(self.kc[l].data_ptr(), rows, ATTN_CHUNK),
+                               _abi.tensor_map_kv(self.vc[l].data_ptr(), rows, ATTN_CHUNK), self.q.data_ptr(),
                                self.attn.data_ptr(), self.attn_ws.data_ptr(), self.attn_counters.data_ptr(), c.L,
                                self.Lmax, c.attn_splits, 1.0 / math.sqrt(128))
             self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,

@@ -19,6 +19,6 @@ for _ in range(3): last = dom.launch(t, k)
 dom.wait(t, last)
 d = dbg.cpu().view(grid[0], 8).tolist()
 def med(f): v = [f(r) / 1e3 for r in d]; return [round(statistics.median(v), 2), round(max(v), 2)]
-print(json.dumps({"loop": med(lambda r: r[1] - r[0]), "wait_full": med(lambda r: r[2]), "phaseA": med(lambda r: r[3]),
-                  "sync": med(lambda r: r[4]), "phaseB": med(lambda r: r[5]), "tail": med(lambda r: r[6] - r[1])}))
+print(json.dumps({"loop(warp0)": med(lambda r: r[1] - r[0]), "wait_full": med(lambda r: r[2]), "qk": med(lambda r: r[3]),
+                  "sync": med(lambda r: r[4]), "pv": med(lambda r: r[5]), "producer": med(lambda r: r[7]), "tail": med(lambda r: r[6] - r[1])}))
 dom.stop(); dom.close()

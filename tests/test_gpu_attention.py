@@ -11,7 +11,7 @@ from paper_2603_15042_b200.runtime import solo_launch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("L,S", [(96, 2), (1024, 2), (333, 3), (32, 1)])
+@pytest.mark.parametrize("L,S", [(96, 2), (1024, 2), (333, 3), (32, 1), (1000, 4)])
 def test_attention_matches_fp32_reference(L, S):
     g = torch.Generator(device="cuda").manual_seed(L)
     Lmax = L + 5
@@ -22,7 +22,7 @@ def test_attention_matches_fp32_reference(L, S):
     ws = torch.zeros(256 * S * 4 * 130, device="cuda")
     ctr = torch.zeros(256, device="cuda", dtype=torch.int32)
     rows = 32 * 8 * Lmax
-    a = _abi.AttnArgs(_abi.tensor_map_bf16(kc.data_ptr(), rows, 128, 32), _abi.tensor_map_bf16(vc.data_ptr(), rows, 128, 32),
+    a = _abi.AttnArgs(_abi.tensor_map_kv(kc.data_ptr(), rows, 64), _abi.tensor_map_kv(vc.data_ptr(), rows, 64),
                       q.data_ptr(), out.data_ptr(), ws.data_ptr(), ctr.data_ptr(), L, Lmax, S, 1.0 / math.sqrt(128), 0)
     solo_launch(0, "attn", _abi.BODY_ATTN_DECODE, (256 * S, 1, 1), a)
     torch.cuda.synchronize()
