@@ -214,6 +214,8 @@ int ds_ctl_log(ds_domain* dom, ds_ctl_record* out, int64_t cap, int64_t* n);
 int ds_clear_logs(ds_domain* dom);
 int ds_globaltimer(ds_domain* dom, uint64_t* ns); /* device %globaltimer now (probe kernel) */
 int ds_debug_dump(ds_domain* dom, char* out, int64_t cap); /* text snapshot of device control state */
+/* host write of the control word -> device install acknowledged in host memory, n samples (ns) */
+int ds_ctl_roundtrip(ds_domain* dom, int n, uint64_t* out_ns);
 
 /* ---- solo baseline: the same body as a plain __global__ grid (exclusive_baseline) ---- */
 int ds_solo_launch(int device, const ds_kernel_desc* desc, void* stream);

@@ -77,4 +77,13 @@ __device__ __forceinline__ void st_release_sys_u64(void* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Wait until every earlier launch of this tenant has completed (acquire).
+__device__ __forceinline__ void wait_prev(const BodyCtx& c) {
+    if (!c.prev_head) return;
+    if (ld_acquire_u32(c.prev_head) < c.seq) {
+        while (ld_acquire_u32(c.prev_head) < c.seq) __nanosleep(64);
+    }
+    __threadfence();  // gpu-scope acquire; also drops stale L1 lines
+}
+
 }  // namespace ds

@@ -64,8 +64,11 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     const int kb0 = (int)((int64_t)s * KB / a.S), kb1 = (int)((int64_t)(s + 1) * KB / a.S);
     uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
     if (dbg && ltid() == 0) dbg[0] = globaltimer();
+    BodyCtx cd = c;
+    cd.dbg = dbg;
     tc_mainloop<kGemvBN, kGemvStages>(base, &a.tmW, &a.tmX, n_blk * kTcBM, 0, kb0, kb1, c.tmem_base, true,
-                                      reinterpret_cast<const char*>(a.w_packed), KB);
+                                      reinterpret_cast<const char*>(a.w_packed), KB, &cd);
+    wait_prev(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
     const int warp = ltid() >> 5, lane = ltid() & 31;
     float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + rvec[32] + flag
@@ -172,14 +175,16 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
 #pragma unroll
                 for (int b = 0; b < 32; ++b) out[(size_t)b * a.N + n] = f_to_bf16(v[b]);
             } else if (a.mode == kGemvResid) {
-                const uint16_t* res = reinterpret_cast<const uint16_t*>(a.resid);
-                uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
+                const uint16_t* __restrict__ res = reinterpret_cast<const uint16_t*>(a.resid);
+                uint16_t* __restrict__ out = reinterpret_cast<uint16_t*>(a.out);
+                uint16_t rv[32];  // all residual loads in flight before any store
+#pragma unroll
+                for (int b = 0; b < 32; ++b) rv[b] = __ldcg(res + (size_t)b * a.N + n);
 #pragma unroll
                 for (int b = 0; b < 32; ++b) {
-                    float h = bf16_to_f(__ldcg(res + (size_t)b * a.N + n)) + v[b];
-                    uint16_t hb = f_to_bf16(h);
+                    const uint16_t hb = f_to_bf16(bf16_to_f(rv[b]) + v[b]);
                     out[(size_t)b * a.N + n] = hb;
-                    float hr = bf16_to_f(hb);
+                    const float hr = bf16_to_f(hb);
                     scratch[row * 33 + b] = hr * hr;
                 }
                 epi_sync();

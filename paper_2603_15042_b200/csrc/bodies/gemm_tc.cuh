@@ -46,7 +46,8 @@ __device__ __forceinline__ char* align1024(char* p) {
 template <int BN, int STAGES>
 __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
                                             int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
-                                            const char* a_packed = nullptr, int a_kblocks = 0) {
+                                            const char* a_packed = nullptr, int a_kblocks = 0,
+                                            const BodyCtx* dep = nullptr) {
     using L = TcSmem<BN, STAGES>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -66,20 +67,36 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
         if (!a_packed) tc::tma_fence_desc(tmA);
         tc::tma_fence_desc(tmB);
         const uint64_t pol = a_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
-        for (int i = 0; i < nkb; ++i) {
+        auto issue_a = [&](int i) {
             const int s = i % STAGES;
-            const uint32_t ph = (i / STAGES) & 1;
-            if (i >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
             char* sa = base + s * L::kStageBytes;
-            char* sb = sa + L::kABytes;
-            tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
-            const int k0 = (kb_begin + i) * kTcBK;
             if (a_packed)
                 tc::bulk_g2s_hint(sa, a_packed + ((size_t)(a_row / kTcBM) * a_kblocks + kb_begin + i) * L::kABytes,
                                   L::kABytes, &full[s], pol);
             else
-                tc::tma_load_2d_hint(sa, tmA, &full[s], k0, a_row, pol);
-            tc::tma_load_2d(sb, tmB, &full[s], k0, b_row);
+                tc::tma_load_2d_hint(sa, tmA, &full[s], (kb_begin + i) * kTcBK, a_row, pol);
+        };
+        auto issue_b = [&](int i) {
+            const int s = i % STAGES;
+            tc::tma_load_2d(base + s * L::kStageBytes + L::kABytes, tmB, &full[s], (kb_begin + i) * kTcBK, b_row);
+        };
+        // With a dependency, the A operand (weights, immutable) streams while
+        // the previous launch finishes; B (its output) only after wait_prev.
+        const int pre = dep ? min(STAGES, nkb) : 0;
+        for (int i = 0; i < pre; ++i) {
+            tc::mbar_arrive_expect_tx(&full[i % STAGES], L::kStageBytes);
+            issue_a(i);
+        }
+        if (dep) wait_prev(*dep);
+        if (dep && dep->dbg) dep->dbg[7] = globaltimer();
+        for (int i = 0; i < pre; ++i) issue_b(i);
+        for (int i = pre; i < nkb; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = (i / STAGES) & 1;
+            if (i >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
+            tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+            issue_a(i);
+            issue_b(i);
         }
     } else if (warp == 1 && lane == 0) {
         constexpr uint32_t idesc = tc::idesc_bf16_f32(kTcBM, BN);

@@ -89,18 +89,21 @@ struct HostCompletion {
 };
 static_assert(sizeof(HostCompletion) == 64, "completion record is one line");
 
+// Host -> device mailbox.  Everything the loader polls sits in one 512-B
+// "hot" block read with a single warp-wide 16-B/lane load per poll:
+//   hot[0] control generation, hot[1] exit, hot[2] periodic-program generation,
+//   hot[64 + t] launch tail of tenant t.
 struct HostMailbox {
-    volatile uint32_t gen;            // control generation written by host
-    volatile uint32_t exit;
-    volatile uint32_t periodic_gen;   // periodic program changed
-    volatile uint32_t pad0;
+    volatile uint32_t hot[128];
     volatile unsigned long long periodic_ns;
-    volatile uint32_t tail[DS_MAX_TENANTS];
     volatile int32_t owner[DS_MAX_SMS];   // by smid
     volatile int32_t lender[DS_MAX_SMS];
     volatile int32_t per_owner[2][DS_MAX_SMS];
     volatile int32_t per_lender[2][DS_MAX_SMS];
+    volatile uint32_t ack_gen;        // device -> host: last host control generation installed
 };
+constexpr int kHotGen = 0, kHotExit = 1, kHotPGen = 2, kHotTail = 64;
+static_assert(kHotTail + DS_MAX_TENANTS <= 128, "tails fit the hot block");
 
 struct DevState {
     DevTenant tenants[DS_MAX_TENANTS];
@@ -129,6 +132,8 @@ struct DevState {
     alignas(128) uint32_t trig_next;   // next armed trigger index
     uint32_t trig_count;
     ClaimTrigger* triggers;            // device array [kMaxTriggers]
+    int32_t per_owner[2][DS_MAX_SMS];  // periodic program, cached from the mailbox
+    int32_t per_lender[2][DS_MAX_SMS];
 };
 
 // Per-block context handed to a tenant body (the "unmodified kernel" sees
@@ -140,6 +145,13 @@ struct BodyCtx {
     char* smem;          // dynamic shared memory (1024-aligned)
     uint32_t smem_bytes;
     uint32_t tmem_base;  // TMEM columns allocated for this CTA (0 if none)
+    // Early-start dependency: launch `seq` of a tenant opens for claims as soon
+    // as launch seq-1 is fully *claimed*; a block must not touch data produced
+    // by earlier launches before wait_prev() (head >= seq).  Null in solo mode
+    // (stream order already serialises launches).
+    const uint32_t* prev_head;
+    uint32_t seq;
+    uint64_t* dbg;  // optional per-block phase timestamps (bodies that support it)
 };
 
 }  // namespace ds

@@ -34,7 +34,12 @@ constexpr uint32_t kLaneTmemCols = kTmemCols / kLanes;
 // ---------------------------------------------------------------------------
 // Body dispatch (shared by the executor and the solo wrapper)
 // ---------------------------------------------------------------------------
+// Bodies that handle the early-start dependency themselves (stream immutable
+// operands before wait_prev); every other body waits before it starts.
+__device__ __forceinline__ bool early_start_body(int body) { return body == DS_BODY_GEMV_BF16; }
+
 __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
+    if (!early_start_body(body)) wait_prev(c);
     switch (body) {
         case DS_BODY_REDUCE_CHUNKS: body_reduce(c); break;
         case DS_BODY_SGEMM: body_sgemm(c); break;
@@ -88,26 +93,46 @@ __device__ void log_ctl(DevState* st, uint32_t gen, uint32_t source) {
     }
 }
 
-// Lane-parallel install of a control word (owner/lender by smid).
+// Lane-parallel install of a control word (owner/lender by smid).  All of a
+// lane's source loads are issued before any store (one PCIe round trip when
+// the source is the host mailbox); the control record is stamped when the
+// install starts.
 __device__ void install_ctl(DevState* st, const int32_t* owner, const int32_t* lender, bool volatile_src,
                             uint32_t source, int lane) {
-    for (int i = lane; i < DS_MAX_SMS; i += 32) {
-        int32_t o, l;
-        if (volatile_src) {
-            o = (int32_t)ld_acquire_sys_u32(owner + i);
-            l = (int32_t)ld_acquire_sys_u32(lender + i);
+    constexpr int kPer = DS_MAX_SMS / 32;
+    const uint64_t t0 = globaltimer();
+    int32_t o[kPer], l[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int i = lane + 32 * j;
+        if (volatile_src) {  // relaxed loads all in flight; one acquire fence below
+            o[j] = (int32_t)ld_volatile_u32(owner + i);
+            l[j] = (int32_t)ld_volatile_u32(lender + i);
         } else {
-            o = owner[i];
-            l = lender[i];
+            o[j] = owner[i];
+            l[j] = lender[i];
         }
-        unsigned long long w = ((unsigned long long)(uint32_t)l << 32) | (uint32_t)o;
-        asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&st->ctl.word[i]), "l"(w) : "memory");
+    }
+    if (volatile_src) asm volatile("fence.acq_rel.sys;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const unsigned long long w = ((unsigned long long)(uint32_t)l[j] << 32) | (uint32_t)o[j];
+        asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&st->ctl.word[lane + 32 * j]), "l"(w) : "memory");
     }
     __syncwarp();
     __threadfence();
     if (lane == 0) {
         uint32_t g = atomicAdd(&st->ctl.gen, 1u) + 1u;
-        log_ctl(st, g, source);
+        if (st->clog_cap) {
+            unsigned long long i = atomicAdd(&st->clog_count, 1ull);
+            if (i < st->clog_cap) {
+                ds_ctl_record r;
+                r.ctl_gen = g;
+                r.source = source;
+                r.t = t0;
+                st->clog[i] = r;
+            }
+        }
     }
     __syncwarp();
 }
@@ -125,7 +150,16 @@ __device__ void loader_loop(DevState* st) {
     uint64_t period = 0, next_flip = 0;
     int phase = 0;
     for (;;) {
-        uint32_t ex = ld_acquire_sys_u32((const void*)&mb->exit);
+        // one PCIe round trip per poll: lane i reads hot[4i .. 4i+3]
+        uint4 hv;
+        asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(hv.x), "=r"(hv.y), "=r"(hv.z), "=r"(hv.w)
+                     : "l"(&mb->hot[4 * lane])
+                     : "memory");
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        const uint32_t ex = __shfl_sync(0xffffffffu, hv.y, 0);
+        const uint32_t g = __shfl_sync(0xffffffffu, hv.x, 0);
+        const uint32_t pg = __shfl_sync(0xffffffffu, hv.z, 0);
         if (ex) {
             if (lane == 0) {
                 __threadfence();
@@ -134,27 +168,31 @@ __device__ void loader_loop(DevState* st) {
             __syncwarp();
             return;
         }
-        // new launches
+        // new launches: tail of tenant t = hot[64 + t] -> lane 16 + t/4, component t%4
         for (int base = 0; base < DS_MAX_TENANTS; base += 32) {
-            int t = base + lane;
-            uint32_t ht = ld_acquire_sys_u32((const void*)&mb->tail[t]);
-            uint32_t kt = known_tail[t];
+            const int t = base + lane;
+            const int src_lane = (kHotTail + t) >> 2, comp = t & 3;
+            const uint32_t cx = __shfl_sync(0xffffffffu, hv.x, src_lane & 31);
+            const uint32_t cy = __shfl_sync(0xffffffffu, hv.y, src_lane & 31);
+            const uint32_t cz = __shfl_sync(0xffffffffu, hv.z, src_lane & 31);
+            const uint32_t cw = __shfl_sync(0xffffffffu, hv.w, src_lane & 31);
+            const uint32_t ht = comp == 0 ? cx : comp == 1 ? cy : comp == 2 ? cz : cw;
+            const uint32_t kt = known_tail[t];
             unsigned pending = __ballot_sync(0xffffffffu, ht != kt);
             while (pending) {
-                int src = __ffs(pending) - 1;
+                const int src = __ffs(pending) - 1;
                 pending &= pending - 1;
-                int tt = base + src;
-                uint32_t from = __shfl_sync(0xffffffffu, kt, src);
-                uint32_t to = __shfl_sync(0xffffffffu, ht, src);
+                const int tt = base + src;
+                const uint32_t from = __shfl_sync(0xffffffffu, kt, src);
+                const uint32_t to = __shfl_sync(0xffffffffu, ht, src);
                 // copy slots [from, to): 16 u32 per slot, 2 slots per warp step
                 for (uint32_t s = from; s < to; s += 2) {
-                    uint32_t my = s + (lane >> 4);
+                    const uint32_t my = s + (lane >> 4);
                     if (my < to) {
-                        uint32_t idx = (uint32_t)tt * (st->ring_mask + 1) + (my & st->ring_mask);
+                        const uint32_t idx = (uint32_t)tt * (st->ring_mask + 1) + (my & st->ring_mask);
                         const uint32_t* hs = reinterpret_cast<const uint32_t*>(&st->host_rings[idx]);
                         uint32_t* ds = reinterpret_cast<uint32_t*>(&st->rings[idx]);
-                        uint32_t v = ld_acquire_sys_u32(hs + (lane & 15));
-                        ds[lane & 15] = v;
+                        ds[lane & 15] = ld_volatile_u32(hs + (lane & 15));
                         __threadfence();
                     }
                 }
@@ -171,23 +209,33 @@ __device__ void loader_loop(DevState* st) {
             }
         }
         // control word
-        uint32_t g = ld_acquire_sys_u32((const void*)&mb->gen);
         if (g != last_gen) {
             install_ctl(st, (const int32_t*)mb->owner, (const int32_t*)mb->lender, true, 0, lane);
             last_gen = g;
+            if (lane == 0) {
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&mb->ack_gen), "r"(g) : "memory");
+            }
         }
-        // periodic device-timer program (config 3 migration sweep)
-        uint32_t pg = ld_acquire_sys_u32((const void*)&mb->periodic_gen);
+        // periodic device-timer program (config 3 migration sweep): both
+        // control words are copied into HBM once per program change, so a flip
+        // is a device-local install
         if (pg != last_pgen) {
             last_pgen = pg;
             period = ld_acquire_sys_u64((const void*)&mb->periodic_ns);
+            for (int k = 0; k < 2; ++k)
+                for (int i = lane; i < DS_MAX_SMS; i += 32) {
+                    st->per_owner[k][i] = (int32_t)ld_volatile_u32((const void*)&mb->per_owner[k][i]);
+                    st->per_lender[k][i] = (int32_t)ld_volatile_u32((const void*)&mb->per_lender[k][i]);
+                }
+            __syncwarp();
+            __threadfence();
             next_flip = globaltimer() + period;
             phase = 0;
         }
         if (period && globaltimer() >= next_flip) {
             phase ^= 1;
-            install_ctl(st, (const int32_t*)mb->per_owner[phase], (const int32_t*)mb->per_lender[phase], true, 2,
-                        lane);
+            install_ctl(st, st->per_owner[phase], st->per_lender[phase], false, 2, lane);
             next_flip += period;
         }
     }
@@ -212,6 +260,22 @@ struct ClaimCache {
     bool more = false;
     LaunchSlot* slot = nullptr;
 };
+
+// Launch s is fully claimed: open s+1 for claims now (its blocks wait for s's
+// completion before touching dependent data — wait_prev).  If s+1 is not
+// enqueued yet, park the word closed; the loader opens it on publish
+// (fence.sc on both sides, Dekker-style, so one of them does).
+__device__ void open_next(DevTenant* T, uint32_t s) {
+    const uint32_t nxt = s + 1;
+    const uint32_t tail = ld_acquire_u32(&T->tail);
+    if (nxt < tail) {
+        atomicExch(&T->claim, (unsigned long long)nxt << 32);
+    } else {
+        atomicExch(&T->claim, ((unsigned long long)nxt << 32) | kSat);
+        __threadfence();
+        try_open(T);
+    }
+}
 
 __device__ __forceinline__ LaunchSlot* slot_of(DevState* st, int t, uint32_t s) {
     return &st->rings[(size_t)t * (st->ring_mask + 1) + (s & st->ring_mask)];
@@ -269,6 +333,7 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
         return false;
     }
     cc.more = b2 + 1 < grid;
+    if (b2 == grid - 1) open_next(T, s2);  // fully claimed: the next launch may start early
     out.tenant = t;
     out.seq = s2;
     out.block = b2;
@@ -280,17 +345,9 @@ __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* s
     DevTenant* T = &st->tenants[t];
     __threadfence();
     const uint64_t tend = globaltimer();
-    // 1. advance the tenant to seq+1 first (critical path of the next kernel)
+    // 1. publish completion first (critical path: early-started blocks of the
+    //    next launch are waiting on head)
     st_release_u32(&T->head, seq + 1);
-    const uint32_t nxt = seq + 1;
-    const uint32_t tail = ld_acquire_u32(&T->tail);
-    if (nxt < tail) {
-        atomicExch(&T->claim, (unsigned long long)nxt << 32);
-    } else {
-        atomicExch(&T->claim, ((unsigned long long)nxt << 32) | kSat);
-        __threadfence();
-        try_open(T);
-    }
     // 2. device -> host completion record (PCIe, off the critical path)
     unsigned long long i = atomicAdd(&st->completion_count, 1ull);
     HostCompletion* hc = &st->completions[i & st->completion_mask];
@@ -456,8 +513,9 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
 // ---------------------------------------------------------------------------
 // Body warps
 // ---------------------------------------------------------------------------
-__device__ void body_loop(Stage* stage, volatile uint64_t* body_t0, char* smem, uint32_t smem_bytes,
+__device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, char* smem, uint32_t smem_bytes,
                           uint32_t tmem_base, int lane_id) {
+    auto prev_head_of = [&](int t) { return &st->tenants[t].head; };
     const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
     for (;;) {
         named_sync(kFull, kBodyThreads + 32);
@@ -476,6 +534,9 @@ __device__ void body_loop(Stage* stage, volatile uint64_t* body_t0, char* smem, 
         c.smem = smem;
         c.smem_bytes = smem_bytes;
         c.tmem_base = tmem_base;
+        c.prev_head = prev_head_of(s.tenant);
+        c.seq = s.seq;
+        c.dbg = nullptr;
         run_body(s.body, c);
         __threadfence();  // this thread's writes visible at gpu scope before retire
         named_arrive(kDone, kBodyThreads + 32);
@@ -504,7 +565,7 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
         scheduler_loop(st, &stage[l], &body_t0[l], sm, l);
     } else {
         const int l = warp >> 3;
-        body_loop(&stage[l], &body_t0[l], smem + l * lane_smem, lane_smem, tmem_base_sh + l * kLaneTmemCols, l);
+        body_loop(st, &stage[l], &body_t0[l], smem + l * lane_smem, lane_smem, tmem_base_sh + l * kLaneTmemCols, l);
     }
     tc::tc_fence_before();
     named_sync(kBarExit, kLanes * (kBodyThreads + 32));
@@ -528,6 +589,9 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     c.args = args;
     c.smem = smem;
     c.smem_bytes = smem_bytes;
+    c.prev_head = nullptr;
+    c.seq = 0;
+    c.dbg = nullptr;
     __shared__ uint32_t tmem_base_sh;
     const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16;
     if (tc_body) {

@@ -180,7 +180,7 @@ int push_control(ds_domain* d) {
         d->mb->lender[sm] = l;
     }
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    d->mb->gen = d->mb->gen + 1;
+    d->mb->hot[ds::kHotGen] = d->mb->hot[ds::kHotGen] + 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
     return DS_OK;
 }
@@ -474,7 +474,7 @@ int ds_start(ds_domain* d) {
         h.tenants[t].claim = ((unsigned long long)seq << 32) | ds::kSat;
         h.tenants[t].tail = (uint32_t)seq;
         h.tenants[t].head = (uint32_t)seq;
-        d->mb->tail[t] = (uint32_t)seq;
+        d->mb->hot[ds::kHotTail + t] = (uint32_t)seq;
     }
     for (int i = 0; i < DS_MAX_SMS; ++i) h.ctl.word[i] = ~0ull;
     h.rings = d->d_rings;
@@ -503,9 +503,9 @@ int ds_start(ds_domain* d) {
     // completions restart from index 0
     std::memset(d->h_comp, 0, sizeof(ds::HostCompletion) * d->comp_cap);
     d->comp_next = 0;
-    d->mb->exit = 0;
+    d->mb->hot[ds::kHotExit] = 0;
     d->mb->periodic_ns = 0;
-    d->mb->gen = 0;
+    d->mb->hot[ds::kHotGen] = 0;
     DS_CUDA(cudaMemcpyAsync(d->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, d->copy_stream));
     DS_CUDA(cudaStreamSynchronize(d->copy_stream));
     d->drain_stop = false;
@@ -526,7 +526,7 @@ int ds_stop(ds_domain* d) {
     std::lock_guard<std::mutex> g(d->mu);
     if (!d->running) return DS_OK;
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    d->mb->exit = 1;
+    d->mb->hot[ds::kHotExit] = 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
     cudaSetDevice(d->device);
     // bounded wait: a wedged tenant body must not hang the caller forever
@@ -581,7 +581,7 @@ static int launch_impl(ds_domain* d, int tenant, int kernel_id, uint64_t tag, ui
     t->launched_grid.push_back(exec_grid);
     t->next_seq = seq + 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    d->mb->tail[tenant] = (uint32_t)(seq + 1);
+    d->mb->hot[ds::kHotTail + tenant] = (uint32_t)(seq + 1);
     std::atomic_thread_fence(std::memory_order_seq_cst);
     d->enqueued++;
     if (seq_out) *seq_out = seq;
@@ -820,8 +820,29 @@ int ds_quota_periodic(ds_domain* d, uint64_t period_ns, const int32_t* oa, const
     }
     d->mb->periodic_ns = period_ns;
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    d->mb->periodic_gen = d->mb->periodic_gen + 1;
+    d->mb->hot[ds::kHotPGen] = d->mb->hot[ds::kHotPGen] + 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
+    return DS_OK;
+}
+
+// Host -> device control round trip: write a control word, spin until the
+// loader acknowledges it installed (host-mapped ack), n times; ns per sample.
+int ds_ctl_roundtrip(ds_domain* d, int n, uint64_t* out_ns) {
+    if (check_dom(d) || !out_ns) return fail(DS_INVALID_ARGUMENT, "null");
+    if (!d->running) return fail(DS_NOT_RUNNING, "executor not running");
+    for (int i = 0; i < n; ++i) {
+        uint32_t want;
+        auto t0 = std::chrono::steady_clock::now();
+        {
+            std::lock_guard<std::mutex> g(d->mu);
+            push_control(d);
+            want = d->mb->hot[ds::kHotGen];
+        }
+        while (d->mb->ack_gen != want) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) return fail(DS_TIMEOUT, "no ack");
+        }
+        out_ns[i] = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    }
     return DS_OK;
 }
 
@@ -946,12 +967,12 @@ int ds_debug_dump(ds_domain* d, char* out, int64_t cap) {
     char line[256];
     snprintf(line, sizeof line, "ctl.gen=%u exit=%u blocks=%llu comp=%llu trig_next=%u trig_count=%u mb.gen=%u host_comp_next=%llu\n",
              st->ctl.gen, st->ctl.exit, st->blocks_executed, st->completion_count, st->trig_next, st->trig_count,
-             d->mb->gen, (unsigned long long)d->comp_next);
+             d->mb->hot[ds::kHotGen], (unsigned long long)d->comp_next);
     s += line;
     for (int t = 0; t < (int)d->tenants.size(); ++t) {
         const ds::DevTenant& T = st->tenants[t];
         snprintf(line, sizeof line, "tenant %d: claim seq=%u blk=%u tail=%u head=%u host_tail=%u next_seq=%llu completed=%llu\n", t,
-                 (unsigned)(T.claim >> 32), (unsigned)(T.claim & 0xffffffffu), T.tail, T.head, d->mb->tail[t],
+                 (unsigned)(T.claim >> 32), (unsigned)(T.claim & 0xffffffffu), T.tail, T.head, d->mb->hot[ds::kHotTail + t],
                  (unsigned long long)d->tenants[t]->next_seq, (unsigned long long)d->tenants[t]->completed.load());
         s += line;
     }

@@ -186,6 +186,11 @@ class Domain:
         check(lib().ds_globaltimer(self.h, ctypes.byref(out)))
         return out.value
 
+    def ctl_roundtrip(self, n: int = 100) -> List[int]:
+        arr = (ctypes.c_uint64 * n)()
+        check(lib().ds_ctl_roundtrip(self.h, n, arr))
+        return list(arr)
+
     def debug(self) -> str:
         buf = ctypes.create_string_buffer(1 << 16)
         check(lib().ds_debug_dump(self.h, buf, len(buf)))

@@ -69,7 +69,7 @@ class DecodeConfig:
 
 
 class DecodeModel:
-    def __init__(self, cfg: DecodeConfig = DecodeConfig(), device="cuda", seed: int = 0):
+    def __init__(self, cfg: DecodeConfig = DecodeConfig(), device="cuda", seed: int = 0, split_override: str = ""):
         assert cfg.batch == 32 and cfg.d == cfg.n_q * 128 and cfg.n_q == 4 * cfg.n_kv
         self.cfg = cfg
         c = cfg
@@ -110,6 +110,14 @@ class DecodeModel:
             "down": pick_split(c.d // 128, c.ffn // 64),
             "lm": pick_split(c.vocab // 128, c.d // 64),
         }
+        # measured on B200 with early start (scripts/timeline.py sweep): fewer,
+        # larger K-splits than the wave-quantisation optimum win once weight
+        # streams overlap the previous kernel
+        self.S.update({"qkv": 3, "o": 3, "gu": 2, "down": 5})
+        if split_override:  # e.g. "o:4,down:5"
+            for kv in split_override.split(","):
+                k, v = kv.split(":")
+                self.S[k] = int(v)
         ws_elems = max(self.S["qkv"] * self.qkv_n, self.S["o"] * c.d, self.S["gu"] * 2 * c.ffn,
                        self.S["down"] * c.d, self.S["lm"] * c.vocab) * 32
         self.ws = torch.zeros(ws_elems, device=device)
