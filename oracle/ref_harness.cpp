@@ -16,10 +16,48 @@
 #include <json.hpp>
 
 #include <chrono>
+#include <csetjmp>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
 #include <cstring>
 #include <string>
 
 using namespace corosim;
+
+// The reference checks its invariants with assert(); an assertion inside the
+// simulator must not abort the process that hosts the checker, so the harness
+// supplies glibc's assertion handler (bound locally, -Bsymbolic) and longjmps
+// back to the entry point, which reports the failed check as an error string
+// (glibc declares the handler noexcept, so it cannot throw).  No reference
+// source is changed; the same check still fires.  The abandoned simulation's
+// memory is leaked — acceptable on this error path.
+namespace {
+thread_local std::jmp_buf* g_assert_jmp = nullptr;
+thread_local std::string g_assert_msg;
+}  // namespace
+
+extern "C" void __assert_fail(const char* expr, const char* file, unsigned int line, const char* func) {
+    g_assert_msg = std::string("reference assertion failed: ") + expr + " (" + file + ":" + std::to_string(line) +
+                   ", " + func + ")";
+    if (g_assert_jmp) std::longjmp(*g_assert_jmp, 1);
+    std::fprintf(stderr, "%s\n", g_assert_msg.c_str());
+    std::abort();
+}
+
+#define REF_GUARDED(out, cap, body)                       \
+    do {                                                  \
+        std::jmp_buf jb;                                  \
+        if (setjmp(jb)) {                                 \
+            g_assert_jmp = nullptr;                       \
+            put(std::string("error: ") + g_assert_msg, out, cap); \
+            return 2;                                     \
+        }                                                 \
+        g_assert_jmp = &jb;                               \
+        int rc_ = [&]() -> int { body }();                \
+        g_assert_jmp = nullptr;                           \
+        return rc_;                                       \
+    } while (0)
 
 namespace {
 
@@ -106,7 +144,7 @@ int ref_reduce_values(int fmt, const char* values_nl, long long n, long long g, 
 // Runs scenario_from_json + SimEngine::simulate + compute_metrics and returns
 // a JSON document {metrics, wall_ns, events, transcripts, logical_progress}.
 int ref_simulate_json(const char* scenario_json, char* out, long cap) {
-    try {
+    REF_GUARDED(out, cap, try {
         auto cfg = nlohmann::json::parse(scenario_json);
         Scenario s = scenario_from_json(cfg, ".");
         auto t0 = std::chrono::steady_clock::now();
@@ -142,12 +180,12 @@ int ref_simulate_json(const char* scenario_json, char* out, long cap) {
     } catch (const std::exception& e) {
         put(std::string("error: ") + e.what(), out, cap);
         return 1;
-    }
+    });
 }
 
 // check_immutable_equivalence (equivalence.cpp:56-95)
 int ref_equivalence_json(const char* scenario_json, char* out, long cap) {
-    try {
+    REF_GUARDED(out, cap, try {
         auto cfg = nlohmann::json::parse(scenario_json);
         Scenario s = scenario_from_json(cfg, ".");
         auto t0 = std::chrono::steady_clock::now();
@@ -163,7 +201,7 @@ int ref_equivalence_json(const char* scenario_json, char* out, long cap) {
     } catch (const std::exception& e) {
         put(std::string("error: ") + e.what(), out, cap);
         return 1;
-    }
+    });
 }
 
 }  // extern "C"
