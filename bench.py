@@ -122,7 +122,8 @@ class ClockSampler:
 # GPU arm
 # ---------------------------------------------------------------------------
 class Colocation:
-    def __init__(self, device, tokens_per_req, kv_len, layers=32, decode_sat=Fraction(1, 2), slo_x=8.0):
+    def __init__(self, device, tokens_per_req, kv_len, layers=32, decode_sat=Fraction(1, 2), slo_x=8.0,
+                 tiers=(Fraction(1, 4), Fraction(3, 4), Fraction(1))):
         import torch
         from paper_2603_15042_b200 import _abi
         from paper_2603_15042_b200.runtime import Domain
@@ -140,7 +141,7 @@ class Colocation:
         # idle SMs are lent to training.  (With a 1/2 tier, the reference
         # SLO-aware rule can defer a bound decode forever once it predicts a
         # TPOT miss: upgrades count the vctx's own tier — SURVEY 8-appendix #2.)
-        self.tiers = [Fraction(1, 4), Fraction(3, 4), Fraction(1)]
+        self.tiers = [Fraction(t) for t in tiers]
         self.dom = Domain(device, tiers=self.tiers, block_log_capacity=0, lend_idle_sms=True)
         self.t_dec = self.dom.tenant("decode", _abi.LATENCY_CRITICAL)
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
@@ -260,8 +261,12 @@ class Colocation:
             tpot = (lasts - firsts) / (self.T - 1) / 1e6
             ttft = (infos[0].t_end - infos[0].t_first_claim) / 1e6
             e2e_tpot = ((host_tok_times[-1] - host_tok_times[0]) / (self.T - 1) / 1e6) if e2e else None
-            log(f"  req {req}: tpot {tpot:.3f} ms")
+            gaps = [(infos[i + 1].t_first_claim - infos[i].t_end) / 1e3 for i in range(self.T - 1)]
+            steps_ms = [(i.t_end - i.t_first_claim) / 1e6 for i in infos[1:]]
+            log(f"  req {req}: tpot {tpot:.3f} ms (step {statistics.mean(steps_ms):.3f} ms, "
+                f"host gap {statistics.mean(gaps):.1f} us)")
             results.append({"tpot_ms": tpot, "first_ms": ttft, "t0": infos[0].t_first_claim, "t1": lasts,
+                            "gap_us": statistics.mean(gaps), "step_ms": statistics.mean(steps_ms),
                             "e2e_tpot_ms": e2e_tpot, "preempted": sum(i.preempted for i in infos)})
             t_next = arrival + period
         stop.set()
@@ -289,6 +294,8 @@ class Colocation:
         dom.set_lend(-1)
         dom.quota_set([-1] * dom.num_sms)
         return {"tpot_ms": [r["tpot_ms"] for r in timed], "e2e_tpot_ms": [r["e2e_tpot_ms"] for r in timed],
+                "gap_us": statistics.mean(r["gap_us"] for r in timed),
+                "step_ms": statistics.mean(r["step_ms"] for r in timed),
                 "window_ms": (w1 - w0) / 1e6, "train_tflops": done_flop / ((w1 - w0) * 1e-9) / 1e12,
                 "counters": counters, "gemm_ms_median": statistics.median(gemm_durs) / 1e6 if gemm_durs else None}
 
@@ -371,7 +378,7 @@ def gpu_arm(args, rank, world):
     peaks, peaks_src = load_peaks()
     log("building tenants")
     co = Colocation(dev, args.tokens, args.kv_len, layers=args.layers, decode_sat=Fraction(args.decode_sat),
-                    slo_x=args.slo_x)
+                    slo_x=args.slo_x, tiers=[Fraction(t) for t in args.tiers.split(",")])
     solo = co.solo(steps=max(3, args.warmup))
     log("solo", {k: v for k, v in solo.items() if k != "per_kernel_ns" and k != "per_kernel_launches"})
     with ClockSampler(dev) as clk:
@@ -399,7 +406,8 @@ def gpu_arm(args, rank, world):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random tokens)",
         "config": {"workload": "config 2: Llama-3-8B-shaped decode (batch 32, KV 1024, 32 layers) + bf16 GEMM "
                                "8192^3 training tenant on 1 B200", "policy": "tpot-first (+idle-SM lending)",
-                   "baseline_policy": f"temporal (time slicing, quantum {args.quantum_ms} ms)",
+                   "baseline_policy": f"temporal (time slicing, quantum {args.quantum_ms} ms)", "tiers": args.tiers,
+                   "decode_saturation": args.decode_sat,
                    "tokens_per_request": args.tokens, "requests_timed": args.steps,
                    "global_batch": 32, "seq_len": args.kv_len, "parallelism": f"independent domain per GPU x{world}",
                    "l2": "inputs larger than L2 (15 GB weights + 4.3 GB KV per step, 384 MB GEMM operands)"},
@@ -453,7 +461,7 @@ def gather_ranks(out, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--tokens", type=int, default=8)
@@ -463,6 +471,7 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--decode-sat", default="1/2", help="decode compute saturation (tier wanted)")
     ap.add_argument("--slo-x", type=float, default=8.0, help="TPOT SLO as a multiple of the solo step")
+    ap.add_argument("--tiers", default="1/4,1/2,3/4,1", help="pctx pool tiers (create_pool; SPEC.md:65 pool)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", 0))

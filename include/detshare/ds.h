@@ -294,6 +294,57 @@ int ds_engine_transcript(ds_engine* eng, int job, uint64_t* rec_ids, int cap, in
 int ds_engine_predict(ds_engine* eng, const char* semantic_id, int64_t grid, int64_t* ns);
 int ds_policy_names(char* out, int cap);
 
+
+/* ---- request streams and workload expansion ----
+ * gen_poisson / gen_burst       proj/src/io/trace.cpp:189-232 (RequestTemplate trace.hpp:41-53)
+ * expand_workload               proj/src/io/workload.cpp:51-174
+ * Arrival times: arrival_q = round(t * 1e9), t in the trace's time unit
+ * (the reference's quantize(), trace.cpp:159-162, as an exact integer). */
+typedef enum ds_request_kind { DS_REQ_INFERENCE = 0, DS_REQ_TRAINING = 1 } ds_request_kind;
+
+typedef struct ds_request_template {
+    int kind;                              /* ds_request_kind */
+    int prompt_tokens, prompt_tokens_max;  /* drawn uniformly in [v, v_max] when v_max > v */
+    int output_tokens, output_tokens_max;
+    int iterations;                        /* training */
+    int streams;                           /* requests round-robin over `streams` job ids */
+} ds_request_template;
+
+typedef struct ds_request {
+    int64_t arrival_q;  /* round(arrival * 1e9) */
+    int32_t stream;     /* job id "<prefix>-<stream>" */
+    int32_t kind;
+    int32_t prompt_tokens, output_tokens, iterations;
+    int32_t pad;
+} ds_request;
+
+typedef struct ds_expand_params {
+    int64_t tokens_per_grid_unit; /* InferenceProfile (workload.hpp:24): prefill grid = ceil(prompt / this) */
+    int64_t decode_grid;          /* InferenceProfile.decode_grid */
+    int64_t train_grid;           /* TrainingProfile.grid */
+    int32_t default_iterations;   /* TrainingProfile.iterations */
+    int32_t pad;
+} ds_expand_params;
+
+typedef struct ds_kernel_plan { /* one expanded Kernel record */
+    int64_t request;            /* index into the request array */
+    int32_t job;                /* vctx index: first appearance of the stream */
+    int32_t phase;              /* ds_phase */
+    int32_t decode_index;       /* -1 unless decode */
+    int32_t pad;
+    int64_t grid_size;
+    int64_t arrival_q;          /* arrival_floor */
+    uint64_t lab_seed;          /* mix_seed(job, position in job) (workload.cpp:10-16) */
+} ds_kernel_plan;
+
+/* out may be NULL / cap 0 to size the result: *n is always the full count */
+int ds_gen_poisson(double rate, double duration, const ds_request_template* tmpl, uint64_t seed, ds_request* out,
+                   int64_t cap, int64_t* n);
+int ds_gen_burst(double base_rate, double burst_rate, double burst_duration, double period, double duration,
+                 const ds_request_template* tmpl, uint64_t seed, ds_request* out, int64_t cap, int64_t* n);
+int ds_expand_workload(const ds_request* reqs, int64_t n_reqs, const ds_expand_params* params, ds_kernel_plan* out,
+                       int64_t cap, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,10 @@ def reference():
                                           ctypes.c_longlong, ctypes.c_int, ctypes.c_char_p, ctypes.c_long]
         lib.ref_simulate_json.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_long]
         lib.ref_equivalence_json.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_long]
+        lib.ref_gen_trace.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)] + [ctypes.c_int] * 7 + [
+            ctypes.c_ulonglong, ctypes.c_char_p, ctypes.c_long]
+        lib.ref_expand.argtypes = [ctypes.c_char_p, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong,
+                                   ctypes.c_int, ctypes.c_char_p, ctypes.c_long]
         _ref = lib
     return _ref
 
@@ -146,3 +150,18 @@ def ref_simulate(scenario_json: str) -> str:
 
 def ref_equivalence(scenario_json: str) -> str:
     return _call(reference().ref_equivalence_json, scenario_json.encode(), cap=1 << 20)
+
+
+def ref_gen_trace(which: str, rates, kind: int, prompt: int, prompt_max: int, output: int, output_max: int,
+                  iterations: int, streams: int, seed: int) -> str:
+    """gen_poisson / gen_burst of the reference (trace.cpp:189-232) as JSONL."""
+    arr = (ctypes.c_double * len(rates))(*rates)
+    return _call(reference().ref_gen_trace, 0 if which == "poisson" else 1, arr, kind, prompt, prompt_max, output,
+                 output_max, iterations, streams, seed, cap=1 << 26)
+
+
+def ref_expand(trace_jsonl: str, tokens_per_grid_unit: int, decode_grid: int, train_grid: int,
+               default_iterations: int) -> str:
+    """expand_workload of the reference (workload.cpp:51-174), one line per kernel."""
+    return _call(reference().ref_expand, trace_jsonl.encode(), tokens_per_grid_unit, decode_grid, train_grid,
+                 default_iterations, cap=1 << 26)

@@ -8,6 +8,8 @@
 #include "corosim/engine/engine.hpp"
 #include "corosim/io/metrics.hpp"
 #include "corosim/io/scenario.hpp"
+#include "corosim/io/trace.hpp"
+#include "corosim/io/workload.hpp"
 #include "corosim/numlab/equivalence.hpp"
 #include "corosim/numlab/float_format.hpp"
 #include "corosim/numlab/reduction.hpp"
@@ -15,12 +17,14 @@
 
 #include <json.hpp>
 
+#include <algorithm>
 #include <chrono>
 #include <csetjmp>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 using namespace corosim;
@@ -202,6 +206,72 @@ int ref_equivalence_json(const char* scenario_json, char* out, long cap) {
         put(std::string("error: ") + e.what(), out, cap);
         return 1;
     });
+}
+
+// gen_poisson (which == 0) / gen_burst (which == 1) (trace.cpp:189-232) with a
+// RequestTemplate (trace.hpp:41-53); returns the serialized JSONL trace
+// (serialize_trace, trace.cpp:153-155).  rates[] = {rate, duration} or
+// {base, burst, burst_duration, period, duration}.
+int ref_gen_trace(int which, const double* rates, int kind, int prompt, int prompt_max, int output, int output_max,
+                  int iterations, int streams, unsigned long long seed, char* out, long cap) {
+    try {
+        RequestTemplate t;
+        t.kind = kind == 0 ? "inference" : "training";
+        t.prompt_tokens = prompt;
+        t.prompt_tokens_max = prompt_max;
+        t.output_tokens = output;
+        t.output_tokens_max = output_max;
+        t.iterations = iterations;
+        t.streams = streams;
+        std::vector<RequestTraceRecord> recs =
+            which == 0 ? gen_poisson(rates[0], rates[1], t, seed)
+                       : gen_burst(rates[0], rates[1], rates[2], rates[3], rates[4], t, seed);
+        std::ostringstream os;
+        serialize_trace(recs, os);
+        return put(os.str(), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+// expand_workload (workload.cpp:51-174) of a JSONL trace with the given
+// profile grids; returns one line per kernel: "job phase grid decode_index
+// request seed" (seed = reduction seed, present when reduction_elements > 0).
+int ref_expand(const char* trace_jsonl, long long tokens_per_grid_unit, long long decode_grid, long long train_grid,
+               int default_iterations, char* out, long cap) {
+    try {
+        auto recs = parse_trace_string(trace_jsonl);
+        WorkloadProfiles prof;
+        prof.inference["default"].tokens_per_grid_unit = tokens_per_grid_unit;
+        prof.inference["default"].decode_grid = decode_grid;
+        prof.inference["default"].reduction_elements = 1;  // attach the lab seed to every kernel
+        prof.training["default"].grid = train_grid;
+        prof.training["default"].iterations = default_iterations;
+        prof.training["default"].reduction_elements = 1;
+        ExpandedWorkload w = expand_workload(recs, prof);
+        std::ostringstream os;
+        std::vector<std::string> lines;
+        // emit in (request, position) order like the native expansion
+        struct Row { long long req; std::size_t job, pos; const Kernel* k; };
+        std::vector<Row> rows;
+        for (std::size_t j = 0; j < w.jobs.size(); ++j)
+            for (std::size_t i = 0; i < w.jobs[j].kernels.size(); ++i)
+                rows.push_back({w.jobs[j].kernels[i].request.value, j, i, &w.jobs[j].kernels[i]});
+        std::stable_sort(rows.begin(), rows.end(), [](const Row& a, const Row& b) {
+            return a.req != b.req ? a.req < b.req : a.pos < b.pos;
+        });
+        for (const Row& r : rows) {
+            const Kernel& k = *r.k;
+            os << r.job << ' ' << static_cast<int>(k.phase) << ' ' << k.signature.grid_size << ' '
+               << k.decode_index << ' ' << k.request.value << ' '
+               << (k.reduction ? k.reduction->value_seed : 0ULL) << ' ' << to_decimal_string(k.arrival_floor) << '\n';
+        }
+        return put(os.str(), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
 }
 
 }  // extern "C"

@@ -247,6 +247,31 @@ class EngineCounters(ctypes.Structure):
                                                "unbinds", "policy_errors")]
 
 
+class RequestTemplate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("prompt_tokens", ctypes.c_int), ("prompt_tokens_max", ctypes.c_int),
+                ("output_tokens", ctypes.c_int), ("output_tokens_max", ctypes.c_int), ("iterations", ctypes.c_int),
+                ("streams", ctypes.c_int)]
+
+
+class Request(ctypes.Structure):
+    _fields_ = [("arrival_q", ctypes.c_int64), ("stream", ctypes.c_int32), ("kind", ctypes.c_int32),
+                ("prompt_tokens", ctypes.c_int32), ("output_tokens", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+class ExpandParams(ctypes.Structure):
+    _fields_ = [("tokens_per_grid_unit", ctypes.c_int64), ("decode_grid", ctypes.c_int64),
+                ("train_grid", ctypes.c_int64), ("default_iterations", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class KernelPlan(ctypes.Structure):
+    _fields_ = [("request", ctypes.c_int64), ("job", ctypes.c_int32), ("phase", ctypes.c_int32),
+                ("decode_index", ctypes.c_int32), ("pad", ctypes.c_int32), ("grid_size", ctypes.c_int64),
+                ("arrival_q", ctypes.c_int64), ("lab_seed", ctypes.c_uint64)]
+
+
+REQ_INFERENCE, REQ_TRAINING = 0, 1
+
 # exported symbols the header declares (checked by the CPU test suite)
 EXPORTS = [
     "ds_status_name", "ds_last_error", "ds_abi_version", "ds_domain_create", "ds_domain_destroy",
@@ -259,6 +284,7 @@ EXPORTS = [
     "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_kv", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
+    "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload",
 ]
 
 _lib = None
@@ -334,6 +360,14 @@ def lib():
                                            ctypes.POINTER(ctypes.c_int)]
         L.ds_engine_predict.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         L.ds_policy_names.argtypes = [ctypes.c_char_p, ctypes.c_int]
+        L.ds_gen_poisson.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.POINTER(RequestTemplate),
+                                     ctypes.c_uint64, ctypes.POINTER(Request), ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_int64)]
+        L.ds_gen_burst.argtypes = [ctypes.c_double] * 5 + [ctypes.POINTER(RequestTemplate), ctypes.c_uint64,
+                                                           ctypes.POINTER(Request), ctypes.c_int64,
+                                                           ctypes.POINTER(ctypes.c_int64)]
+        L.ds_expand_workload.argtypes = [ctypes.POINTER(Request), ctypes.c_int64, ctypes.POINTER(ExpandParams),
+                                         ctypes.POINTER(KernelPlan), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         _lib = L
     return _lib
 

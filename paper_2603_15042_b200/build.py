@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUTLASS_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/flashinfer/data/cutlass/include"
 
 CU_SOURCES = ["executor.cu"]
-CPP_SOURCES = ["runtime.cpp", "policy.cpp", "engine.cpp"]
+CPP_SOURCES = ["runtime.cpp", "policy.cpp", "engine.cpp", "workload.cpp"]
 
 
 def sources():
@@ -59,8 +59,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC] + common + ["-std=c++20", "-x", "cu"] + ARCH + ["-c", os.path.join(CSRC, src), "-o", obj]
         _run(cmd, verbose)
         objs.append(obj)
+    # export only the C ABI (ds_*): no std:: template instances that another
+    # C++ library in the same process (e.g. the oracle) could bind to
     cmd = [NVCC, "-shared", "-Xcompiler", "-fPIC"] + ARCH + objs + ["-cudart", "static", "-o", LIB,
-                                                                     "-Xlinker", "-lpthread"]
+                                                                     "-Xlinker", "-lpthread", "-Xlinker",
+                                                                     "--version-script=" + os.path.join(CSRC, "exports.map")]
     _run(cmd, verbose)
     return LIB
 

@@ -8,12 +8,27 @@ src/engine/engine.cpp:620-806).
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
+import weakref
 from fractions import Fraction
 from typing import Iterable, List, Optional, Sequence, Tuple
 
 from . import _abi
 from ._abi import check, check_engine, lib
+
+
+_LIVE: "weakref.WeakSet[Domain]" = weakref.WeakSet()
+
+
+@atexit.register
+def _stop_live_domains():
+    for d in list(_LIVE):
+        try:
+            d.stop()
+            d.close()
+        except Exception:
+            pass
 
 
 class Domain:
@@ -39,6 +54,10 @@ class Domain:
         check(lib().ds_num_sms(self.h, ctypes.byref(n)))
         self.num_sms = n.value
         self._args_keep = []
+        # a script that dies with the persistent executor still resident would
+        # hang process teardown (the CUDA context waits for the kernel): stop
+        # it at interpreter exit
+        _LIVE.add(self)
 
     # -- lifecycle --
     def close(self):

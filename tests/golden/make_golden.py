@@ -12,6 +12,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, os.path.dirname(HERE))
 
 from oracle import loader, numlab as nl  # noqa: E402
 
@@ -48,6 +49,18 @@ def main():
     with open(os.path.join(HERE, "round_to_golden.json"), "w") as f:
         json.dump({"source": out["source"], "cases": rt}, f, indent=0)
     print("wrote", len(out["cases"]), "reduction cases,", len(rt), "round_to cases")
+    # request streams + expansion (trace.cpp:189-232, workload.cpp:51-174) from the reference
+    import test_workload as tw  # noqa: E402  (tests/ on sys.path below)
+    wcases = []
+    for gen, rates, tk, seed in tw.CASES[:4]:
+        recs = [list(tw.ref_tuple(j)) for j in tw.ref_records(gen, rates, tk, seed)]
+        text = "\n".join(json.dumps(j) for j in tw.ref_records(gen, rates, tk, seed))
+        plan = [[int(x) for x in line.split()[:6]] for line in loader.ref_expand(text, 8, 164, 2048, 5).splitlines()]
+        wcases.append({"gen": gen, "rates": list(rates), "template": tk, "seed": seed, "records": recs,
+                       "plan": plan})
+    with open(os.path.join(HERE, "workload_golden.json"), "w") as f:
+        json.dump({"source": out["source"], "cases": wcases}, f)
+    print("wrote", len(wcases), "workload cases")
 
 
 if __name__ == "__main__":
