@@ -170,10 +170,14 @@ class Colocation:
         n = len(self.dec_kernels)
         ends = [cs[(i + 1) * n - 1].t_end for i in range(steps)]
         step_ns = [(ends[i] - ends[i - 1]) for i in range(1, steps)]
+        # per-kernel device time on the step's critical path: from the later of
+        # its first claim and the previous launch's completion (early-started
+        # blocks stream operands while the previous launch finishes) to its end
         per_kernel = {}
         for i, c in enumerate(cs):
             sid = self.model.records[i % n][0]
-            per_kernel.setdefault(sid, []).append(c.t_end - c.t_first_claim)
+            start = c.t_first_claim if i == 0 else max(c.t_first_claim, cs[i - 1].t_end)
+            per_kernel.setdefault(sid, []).append(c.t_end - start)
         dom.quota_set(dom.mask(self.t_trn, 0, dom.num_sms))
         for _ in range(3):
             last = dom.launch(self.t_trn, self.gemm_kernel)
@@ -392,7 +396,8 @@ def gpu_arm(args, rank, world):
     p99_tm = nearest_rank(tm["tpot_ms"], 99)
     p99_e2e = nearest_rank(e2e["e2e_tpot_ms"], 99)
     m = co.model
-    # roofline: per-launch algorithmic bytes / solo per-launch duration (device timestamps)
+    # roofline: per-launch algorithmic bytes / per-launch critical-path duration
+    # (device %globaltimer, solo decode steps through the executor, full GPU)
     kn = solo["per_kernel_ns"]
     bytes_by = {sid: b for sid, _, _, _, b in m.records}
     share = {sid: kn[sid] * solo["per_kernel_launches"][sid] for sid in kn}

@@ -376,7 +376,18 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         tc::fence_mbar_init();
         tc::tma_fence_desc(&a.tmK);
         tc::tma_fence_desc(&a.tmV);
-        for (int i = 0; i < min(kAttnStages, nch); ++i) issue(i);
+    }
+    // Early start: the cache rows below L-1 are immutable for this step (the
+    // preceding QKV launch appends position L-1 only), so their first stages
+    // stream while that launch finishes; the chunk holding L-1 and the query
+    // rows are read only after wait_prev (launch order + acquire).
+    int pre = 0;
+    if (ltid() == 0) {
+        while (pre < min(kAttnStages, nch) && p0 + (pre + 1) * kAttnChunk <= a.L - 1) issue(pre++);
+    }
+    wait_prev(c);
+    if (ltid() == 0) {
+        for (int i = pre; i < min(kAttnStages, nch); ++i) issue(i);
     }
     body_sync();
     const float scale = a.scale;

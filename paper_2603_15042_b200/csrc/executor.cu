@@ -36,7 +36,9 @@ constexpr uint32_t kLaneTmemCols = kTmemCols / kLanes;
 // ---------------------------------------------------------------------------
 // Bodies that handle the early-start dependency themselves (stream immutable
 // operands before wait_prev); every other body waits before it starts.
-__device__ __forceinline__ bool early_start_body(int body) { return body == DS_BODY_GEMV_BF16; }
+__device__ __forceinline__ bool early_start_body(int body) {
+    return body == DS_BODY_GEMV_BF16 || body == DS_BODY_ATTN_DECODE;
+}
 
 __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
     if (!early_start_body(body)) wait_prev(c);
