@@ -147,7 +147,99 @@ class Colocation:
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
         self.dec_kernels = self.model.register(self.dom)
         self.gemm_kernel = self.train.register(self.dom)
+        self.resnet = None
         self.dom.start()
+
+    def add_resnet(self):
+        """Config 4 training tenant: the ResNet-50-shaped kernel stream."""
+        from paper_2603_15042_b200.tenants import ResNetStream
+        self.resnet = ResNetStream(device=f"cuda:{self.device}")
+        self.t_res = self.dom.tenant("resnet", self._abi.BEST_EFFORT)
+        self.res_kernels = self.resnet.register(self.dom)
+        dom = self.dom
+        dom.quota_set(dom.mask(self.t_res, 0, dom.num_sms))
+        for _ in range(2):
+            for k in self.res_kernels:
+                last = dom.launch(self.t_res, k)
+        dom.wait(self.t_res, last)
+        cs = [c for c in dom.poll(1 << 20) if c.tenant == self.t_res]
+        n = len(self.res_kernels)
+        self.res_iter_ns = cs[-1].t_end - cs[-n].t_first_claim
+        dom.quota_set([-1] * dom.num_sms)
+        return self.res_iter_ns / 1e6
+
+    def run_bursty(self, policy, arrivals_ns, tokens, step_ns, quantum_ms=5.0):
+        """Config 4: bursty decode requests (arrivals from the reference's
+        gen_burst) co-located with the ResNet-50 training stream.  Returns
+        per-request TTFT / TPOT / latency and training images/s."""
+        from paper_2603_15042_b200.runtime import Engine
+        _abi, dom = self._abi, self.dom
+        lend = self.t_res if policy != "temporal" else -1
+        eng = Engine(dom, policy=policy, quantum_ns=int(quantum_ms * 1e6), lend_tenant=lend, fair_handover=True)
+        jd = eng.add_job(self.t_dec, _abi.LATENCY_CRITICAL)
+        jt = eng.add_job(self.t_res, _abi.BEST_EFFORT)
+        dom.set_lend(lend)
+        eng.start()
+        stop = threading.Event()
+        train_recs = []
+
+        def trainer():
+            outstanding = []
+            while not stop.is_set():
+                while len(outstanding) < 2:
+                    r = eng.submit(jt, self.res_kernels, "resnet/iter", _abi.TRAINING, grid_size=len(self.res_kernels),
+                                   base_hint_ns=self.res_iter_ns, saturation=Fraction(1))
+                    outstanding.append(r)
+                    train_recs.append(r)
+                outstanding = [r for r in outstanding if eng.record(r).state != 2]
+                time.sleep(0.0005)
+
+        th = threading.Thread(target=trainer, daemon=True)
+        th.start()
+        time.sleep(0.05)
+        t0 = eng.now() + 10_000_000
+        tpot_slo, ttft_slo = int(self.slo_x * step_ns), int(4 * self.slo_x * step_ns)
+        reqs = []
+        for i, a in enumerate(arrivals_ns):
+            while eng.now() < t0 + a:
+                time.sleep(0.0001)
+            arr = eng.now()
+            recs = [eng.submit(jd, self.dec_kernels, "decode/step", _abi.DECODE, grid_size=len(self.dec_kernels),
+                               request=i, decode_index=k, request_arrival_ns=arr, ttft_ns=ttft_slo, tpot_ns=tpot_slo,
+                               base_hint_ns=step_ns, saturation=self.decode_sat) for k in range(tokens)]
+            reqs.append((arr, recs))
+        for _, recs in reqs:
+            eng.wait(recs[-1], timeout_ms=120000)
+        stop.set()
+        th.join()
+        for r in train_recs:
+            eng.wait(r)
+        out = []
+        for arr, recs in reqs:
+            inf = [eng.record(r) for r in recs]
+            out.append({"ttft_ms": (inf[0].finish_host_ns - arr) / 1e6,
+                        "tpot_ms": (inf[-1].t_end - inf[0].t_end) / (tokens - 1) / 1e6,
+                        "latency_ms": (inf[-1].finish_host_ns - arr) / 1e6,
+                        "w0": inf[0].t_first_claim, "w1": inf[-1].t_end})
+        w0 = min(o["w0"] for o in out)
+        w1 = max(o["w1"] for o in out)
+        iters = 0.0
+        for ti in (eng.record(r) for r in train_recs):
+            a, b = ti.t_first_claim, ti.t_end
+            if b > a:
+                iters += max(0, min(b, w1) - max(a, w0)) / (b - a)
+        counters = eng.counters()
+        eng.stop()
+        eng.close()
+        dom.set_lend(-1)
+        dom.quota_set([-1] * dom.num_sms)
+        win_s = (w1 - w0) * 1e-9
+        return {"requests": len(out), "p99_tpot_ms": round(nearest_rank([o["tpot_ms"] for o in out], 99), 3),
+                "p99_ttft_ms": round(nearest_rank([o["ttft_ms"] for o in out], 99), 3),
+                "p99_latency_ms": round(nearest_rank([o["latency_ms"] for o in out], 99), 3),
+                "train_images_per_s": round(iters * self.resnet.batch / win_s, 1),
+                "train_tflops": round(iters * self.resnet.flops / win_s / 1e12, 1),
+                "window_ms": round(win_s * 1e3, 1), "engine_counters": counters}
 
     def close(self):
         self.dom.stop()
@@ -391,6 +483,24 @@ def gpu_arm(args, rank, world):
     clocks = clk.summary()
     e2e = co.run("tpot-first", args.steps, args.warmup, solo, e2e=True)
     exact = co.bit_exact_check()
+    config4 = None
+    if not args.no_config4:
+        from paper_2603_15042_b200 import workload as wl
+        res_ms = co.add_resnet()
+        unit_ms = 50.0
+        reqs = wl.gen_burst(0.5, 4.0, 2.0, 20.0, args.burst_units, wl.RequestTemplate(output_tokens=4), seed=0)
+        arrivals = [int(r.arrival_q * unit_ms * 1e-3) for r in reqs]  # arrival_q = round(t*1e9) -> ns
+        step_ns = int(solo["decode_step_ms"] * 1e6)
+        log(f"config 4: {len(arrivals)} bursty requests, resnet solo iter {res_ms:.2f} ms")
+        c4 = {p: co.run_bursty(p, arrivals, 4, step_ns, quantum_ms=args.quantum_ms) for p in ("tpot-first", "temporal")}
+        config4 = {"workload": "config 4: ResNet-50-shaped training stream (53 convs + FC, fwd/dgrad/wgrad = 161 "
+                               "tcgen05 GEMMs + split-K folds per iteration, batch 128, 224^2, bf16) co-located with "
+                               "bursty decode requests (4 tokens each)",
+                   "arrivals": f"gen_burst(base 0.5, burst 4.0, burst_duration 2, period 20, duration "
+                               f"{args.burst_units}) x {unit_ms} ms/unit (trace.cpp:204-232), seed 0",
+                   "resnet_solo_iter_ms": round(res_ms, 3),
+                   "resnet_solo_images_per_s": round(co.resnet.batch / (res_ms * 1e-3), 1),
+                   "tpot_first": c4["tpot-first"], "temporal": c4["temporal"]}
     co.close()
     p99 = nearest_rank(sp["tpot_ms"], 99)
     p99_tm = nearest_rank(tm["tpot_ms"], 99)
@@ -434,6 +544,7 @@ def gpu_arm(args, rank, world):
                           "traffic": ncu_traffic("train/gemm_bf16"), "algorithmic_bytes": 3 * 8192 * 8192 * 2},
         "clocks": clocks,
         "gpu_launches": len(m.records) * (args.steps + args.warmup) * args.tokens,
+        "config4": config4,
     }
     return out, solo
 
@@ -476,6 +587,8 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--decode-sat", default="1/2", help="decode compute saturation (tier wanted)")
     ap.add_argument("--slo-x", type=float, default=8.0, help="TPOT SLO as a multiple of the solo step")
+    ap.add_argument("--no-config4", action="store_true", help="skip the config 4 (ResNet + bursty decode) leg")
+    ap.add_argument("--burst-units", type=float, default=60.0, help="config 4 trace duration (units of 50 ms)")
     ap.add_argument("--tiers", default="1/4,1/2,3/4,1", help="pctx pool tiers (create_pool; SPEC.md:65 pool)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -71,7 +71,8 @@ typedef enum ds_body_id {
     DS_BODY_RMSNORM = 8,        /* row RMS statistics for the decode tenant */
     DS_BODY_EMBED = 9,          /* token embedding gather (decode step input) */
     DS_BODY_ARGMAX = 10,        /* greedy sampling (decode step result) */
-    DS_BODY_COUNT = 11
+    DS_BODY_SPLITK_REDUCE = 11, /* fold a split-K GEMM's fp32 partials in fixed split order */
+    DS_BODY_COUNT = 12
 } ds_body_id;
 
 typedef enum ds_priority { DS_LATENCY_CRITICAL = 0, DS_BEST_EFFORT = 1 } ds_priority; /* types.hpp:24 */

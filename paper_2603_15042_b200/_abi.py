@@ -27,6 +27,7 @@ BODY_GEMM_BF16 = 7
 BODY_RMSNORM = 8
 BODY_EMBED = 9
 BODY_ARGMAX = 10
+BODY_SPLITK_REDUCE = 11
 
 LATENCY_CRITICAL, BEST_EFFORT = 0, 1
 PREFILL, DECODE, TRAINING, OTHER = 0, 1, 2, 3
@@ -153,7 +154,13 @@ class TmaDesc(ctypes.Structure):
 class GemmArgs(ctypes.Structure):
     """C[M,N] bf16 = A[M,K] . B[N,K]^T (csrc/bodies/gemm_tc.cuh)."""
     _fields_ = [("tmA", TmaDesc), ("tmB", TmaDesc), ("C", ctypes.c_uint64), ("M", ctypes.c_int32),
-                ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32)]
+                ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32),
+                ("splits", ctypes.c_int32), ("ws", ctypes.c_uint64)]
+
+
+class SplitkReduceArgs(ctypes.Structure):
+    _fields_ = [("ws", ctypes.c_uint64), ("C", ctypes.c_uint64), ("M", ctypes.c_int32), ("N", ctypes.c_int32),
+                ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32), ("splits", ctypes.c_int32)]
 
 
 def tensor_map_bf16(ptr: int, rows: int, cols: int, box_rows: int, box_cols: int = 64) -> TmaDesc:
@@ -171,14 +178,30 @@ def tensor_map_kv(ptr: int, rows: int, box_rows: int = 32) -> TmaDesc:
 GEMM_BM, GEMM_BN = 128, 256
 
 
-def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16) -> "GemmArgs":
-    if M % GEMM_BM or N % GEMM_BN or K % 64:
-        raise DsError(10, f"gemm shape {M}x{N}x{K} must tile by 128x256x64")
-    return GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM), tensor_map_bf16(B, N, K, GEMM_BN), C, M, N, K, group_m)
+def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16, bn: int = GEMM_BN,
+              splits: int = 1, ws: int = 0) -> "GemmArgs":
+    if bn not in (64, 128, 256):
+        raise DsError(10, f"gemm tile width {bn} not in (64, 128, 256)")
+    if M % GEMM_BM or N % bn or K % 64:
+        raise DsError(10, f"gemm shape {M}x{N}x{K} must tile by 128x{bn}x64")
+    if splits > 1 and (not ws or splits > K // 64):
+        raise DsError(10, "split-K needs a workspace and <= K/64 splits")
+    return GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM), tensor_map_bf16(B, N, K, bn), C, M, N, K, group_m, bn,
+                    max(1, splits), ws)
 
 
-def gemm_grid(M: int, N: int):
-    return ((M // GEMM_BM) * (N // GEMM_BN), 1, 1)
+def gemm_grid(M: int, N: int, bn: int = GEMM_BN, splits: int = 1):
+    return ((M // GEMM_BM) * (N // bn) * max(1, splits), 1, 1)
+
+
+def splitk_ws_elems(M: int, N: int, bn: int, splits: int) -> int:
+    """fp32 workspace elements for a split-K GEMM: [tiles][S][128][bn]."""
+    return (M // GEMM_BM) * (N // bn) * splits * GEMM_BM * bn
+
+
+def splitk_reduce(ws: int, C: int, M: int, N: int, K: int, group_m: int, bn: int, splits: int):
+    """(args, grid) of the split-K fold launch that follows a split GEMM."""
+    return (SplitkReduceArgs(ws, C, M, N, K, group_m, bn, splits), ((M // GEMM_BM) * (N // bn) * 8, 1, 1))
 
 
 class GemvArgs(ctypes.Structure):

@@ -143,58 +143,136 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 // ---------------------------------------------------------------------------
 // Training GEMM tenant: C[M,N] (bf16) = A[M,K] . B[N,K]^T, fp32 accumulate.
-// Logical block t -> output tile (m_blk, n_blk), grouped raster so ~148
-// concurrent tiles share A/B panels in L2.
+// Tile 128 x BN (BN in {64, 128, 256}), optional split-K S: logical block
+// t -> (tile = t / S, split = t % S); tiles follow a grouped raster so the
+// concurrently running tiles share A/B panels in L2.  S > 1 writes each
+// split's fp32 partial to a workspace and a DS_BODY_SPLITK_REDUCE launch
+// folds them in fixed split order (deterministic wherever blocks run).
 // ---------------------------------------------------------------------------
 struct GemmArgs {
     TmaDesc tmA;  // A [M][K] bf16, box {64, 128}
-    TmaDesc tmB;  // B [N][K] bf16, box {64, 256}
+    TmaDesc tmB;  // B [N][K] bf16, box {64, BN}
     uint64_t C;   // bf16 [M][N]
     int32_t M, N, K;
     int32_t group_m;
+    int32_t bn;      // 0 or 256, 128, 64
+    int32_t splits;  // split-K factor S (0/1 = none)
+    uint64_t ws;     // fp32 [tiles][S][128][BN] when S > 1
 };
 
 constexpr int kGemmBN = 256;
 constexpr int kGemmStages = kCtasPerSm == 2 ? 2 : 4;
 
-__device__ void body_gemm_bf16(const BodyCtx& c) {
-    const GemmArgs& a = *reinterpret_cast<const GemmArgs*>(c.args);
-    char* base = align1024(c.smem);
-    const int m_blocks = a.M / kTcBM, n_blocks = a.N / kGemmBN;
-    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+__device__ __forceinline__ void gemm_tile_coords(const GemmArgs& a, int bn, int tile, int& m_blk, int& n_blk) {
+    const int m_blocks = a.M / kTcBM, n_blocks = a.N / bn;
     const int gm = a.group_m > 0 ? a.group_m : 16;
     const int group_size = gm * n_blocks;
-    const int g = t / group_size;
+    const int g = tile / group_size;
     const int first_m = g * gm;
     const int rows = min(gm, m_blocks - first_m);
-    const int r = t % group_size;
-    const int m_blk = first_m + r % rows;
-    const int n_blk = r / rows;
-    tc_mainloop<kGemmBN, kGemmStages>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * kGemmBN, 0, a.K / kTcBK, c.tmem_base,
-                                      false);
+    const int r = tile % group_size;
+    m_blk = first_m + r % rows;
+    n_blk = r / rows;
+}
+
+template <int BN, int STAGES>
+__device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a) {
+    char* base = align1024(c.smem);
+    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int S = a.splits > 1 ? a.splits : 1;
+    const int tile = t / S, sp = t % S;
+    int m_blk, n_blk;
+    gemm_tile_coords(a, BN, tile, m_blk, n_blk);
+    const int kbs = a.K / kTcBK;
+    const int kb0 = (int)((int64_t)sp * kbs / S), kb1 = (int)((int64_t)(sp + 1) * kbs / S);
+    tc_mainloop<BN, STAGES>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb0, kb1, c.tmem_base, false);
     const int warp = ltid() >> 5, lane = ltid() & 31;
     if (warp >= 4) {
         const int q = warp & 3;
-        const int row = m_blk * kTcBM + q * 32 + lane;
-        __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(a.C);
-        uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * a.N + n_blk * kGemmBN);
+        if (S == 1) {
+            const int row = m_blk * kTcBM + q * 32 + lane;
+            __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(a.C);
+            uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * a.N + n_blk * BN);
 #pragma unroll 1
-        for (int ch = 0; ch < kGemmBN / 32; ++ch) {
-            uint32_t v[32];
-            tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, v);
-            tc::tmem_ld_wait();
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, v);
+                tc::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint4 o;
-                o.x = pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
-                o.y = pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
-                o.z = pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
-                o.w = pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
-                dst[ch * 4 + j] = o;
+                for (int j = 0; j < 4; ++j) {
+                    uint4 o;
+                    o.x = pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                    o.y = pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                    o.z = pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                    o.w = pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                    dst[ch * 4 + j] = o;
+                }
+            }
+        } else {
+            // fp32 partial of this split: ws[tile][sp][row][BN]
+            float* ws = reinterpret_cast<float*>(a.ws) + (((size_t)tile * S + sp) * kTcBM + q * 32 + lane) * BN;
+            uint4* dst = reinterpret_cast<uint4*>(ws);
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dst[ch * 8 + j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
         }
     }
-    tc_teardown<kGemmBN, kGemmStages>(base);
+    tc_teardown<BN, STAGES>(base);
+}
+
+__device__ void body_gemm_bf16(const BodyCtx& c) {
+    const GemmArgs& a = *reinterpret_cast<const GemmArgs*>(c.args);
+    switch (a.bn) {
+        case 64: gemm_body_bn<64, kCtasPerSm == 2 ? 4 : 8>(c, a); break;
+        case 128: gemm_body_bn<128, kCtasPerSm == 2 ? 3 : 6>(c, a); break;
+        default: gemm_body_bn<kGemmBN, kGemmStages>(c, a); break;
+    }
+}
+
+// Split-K fold: block (tile, 16-row group) sums the S fp32 partials of its
+// rows in split order 0..S-1 and stores bf16.  grid = tiles * 8.
+struct SplitkReduceArgs {
+    uint64_t ws;  // fp32 [tiles][S][128][BN]
+    uint64_t C;   // bf16 [M][N]
+    int32_t M, N, K;
+    int32_t group_m;
+    int32_t bn;
+    int32_t splits;
+};
+
+__device__ void body_splitk_reduce(const BodyCtx& c) {
+    const SplitkReduceArgs& r = *reinterpret_cast<const SplitkReduceArgs*>(c.args);
+    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int tile = t >> 3, rg = t & 7;
+    GemmArgs g;
+    g.M = r.M;
+    g.N = r.N;
+    g.group_m = r.group_m;
+    int m_blk, n_blk;
+    gemm_tile_coords(g, r.bn, tile, m_blk, n_blk);
+    const int S = r.splits, BN = r.bn;
+    const float* ws = reinterpret_cast<const float*>(r.ws) + (size_t)tile * S * kTcBM * BN;
+    __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(r.C);
+    for (int idx = 4 * (int)ltid(); idx < 16 * BN; idx += 4 * kBodyThreads) {
+        const int row = rg * 16 + idx / BN, col = idx % BN;
+        float4 acc = __ldcg(reinterpret_cast<const float4*>(ws + (size_t)row * BN + col));
+        for (int s = 1; s < S; ++s) {
+            const float4 p = __ldcg(reinterpret_cast<const float4*>(ws + ((size_t)s * kTcBM + row) * BN + col));
+            acc.x += p.x;
+            acc.y += p.y;
+            acc.z += p.z;
+            acc.w += p.w;
+        }
+        uint2 o;
+        o.x = pack_bf16x2(acc.x, acc.y);
+        o.y = pack_bf16x2(acc.z, acc.w);
+        *reinterpret_cast<uint2*>(C + (size_t)(m_blk * kTcBM + row) * r.N + n_blk * BN + col) = o;
+    }
 }
 
 }  // namespace ds

@@ -52,6 +52,7 @@ __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
         case DS_BODY_RMSNORM: body_rmsnorm(c); break;
         case DS_BODY_EMBED: body_embed(c); break;
         case DS_BODY_ARGMAX: body_argmax(c); break;
+        case DS_BODY_SPLITK_REDUCE: body_splitk_reduce(c); break;
         default: break;
     }
 }
@@ -676,6 +677,7 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_RMSNORM: return 1024;
         case DS_BODY_EMBED: return 1024;
         case DS_BODY_ARGMAX: return 1024;
+        case DS_BODY_SPLITK_REDUCE: return 1024;
         default: return ds::kDefaultSmem;
     }
 }

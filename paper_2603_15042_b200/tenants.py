@@ -256,3 +256,103 @@ class TrainGemm:
 
     def register(self, dom, phase=_abi.TRAINING) -> int:
         return dom.kernel("train/gemm_bf16", _abi.BODY_GEMM_BF16, self.grid, self.args, phase=phase)
+
+
+# ---------------------------------------------------------------------------
+# Config 4: ResNet-50-shaped training kernel stream
+# ---------------------------------------------------------------------------
+def resnet50_convs(batch: int = 128, image: int = 224):
+    """The 53 convolutions + FC of ResNet-50 (v1.5: stride on the 3x3) as
+    (name, Cin, Cout, k, H_in, H_out) with H the square spatial size."""
+    convs = [("conv1", 3, 64, 7, image, image // 2)]
+    h = image // 4  # after the stride-2 max-pool
+    cin = 64
+    for stage, (width, blocks) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
+        out = width * 4
+        for blk in range(blocks):
+            stride = 2 if (blk == 0 and stage > 0) else 1
+            ho = h // stride
+            nm = f"s{stage + 2}b{blk}"
+            convs.append((nm + "_1x1a", cin, width, 1, h, h))
+            convs.append((nm + "_3x3", width, width, 3, h, ho))
+            convs.append((nm + "_1x1b", width, out, 1, ho, ho))
+            if blk == 0:
+                convs.append((nm + "_proj", cin, out, 1, h, ho))
+            cin = out
+            h = ho
+    return convs
+
+
+def _round(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def resnet50_gemms(batch: int = 128, image: int = 224):
+    """Implicit-GEMM shapes of one training iteration (forward, data-gradient
+    and weight-gradient of every conv + the FC layer), in execution order:
+    forward front to back, then backward back to front (wgrad before dgrad).
+    Each entry (name, M, N, K) with true (unpadded) sizes; conv1's dgrad (the
+    input-image gradient) is not computed, as in any training framework."""
+    convs = resnet50_convs(batch, image)
+    fwd, bwd = [], []
+    for name, ci, co, k, hi, ho in convs:
+        fwd.append((name + "/fwd", batch * ho * ho, co, ci * k * k))
+    fwd.append(("fc/fwd", batch, 1000, 2048))
+    bwd.append(("fc/wgrad", 1000, 2048, batch))
+    bwd.append(("fc/dgrad", batch, 2048, 1000))
+    for name, ci, co, k, hi, ho in reversed(convs):
+        bwd.append((name + "/wgrad", co, ci * k * k, batch * ho * ho))
+        if name != "conv1":
+            bwd.append((name + "/dgrad", batch * hi * hi, ci, co * k * k))
+    return fwd + bwd
+
+
+def plan_gemm(M: int, N: int, K: int, workers: int = WORKERS):
+    """Tile width and split-K for a padded GEMM: the widest tile giving >= one
+    wave of logical blocks, else the narrowest that divides N; split K while
+    the grid is short of a wave and every split keeps >= 8 k-blocks."""
+    Mp, Kp = _round(M, 128), _round(K, 64)
+    Np = _round(N, 64)
+    choices = [bn for bn in (256, 128, 64) if Np % bn == 0]
+    bn = next((b for b in choices if (Mp // 128) * (Np // b) >= workers), choices[-1])
+    tiles = (Mp // 128) * (Np // bn)
+    splits = 1
+    if tiles < workers:
+        splits = max(1, min(64, -(-workers // tiles), (Kp // 64) // 8))
+    return Mp, Np, Kp, bn, splits
+
+
+class ResNetStream:
+    """One ResNet-50 training iteration (batch 128, 224^2, bf16) as a stream of
+    tcgen05 GEMM launches (+ split-K folds), one per conv pass.  Operands are
+    padded to tile multiples and share three arenas (contents are synthetic;
+    shapes, flops and launch order are ResNet-50's)."""
+
+    def __init__(self, batch: int = 128, image: int = 224, device="cuda", seed: int = 2):
+        self.gemms = resnet50_gemms(batch, image)
+        self.batch = batch
+        self.flops = sum(2.0 * M * N * K for _, M, N, K in self.gemms)  # algorithmic (unpadded)
+        plans = [plan_gemm(M, N, K) for _, M, N, K in self.gemms]
+        self.padded_flops = sum(2.0 * Mp * Np * Kp for Mp, Np, Kp, _, _ in plans)
+        a_el = max(Mp * Kp for Mp, Np, Kp, _, _ in plans)
+        b_el = max(Np * Kp for Mp, Np, Kp, _, _ in plans)
+        c_el = max(Mp * Np for Mp, Np, Kp, _, _ in plans)
+        ws_el = max((_abi.splitk_ws_elems(Mp, Np, bn, s) if s > 1 else 0) for Mp, Np, Kp, bn, s in plans)
+        g = torch.Generator(device=device).manual_seed(seed)
+        self.A = (torch.rand(a_el, device=device, generator=g) * 2 - 1).to(torch.bfloat16)
+        self.B = (torch.rand(b_el, device=device, generator=g) * 2 - 1).to(torch.bfloat16)
+        self.C = torch.zeros(c_el, device=device, dtype=torch.bfloat16)
+        self.ws = torch.zeros(max(1, ws_el), device=device, dtype=torch.float32)
+        self.records = []  # (semantic_id, body, grid, args, flops)
+        for (name, M, N, K), (Mp, Np, Kp, bn, s) in zip(self.gemms, plans):
+            ga = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, bn=bn,
+                                splits=s, ws=self.ws.data_ptr() if s > 1 else 0)
+            self.records.append((f"resnet/{name}", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, s), ga,
+                                 2.0 * M * N * K))
+            if s > 1:
+                ra, rg = _abi.splitk_reduce(self.ws.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, 16, bn, s)
+                self.records.append((f"resnet/{name}/fold", _abi.BODY_SPLITK_REDUCE, rg, ra, 0.0))
+        self.plans = plans
+
+    def register(self, dom, phase=_abi.TRAINING) -> List[int]:
+        return [dom.kernel(sid, body, grid, args, phase=phase) for sid, body, grid, args, _ in self.records]

@@ -1,0 +1,40 @@
+"""ResNet-50-shaped training stream (config 4) through the executor on the
+full GPU: iteration time, achieved TFLOP/s, slowest GEMMs."""
+import os, sys, json, statistics, collections
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from fractions import Fraction
+from paper_2603_15042_b200 import _abi
+from paper_2603_15042_b200.runtime import Domain
+from paper_2603_15042_b200.tenants import ResNetStream
+
+rs = ResNetStream()
+torch.cuda.synchronize()
+print("launches/iter", len(rs.records), "TFLOP/iter", rs.flops / 1e12, "padded", rs.padded_flops / 1e12, flush=True)
+dom = Domain(0, tiers=[Fraction(1)], block_log_capacity=0)
+t = dom.tenant("train", _abi.BEST_EFFORT)
+kids = rs.register(dom)
+dom.start()
+dom.quota_set(dom.mask(t, 0, dom.num_sms))
+for k in kids: last = dom.launch(t, k)
+dom.wait(t, last); dom.poll(1 << 20)
+iters = 3
+for _ in range(iters):
+    for k in kids: last = dom.launch(t, k)
+dom.wait(t, last)
+cs = dom.poll(1 << 20)
+n = len(kids)
+it = [(cs[(i + 1) * n - 1].t_end - cs[i * n].t_first_claim) / 1e6 for i in range(iters)]
+ms = statistics.median(it)
+per = collections.defaultdict(list)
+for i, c in enumerate(cs):
+    start = c.t_first_claim if i == 0 else max(c.t_first_claim, cs[i - 1].t_end)
+    per[rs.records[i % n][0]].append((c.t_end - start) / 1e3)
+rows = sorted(((statistics.median(v), k) for k, v in per.items()), reverse=True)
+fl = {r[0]: r[4] for r in rs.records}
+out = {"iter_ms": ms, "tflops": rs.flops / (ms * 1e-3) / 1e12, "images_per_s": rs.batch / (ms * 1e-3),
+       "top": [(k, round(us, 1), round(fl[k] / (us * 1e-6) / 1e12, 1)) for us, k in rows[:15]]}
+print(json.dumps(out, indent=0), flush=True)
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump(out, open("gpurun_out/perf_resnet.json", "w"), indent=1)
+dom.stop(); dom.close()

@@ -55,3 +55,55 @@ def test_gemm_coroutine_bit_exact_vs_solo():
         log = [b for b in dom.block_log() if b.tenant == t]
     assert sorted(b.block for b in log) == list(range(nblk))
     assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
+
+
+def run_split(A, B, C, M, N, K, bn, S, ws, dom=None, t=None):
+    args = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, bn=bn, splits=S,
+                          ws=ws.data_ptr() if S > 1 else 0)
+    grid = _abi.gemm_grid(M, N, bn, S)
+    launches = [("gemm", _abi.BODY_GEMM_BF16, grid, args)]
+    if S > 1:
+        ra, rg = _abi.splitk_reduce(ws.data_ptr(), C.data_ptr(), M, N, K, 16, bn, S)
+        launches.append(("fold", _abi.BODY_SPLITK_REDUCE, rg, ra))
+    if dom is None:
+        for sid, body, g, a in launches:
+            solo_launch(0, sid, body, g, a)
+        torch.cuda.synchronize()
+        return None
+    kids = [dom.kernel(sid, body, g, a, phase=_abi.TRAINING) for sid, body, g, a in launches]
+    seqs = [dom.launch(t, k) for k in kids]
+    return seqs, grid[0]
+
+
+@pytest.mark.parametrize("shape", [(256, 192, 128, 64, 1), (384, 384, 512, 128, 1), (128, 64, 4096, 64, 16),
+                                   (256, 256, 2048, 128, 5), (128, 256, 3200, 256, 7)])
+def test_gemm_tile_widths_and_splitk_match_fp32_reference(shape):
+    """Config 4 GEMM variants: 128x64 / 128x128 tiles and split-K with the
+    fixed-order fold launch."""
+    M, N, K, bn, S = shape
+    A, B, C = make(M, N, K, seed=3)
+    ws = torch.zeros(max(1, _abi.splitk_ws_elems(M, N, bn, S)), device="cuda")
+    run_split(A, B, C, M, N, K, bn, S, ws)
+    ref = A.float() @ B.float().t()
+    err = (C.float() - ref).abs()
+    tol = ref.abs() * 2 ** -7 + 2 ** -6
+    assert bool((err <= tol).all()), float((err - tol).max())
+
+
+def test_splitk_coroutine_bit_exact_vs_solo():
+    M, N, K, bn, S = 256, 192, 8192, 64, 12
+    A, B, C_solo = make(M, N, K, seed=4)
+    C_co = torch.zeros_like(C_solo)
+    ws = torch.zeros(_abi.splitk_ws_elems(M, N, bn, S), device="cuda")
+    run_split(A, B, C_solo, M, N, K, bn, S, ws)
+    ws.zero_()
+    with Domain(0, block_log_capacity=1 << 16) as dom:
+        dom.start()
+        t = dom.tenant("train", _abi.BEST_EFFORT)
+        dom.quota_set(dom.mask(t, 0, 16))
+        dom.quota_at_claim(t, 0, 20, dom.mask(t, 40, 60))
+        seqs, nblk = run_split(A, B, C_co, M, N, K, bn, S, ws, dom, t)
+        dom.wait(t, seqs[-1])
+        got = C_co.cpu()
+    assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
+

@@ -27,3 +27,18 @@ def test_pack_sw128_is_the_tma_swizzle_image():
                 for c in range(8):
                     p = c ^ (r % 8)
                     assert torch.equal(t[r, p * 8:(p + 1) * 8], W[slab * 128 + r, kb * 64 + c * 8:kb * 64 + (c + 1) * 8])
+
+
+def test_resnet_stream_plan_covers_resnet50():
+    """Config 4 layer table: 53 convs, 161 GEMMs per iteration (fwd + dgrad +
+    wgrad, no input-image dgrad), 4.09 GMAC/image forward at 224^2."""
+    from paper_2603_15042_b200.tenants import plan_gemm, resnet50_convs, resnet50_gemms
+    assert len(resnet50_convs()) == 53
+    g = resnet50_gemms()
+    assert len(g) == 161
+    fwd = sum(M * N * K for n, M, N, K in g if n.endswith("/fwd"))
+    assert abs(fwd / 128 / 1e9 - 4.09) < 0.02
+    for _, M, N, K in g:
+        Mp, Np, Kp, bn, s = plan_gemm(M, N, K)
+        assert Mp % 128 == 0 and Np % bn == 0 and Kp % 64 == 0 and Mp >= M and Np >= N and Kp >= K
+        assert 1 <= s <= Kp // 64
