@@ -346,6 +346,20 @@ int ds_gen_burst(double base_rate, double burst_rate, double burst_duration, dou
 int ds_expand_workload(const ds_request* reqs, int64_t n_reqs, const ds_expand_params* params, ds_kernel_plan* out,
                        int64_t cap, int64_t* n);
 
+/* ---- workload-aware placement across GPUs (config 5) ----
+ * Replaces first-fit pick_bind_target across devices (policies.cpp:74-94) for
+ * whole tenants: balances per-device HBM and tensor load, spreads
+ * latency-critical tenants, respects a resident-memory cap.  Deterministic. */
+typedef struct ds_tenant_demand {
+    int32_t priority;    /* ds_priority */
+    int32_t phase;       /* ds_phase of its kernels */
+    double hbm_frac;     /* solo HBM bytes/s / device peak */
+    double tensor_frac;  /* solo tensor flop/s / device peak */
+    double mem_gb;       /* resident footprint */
+} ds_tenant_demand;
+
+int ds_place_tenants(const ds_tenant_demand* tenants, int n, int n_devices, double mem_cap_gb, int32_t* device_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -295,6 +295,11 @@ class KernelPlan(ctypes.Structure):
 
 REQ_INFERENCE, REQ_TRAINING = 0, 1
 
+
+class TenantDemand(ctypes.Structure):
+    _fields_ = [("priority", ctypes.c_int32), ("phase", ctypes.c_int32), ("hbm_frac", ctypes.c_double),
+                ("tensor_frac", ctypes.c_double), ("mem_gb", ctypes.c_double)]
+
 # exported symbols the header declares (checked by the CPU test suite)
 EXPORTS = [
     "ds_status_name", "ds_last_error", "ds_abi_version", "ds_domain_create", "ds_domain_destroy",
@@ -307,7 +312,7 @@ EXPORTS = [
     "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_kv", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
-    "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload",
+    "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",
 ]
 
 _lib = None
@@ -389,6 +394,8 @@ def lib():
         L.ds_gen_burst.argtypes = [ctypes.c_double] * 5 + [ctypes.POINTER(RequestTemplate), ctypes.c_uint64,
                                                            ctypes.POINTER(Request), ctypes.c_int64,
                                                            ctypes.POINTER(ctypes.c_int64)]
+        L.ds_place_tenants.argtypes = [ctypes.POINTER(TenantDemand), ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                       ctypes.POINTER(ctypes.c_int32)]
         L.ds_expand_workload.argtypes = [ctypes.POINTER(Request), ctypes.c_int64, ctypes.POINTER(ExpandParams),
                                          ctypes.POINTER(KernelPlan), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         _lib = L

@@ -1,0 +1,96 @@
+"""Config 5 placement (csrc/placement.cpp, ds_place_tenants): determinism,
+balance of the 2-D (HBM, tensor) load, latency-critical spreading, memory
+cap, and agreement across gloo ranks (every rank computes the same map)."""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_15042_b200 import _abi
+from paper_2603_15042_b200.placement import TenantSpec, config5_mix, place
+
+
+def loads(mix, p, n):
+    h = [0.0] * n
+    t = [0.0] * n
+    for s, d in zip(mix, p):
+        h[d] += s.hbm_frac
+        t[d] += s.tensor_frac
+    return h, t
+
+
+def test_one_device_takes_everything():
+    mix = config5_mix()
+    assert place(mix, 1) == [0] * 16
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_balanced_and_spread(n):
+    mix = config5_mix()
+    p = place(mix, n)
+    assert p == place(mix, n)  # deterministic
+    assert sorted(set(p)) == list(range(n))
+    lc = [sum(1 for s, d in zip(mix, p) if d == k and s.priority == _abi.LATENCY_CRITICAL) for k in range(n)]
+    assert max(lc) - min(lc) <= 1  # latency-critical tenants spread evenly
+    h, t = loads(mix, p, n)
+    # no device carries more than the mean plus one largest tenant on either axis
+    assert max(h) <= sum(h) / n + max(s.hbm_frac for s in mix) + 1e-9
+    assert max(t) <= sum(t) / n + max(s.tensor_frac for s in mix) + 1e-9
+    if n == 8:  # one decode + one training tenant per GPU
+        assert all(c == 1 for c in lc)
+
+
+def test_pairs_decode_with_training():
+    mix = [TenantSpec("d0", "decode", _abi.LATENCY_CRITICAL, 0.8, 0.05, 10),
+           TenantSpec("d1", "decode", _abi.LATENCY_CRITICAL, 0.7, 0.05, 10),
+           TenantSpec("t0", "train", _abi.BEST_EFFORT, 0.05, 0.9, 1),
+           TenantSpec("t1", "train", _abi.BEST_EFFORT, 0.05, 0.8, 1)]
+    p = place(mix, 2)
+    assert p[0] != p[1] and p[2] != p[3]
+
+
+def test_memory_cap():
+    mix = [TenantSpec(f"t{i}", "train", _abi.BEST_EFFORT, 0.1, 0.1, 100.0) for i in range(3)]
+    assert place(mix, 2, mem_cap_gb=200.0).count(0) <= 2
+    with pytest.raises(_abi.DsError):
+        place(mix, 1, mem_cap_gb=150.0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_15042_b200.placement import config5_mix, place
+    mix = config5_mix()
+    p = place(mix, world)
+    mine = [i for i, d in enumerate(p) if d == rank]
+    allp = [None] * world
+    dist.all_gather_object(allp, (p, mine))
+    if rank == 0:
+        q.put(allp)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_ranks_agree_and_partition():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    allp = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert allp[0][0] == allp[1][0]
+    assert sorted(allp[0][1] + allp[1][1]) == list(range(16))
