@@ -72,7 +72,8 @@ typedef enum ds_body_id {
     DS_BODY_EMBED = 9,          /* token embedding gather (decode step input) */
     DS_BODY_ARGMAX = 10,        /* greedy sampling (decode step result) */
     DS_BODY_SPLITK_REDUCE = 11, /* fold a split-K GEMM's fp32 partials in fixed split order */
-    DS_BODY_COUNT = 12
+    DS_BODY_ALLREDUCE_P2P = 12, /* DP gradient all-reduce over NVLink peer memory, rank-ordered sum */
+    DS_BODY_COUNT = 13
 } ds_body_id;
 
 typedef enum ds_priority { DS_LATENCY_CRITICAL = 0, DS_BEST_EFFORT = 1 } ds_priority; /* types.hpp:24 */
@@ -345,6 +346,15 @@ int ds_gen_burst(double base_rate, double burst_rate, double burst_duration, dou
                  const ds_request_template* tmpl, uint64_t seed, ds_request* out, int64_t cap, int64_t* n);
 int ds_expand_workload(const ds_request* reqs, int64_t n_reqs, const ds_expand_params* params, ds_kernel_plan* out,
                        int64_t cap, int64_t* n);
+
+/* ---- peer memory for the data-parallel training tenant's all-reduce body ----
+ * (one process per GPU; handles travel over the host process group).
+ * Buffers are zero-filled.  handle = 64 opaque bytes (cudaIpcMemHandle_t). */
+int ds_ipc_alloc(int device, uint64_t bytes, void** ptr);
+int ds_ipc_free(int device, void* ptr);
+int ds_ipc_handle(void* ptr, void* handle64);
+int ds_ipc_open(int device, const void* handle64, void** ptr);
+int ds_ipc_close(int device, void* ptr);
 
 /* ---- workload-aware placement across GPUs (config 5) ----
  * Replaces first-fit pick_bind_target across devices (policies.cpp:74-94) for

@@ -28,6 +28,9 @@ BODY_RMSNORM = 8
 BODY_EMBED = 9
 BODY_ARGMAX = 10
 BODY_SPLITK_REDUCE = 11
+BODY_ALLREDUCE_P2P = 12
+MAX_DP_RANKS = 8
+DP_SLOTS = 64
 
 LATENCY_CRITICAL, BEST_EFFORT = 0, 1
 PREFILL, DECODE, TRAINING, OTHER = 0, 1, 2, 3
@@ -296,6 +299,13 @@ class KernelPlan(ctypes.Structure):
 REQ_INFERENCE, REQ_TRAINING = 0, 1
 
 
+class AllreduceArgs(ctypes.Structure):
+    """csrc/bodies/collective.cuh"""
+    _fields_ = [("grad", ctypes.c_uint64 * 8), ("flags", ctypes.c_uint64 * 8), ("out", ctypes.c_uint64),
+                ("n", ctypes.c_int64), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("chunk", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
 class TenantDemand(ctypes.Structure):
     _fields_ = [("priority", ctypes.c_int32), ("phase", ctypes.c_int32), ("hbm_frac", ctypes.c_double),
                 ("tensor_frac", ctypes.c_double), ("mem_gb", ctypes.c_double)]
@@ -313,6 +323,7 @@ EXPORTS = [
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
     "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",
+    "ds_ipc_alloc", "ds_ipc_free", "ds_ipc_handle", "ds_ipc_open", "ds_ipc_close",
 ]
 
 _lib = None
@@ -394,6 +405,11 @@ def lib():
         L.ds_gen_burst.argtypes = [ctypes.c_double] * 5 + [ctypes.POINTER(RequestTemplate), ctypes.c_uint64,
                                                            ctypes.POINTER(Request), ctypes.c_int64,
                                                            ctypes.POINTER(ctypes.c_int64)]
+        L.ds_ipc_alloc.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(vp)]
+        L.ds_ipc_free.argtypes = [ctypes.c_int, vp]
+        L.ds_ipc_handle.argtypes = [vp, ctypes.c_char_p]
+        L.ds_ipc_open.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.ds_ipc_close.argtypes = [ctypes.c_int, vp]
         L.ds_place_tenants.argtypes = [ctypes.POINTER(TenantDemand), ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                        ctypes.POINTER(ctypes.c_int32)]
         L.ds_expand_workload.argtypes = [ctypes.POINTER(Request), ctypes.c_int64, ctypes.POINTER(ExpandParams),

@@ -24,6 +24,7 @@
 #include "bodies/sgemm.cuh"
 #include "bodies/gemm_tc.cuh"
 #include "bodies/decode.cuh"
+#include "bodies/collective.cuh"
 #include "ds_device.cuh"
 
 namespace ds {
@@ -53,6 +54,7 @@ __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
         case DS_BODY_EMBED: body_embed(c); break;
         case DS_BODY_ARGMAX: body_argmax(c); break;
         case DS_BODY_SPLITK_REDUCE: body_splitk_reduce(c); break;
+        case DS_BODY_ALLREDUCE_P2P: body_allreduce_p2p(c); break;
         default: break;
     }
 }
@@ -678,6 +680,7 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_EMBED: return 1024;
         case DS_BODY_ARGMAX: return 1024;
         case DS_BODY_SPLITK_REDUCE: return 1024;
+        case DS_BODY_ALLREDUCE_P2P: return 1024;
         default: return ds::kDefaultSmem;
     }
 }

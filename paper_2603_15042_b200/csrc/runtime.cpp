@@ -1077,3 +1077,48 @@ int ds_solo_launch_registered(ds_domain* d, int kernel_id, void* stream) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Peer memory for the DP all-reduce body (bodies/collective.cuh)
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int ds_ipc_alloc(int device, uint64_t bytes, void** ptr) {
+    if (!ptr || bytes == 0) return fail(DS_INVALID_ARGUMENT, "null / empty");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(DS_NO_DEVICE, "bad device ordinal");
+    if (cudaMalloc(ptr, bytes) != cudaSuccess) return fail(DS_CUDA_ERROR, "cudaMalloc");
+    if (cudaMemset(*ptr, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+        return fail(DS_CUDA_ERROR, "cudaMemset");
+    return DS_OK;
+}
+
+int ds_ipc_free(int device, void* ptr) {
+    if (cudaSetDevice(device) != cudaSuccess) return fail(DS_NO_DEVICE, "bad device ordinal");
+    return cudaFree(ptr) == cudaSuccess ? DS_OK : fail(DS_CUDA_ERROR, "cudaFree");
+}
+
+int ds_ipc_handle(void* ptr, void* handle64) {
+    if (!ptr || !handle64) return fail(DS_INVALID_ARGUMENT, "null");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, ptr) != cudaSuccess) return fail(DS_CUDA_ERROR, "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
+    std::memcpy(handle64, &h, 64);
+    return DS_OK;
+}
+
+int ds_ipc_open(int device, const void* handle64, void** ptr) {
+    if (!ptr || !handle64) return fail(DS_INVALID_ARGUMENT, "null");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(DS_NO_DEVICE, "bad device ordinal");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    if (cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return fail(DS_CUDA_ERROR, "cudaIpcOpenMemHandle");
+    return DS_OK;
+}
+
+int ds_ipc_close(int device, void* ptr) {
+    if (cudaSetDevice(device) != cudaSuccess) return fail(DS_NO_DEVICE, "bad device ordinal");
+    return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? DS_OK : fail(DS_CUDA_ERROR, "cudaIpcCloseMemHandle");
+}
+
+}  // extern "C"

@@ -94,3 +94,47 @@ def test_ranks_agree_and_partition():
         assert pr.exitcode == 0
     assert allp[0][0] == allp[1][0]
     assert sorted(allp[0][1] + allp[1][1]) == list(range(16))
+
+
+def test_dp_peer_table_orders_by_rank():
+    """Host side of the DP all-reduce: rank-ordered pointer table, own buffer
+    local, every peer opened from its handle exactly once."""
+    from paper_2603_15042_b200 import dp
+    opened = []
+    t = dp.peer_table(111, 1, [b"a", b"b", b"c"], lambda h: opened.append(h) or len(opened) * 1000)
+    assert t == [1000, 111, 2000] and opened == [b"a", b"c"]
+
+
+def _dp_worker(rank, world, port, q):
+    """Handles exchanged over a gloo group land rank-ordered on every rank."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_15042_b200 import dp
+
+    def gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    hs = gather(bytes([rank]) * 64)
+    table = dp.peer_table(10 + rank, rank, hs, lambda h: 100 + h[0])
+    res = [None] * world
+    dist.all_gather_object(res, table)
+    if rank == 0:
+        q.put(res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dp_handle_exchange_two_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res == [[10, 101], [100, 11]]
