@@ -549,6 +549,157 @@ def gpu_arm(args, rank, world):
     return out, solo
 
 
+def config5_leg(args, rank, world, dev, gather_fn):
+    """Config 5: the 16-tenant mix (8 decode + 8 training) partitioned over
+    the ranks by the native workload-aware placement, plus one data-parallel
+    training tenant spanning every rank (GEMM 4096^3 -> gradient all-reduce
+    body over peer memory).  Each rank runs its tenants under TPOT-First for
+    a fixed window; returns this rank's throughputs and TPOT samples."""
+    import torch
+    from paper_2603_15042_b200 import _abi, dp
+    from paper_2603_15042_b200.placement import config5_mix, place
+    from paper_2603_15042_b200.runtime import Domain, Engine
+    from paper_2603_15042_b200.tenants import DecodeConfig, DecodeModel, TrainGemm
+    mix = config5_mix()
+    where = place(mix, world, mem_cap_gb=150.0)
+    mine = [mix[i] for i, d in enumerate(where) if d == rank]
+    dec = [(spec, DecodeModel(DecodeConfig(L=args.kv_len, layers=spec.size), device=f"cuda:{dev}", seed=i))
+           for i, spec in enumerate(mine) if spec.kind == "decode"]
+    trn = [(spec, TrainGemm(M=spec.size, N=spec.size, K=spec.size, device=f"cuda:{dev}", seed=i))
+           for i, spec in enumerate(mine) if spec.kind == "train"]
+    dpg = dp.DpGroup(dev, 4096 * 4096, rank, world, gather_fn)
+    dp_gemm = TrainGemm(M=4096, N=4096, K=4096, device=f"cuda:{dev}", seed=99)
+    dp_gemm.args = _abi.gemm_args(dp_gemm.A.data_ptr(), dp_gemm.B.data_ptr(), dpg.grad, 4096, 4096, 4096)
+    torch.cuda.synchronize()
+    tiers = [Fraction(1, 16)] * 8 + [Fraction(1, 8)] * 4 + [Fraction(1, 4)] * 2 + [Fraction(1, 2), Fraction(1)]
+    dom = Domain(dev, tiers=tiers, block_log_capacity=0, lend_idle_sms=True)
+    td = [(dom.tenant(sp.name, _abi.LATENCY_CRITICAL), m.register(dom), m) for sp, m in dec]
+    tt = [(dom.tenant(sp.name, _abi.BEST_EFFORT), [g.register(dom)], g) for sp, g in trn]
+    t_dp = dom.tenant("dp_train", _abi.BEST_EFFORT)
+    dp_kernels = [dom.kernel("train/dp_gemm", _abi.BODY_GEMM_BF16, dp_gemm.grid, dp_gemm.args, phase=_abi.TRAINING),
+                  dpg.register(dom)]
+    dom.start()
+    eng = Engine(dom, policy="tpot-first", lend_tenant=tt[0][0] if tt else t_dp, fair_handover=True)
+    jobs_d = [(eng.add_job(t, _abi.LATENCY_CRITICAL), ks, m) for t, ks, m in td]
+    jobs_t = [(eng.add_job(t, _abi.BEST_EFFORT), ks, g.flops) for t, ks, g in tt]
+    j_dp = eng.add_job(t_dp, _abi.BEST_EFFORT)
+    jobs_t.append((j_dp, dp_kernels, dp_gemm.flops))
+    # every rank runs the same number of DP iterations (the all-reduce is a
+    # rendezvous: an extra iteration on one rank would wait for its peers)
+    dp_submitted = [0]
+    dom.set_lend(tt[0][0] if tt else t_dp)
+    eng.start()
+    T = 4
+    step_hint = 2_000_000
+    live_d = {j: None for j, _, _ in jobs_d}
+    live_t = {j: [] for j, _, _ in jobs_t}
+    done_reqs, train_done = [], []
+    t_end = time.time() + args.c5_seconds
+    req_id = 0
+    last_log = time.time()
+    while time.time() < t_end:
+        if time.time() - last_log > 1.0:
+            last_log = time.time()
+            log(f"config 5 rank {rank}: {len(done_reqs)} requests, {len(train_done)} train iters, dp "
+                f"{dp_submitted[0]}", eng.counters())
+        for j, ks, m in jobs_d:
+            cur = live_d[j]
+            if cur is None or eng.record(cur[-1]).state == 2:
+                if cur is not None:
+                    done_reqs.append((j, cur))
+                live_d[j] = [eng.submit(j, ks, "decode/step", _abi.DECODE, grid_size=len(ks), request=req_id,
+                                        decode_index=k, tpot_ns=50_000_000, ttft_ns=200_000_000,
+                                        base_hint_ns=step_hint, saturation=Fraction(1, 2)) for k in range(T)]
+                req_id += 1
+        for j, ks, fl in jobs_t:
+            out = [r for r in live_t[j] if eng.record(r).state != 2]
+            train_done += [(r, fl) for r in live_t[j] if r not in out]
+            while len(out) < 2 and (j != j_dp or dp_submitted[0] < args.c5_dp_iters):
+                dp_submitted[0] += j == j_dp
+                out.append(eng.submit(j, ks, "train/iter", _abi.TRAINING, grid_size=len(ks), base_hint_ns=step_hint,
+                                      saturation=Fraction(1, 4)))
+            live_t[j] = out
+        time.sleep(0.0005)
+    # drain: decode requests in flight, then the rest of the DP program (other
+    # trainers stop submitting, so every tenant gets SMs), then the trainers;
+    # bounded so a starved tenant cannot hang the bench
+    deadline = time.time() + args.c5_drain_s
+    log(f"config 5 rank {rank}: window over, draining (dp {dp_submitted[0]}/{args.c5_dp_iters})")
+
+    def settle(r):
+        while eng.record(r).state != 2:
+            if time.time() > deadline:
+                return False
+            time.sleep(0.0005)
+        return True
+
+    incomplete = 0
+    for j, cur in live_d.items():
+        if cur is not None:
+            if settle(cur[-1]):
+                done_reqs.append((j, cur))
+            else:
+                incomplete += 1
+    while dp_submitted[0] < args.c5_dp_iters and time.time() < deadline:
+        out = [r for r in live_t[j_dp] if eng.record(r).state != 2]
+        train_done += [(r, dp_gemm.flops) for r in live_t[j_dp] if r not in out]
+        if len(out) < 2:
+            out.append(eng.submit(j_dp, dp_kernels, "train/iter", _abi.TRAINING, grid_size=2, base_hint_ns=step_hint,
+                                  saturation=Fraction(1, 4)))
+            dp_submitted[0] += 1
+        live_t[j_dp] = out
+        time.sleep(0.0005)
+    for j, rs in live_t.items():
+        fl = next(f for jj, _, f in jobs_t if jj == j)
+        for r in rs:
+            if settle(r):
+                train_done.append((r, fl))
+            else:
+                incomplete += 1
+    if incomplete:
+        log(f"config 5 rank {rank}: {incomplete} records incomplete at the drain deadline", eng.counters())
+    tpots, tokens, t0, t1 = [], 0, None, None
+    for j, recs in done_reqs:
+        inf = [eng.record(r) for r in recs]
+        tpots.append((inf[-1].t_end - inf[0].t_end) / (T - 1) / 1e6)
+        tokens += T * 32  # batch 32 sequences per step
+        t0 = inf[0].t_first_claim if t0 is None else min(t0, inf[0].t_first_claim)
+        t1 = inf[-1].t_end if t1 is None else max(t1, inf[-1].t_end)
+    flop = sum(fl for _, fl in train_done)
+    for r, _ in train_done:
+        i = eng.record(r)
+        t0 = i.t_first_claim if t0 is None else min(t0, i.t_first_claim)
+        t1 = i.t_end if t1 is None else max(t1, i.t_end)
+    counters = eng.counters()
+    if incomplete:
+        dpg.abort()  # a starved DP iteration must not keep peers' blocks waiting
+    eng.stop()
+    eng.close()
+    dom.stop()
+    dom.close()
+    win = (t1 - t0) * 1e-9 if t0 is not None else 1.0
+    counters["incomplete_records"] = incomplete
+    return {"rank": rank, "tenants": [s.name for s in mine] + ["dp_train"], "tpot_ms": tpots,
+            "decode_tokens_per_s": tokens / win, "train_tflops": flop / win / 1e12, "window_s": win,
+            "train_iters": len(train_done), "requests": len(done_reqs), "dp_iters": dp_submitted[0],
+            "engine_counters": counters}
+
+
+def aggregate_config5(parts):
+    tp = [x for p in parts for x in p["tpot_ms"]]
+    return {"workload": "config 5: 16 synthetic tenants (8 Llama-3-8B-shaped decode, 2-8 layers, batch 32, KV "
+                        "1024; 8 bf16 GEMM trainers 2048^3-8192^3) placed over the GPUs by ds_place_tenants, plus "
+                        "one data-parallel GEMM 4096^3 tenant with the peer-memory gradient all-reduce body; "
+                        "TPOT-First per GPU",
+            "n_gpus": len(parts), "placement": {p["rank"]: p["tenants"] for p in parts},
+            "decode_tokens_per_s": round(sum(p["decode_tokens_per_s"] for p in parts), 1),
+            "train_tflops": round(sum(p["train_tflops"] for p in parts), 1),
+            "p99_tpot_ms": round(nearest_rank(tp, 99), 3) if tp else None,
+            "requests": sum(p["requests"] for p in parts), "train_iters": sum(p["train_iters"] for p in parts),
+            "dp_iters_submitted": [p["dp_iters"] for p in parts],
+            "incomplete_records": sum(p["engine_counters"].get("incomplete_records", 0) for p in parts)}
+
+
 def aggregate_ranks(vals):
     """Whole-job line from per-rank lines (independent domains, weak scaling):
     latency metrics take the worst rank, throughputs sum, timing is the max
@@ -587,6 +738,11 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--decode-sat", default="1/2", help="decode compute saturation (tier wanted)")
     ap.add_argument("--slo-x", type=float, default=8.0, help="TPOT SLO as a multiple of the solo step")
+    ap.add_argument("--no-config5", action="store_true", help="skip the config 5 (16-tenant placement) leg")
+    ap.add_argument("--c5-seconds", type=float, default=3.0, help="config 5 run window per rank")
+    ap.add_argument("--c5-dp-iters", type=int, default=40, help="config 5 data-parallel tenant iterations")
+    ap.add_argument("--c5-drain-s", type=float, default=30.0, help="config 5 drain deadline")
+    ap.add_argument("--only-config5", action="store_true", help="run the config 5 leg alone (debug)")
     ap.add_argument("--no-config4", action="store_true", help="skip the config 4 (ResNet + bursty decode) leg")
     ap.add_argument("--burst-units", type=float, default=60.0, help="config 4 trace duration (units of 50 ms)")
     ap.add_argument("--tiers", default="1/4,1/2,3/4,1", help="pctx pool tiers (create_pool; SPEC.md:65 pool)")
@@ -622,11 +778,32 @@ def main():
             line = {"impl": "reference", "unavailable": f"reference simulator not built: {e}"}
         print(json.dumps(line))
         return
-    out, solo = gpu_arm(args, rank, world)
-    if world > 1:
+    if args.only_config5:
+        out, solo = {}, None
+    else:
+        out, solo = gpu_arm(args, rank, world)
+    if world > 1 and not args.only_config5:
         out = gather_ranks(out, world)
+    if not args.no_config5:
+        import torch
+        torch.cuda.empty_cache()
+        dev = int(os.environ.get("LOCAL_RANK", rank))
+
+        def gather(obj):
+            if world == 1:
+                return [obj]
+            import torch.distributed as dist
+            res = [None] * world
+            dist.all_gather_object(res, obj)
+            return res
+
+        log("config 5 leg")
+        part = config5_leg(args, rank, world, dev, gather)
+        c5 = aggregate_config5(gather(part))
+        if rank == 0:
+            out["config5"] = c5
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and solo is not None:
             try:
                 out["cpu_baseline"] = cpu_baseline_leg(solo, args.steps, args.tokens)
             except Exception as e:

@@ -355,6 +355,8 @@ int ds_ipc_free(int device, void* ptr);
 int ds_ipc_handle(void* ptr, void* handle64);
 int ds_ipc_open(int device, const void* handle64, void** ptr);
 int ds_ipc_close(int device, void* ptr);
+/* release this rank's all-reduce blocks still waiting on peers (shutdown) */
+int ds_dp_abort(int device, void* flags);
 
 /* ---- workload-aware placement across GPUs (config 5) ----
  * Replaces first-fit pick_bind_target across devices (policies.cpp:74-94) for

@@ -323,7 +323,7 @@ EXPORTS = [
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
     "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",
-    "ds_ipc_alloc", "ds_ipc_free", "ds_ipc_handle", "ds_ipc_open", "ds_ipc_close",
+    "ds_ipc_alloc", "ds_ipc_free", "ds_ipc_handle", "ds_ipc_open", "ds_ipc_close", "ds_dp_abort",
 ]
 
 _lib = None
@@ -410,6 +410,7 @@ def lib():
         L.ds_ipc_handle.argtypes = [vp, ctypes.c_char_p]
         L.ds_ipc_open.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.ds_ipc_close.argtypes = [ctypes.c_int, vp]
+        L.ds_dp_abort.argtypes = [ctypes.c_int, vp]
         L.ds_place_tenants.argtypes = [ctypes.POINTER(TenantDemand), ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                        ctypes.POINTER(ctypes.c_int32)]
         L.ds_expand_workload.argtypes = [ctypes.POINTER(Request), ctypes.c_int64, ctypes.POINTER(ExpandParams),

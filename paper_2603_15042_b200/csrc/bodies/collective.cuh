@@ -23,6 +23,11 @@ namespace ds {
 
 constexpr int kMaxDpRanks = 8;
 constexpr int kDpSlots = 64;
+// flags of a rank: u64 ready[kDpSlots], done[kDpSlots], abort.  The host sets
+// its own rank's abort word (ds_dp_abort) to release blocks still waiting for
+// a peer that will never come (shutdown with a starved rank); results of an
+// aborted launch are undefined, nothing hangs.
+constexpr int kDpAbortWord = 2 * kDpSlots;
 
 struct AllreduceArgs {
     uint64_t grad[kMaxDpRanks];   // bf16 [n] of rank p (peer-mapped pointers; own rank = local)
@@ -53,7 +58,10 @@ __device__ void body_allreduce_p2p(const BodyCtx& c) {
         st_release_sys_u64(ready, epoch);
         for (int p = 0; p < a.world; ++p) {
             const void* pr = reinterpret_cast<const unsigned long long*>(a.flags[p]) + slot;
-            while (ld_acquire_sys_u64_(pr) != epoch) __nanosleep(128);
+            while (ld_acquire_sys_u64_(pr) != epoch) {
+                if (ld_volatile_u64(reinterpret_cast<const unsigned long long*>(a.flags[a.rank]) + kDpAbortWord)) break;
+                __nanosleep(128);
+            }
         }
     }
     body_sync();
@@ -99,7 +107,11 @@ __device__ void body_allreduce_p2p(const BodyCtx& c) {
             const unsigned long long want = ((unsigned long long)epoch << 32) | (unsigned long long)G;
             for (int p = 0; p < a.world; ++p) {
                 const void* pd = reinterpret_cast<const unsigned long long*>(a.flags[p]) + kDpSlots + slot;
-                while (ld_acquire_sys_u64_(pd) != want) __nanosleep(256);
+                while (ld_acquire_sys_u64_(pd) != want) {
+                    if (ld_volatile_u64(reinterpret_cast<const unsigned long long*>(a.flags[a.rank]) + kDpAbortWord))
+                        break;
+                    __nanosleep(256);
+                }
             }
         }
     }

@@ -73,6 +73,12 @@ struct ds_engine {
     std::vector<Rec> recs;  // by id
     std::vector<int> pctx_bound;  // pctx -> job (-1)
     std::vector<Frac> pctx_tier;
+    // a preempted pctx is unavailable while its SMs drain and the context
+    // switches (on_preempt_boundary: unavailable for preempt_overhead,
+    // engine.cpp:925-984); without it a best-effort victim rebinds the pctx in
+    // the same pump and the launcher preempts it again, forever
+    std::vector<Time> pctx_unavail_until;
+    Time preempt_hold_ns = 200000;
     std::mutex mu;
     std::thread th;
     std::atomic<bool> stop{false};
@@ -124,6 +130,7 @@ struct ds_engine {
             PolicyView::PctxEntry e;
             e.id = (int)p;
             e.tier = pctx_tier[p];
+            e.available = pctx_unavail_until[p] <= v.now;
             if (pctx_bound[p] >= 0) {
                 e.bound = pctx_bound[p];
                 const Job& j = jobs[pctx_bound[p]];
@@ -226,6 +233,7 @@ struct ds_engine {
             case K::DispatchRemap: {
                 if (d.target < 0 || d.target >= (int)pctx_tier.size()) return fail();
                 if (pctx_bound[d.target] >= 0) return fail();
+                if (pctx_unavail_until[d.target] > now()) return fail();
                 Frac sum{0, 1};
                 for (size_t p = 0; p < pctx_tier.size(); ++p)
                     if (pctx_bound[p] >= 0) sum = sum + pctx_tier[p];
@@ -241,12 +249,18 @@ struct ds_engine {
                 if (victim == ji) return fail();      // self-preemption
                 ds_preempt(dom, d.target);
                 pctx_bound[d.target] = -1;
+                hold(d.target);
                 if (jobs[victim].running >= 0) recs[jobs[victim].running].preempted++;
                 ctr.preemptions++;
                 return kDeferPolicy;
             }
         }
         return kDeferPolicy;
+    }
+
+    void hold(int p) {
+        pctx_unavail_until[p] = now() + preempt_hold_ns;
+        if (next_review < 0 || pctx_unavail_until[p] < next_review) next_review = pctx_unavail_until[p];
     }
 
     bool pool_exhausted() const {
@@ -269,6 +283,7 @@ struct ds_engine {
             if (holder >= 0 && holder != *owner && launchable_or_pending(*owner)) {
                 ds_preempt(dom, (int)p);
                 pctx_bound[p] = -1;
+                hold((int)p);
                 if (jobs[holder].running >= 0) recs[jobs[holder].running].preempted++;
                 ctr.preemptions++;
             }
@@ -412,6 +427,7 @@ int ds_engine_create(ds_domain* dom, const ds_engine_config* cfg, ds_engine** ou
         ds_pctx_info(dom, p, &num, &den, &nsm, &bound);
         e->pctx_tier.push_back(Frac{num, den});
         e->pctx_bound.push_back(-1);
+        e->pctx_unavail_until.push_back(0);
         if (num == den) has_full = true;
     }
     if (e->pcfg.name == "temporal" && !has_full) {  // engine.cpp:193-202

@@ -308,12 +308,14 @@ int ds_domain_create(const ds_domain_config* cfg, ds_domain** out) {
     d->owner.assign(d->num_sms, -1);
     d->lender.assign(d->num_sms, -1);
 
-    // pool (create_pool): one pctx per tier; SM count = round(tier * num_sms), >= 1
+    // pool (create_pool): one pctx per tier; SM count = floor(tier * num_sms),
+    // >= 1, so every set of pctxs the policy may bind together (sum of tiers
+    // <= 1, engine.cpp:721-725) also fits in the SMs (rounding up could not)
     for (int i = 0; i < cfg->n_tiers; ++i) {
         Pctx p;
         p.num = cfg->tier_num[i];
         p.den = cfg->tier_den[i];
-        p.n_sms = (int)((p.num * d->num_sms * 2 + p.den) / (2 * p.den));
+        p.n_sms = (int)(p.num * d->num_sms / p.den);
         if (p.n_sms < 1) p.n_sms = 1;
         if (p.n_sms > d->num_sms) p.n_sms = d->num_sms;
         d->pctxs.push_back(p);
@@ -1113,6 +1115,16 @@ int ds_ipc_open(int device, const void* handle64, void** ptr) {
     std::memcpy(&h, handle64, 64);
     if (cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
         return fail(DS_CUDA_ERROR, "cudaIpcOpenMemHandle");
+    return DS_OK;
+}
+
+int ds_dp_abort(int device, void* flags) {
+    if (!flags) return fail(DS_INVALID_ARGUMENT, "null");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(DS_NO_DEVICE, "bad device ordinal");
+    const unsigned long long one = 1;
+    // a copy-engine write: works while the resident executor holds every SM
+    if (cudaMemcpy(static_cast<unsigned long long*>(flags) + 2 * 64, &one, 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(DS_CUDA_ERROR, "cudaMemcpy");
     return DS_OK;
 }
 

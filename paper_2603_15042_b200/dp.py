@@ -18,7 +18,7 @@ from typing import Callable, List, Sequence
 from . import _abi
 from ._abi import check, lib
 
-FLAG_BYTES = 2 * _abi.DP_SLOTS * 8
+FLAG_BYTES = (2 * _abi.DP_SLOTS + 1) * 8  # ready, done, abort
 
 
 def _alloc(device: int, nbytes: int) -> int:
@@ -74,6 +74,10 @@ class DpGroup:
         self.grads = peer_table(self.grad, rank, [h[0] for h in hs], opener)
         self.flag_ptrs = peer_table(self.flags, rank, [h[1] for h in hs], opener)
         self.args = make_args(self.grads, self.flag_ptrs, self.out, n, rank, chunk)
+
+    def abort(self):
+        """Release this rank's blocks still waiting for a peer (shutdown)."""
+        check(lib().ds_dp_abort(self.device, ctypes.c_void_p(self.flags)))
 
     def register(self, dom, semantic_id="train/dp_allreduce") -> int:
         return dom.kernel(semantic_id, _abi.BODY_ALLREDUCE_P2P, grid_for(self.n, self.chunk), self.args,
