@@ -250,6 +250,9 @@ typedef struct ds_engine_config {
     int n_assignments;         /* static partition map */
     int32_t assign_vctx[64];
     int32_t assign_pctx[64];
+    int hang_detection;        /* EngineConfig.hang_detection (engine.hpp:63) */
+    double hang_threshold;     /* EngineConfig.hang_threshold (default 3) */
+    int capture_log;           /* EngineConfig.capture_log: JSONL event log */
 } ds_engine_config;
 
 typedef struct ds_record_desc {
@@ -295,6 +298,10 @@ int ds_engine_counters_get(ds_engine* eng, ds_engine_counters* out);
 int ds_engine_transcript(ds_engine* eng, int job, uint64_t* rec_ids, int cap, int* n);
 int ds_engine_predict(ds_engine* eng, const char* semantic_id, int64_t grid, int64_t* ns);
 int ds_policy_names(char* out, int cap);
+/* JSONL event log {"t","seq","kind",...} (engine.cpp:316-329); *len = full length */
+int ds_engine_event_log(ds_engine* eng, char* out, int64_t cap, int64_t* len);
+/* quarantined vctxs (SimulationReport.quarantines, engine.hpp:136) */
+int ds_engine_quarantines(ds_engine* eng, int32_t* jobs, int64_t* t_ns, int cap, int* n);
 
 
 /* ---- request streams and workload expansion ----

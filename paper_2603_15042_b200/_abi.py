@@ -249,7 +249,8 @@ class EngineConfig(ctypes.Structure):
     _fields_ = [("policy", ctypes.c_char_p), ("quantum_ns", ctypes.c_int64), ("alpha", ctypes.c_double),
                 ("cold_start_ns", ctypes.c_int64), ("release_on_idle", ctypes.c_int), ("fair_handover", ctypes.c_int),
                 ("lend_tenant", ctypes.c_int), ("n_assignments", ctypes.c_int), ("assign_vctx", ctypes.c_int32 * 64),
-                ("assign_pctx", ctypes.c_int32 * 64)]
+                ("assign_pctx", ctypes.c_int32 * 64), ("hang_detection", ctypes.c_int), ("hang_threshold", ctypes.c_double),
+                ("capture_log", ctypes.c_int)]
 
 
 class RecordDesc(ctypes.Structure):
@@ -324,6 +325,7 @@ EXPORTS = [
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
     "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",
     "ds_ipc_alloc", "ds_ipc_free", "ds_ipc_handle", "ds_ipc_open", "ds_ipc_close", "ds_dp_abort",
+    "ds_engine_event_log", "ds_engine_quarantines",
 ]
 
 _lib = None
@@ -410,6 +412,9 @@ def lib():
         L.ds_ipc_handle.argtypes = [vp, ctypes.c_char_p]
         L.ds_ipc_open.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.ds_ipc_close.argtypes = [ctypes.c_int, vp]
+        L.ds_engine_event_log.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_engine_quarantines.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
+                                            ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         L.ds_dp_abort.argtypes = [ctypes.c_int, vp]
         L.ds_place_tenants.argtypes = [ctypes.POINTER(TenantDemand), ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                        ctypes.POINTER(ctypes.c_int32)]

@@ -48,6 +48,8 @@ struct ds_engine {
         uint64_t t_first_claim = 0, t_end = 0;
         int pctx = -1;
         int preempted = 0;
+        Time hang_needed = 0;  // arm_hang_check (engine.cpp:542-561): threshold x prediction
+        bool hang_armed = false;
     };
     struct Job {
         int tenant = -1;
@@ -87,7 +89,31 @@ struct ds_engine {
     Time last_review = -1;
     Time next_review = -1;
     ds_engine_counters ctr{};
+    // fault containment (engine.cpp:542-561, 1011-1035) and the JSONL event
+    // log (engine.cpp:316-329, 1343-1352)
+    bool hang_detection = false;
+    double hang_threshold = 3.0;
+    bool capture_log = false;
+    uint64_t log_seq = 0;
+    std::vector<std::string> event_log;
+    struct Quarantine {
+        int job;
+        Frac tier;
+        Time t;
+    };
+    std::vector<Quarantine> quarantines;
     ds_engine() : predictor(0.3, 1000000000) {}
+
+    // {"t","seq","kind",...} as the reference's log_event; t in engine ns
+    void log(Time t, const char* kind, const std::string& fields) {
+        if (!capture_log) return;
+        std::string line = "{\"t\":\"" + std::to_string(t) + "\",\"seq\":" + std::to_string(log_seq++) +
+                           ",\"kind\":\"" + kind + "\"";
+        if (!fields.empty()) line += "," + fields;
+        line += "}";
+        event_log.push_back(std::move(line));
+    }
+    static std::string kv(const char* k, long long v) { return std::string("\"") + k + "\":" + std::to_string(v); }
 
     Time now() const {
         return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
@@ -184,6 +210,7 @@ struct ds_engine {
         if (src >= 0) pctx_bound[src] = -1;
         pctx_bound[p] = ji;
         ctr.migrations++;
+        log(now(), "MigrationDone", kv("vctx", ji) + "," + kv("pctx", p) + "," + kv("from", src));
         return 0;
     }
     void do_unbind(int ji) {
@@ -195,7 +222,13 @@ struct ds_engine {
     }
     void dispatch(int ji) {
         Job& j = jobs[ji];
-        if (j.running >= 0) return;  // paused record resumes in place
+        if (j.running >= 0) {  // paused record resumes in place on its new binding
+            Rec& pr = recs[j.running];
+            pr.pctx = bound_pctx(ji);
+            log(now(), "KernelStart", kv("vctx", ji) + "," + kv("pctx", pr.pctx) + "," +
+                                          kv("kernel_id", (long long)pr.r.id) + ",\"resume\":true");
+            return;
+        }
         uint64_t id = j.pending.front();
         j.pending.pop_front();
         Rec& r = recs[id];
@@ -210,6 +243,13 @@ struct ds_engine {
         r.pctx = bound_pctx(ji);
         j.running = (int64_t)id;
         ctr.dispatches++;
+        if (hang_detection && !j.quarantined) {
+            r.hang_needed = (Time)(hang_threshold * (double)predictor.predict(r.r.signature, r.r.base_duration));
+            r.hang_armed = true;
+        }
+        log(r.dispatch_host, "KernelStart",
+            kv("vctx", ji) + "," + kv("pctx", r.pctx) + "," + kv("kernel_id", (long long)id) + "," +
+                kv("grid", r.r.signature.grid_size));
     }
 
     enum Outcome { kDirect, kRemap, kDeferPolicy, kDeferError };
@@ -250,6 +290,7 @@ struct ds_engine {
                 ds_preempt(dom, d.target);
                 pctx_bound[d.target] = -1;
                 hold(d.target);
+                log(now(), "PreemptSignal", kv("vctx", victim) + "," + kv("pctx", d.target) + "," + kv("by", ji));
                 if (jobs[victim].running >= 0) recs[jobs[victim].running].preempted++;
                 ctr.preemptions++;
                 return kDeferPolicy;
@@ -350,6 +391,9 @@ struct ds_engine {
         j.has_last_finish = true;
         if (r.t_end > r.t_first_claim) predictor.observe(r.r.signature, (Time)(r.t_end - r.t_first_claim));
         ctr.completed++;
+        log(r.finish_host, "KernelFinish",
+            kv("vctx", ji) + "," + kv("pctx", r.pctx) + "," + kv("kernel_id", (long long)r.r.id) + "," +
+                kv("device_ns", (long long)(r.t_end - r.t_first_claim)));
         {
             PolicyView v = build_view();
             PolicyDecision d = policy->on_completion(v, launch_context(ji));
@@ -358,6 +402,35 @@ struct ds_engine {
         if (release_on_idle) {
             bool next_ready = !j.pending.empty() && recs[j.pending.front()].r.arrival <= now();
             if (!next_ready) do_unbind(ji);
+        }
+    }
+
+    // on_hang_check (engine.cpp:1011-1035): a record running longer than
+    // threshold x its prediction marks its vctx quarantined — its SMs yield at
+    // the next logical-block boundary and it may only bind the pool's minimum
+    // tier from then on (eligible_bind) — so a soft-hung tenant is confined to
+    // the smallest SM set instead of holding its quota
+    void hang_check(Time t) {
+        for (size_t ji = 0; ji < jobs.size(); ++ji) {
+            Job& j = jobs[ji];
+            if (j.quarantined || j.running < 0) continue;
+            Rec& r = recs[j.running];
+            if (!r.hang_armed || t - r.dispatch_host < r.hang_needed) continue;
+            Frac mn{2, 1};
+            for (const auto& f : pctx_tier)
+                if (f < mn) mn = f;
+            j.quarantined = true;
+            quarantines.push_back({(int)ji, mn, t});
+            log(t, "HangCheck", kv("vctx", (long long)ji) + "," + kv("pctx", bound_pctx((int)ji)) +
+                                    ",\"flagged\":true," + kv("elapsed", t - r.dispatch_host));
+            int p = bound_pctx((int)ji);
+            if (p >= 0 && pctx_tier[p] != mn) {
+                ds_preempt(dom, p);
+                pctx_bound[p] = -1;
+                hold(p);
+                r.preempted++;
+                ctr.preemptions++;
+            }
         }
     }
 
@@ -384,6 +457,7 @@ struct ds_engine {
                     work = true;
                 }
                 Time t = now();
+                if (hang_detection) hang_check(t);
                 bool review = next_review >= 0 && t >= next_review;
                 if (review) next_review = -1;
                 bool arrivals = false;
@@ -416,6 +490,9 @@ int ds_engine_create(ds_domain* dom, const ds_engine_config* cfg, ds_engine** ou
         return efail(DS_CONFIG_ERROR, ex.what());
     }
     e->release_on_idle = cfg->release_on_idle;
+    e->hang_detection = cfg->hang_detection != 0;
+    if (cfg->hang_threshold > 0) e->hang_threshold = cfg->hang_threshold;
+    e->capture_log = cfg->capture_log != 0;
     e->fair_handover = cfg->fair_handover;
     e->lend_tenant = cfg->lend_tenant;
     int np = 0;
@@ -487,6 +564,7 @@ int ds_engine_submit(ds_engine* e, int job, const ds_record_desc* d, uint64_t* r
     e->recs.push_back(std::move(r));
     jb.pending.push_back(e->recs.back().r.id);
     *rec_id = e->recs.back().r.id;
+    e->log(now, "Arrival", ds_engine::kv("vctx", job) + "," + ds_engine::kv("kernel_id", (long long)*rec_id));
     return DS_OK;
 }
 
@@ -573,6 +651,32 @@ int ds_engine_predict(ds_engine* e, const char* semantic_id, int64_t grid, int64
     if (!e || !ns) return efail(DS_INVALID_ARGUMENT, "null");
     std::lock_guard<std::mutex> g(e->mu);
     *ns = e->predictor.predict(KernelSignature{semantic_id ? semantic_id : "", grid});
+    return DS_OK;
+}
+
+int ds_engine_event_log(ds_engine* e, char* out, int64_t cap, int64_t* len) {
+    if (!e || !len) return efail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(e->mu);
+    std::string s;
+    for (const auto& l : e->event_log) s += l + "\n";
+    *len = (int64_t)s.size();
+    if (out && cap > 0) {
+        int64_t m = std::min<int64_t>(cap - 1, (int64_t)s.size());
+        std::memcpy(out, s.data(), (size_t)m);
+        out[m] = 0;
+    }
+    return DS_OK;
+}
+
+int ds_engine_quarantines(ds_engine* e, int32_t* jobs, int64_t* t_ns, int cap, int* n) {
+    if (!e || !n) return efail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(e->mu);
+    int m = std::min<int>(cap, (int)e->quarantines.size());
+    for (int i = 0; i < m; ++i) {
+        if (jobs) jobs[i] = e->quarantines[i].job;
+        if (t_ns) t_ns[i] = e->quarantines[i].t;
+    }
+    *n = (int)e->quarantines.size();
     return DS_OK;
 }
 

@@ -246,8 +246,12 @@ class Engine:
 
     def __init__(self, dom: Domain, policy: str = "tpot-first", quantum_ns: int = 5_000_000, alpha: float = 0.3,
                  cold_start_ns: int = 1_000_000_000, release_on_idle: bool = True, fair_handover: bool = True,
-                 lend_tenant: int = -1, assignments=None):
+                 lend_tenant: int = -1, assignments=None, hang_detection: bool = False, hang_threshold: float = 3.0,
+                 capture_log: bool = False):
         cfg = _abi.EngineConfig()
+        cfg.hang_detection = int(hang_detection)
+        cfg.hang_threshold = hang_threshold
+        cfg.capture_log = int(capture_log)
         cfg.policy = policy.encode()
         cfg.quantum_ns = quantum_ns
         cfg.alpha = alpha
@@ -312,6 +316,23 @@ class Engine:
         c = _abi.EngineCounters()
         check_engine(lib().ds_engine_counters_get(self.h, ctypes.byref(c)))
         return {n: getattr(c, n) for n, _ in _abi.EngineCounters._fields_}
+
+    def event_log(self) -> List[dict]:
+        """The JSONL event log (reference schema, engine.cpp:316-329), parsed."""
+        import json
+        n = ctypes.c_int64()
+        check_engine(lib().ds_engine_event_log(self.h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        check_engine(lib().ds_engine_event_log(self.h, buf, n.value + 1, ctypes.byref(n)))
+        return [json.loads(x) for x in buf.value.decode().splitlines() if x]
+
+    def quarantines(self) -> List[Tuple[int, int]]:
+        n = ctypes.c_int()
+        check_engine(lib().ds_engine_quarantines(self.h, None, None, 0, ctypes.byref(n)))
+        jobs = (ctypes.c_int32 * max(1, n.value))()
+        ts = (ctypes.c_int64 * max(1, n.value))()
+        check_engine(lib().ds_engine_quarantines(self.h, jobs, ts, n.value, ctypes.byref(n)))
+        return [(jobs[i], ts[i]) for i in range(n.value)]
 
     def transcript(self, job: int) -> List[int]:
         n = ctypes.c_int()
