@@ -73,10 +73,26 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     const int warp = ltid() >> 5, lane = ltid() & 31;
     float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + rvec[32] + flag
     float* rvec = scratch + 128 * 33;
-    volatile int* flag = reinterpret_cast<volatile int*>(scratch + 128 * 33 + 32 + 16);
     const int q = warp & 3;
     const int row = q * 32 + lane;  // epilogue warps: row within the slab
     const int n = n_blk * kTcBM + row;
+    // Split-K: split S-1 of each slab is its combiner (claimed after every
+    // other split of every slab: claims follow the logical index, so it never
+    // waits on an unclaimed block).  The other splits store their partial and
+    // arrive (fire-and-forget release); the combiner waits for S-1 arrivals and
+    // sums s = 0..S-1 in order.
+    const bool combiner = a.S == 1 || s == a.S - 1;
+    // RMSNorm scale of the input rows (statistics of an earlier launch): load
+    // it now, its latency hides under the partial exchange
+    if (combiner && a.stats_in && warp >= 4) {
+        float* red = scratch + 128 * 33 + 64;  // [4][32]
+        const float* st = reinterpret_cast<const float*>(a.stats_in);
+        const int p0 = q * a.P_in / 4, p1 = (q + 1) * a.P_in / 4;
+        float ss = 0.f;
+#pragma unroll 8
+        for (int p = p0; p < p1; ++p) ss += __ldcg(st + p * 32 + lane);
+        red[q * 32 + lane] = ss;
+    }
     float v[32];
     if (warp >= 4) {
         uint32_t raw[32];
@@ -85,30 +101,27 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
 #pragma unroll
         for (int b = 0; b < 32; ++b) v[b] = __uint_as_float(raw[b]);
     }
-    bool proceed = true;
+    const bool proceed = combiner;
     if (a.S > 1) {
         if (warp >= 4) {
             float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.ws) + ((size_t)s * a.N + n) * 32);
 #pragma unroll
             for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
-        body_sync();
-        if (ltid() == 0) {
-            // one release/acquire RMW publishes the whole CTA's partial (the
-            // bar.sync above orders the other threads' stores before it)
-            uint32_t tk;
-            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
-                         : "=r"(tk) : "l"(reinterpret_cast<uint32_t*>(a.counters) + n_blk) : "memory");
-            *flag = (tk == (uint32_t)a.S - 1);
-        }
-        body_sync();
-        proceed = *flag != 0;
-        if (dbg && ltid() == 0) dbg[2] = globaltimer() | ((uint64_t)proceed << 63);
-        if (proceed) {
+        body_sync();  // orders the CTA's partial stores before thread 0's release
+        uint32_t* ctr = reinterpret_cast<uint32_t*>(a.counters) + n_blk;
+        if (!combiner) {
+            if (ltid() == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        } else {
+            if (ltid() == 0) {
+                while (ld_acquire_u32(ctr) != (uint32_t)(a.S - 1)) __nanosleep(32);
+                *ctr = 0;  // at rest for the next launch (which only arrives after this one completes)
+            }
+            body_sync();
+            if (dbg && ltid() == 0) dbg[2] = globaltimer() | (1ull << 63);
             // all 256 threads, coalesced: thread owns float4 f = ltid() + 256 j
             // of the slab's [128 rows][32] block; partials summed in the fixed
             // order s = 0..S-1
-            __threadfence();
             const float4* wsb = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.ws) +
                                                                 (size_t)n_blk * kTcBM * 32);
             const size_t sstride4 = (size_t)a.N * 8;
@@ -128,6 +141,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
                     acc[j].w += x[j].w;
                 }
             }
+            body_sync();  // every thread's TMEM-side reads of the stats scratch are done
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int f = ltid() + 256 * j;
@@ -137,7 +151,6 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
                 dst[2] = acc[j].z;
                 dst[3] = acc[j].w;
             }
-            if (ltid() == 0) reinterpret_cast<uint32_t*>(a.counters)[n_blk] = 0;
             body_sync();
             if (warp >= 4) {
 #pragma unroll
@@ -149,17 +162,10 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     }
     if (warp >= 4) {
         if (proceed) {
-            // RMSNorm of the input rows folded in as a per-row scale
+            // RMSNorm of the input rows folded in as a per-row scale (sums
+            // loaded before the partial exchange)
             if (a.stats_in) {
                 float* red = scratch + 128 * 33 + 64;  // [4][32]
-                {
-                    const float* st = reinterpret_cast<const float*>(a.stats_in);
-                    const int p0 = q * a.P_in / 4, p1 = (q + 1) * a.P_in / 4;
-                    float ss = 0.f;
-#pragma unroll 8
-                    for (int p = p0; p < p1; ++p) ss += __ldcg(st + p * 32 + lane);
-                    red[q * 32 + lane] = ss;
-                }
                 epi_sync();
                 if (warp == 4) {
                     const float ss = ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];

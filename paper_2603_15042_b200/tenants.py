@@ -110,10 +110,11 @@ class DecodeModel:
             "down": pick_split(c.d // 128, c.ffn // 64),
             "lm": pick_split(c.vocab // 128, c.d // 64),
         }
-        # measured on B200 with early start (scripts/timeline.py sweep): fewer,
-        # larger K-splits than the wave-quantisation optimum win once weight
-        # streams overlap the previous kernel
-        self.S.update({"qkv": 3, "o": 3, "gu": 2, "down": 5})
+        # measured on B200 (scripts/split_sweep.py, decode step at 74 and 148
+        # SMs): every block pays ~8 us of prologue / partial exchange /
+        # epilogue around its weight stream, so the fewest splits that still
+        # fill the lanes win — no split at all for gate_up and the LM head
+        self.S.update({"qkv": 3, "o": 4, "gu": 1, "down": 4, "lm": 1})
         if split_override:  # e.g. "o:4,down:5"
             for kv in split_override.split(","):
                 k, v = kv.split(":")
