@@ -420,10 +420,11 @@ class Colocation:
         return bool(torch.equal(ref.view(torch.int16), got.view(torch.int16)))
 
 
-def reference_sim(solo, requests, tokens, policy="tpot-first", scale=1):
+def reference_sim(solo, requests, tokens, policy="tpot-first", scale=1, slo_x=8.0):
     """Time the reference simulator (corosim SimEngine, oracle/_ref) on the
     same two-tenant scenario, time unit = 1 us, calibrated with the measured
-    solo durations.  Returns (simulated P99 TPOT ms, wall s, events).
+    solo durations and the GPU arm's SLOs (TPOT slo_x x step, TTFT twice
+    that).  Returns (simulated P99 TPOT ms, wall s, events).
 
     Bandwidth demands sum to 1 (decode 0.75 + training 0.25): with an
     oversubscribed HBM (sum > 1) the reference's own work-conservation check
@@ -439,7 +440,7 @@ def reference_sim(solo, requests, tokens, policy="tpot-first", scale=1):
     for r in range(n_req):
         recs.append({"arrival_time": str(period_us // 4 + r * period_us), "job_id": "chat", "kind": "inference",
                      "prompt_tokens": 8, "output_tokens": tokens, "priority": "latency_critical",
-                     "slo": {"ttft": str(3 * step_us), "tpot": str(int(1.5 * step_us))}})
+                     "slo": {"ttft": str(int(2 * slo_x * step_us)), "tpot": str(int(slo_x * step_us))}})
     sc = {"devices": [{"tiers": ["0.25", "0.5", "0.75", "1"]}], "policy": policy,
           "policy_params": {"quantum": "5000"},
           "segments_per_kernel": 16, "event_budget": 100000000,
