@@ -550,6 +550,111 @@ def gpu_arm(args, rank, world):
     return out, solo
 
 
+def config1_leg(dev):
+    """Config 1: one unmodified SGEMM 1024^3 (fp32 FFMA, 64x64 logical tiles,
+    k-ascending fma chain) as a GPU coroutine with a mid-kernel SM-quota change
+    (100% -> 25% at 30% of claimed blocks -> 100% at 60%), bit-exact vs its
+    solo launch; solo and coroutine device times."""
+    import numpy as np
+    import torch
+    from paper_2603_15042_b200 import _abi
+    from paper_2603_15042_b200.runtime import Domain
+    M = N = K = 1024
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1)
+    A = torch.rand(M, K, device=f"cuda:{dev}", generator=g) * 2 - 1
+    B = torch.rand(K, N, device=f"cuda:{dev}", generator=g) * 2 - 1
+    C_solo = torch.zeros(M, N, device=f"cuda:{dev}")
+    C_co = torch.zeros(M, N, device=f"cuda:{dev}")
+    grid = (N // 64, M // 64, 1)
+    a_solo = _abi.SgemmArgs(A.data_ptr(), B.data_ptr(), C_solo.data_ptr(), M, N, K, 0)
+    a_co = _abi.SgemmArgs(A.data_ptr(), B.data_ptr(), C_co.data_ptr(), M, N, K, 0)
+    with Domain(dev, block_log_capacity=1 << 14) as dom:
+        # solo: the same body as a plain grid on a stream (registered args, no per-launch setup)
+        ks = dom.kernel("sgemm/solo", _abi.BODY_SGEMM, grid, a_solo)
+        stream = torch.cuda.current_stream().cuda_stream
+        for _ in range(3):
+            dom.solo(ks, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            dom.solo(ks, stream)
+        e1.record()
+        torch.cuda.synchronize()
+        solo_ms = e0.elapsed_time(e1) / 5
+        dom.start()
+        t = dom.tenant("sgemm", _abi.BEST_EFFORT)
+        dom.quota_set(dom.mask(t, 0, dom.num_sms))
+        kid = dom.kernel("sgemm", _abi.BODY_SGEMM, grid, a_co)
+        nblk = grid[0] * grid[1]
+        for _ in range(2):
+            s = dom.launch(t, kid)
+        dom.wait(t, s)
+        dom.clear_logs()
+        dom.poll(1 << 16)
+        dom.quota_at_claim(t, s + 1, int(0.3 * nblk), dom.mask(t, 0, dom.num_sms // 4))
+        dom.quota_at_claim(t, s + 1, int(0.6 * nblk), dom.mask(t, 0, dom.num_sms))
+        s = dom.launch(t, kid)
+        dom.wait(t, s)
+        c = [x for x in dom.poll(1 << 16) if x.tenant == t][-1]
+        blocks = sorted(b.block for b in dom.block_log() if b.tenant == t and b.seq == s)
+        switches = len(dom.switch_log())
+    exact = bool(np.array_equal(C_co.cpu().numpy().view(np.uint32), C_solo.cpu().numpy().view(np.uint32)))
+    co_ms = (c.t_end - c.t_first_claim) / 1e6
+    flop = 2.0 * M * N * K
+    ffma_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s, fp32 FFMA at max clock
+    ach = flop / (min(solo_ms, co_ms) * 1e-3) / 1e12
+    return {"workload": "config 1: SGEMM 1024^3 fp32 (64x64 logical tiles, 256 blocks) as one coroutine, quota "
+                        "100% -> 25% at 30% of claimed blocks -> 100% at 60%",
+            "bit_exact_vs_solo": exact, "all_blocks_once": blocks == list(range(nblk)),
+            "solo_ms": round(solo_ms, 4), "coroutine_ms": round(co_ms, 4), "ctl_switch_records": switches,
+            "roofline": {"bound": "fp32 FFMA", "achieved": round(ach, 2), "peak": round(ffma_peak, 1),
+                         "unit": "TFLOP/s", "frac": round(ach / ffma_peak, 4),
+                         "peak_source": "148 SMs x 128 FFMA lanes x 2 x 1965 MHz (nominal; no measured fp32 peak)"}}
+
+
+def config3_leg(dev):
+    """Config 3: SM-quota migration sweep.  The device timer flips a tenant
+    between all SMs and a quarter of them every 50 us .. 5 ms; yield / drain
+    / grant latency (us) and lost throughput from the device switch log, for
+    5-us logical blocks and for the training GEMM's 128x256 tiles; plus the
+    host -> device control round trip."""
+    import torch
+    from paper_2603_15042_b200 import _abi, migration as mg
+    from paper_2603_15042_b200.runtime import Domain
+    from paper_2603_15042_b200.tenants import TrainGemm
+    # 16384 x 16384 x 8192 (~4 ms): long enough for flips every 200 us .. 2 ms;
+    # 128x256 tiles (the throughput choice) and 128x64 tiles (4x shorter
+    # logical blocks: the latency choice)
+    gemm = TrainGemm(M=16384, N=16384, K=8192, device=f"cuda:{dev}", seed=5)
+    narrow = _abi.gemm_args(gemm.A.data_ptr(), gemm.B.data_ptr(), gemm.C.data_ptr(), 16384, 16384, 8192, bn=64)
+    torch.cuda.synchronize()
+    rows = []
+    with Domain(dev, tiers=[Fraction(1)], block_log_capacity=0, lend_idle_sms=False) as dom:
+        t = dom.tenant("migrating", _abi.BEST_EFFORT)
+        nspin = int(2 * 148 * 2 * 30000 / 5 / 8)  # ~30 ms of 5-us blocks at full quota
+        spin = mg.spin_kernel(dom, 5, nspin)
+        gk = gemm.register(dom)
+        gn = dom.kernel("train/gemm_bf16/bn64", _abi.BODY_GEMM_BF16, _abi.gemm_grid(16384, 16384, 64), narrow,
+                        phase=_abi.TRAINING)
+        dom.start()
+        base = mg.run(dom, t, spin, 0)
+        for p in (50, 200, 1000, 5000):
+            rows.append(dict(unit="spin 5 us", period_us=p, **mg.summarize(mg.run(dom, t, spin, p), base["blocks_per_s"])))
+        gemm_rows = {}
+        for name, k, tile_flop in (("gemm tile 128x256x8192", gk, 2 * 128 * 256 * 8192),
+                                   ("gemm tile 128x64x8192", gn, 2 * 128 * 64 * 8192)):
+            gbase = mg.run(dom, t, k, 0)
+            gemm_rows[name] = {"unflipped_tflops": round(gbase["blocks_per_s"] * tile_flop / 1e12, 1),
+                               "block_us": round(1e6 / gbase["blocks_per_s"] * 2 * 148, 1)}
+            for p in (200, 1000):
+                rows.append(dict(unit=name, period_us=p, **mg.summarize(mg.run(dom, t, k, p), gbase["blocks_per_s"])))
+        rtt = [x / 1e3 for x in dom.ctl_roundtrip(100)]
+    return {"workload": "config 3: quota flips 100% <-> 25% of the SMs by the device timer (no host round trip)",
+            "sweep": rows, "gemm_tiles": gemm_rows,
+            "host_device_ctl_roundtrip_us": {"p50": round(mg.pct(rtt, .5), 2), "p99": round(mg.pct(rtt, .99), 2)}}
+
+
 def config5_leg(args, rank, world, dev, gather_fn):
     """Config 5: the 16-tenant mix (8 decode + 8 training) partitioned over
     the ranks by the native workload-aware placement, plus one data-parallel
@@ -739,6 +844,7 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--decode-sat", default="1/2", help="decode compute saturation (tier wanted)")
     ap.add_argument("--slo-x", type=float, default=8.0, help="TPOT SLO as a multiple of the solo step")
+    ap.add_argument("--no-config13", action="store_true", help="skip the config 1 / config 3 legs")
     ap.add_argument("--no-config5", action="store_true", help="skip the config 5 (16-tenant placement) leg")
     ap.add_argument("--c5-seconds", type=float, default=3.0, help="config 5 run window per rank")
     ap.add_argument("--c5-dp-iters", type=int, default=40, help="config 5 data-parallel tenant iterations")
@@ -785,6 +891,14 @@ def main():
         out, solo = gpu_arm(args, rank, world)
     if world > 1 and not args.only_config5:
         out = gather_ranks(out, world)
+    if not args.no_config13 and not args.only_config5:
+        import torch
+        torch.cuda.empty_cache()
+        dev = int(os.environ.get("LOCAL_RANK", rank))
+        log("config 1 and 3 legs")
+        c1, c3 = config1_leg(dev), config3_leg(dev)
+        if rank == 0:
+            out["config1"], out["config3"] = c1, c3
     if not args.no_config5:
         import torch
         torch.cuda.empty_cache()
