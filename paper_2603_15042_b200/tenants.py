@@ -65,7 +65,7 @@ class DecodeConfig:
     batch: int = 32
     L: int = 1024          # attended KV length (positions 0..L-1; the new token writes L-1)
     eps: float = 1e-5
-    attn_splits: int = 2
+    attn_splits: int = 1   # one block per (batch row, kv head): measured best (scripts/block_stats.py ASPLIT sweep)
 
 
 class DecodeModel:
