@@ -225,6 +225,9 @@ class RmsArgs(ctypes.Structure):
     _fields_ = [("x", ctypes.c_uint64), ("stats", ctypes.c_uint64), ("K", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
+ATTN_CHUNK = 64  # KV positions per attention TMA box / pipeline stage (csrc/bodies/decode.cuh kAttnChunk)
+
+
 class AttnArgs(ctypes.Structure):
     _fields_ = [("tmK", TmaDesc), ("tmV", TmaDesc), ("q", ctypes.c_uint64), ("out", ctypes.c_uint64),
                 ("ws", ctypes.c_uint64), ("counters", ctypes.c_uint64), ("L", ctypes.c_int32),

@@ -302,13 +302,16 @@ struct AttnArgs {
     uint64_t dbg;       // optional [grid][8] timestamps
 };
 
-constexpr int kAttnChunk = 64;   // KV positions per staged chunk (8 n-tiles: one per warp in QK)
-constexpr int kAttnStages = 3;
+constexpr int kAttnChunk = 64;   // KV positions per staged chunk (QK warp w: positions w*kQkPos ..)
+constexpr int kQkPos = kAttnChunk / 4;  // positions per QK warp per chunk
+constexpr int kQkNt = kQkPos / 8;       // mma n-tiles per QK warp per chunk
+constexpr int kAttnStages = 3;  // 3 x 32 KB (K + V of 64 positions)
 constexpr uint32_t kAttnTile = kAttnChunk * 256;                      // 64 rows x 128 dims bf16 = 16 KB
 constexpr uint32_t kAttnStageBytes = 2 * kAttnTile;                   // K + V = 32 KB
 constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStageBytes;       // 64 KB
-constexpr uint32_t kAttnSOff = kAttnBarOff + 1024;                    // scores fp32 [4][64]
-constexpr uint32_t kAttnSmem = kAttnSOff + 4 * kAttnChunk * 4 + 1024;
+constexpr uint32_t kAttnSOff = kAttnBarOff + 1024;                    // scores fp32 [2][4][64]
+constexpr uint32_t kAttnSBytes = 4 * kAttnChunk * 4;                   // one S buffer
+constexpr uint32_t kAttnSmem = kAttnSOff + 2 * kAttnSBytes + 1024;
 
 // byte address of (position r, dim d (multiple of 8)) in a K/V tile loaded
 // through the {64, 2, rows} view: smem 128-B row R = 2r + d/64, SWIZZLE_128B
@@ -360,8 +363,11 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     const uint32_t sbase = tc::smem_u32(base);
     uint64_t* full = reinterpret_cast<uint64_t*>(base + kAttnBarOff);
     uint64_t* empty = full + kAttnStages;
-    const uint32_t Ssm = sbase + kAttnSOff;  // scores fp32 [4][kAttnChunk]
-    const int BAR_SFULL = body_lane() ? 14 : 6, BAR_SEMPTY = body_lane() ? 15 : 13;
+    const uint32_t Ssm = sbase + kAttnSOff;  // scores fp32 [2][4][kAttnChunk], double-buffered
+    // S handoff QK -> PV through two buffers: QK warps run up to two chunks
+    // ahead of the PV warps (mbarriers, 128 arrivals each)
+    uint64_t* sfull = empty + kAttnStages;   // [2]
+    uint64_t* sempty = sfull + 2;            // [2]
     const int row0 = (b * 8 + h) * a.Lmax + p0;
     uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
     if (dbg && ltid() == 128) dbg[0] = globaltimer();
@@ -378,6 +384,10 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         for (int s = 0; s < kAttnStages; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 8);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&sfull[b], 128);
+            tc::mbar_init(&sempty[b], 128);
         }
         tc::fence_mbar_init();
         tc::tma_fence_desc(&a.tmK);
@@ -421,11 +431,11 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             tc::mbar_wait(&full[s], (ci / kAttnStages) & 1);
             const uint32_t kt = sbase + s * kAttnStageBytes;
             const int valid = min(kAttnChunk, p1 - (p0 + ci * kAttnChunk));
-            float sv[2][2];
+            float sv[kQkNt][2];
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {  // positions 16w + 8nt .. +7
+            for (int nt = 0; nt < kQkNt; ++nt) {  // positions kQkPos*w + 8nt .. +7
                 float acc4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-                const int prow = warp * 16 + nt * 8 + (lane & 7);
+                const int prow = warp * kQkPos + nt * 8 + (lane & 7);
 #pragma unroll
                 for (int kk = 0; kk < 8; kk += 2) {
                     uint32_t b0, b1, b2, b3;
@@ -433,41 +443,42 @@ __device__ void body_attn_decode(const BodyCtx& c) {
                     mma16816(acc4[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
                     mma16816(acc4[1], qa[kk + 1][0], 0u, qa[kk + 1][1], 0u, b2, b3);
                 }
-                const int pc = warp * 16 + nt * 8 + 2 * tq;
+                const int pc = warp * kQkPos + nt * 8 + 2 * tq;
                 sv[nt][0] = pc < valid ? (acc4[0][0] + acc4[1][0]) * scale : kNegInf;
                 sv[nt][1] = pc + 1 < valid ? (acc4[0][1] + acc4[1][1]) * scale : kNegInf;
             }
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&empty[s]);  // K of this slot consumed
-            if (ci > 0) nbar_sync(BAR_SEMPTY);           // PV warps have read the previous S
+            const int sb = ci & 1;
+            if (ci >= 2) tc::mbar_wait(&sempty[sb], ((ci - 2) >> 1) & 1);  // PV read chunk ci-2's S
             if (g < 4) {
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    const uint32_t sa = Ssm + (g * kAttnChunk + warp * 16 + nt * 8 + 2 * tq) * 4;
+                for (int nt = 0; nt < kQkNt; ++nt) {
+                    const uint32_t sa = Ssm + sb * kAttnSBytes + (g * kAttnChunk + warp * kQkPos + nt * 8 + 2 * tq) * 4;
                     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(sa), "f"(sv[nt][0]), "f"(sv[nt][1])
                                  : "memory");
                 }
             }
-            nbar_arrive(BAR_SFULL);
-            if (ltid() == 0 && ci + kAttnStages < nch) {
-                tc::mbar_wait(&empty[s], (ci / kAttnStages) & 1);  // K and V of the slot consumed
-                issue(ci + kAttnStages);
-            }
+            tc::mbar_arrive(&sfull[sb]);  // release: this thread's S stores
         }
-        if (nch > 0) nbar_sync(BAR_SEMPTY);  // balance the PV warps' last release
     } else {
         // ================= PV warps =================
         const int pw = warp - 4;  // dims 32 pw .. 32 pw + 31
         constexpr int KS = kAttnChunk / 16;
         const int m4 = lane >> 3;
+        if (pw == 0 && lane == 0) {  // this thread issues the refills
+            tc::tma_fence_desc(&a.tmK);
+            tc::tma_fence_desc(&a.tmV);
+        }
         for (int ci = 0; ci < nch; ++ci) {
             const int s = ci % kAttnStages;
             tc::mbar_wait(&full[s], (ci / kAttnStages) & 1);
             const uint32_t vt = sbase + s * kAttnStageBytes + kAttnTile;
-            nbar_sync(BAR_SFULL);
+            const int sb = ci & 1;
+            tc::mbar_wait(&sfull[sb], (ci >> 1) & 1);
             float pv[KS][4];  // [k-step][a0.x, a0.y, a2.x, a2.y]
             {
-                const uint32_t sr = Ssm + ((g & 3) * kAttnChunk + 2 * tq) * 4;
+                const uint32_t sr = Ssm + sb * kAttnSBytes + ((g & 3) * kAttnChunk + 2 * tq) * 4;
 #pragma unroll
                 for (int kk = 0; kk < KS; ++kk) {
                     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(pv[kk][0]), "=f"(pv[kk][1]) : "r"(sr + 64 * kk));
@@ -475,7 +486,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
                                  : "r"(sr + 64 * kk + 32));
                 }
             }
-            nbar_arrive(BAR_SEMPTY);  // S copied into registers
+            tc::mbar_arrive(&sempty[sb]);  // S copied into registers
             float cm = kNegInf;
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk)
@@ -517,6 +528,12 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             }
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&empty[s]);  // V of this slot consumed
+            // refill by the last consumer (the PV side), so no QK warp ever
+            // waits for PV: QK runs ahead as far as data and S buffers allow
+            if (pw == 0 && lane == 0 && ci + kAttnStages < nch) {
+                tc::mbar_wait(&empty[s], (ci / kAttnStages) & 1);  // K and V of the slot consumed
+                issue(ci + kAttnStages);
+            }
         }
     }
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
@@ -581,7 +598,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     body_sync();
     if (dbg && ltid() == 128) dbg[6] = globaltimer();
     if (ltid() == 0)
-        for (int s = 0; s < 2 * kAttnStages; ++s) tc::mbar_inval(&full[s]);
+        for (int s = 0; s < 2 * kAttnStages + 4; ++s) tc::mbar_inval(&full[s]);
 }
 
 }  // namespace ds

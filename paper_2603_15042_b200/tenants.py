@@ -20,7 +20,7 @@ import torch
 from . import _abi
 
 SMS = 148
-ATTN_CHUNK = 64  # KV positions per attention TMA box (bodies/decode.cuh kAttnChunk)
+ATTN_CHUNK = _abi.ATTN_CHUNK  # KV positions per attention TMA box (bodies/decode.cuh kAttnChunk)
 LANES = 2
 WORKERS = SMS * LANES  # concurrent logical blocks (2 worker lanes per SM)
 

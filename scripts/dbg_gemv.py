@@ -20,7 +20,7 @@ for name in ("decode/qkv", "decode/o", "decode/down"):
     dbgs[name] = (dom.kernel(sid, body, grid, args), dbg, grid[0])
 torch.cuda.synchronize()
 dom.start()
-dom.quota_set(dom.mask(t, 0, dom.num_sms))
+dom.quota_set(dom.mask(t, 0, int(os.environ.get("NSM", "148"))))
 for name, (kid, dbg, g) in dbgs.items():
     for _ in range(3): last = dom.launch(t, kid)
     dom.wait(t, last)
@@ -28,6 +28,8 @@ for name, (kid, dbg, g) in dbgs.items():
     t0 = min(r[0] for r in d)
     last_blocks = [r for r in d if (r[2] >> 63) & 1]
     other = [r for r in d if not ((r[2] >> 63) & 1)]
+    if not other:
+        other = last_blocks
     def ph(rows, a, b, mask=False):
         v = [((r[b] & ((1 << 63) - 1)) - (r[a] & ((1 << 63) - 1))) / 1e3 for r in rows]
         return [round(statistics.median(v), 2), round(max(v), 2)]
