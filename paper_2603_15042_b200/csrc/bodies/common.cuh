@@ -80,10 +80,9 @@ __device__ __forceinline__ void st_release_sys_u64(void* p, uint64_t v) {
 // Wait until every earlier launch of this tenant has completed (acquire).
 __device__ __forceinline__ void wait_prev(const BodyCtx& c) {
     if (!c.prev_head) return;
-    if (ld_acquire_u32(c.prev_head) < c.seq) {
-        while (ld_acquire_u32(c.prev_head) < c.seq) __nanosleep(64);
-    }
-    __threadfence();  // gpu-scope acquire; also drops stale L1 lines
+    // gpu-scope acquire: later loads (incl. L1) observe every write the
+    // completed launches released through their retire atomics
+    while (ld_acquire_u32(c.prev_head) < c.seq) __nanosleep(32);
 }
 
 }  // namespace ds

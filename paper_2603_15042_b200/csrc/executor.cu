@@ -348,7 +348,7 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
 
 __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* slot) {
     DevTenant* T = &st->tenants[t];
-    __threadfence();
+    // ordered after every block's writes by the acq_rel retire atomic
     const uint64_t tend = globaltimer();
     // 1. publish completion first (critical path: early-started blocks of the
     //    next launch are waiting on head)
@@ -403,8 +403,11 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
             if (lane == 0) {
                 uint64_t t1 = globaltimer();
                 uint64_t t0 = *body_t0;
-                __threadfence();
-                uint32_t r = atomicAdd(&prev.slot->retired, 1u);
+                // release: the body's writes (ordered before this thread by the
+                // kDone barrier, cumulativity) are published with the retire;
+                // acquire: the completer sees every other block's writes
+                uint32_t r;
+                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(r) : "l"(&prev.slot->retired) : "memory");
                 atomicAdd(&st->blocks_executed, 1ull);
                 if (st->blog_cap) {
                     unsigned long long i = atomicAdd(&st->blog_count, 1ull);
@@ -456,7 +459,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
             }
             if (got) {
                 backoff = 32;
-                __threadfence();  // acquire: prior launches' results (and invalidate L1)
+                // no fence here: bodies acquire earlier launches' results in wait_prev
                 Stage s;
                 s.tenant = w.tenant;
                 s.body = ld_volatile_u32(&w.slot->body);
@@ -543,7 +546,8 @@ __device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0
         c.seq = s.seq;
         c.dbg = nullptr;
         run_body(s.body, c);
-        __threadfence();  // this thread's writes visible at gpu scope before retire
+        // the scheduler's release (acq_rel retire atomic after this barrier)
+        // publishes this thread's writes at gpu scope
         named_arrive(kDone, kBodyThreads + 32);
     }
 }
