@@ -46,6 +46,7 @@ constexpr int kGemvStages = kCtasPerSm == 2 ? 5 : 8;
 // epilogue scratch [128][33] fp32 + rvec/flag reuses the TMA ring: every
 // stage has been consumed once the accumulator is complete
 constexpr uint32_t kGemvScratch = 0;
+constexpr uint32_t kGemvOwnOff = 32768;  // combiner's own partial (16 KB), clear of the scratch
 
 __device__ __forceinline__ float bf16_to_f(uint16_t v) { return __uint_as_float((uint32_t)v << 16); }
 __device__ __forceinline__ uint16_t f_to_bf16(float f) {
@@ -102,17 +103,24 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
         for (int b = 0; b < 32; ++b) v[b] = __uint_as_float(raw[b]);
     }
     const bool proceed = combiner;
+    // the combiner's own partial stays on chip: [128 rows][8 float4] in the
+    // (consumed) ring, same element order as a workspace slab
+    float4* own = reinterpret_cast<float4*>(base + kGemvOwnOff);
     if (a.S > 1) {
-        if (warp >= 4) {
-            float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.ws) + ((size_t)s * a.N + n) * 32);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        }
-        body_sync();  // orders the CTA's partial stores before thread 0's release
         uint32_t* ctr = reinterpret_cast<uint32_t*>(a.counters) + n_blk;
         if (!combiner) {
+            if (warp >= 4) {
+                float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.ws) + ((size_t)s * a.N + n) * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+            body_sync();  // orders the CTA's partial stores before thread 0's release
             if (ltid() == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
         } else {
+            if (warp >= 4) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) own[row * 8 + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
             if (ltid() == 0) {
                 while (ld_acquire_u32(ctr) != (uint32_t)(a.S - 1)) __nanosleep(32);
                 *ctr = 0;  // at rest for the next launch (which only arrives after this one completes)
@@ -131,8 +139,13 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
 #pragma unroll 3
             for (int sp = 0; sp < a.S; ++sp) {
                 float4 x[4];
+                if (sp < a.S - 1) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) x[j] = __ldcg(wsb + sp * sstride4 + ltid() + 256 * j);
+                    for (int j = 0; j < 4; ++j) x[j] = __ldcg(wsb + sp * sstride4 + ltid() + 256 * j);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) x[j] = own[ltid() + 256 * j];
+                }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     acc[j].x += x[j].x;

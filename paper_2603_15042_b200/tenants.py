@@ -251,7 +251,9 @@ class TrainGemm:
         self.A = (torch.rand(M, K, device=device, generator=g) * 2 - 1).to(torch.bfloat16)
         self.B = (torch.rand(N, K, device=device, generator=g) * 2 - 1).to(torch.bfloat16)
         self.C = torch.zeros(M, N, device=device, dtype=torch.bfloat16)
-        self.args = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), M, N, K)
+        # 32-row tile groups: the ~296 concurrently claimed tiles share A/B
+        # panels in L2 (scripts/perf_gemm.py GM sweep)
+        self.args = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), M, N, K, group_m=32)
         self.grid = _abi.gemm_grid(M, N)
         self.flops = 2.0 * M * N * K
 
