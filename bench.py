@@ -864,8 +864,17 @@ def main():
         if rank != 0:
             return
         # the reference's own CPU implementation of the path: the corosim
-        # simulator (oracle/_ref), calibrated with nominal solo durations
-        solo = {"decode_step_ms": 3.0, "gemm_ms": 0.78}
+        # simulator (oracle/_ref), calibrated with the solo durations last
+        # measured on B200 by this bench (committed record), else nominal
+        # HBM / tensor floors
+        solo, calib = {"decode_step_ms": 3.0, "gemm_ms": 0.78}, "nominal B200 floors: 3.0 ms/decode step, 0.78 ms/GEMM"
+        try:
+            rec = json.load(open(os.path.join(ROOT, "profiles", "r1_bench_latest.json")))["solo"]
+            solo = {"decode_step_ms": float(rec["decode_step_ms"]), "gemm_ms": float(rec["gemm_ms"])}
+            calib = (f"solo durations measured on B200 (profiles/r1_bench_latest.json): "
+                     f"{solo['decode_step_ms']} ms/decode step, {solo['gemm_ms']} ms/GEMM")
+        except Exception:
+            pass
         try:
             p99, wall, ev = reference_sim(solo, args.steps, args.tokens)
             steps_wall = []
@@ -876,8 +885,8 @@ def main():
                     "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                     "ms_per_step": statistics.median(steps_wall[args.warmup:]) * 1e3, "higher_is_better": False,
                     "scaling": "weak", "vs_baseline": None, "dtype": "rational (exact)", "data": "synthetic",
-                    "config": {"workload": "config 2 scenario in the reference simulator (corosim), nominal "
-                                           "B200 solo durations 3.0 ms/decode step, 0.78 ms/GEMM"},
+                    "config": {"workload": "config 2 scenario in the reference simulator (corosim)",
+                               "calibration": calib},
                     "cpu_baseline": {"value": p99, "unit": "ms", "cores": 1, "kind": "reference",
                                      "sample": f"{args.steps} requests x {args.tokens} tokens, {ev} events"},
                     "e2e": {"value": p99, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

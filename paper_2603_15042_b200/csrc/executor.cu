@@ -253,6 +253,7 @@ struct Claimed {
     int32_t tenant;
     uint32_t seq;
     uint32_t block;
+    uint32_t grid;  // executed grid of the launch (known at claim: no re-read at retire)
     LaunchSlot* slot;
 };
 
@@ -342,6 +343,7 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
     out.tenant = t;
     out.seq = s2;
     out.block = b2;
+    out.grid = grid;
     out.slot = slot;
     return true;
 }
@@ -423,7 +425,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                         st->blog[i] = br;
                     }
                 }
-                if (r == ld_volatile_u32(&prev.slot->grid) - 1) complete_launch(st, prev.tenant, prev.seq, prev.slot);
+                if (r == prev.grid - 1) complete_launch(st, prev.tenant, prev.seq, prev.slot);
             }
             __syncwarp();
             have_prev = false;
@@ -460,16 +462,24 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
             if (got) {
                 backoff = 32;
                 // no fence here: bodies acquire earlier launches' results in wait_prev
+                // the slot's first 32 B (body, grid, gx, gy, gz, kernel_id, args)
+                // in two vector loads issued together: one L2 round trip
+                uint4 h0, h1;
+                asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(h0.x), "=r"(h0.y), "=r"(h0.z), "=r"(h0.w) : "l"(w.slot) : "memory");
+                asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(h1.x), "=r"(h1.y), "=r"(h1.z), "=r"(h1.w)
+                             : "l"(reinterpret_cast<const char*>(w.slot) + 16) : "memory");
                 Stage s;
                 s.tenant = w.tenant;
-                s.body = ld_volatile_u32(&w.slot->body);
+                s.body = (int32_t)h0.x;
                 s.seq = w.seq;
                 s.block = w.block;
-                s.gx = ld_volatile_u32(&w.slot->gx);
-                s.gy = ld_volatile_u32(&w.slot->gy);
-                s.gz = ld_volatile_u32(&w.slot->gz);
+                s.gx = h0.z;
+                s.gy = h0.w;
+                s.gz = h1.x;
                 s.pad = 0;
-                s.args = ld_volatile_u64(&w.slot->args);
+                s.args = ((uint64_t)h1.w << 32) | h1.z;
                 *stage = s;
             } else {
                 stage->tenant = -1;
@@ -487,6 +497,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
         w.seq = __shfl_sync(0xffffffffu, w.seq, 0);
         w.block = __shfl_sync(0xffffffffu, w.block, 0);
         w.slot = (LaunchSlot*)__shfl_sync(0xffffffffu, (unsigned long long)w.slot, 0);
+        w.grid = __shfl_sync(0xffffffffu, w.grid, 0);
         // ---- bookkeeping while the body runs ----
         if (lane == 0) {
             if (w.block == 0) w.slot->t_first = globaltimer();
