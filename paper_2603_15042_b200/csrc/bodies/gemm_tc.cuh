@@ -23,10 +23,10 @@ struct alignas(64) TmaDesc {
 constexpr int kTcBM = 128;
 constexpr int kTcBK = 64;  // 64 bf16 = one 128-B swizzle row
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int BK = kTcBK>
 struct TcSmem {
-    static constexpr uint32_t kABytes = kTcBM * kTcBK * 2;  // 16 KB
-    static constexpr uint32_t kBBytes = BN * kTcBK * 2;
+    static constexpr uint32_t kABytes = kTcBM * BK * 2;  // 16 KB at BK = 64
+    static constexpr uint32_t kBBytes = BN * BK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
     static constexpr uint32_t kBarOff = STAGES * kStageBytes;
     static constexpr uint32_t kBytes = kBarOff + 1024;  // barriers + epilogue scratch follow
@@ -43,12 +43,14 @@ __device__ __forceinline__ char* align1024(char* p) {
 // smem image of consecutive [128 x 64] tiles (row slab a_row/128, k-block kb at
 // ((a_row/128) * a_kblocks + kb) * 16 KB), fetched with one contiguous 16-KB
 // bulk copy per stage instead of 128 strided row segments.
-template <int BN, int STAGES>
+// BK = 64: SWIZZLE_128B tiles (one 128-B row per K block); BK = 32:
+// SWIZZLE_64B tiles (half the bytes per stage, twice the stages in the same smem)
+template <int BN, int STAGES, int BK = kTcBK>
 __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
                                             int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
                                             const char* a_packed = nullptr, int a_kblocks = 0,
                                             const BodyCtx* dep = nullptr) {
-    using L = TcSmem<BN, STAGES>;
+    using L = TcSmem<BN, STAGES, BK>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;
@@ -74,11 +76,11 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
                 tc::bulk_g2s_hint(sa, a_packed + ((size_t)(a_row / kTcBM) * a_kblocks + kb_begin + i) * L::kABytes,
                                   L::kABytes, &full[s], pol);
             else
-                tc::tma_load_2d_hint(sa, tmA, &full[s], (kb_begin + i) * kTcBK, a_row, pol);
+                tc::tma_load_2d_hint(sa, tmA, &full[s], (kb_begin + i) * BK, a_row, pol);
         };
         auto issue_b = [&](int i) {
             const int s = i % STAGES;
-            tc::tma_load_2d(base + s * L::kStageBytes + L::kABytes, tmB, &full[s], (kb_begin + i) * kTcBK, b_row);
+            tc::tma_load_2d(base + s * L::kStageBytes + L::kABytes, tmB, &full[s], (kb_begin + i) * BK, b_row);
         };
         // With a dependency, the A operand (weights, immutable) streams while
         // the previous launch finishes; B (its output) only after wait_prev.
@@ -107,10 +109,10 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             tc::tc_fence_after();
             char* sa = base + s * L::kStageBytes;
             char* sb = sa + L::kABytes;
-            const uint64_t ad = tc::smem_desc_k_sw128(sa);
-            const uint64_t bd = tc::smem_desc_k_sw128(sb);
+            const uint64_t ad = BK == 64 ? tc::smem_desc_k_sw128(sa) : tc::smem_desc_k_sw64(sa);
+            const uint64_t bd = BK == 64 ? tc::smem_desc_k_sw128(sb) : tc::smem_desc_k_sw64(sb);
 #pragma unroll
-            for (int k = 0; k < kTcBK / 16; ++k) {
+            for (int k = 0; k < BK / 16; ++k) {
                 // +32 B per K=16 step inside the 128-B swizzle row
                 tc::mma_bf16(tmem_base, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
             }
@@ -124,9 +126,9 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
     }
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int BK = kTcBK>
 __device__ __forceinline__ void tc_teardown(char* base) {
-    using L = TcSmem<BN, STAGES>;
+    using L = TcSmem<BN, STAGES, BK>;
     tc::tc_fence_before();
     body_sync();
     if (ltid() == 0) {
@@ -158,6 +160,8 @@ struct GemmArgs {
     int32_t bn;      // 0 or 256, 128, 64
     int32_t splits;  // split-K factor S (0/1 = none)
     uint64_t ws;     // fp32 [tiles][S][128][BN] when S > 1
+    int32_t bk;      // 0 or 64: SWIZZLE_128B K blocks of 64; 32: SWIZZLE_64B K blocks of 32 (4-stage ring)
+    int32_t pad;
 };
 
 constexpr int kGemmBN = 256;
@@ -175,7 +179,7 @@ __device__ __forceinline__ void gemm_tile_coords(const GemmArgs& a, int bn, int 
     n_blk = r / rows;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int BK = kTcBK>
 __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a) {
     char* base = align1024(c.smem);
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
@@ -183,9 +187,9 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
     const int tile = t / S, sp = t % S;
     int m_blk, n_blk;
     gemm_tile_coords(a, BN, tile, m_blk, n_blk);
-    const int kbs = a.K / kTcBK;
+    const int kbs = a.K / BK;
     const int kb0 = (int)((int64_t)sp * kbs / S), kb1 = (int)((int64_t)(sp + 1) * kbs / S);
-    tc_mainloop<BN, STAGES>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb0, kb1, c.tmem_base, false);
+    tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb0, kb1, c.tmem_base, false);
     const int warp = ltid() >> 5, lane = ltid() & 31;
     if (warp >= 4) {
         const int q = warp & 3;
@@ -222,11 +226,15 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
             }
         }
     }
-    tc_teardown<BN, STAGES>(base);
+    tc_teardown<BN, STAGES, BK>(base);
 }
 
 __device__ void body_gemm_bf16(const BodyCtx& c) {
     const GemmArgs& a = *reinterpret_cast<const GemmArgs*>(c.args);
+    if (a.bk == 32 && (a.bn == 0 || a.bn == 256)) {  // 4 x 24 KB stages per lane
+        gemm_body_bn<kGemmBN, kCtasPerSm == 2 ? 4 : 8, 32>(c, a);
+        return;
+    }
     switch (a.bn) {
         case 64: gemm_body_bn<64, kCtasPerSm == 2 ? 4 : 8>(c, a); break;
         case 128: gemm_body_bn<128, kCtasPerSm == 2 ? 3 : 6>(c, a); break;

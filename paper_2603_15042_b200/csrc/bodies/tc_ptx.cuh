@@ -162,6 +162,19 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw128(const void* smem_tile) {
     return d;
 }
 
+// Same for SWIZZLE_64B K-major tiles (rows of 64 B = 32 bf16; 8-row groups
+// 512 B apart; layout type 4).  The K=16 step is +32 B inside the row as well.
+__device__ __forceinline__ uint64_t smem_desc_k_sw64(const void* smem_tile) {
+    uint64_t addr = smem_u32(smem_tile);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
+    return d;
+}
+
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major.
 //   bits 4-5 c_format (1 = F32), 7-9 a_format (1 = BF16), 10-12 b_format (1 = BF16),
 //   15/16 a/b major (0 = K), 17-22 N >> 3, 24-28 M >> 4

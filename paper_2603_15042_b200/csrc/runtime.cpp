@@ -999,7 +999,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                           uint32_t box_cols) {
     if (!out128 || !base) return fail(DS_INVALID_ARGUMENT, "null");
-    if (box_cols * 2 != 128) return fail(DS_CONFIG_ERROR, "box inner extent must be 128 B (SWIZZLE_128B)");
+    if (box_cols * 2 != 128 && box_cols * 2 != 64)
+        return fail(DS_CONFIG_ERROR, "box inner extent must be 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B)");
     if ((cols * 2) % 16 != 0 || ((uintptr_t)base & 15)) return fail(DS_CONFIG_ERROR, "row pitch / base must be 16-B aligned");
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
@@ -1015,7 +1016,8 @@ int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(DS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     std::memcpy(out128, &m, 128);
@@ -1043,7 +1045,8 @@ int ds_tensor_map_bf16_kv(void* out128, const void* base, uint64_t rows, uint32_
     cuuint32_t box[3] = {64, 2, box_rows};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(DS_CUDA_ERROR, "cuTensorMapEncodeTiled(kv) failed (" + std::to_string((int)r) + ")");
     std::memcpy(out128, &m, 128);

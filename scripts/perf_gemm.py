@@ -11,8 +11,9 @@ A = (torch.rand(M, K, device="cuda") * 2 - 1).to(torch.bfloat16)
 B = (torch.rand(N, K, device="cuda") * 2 - 1).to(torch.bfloat16)
 C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
 BN = int(os.environ.get("BN", "256"))
+BK = int(os.environ.get("BK", "64"))
 GM = int(os.environ.get("GM", "16"))
-args = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, group_m=GM, bn=BN)
+args = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, group_m=GM, bn=BN, bk=BK)
 grid = _abi.gemm_grid(M, N, BN)
 flop = 2.0 * M * N * K
 desc = __import__("paper_2603_15042_b200.runtime", fromlist=["make_desc"]).make_desc("gemm", _abi.BODY_GEMM_BF16, grid, args)

@@ -107,3 +107,37 @@ def test_splitk_coroutine_bit_exact_vs_solo():
         got = C_co.cpu()
     assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
 
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 1024), (384, 768, 4096)])
+def test_gemm_bk32_sw64_matches_fp32_reference(shape):
+    """K blocks of 32 staged as SWIZZLE_64B tiles in a 4-stage ring."""
+    M, N, K = shape
+    A, B, C = make(M, N, K, seed=5)
+    args = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, bk=32)
+    solo_launch(0, "gemm", _abi.BODY_GEMM_BF16, _abi.gemm_grid(M, N), args)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    err = (C.float() - ref).abs()
+    tol = ref.abs() * 2 ** -7 + 2 ** -6
+    assert bool((err <= tol).all()), float((err - tol).max())
+
+
+def test_gemm_bk32_coroutine_bit_exact_vs_solo():
+    M, N, K = 1024, 1024, 2048
+    A, B, C_solo = make(M, N, K, seed=6)
+    C_co = torch.zeros_like(C_solo)
+    grid = _abi.gemm_grid(M, N)
+    solo_launch(0, "gemm", _abi.BODY_GEMM_BF16, grid, _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_solo.data_ptr(), M, N, K, bk=32))
+    torch.cuda.synchronize()
+    a_co = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_co.data_ptr(), M, N, K, bk=32)
+    with Domain(0, block_log_capacity=0) as dom:
+        dom.start()
+        t = dom.tenant("train", _abi.BEST_EFFORT)
+        dom.quota_set(dom.mask(t, 0, dom.num_sms))
+        kid = dom.kernel("gemm", _abi.BODY_GEMM_BF16, grid, a_co, phase=_abi.TRAINING)
+        dom.quota_at_claim(t, 0, grid[0] // 2, dom.mask(t, 0, 30))
+        s = dom.launch(t, kid)
+        dom.wait(t, s)
+        got = C_co.cpu()
+    assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
