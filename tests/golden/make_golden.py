@@ -61,6 +61,19 @@ def main():
     with open(os.path.join(HERE, "workload_golden.json"), "w") as f:
         json.dump({"source": out["source"], "cases": wcases}, f)
     print("wrote", len(wcases), "workload cases")
+    # per-vctx transcripts / logical progress of the reference simulator on a
+    # two-job trace (integer bookkeeping the GPU engine must reproduce)
+    import test_transcript_parity as tp  # noqa: E402
+    sc, _ = tp.scenario()
+    out = json.loads(loader.ref_simulate(json.dumps(sc)))
+    with open(os.path.join(HERE, "transcript_golden.json"), "w") as f:
+        json.dump({"source": out_src(out), "scenario": sc, "transcripts": out["transcripts"],
+                   "logical_progress": out["logical_progress"], "kernels_completed": out["kernels_completed"]}, f)
+    print("wrote transcript golden:", out["kernels_completed"], "kernels")
+
+
+def out_src(out):
+    return "oracle/_ref SimEngine::simulate (reference corosim compiled from /root/reference)"
 
 
 if __name__ == "__main__":
