@@ -202,6 +202,8 @@ int ds_set_lend(ds_domain* dom, int lend_tenant); /* tenant allowed on idle SMs 
  * quota changes (config 1) and the migration sweep (config 3). */
 int ds_quota_at_claim(ds_domain* dom, int tenant, uint64_t seq, uint32_t block, const int32_t* owner,
                       const int32_t* lender, int n);
+/* empty the claim-trigger table (triggers fire in install order) */
+int ds_quota_triggers_reset(ds_domain* dom);
 /* periodic device-timer flips between two control words (period ns, 0 = off) */
 int ds_quota_periodic(ds_domain* dom, uint64_t period_ns, const int32_t* owner_a, const int32_t* lender_a,
                       const int32_t* owner_b, const int32_t* lender_b, int n);

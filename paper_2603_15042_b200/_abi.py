@@ -330,7 +330,7 @@ EXPORTS = [
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
     "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",
     "ds_ipc_alloc", "ds_ipc_free", "ds_ipc_handle", "ds_ipc_open", "ds_ipc_close", "ds_dp_abort",
-    "ds_engine_event_log", "ds_engine_quarantines",
+    "ds_engine_event_log", "ds_engine_quarantines", "ds_quota_triggers_reset",
 ]
 
 _lib = None
@@ -417,6 +417,7 @@ def lib():
         L.ds_ipc_handle.argtypes = [vp, ctypes.c_char_p]
         L.ds_ipc_open.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.ds_ipc_close.argtypes = [ctypes.c_int, vp]
+        L.ds_quota_triggers_reset.argtypes = [vp]
         L.ds_engine_event_log.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         L.ds_engine_quarantines.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
                                             ctypes.c_int, ctypes.POINTER(ctypes.c_int)]

@@ -933,6 +933,19 @@ int ds_ctl_log(ds_domain* d, ds_ctl_record* out, int64_t cap, int64_t* n) {
     return copy_log(d, d->d_clog, &d->d_state->clog_count, d->clog_cap, out, cap, n);
 }
 
+// Empty the claim-trigger table (all installed triggers must have fired or
+// belong to launches that will not run again): triggers fire in install order.
+int ds_quota_triggers_reset(ds_domain* d) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    cudaSetDevice(d->device);
+    uint32_t z[2] = {0, 0};  // trig_next, trig_count (adjacent)
+    DS_CUDA(cudaMemcpyAsync(&d->d_state->trig_next, z, sizeof(z), cudaMemcpyHostToDevice, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    d->n_triggers = 0;
+    return DS_OK;
+}
+
 int ds_clear_logs(ds_domain* d) {
     if (check_dom(d)) return DS_INVALID_ARGUMENT;
     cudaSetDevice(d->device);

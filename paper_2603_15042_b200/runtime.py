@@ -151,6 +151,9 @@ class Domain:
         check(lib().ds_quota_at_claim(self.h, tenant, seq, block, self._arr(owner), self._arr(lender),
                                       self.num_sms))
 
+    def quota_triggers_reset(self):
+        check(lib().ds_quota_triggers_reset(self.h))
+
     def quota_periodic(self, period_ns: int, owner_a, owner_b, lender_a=None, lender_b=None):
         check(lib().ds_quota_periodic(self.h, period_ns, self._arr(owner_a), self._arr(lender_a),
                                       self._arr(owner_b), self._arr(lender_b), self.num_sms))
