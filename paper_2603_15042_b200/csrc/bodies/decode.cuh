@@ -318,10 +318,14 @@ struct AttnArgs {
 constexpr int kAttnChunk = 64;   // KV positions per staged chunk (QK warp w: positions w*kQkPos ..)
 constexpr int kQkPos = kAttnChunk / 4;  // positions per QK warp per chunk
 constexpr int kQkNt = kQkPos / 8;       // mma n-tiles per QK warp per chunk
-constexpr int kAttnStages = 3;  // 3 x 32 KB (K + V of 64 positions)
+// Separate K and V rings: K is consumed by the QK warps (which run ahead),
+// V by the PV warps; V gets the deeper ring so its refills (issued when the
+// PV side releases a slot) have the most chunks of lookahead.
+constexpr int kAttnKSlots = 2;
+constexpr int kAttnVSlots = 4;
 constexpr uint32_t kAttnTile = kAttnChunk * 256;                      // 64 rows x 128 dims bf16 = 16 KB
-constexpr uint32_t kAttnStageBytes = 2 * kAttnTile;                   // K + V = 32 KB
-constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStageBytes;       // 64 KB
+constexpr uint32_t kAttnVOff = kAttnKSlots * kAttnTile;               // V ring after the K ring
+constexpr uint32_t kAttnBarOff = (kAttnKSlots + kAttnVSlots) * kAttnTile;  // 96 KB
 constexpr uint32_t kAttnSOff = kAttnBarOff + 1024;                    // scores fp32 [2][4][64]
 constexpr uint32_t kAttnSBytes = 4 * kAttnChunk * 4;                   // one S buffer
 constexpr uint32_t kAttnSmem = kAttnSOff + 2 * kAttnSBytes + 1024;
@@ -374,29 +378,38 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     const int nch = (p1 - p0 + kAttnChunk - 1) / kAttnChunk;
     char* base = align1024(c.smem);
     const uint32_t sbase = tc::smem_u32(base);
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + kAttnBarOff);
-    uint64_t* empty = full + kAttnStages;
+    uint64_t* kfull = reinterpret_cast<uint64_t*>(base + kAttnBarOff);  // [kAttnKSlots]
+    uint64_t* kempty = kfull + kAttnKSlots;
+    uint64_t* vfull = kempty + kAttnKSlots;                                // [kAttnVSlots]
+    uint64_t* vempty = vfull + kAttnVSlots;
     const uint32_t Ssm = sbase + kAttnSOff;  // scores fp32 [2][4][kAttnChunk], double-buffered
     // S handoff QK -> PV through two buffers: QK warps run up to two chunks
     // ahead of the PV warps (mbarriers, 128 arrivals each)
-    uint64_t* sfull = empty + kAttnStages;   // [2]
+    uint64_t* sfull = vempty + kAttnVSlots;  // [2]
     uint64_t* sempty = sfull + 2;            // [2]
     const int row0 = (b * 8 + h) * a.Lmax + p0;
     uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
     if (dbg && ltid() == 128) dbg[0] = globaltimer();
-    auto issue = [&](int i) {
-        const int s = i % kAttnStages;
-        char* dst = base + s * kAttnStageBytes;
-        const int r = row0 + i * kAttnChunk;
-        const uint64_t pol = tc::policy_evict_first();
-        tc::mbar_arrive_expect_tx(&full[s], kAttnStageBytes);
-        tc::tma_load_3d_hint(dst, &a.tmK, &full[s], 0, 0, r, pol);
-        tc::tma_load_3d_hint(dst + kAttnTile, &a.tmV, &full[s], 0, 0, r, pol);
+    auto issue_k = [&](int i) {
+        const int s = i % kAttnKSlots;
+        tc::mbar_arrive_expect_tx(&kfull[s], kAttnTile);
+        tc::tma_load_3d_hint(base + s * kAttnTile, &a.tmK, &kfull[s], 0, 0, row0 + i * kAttnChunk,
+                             tc::policy_evict_first());
+    };
+    auto issue_v = [&](int i) {
+        const int s = i % kAttnVSlots;
+        tc::mbar_arrive_expect_tx(&vfull[s], kAttnTile);
+        tc::tma_load_3d_hint(base + kAttnVOff + s * kAttnTile, &a.tmV, &vfull[s], 0, 0, row0 + i * kAttnChunk,
+                             tc::policy_evict_first());
     };
     if (ltid() == 0) {
-        for (int s = 0; s < kAttnStages; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 8);
+        for (int s = 0; s < kAttnKSlots; ++s) {
+            tc::mbar_init(&kfull[s], 1);
+            tc::mbar_init(&kempty[s], 4);  // the 4 QK warps
+        }
+        for (int s = 0; s < kAttnVSlots; ++s) {
+            tc::mbar_init(&vfull[s], 1);
+            tc::mbar_init(&vempty[s], 4);  // the 4 PV warps
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&sfull[b], 128);
@@ -410,13 +423,16 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     // preceding QKV launch appends position L-1 only), so their first stages
     // stream while that launch finishes; the chunk holding L-1 and the query
     // rows are read only after wait_prev (launch order + acquire).
-    int pre = 0;
     if (ltid() == 0) {
-        while (pre < min(kAttnStages, nch) && p0 + (pre + 1) * kAttnChunk <= a.L - 1) issue(pre++);
-    }
-    wait_prev(c);
-    if (ltid() == 0) {
-        for (int i = pre; i < min(kAttnStages, nch); ++i) issue(i);
+        auto immutable = [&](int i) { return p0 + (i + 1) * kAttnChunk <= a.L - 1; };
+        int pk = 0, pv = 0;
+        while (pk < min(kAttnKSlots, nch) && immutable(pk)) issue_k(pk++);
+        while (pv < min(kAttnVSlots, nch) && immutable(pv)) issue_v(pv++);
+        wait_prev(c);
+        for (int i = pk; i < min(kAttnKSlots, nch); ++i) issue_k(i);
+        for (int i = pv; i < min(kAttnVSlots, nch); ++i) issue_v(i);
+    } else {
+        wait_prev(c);
     }
     body_sync();
     const float scale = a.scale;
@@ -440,9 +456,9 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         }
         const int m4 = lane >> 3;
         for (int ci = 0; ci < nch; ++ci) {
-            const int s = ci % kAttnStages;
-            tc::mbar_wait(&full[s], (ci / kAttnStages) & 1);
-            const uint32_t kt = sbase + s * kAttnStageBytes;
+            const int s = ci % kAttnKSlots;
+            tc::mbar_wait(&kfull[s], (ci / kAttnKSlots) & 1);
+            const uint32_t kt = sbase + s * kAttnTile;
             const int valid = min(kAttnChunk, p1 - (p0 + ci * kAttnChunk));
             float sv[kQkNt][2];
 #pragma unroll
@@ -461,7 +477,13 @@ __device__ void body_attn_decode(const BodyCtx& c) {
                 sv[nt][1] = pc + 1 < valid ? (acc4[0][1] + acc4[1][1]) * scale : kNegInf;
             }
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&empty[s]);  // K of this slot consumed
+            if (lane == 0) tc::mbar_arrive(&kempty[s]);  // K of this slot consumed
+            // K refill by the QK side (warp 0 lane 0), as soon as all 4 QK warps
+            // released the slot
+            if (warp == 0 && lane == 0 && ci + kAttnKSlots < nch) {
+                tc::mbar_wait(&kempty[s], (ci / kAttnKSlots) & 1);
+                issue_k(ci + kAttnKSlots);
+            }
             const int sb = ci & 1;
             if (ci >= 2) tc::mbar_wait(&sempty[sb], ((ci - 2) >> 1) & 1);  // PV read chunk ci-2's S
             if (g < 4) {
@@ -484,9 +506,9 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             tc::tma_fence_desc(&a.tmV);
         }
         for (int ci = 0; ci < nch; ++ci) {
-            const int s = ci % kAttnStages;
-            tc::mbar_wait(&full[s], (ci / kAttnStages) & 1);
-            const uint32_t vt = sbase + s * kAttnStageBytes + kAttnTile;
+            const int s = ci % kAttnVSlots;
+            tc::mbar_wait(&vfull[s], (ci / kAttnVSlots) & 1);
+            const uint32_t vt = sbase + kAttnVOff + s * kAttnTile;
             const int sb = ci & 1;
             tc::mbar_wait(&sfull[sb], (ci >> 1) & 1);
             float pv[KS][4];  // [k-step][a0.x, a0.y, a2.x, a2.y]
@@ -540,12 +562,11 @@ __device__ void body_attn_decode(const BodyCtx& c) {
                 }
             }
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&empty[s]);  // V of this slot consumed
-            // refill by the last consumer (the PV side), so no QK warp ever
-            // waits for PV: QK runs ahead as far as data and S buffers allow
-            if (pw == 0 && lane == 0 && ci + kAttnStages < nch) {
-                tc::mbar_wait(&empty[s], (ci / kAttnStages) & 1);  // K and V of the slot consumed
-                issue(ci + kAttnStages);
+            if (lane == 0) tc::mbar_arrive(&vempty[s]);  // V of this slot consumed
+            // V refill by the PV side: no QK warp ever waits for PV
+            if (pw == 0 && lane == 0 && ci + kAttnVSlots < nch) {
+                tc::mbar_wait(&vempty[s], (ci / kAttnVSlots) & 1);
+                issue_v(ci + kAttnVSlots);
             }
         }
     }
@@ -611,7 +632,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     body_sync();
     if (dbg && ltid() == 128) dbg[6] = globaltimer();
     if (ltid() == 0)
-        for (int s = 0; s < 2 * kAttnStages + 4; ++s) tc::mbar_inval(&full[s]);
+        for (int s = 0; s < 2 * (kAttnKSlots + kAttnVSlots) + 4; ++s) tc::mbar_inval(&kfull[s]);
 }
 
 }  // namespace ds
