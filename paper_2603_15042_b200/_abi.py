@@ -158,7 +158,8 @@ class GemmArgs(ctypes.Structure):
     """C[M,N] bf16 = A[M,K] . B[N,K]^T (csrc/bodies/gemm_tc.cuh)."""
     _fields_ = [("tmA", TmaDesc), ("tmB", TmaDesc), ("C", ctypes.c_uint64), ("M", ctypes.c_int32),
                 ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32),
-                ("splits", ctypes.c_int32), ("ws", ctypes.c_uint64), ("bk", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("splits", ctypes.c_int32), ("ws", ctypes.c_uint64), ("bk", ctypes.c_int32),
+                ("tma_store", ctypes.c_int32), ("pad2", ctypes.c_uint8 * 16), ("tmC", TmaDesc)]  # tmC: alignas(64)
 
 
 class SplitkReduceArgs(ctypes.Structure):
@@ -182,7 +183,7 @@ GEMM_BM, GEMM_BN = 128, 256
 
 
 def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16, bn: int = GEMM_BN,
-              splits: int = 1, ws: int = 0, bk: int = 64) -> "GemmArgs":
+              splits: int = 1, ws: int = 0, bk: int = 64, tma_store: bool = True) -> "GemmArgs":
     if bn not in (64, 128, 256):
         raise DsError(10, f"gemm tile width {bn} not in (64, 128, 256)")
     if M % GEMM_BM or N % bn or K % 64:
@@ -191,8 +192,11 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
         raise DsError(10, "split-K needs a workspace and <= K/64 splits")
     if bk not in (64, 32) or (bk == 32 and bn != 256):
         raise DsError(10, "bk 32 (SWIZZLE_64B, 4 stages) is built for 128x256 tiles only")
-    return GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM, bk), tensor_map_bf16(B, N, K, bn, bk), C, M, N, K, group_m, bn,
-                    max(1, splits), ws, bk, 0)
+    tmC = tensor_map_bf16(C, M, N, GEMM_BM, 64) if tma_store else TmaDesc()
+    a = GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM, bk), tensor_map_bf16(B, N, K, bn, bk), C, M, N, K, group_m, bn,
+                 max(1, splits), ws, bk, int(tma_store))
+    a.tmC = tmC
+    return a
 
 
 def gemm_grid(M: int, N: int, bn: int = GEMM_BN, splits: int = 1):

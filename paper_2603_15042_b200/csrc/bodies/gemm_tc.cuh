@@ -161,8 +161,10 @@ struct GemmArgs {
     int32_t splits;  // split-K factor S (0/1 = none)
     uint64_t ws;     // fp32 [tiles][S][128][BN] when S > 1
     int32_t bk;      // 0 or 64: SWIZZLE_128B K blocks of 64; 32: SWIZZLE_64B K blocks of 32 (4-stage ring)
-    int32_t pad;
+    int32_t tma_store;  // 1: epilogue stages the bf16 tile in smem and writes it with TMA stores (tmC)
+    TmaDesc tmC;        // C [M][N] bf16, box {64, 128}, SWIZZLE_128B
 };
+static_assert(offsetof(GemmArgs, tmC) == 320 && sizeof(GemmArgs) == 448, "GemmArgs layout (mirrored in _abi.py)");
 
 constexpr int kGemmBN = 256;
 constexpr int kGemmStages = kCtasPerSm == 2 ? 2 : 4;
@@ -191,7 +193,39 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
     const int kb0 = (int)((int64_t)sp * kbs / S), kb1 = (int)((int64_t)(sp + 1) * kbs / S);
     tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb0, kb1, c.tmem_base, false);
     const int warp = ltid() >> 5, lane = ltid() & 31;
-    if (warp >= 4) {
+    if (warp >= 4 && S == 1 && a.tma_store) {
+        // bf16 tile staged in the (consumed) ring as BN/64 SWIZZLE_128B
+        // [128 rows][64 cols] sub-tiles (conflict-free 16-B chunk writes),
+        // then one thread issues BN/64 bulk tensor stores
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+            uint32_t v[32];
+            tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, v);
+            tc::tmem_ld_wait();
+            char* sub = base + (ch >> 1) * 16384 + r * 128;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint4 o;
+                o.x = pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                o.y = pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                o.z = pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                o.w = pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                const int chunk = (ch & 1) * 4 + j;
+                *reinterpret_cast<uint4*>(sub + ((chunk ^ (r & 7)) << 4)) = o;
+            }
+        }
+        tc::fence_proxy_async();  // generic smem writes -> async proxy
+        epi_sync();
+        if (q == 0 && lane == 0) {
+            for (int sub = 0; sub < BN / 64; ++sub)
+                tc::tma_store_2d(&a.tmC, base + sub * 16384, n_blk * BN + sub * 64, m_blk * kTcBM);
+            tc::bulk_commit();
+            tc::bulk_wait_all();  // global writes complete before the block retires
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+    } else if (warp >= 4) {
         const int q = warp & 3;
         if (S == 1) {
             const int row = m_blk * kTcBM + q * 32 + lane;
