@@ -321,7 +321,7 @@ def plan_gemm(M: int, N: int, K: int, workers: int = WORKERS):
     tiles = (Mp // 128) * (Np // bn)
     splits = 1
     if tiles < workers:
-        splits = max(1, min(64, -(-workers // tiles), (Kp // 64) // 8))
+        splits = max(1, min(256, -(-workers // tiles), (Kp // 64) // 8))
     return Mp, Np, Kp, bn, splits
 
 
@@ -335,6 +335,13 @@ class ResNetStream:
         self.gemms = resnet50_gemms(batch, image)
         self.batch = batch
         self.flops = sum(2.0 * M * N * K for _, M, N, K in self.gemms)  # algorithmic (unpadded)
+        # each GEMM may run as C or C^T (operands swapped): take the
+        # orientation with the smaller padded output (e.g. weight gradients
+        # with 64 output channels would waste half of every 128-row tile)
+        def orient(M, N):
+            pad = lambda m, n: _round(m, 128) * _round(n, 64)  # noqa: E731
+            return (N, M) if pad(N, M) < pad(M, N) else (M, N)
+        self.gemms = [(name,) + orient(M, N) + (K,) for name, M, N, K in self.gemms]
         plans = [plan_gemm(M, N, K) for _, M, N, K in self.gemms]
         self.padded_flops = sum(2.0 * Mp * Np * Kp for Mp, Np, Kp, _, _ in plans)
         a_el = max(Mp * Kp for Mp, Np, Kp, _, _ in plans)
