@@ -469,6 +469,27 @@ def cpu_baseline_leg(solo, requests, tokens, budget_s=10.0):
                       f"calibrated with measured solo durations; {ev} events in {wall:.2f} s wall"}
 
 
+def config4_leg(co, args, solo):
+    """Config 4: the ResNet-50-shaped training stream co-located with bursty
+    decode requests (gen_burst arrivals), TPOT-First vs time slicing."""
+    from paper_2603_15042_b200 import workload as wl
+    res_ms = co.add_resnet()
+    unit_ms = 50.0
+    reqs = wl.gen_burst(0.5, 4.0, 2.0, 20.0, args.burst_units, wl.RequestTemplate(output_tokens=4), seed=0)
+    arrivals = [int(r.arrival_q * unit_ms * 1e-3) for r in reqs]  # arrival_q = round(t*1e9) -> ns
+    step_ns = int(solo["decode_step_ms"] * 1e6)
+    log(f"config 4: {len(arrivals)} bursty requests, resnet solo iter {res_ms:.2f} ms")
+    c4 = {p: co.run_bursty(p, arrivals, 4, step_ns, quantum_ms=args.quantum_ms) for p in ("tpot-first", "temporal")}
+    return {"workload": "config 4: ResNet-50-shaped training stream (53 convs + FC, fwd/dgrad/wgrad = 161 "
+                        "tcgen05 GEMMs + split-K folds per iteration, batch 128, 224^2, bf16) co-located with "
+                        "bursty decode requests (4 tokens each)",
+            "arrivals": f"gen_burst(base 0.5, burst 4.0, burst_duration 2, period 20, duration "
+                        f"{args.burst_units}) x {unit_ms} ms/unit (trace.cpp:204-232), seed 0",
+            "resnet_solo_iter_ms": round(res_ms, 3),
+            "resnet_solo_images_per_s": round(co.resnet.batch / (res_ms * 1e-3), 1),
+            "tpot_first": c4["tpot-first"], "temporal": c4["temporal"]}
+
+
 def gpu_arm(args, rank, world):
     import torch
     dev = int(os.environ.get("LOCAL_RANK", rank))
@@ -486,22 +507,10 @@ def gpu_arm(args, rank, world):
     exact = co.bit_exact_check()
     config4 = None
     if not args.no_config4:
-        from paper_2603_15042_b200 import workload as wl
-        res_ms = co.add_resnet()
-        unit_ms = 50.0
-        reqs = wl.gen_burst(0.5, 4.0, 2.0, 20.0, args.burst_units, wl.RequestTemplate(output_tokens=4), seed=0)
-        arrivals = [int(r.arrival_q * unit_ms * 1e-3) for r in reqs]  # arrival_q = round(t*1e9) -> ns
-        step_ns = int(solo["decode_step_ms"] * 1e6)
-        log(f"config 4: {len(arrivals)} bursty requests, resnet solo iter {res_ms:.2f} ms")
-        c4 = {p: co.run_bursty(p, arrivals, 4, step_ns, quantum_ms=args.quantum_ms) for p in ("tpot-first", "temporal")}
-        config4 = {"workload": "config 4: ResNet-50-shaped training stream (53 convs + FC, fwd/dgrad/wgrad = 161 "
-                               "tcgen05 GEMMs + split-K folds per iteration, batch 128, 224^2, bf16) co-located with "
-                               "bursty decode requests (4 tokens each)",
-                   "arrivals": f"gen_burst(base 0.5, burst 4.0, burst_duration 2, period 20, duration "
-                               f"{args.burst_units}) x {unit_ms} ms/unit (trace.cpp:204-232), seed 0",
-                   "resnet_solo_iter_ms": round(res_ms, 3),
-                   "resnet_solo_images_per_s": round(co.resnet.batch / (res_ms * 1e-3), 1),
-                   "tpot_first": c4["tpot-first"], "temporal": c4["temporal"]}
+        try:
+            config4 = config4_leg(co, args, solo)
+        except Exception as e:  # an auxiliary leg must not cost the headline line
+            config4 = {"error": repr(e)}
     co.close()
     p99 = nearest_rank(sp["tpot_ms"], 99)
     p99_tm = nearest_rank(tm["tpot_ms"], 99)
@@ -669,11 +678,13 @@ def config5_leg(args, rank, world, dev, gather_fn):
     mix = config5_mix()
     where = place(mix, world, mem_cap_gb=150.0)
     mine = [mix[i] for i, d in enumerate(where) if d == rank]
+    # the only collective of the leg (IPC handle exchange) comes first, before
+    # any large allocation that could fail on one rank
+    dpg = dp.DpGroup(dev, 4096 * 4096, rank, world, gather_fn)
     dec = [(spec, DecodeModel(DecodeConfig(L=args.kv_len, layers=spec.size), device=f"cuda:{dev}", seed=i))
            for i, spec in enumerate(mine) if spec.kind == "decode"]
     trn = [(spec, TrainGemm(M=spec.size, N=spec.size, K=spec.size, device=f"cuda:{dev}", seed=i))
            for i, spec in enumerate(mine) if spec.kind == "train"]
-    dpg = dp.DpGroup(dev, 4096 * 4096, rank, world, gather_fn)
     dp_gemm = TrainGemm(M=4096, N=4096, K=4096, device=f"cuda:{dev}", seed=99)
     dp_gemm.args = _abi.gemm_args(dp_gemm.A.data_ptr(), dp_gemm.B.data_ptr(), dpg.grad, 4096, 4096, 4096)
     torch.cuda.synchronize()
@@ -858,8 +869,11 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if world > 1:
+        import datetime
         import torch.distributed as dist
-        dist.init_process_group("gloo")
+        # host-side plumbing only (line aggregation, DP handle exchange); a
+        # bounded timeout so a failed rank cannot hang the others forever
+        dist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
     if args.impl == "reference":
         if rank != 0:
             return
@@ -905,7 +919,14 @@ def main():
         torch.cuda.empty_cache()
         dev = int(os.environ.get("LOCAL_RANK", rank))
         log("config 1 and 3 legs")
-        c1, c3 = config1_leg(dev), config3_leg(dev)
+        try:
+            c1 = config1_leg(dev)
+        except Exception as e:  # an auxiliary leg must not cost the headline line
+            c1 = {"error": repr(e)}
+        try:
+            c3 = config3_leg(dev)
+        except Exception as e:
+            c3 = {"error": repr(e)}
         if rank == 0:
             out["config1"], out["config3"] = c1, c3
     if not args.no_config5:
@@ -922,8 +943,13 @@ def main():
             return res
 
         log("config 5 leg")
-        part = config5_leg(args, rank, world, dev, gather)
-        c5 = aggregate_config5(gather(part))
+        try:
+            part = config5_leg(args, rank, world, dev, gather)
+        except Exception as e:
+            part = {"rank": rank, "error": repr(e)}
+        parts = gather(part)
+        errors = [p["error"] for p in parts if "error" in p]
+        c5 = {"error": errors} if errors else aggregate_config5(parts)
         if rank == 0:
             out["config5"] = c5
     if rank == 0:
