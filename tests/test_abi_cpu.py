@@ -65,3 +65,20 @@ def test_invalid_tier_rejected_before_device():
     h = ctypes.c_void_p()
     rc = _abi.lib().ds_domain_create(ctypes.byref(cfg), ctypes.byref(h))
     assert rc in (1, 101)
+
+
+def test_plain_c_caller_links_and_runs(tmp_path):
+    """The C ABI from C (examples/ds_cabi_demo.c): header + library only."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "ds_demo"
+    libdir = os.path.join(root, "paper_2603_15042_b200")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I" + os.path.join(root, "include"),
+                    os.path.join(root, "examples", "ds_cabi_demo.c"), "-L" + libdir, "-ldetshare",
+                    "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines()
+    n = int(out[0].split()[1])
+    assert n > 0 and "kernels" in out[0]
+    where = [int(x) for x in out[1].split()[1:]]
+    assert sorted(set(where)) == list(range(8))
+    assert out[2].split("-> ")[1] in ("InvalidTier", "NoDevice")
