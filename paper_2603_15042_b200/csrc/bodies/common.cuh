@@ -78,11 +78,20 @@ __device__ __forceinline__ void st_release_sys_u64(void* p, uint64_t v) {
 }
 
 // Wait until every earlier launch of this tenant has completed (acquire).
+// Single-thread form (the caller alone polls); see wait_prev_all.
 __device__ __forceinline__ void wait_prev(const BodyCtx& c) {
     if (!c.prev_head) return;
     // gpu-scope acquire: later loads (incl. L1) observe every write the
     // completed launches released through their retire atomics
     while (ld_acquire_u32(c.prev_head) < c.seq) __nanosleep(32);
+}
+
+// All 256 body threads: one thread polls, the lane barrier carries its
+// acquire to the others (so ~300 lanes x 256 threads never hammer one word).
+__device__ __forceinline__ void wait_prev_all(const BodyCtx& c) {
+    if (!c.prev_head) return;
+    if (ltid() == 0) wait_prev(c);
+    body_sync();
 }
 
 }  // namespace ds

@@ -69,7 +69,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     cd.dbg = dbg;
     tc_mainloop<kGemvBN, kGemvStages>(base, &a.tmW, &a.tmX, n_blk * kTcBM, 0, kb0, kb1, c.tmem_base, true,
                                       reinterpret_cast<const char*>(a.w_packed), KB, &cd);
-    wait_prev(c);  // the epilogue reads residual / norm statistics of earlier launches
+    wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
     const int warp = ltid() >> 5, lane = ltid() & 31;
     float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + rvec[32] + flag
@@ -431,10 +431,8 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         wait_prev(c);
         for (int i = pk; i < min(kAttnKSlots, nch); ++i) issue_k(i);
         for (int i = pv; i < min(kAttnVSlots, nch); ++i) issue_v(i);
-    } else {
-        wait_prev(c);
     }
-    body_sync();
+    body_sync();  // carries thread 0's acquire (wait_prev) to the whole lane
     const float scale = a.scale;
     float m = kNegInf, lsum = 0.f;
     float o[4][4];

@@ -42,7 +42,7 @@ __device__ __forceinline__ bool early_start_body(int body) {
 }
 
 __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
-    if (!early_start_body(body)) wait_prev(c);
+    if (!early_start_body(body)) wait_prev_all(c);
     switch (body) {
         case DS_BODY_REDUCE_CHUNKS: body_reduce(c); break;
         case DS_BODY_SGEMM: body_sgemm(c); break;
