@@ -435,8 +435,10 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
         bool got = false, exit_now = false;
         if (lane == 0) {
             for (;;) {
-                if (ld_volatile_u32(&st->ctl.exit)) { exit_now = true; break; }
+                // both words requested before either is used: one L2 round trip
+                const uint32_t ex = ld_volatile_u32(&st->ctl.exit);
                 const unsigned long long cw = ld_volatile_u64(&st->ctl.word[sm]);
+                if (ex) { exit_now = true; break; }
                 const int32_t ow = (int32_t)(uint32_t)cw;
                 const int32_t ln = (int32_t)(uint32_t)(cw >> 32);
                 if (ow >= 0 && ow < DS_MAX_TENANTS && try_claim(st, ow, w, cc)) { got = true; break; }
