@@ -691,7 +691,8 @@ __device__ void body_argmax(const BodyCtx& c) {
     // 16-B vector body over the 8-aligned interior, scalar edges
     const int va = (v0 + 7) & ~7, vb = v1 & ~7;
     for (int v = v0 + (int)ltid(); v < min(va, v1); v += kBodyThreads) amax_merge(best, idx, bf16_to_f(row[v]), v);
-    for (int v = va + 8 * (int)ltid(); v < vb; v += 8 * kBodyThreads) {
+#pragma unroll 4
+    for (int v = va + 8 * (int)ltid(); v < vb; v += 8 * kBodyThreads) {  // 4 loads in flight per thread
         uint4 q = __ldcs(reinterpret_cast<const uint4*>(row + v));
         uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll

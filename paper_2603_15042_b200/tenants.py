@@ -187,7 +187,7 @@ class DecodeModel:
         a, g = self._gemv(self.lm, hfin, c.vocab, c.d, self.S["lm"], _abi.GEMV_STORE, self.logits,
                           stats_in=self.st_h, P_in=c.d // 128)
         self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
-        chunks = max(1, min(16, c.vocab // 2048))
+        chunks = max(1, min(4, c.vocab // 2048))  # 128 blocks: one wave; every block pays a claim + ticket
         am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), self.amax_ws.data_ptr(),
                              self.amax_counters.data_ptr(), c.vocab, chunks)
         self.records.append(("decode/argmax", _abi.BODY_ARGMAX, (32 * chunks, 1, 1), am, 32 * c.vocab * 2))
