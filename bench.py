@@ -1,7 +1,7 @@
 """Benchmark: BASELINE config 2 on B200 — two tenants on one GPU.
 
   decode tenant  : Llama-3-8B-shaped decode step, batch 32, KV length 1024,
-                   bf16, 164 launches/step (HBM-bound; tcgen05 swap-AB GEMV)
+                   bf16, 163 launches/step (HBM-bound; tcgen05 swap-AB GEMV)
   training tenant: bf16 GEMM 8192^3 per iteration on tcgen05/TMEM
 
 A *step* = one decode request of T tokens arriving while the training tenant
@@ -446,7 +446,7 @@ def reference_sim(solo, requests, tokens, policy="tpot-first", scale=1, slo_x=8.
           "segments_per_kernel": 16, "event_budget": 100000000,
           "profiles": {"inference": {"default": {"decode_cost": str(step_us), "prefill_cost_per_token": "1",
                                                  "decode_saturation": "0.75", "decode_mem_bound": "0.8",
-                                                 "decode_bw_demand": "0.75", "decode_grid": 164}},
+                                                 "decode_bw_demand": "0.75", "decode_grid": 163}},
                        "training": {"gemm": {"iteration_cost": str(gemm_us), "saturation": "0.25",
                                              "mem_bound": "0.1", "bw_demand": "0.25", "grid": 2048}}},
           "workload": {"records": recs}}

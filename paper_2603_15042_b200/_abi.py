@@ -242,7 +242,7 @@ class AttnArgs(ctypes.Structure):
 
 class EmbedArgs(ctypes.Structure):
     _fields_ = [("table", ctypes.c_uint64), ("tokens", ctypes.c_uint64), ("h", ctypes.c_uint64),
-                ("d", ctypes.c_int32), ("vocab", ctypes.c_int32)]
+                ("d", ctypes.c_int32), ("vocab", ctypes.c_int32), ("stats", ctypes.c_uint64)]
 
 
 class ArgmaxArgs(ctypes.Structure):

@@ -645,6 +645,8 @@ struct EmbedArgs {
     uint64_t tokens;  // int32 [32]
     uint64_t h;       // bf16 [32][d]
     int32_t d, vocab;
+    uint64_t stats;   // fp32 [1][32]: sum of squares of each gathered row (0 = skip); bitwise what
+                      // DS_BODY_RMSNORM computes over the written row, one launch fewer per step
 };
 
 __device__ void body_embed(const BodyCtx& c) {
@@ -654,7 +656,32 @@ __device__ void body_embed(const BodyCtx& c) {
     tok = tok < 0 ? 0 : (tok >= a.vocab ? a.vocab - 1 : tok);
     const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.table) + (size_t)tok * a.d);
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.h) + (size_t)b * a.d);
-    for (int i = ltid(); i < a.d / 8; i += kBodyThreads) dst[i] = __ldcs(src + i);
+    float ss = 0.f;
+    for (int i = ltid(); i < a.d / 8; i += kBodyThreads) {
+        const uint4 v = __ldcs(src + i);
+        dst[i] = v;
+        // same per-thread order, tree and partial sum as body_rmsnorm
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float lo = __uint_as_float(w[j] << 16), hi = __uint_as_float(w[j] & 0xffff0000u);
+            ss += lo * lo + hi * hi;
+        }
+    }
+    if (a.stats) {
+        const int warp = ltid() >> 5, lane = ltid() & 31;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        __shared__ float epart_l[2][8];
+        float* part = epart_l[body_lane()];
+        if (lane == 0) part[warp] = ss;
+        body_sync();
+        if (ltid() == 0) {
+            float t = 0.f;
+            for (int w = 0; w < 8; ++w) t += part[w];
+            reinterpret_cast<float*>(a.stats)[b] = t;
+        }
+    }
     body_sync();
 }
 

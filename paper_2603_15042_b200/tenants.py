@@ -3,7 +3,8 @@
 * ``DecodeModel`` — Llama-3-8B-shaped decode step, batch 32 (config 2): per
   layer RMSNorm-folded QKV projection (+ KV-cache append), GQA attention,
   O projection (+ residual), gate/up projection (+ SiLU*up), down projection
-  (+ residual); final norm + LM head.  162 launches per decode step.
+  (+ residual); final norm + LM head + argmax.  163 launches per decode step
+  (embed with the RMS statistics of its rows, 5 per layer, LM head, argmax).
 * ``TrainGemm`` — bf16 GEMM 8192^3 training step on tcgen05 (config 2).
 
 Weights are random (synthetic data, no checkpoints); shapes are exactly the
@@ -157,10 +158,10 @@ class DecodeModel:
         c = self.cfg
         self.records = []  # (semantic_id, body, grid, args, bytes)
         self._packed = []  # pre-packed weights (the copies the GEMV bodies stream)
-        ea = _abi.EmbedArgs(self.embed.data_ptr(), self.tokens.data_ptr(), self.H[0].data_ptr(), c.d, c.vocab)
+        # token gather + the input rows' RMS statistics in one launch
+        ea = _abi.EmbedArgs(self.embed.data_ptr(), self.tokens.data_ptr(), self.H[0].data_ptr(), c.d, c.vocab,
+                            self.st0.data_ptr())
         self.records.append(("decode/embed", _abi.BODY_EMBED, (32, 1, 1), ea, 32 * c.d * 2 * 2))
-        ra = _abi.RmsArgs(self.H[0].data_ptr(), self.st0.data_ptr(), c.d, 0)
-        self.records.append(("decode/rms0", _abi.BODY_RMSNORM, (32, 1, 1), ra, 32 * c.d * 2))
         for l in range(c.layers):
             hin, hout = self.H[l % 2], self.H[(l + 1) % 2]
             st_in, p_in = (self.st0, 1) if l == 0 else (self.st_h, c.d // 128)

@@ -1,7 +1,7 @@
 """Solo (plain grid) launches of the tenant bodies for ncu.
 
   python scripts/profile_solo.py gemm        # bf16 GEMM 8192^3 x3
-  python scripts/profile_solo.py decode      # one full decode step (164 launches) x2
+  python scripts/profile_solo.py decode      # one full decode step (163 launches) x2
   python scripts/profile_solo.py gate_up|attn|qkv|lm_head   # that decode kernel x3
 """
 import os, sys
