@@ -299,9 +299,9 @@ __device__ void body_rmsnorm(const BodyCtx& c) {
 
 // ---------------------------------------------------------------------------
 // GQA decode attention (32 q heads, 8 kv heads, d = 128, batch 32) over a
-// KV cache of L positions.  Logical block t -> (b, kv head h, split sp).
-// 8 warps stride over the split's positions with an online softmax per warp;
-// warps merge in order 0..7, splits merge in order 0..S-1 (last block).
+// KV cache of L positions.  Logical block t -> (b, kv head h, split sp)
+// (the decode tenant uses S = 1: one block per (b, h)); with S > 1 the
+// splits' (m, l, O) merge in order 0..S-1 in the block that retires last.
 // ---------------------------------------------------------------------------
 struct AttnArgs {
     TmaDesc tmK;        // K cache rows as a {64, 2, rows} view, box {64, 2, 32}: 8 KB contiguous, SWIZZLE_128B
@@ -356,17 +356,15 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
 }
 
 // GQA decode attention on tensor cores, warp-specialised.  K/V chunks of 64
-// positions arrive by TMA (SWIZZLE_128B, one contiguous 16-KB box each).
+// positions arrive by TMA (SWIZZLE_128B, one contiguous 16-KB box each) into
+// separate K and V rings.
 //   warps 0-3 (QK):  S = Q.K^T for 16 positions each (M = 16 rows, the kv
 //                    group's 4 query heads real; K = 128 dims, 8 mma k-steps)
 //   warps 4-7 (PV):  softmax over the chunk (one rescale per chunk) and
 //                    O += P.V for 32 dims each (P reused from registers as A)
-// S is handed over through smem with a FULL/EMPTY named-barrier pair, so QK
-// of chunk i+1 overlaps softmax/PV of chunk i.  Deterministic: fixed chunk
+// S is handed over through two smem buffers with FULL/EMPTY mbarriers, so QK
+// runs up to two chunks ahead of softmax/PV.  Deterministic: fixed chunk
 // order, fixed reduction trees.
-__device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 256;" ::"r"(id) : "memory"); }
-
 __device__ void body_attn_decode(const BodyCtx& c) {
     const AttnArgs& a = *reinterpret_cast<const AttnArgs*>(c.args);
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
