@@ -42,12 +42,13 @@ with Domain(0, block_log_capacity=0) as dom:
         s = dom.launch(t, kid)
     dom.wait(t, s)
     dom.poll()
-    n = 10
+    n = int(os.environ.get("ITERS", "10"))
     for i in range(n):
         s = dom.launch(t, kid)
     dom.wait(t, s)
     cs = dom.poll()
     t0 = min(c.t_first_claim for c in cs); t1 = max(c.t_end for c in cs)
     per = [(c.t_end - c.t_first_claim) / 1e6 for c in cs]
-    print(json.dumps({"coroutine_ms_per_gemm": (t1 - t0) / 1e6 / n, "coroutine_tflops": flop * n / ((t1 - t0) * 1e-9) / 1e12,
+    import statistics as _st
+    print(json.dumps({"sustained_median_ms": _st.median(per[n // 2:]), "coroutine_ms_per_gemm": (t1 - t0) / 1e6 / n, "coroutine_tflops": flop * n / ((t1 - t0) * 1e-9) / 1e12,
                       "per_launch_ms": per[:4], "sms_used": [c.sms_used for c in cs[:3]]}))
