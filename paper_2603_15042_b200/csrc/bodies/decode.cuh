@@ -38,11 +38,14 @@ struct GemvArgs {
     int32_t Lmax;
     int32_t q_dim, kv_dim;
     uint64_t dbg;       // optional phase timestamps [grid][8] (0 = off)
-    uint64_t w_packed;  // W pre-packed as SWIZZLE_128B [N/128][K/64][128][64] tiles (0 = use tmW)
+    uint64_t w_packed;  // W pre-packed as SWIZZLE_128B [N/BM][K/64][BM][64] tiles (0 = use tmW)
+    int32_t bm;         // slab rows: 128 (0) or 64 (not for kGemvSiluMul)
+    int32_t pad2;
 };
 
 constexpr int kGemvBN = 32;
-constexpr int kGemvStages = kCtasPerSm == 2 ? 5 : 8;
+constexpr int kGemvStages = kCtasPerSm == 2 ? 5 : 8;     // 20-KB stages (128-row W tile + X)
+constexpr int kGemvStages64 = kCtasPerSm == 2 ? 8 : 12;  // 12-KB stages (64-row W tile + X)
 // epilogue scratch [128][33] fp32 + rvec/flag reuses the TMA ring: every
 // stage has been consumed once the accumulator is complete
 constexpr uint32_t kGemvScratch = 0;
@@ -55,10 +58,14 @@ __device__ __forceinline__ uint16_t f_to_bf16(float f) {
 }
 
 
-__device__ void body_gemv_bf16(const BodyCtx& c) {
-    const GemvArgs& a = *reinterpret_cast<const GemvArgs*>(c.args);
+// BM = 128 or 64 weight rows per slab (M = 64: smaller blocks for the small
+// projections; rows 16q..16q+15 sit in TMEM lanes 32q.. of epilogue warp q).
+template <int BM, int STAGES>
+__device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
+    constexpr int QR = BM / 4;            // slab rows per epilogue warp
+    constexpr int FJ = BM * 8 / kBodyThreads;  // float4 per thread over a [BM][32] block
     char* base = align1024(c.smem);
-    const int nb = a.N / kTcBM;
+    const int nb = a.N / BM;
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
     const int n_blk = t % nb, s = t / nb;
     const int KB = a.K / kTcBK;
@@ -67,16 +74,17 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     if (dbg && ltid() == 0) dbg[0] = globaltimer();
     BodyCtx cd = c;
     cd.dbg = dbg;
-    tc_mainloop<kGemvBN, kGemvStages>(base, &a.tmW, &a.tmX, n_blk * kTcBM, 0, kb0, kb1, c.tmem_base, true,
-                                      reinterpret_cast<const char*>(a.w_packed), KB, &cd);
+    tc_mainloop<kGemvBN, STAGES, kTcBK, BM>(base, &a.tmW, &a.tmX, n_blk * BM, 0, kb0, kb1, c.tmem_base, true,
+                                             reinterpret_cast<const char*>(a.w_packed), KB, &cd);
     wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
     const int warp = ltid() >> 5, lane = ltid() & 31;
     float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + rvec[32] + flag
     float* rvec = scratch + 128 * 33;
     const int q = warp & 3;
-    const int row = q * 32 + lane;  // epilogue warps: row within the slab
-    const int n = n_blk * kTcBM + row;
+    const bool active = lane < QR;  // lanes holding a slab row (all of them at BM = 128)
+    const int row = q * QR + lane;  // epilogue warps: row within the slab
+    const int n = n_blk * BM + row;
     // Split-K: split S-1 of each slab is its combiner (claimed after every
     // other split of every slab: claims follow the logical index, so it never
     // waits on an unclaimed block).  The other splits store their partial and
@@ -109,7 +117,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
     if (a.S > 1) {
         uint32_t* ctr = reinterpret_cast<uint32_t*>(a.counters) + n_blk;
         if (!combiner) {
-            if (warp >= 4) {
+            if (warp >= 4 && active) {
                 float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.ws) + ((size_t)s * a.N + n) * 32);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -117,7 +125,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
             body_sync();  // orders the CTA's partial stores before thread 0's release
             if (ltid() == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
         } else {
-            if (warp >= 4) {
+            if (warp >= 4 && active) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) own[row * 8 + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
@@ -131,23 +139,23 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
             // of the slab's [128 rows][32] block; partials summed in the fixed
             // order s = 0..S-1
             const float4* wsb = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.ws) +
-                                                                (size_t)n_blk * kTcBM * 32);
+                                                                (size_t)n_blk * BM * 32);
             const size_t sstride4 = (size_t)a.N * 8;
-            float4 acc[4];
+            float4 acc[FJ];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < FJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 3
             for (int sp = 0; sp < a.S; ++sp) {
-                float4 x[4];
+                float4 x[FJ];
                 if (sp < a.S - 1) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) x[j] = __ldcg(wsb + sp * sstride4 + ltid() + 256 * j);
+                    for (int j = 0; j < FJ; ++j) x[j] = __ldcg(wsb + sp * sstride4 + ltid() + 256 * j);
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) x[j] = own[ltid() + 256 * j];
+                    for (int j = 0; j < FJ; ++j) x[j] = own[ltid() + 256 * j];
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < FJ; ++j) {
                     acc[j].x += x[j].x;
                     acc[j].y += x[j].y;
                     acc[j].z += x[j].z;
@@ -156,7 +164,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
             }
             body_sync();  // every thread's TMEM-side reads of the stats scratch are done
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < FJ; ++j) {
                 const int f = ltid() + 256 * j;
                 float* dst = scratch + (f >> 3) * 33 + (f & 7) * 4;
                 dst[0] = acc[j].x;
@@ -165,7 +173,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
                 dst[3] = acc[j].w;
             }
             body_sync();
-            if (warp >= 4) {
+            if (warp >= 4 && active) {
 #pragma unroll
                 for (int b = 0; b < 32; ++b) v[b] = scratch[row * 33 + b];
             }
@@ -191,34 +199,38 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
             if (dbg && ltid() == 128) dbg[4] = globaltimer();
             if (a.mode == kGemvStore) {
                 uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
+                if (active) {
 #pragma unroll
-                for (int b = 0; b < 32; ++b) out[(size_t)b * a.N + n] = f_to_bf16(v[b]);
+                    for (int b = 0; b < 32; ++b) out[(size_t)b * a.N + n] = f_to_bf16(v[b]);
+                }
             } else if (a.mode == kGemvResid) {
                 const uint16_t* __restrict__ res = reinterpret_cast<const uint16_t*>(a.resid);
                 uint16_t* __restrict__ out = reinterpret_cast<uint16_t*>(a.out);
-                uint16_t rv[32];  // all residual loads in flight before any store
+                if (active) {
+                    uint16_t rv[32];  // all residual loads in flight before any store
 #pragma unroll
-                for (int b = 0; b < 32; ++b) rv[b] = __ldcg(res + (size_t)b * a.N + n);
+                    for (int b = 0; b < 32; ++b) rv[b] = __ldcg(res + (size_t)b * a.N + n);
 #pragma unroll
-                for (int b = 0; b < 32; ++b) {
-                    const uint16_t hb = f_to_bf16(bf16_to_f(rv[b]) + v[b]);
-                    out[(size_t)b * a.N + n] = hb;
-                    const float hr = bf16_to_f(hb);
-                    scratch[row * 33 + b] = hr * hr;
+                    for (int b = 0; b < 32; ++b) {
+                        const uint16_t hb = f_to_bf16(bf16_to_f(rv[b]) + v[b]);
+                        out[(size_t)b * a.N + n] = hb;
+                        const float hr = bf16_to_f(hb);
+                        scratch[row * 33 + b] = hr * hr;
+                    }
                 }
                 epi_sync();
-                {  // fixed-order sum over the 128 rows: 4 quarter sums, then in order
+                {  // fixed-order sum over the slab's rows: 4 quarter sums, then in order
                     float* red = scratch + 128 * 33 + 64;
                     float ss = 0.f;
 #pragma unroll 8
-                    for (int r = q * 32; r < q * 32 + 32; ++r) ss += scratch[r * 33 + lane];
+                    for (int r = q * QR; r < q * QR + QR; ++r) ss += scratch[r * 33 + lane];
                     red[q * 32 + lane] = ss;
                     epi_sync();
                     if (warp == 4)
                         reinterpret_cast<float*>(a.stats_out)[n_blk * 32 + lane] =
                             ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
                 }
-            } else if (a.mode == kGemvSiluMul) {
+            } else if (a.mode == kGemvSiluMul && BM == 128) {
                 // slab rows [0,64) are gate features, [64,128) the matching up features
 #pragma unroll
                 for (int b = 0; b < 32; ++b) scratch[row * 33 + b] = v[b];
@@ -234,7 +246,7 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
                         out[(size_t)b * F + f] = f_to_bf16(act);
                     }
                 }
-            } else if (a.mode == kGemvQKV) {
+            } else if (a.mode == kGemvQKV && active) {
                 if (n < a.q_dim) {
                     uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
 #pragma unroll
@@ -253,8 +265,14 @@ __device__ void body_gemv_bf16(const BodyCtx& c) {
         }
     }
     if (dbg && ltid() == 128) dbg[5] = globaltimer();
-    tc_teardown<kGemvBN, kGemvStages>(base);
+    tc_teardown<kGemvBN, STAGES, kTcBK, BM>(base);
     if (dbg && ltid() == 0) dbg[6] = globaltimer();
+}
+
+__device__ void body_gemv_bf16(const BodyCtx& c) {
+    const GemvArgs& a = *reinterpret_cast<const GemvArgs*>(c.args);
+    if (a.bm == 64) gemv_body<64, kGemvStages64>(c, a);
+    else gemv_body<128, kGemvStages>(c, a);
 }
 
 // ---------------------------------------------------------------------------

@@ -23,9 +23,9 @@ struct alignas(64) TmaDesc {
 constexpr int kTcBM = 128;
 constexpr int kTcBK = 64;  // 64 bf16 = one 128-B swizzle row
 
-template <int BN, int STAGES, int BK = kTcBK>
+template <int BN, int STAGES, int BK = kTcBK, int BM = kTcBM>
 struct TcSmem {
-    static constexpr uint32_t kABytes = kTcBM * BK * 2;  // 16 KB at BK = 64
+    static constexpr uint32_t kABytes = BM * BK * 2;  // 16 KB at BM = 128, BK = 64
     static constexpr uint32_t kBBytes = BN * BK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
     static constexpr uint32_t kBarOff = STAGES * kStageBytes;
@@ -45,12 +45,14 @@ __device__ __forceinline__ char* align1024(char* p) {
 // bulk copy per stage instead of 128 strided row segments.
 // BK = 64: SWIZZLE_128B tiles (one 128-B row per K block); BK = 32:
 // SWIZZLE_64B tiles (half the bytes per stage, twice the stages in the same smem)
-template <int BN, int STAGES, int BK = kTcBK>
+// BM = 128 (default) or 64: with M = 64 the accumulator's rows 16q..16q+15
+// sit in TMEM lanes 32q..32q+15 (half sub-partitions).
+template <int BN, int STAGES, int BK = kTcBK, int BM = kTcBM>
 __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
                                             int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
                                             const char* a_packed = nullptr, int a_kblocks = 0,
                                             const BodyCtx* dep = nullptr) {
-    using L = TcSmem<BN, STAGES, BK>;
+    using L = TcSmem<BN, STAGES, BK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;
@@ -73,7 +75,7 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             const int s = i % STAGES;
             char* sa = base + s * L::kStageBytes;
             if (a_packed)
-                tc::bulk_g2s_hint(sa, a_packed + ((size_t)(a_row / kTcBM) * a_kblocks + kb_begin + i) * L::kABytes,
+                tc::bulk_g2s_hint(sa, a_packed + ((size_t)(a_row / BM) * a_kblocks + kb_begin + i) * L::kABytes,
                                   L::kABytes, &full[s], pol);
             else
                 tc::tma_load_2d_hint(sa, tmA, &full[s], (kb_begin + i) * BK, a_row, pol);
@@ -101,7 +103,7 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             issue_b(i);
         }
     } else if (warp == 1 && lane == 0) {
-        constexpr uint32_t idesc = tc::idesc_bf16_f32(kTcBM, BN);
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
         for (int i = 0; i < nkb; ++i) {
             const int s = i % STAGES;
             const uint32_t ph = (i / STAGES) & 1;
@@ -126,9 +128,9 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
     }
 }
 
-template <int BN, int STAGES, int BK = kTcBK>
+template <int BN, int STAGES, int BK = kTcBK, int BM = kTcBM>
 __device__ __forceinline__ void tc_teardown(char* base) {
-    using L = TcSmem<BN, STAGES, BK>;
+    using L = TcSmem<BN, STAGES, BK, BM>;
     tc::tc_fence_before();
     body_sync();
     if (ltid() == 0) {

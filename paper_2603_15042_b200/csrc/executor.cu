@@ -691,7 +691,11 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_SGEMM: return (32 * 68 + 32 * 64) * 4 + 1024;
         case DS_BODY_SPIN: return 1024;
         case DS_BODY_GEMM_BF16: return ds::TcSmem<ds::kGemmBN, ds::kGemmStages>::kBytes + 1024;
-        case DS_BODY_GEMV_BF16: return ds::TcSmem<ds::kGemvBN, ds::kGemvStages>::kBytes + 1024;
+        case DS_BODY_GEMV_BF16: {
+            const uint32_t a = ds::TcSmem<ds::kGemvBN, ds::kGemvStages>::kBytes;
+            const uint32_t b = ds::TcSmem<ds::kGemvBN, ds::kGemvStages64, ds::kTcBK, 64>::kBytes;
+            return (a > b ? a : b) + 1024;
+        }
         case DS_BODY_ATTN_DECODE: return ds::kAttnSmem + 1024;
         case DS_BODY_RMSNORM: return 1024;
         case DS_BODY_EMBED: return 1024;

@@ -41,17 +41,17 @@ def pick_split(nb: int, kblocks: int, sms: int = WORKERS, max_s: int = 16, min_k
     return min(s for s, e in effs.items() if e >= best - slack)
 
 
-def pack_sw128(W: torch.Tensor) -> torch.Tensor:
-    """[N, K] bf16 -> the SWIZZLE_128B shared-memory image of its [128 x 64]
-    tiles, tile (slab, kblock) contiguous at ((slab * K/64) + kblock) * 16 KB:
+def pack_sw128(W: torch.Tensor, bm: int = 128) -> torch.Tensor:
+    """[N, K] bf16 -> the SWIZZLE_128B shared-memory image of its [bm x 64]
+    tiles, tile (slab, kblock) contiguous at ((slab * K/64) + kblock) * bm*128 B:
     within a tile, row r's 16-B chunk c is stored at chunk c ^ (r % 8)
     (exactly what a TMA SWIZZLE_128B load would place in smem)."""
     N, K = W.shape
-    assert N % 128 == 0 and K % 64 == 0
-    t = W.reshape(N // 128, 128, K // 64, 8, 8).permute(0, 2, 1, 3, 4)  # [nb][kb][r][chunk][8]
-    r = torch.arange(128, device=W.device).view(128, 1)
+    assert N % bm == 0 and K % 64 == 0
+    t = W.reshape(N // bm, bm, K // 64, 8, 8).permute(0, 2, 1, 3, 4)  # [nb][kb][r][chunk][8]
+    r = torch.arange(bm, device=W.device).view(bm, 1)
     c = torch.arange(8, device=W.device).view(1, 8)
-    src = (c ^ (r % 8)).view(1, 1, 128, 8, 1).expand(t.shape[0], t.shape[1], 128, 8, 8)
+    src = (c ^ (r % 8)).view(1, 1, bm, 8, 1).expand(t.shape[0], t.shape[1], bm, 8, 8)
     return torch.gather(t, 3, src).contiguous()
 
 
@@ -70,7 +70,8 @@ class DecodeConfig:
 
 
 class DecodeModel:
-    def __init__(self, cfg: DecodeConfig = DecodeConfig(), device="cuda", seed: int = 0, split_override: str = ""):
+    def __init__(self, cfg: DecodeConfig = DecodeConfig(), device="cuda", seed: int = 0, split_override: str = "",
+                 bm_override: str = ""):
         assert cfg.batch == 32 and cfg.d == cfg.n_q * 128 and cfg.n_q == 4 * cfg.n_kv
         self.cfg = cfg
         c = cfg
@@ -101,8 +102,8 @@ class DecodeModel:
         self.act = torch.zeros(32, c.ffn, device=device, dtype=bf)
         self.logits = torch.zeros(32, c.vocab, device=device, dtype=bf)
         self.st0 = torch.zeros(1, 32, device=device)
-        self.st_h = torch.zeros(c.d // 128, 32, device=device)
-        self.st_mid = torch.zeros(c.d // 128, 32, device=device)
+        self.st_h = torch.zeros(c.d // 64, 32, device=device)    # per-slab partial RMS sums (64- or 128-row slabs)
+        self.st_mid = torch.zeros(c.d // 64, 32, device=device)
         # split-K plans and workspaces
         self.S = {
             "qkv": pick_split(self.qkv_n // 128, c.d // 64),
@@ -120,6 +121,14 @@ class DecodeModel:
             for kv in split_override.split(","):
                 k, v = kv.split(":")
                 self.S[k] = int(v)
+        # weight rows per slab (M of the swap-AB MMA): 128, or 64 for the small
+        # projections (gate_up's SiLU pairing needs 128-row slabs)
+        self.BM = {"qkv": 128, "o": 128, "gu": 128, "down": 128, "lm": 128}
+        if bm_override:  # e.g. "o:64,qkv:64"
+            for kv in bm_override.split(","):
+                k, v = kv.split(":")
+                self.BM[k] = int(v)
+        assert self.BM["gu"] == 128
         ws_elems = max(self.S["qkv"] * self.qkv_n, self.S["o"] * c.d, self.S["gu"] * 2 * c.ffn,
                        self.S["down"] * c.d, self.S["lm"] * c.vocab) * 32
         self.ws = torch.zeros(ws_elems, device=device)
@@ -131,10 +140,10 @@ class DecodeModel:
         self._build_args()
 
     # ---- launch records ----
-    def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None):
-        Wp = pack_sw128(W)
+    def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None, bm=128):
+        Wp = pack_sw128(W, bm)
         self._packed.append(Wp)
-        tmW = _abi.tensor_map_bf16(W.data_ptr(), N, K, 128)
+        tmW = _abi.tensor_map_bf16(W.data_ptr(), N, K, bm)
         tmX = _abi.tensor_map_bf16(X.data_ptr(), 32, K, 32)
         a = _abi.GemvArgs()
         a.tmW, a.tmX = tmW, tmX
@@ -152,7 +161,8 @@ class DecodeModel:
         a.Lmax = self.Lmax
         a.q_dim, a.kv_dim = self.cfg.d, self.kv_dim
         a.w_packed = Wp.data_ptr()
-        return a, ((N // 128) * S, 1, 1)
+        a.bm = bm
+        return a, ((N // bm) * S, 1, 1)
 
     def _build_args(self):
         c = self.cfg
@@ -164,9 +174,9 @@ class DecodeModel:
         self.records.append(("decode/embed", _abi.BODY_EMBED, (32, 1, 1), ea, 32 * c.d * 2 * 2))
         for l in range(c.layers):
             hin, hout = self.H[l % 2], self.H[(l + 1) % 2]
-            st_in, p_in = (self.st0, 1) if l == 0 else (self.st_h, c.d // 128)
+            st_in, p_in = (self.st0, 1) if l == 0 else (self.st_h, c.d // self.BM["down"])
             a, g = self._gemv(self.Wqkv[l], hin, self.qkv_n, c.d, self.S["qkv"], _abi.GEMV_QKV, self.q,
-                              stats_in=st_in, P_in=p_in, l=l)
+                              stats_in=st_in, P_in=p_in, l=l, bm=self.BM["qkv"])
             self.records.append((f"decode/qkv", _abi.BODY_GEMV_BF16, g, a, self.qkv_n * c.d * 2))
             rows = 32 * c.n_kv * self.Lmax
             at = _abi.AttnArgs(_abi.tensor_map_kv(self.kc[l].data_ptr(), rows, ATTN_CHUNK),
@@ -176,17 +186,17 @@ class DecodeModel:
             self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,
                                  2 * 32 * c.n_kv * c.L * 128 * 2))
             a, g = self._gemv(self.Wo[l], self.attn, c.d, c.d, self.S["o"], _abi.GEMV_RESID, self.h_mid, resid=hin,
-                              stats_out=self.st_mid)
+                              stats_out=self.st_mid, bm=self.BM["o"])
             self.records.append(("decode/o", _abi.BODY_GEMV_BF16, g, a, c.d * c.d * 2))
             a, g = self._gemv(self.Wgu[l], self.h_mid, 2 * c.ffn, c.d, self.S["gu"], _abi.GEMV_SILU_MUL, self.act,
-                              stats_in=self.st_mid, P_in=c.d // 128)
+                              stats_in=self.st_mid, P_in=c.d // self.BM["o"])
             self.records.append(("decode/gate_up", _abi.BODY_GEMV_BF16, g, a, 2 * c.ffn * c.d * 2))
             a, g = self._gemv(self.Wd[l], self.act, c.d, c.ffn, self.S["down"], _abi.GEMV_RESID, hout,
-                              resid=self.h_mid, stats_out=self.st_h)
+                              resid=self.h_mid, stats_out=self.st_h, bm=self.BM["down"])
             self.records.append(("decode/down", _abi.BODY_GEMV_BF16, g, a, c.d * c.ffn * 2))
         hfin = self.H[c.layers % 2]
         a, g = self._gemv(self.lm, hfin, c.vocab, c.d, self.S["lm"], _abi.GEMV_STORE, self.logits,
-                          stats_in=self.st_h, P_in=c.d // 128)
+                          stats_in=self.st_h, P_in=c.d // self.BM["down"], bm=self.BM["lm"])
         self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
         chunks = max(1, min(4, c.vocab // 2048))  # 128 blocks: one wave; every block pays a claim + ticket
         am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), self.amax_ws.data_ptr(),

@@ -11,7 +11,7 @@ from paper_2603_15042_b200.tenants import DecodeModel, DecodeConfig
 layers = int(os.environ.get("LAYERS", "8"))
 nsm = int(os.environ.get("NSM", "74"))
 m = DecodeModel(DecodeConfig(layers=layers, attn_splits=int(os.environ.get("ASPLIT", "1"))),
-                split_override=os.environ.get("SPLITS", ""))
+                split_override=os.environ.get("SPLITS", ""), bm_override=os.environ.get("BMS", ""))
 torch.cuda.synchronize()
 dom = Domain(0, tiers=[Fraction(1)], block_log_capacity=1 << 22)
 t = dom.tenant("decode", 0)

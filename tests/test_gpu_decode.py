@@ -17,13 +17,17 @@ from paper_2603_15042_b200.tenants import DecodeConfig, DecodeModel, pick_split
 pytestmark = pytest.mark.gpu
 
 
-def small_model():
+BM_VARIANTS = ["", "qkv:64,o:64,down:64,lm:64"]
+
+
+def small_model(bms=""):
     cfg = DecodeConfig(layers=2, vocab=2048, L=96, attn_splits=2)
-    return DecodeModel(cfg, seed=5)
+    return DecodeModel(cfg, seed=5, bm_override=bms)
 
 
-def test_decode_step_matches_torch_reference():
-    m = small_model()
+@pytest.mark.parametrize("bms", BM_VARIANTS)
+def test_decode_step_matches_torch_reference(bms):
+    m = small_model(bms)
     tok0 = m.tokens.clone()
     kc0 = [k.clone() for k in m.kc]
     vc0 = [v.clone() for v in m.vc]
@@ -45,8 +49,9 @@ def test_decode_step_matches_torch_reference():
     assert torch.equal(m.tokens.cpu()[clear.cpu()], ref_tok.cpu()[clear.cpu()])
 
 
-def test_decode_step_coroutine_bit_exact_vs_solo():
-    m = small_model()
+@pytest.mark.parametrize("bms", BM_VARIANTS)
+def test_decode_step_coroutine_bit_exact_vs_solo(bms):
+    m = small_model(bms)
     tok0 = m.tokens.clone()
     kc0 = [k.clone() for k in m.kc]
     vc0 = [v.clone() for v in m.vc]
