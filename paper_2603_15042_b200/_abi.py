@@ -11,7 +11,8 @@ import os
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+# DS_LIB: an experiment build of the same library (e.g. one lane per SM)
+LIB_PATH = os.environ.get("DS_LIB", _build.LIB)
 
 DS_MAX_TENANTS = 64
 DS_MAX_SMS = 256

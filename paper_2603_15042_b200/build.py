@@ -41,13 +41,16 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, lanes: int = 0, out: str = "", defines=()) -> str:
+    """lanes / out: an experiment variant (e.g. one worker lane per SM) built
+    to another file; the product library is LIB with the default lanes."""
+    lib = out or LIB
+    if not force and not out and up_to_date():
         return LIB
-    objdir = os.path.join(PKG, "_obj")
+    objdir = os.path.join(PKG, "_obj" + (f"_l{lanes}" if lanes else "") + ("_v" if out else ""))
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
-              "-I" + CSRC]
+              "-I" + CSRC] + ([f"-DDS_LANES={lanes}"] if lanes else []) + [f"-D{d}" for d in defines]
     objs = []
     for src in CU_SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
@@ -61,11 +64,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     # export only the C ABI (ds_*): no std:: template instances that another
     # C++ library in the same process (e.g. the oracle) could bind to
-    cmd = [NVCC, "-shared", "-Xcompiler", "-fPIC"] + ARCH + objs + ["-cudart", "static", "-o", LIB,
+    cmd = [NVCC, "-shared", "-Xcompiler", "-fPIC"] + ARCH + objs + ["-cudart", "static", "-o", lib,
                                                                      "-Xlinker", "-lpthread", "-Xlinker",
                                                                      "--version-script=" + os.path.join(CSRC, "exports.map")]
     _run(cmd, verbose)
-    return LIB
+    return lib
 
 
 def _run(cmd, verbose):
