@@ -118,12 +118,42 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def _guarded(fn):
+    """A run that raises must not leave its policy engine polling a domain
+    that is about to be stopped and destroyed: stop the feeder thread, stop
+    and close the engine, reset the control word, then re-raise."""
+    def w(self, *a, **k):
+        self._cur_eng = self._cur_stop = self._cur_th = None
+        try:
+            return fn(self, *a, **k)
+        except BaseException:
+            if self._cur_stop is not None:
+                self._cur_stop.set()
+            if self._cur_th is not None:
+                self._cur_th.join(timeout=10)
+            if self._cur_eng is not None:
+                try:
+                    self._cur_eng.stop()
+                    self._cur_eng.close()
+                except Exception:
+                    pass
+            try:
+                self.dom.set_lend(-1)
+                self.dom.quota_set([-1] * self.dom.num_sms)
+            except Exception:
+                pass
+            raise
+    w.__name__ = fn.__name__
+    w.__doc__ = fn.__doc__
+    return w
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 class Colocation:
     def __init__(self, device, tokens_per_req, kv_len, layers=32, decode_sat=Fraction(1, 2), slo_x=8.0,
-                 tiers=(Fraction(1, 4), Fraction(3, 4), Fraction(1))):
+                 tiers=(Fraction(1, 4), Fraction(3, 4), Fraction(1)), prefill_mix=False):
         import torch
         from paper_2603_15042_b200 import _abi
         from paper_2603_15042_b200.runtime import Domain
@@ -136,6 +166,13 @@ class Colocation:
         self.decode_sat = decode_sat
         self.slo_x = slo_x
         self.train = TrainGemm(device=f"cuda:{device}")
+        # prefill mix (config 4b): a second chat stream (its own model state)
+        # and both streams' prefill GEMM records, built before the executor
+        # owns the SMs
+        self.model2 = None
+        if prefill_mix:
+            self.model2 = DecodeModel(DecodeConfig(L=kv_len, layers=layers), device=f"cuda:{device}", seed=1)
+            self.pf_recs = [self.model.prefill_records(256), self.model2.prefill_records(256)]
         torch.cuda.synchronize()
         # pool: decode binds 3/4 (smallest tier >= its fair share 1/2), training 1/4;
         # idle SMs are lent to training.  (With a 1/2 tier, the reference
@@ -148,6 +185,11 @@ class Colocation:
         self.dec_kernels = self.model.register(self.dom)
         self.gemm_kernel = self.train.register(self.dom)
         self.resnet = None
+        if self.model2 is not None:
+            self.t_dec2 = self.dom.tenant("decode2", _abi.LATENCY_CRITICAL)
+            self.dec2_kernels = self.model2.register(self.dom)
+            self.pf_kernels = [[self.dom.kernel(sid, body, grid, args, phase=_abi.PREFILL)
+                                for sid, body, grid, args, _ in recs] for recs, _ in self.pf_recs]
         self.dom.start()
 
     def add_resnet(self):
@@ -168,6 +210,7 @@ class Colocation:
         dom.quota_set([-1] * dom.num_sms)
         return self.res_iter_ns / 1e6
 
+    @_guarded
     def run_bursty(self, policy, arrivals_ns, tokens, step_ns, quantum_ms=5.0, tpot_slo_ns=0, ttft_slo_ns=0):
         """Config 4: bursty decode requests (arrivals from the reference's
         gen_burst) co-located with the ResNet-50 training stream.  Returns
@@ -180,8 +223,10 @@ class Colocation:
         jd = eng.add_job(self.t_dec, _abi.LATENCY_CRITICAL)
         jt = eng.add_job(self.t_res, _abi.BEST_EFFORT)
         dom.set_lend(lend)
+        self._cur_eng = eng
         eng.start()
         stop = threading.Event()
+        self._cur_stop = stop
         train_recs = []
 
         def trainer():
@@ -196,6 +241,7 @@ class Colocation:
                 time.sleep(0.0005)
 
         th = threading.Thread(target=trainer, daemon=True)
+        self._cur_th = th
         th.start()
         time.sleep(0.05)
         t0 = eng.now() + 10_000_000
@@ -288,11 +334,13 @@ class Colocation:
         # throughput over back-to-back launches (consecutive GEMMs overlap at
         # the launch boundary through early start): span / launches
         gemm_ms = (gs[-1].t_end - gs[0].t_first_claim) / 1e6 / n_gemm
+        self.gemm_ns = gemm_ms * 1e6
         dom.quota_set([-1] * dom.num_sms)
         return {"decode_step_ms": statistics.median(step_ns) / 1e6, "gemm_ms": gemm_ms,
                 "per_kernel_ns": {k: statistics.median(v) for k, v in per_kernel.items()},
                 "per_kernel_launches": {k: len(v) for k, v in per_kernel.items()}}
 
+    @_guarded
     def run(self, policy, requests, warmup, solo, e2e=False, quantum_ms=5.0):
         """Co-located run: returns per-request TPOT (ms), training TFLOP/s in
         the timed window, and engine counters."""
@@ -309,8 +357,10 @@ class Colocation:
         tpot_slo = int(self.slo_x * step_ns)
         ttft_slo = int(2 * self.slo_x * step_ns)
         period = int(2 * self.T * step_ns)  # decode busy ~50% of the time when solo
+        self._cur_eng = eng
         eng.start()
         stop = threading.Event()
+        self._cur_stop = stop
         train_recs = []
 
         def trainer():
@@ -326,6 +376,7 @@ class Colocation:
                 time.sleep(0.0002)
 
         th = threading.Thread(target=trainer, daemon=True)
+        self._cur_th = th
         th.start()
         time.sleep(0.05)
         pinned_tok = torch.zeros(32, dtype=torch.int32).pin_memory()
@@ -403,6 +454,86 @@ class Colocation:
                 "window_ms": (w1 - w0) / 1e6, "train_tflops": done_flop / ((w1 - w0) * 1e-9) / 1e12,
                 "counters": counters, "gemm_ms_median": statistics.median(gemm_durs) / 1e6 if gemm_durs else None}
 
+    @_guarded
+    def run_prefill_mix(self, policy, arrivals, tokens, step_ns, prefill_ns, tpot_slo_ns, ttft_slo_ns, quantum_ms=5.0):
+        """Config 4b: two chat streams (requests alternate between them), each
+        request a prefill record (256 prompt tokens: 128 tcgen05 GEMMs) then
+        `tokens` decode steps, beside the training GEMM.  This is where
+        TPOT-First differs from the default policy: a prefill is admitted only
+        if the running decodes keep their TPOT (policies.cpp:184-204)."""
+        from paper_2603_15042_b200.runtime import Engine
+        _abi, dom = self._abi, self.dom
+        lend = self.t_trn if policy != "temporal" else -1
+        eng = Engine(dom, policy=policy, quantum_ns=int(quantum_ms * 1e6), lend_tenant=lend, fair_handover=True)
+        jobs = [eng.add_job(self.t_dec, _abi.LATENCY_CRITICAL), eng.add_job(self.t_dec2, _abi.LATENCY_CRITICAL)]
+        jt = eng.add_job(self.t_trn, _abi.BEST_EFFORT)
+        dec = [self.dec_kernels, self.dec2_kernels]
+        dom.set_lend(lend)
+        self._cur_eng = eng
+        eng.start()
+        stop = threading.Event()
+        self._cur_stop = stop
+        train_recs = []
+
+        def trainer():
+            outstanding = []
+            while not stop.is_set():
+                while len(outstanding) < 2:
+                    r = eng.submit(jt, [self.gemm_kernel], "train/gemm_bf16", _abi.TRAINING, grid_size=2048,
+                                   base_hint_ns=int(self.gemm_ns), saturation=Fraction(1, 4))
+                    outstanding.append(r)
+                    train_recs.append(r)
+                outstanding = [r for r in outstanding if eng.record(r).state != 2]
+                time.sleep(0.0005)
+
+        th = threading.Thread(target=trainer, daemon=True)
+        self._cur_th = th
+        th.start()
+        time.sleep(0.05)
+        t0 = eng.now() + 10_000_000
+        reqs = []
+        for i, (a, stream) in enumerate(arrivals):
+            while eng.now() < t0 + a:
+                time.sleep(0.0001)
+            arr = eng.now()
+            j = jobs[stream]
+            pf = eng.submit(j, self.pf_kernels[stream], "prefill/default", _abi.PREFILL, grid_size=1, request=i,
+                            request_arrival_ns=arr, ttft_ns=ttft_slo_ns, tpot_ns=tpot_slo_ns, base_hint_ns=prefill_ns,
+                            saturation=Fraction(9, 10))
+            recs = [eng.submit(j, dec[stream], "decode/step", _abi.DECODE, grid_size=len(dec[stream]), request=i,
+                               decode_index=k, request_arrival_ns=arr, ttft_ns=ttft_slo_ns, tpot_ns=tpot_slo_ns,
+                               base_hint_ns=step_ns, saturation=self.decode_sat) for k in range(tokens)]
+            reqs.append((arr, pf, recs))
+        for _, _, recs in reqs:
+            eng.wait(recs[-1], timeout_ms=120000)
+        stop.set()
+        th.join()
+        for r in train_recs:
+            eng.wait(r)
+        out = []
+        for arr, pf, recs in reqs:
+            inf = [eng.record(r) for r in recs]
+            out.append({"ttft_ms": (inf[0].finish_host_ns - arr) / 1e6,  # first decode completion (metrics.cpp:46)
+                        "tpot_ms": (inf[-1].t_end - inf[0].t_end) / (tokens - 1) / 1e6,
+                        "w0": eng.record(pf).t_first_claim, "w1": inf[-1].t_end})
+        w0, w1 = min(o["w0"] for o in out), max(o["w1"] for o in out)
+        done = 0.0
+        for ti in (eng.record(r) for r in train_recs):
+            a, b = ti.t_first_claim, ti.t_end
+            if b > a:
+                done += self.train.flops * max(0, min(b, w1) - max(a, w0)) / (b - a)
+        counters = eng.counters()
+        eng.stop()
+        eng.close()
+        dom.set_lend(-1)
+        dom.quota_set([-1] * dom.num_sms)
+        tp, tt = [o["tpot_ms"] for o in out], [o["ttft_ms"] for o in out]
+        return {"requests": len(out), "p99_tpot_ms": round(nearest_rank(tp, 99), 3),
+                "p99_ttft_ms": round(nearest_rank(tt, 99), 3),
+                "tpot_slo_violation_rate": round(sum(x * 1e6 > tpot_slo_ns for x in tp) / len(tp), 4),
+                "ttft_slo_violation_rate": round(sum(x * 1e6 > ttft_slo_ns for x in tt) / len(tt), 4),
+                "train_tflops": round(done / ((w1 - w0) * 1e-9) / 1e12, 1), "engine_counters": counters}
+
     def bit_exact_check(self):
         """The decode step's logits after a co-located run must equal a solo
         replay of the same step from the same state (no kernel or reduction
@@ -477,6 +608,40 @@ def cpu_baseline_leg(solo, requests, tokens, budget_s=10.0):
                       f"calibrated with measured solo durations; {ev} events in {wall:.2f} s wall"}
 
 
+def config4b_leg(co, args, solo):
+    """Two chat streams with prefill (256-token prompts) + the training GEMM:
+    TPOT-First vs the reference default (slo-aware) vs time slicing, in P99
+    TPOT / TTFT and SLO violation rates (the paper's TPOT-First comparison,
+    PAPER.md:457-458)."""
+    from paper_2603_15042_b200 import workload as wl
+    dom, _abi = co.dom, co._abi
+    # prefill's solo duration on the whole GPU (predictor hint)
+    dom.quota_set(dom.mask(co.t_dec, 0, dom.num_sms))
+    for _ in range(2):
+        for k in co.pf_kernels[0]:
+            last = dom.launch(co.t_dec, k)
+    dom.wait(co.t_dec, last)
+    cs = [c for c in dom.poll(1 << 20) if c.tenant == co.t_dec]
+    n = len(co.pf_kernels[0])
+    prefill_ns = cs[-1].t_end - cs[-n].t_first_claim
+    dom.quota_set([-1] * dom.num_sms)
+    step_ns = int(solo["decode_step_ms"] * 1e6)
+    reqs = wl.gen_burst(0.5, 4.0, 2.0, 20.0, args.burst_units, wl.RequestTemplate(output_tokens=4, streams=2), seed=1)
+    arrivals = [(int(r.arrival_q * 50.0 * 1e-3), r.stream) for r in reqs]
+    # TPOT SLO 3x the solo step: with tighter SLOs the reference SLO-aware
+    # rule (inherited by TPOT-First) defers a bound decode forever once it
+    # predicts a miss it cannot fix at its tier (SURVEY 8-appendix #2)
+    tpot_slo, ttft_slo = 3 * step_ns, 150_000_000
+    log(f"config 4b: {len(arrivals)} requests over 2 streams, prefill solo {prefill_ns / 1e6:.2f} ms")
+    res = {p: co.run_prefill_mix(p, arrivals, 4, step_ns, prefill_ns, tpot_slo, ttft_slo, quantum_ms=args.quantum_ms)
+           for p in ("tpot-first", "slo-aware", "temporal")}
+    return {"workload": "config 4b: two chat streams (batch-32 Llama-3-8B-shaped decode each; requests alternate, "
+                        "gen_burst arrivals) with 256-token prefill (128 tcgen05 GEMMs) before 4 decode steps, "
+                        "beside the bf16 GEMM 8192^3 training tenant",
+            "prefill_solo_ms": round(prefill_ns / 1e6, 3), "slo_ms": {"tpot": tpot_slo / 1e6, "ttft": ttft_slo / 1e6},
+            "tpot_first": res["tpot-first"], "slo_aware": res["slo-aware"], "temporal": res["temporal"]}
+
+
 def config4_leg(co, args, solo):
     """Config 4: the ResNet-50-shaped training stream co-located with bursty
     decode requests (gen_burst arrivals), TPOT-First vs time slicing."""
@@ -487,10 +652,10 @@ def config4_leg(co, args, solo):
     arrivals = [int(r.arrival_q * unit_ms * 1e-3) for r in reqs]  # arrival_q = round(t*1e9) -> ns
     step_ns = int(solo["decode_step_ms"] * 1e6)
     log(f"config 4: {len(arrivals)} bursty requests, resnet solo iter {res_ms:.2f} ms")
-    # SLOs tight enough to separate the policies: TPOT 2x the solo decode
+    # SLOs tight enough to separate the policies: TPOT 3x the solo decode
     # step, TTFT 150 ms (the paper's TPOT-First-vs-Default comparison is in
     # SLO violation rates)
-    slo = dict(tpot_slo_ns=2 * step_ns, ttft_slo_ns=150_000_000)
+    slo = dict(tpot_slo_ns=3 * step_ns, ttft_slo_ns=150_000_000)
     c4 = {p: co.run_bursty(p, arrivals, 4, step_ns, quantum_ms=args.quantum_ms, **slo)
           for p in ("tpot-first", "slo-aware", "temporal")}
     return {"workload": "config 4: ResNet-50-shaped training stream (53 convs + FC, fwd/dgrad/wgrad = 161 "
@@ -509,7 +674,8 @@ def gpu_arm(args, rank, world):
     peaks, peaks_src = load_peaks()
     log("building tenants")
     co = Colocation(dev, args.tokens, args.kv_len, layers=args.layers, decode_sat=Fraction(args.decode_sat),
-                    slo_x=args.slo_x, tiers=[Fraction(t) for t in args.tiers.split(",")])
+                    slo_x=args.slo_x, tiers=[Fraction(t) for t in args.tiers.split(",")],
+                    prefill_mix=not args.no_config4b)
     solo = co.solo(steps=max(3, args.warmup))
     log("solo", {k: v for k, v in solo.items() if k != "per_kernel_ns" and k != "per_kernel_launches"})
     with ClockSampler(dev) as clk:
@@ -521,6 +687,12 @@ def gpu_arm(args, rank, world):
     tm_fine = co.run("temporal", args.steps, args.warmup, solo, quantum_ms=args.quantum_ms / 5)
     e2e = co.run("tpot-first", args.steps, args.warmup, solo, e2e=True)
     exact = co.bit_exact_check()
+    config4b = None
+    if not args.no_config4b:
+        try:
+            config4b = config4b_leg(co, args, solo)
+        except Exception as e:  # an auxiliary leg must not cost the headline line
+            config4b = {"error": repr(e)}
     config4 = None
     if not args.no_config4:
         try:
@@ -575,6 +747,7 @@ def gpu_arm(args, rank, world):
         "clocks": clocks,
         "gpu_launches": len(m.records) * (args.steps + args.warmup) * args.tokens,
         "config4": config4,
+        "config4b": config4b,
     }
     return out, solo
 
@@ -881,6 +1054,7 @@ def main():
     ap.add_argument("--c5-dp-iters", type=int, default=40, help="config 5 data-parallel tenant iterations")
     ap.add_argument("--c5-drain-s", type=float, default=30.0, help="config 5 drain deadline")
     ap.add_argument("--only-config5", action="store_true", help="run the config 5 leg alone (debug)")
+    ap.add_argument("--no-config4b", action="store_true", help="skip the two-stream prefill mix leg")
     ap.add_argument("--no-config4", action="store_true", help="skip the config 4 (ResNet + bursty decode) leg")
     ap.add_argument("--burst-units", type=float, default=60.0, help="config 4 trace duration (units of 50 ms)")
     ap.add_argument("--tiers", default="1/4,1/2,3/4,1", help="pctx pool tiers (create_pool; SPEC.md:65 pool)")

@@ -241,6 +241,19 @@ def solo_launch(device: int, semantic_id: str, body: int, grid, args, stream: in
     check(lib().ds_solo_launch(device, ctypes.byref(desc), ctypes.c_void_p(stream)))
 
 
+_LIVE_ENGINES: "weakref.WeakSet[Engine]" = weakref.WeakSet()
+
+
+@atexit.register  # registered after the domain hook, so it runs first (LIFO)
+def _stop_live_engines():
+    for e in list(_LIVE_ENGINES):
+        try:
+            e.stop()
+            e.close()
+        except Exception:
+            pass
+
+
 class Engine:
     """SimEngine-like dispatch loop over one domain (C++ engine thread).
 
@@ -272,6 +285,7 @@ class Engine:
         self.h = h
         self.dom = dom
         self._keep = []
+        _LIVE_ENGINES.add(self)
 
     def add_job(self, tenant: int, priority: int) -> int:
         out = ctypes.c_int()

@@ -216,6 +216,30 @@ class DecodeModel:
     def register(self, dom, phase=_abi.DECODE) -> List[int]:
         return [dom.kernel(sid, body, grid, args, phase=phase) for sid, body, grid, args, _ in self.records]
 
+    def prefill_records(self, prompt_tokens: int = 256):
+        """A prompt's prefill on the same weights: per layer the four
+        projection GEMMs over `prompt_tokens` rows (tcgen05 GEMM body; the
+        weights [N][K] are already the K-major B operand).  Activations are
+        synthetic (one shared input / output buffer), so this prices and
+        schedules prefill without modelling attention over the prompt.
+        Returns (records, flops)."""
+        c = self.cfg
+        P = (prompt_tokens + 127) // 128 * 128
+        dev = self.q.device
+        self.pf_x = (torch.rand(P, max(c.d, c.ffn), device=dev) * 2 - 1).to(torch.bfloat16)
+        self.pf_y = torch.zeros(P, max(self.qkv_n, 2 * c.ffn, c.d), device=dev, dtype=torch.bfloat16)
+        recs, flops = [], 0.0
+        for l in range(c.layers):
+            for name, W in (("qkv", self.Wqkv[l]), ("o", self.Wo[l]), ("gate_up", self.Wgu[l]), ("down", self.Wd[l])):
+                N, K = W.shape
+                # row-major views with the GEMM's own row pitch (x: [P][K], y: [P][N])
+                x = self.pf_x.view(-1)[: P * K].view(P, K)
+                y = self.pf_y.view(-1)[: P * N].view(P, N)
+                ga = _abi.gemm_args(x.data_ptr(), W.data_ptr(), y.data_ptr(), P, N, K, group_m=4)
+                recs.append((f"prefill/{name}", _abi.BODY_GEMM_BF16, _abi.gemm_grid(P, N), ga, 2.0 * P * N * K))
+                flops += 2.0 * prompt_tokens * N * K
+        return recs, flops
+
     def solo_step(self, device: int = 0):
         from .runtime import solo_launch
         for sid, body, grid, args, _ in self.records:
