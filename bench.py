@@ -449,6 +449,7 @@ class Colocation:
         dom.set_lend(-1)
         dom.quota_set([-1] * dom.num_sms)
         return {"tpot_ms": [r["tpot_ms"] for r in timed], "e2e_tpot_ms": [r["e2e_tpot_ms"] for r in timed],
+                "train_launches": len(train_recs),
                 "gap_us": statistics.mean(r["gap_us"] for r in timed),
                 "step_ms": statistics.mean(r["step_ms"] for r in timed),
                 "window_ms": (w1 - w0) / 1e6, "train_tflops": done_flop / ((w1 - w0) * 1e-9) / 1e12,
@@ -745,7 +746,9 @@ def gpu_arm(args, rank, world):
                           "frac": round(gemm_tf / peaks["bf16_tflops"], 4), "peak_source": peaks_src,
                           "traffic": ncu_traffic("train/gemm_bf16"), "algorithmic_bytes": 3 * 8192 * 8192 * 2},
         "clocks": clocks,
-        "gpu_launches": len(m.records) * (args.steps + args.warmup) * args.tokens,
+        # logical launches through the executor in the timed tpot-first run:
+        # decode kernels of every step + training GEMM launches
+        "gpu_launches": len(m.records) * (args.steps + args.warmup) * args.tokens + sp.get("train_launches", 0),
         "config4": config4,
         "config4b": config4b,
     }
