@@ -381,6 +381,27 @@ typedef struct ds_tenant_demand {
 
 int ds_place_tenants(const ds_tenant_demand* tenants, int n, int n_devices, double mem_cap_gb, int32_t* device_out);
 
+/* ---- working-set migration across places ----
+ * compute_migration_set / full_eager_set (proj/src/runtime/migration.cpp:21-58):
+ * eager = touched regions that are dirty or not resident on dst (sorted,
+ * unique); lazy = the remaining dirty regions (ascending id).  A touched
+ * region outside the working set -> DS_TRACE_VIOLATION.  Output arrays hold
+ * up to n_ws ids.  ds_migrate_regions copies regions peer to peer (copy
+ * engines over NVLink; no SMs taken from the resident executors). */
+typedef struct ds_region {
+    int32_t id;
+    int32_t dirty;
+    uint64_t bytes;
+    uint64_t resident_mask; /* bit p: resident on place p (pctx or GPU, p < 64) */
+} ds_region;
+
+int ds_compute_migration_set(const ds_region* ws, int n_ws, const int32_t* touched, int n_touched, int dst,
+                             int32_t* eager, int* n_eager, uint64_t* eager_bytes, int32_t* lazy, int* n_lazy,
+                             uint64_t* lazy_bytes);
+int ds_full_eager_set(const ds_region* ws, int n_ws, int32_t* eager, int* n_eager, uint64_t* eager_bytes);
+int ds_migrate_regions(int src_device, int dst_device, const void* const* src_ptrs, void* const* dst_ptrs,
+                       const uint64_t* bytes, int n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,8 @@ def reference():
         lib.ref_equivalence_json.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_long]
         lib.ref_gen_trace.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)] + [ctypes.c_int] * 7 + [
             ctypes.c_ulonglong, ctypes.c_char_p, ctypes.c_long]
+        lib.ref_migration_set.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_char_p, ctypes.c_long]
         lib.ref_expand.argtypes = [ctypes.c_char_p, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong,
                                    ctypes.c_int, ctypes.c_char_p, ctypes.c_long]
         _ref = lib
@@ -165,3 +167,10 @@ def ref_expand(trace_jsonl: str, tokens_per_grid_unit: int, decode_grid: int, tr
     """expand_workload of the reference (workload.cpp:51-174), one line per kernel."""
     return _call(reference().ref_expand, trace_jsonl.encode(), tokens_per_grid_unit, decode_grid, train_grid,
                  default_iterations, cap=1 << 26)
+
+
+def ref_migration_set(regions, touched, dst: int, full: bool = False) -> str:
+    """compute_migration_set / full_eager_set of the reference (migration.cpp:21-58).
+    regions: [(id, bytes, dirty, [places])]."""
+    text = "\n".join(f"{i} {b} {int(d)} {','.join(map(str, p)) or '-'}" for i, b, d, p in regions)
+    return _call(reference().ref_migration_set, text.encode(), " ".join(map(str, touched)).encode(), dst, int(full))

@@ -13,6 +13,7 @@
 #include "corosim/numlab/equivalence.hpp"
 #include "corosim/numlab/float_format.hpp"
 #include "corosim/numlab/reduction.hpp"
+#include "corosim/runtime/migration.hpp"
 #include "corosim/rational.hpp"
 
 #include <json.hpp>
@@ -268,6 +269,51 @@ int ref_expand(const char* trace_jsonl, long long tokens_per_grid_unit, long lon
                << (k.reduction ? k.reduction->value_seed : 0ULL) << ' ' << to_decimal_string(k.arrival_floor) << '\n';
         }
         return put(os.str(), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+// compute_migration_set / full_eager_set (migration.cpp:21-58) on a working
+// set given as lines "id bytes dirty place,place,..." and touched region ids
+// "id id ...".  Returns "eager ids | eager_bytes | lazy ids | lazy_bytes" or
+// "error: <Errc>".
+int ref_migration_set(const char* regions_nl, const char* touched_sp, int dst, int full, char* out, long cap) {
+    try {
+        VirtualContext v;
+        std::istringstream rs(regions_nl);
+        std::string line;
+        while (std::getline(rs, line)) {
+            if (line.empty()) continue;
+            std::istringstream ls(line);
+            long long id, bytes;
+            int dirty;
+            std::string places;
+            ls >> id >> bytes >> dirty >> places;
+            MemoryRegion r;
+            r.id = RegionId(static_cast<std::int32_t>(id));
+            r.bytes = static_cast<std::uint64_t>(bytes);
+            r.dirty = dirty != 0;
+            std::istringstream ps(places == "-" ? "" : places);
+            std::string p;
+            while (std::getline(ps, p, ',')) r.resident_on.insert(PctxId(std::stoi(p)));
+            v.working_set[r.id] = r;
+        }
+        Kernel k;
+        std::istringstream ts(touched_sp);
+        long long t;
+        while (ts >> t) k.touched_regions.push_back(RegionId(static_cast<std::int32_t>(t)));
+        MigrationSet m = full ? full_eager_set(v) : compute_migration_set(v, k, PctxId(dst));
+        std::ostringstream os;
+        for (RegionId r : m.eager) os << r.value << ' ';
+        os << "| " << m.eager_bytes << " | ";
+        for (RegionId r : m.lazy) os << r.value << ' ';
+        os << "| " << m.lazy_bytes;
+        return put(os.str(), out, cap);
+    } catch (const SimError& e) {
+        put(std::string("error: ") + errc_name(e.code()), out, cap);
+        return 0;
     } catch (const std::exception& e) {
         put(std::string("error: ") + e.what(), out, cap);
         return 1;

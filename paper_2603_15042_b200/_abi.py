@@ -317,6 +317,11 @@ class AllreduceArgs(ctypes.Structure):
                 ("chunk", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
+class Region(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int32), ("dirty", ctypes.c_int32), ("bytes", ctypes.c_uint64),
+                ("resident_mask", ctypes.c_uint64)]
+
+
 class TenantDemand(ctypes.Structure):
     _fields_ = [("priority", ctypes.c_int32), ("phase", ctypes.c_int32), ("hbm_frac", ctypes.c_double),
                 ("tensor_frac", ctypes.c_double), ("mem_gb", ctypes.c_double)]
@@ -336,6 +341,7 @@ EXPORTS = [
     "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",
     "ds_ipc_alloc", "ds_ipc_free", "ds_ipc_handle", "ds_ipc_open", "ds_ipc_close", "ds_dp_abort",
     "ds_engine_event_log", "ds_engine_quarantines", "ds_quota_triggers_reset",
+    "ds_compute_migration_set", "ds_full_eager_set", "ds_migrate_regions",
 ]
 
 _lib = None
@@ -423,6 +429,12 @@ def lib():
         L.ds_ipc_open.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.ds_ipc_close.argtypes = [ctypes.c_int, vp]
         L.ds_quota_triggers_reset.argtypes = [vp]
+        i32p_, u64p_, ip_ = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_int)
+        L.ds_compute_migration_set.argtypes = [ctypes.POINTER(Region), ctypes.c_int, i32p_, ctypes.c_int, ctypes.c_int,
+                                               i32p_, ip_, u64p_, i32p_, ip_, u64p_]
+        L.ds_full_eager_set.argtypes = [ctypes.POINTER(Region), ctypes.c_int, i32p_, ip_, u64p_]
+        L.ds_migrate_regions.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp), u64p_,
+                                         ctypes.c_int, vp]
         L.ds_engine_event_log.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         L.ds_engine_quarantines.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
                                             ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
