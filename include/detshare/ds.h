@@ -53,8 +53,13 @@ typedef enum ds_status {
     DS_TIMEOUT = 103,
     DS_RING_FULL = 104,
     DS_INVALID_ARGUMENT = 105,
-    DS_ALREADY_RUNNING = 106
+    DS_ALREADY_RUNNING = 106,
+    DS_TENANT_FAILED = 107      /* the tenant raised a local exception (ds_tenant_fault) */
 } ds_status;
+
+/* Local-exception codes a tenant body raises (any nonzero code may be injected). */
+#define DS_FAULT_BAD_INPUT 1u   /* e.g. a token id outside the embedding table */
+#define DS_FAULT_INJECTED 2u    /* ds_engine_fault_local */
 
 /* Tenant bodies compiled into the executor ("unmodified kernels": each is a
  * device function of the logical block index, also launchable solo as a
@@ -183,7 +188,23 @@ int ds_launch(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, uint64_t*
 /* negative-control mutant (engine.hpp:68-71): executed grid = max(1, floor(grid * tier)) */
 int ds_launch_atomized(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, int64_t tier_num,
                        int64_t tier_den, uint64_t* seq);
-int ds_wait_tenant(ds_domain* dom, int tenant, uint64_t seq, int timeout_ms); /* until seq completed */
+int ds_wait_tenant(ds_domain* dom, int tenant, uint64_t seq, int timeout_ms); /* until seq completed;
+                                                                               DS_TENANT_FAILED once the tenant failed */
+/* Local exception (FaultSpec::LocalException, apply_local_exception engine.cpp:1049-1083):
+ * the tenant fails alone — no SM claims another of its blocks, blocks already
+ * running finish, its pending launches never complete, later ds_launch calls
+ * return DS_TENANT_FAILED.  Other tenants are unaffected (bit-exact).
+ * code must be nonzero; the first fault of a tenant wins. */
+int ds_fault_inject(ds_domain* dom, int tenant, uint32_t code);
+typedef struct ds_fault_info {
+    uint32_t code;          /* 0 = healthy */
+    uint32_t block;         /* logical block that raised it (0xffffffff: injected) */
+    uint64_t seq;           /* launch that raised it (injected: the launch open for claims) */
+    uint64_t first_failed;  /* launches >= this never count as completed (the tenant's head
+                               when it faulted: earlier launches had finished intact) */
+    uint64_t t_ns;          /* %globaltimer */
+} ds_fault_info;
+int ds_tenant_fault(ds_domain* dom, int tenant, ds_fault_info* out);
 int ds_poll(ds_domain* dom, ds_completion* out, int cap, int* n);
 
 /* ---- arbiter: pctx binding and raw SM quota ---- */
@@ -255,6 +276,7 @@ typedef struct ds_engine_config {
     int hang_detection;        /* EngineConfig.hang_detection (engine.hpp:63) */
     double hang_threshold;     /* EngineConfig.hang_threshold (default 3) */
     int capture_log;           /* EngineConfig.capture_log: JSONL event log */
+    int64_t reset_delay_ns;    /* EngineConfig.reset_delay: pctx downtime after a local exception (0: 200 us) */
 } ds_engine_config;
 
 typedef struct ds_record_desc {
@@ -274,7 +296,7 @@ typedef struct ds_record_desc {
 
 typedef struct ds_record_info {
     uint64_t id;
-    int32_t job, state;        /* state: 0 queued, 1 dispatched, 2 done */
+    int32_t job, state;        /* state: 0 queued, 1 dispatched, 2 done, 3 failed (job hit a local exception) */
     int32_t pctx, preempted;
     int32_t phase, decode_index;
     int64_t request;
@@ -284,6 +306,7 @@ typedef struct ds_record_info {
 
 typedef struct ds_engine_counters {
     uint64_t decisions, dispatches, completed, preemptions, migrations, unbinds, policy_errors;
+    uint64_t failed_jobs;      /* local exceptions (VctxStatus::Failed) */
 } ds_engine_counters;
 
 const char* ds_engine_last_error(void);
@@ -304,6 +327,13 @@ int ds_policy_names(char* out, int cap);
 int ds_engine_event_log(ds_engine* eng, char* out, int64_t cap, int64_t* len);
 /* quarantined vctxs (SimulationReport.quarantines, engine.hpp:136) */
 int ds_engine_quarantines(ds_engine* eng, int32_t* jobs, int64_t* t_ns, int cap, int* n);
+/* FaultSpec{LocalException, pctx} at engine time now: the job bound to pctx
+ * fails (status Failed, pending records dropped, unbound), the pctx is held
+ * unavailable for reset_delay; no effect on an unbound pctx (logged).
+ * Device-raised faults (ds_tenant_fault) take the same path automatically. */
+int ds_engine_fault_local(ds_engine* eng, int pctx);
+/* SimulationReport.vctx_status: 0 Active, 1 Failed, 2 Stranded (types.hpp:77) */
+int ds_engine_job_status(ds_engine* eng, int job, int* status);
 
 
 /* ---- request streams and workload expansion ----

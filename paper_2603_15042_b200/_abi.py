@@ -40,8 +40,11 @@ STATUS = {
     0: "Ok", 1: "InvalidTier", 2: "BindConflict", 3: "DoubleBind", 4: "CausalityViolation",
     5: "EventBudgetExceeded", 6: "TraceViolation", 7: "PlanMismatch", 8: "InvalidSplit",
     9: "ParseError", 10: "ConfigError", 100: "CudaError", 101: "NoDevice", 102: "NotRunning",
-    103: "Timeout", 104: "RingFull", 105: "InvalidArgument", 106: "AlreadyRunning",
+    103: "Timeout", 104: "RingFull", 105: "InvalidArgument", 106: "AlreadyRunning", 107: "TenantFailed",
 }
+TENANT_FAILED = 107
+FAULT_BAD_INPUT, FAULT_INJECTED = 1, 2
+ACTIVE, FAILED, STRANDED = 0, 1, 2  # VctxStatus (types.hpp:77)
 
 
 class DsError(RuntimeError):
@@ -260,7 +263,7 @@ class EngineConfig(ctypes.Structure):
                 ("cold_start_ns", ctypes.c_int64), ("release_on_idle", ctypes.c_int), ("fair_handover", ctypes.c_int),
                 ("lend_tenant", ctypes.c_int), ("n_assignments", ctypes.c_int), ("assign_vctx", ctypes.c_int32 * 64),
                 ("assign_pctx", ctypes.c_int32 * 64), ("hang_detection", ctypes.c_int), ("hang_threshold", ctypes.c_double),
-                ("capture_log", ctypes.c_int)]
+                ("capture_log", ctypes.c_int), ("reset_delay_ns", ctypes.c_int64)]
 
 
 class RecordDesc(ctypes.Structure):
@@ -281,7 +284,12 @@ class RecordInfo(ctypes.Structure):
 
 class EngineCounters(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ("decisions", "dispatches", "completed", "preemptions", "migrations",
-                                               "unbinds", "policy_errors")]
+                                               "unbinds", "policy_errors", "failed_jobs")]
+
+
+class FaultInfo(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_uint32), ("block", ctypes.c_uint32), ("seq", ctypes.c_uint64),
+                ("first_failed", ctypes.c_uint64), ("t_ns", ctypes.c_uint64)]
 
 
 class RequestTemplate(ctypes.Structure):
@@ -342,6 +350,7 @@ EXPORTS = [
     "ds_ipc_alloc", "ds_ipc_free", "ds_ipc_handle", "ds_ipc_open", "ds_ipc_close", "ds_dp_abort",
     "ds_engine_event_log", "ds_engine_quarantines", "ds_quota_triggers_reset",
     "ds_compute_migration_set", "ds_full_eager_set", "ds_migrate_regions",
+    "ds_fault_inject", "ds_tenant_fault", "ds_engine_fault_local", "ds_engine_job_status",
 ]
 
 _lib = None
@@ -439,6 +448,10 @@ def lib():
         L.ds_engine_quarantines.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
                                             ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         L.ds_dp_abort.argtypes = [ctypes.c_int, vp]
+        L.ds_fault_inject.argtypes = [vp, ctypes.c_int, ctypes.c_uint32]
+        L.ds_tenant_fault.argtypes = [vp, ctypes.c_int, ctypes.POINTER(FaultInfo)]
+        L.ds_engine_fault_local.argtypes = [vp, ctypes.c_int]
+        L.ds_engine_job_status.argtypes = [vp, ctypes.c_int, ip_]
         L.ds_place_tenants.argtypes = [ctypes.POINTER(TenantDemand), ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                        ctypes.POINTER(ctypes.c_int32)]
         L.ds_expand_workload.argtypes = [ctypes.POINTER(Request), ctypes.c_int64, ctypes.POINTER(ExpandParams),

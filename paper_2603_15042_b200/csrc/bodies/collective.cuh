@@ -60,6 +60,7 @@ __device__ void body_allreduce_p2p(const BodyCtx& c) {
             const void* pr = reinterpret_cast<const unsigned long long*>(a.flags[p]) + slot;
             while (ld_acquire_sys_u64_(pr) != epoch) {
                 if (ld_volatile_u64(reinterpret_cast<const unsigned long long*>(a.flags[a.rank]) + kDpAbortWord)) break;
+                if (tenant_failed(c)) break;
                 __nanosleep(128);
             }
         }
@@ -110,6 +111,7 @@ __device__ void body_allreduce_p2p(const BodyCtx& c) {
                 while (ld_acquire_sys_u64_(pd) != want) {
                     if (ld_volatile_u64(reinterpret_cast<const unsigned long long*>(a.flags[a.rank]) + kDpAbortWord))
                         break;
+                    if (tenant_failed(c)) break;
                     __nanosleep(256);
                 }
             }

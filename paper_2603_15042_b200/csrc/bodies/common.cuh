@@ -77,13 +77,66 @@ __device__ __forceinline__ void st_release_sys_u64(void* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Local exceptions (reference apply_local_exception, engine.cpp:1049-1083)
+// ---------------------------------------------------------------------------
+// A failed tenant's claim word is parked at kDead: no SM claims another of its
+// blocks, blocks already running finish (their in-launch waits give up, see
+// tenant_failed), and its launches never complete.  Other tenants' claim
+// words, rings and buffers are untouched, so they carry on bit-exactly.
+__device__ __forceinline__ void kill_claim(DevTenant* T) {
+    unsigned long long w = ld_volatile_u64(&T->claim);
+    for (;;) {
+        if ((uint32_t)w >= kDead) return;
+        const unsigned long long o = atomicCAS(&T->claim, w, (w & 0xffffffff00000000ull) | kDead);
+        if (o == w) return;
+        w = o;
+    }
+}
+
+// First raise wins; later raises (and injections) of the same tenant are no-ops.
+__device__ inline void fault_tenant(DevState* st, int t, uint32_t code, uint32_t seq, uint32_t block) {
+    DevTenant* T = &st->tenants[t];
+    if (atomicCAS(&T->fault, 0u, code) != 0u) return;
+    // fence.sc: pairs with the one in try_open/open_next (Dekker) so a launch
+    // opened concurrently is re-killed by whichever side comes second
+    __threadfence();
+    kill_claim(T);
+    HostFault* hf = &st->mailbox->faults[t];
+    hf->seq = seq;
+    hf->block = block;
+    // launches before head completed intact; from head on, early-started
+    // blocks may have stopped waiting for their predecessor (wait_prev), so
+    // none of them counts as completed
+    hf->head = ld_acquire_u32(&T->head);
+    hf->t = globaltimer();
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&hf->code), "r"(code) : "memory");
+}
+
+__device__ __forceinline__ bool tenant_failed(const BodyCtx& c) {
+    return c.st && ld_volatile_u32(&c.st->tenants[c.tenant].fault) != 0u;
+}
+
+// Called by one thread of a block whose input is invalid (e.g. a token id
+// outside the vocabulary): the tenant fails alone instead of faulting the
+// shared executor.  The block itself must skip the invalid access.
+__device__ __forceinline__ void raise_fault(const BodyCtx& c, uint32_t code) {
+    if (!c.st) return;  // solo grid: nothing to contain
+    fault_tenant(c.st, c.tenant, code, c.seq, c.bx + c.gx * (c.by + c.gy * c.bz));
+}
+
 // Wait until every earlier launch of this tenant has completed (acquire).
-// Single-thread form (the caller alone polls); see wait_prev_all.
+// Single-thread form (the caller alone polls); see wait_prev_all.  Gives up
+// if the tenant failed (its earlier launch will never complete).
 __device__ __forceinline__ void wait_prev(const BodyCtx& c) {
     if (!c.prev_head) return;
     // gpu-scope acquire: later loads (incl. L1) observe every write the
     // completed launches released through their retire atomics
-    while (ld_acquire_u32(c.prev_head) < c.seq) __nanosleep(32);
+    while (ld_acquire_u32(c.prev_head) < c.seq) {
+        if (tenant_failed(c)) return;
+        __nanosleep(32);
+    }
 }
 
 // All 256 body threads: one thread polls, the lane barrier carries its

@@ -130,7 +130,10 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
                 for (int j = 0; j < 8; ++j) own[row * 8 + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
             if (ltid() == 0) {
-                while (ld_acquire_u32(ctr) != (uint32_t)(a.S - 1)) __nanosleep(32);
+                while (ld_acquire_u32(ctr) != (uint32_t)(a.S - 1)) {
+                    if (tenant_failed(c)) break;  // a split that will never be claimed
+                    __nanosleep(32);
+                }
                 *ctr = 0;  // at rest for the next launch (which only arrives after this one completes)
             }
             body_sync();
@@ -669,7 +672,13 @@ __device__ void body_embed(const BodyCtx& c) {
     const EmbedArgs& a = *reinterpret_cast<const EmbedArgs*>(c.args);
     const int b = c.bx;
     int tok = __ldcg(reinterpret_cast<const int*>(a.tokens) + b);
-    tok = tok < 0 ? 0 : (tok >= a.vocab ? a.vocab - 1 : tok);
+    if (tok < 0 || tok >= a.vocab) {
+        // a token outside the vocabulary is a local exception of this tenant
+        // (the gather would read outside the table); the row is clamped so
+        // the block itself stays in bounds
+        if (ltid() == 0) raise_fault(c, DS_FAULT_BAD_INPUT);
+        tok = tok < 0 ? 0 : a.vocab - 1;
+    }
     const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.table) + (size_t)tok * a.d);
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.h) + (size_t)b * a.d);
     float ss = 0.f;

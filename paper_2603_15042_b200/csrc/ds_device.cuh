@@ -26,6 +26,7 @@ namespace ds {
 constexpr int kLanes = DS_LANES;
 constexpr int kCtasPerSm = kLanes;  // tile/pipeline sizing follows the number of concurrent workers per SM
 constexpr uint32_t kSat = 0x40000000u;      // claim-word block field >= kSat: kernel not open
+constexpr uint32_t kDead = 0x80000000u;     // claim-word block field of a failed tenant (never reopens)
 constexpr int kBodyThreads = 256;           // warps 8L..8L+7 run lane L's tenant bodies
 constexpr int kSchedWarp0 = 8 * kLanes;     // scheduler warp of lane L = kSchedWarp0 + L
 constexpr int kLoaderWarp = 9 * kLanes;     // CTA 0 only: host mailbox poller
@@ -62,7 +63,8 @@ struct alignas(128) DevTenant {
     uint32_t tail;             // launches visible to the device
     uint32_t head;             // launches completed
     unsigned long long blocks; // blocks executed (stats)
-    uint32_t pad[26];
+    uint32_t fault;            // local-exception code, 0 = healthy (set once, never cleared)
+    uint32_t pad[25];
 };
 static_assert(sizeof(DevTenant) == 128, "tenant word owns a 128-byte line");
 
@@ -89,10 +91,22 @@ struct HostCompletion {
 };
 static_assert(sizeof(HostCompletion) == 64, "completion record is one line");
 
+// Device -> host record of a tenant's local exception (written once; `code`
+// last, with release).
+struct HostFault {
+    volatile uint32_t code;
+    volatile uint32_t seq;    // launch that was running (raise) or next to claim (injection)
+    volatile uint32_t block;  // logical block that raised (0xffffffff: injected)
+    volatile uint32_t head;   // launches completed when it faulted (= first failed launch)
+    volatile unsigned long long t;  // %globaltimer ns
+    unsigned long long pad2;
+};
+static_assert(sizeof(HostFault) == 32, "fault record");
+
 // Host -> device mailbox.  Everything the loader polls sits in one 512-B
 // "hot" block read with a single warp-wide 16-B/lane load per poll:
 //   hot[0] control generation, hot[1] exit, hot[2] periodic-program generation,
-//   hot[64 + t] launch tail of tenant t.
+//   hot[3] fault-request generation, hot[64 + t] launch tail of tenant t.
 struct HostMailbox {
     volatile uint32_t hot[128];
     volatile unsigned long long periodic_ns;
@@ -101,8 +115,10 @@ struct HostMailbox {
     volatile int32_t per_owner[2][DS_MAX_SMS];
     volatile int32_t per_lender[2][DS_MAX_SMS];
     volatile uint32_t ack_gen;        // device -> host: last host control generation installed
+    volatile uint32_t fault_req[DS_MAX_TENANTS];  // host -> device: injected local exception code
+    HostFault faults[DS_MAX_TENANTS];             // device -> host
 };
-constexpr int kHotGen = 0, kHotExit = 1, kHotPGen = 2, kHotTail = 64;
+constexpr int kHotGen = 0, kHotExit = 1, kHotPGen = 2, kHotFGen = 3, kHotTail = 64;
 static_assert(kHotTail + DS_MAX_TENANTS <= 128, "tails fit the hot block");
 
 struct DevState {
@@ -152,6 +168,10 @@ struct BodyCtx {
     const uint32_t* prev_head;
     uint32_t seq;
     uint64_t* dbg;  // optional per-block phase timestamps (bodies that support it)
+    // Local exceptions (raise_fault): the domain and tenant the block runs
+    // for.  Null in solo mode.
+    DevState* st;
+    int32_t tenant;
 };
 
 }  // namespace ds

@@ -50,6 +50,7 @@ struct ds_engine {
         int preempted = 0;
         Time hang_needed = 0;  // arm_hang_check (engine.cpp:542-561): threshold x prediction
         bool hang_armed = false;
+        bool failed = false;   // its job failed before it finished (never completes)
     };
     struct Job {
         int tenant = -1;
@@ -57,6 +58,7 @@ struct ds_engine {
         std::deque<uint64_t> pending;  // not yet dispatched, program order
         int64_t running = -1;          // dispatched, unfinished record
         bool quarantined = false;
+        int status = 0;                // VctxStatus: 0 Active, 1 Failed, 2 Stranded (types.hpp:77)
         Time last_finish = 0;
         bool has_last_finish = false;
         int64_t logical_progress = 0;
@@ -81,6 +83,7 @@ struct ds_engine {
     // the same pump and the launcher preempts it again, forever
     std::vector<Time> pctx_unavail_until;
     Time preempt_hold_ns = 200000;
+    Time reset_delay_ns = 200000;  // EngineConfig.reset_delay (engine.hpp:65)
     std::mutex mu;
     std::thread th;
     std::atomic<bool> stop{false};
@@ -200,6 +203,40 @@ struct ds_engine {
             lc.request_arrival = h->r.request_arrival;
         }
         return lc;
+    }
+
+    // apply_local_exception (engine.cpp:1049-1083): the job bound to the
+    // faulting pctx fails — its records are dropped, it is unbound, and the
+    // pctx is held unavailable for reset_delay.  The device already stopped
+    // claiming its blocks (ds_fault_inject / a body's raise_fault), so the
+    // other jobs keep running on their SMs untouched.
+    void local_exception(int ji, uint32_t code) {
+        Job& j = jobs[ji];
+        if (j.status != 0) return;
+        int p = bound_pctx(ji);
+        Time t = now();
+        log(t, "FaultInjected", std::string("\"fault\":\"local\",") + kv("pctx", p) + "," + kv("vctx", ji) + "," +
+                                   kv("code", (long long)code));
+        if (j.running >= 0) recs[j.running].failed = true;
+        for (uint64_t id : j.pending) recs[id].failed = true;
+        j.pending.clear();
+        j.running = -1;
+        j.status = 1;
+        ctr.failed_jobs++;
+        if (p >= 0) {
+            ds_unbind(dom, j.tenant);
+            pctx_bound[p] = -1;
+            ctr.unbinds++;
+            pctx_unavail_until[p] = t + reset_delay_ns;
+            if (next_review < 0 || pctx_unavail_until[p] < next_review) next_review = pctx_unavail_until[p];
+        }
+    }
+    void check_faults() {
+        for (size_t ji = 0; ji < jobs.size(); ++ji) {
+            if (jobs[ji].status != 0) continue;
+            ds_fault_info f;
+            if (ds_tenant_fault(dom, jobs[ji].tenant, &f) == DS_OK && f.code) local_exception((int)ji, f.code);
+        }
     }
 
     // ---- mechanism ----
@@ -456,6 +493,7 @@ struct ds_engine {
                     }
                     work = true;
                 }
+                check_faults();
                 Time t = now();
                 if (hang_detection) hang_check(t);
                 bool review = next_review >= 0 && t >= next_review;
@@ -493,6 +531,7 @@ int ds_engine_create(ds_domain* dom, const ds_engine_config* cfg, ds_engine** ou
     e->hang_detection = cfg->hang_detection != 0;
     if (cfg->hang_threshold > 0) e->hang_threshold = cfg->hang_threshold;
     e->capture_log = cfg->capture_log != 0;
+    if (cfg->reset_delay_ns > 0) e->reset_delay_ns = cfg->reset_delay_ns;
     e->fair_handover = cfg->fair_handover;
     e->lend_tenant = cfg->lend_tenant;
     int np = 0;
@@ -559,6 +598,8 @@ int ds_engine_submit(ds_engine* e, int job, const ds_record_desc* d, uint64_t* r
     r.submit_host = now;
     // arrival floors are non-decreasing per job (engine.cpp:172-176)
     auto& jb = e->jobs[job];
+    // arrivals of a failed vctx are dropped (engine.cpp:810-819)
+    if (jb.status != 0) return efail(DS_TENANT_FAILED, "job failed (local exception)");
     if (!jb.pending.empty() && e->recs[jb.pending.back()].r.arrival > r.r.arrival)
         return efail(DS_CONFIG_ERROR, "kernel arrival floors must be non-decreasing");
     e->recs.push_back(std::move(r));
@@ -602,6 +643,7 @@ int ds_engine_wait(ds_engine* e, uint64_t rec_id, int timeout_ms) {
             std::lock_guard<std::mutex> g(e->mu);
             if (rec_id >= e->recs.size()) return efail(DS_INVALID_ARGUMENT, "unknown record");
             if (e->recs[rec_id].done) return DS_OK;
+            if (e->recs[rec_id].failed) return efail(DS_TENANT_FAILED, "record's job failed (local exception)");
         }
         if (std::chrono::steady_clock::now() > deadline) return efail(DS_TIMEOUT, "record wait timed out");
         std::this_thread::sleep_for(std::chrono::microseconds(20));
@@ -615,7 +657,7 @@ int ds_engine_record(ds_engine* e, uint64_t rec_id, ds_record_info* out) {
     const auto& r = e->recs[rec_id];
     out->id = r.r.id;
     out->job = r.r.job;
-    out->state = r.done ? 2 : (r.dispatched ? 1 : 0);
+    out->state = r.done ? 2 : (r.failed ? 3 : (r.dispatched ? 1 : 0));
     out->pctx = r.pctx;
     out->preempted = r.preempted;
     out->phase = (int)r.r.phase;
@@ -677,6 +719,30 @@ int ds_engine_quarantines(ds_engine* e, int32_t* jobs, int64_t* t_ns, int cap, i
         if (t_ns) t_ns[i] = e->quarantines[i].t;
     }
     *n = (int)e->quarantines.size();
+    return DS_OK;
+}
+
+int ds_engine_fault_local(ds_engine* e, int pctx) {
+    if (!e) return efail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(e->mu);
+    if (pctx < 0 || pctx >= (int)e->pctx_bound.size()) return efail(DS_INVALID_ARGUMENT, "unknown pctx");
+    const int ji = e->pctx_bound[pctx];
+    if (ji < 0) {  // engine.cpp:1051-1058: no bound vctx, no effect
+        e->log(e->now(), "FaultInjected", std::string("\"fault\":\"local\",") + ds_engine::kv("pctx", pctx) +
+                                              ",\"effect\":\"none\"");
+        return DS_OK;
+    }
+    int rc = ds_fault_inject(e->dom, e->jobs[ji].tenant, DS_FAULT_INJECTED);
+    if (rc) return efail(rc, "fault injection");
+    e->local_exception(ji, DS_FAULT_INJECTED);
+    return DS_OK;
+}
+
+int ds_engine_job_status(ds_engine* e, int job, int* status) {
+    if (!e || !status) return efail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(e->mu);
+    if (job < 0 || job >= (int)e->jobs.size()) return efail(DS_INVALID_ARGUMENT, "unknown job");
+    *status = e->jobs[job].status;
     return DS_OK;
 }
 

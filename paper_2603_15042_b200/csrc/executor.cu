@@ -75,14 +75,21 @@ struct Stage {
 // Open launch `seq` if it is enqueued and its word is still closed.  Called by
 // the completer of seq-1 and by the loader after publishing a new tail (the
 // two sides are ordered by fence.sc, Dekker-style, so one of them opens it).
+// A failed tenant never reopens: the fault word is checked before, and after
+// a fence.sc past, the CAS (fault_tenant sets the word, fences, then kills).
 __device__ void try_open(DevTenant* T) {
     for (;;) {
+        if (ld_volatile_u32(&T->fault)) return;
         unsigned long long w = ld_volatile_u64(&T->claim);
         uint32_t s = (uint32_t)(w >> 32), b = (uint32_t)w;
         if (b < kSat) return;
         uint32_t tail = ld_volatile_u32(&T->tail);
         if (s >= tail) return;
-        if (atomicCAS(&T->claim, w, (unsigned long long)s << 32) == w) return;
+        if (atomicCAS(&T->claim, w, (unsigned long long)s << 32) == w) {
+            __threadfence();
+            if (ld_volatile_u32(&T->fault)) kill_claim(T);
+            return;
+        }
     }
 }
 
@@ -151,7 +158,7 @@ __device__ void loader_loop(DevState* st) {
     __shared__ uint32_t known_tail[DS_MAX_TENANTS];
     for (int i = lane; i < DS_MAX_TENANTS; i += 32) known_tail[i] = 0;
     __syncwarp();
-    uint32_t last_gen = 0, last_pgen = 0;
+    uint32_t last_gen = 0, last_pgen = 0, last_fgen = 0;
     uint64_t period = 0, next_flip = 0;
     int phase = 0;
     for (;;) {
@@ -165,6 +172,7 @@ __device__ void loader_loop(DevState* st) {
         const uint32_t ex = __shfl_sync(0xffffffffu, hv.y, 0);
         const uint32_t g = __shfl_sync(0xffffffffu, hv.x, 0);
         const uint32_t pg = __shfl_sync(0xffffffffu, hv.z, 0);
+        const uint32_t fg = __shfl_sync(0xffffffffu, hv.w, 0);
         if (ex) {
             if (lane == 0) {
                 __threadfence();
@@ -212,6 +220,19 @@ __device__ void loader_loop(DevState* st) {
                 if (lane == src) known_tail[t] = to;
                 __syncwarp();
             }
+        }
+        // injected local exceptions (ds_fault_inject): lane t/32 .. per tenant
+        if (fg != last_fgen) {
+            last_fgen = fg;
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            for (int t = lane; t < DS_MAX_TENANTS; t += 32) {
+                const uint32_t code = ld_volatile_u32((const void*)&mb->fault_req[t]);
+                if (code && !ld_volatile_u32(&st->tenants[t].fault)) {
+                    const uint32_t next = (uint32_t)(ld_volatile_u64(&st->tenants[t].claim) >> 32);
+                    fault_tenant(st, t, code, next, 0xffffffffu);
+                }
+            }
+            __syncwarp();
         }
         // control word
         if (g != last_gen) {
@@ -276,6 +297,8 @@ __device__ void open_next(DevTenant* T, uint32_t s) {
     const uint32_t tail = ld_acquire_u32(&T->tail);
     if (nxt < tail) {
         atomicExch(&T->claim, (unsigned long long)nxt << 32);
+        __threadfence();
+        if (ld_volatile_u32(&T->fault)) kill_claim(T);
     } else {
         atomicExch(&T->claim, ((unsigned long long)nxt << 32) | kSat);
         __threadfence();
@@ -558,6 +581,8 @@ __device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0
         c.prev_head = prev_head_of(s.tenant);
         c.seq = s.seq;
         c.dbg = nullptr;
+        c.st = st;
+        c.tenant = s.tenant;
         run_body(s.body, c);
         // the scheduler's release (acq_rel retire atomic after this barrier)
         // publishes this thread's writes at gpu scope
@@ -614,6 +639,8 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     c.prev_head = nullptr;
     c.seq = 0;
     c.dbg = nullptr;
+    c.st = nullptr;
+    c.tenant = -1;
     __shared__ uint32_t tmem_base_sh;
     const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16;
     if (tc_body) {

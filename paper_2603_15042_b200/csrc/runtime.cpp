@@ -199,6 +199,22 @@ std::vector<int> pick_slots(ds_domain* d, int n) {
     return out;
 }
 
+// The device keeps 32-bit launch sequence numbers; widen one against the
+// host's 64-bit count (it is at most 2^32 behind).
+uint64_t widen_seq(uint64_t host_next, uint32_t dev) {
+    uint64_t v = (host_next & ~0xffffffffull) | dev;
+    if (v > host_next) v -= 1ull << 32;
+    return v;
+}
+
+// Launch seq of a tenant will never complete intact (local exception).
+bool seq_failed(ds_domain* d, int tenant, uint64_t seq) {
+    const ds::HostFault& f = d->mb->faults[tenant];
+    if (!f.code) return false;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return seq >= widen_seq(d->tenants[tenant]->next_seq, f.head);
+}
+
 int check_dom(ds_domain* d) {
     if (!d) return fail(DS_INVALID_ARGUMENT, "null domain");
     return DS_OK;
@@ -228,6 +244,7 @@ const char* ds_status_name(int status) {
         case DS_RING_FULL: return "RingFull";
         case DS_INVALID_ARGUMENT: return "InvalidArgument";
         case DS_ALREADY_RUNNING: return "AlreadyRunning";
+        case DS_TENANT_FAILED: return "TenantFailed";
     }
     return "UnknownError";  // errors.cpp:19
 }
@@ -472,6 +489,15 @@ int ds_start(ds_domain* d) {
     for (int t = 0; t < DS_MAX_TENANTS; ++t) {
         uint64_t seq = t < (int)d->tenants.size() ? d->tenants[t]->next_seq : 0;
         uint64_t done = t < (int)d->tenants.size() ? d->tenants[t]->completed.load() : 0;
+        const uint32_t fault = d->mb->faults[t].code;
+        if (fault) {  // a failed tenant stays failed across restarts
+            h.tenants[t].fault = fault;
+            h.tenants[t].claim = ((unsigned long long)seq << 32) | ds::kDead;
+            h.tenants[t].tail = (uint32_t)seq;
+            h.tenants[t].head = (uint32_t)done;
+            d->mb->hot[ds::kHotTail + t] = (uint32_t)seq;
+            continue;
+        }
         if (seq != done) return fail(DS_CONFIG_ERROR, "tenant has launches in flight from a previous run");
         h.tenants[t].claim = ((unsigned long long)seq << 32) | ds::kSat;
         h.tenants[t].tail = (uint32_t)seq;
@@ -508,6 +534,7 @@ int ds_start(ds_domain* d) {
     d->mb->hot[ds::kHotExit] = 0;
     d->mb->periodic_ns = 0;
     d->mb->hot[ds::kHotGen] = 0;
+    d->mb->hot[ds::kHotFGen] = 0;
     DS_CUDA(cudaMemcpyAsync(d->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, d->copy_stream));
     DS_CUDA(cudaStreamSynchronize(d->copy_stream));
     d->drain_stop = false;
@@ -558,10 +585,13 @@ static int launch_impl(ds_domain* d, int tenant, int kernel_id, uint64_t tag, ui
     TenantRecord* t = d->tenants[tenant];
     const KernelRecord& k = d->kernels[kernel_id];
     uint64_t seq = t->next_seq;
+    // arrivals of a failed vctx are dropped (engine.cpp:810-819)
+    if (d->mb->faults[tenant].code) return fail(DS_TENANT_FAILED, "tenant failed (local exception)");
     // ring flow control: slot seq % R is free once seq - R completed
     auto t0 = std::chrono::steady_clock::now();
     while (seq - t->completed.load(std::memory_order_acquire) >= (uint64_t)d->ring_cap) {
         if (!d->running) return fail(DS_RING_FULL, "ring full and executor stopped");
+        if (d->mb->faults[tenant].code) return fail(DS_TENANT_FAILED, "tenant failed (local exception)");
         if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) return fail(DS_RING_FULL, "ring full");
         std::this_thread::yield();
     }
@@ -618,12 +648,59 @@ int ds_wait_tenant(ds_domain* d, int tenant, uint64_t seq, int timeout_ms) {
     if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
     TenantRecord* t = d->tenants[tenant];
     auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms < 0 ? 1 << 30 : timeout_ms);
-    while (t->completed.load(std::memory_order_acquire) <= seq) {
+    for (;;) {
+        if (seq_failed(d, tenant, seq)) return fail(DS_TENANT_FAILED, "tenant failed (local exception)");
+        if (t->completed.load(std::memory_order_acquire) > seq) break;
         if (!d->running) return fail(DS_NOT_RUNNING, "executor not running");
         if (std::chrono::steady_clock::now() > deadline) return fail(DS_TIMEOUT, "wait timed out");
         std::unique_lock<std::mutex> lk(d->comp_mu);
         d->comp_cv.wait_for(lk, std::chrono::microseconds(200));
     }
+    return DS_OK;
+}
+
+int ds_fault_inject(ds_domain* d, int tenant, uint32_t code) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    if (code == 0) return fail(DS_INVALID_ARGUMENT, "fault code must be nonzero");
+    std::lock_guard<std::mutex> g(d->mu);
+    if (d->mb->faults[tenant].code) return DS_OK;  // first fault wins
+    if (!d->running) {  // nothing on the device: record it directly
+        ds::HostFault& f = d->mb->faults[tenant];
+        f.seq = (uint32_t)d->tenants[tenant]->next_seq;
+        f.head = (uint32_t)d->tenants[tenant]->completed.load();
+        f.block = 0xffffffffu;
+        f.t = 0;
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        f.code = code;
+        return DS_OK;
+    }
+    d->mb->fault_req[tenant] = code;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    d->mb->hot[ds::kHotFGen] = d->mb->hot[ds::kHotFGen] + 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    // the loader applies it within one poll; return once it is visible
+    auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(5);
+    while (!d->mb->faults[tenant].code) {
+        if (std::chrono::steady_clock::now() > deadline) return fail(DS_TIMEOUT, "fault not acknowledged");
+        std::this_thread::yield();
+    }
+    return DS_OK;
+}
+
+int ds_tenant_fault(ds_domain* d, int tenant, ds_fault_info* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    const ds::HostFault& f = d->mb->faults[tenant];
+    std::memset(out, 0, sizeof(*out));
+    const uint32_t c = f.code;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (!c) return DS_OK;
+    out->code = c;
+    out->block = f.block;
+    out->seq = widen_seq(d->tenants[tenant]->next_seq, f.seq);
+    out->first_failed = widen_seq(d->tenants[tenant]->next_seq, f.head);
+    out->t_ns = f.t;
     return DS_OK;
 }
 

@@ -112,6 +112,19 @@ class Domain:
     def wait(self, tenant: int, seq: int, timeout_ms: int = 60000):
         check(lib().ds_wait_tenant(self.h, tenant, seq, timeout_ms))
 
+    # -- local exceptions (apply_local_exception, engine.cpp:1049-1083) --
+    def fault_inject(self, tenant: int, code: int = _abi.FAULT_INJECTED):
+        check(lib().ds_fault_inject(self.h, tenant, code))
+
+    def tenant_fault(self, tenant: int) -> Optional[dict]:
+        """None while healthy, else the first fault: {code, block, seq,
+        first_failed, t} (launches >= first_failed never complete intact)."""
+        f = _abi.FaultInfo()
+        check(lib().ds_tenant_fault(self.h, tenant, ctypes.byref(f)))
+        if not f.code:
+            return None
+        return {"code": f.code, "block": f.block, "seq": f.seq, "first_failed": f.first_failed, "t": f.t_ns}
+
     def poll(self, cap: int = 4096) -> List[_abi.Completion]:
         arr = (_abi.Completion * cap)()
         n = ctypes.c_int()
@@ -263,8 +276,9 @@ class Engine:
     def __init__(self, dom: Domain, policy: str = "tpot-first", quantum_ns: int = 5_000_000, alpha: float = 0.3,
                  cold_start_ns: int = 1_000_000_000, release_on_idle: bool = True, fair_handover: bool = True,
                  lend_tenant: int = -1, assignments=None, hang_detection: bool = False, hang_threshold: float = 3.0,
-                 capture_log: bool = False):
+                 capture_log: bool = False, reset_delay_ns: int = 0):
         cfg = _abi.EngineConfig()
+        cfg.reset_delay_ns = reset_delay_ns
         cfg.hang_detection = int(hang_detection)
         cfg.hang_threshold = hang_threshold
         cfg.capture_log = int(capture_log)
@@ -350,6 +364,15 @@ class Engine:
         ts = (ctypes.c_int64 * max(1, n.value))()
         check_engine(lib().ds_engine_quarantines(self.h, jobs, ts, n.value, ctypes.byref(n)))
         return [(jobs[i], ts[i]) for i in range(n.value)]
+
+    def fault_local(self, pctx: int):
+        """FaultSpec{LocalException, pctx} now (engine.cpp:1049-1083)."""
+        check_engine(lib().ds_engine_fault_local(self.h, pctx))
+
+    def job_status(self, job: int) -> int:
+        out = ctypes.c_int()
+        check_engine(lib().ds_engine_job_status(self.h, job, ctypes.byref(out)))
+        return out.value
 
     def transcript(self, job: int) -> List[int]:
         n = ctypes.c_int()
