@@ -13,10 +13,13 @@
 #include "corosim/numlab/equivalence.hpp"
 #include "corosim/numlab/float_format.hpp"
 #include "corosim/numlab/reduction.hpp"
+#include "corosim/policy/policies.hpp"
 #include "corosim/runtime/migration.hpp"
 #include "corosim/rational.hpp"
 
 #include <json.hpp>
+
+#include "policy_case.h"
 
 #include <algorithm>
 #include <chrono>
@@ -316,6 +319,115 @@ int ref_migration_set(const char* regions_nl, const char* touched_sp, int dst, i
         return 0;
     } catch (const std::exception& e) {
         put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
+
+// Every hook of a reference policy on one flat snapshot (oracle/policy_case.h):
+// on_launch, on_congestion (pool_exhausted set), on_completion,
+// launch_order_key, next_review_time, and predict_hol_blocking per pctx.
+int ref_policy_eval(const pc_case* c, pc_result* out) {
+    try {
+        auto sig = [](int i) {
+            return KernelSignature{PC_SIG_NAMES[(i / 2) % 4], (i & 1) ? 128 : 256};
+        };
+        auto R = [](long long x) { return Rational(x); };
+        DurationPredictor pred(Rational(3, 10), R(c->cold_default));
+        for (int i = 0; i < c->n_obs; ++i) pred.observe(sig(c->obs_sig[i]), R(c->obs_dur[i]));
+        PolicyView v;
+        v.now = R(c->now);
+        v.predictor = &pred;
+        v.active_vctx_count = c->active_vctx_count;
+        for (int i = 0; i < c->n_p; ++i) {
+            const pc_pctx& q = c->p[i];
+            PolicyView::PctxEntry e;
+            e.id = PctxId(i);
+            e.device = DeviceId(q.device);
+            e.tier = Rational(BigInt(q.tier_num), BigInt(q.tier_den));
+            e.standby = q.standby != 0;
+            if (q.bound >= 0) e.bound = VctxId(q.bound);
+            e.available = q.available != 0;
+            if (q.running_kernel >= 0) e.running_kernel = KernelId((std::int32_t)q.running_kernel);
+            e.running_signature = sig(q.running_sig);
+            e.running_remaining = R(q.running_remaining);
+            e.running_phase = (Phase)q.running_phase;
+            e.running_priority = (PriorityClass)q.running_priority;
+            for (int k = 0; k < q.n_queued; ++k) e.queued.push_back({sig(q.queued_sig[k]), R(q.queued_hint[k])});
+            v.pctxs.push_back(e);
+        }
+        for (const auto& e : v.pctxs) {  // as the engine's build_view (engine.cpp:345-365)
+            if (e.bound) v.bound_tier_sums[e.device] += e.tier;
+            auto it = v.min_tiers.find(e.device);
+            if (it == v.min_tiers.end() || e.tier < it->second) v.min_tiers[e.device] = e.tier;
+        }
+        for (int i = 0; i < c->n_v; ++i) {
+            const pc_vctx& q = c->v[i];
+            PolicyView::VctxEntry e;
+            e.id = VctxId(i);
+            e.priority = (PriorityClass)q.priority;
+            e.quarantined = q.quarantined != 0;
+            e.bound = q.bound != 0;
+            e.pending = q.pending;
+            e.head_phase = (Phase)q.head_phase;
+            e.decoding = q.decoding != 0;
+            v.vctxs.push_back(e);
+        }
+        Kernel k;
+        k.signature = sig(c->l_sig);
+        k.base_duration = R(c->l_base);
+        k.compute_saturation = Rational(BigInt(c->l_sat_num), BigInt(c->l_sat_den));
+        k.phase = (Phase)c->l_phase;
+        LaunchContext l;
+        l.vctx = VctxId(c->l_vctx);
+        if (c->l_has_kernel) l.kernel = &k;
+        l.request_arrival = R(c->l_request_arrival);
+        if (c->l_has_slo) l.slo = SloSpec{R(c->l_ttft), R(c->l_tpot), std::nullopt};
+        PolicyConfig cfg;
+        static const char* names[4] = {"slo-aware", "tpot-first", "temporal", "static"};
+        cfg.name = names[c->policy];
+        cfg.quantum = R(c->quantum);
+        for (int i = 0; i < c->n_assign; ++i) cfg.assignments[VctxId(c->assign_v[i])] = PctxId(c->assign_p[i]);
+        auto pol = make_policy(cfg);
+        auto put_d = [](const PolicyDecision& d, int32_t* kind, int32_t* target) {
+            *kind = (int32_t)d.kind;  // DispatchDirect, DispatchRemap, DispatchDefer, Preempt, NoAction
+            *target = d.target.value;
+        };
+        put_d(pol->on_launch(v, l), &out->launch_kind, &out->launch_target);
+        put_d(pol->on_completion(v, l), &out->completion_kind, &out->completion_target);
+        LaunchContext lc = l;
+        lc.pool_exhausted = true;
+        put_d(pol->on_congestion(v, lc), &out->congestion_kind, &out->congestion_target);
+        out->order_key = pol->launch_order_key(l);
+        auto r = pol->next_review_time(v);
+        out->has_review = r.has_value();
+        auto to_i64 = [](const Rational& x) -> long long {
+            // integral inputs keep every quantity integral; floor otherwise
+            BigInt q = numerator(x) / denominator(x);
+            return q.convert_to<long long>();
+        };
+        out->review = r ? to_i64(*r) : 0;
+        for (int i = 0; i < c->n_p && i < PC_MAXP; ++i) out->hol[i] = to_i64(predict_hol_blocking(v, v.pctxs[i], pred));
+        return 0;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "ref_policy_eval: %s\n", e.what());
+        return 1;
+    }
+}
+
+// The reference EWMA predictor (predictor.cpp:14-25) over n observations of
+// one signature at alpha = an/ad: floor and ceil of the exact prediction.
+int ref_predict_ewma(int n, const long long* durs, long long an, long long ad, long long* lo, long long* hi) {
+    try {
+        DurationPredictor p(Rational(BigInt(an), BigInt(ad)), Rational(1));
+        KernelSignature sig{"k", 1};
+        for (int i = 0; i < n; ++i) p.observe(sig, Rational(durs[i]));
+        Rational x = p.predict(sig);
+        BigInt q = numerator(x) / denominator(x);
+        *lo = q.convert_to<long long>();
+        *hi = (Rational(q) == x) ? *lo : *lo + 1;
+        return 0;
+    } catch (const std::exception&) {
         return 1;
     }
 }

@@ -1,0 +1,246 @@
+// Differential test: the B200 runtime's policies (csrc/policy.cpp) against the
+// reference's (policies.cpp, compiled unmodified into oracle/_ref) on random
+// PolicyView / LaunchContext snapshots.  Every hook is compared: on_launch,
+// on_congestion, on_completion, launch_order_key, next_review_time and
+// predict_hol_blocking.  Built and run by tests/test_policy_diff.py (no GPU).
+//
+//   policy_diff <libcorosim_ref.so> <cases> <seed>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "../../oracle/policy_case.h"
+#include "../../paper_2603_15042_b200/csrc/policy.hpp"
+
+using namespace detshare;
+
+static KernelSignature sig(int i) { return KernelSignature{PC_SIG_NAMES[(i / 2) % 4], (i & 1) ? 128 : 256}; }
+
+static void native_eval(const pc_case* c, pc_result* out) {
+    DurationPredictor pred(0.3, c->cold_default);
+    for (int i = 0; i < c->n_obs; ++i) pred.observe(sig(c->obs_sig[i]), c->obs_dur[i]);
+    PolicyView v;
+    v.now = c->now;
+    v.predictor = &pred;
+    v.active_vctx_count = c->active_vctx_count;
+    for (int i = 0; i < c->n_p; ++i) {
+        const pc_pctx& q = c->p[i];
+        PolicyView::PctxEntry e;
+        e.id = i;
+        e.device = q.device;
+        e.tier = Frac{q.tier_num, q.tier_den};
+        e.standby = q.standby != 0;
+        if (q.bound >= 0) e.bound = q.bound;
+        e.available = q.available != 0;
+        if (q.running_kernel >= 0) e.running_kernel = (uint64_t)q.running_kernel;
+        e.running_signature = sig(q.running_sig);
+        e.running_remaining = q.running_remaining;
+        e.running_phase = (Phase)q.running_phase;
+        e.running_priority = (PriorityClass)q.running_priority;
+        for (int k = 0; k < q.n_queued; ++k) e.queued.push_back({sig(q.queued_sig[k]), q.queued_hint[k]});
+        v.pctxs.push_back(e);
+    }
+    for (const auto& e : v.pctxs) {  // as ds_engine::build_view
+        if (e.bound) v.bound_tier_sums[e.device] = v.bound_tier_sums.count(e.device)
+                                                       ? v.bound_tier_sums[e.device] + e.tier
+                                                       : e.tier;
+        auto it = v.min_tiers.find(e.device);
+        if (it == v.min_tiers.end() || e.tier < it->second) v.min_tiers[e.device] = e.tier;
+    }
+    for (int i = 0; i < c->n_v; ++i) {
+        const pc_vctx& q = c->v[i];
+        PolicyView::VctxEntry e;
+        e.id = i;
+        e.priority = (PriorityClass)q.priority;
+        e.quarantined = q.quarantined != 0;
+        e.bound = q.bound != 0;
+        e.pending = q.pending;
+        e.head_phase = (Phase)q.head_phase;
+        e.decoding = q.decoding != 0;
+        v.vctxs.push_back(e);
+    }
+    LaunchRecord k;
+    k.signature = sig(c->l_sig);
+    k.base_duration = c->l_base;
+    k.compute_saturation = Frac{c->l_sat_num, c->l_sat_den};
+    k.phase = (Phase)c->l_phase;
+    LaunchContext l;
+    l.vctx = c->l_vctx;
+    if (c->l_has_kernel) l.kernel = &k;
+    l.request_arrival = c->l_request_arrival;
+    if (c->l_has_slo) l.slo = SloSpec{c->l_ttft, c->l_tpot};
+    PolicyConfig cfg;
+    static const char* names[4] = {"slo-aware", "tpot-first", "temporal", "static"};
+    cfg.name = names[c->policy];
+    cfg.quantum = c->quantum;
+    for (int i = 0; i < c->n_assign; ++i) cfg.assignments[c->assign_v[i]] = c->assign_p[i];
+    auto pol = make_policy(cfg);
+    auto put = [](const PolicyDecision& d, int32_t* kind, int32_t* target) {
+        *kind = (int32_t)d.kind;
+        *target = d.target;
+    };
+    put(pol->on_launch(v, l), &out->launch_kind, &out->launch_target);
+    put(pol->on_completion(v, l), &out->completion_kind, &out->completion_target);
+    LaunchContext lc = l;
+    lc.pool_exhausted = true;
+    put(pol->on_congestion(v, lc), &out->congestion_kind, &out->congestion_target);
+    out->order_key = pol->launch_order_key(l);
+    auto r = pol->next_review_time(v);
+    out->has_review = r.has_value();
+    out->review = r ? *r : 0;
+    for (int i = 0; i < c->n_p; ++i) out->hol[i] = predict_hol_blocking(v, v.pctxs[i], pred);
+}
+
+static void gen(std::mt19937_64& g, pc_case* c) {
+    auto U = [&](int64_t lo, int64_t hi) { return std::uniform_int_distribution<int64_t>(lo, hi)(g); };
+    auto P = [&](double p) { return std::uniform_real_distribution<double>(0, 1)(g) < p; };
+    static const int64_t tiers[][2] = {{1, 4}, {1, 2}, {3, 4}, {1, 1}, {1, 3}, {2, 3}, {1, 8}};
+    std::memset(c, 0, sizeof(*c));
+    c->policy = (int)U(0, 3);
+    c->n_v = (int)U(1, PC_MAXV);
+    c->n_p = (int)U(1, 8);
+    c->quantum = U(1, 400);
+    c->now = U(0, 5000);
+    c->cold_default = U(1, 2000);
+    const int devices = P(0.3) ? 2 : 1;
+    bool vbound[PC_MAXV] = {};
+    for (int i = 0; i < c->n_p; ++i) {
+        pc_pctx& q = c->p[i];
+        const int t = (int)U(0, P(0.6) ? 3 : 6);
+        q.tier_num = tiers[t][0];
+        q.tier_den = tiers[t][1];
+        q.device = (int)U(0, devices - 1);
+        q.standby = P(0.08);
+        q.available = !P(0.1);
+        q.bound = -1;
+        if (P(0.45)) {
+            const int vb = (int)U(0, c->n_v - 1);
+            if (!vbound[vb]) {
+                vbound[vb] = true;
+                q.bound = vb;
+            }
+        }
+        q.running_kernel = (q.bound >= 0 && P(0.8)) || P(0.05) ? U(0, 100) : -1;
+        q.running_sig = (int)U(0, PC_NSIG - 1);
+        q.running_phase = (int)U(0, 3);
+        q.running_priority = (int)U(0, 1);
+        q.running_remaining = P(0.2) ? U(0, 3) : U(0, 3000);
+        q.n_queued = P(0.2) ? (int)U(1, PC_MAXQ) : 0;
+        for (int k = 0; k < q.n_queued; ++k) {
+            q.queued_sig[k] = (int)U(0, PC_NSIG - 1);
+            q.queued_hint[k] = U(1, 500);
+        }
+    }
+    int active = 0;
+    for (int i = 0; i < c->n_v; ++i) {
+        pc_vctx& q = c->v[i];
+        q.priority = (int)U(0, 1);
+        q.quarantined = P(0.1);
+        q.bound = P(0.95) ? vbound[i] : !vbound[i];  // mostly consistent with the pctx table
+        q.pending = P(0.3) ? 0 : U(1, 4);
+        q.head_phase = (int)U(0, 3);
+        q.decoding = q.head_phase == 1;
+        active += q.pending > 0 || q.bound;
+    }
+    c->active_vctx_count = P(0.85) ? active : U(0, c->n_v);
+    c->n_obs = (int)U(0, PC_MAXO);
+    bool used[PC_NSIG] = {};
+    int n = 0;
+    for (int i = 0; i < c->n_obs; ++i) {  // one observation per signature: EWMA stays the observation
+        const int s = (int)U(0, PC_NSIG - 1);
+        if (used[s]) continue;
+        used[s] = true;
+        c->obs_sig[n] = s;
+        c->obs_dur[n] = U(1, 1500);
+        ++n;
+    }
+    c->n_obs = n;
+    c->l_vctx = P(0.97) ? (int)U(0, c->n_v - 1) : c->n_v;  // occasionally unknown
+    c->l_has_kernel = 1;  // the engines always pass the head record (pick_bind_target dereferences it)
+    c->l_sig = (int)U(0, PC_NSIG - 1);
+    c->l_phase = (int)U(0, 3);
+    c->l_has_slo = P(0.75);
+    c->l_base = U(1, 1500);
+    const int s = (int)U(0, 6);
+    c->l_sat_num = tiers[s][0];
+    c->l_sat_den = tiers[s][1];
+    c->l_request_arrival = U(0, c->now);
+    c->l_ttft = U(0, 6000);
+    c->l_tpot = P(0.2) ? U(0, 50) : U(0, 4000);
+    c->n_assign = 0;
+    for (int i = 0; i < c->n_v; ++i)
+        if (P(0.7)) {
+            c->assign_v[c->n_assign] = i;
+            c->assign_p[c->n_assign] = (int)U(0, c->n_p - 1);
+            ++c->n_assign;
+        }
+}
+
+int main(int argc, char** argv) {
+    if (argc < 4) return 2;
+    void* h = dlopen(argv[1], RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+        std::printf("dlopen: %s\n", dlerror());
+        return 2;
+    }
+    auto ref_eval = (int (*)(const pc_case*, pc_result*))dlsym(h, "ref_policy_eval");
+    if (!ref_eval) return 2;
+    const long n = std::atol(argv[2]);
+    std::mt19937_64 g(std::strtoull(argv[3], nullptr, 10));
+    // predictor: the native EWMA (double, truncated to ns) stays within 1 ns
+    // of the reference's exact rational EWMA at the default alpha 3/10
+    auto ref_ewma = (int (*)(int, const long long*, long long, long long, long long*, long long*))dlsym(
+        h, "ref_predict_ewma");
+    if (!ref_ewma) return 2;
+    long ewma_off = 0, ewma_exact = 0;
+    for (int t = 0; t < 2000; ++t) {
+        const int m = 1 + (int)(g() % 40);
+        long long d[40];
+        DurationPredictor np(0.3, 1);
+        for (int i = 0; i < m; ++i) {
+            d[i] = 1 + (long long)(g() % (t % 2 ? 5000000ull : 3000ull));
+            np.observe(KernelSignature{"k", 1}, d[i]);
+        }
+        long long lo = 0, hi = 0;
+        if (ref_ewma(m, d, 3, 10, &lo, &hi)) return 2;
+        const long long got = np.predict(KernelSignature{"k", 1});
+        if (got < lo - 1 || got > hi) ++ewma_off;
+        if (got == lo) ++ewma_exact;
+    }
+    std::printf("ewma sequences 2000 outside_1ns %ld equal_floor %ld\n", ewma_off, ewma_exact);
+    if (ewma_off) return 1;
+    long mism = 0, errors = 0;
+    long kinds[4][5] = {};
+    for (long i = 0; i < n; ++i) {
+        pc_case c;
+        gen(g, &c);
+        pc_result a, b;
+        std::memset(&a, 0, sizeof(a));
+        std::memset(&b, 0, sizeof(b));
+        native_eval(&c, &a);
+        if (ref_eval(&c, &b)) {
+            ++errors;
+            continue;
+        }
+        kinds[c.policy][b.launch_kind]++;
+        if (std::memcmp(&a, &b, sizeof(a)) != 0) {
+            if (mism < 5)
+                std::printf("MISMATCH case %ld policy %d: launch %d/%d vs %d/%d, congestion %d/%d vs %d/%d, "
+                            "completion %d/%d vs %d/%d, key %d vs %d, review %d:%lld vs %d:%lld\n",
+                            i, c.policy, a.launch_kind, a.launch_target, b.launch_kind, b.launch_target,
+                            a.congestion_kind, a.congestion_target, b.congestion_kind, b.congestion_target,
+                            a.completion_kind, a.completion_target, b.completion_kind, b.completion_target,
+                            a.order_key, b.order_key, a.has_review, (long long)a.review, b.has_review,
+                            (long long)b.review);
+            ++mism;
+        }
+    }
+    // decision coverage: how often each policy's on_launch took each branch
+    for (int p = 0; p < 4; ++p)
+        std::printf("policy %d on_launch kinds: direct %ld remap %ld defer %ld preempt %ld none %ld\n", p, kinds[p][0],
+                    kinds[p][1], kinds[p][2], kinds[p][3], kinds[p][4]);
+    std::printf("cases %ld mismatches %ld ref_errors %ld\n", n, mism, errors);
+    return mism == 0 && errors == 0 ? 0 : 1;
+}
