@@ -418,6 +418,36 @@ int ds_place_tenants(const ds_tenant_demand* tenants, int n, int n_devices, doub
  * region outside the working set -> DS_TRACE_VIOLATION.  Output arrays hold
  * up to n_ws ids.  ds_migrate_regions copies regions peer to peer (copy
  * engines over NVLink; no SMs taken from the resident executors). */
+/* ---- metrics over measured request outcomes (compute_metrics, metrics.cpp:9-85) ---- */
+typedef struct ds_request_outcome {  /* RequestOutcome engine.hpp:117-125 + RequestMeta :50-57; ns */
+    int32_t inference, completed;
+    int32_t output_tokens, has_slo;
+    int64_t arrival_ns, first_decode_finish_ns, last_finish_ns;
+    int64_t ttft_slo_ns, tpot_slo_ns;
+    int64_t kernels_done;
+} ds_request_outcome;
+
+typedef struct ds_dist {  /* DistSummary metrics.hpp:14-20; percentiles exact (TPOT is a ratio) */
+    int64_t count;
+    double mean;
+    int64_t p50_num, p50_den, p90_num, p90_den, p99_num, p99_den;
+} ds_dist;
+
+typedef struct ds_metrics {  /* MetricsReport metrics.hpp:22-46 (throughputs per ns) */
+    int64_t makespan_ns, kernels_completed, inference_completed, training_kernels_completed;
+    double inference_throughput, training_throughput;
+    ds_dist ttft, tpot;
+    int64_t tpot_excluded, slo_requests, ttft_violations, tpot_violations;
+    double ttft_violation_rate, tpot_violation_rate;
+} ds_metrics;
+
+/* TTFT = first decode finish - arrival (metrics.cpp:46), TPOT = (last - first
+ * decode finish) / (tokens - 1) for >= 2 tokens, nearest-rank percentiles
+ * (k = ceil(pct n / 100), metrics.cpp:9-16), SLO violations strictly above the
+ * deadline; incomplete or non-inference requests count only toward training. */
+int ds_compute_metrics(const ds_request_outcome* reqs, int64_t n, int64_t makespan_ns, int64_t kernels_completed,
+                       ds_metrics* out);
+
 typedef struct ds_region {
     int32_t id;
     int32_t dirty;

@@ -174,3 +174,20 @@ def ref_migration_set(regions, touched, dst: int, full: bool = False) -> str:
     regions: [(id, bytes, dirty, [places])]."""
     text = "\n".join(f"{i} {b} {int(d)} {','.join(map(str, p)) or '-'}" for i, b, d, p in regions)
     return _call(reference().ref_migration_set, text.encode(), " ".join(map(str, touched)).encode(), dst, int(full))
+
+
+def ref_compute_metrics(outcomes, makespan: int, kernels_completed: int) -> dict:
+    """compute_metrics of the reference (metrics.cpp:35-85) over outcomes
+    [dict(inference, completed, output_tokens, has_slo, arrival, first, last,
+    ttft_slo, tpot_slo, kernels_done)] with integer times; exact Fractions."""
+    n = len(outcomes)
+    I = lambda k: (ctypes.c_int * max(1, n))(*[int(o[k]) for o in outcomes])
+    L = lambda k: (ctypes.c_longlong * max(1, n))(*[int(o[k]) for o in outcomes])
+    text = _call(reference().ref_compute_metrics, ctypes.c_longlong(n), I("inference"), I("completed"),
+                 I("output_tokens"), I("has_slo"), L("arrival"), L("first"), L("last"), L("ttft_slo"),
+                 L("tpot_slo"), L("kernels_done"), ctypes.c_longlong(makespan), ctypes.c_longlong(kernels_completed))
+    out = {}
+    for line in text.splitlines():
+        k, v = line.split()
+        out[k] = Fraction(v) if "/" in v else int(v)
+    return out

@@ -432,4 +432,59 @@ int ref_predict_ewma(int n, const long long* durs, long long an, long long ad, l
     }
 }
 
+// compute_metrics (metrics.cpp:35-85) over request outcomes given as
+// parallel arrays (integer times).  Output: "key num/den" lines, exact.
+int ref_compute_metrics(long long n, const int* inference, const int* completed, const int* tokens,
+                        const int* has_slo, const long long* arrival, const long long* first,
+                        const long long* last, const long long* ttft_slo, const long long* tpot_slo,
+                        const long long* kernels_done, long long makespan, long long kernels_completed, char* out,
+                        long cap) {
+    try {
+        SimulationReport rep;
+        rep.end_clock = Rational(makespan);
+        rep.kernels_completed = kernels_completed;
+        for (long long i = 0; i < n; ++i) {
+            RequestOutcome r;
+            r.meta.id = RequestId((std::int32_t)i);
+            r.meta.arrival = Rational(arrival[i]);
+            r.meta.inference = inference[i] != 0;
+            r.meta.output_tokens = tokens[i];
+            if (has_slo[i]) r.meta.slo = SloSpec{Rational(ttft_slo[i]), Rational(tpot_slo[i]), std::nullopt};
+            r.completed = completed[i] != 0;
+            r.first_decode_finish = Rational(first[i]);
+            r.last_finish = Rational(last[i]);
+            r.kernels_done = (int)kernels_done[i];
+            rep.requests.push_back(r);
+        }
+        MetricsReport m = compute_metrics(rep);
+        std::ostringstream os;
+        auto q = [&](const char* k, const Rational& x) { os << k << ' ' << numerator(x).str() << '/' << denominator(x).str() << '\n'; };
+        auto dist = [&](const char* k, const DistSummary& d) {
+            os << k << "_count " << d.count << '\n';
+            if (d.count == 0) return;
+            std::string b(k);
+            q((b + "_mean").c_str(), d.mean);
+            q((b + "_p50").c_str(), d.p50);
+            q((b + "_p90").c_str(), d.p90);
+            q((b + "_p99").c_str(), d.p99);
+        };
+        os << "inference_completed " << m.inference_completed << '\n';
+        os << "training_kernels_completed " << m.training_kernels_completed << '\n';
+        os << "tpot_excluded " << m.tpot_excluded << '\n';
+        os << "slo_requests " << m.slo_requests << '\n';
+        os << "ttft_violations " << m.ttft_violations << '\n';
+        os << "tpot_violations " << m.tpot_violations << '\n';
+        q("inference_throughput", m.inference_throughput);
+        q("training_throughput", m.training_throughput);
+        q("ttft_violation_rate", m.ttft_violation_rate);
+        q("tpot_violation_rate", m.tpot_violation_rate);
+        dist("ttft", m.ttft);
+        dist("tpot", m.tpot);
+        return put(os.str(), out, cap);
+    } catch (const std::exception& e) {
+        put(std::string("error: ") + e.what(), out, cap);
+        return 1;
+    }
+}
+
 }  // extern "C"

@@ -292,6 +292,27 @@ class FaultInfo(ctypes.Structure):
                 ("first_failed", ctypes.c_uint64), ("t_ns", ctypes.c_uint64)]
 
 
+class RequestOutcome(ctypes.Structure):
+    _fields_ = [("inference", ctypes.c_int32), ("completed", ctypes.c_int32), ("output_tokens", ctypes.c_int32),
+                ("has_slo", ctypes.c_int32), ("arrival_ns", ctypes.c_int64), ("first_decode_finish_ns", ctypes.c_int64),
+                ("last_finish_ns", ctypes.c_int64), ("ttft_slo_ns", ctypes.c_int64), ("tpot_slo_ns", ctypes.c_int64),
+                ("kernels_done", ctypes.c_int64)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64), ("mean", ctypes.c_double)] + [
+        (f"{p}_{x}", ctypes.c_int64) for p in ("p50", "p90", "p99") for x in ("num", "den")]
+
+
+class Metrics(ctypes.Structure):
+    _fields_ = [("makespan_ns", ctypes.c_int64), ("kernels_completed", ctypes.c_int64),
+                ("inference_completed", ctypes.c_int64), ("training_kernels_completed", ctypes.c_int64),
+                ("inference_throughput", ctypes.c_double), ("training_throughput", ctypes.c_double),
+                ("ttft", Dist), ("tpot", Dist), ("tpot_excluded", ctypes.c_int64), ("slo_requests", ctypes.c_int64),
+                ("ttft_violations", ctypes.c_int64), ("tpot_violations", ctypes.c_int64),
+                ("ttft_violation_rate", ctypes.c_double), ("tpot_violation_rate", ctypes.c_double)]
+
+
 class RequestTemplate(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("prompt_tokens", ctypes.c_int), ("prompt_tokens_max", ctypes.c_int),
                 ("output_tokens", ctypes.c_int), ("output_tokens_max", ctypes.c_int), ("iterations", ctypes.c_int),
@@ -351,6 +372,7 @@ EXPORTS = [
     "ds_engine_event_log", "ds_engine_quarantines", "ds_quota_triggers_reset",
     "ds_compute_migration_set", "ds_full_eager_set", "ds_migrate_regions",
     "ds_fault_inject", "ds_tenant_fault", "ds_engine_fault_local", "ds_engine_job_status",
+    "ds_compute_metrics",
 ]
 
 _lib = None
@@ -451,6 +473,8 @@ def lib():
         L.ds_fault_inject.argtypes = [vp, ctypes.c_int, ctypes.c_uint32]
         L.ds_tenant_fault.argtypes = [vp, ctypes.c_int, ctypes.POINTER(FaultInfo)]
         L.ds_engine_fault_local.argtypes = [vp, ctypes.c_int]
+        L.ds_compute_metrics.argtypes = [ctypes.POINTER(RequestOutcome), ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.POINTER(Metrics)]
         L.ds_engine_job_status.argtypes = [vp, ctypes.c_int, ip_]
         L.ds_place_tenants.argtypes = [ctypes.POINTER(TenantDemand), ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                        ctypes.POINTER(ctypes.c_int32)]
