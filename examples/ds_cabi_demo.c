@@ -7,7 +7,8 @@
  * 1. gen_burst (reference trace.cpp:204-232) -> a bursty request stream
  * 2. expand_workload (workload.cpp:51-174) -> kernel records per request
  * 3. place_tenants -> a 16-tenant mix partitioned over 8 GPUs
- * 4. the error path: an invalid tier pool is refused with a status code
+ * 4. compute_metrics (metrics.cpp:35-85) over request outcomes
+ * 5. the error path: an invalid tier pool is refused with a status code
  *    (InvalidTier on a GPU host, create_pool types.cpp:87-98; NoDevice on a
  *    CPU host, where the device probe comes first). */
 #include <stdio.h>
@@ -41,6 +42,18 @@ int main(void) {
     printf("placement");
     for (int i = 0; i < 16; ++i) printf(" %d", where[i]);
     printf("\n");
+
+    /* three requests: TTFT 5/7/9 us, TPOTs 10/3, 2, 4 us, SLO tpot 3.5 us */
+    ds_request_outcome o[3] = {
+        {1, 1, 4, 1, 0, 5000, 15000, 8000, 3500, 0},
+        {1, 1, 2, 1, 1000, 8000, 10000, 8000, 3500, 0},
+        {1, 1, 3, 1, 2000, 11000, 19000, 8000, 3500, 0},
+    };
+    ds_metrics m;
+    if (ds_compute_metrics(o, 3, 20000, 0, &m) != DS_OK) return 1;
+    printf("metrics ttft_p99 %lld/%lld tpot_p50 %lld/%lld tpot_violations %lld\n", (long long)m.ttft.p99_num,
+           (long long)m.ttft.p99_den, (long long)m.tpot.p50_num, (long long)m.tpot.p50_den,
+           (long long)m.tpot_violations);
 
     ds_domain_config bad = {0};
     bad.n_tiers = 1;

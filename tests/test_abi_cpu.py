@@ -81,4 +81,6 @@ def test_plain_c_caller_links_and_runs(tmp_path):
     assert n > 0 and "kernels" in out[0]
     where = [int(x) for x in out[1].split()[1:]]
     assert sorted(set(where)) == list(range(8))
-    assert out[2].split("-> ")[1] in ("InvalidTier", "NoDevice")
+    # metrics: TTFT p99 9000 ns; TPOT p50 = 10000/3 (exact); one TPOT above 3.5 us
+    assert out[2] == "metrics ttft_p99 9000/1 tpot_p50 10000/3 tpot_violations 1"
+    assert out[3].split("-> ")[1] in ("InvalidTier", "NoDevice")
