@@ -217,6 +217,13 @@ int ds_bound_pctx(ds_domain* dom, int tenant, int* pctx);
  * when the owner has no claimable block; -1 = none */
 int ds_quota_set(ds_domain* dom, const int32_t* owner, const int32_t* lender, int n);
 int ds_quota_get(ds_domain* dom, int32_t* owner, int32_t* lender, int n);
+/* Lane split: every SM owned by a tenant also runs the lend tenant on its
+ * second worker lane (mode 1: lane 0 runs the owner, then the lend tenant when
+ * the owner has nothing; mode 2: lane 0 runs the owner only).  A memory-bound
+ * owner (decode) and a compute-bound lender (training GEMM) then share each SM
+ * instead of splitting the SM set.  Modes 3, 4: as 1, 2 on every other owned
+ * SM only (the rest keep both lanes for the owner).  0 = off (default). */
+int ds_set_lane_split(ds_domain* dom, int mode);
 int ds_set_lend(ds_domain* dom, int lend_tenant); /* tenant allowed on idle SMs (-1 none) */
 /* device-side control program: when tenant's launch `seq` has claimed `block`
  * blocks, install owner/lender (n entries).  Used for exact mid-kernel

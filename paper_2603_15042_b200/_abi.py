@@ -372,7 +372,7 @@ EXPORTS = [
     "ds_engine_event_log", "ds_engine_quarantines", "ds_quota_triggers_reset",
     "ds_compute_migration_set", "ds_full_eager_set", "ds_migrate_regions",
     "ds_fault_inject", "ds_tenant_fault", "ds_engine_fault_local", "ds_engine_job_status",
-    "ds_compute_metrics",
+    "ds_compute_metrics", "ds_set_lane_split",
 ]
 
 _lib = None
@@ -473,6 +473,7 @@ def lib():
         L.ds_fault_inject.argtypes = [vp, ctypes.c_int, ctypes.c_uint32]
         L.ds_tenant_fault.argtypes = [vp, ctypes.c_int, ctypes.POINTER(FaultInfo)]
         L.ds_engine_fault_local.argtypes = [vp, ctypes.c_int]
+        L.ds_set_lane_split.argtypes = [vp, ctypes.c_int]
         L.ds_compute_metrics.argtypes = [ctypes.POINTER(RequestOutcome), ctypes.c_int64, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.POINTER(Metrics)]
         L.ds_engine_job_status.argtypes = [vp, ctypes.c_int, ip_]

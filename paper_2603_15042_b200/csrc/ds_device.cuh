@@ -77,6 +77,14 @@ struct ClaimTrigger {
     int32_t lender[DS_MAX_SMS];
 };
 
+// Owner-field flags of a control word (owner >= 0 only): lane split — the
+// SM's two worker lanes serve different tenants.  Lane 1 claims the lender
+// first (then the owner); with kCtlOwnerOnly0, lane 0 never runs the lender.
+// A memory-bound owner and a compute-bound lender then share every SM.
+constexpr int32_t kCtlSplit = 1 << 30;
+constexpr int32_t kCtlOwnerOnly0 = 1 << 29;
+constexpr int32_t kCtlTenantMask = 0xffff;
+
 struct alignas(128) DevControl {
     unsigned long long word[DS_MAX_SMS];  // by physical smid: (lender << 32) | owner, -1 = none
     uint32_t gen;                // bumped on every control change (any source)

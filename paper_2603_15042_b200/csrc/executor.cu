@@ -462,10 +462,25 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                 const uint32_t ex = ld_volatile_u32(&st->ctl.exit);
                 const unsigned long long cw = ld_volatile_u64(&st->ctl.word[sm]);
                 if (ex) { exit_now = true; break; }
-                const int32_t ow = (int32_t)(uint32_t)cw;
+                int32_t ow = (int32_t)(uint32_t)cw;
                 const int32_t ln = (int32_t)(uint32_t)(cw >> 32);
-                if (ow >= 0 && ow < DS_MAX_TENANTS && try_claim(st, ow, w, cc)) { got = true; break; }
-                if (ln >= 0 && ln < DS_MAX_TENANTS && ln != ow && try_claim(st, ln, w, cc)) { got = true; break; }
+                int32_t first = ow, second = ln;
+                if (ow >= 0) {
+                    ow &= kCtlTenantMask;
+                    first = ow;
+                    const int32_t f = (int32_t)(uint32_t)cw;
+                    if ((f & kCtlSplit) && lane_id == 1) {
+                        first = ln;
+                        second = ow;
+                    } else if ((f & kCtlOwnerOnly0) && lane_id == 0) {
+                        second = -1;
+                    }
+                }
+                if (first >= 0 && first < DS_MAX_TENANTS && try_claim(st, first, w, cc)) { got = true; break; }
+                if (second >= 0 && second < DS_MAX_TENANTS && second != first && try_claim(st, second, w, cc)) {
+                    got = true;
+                    break;
+                }
                 if (!idle_logged && last_tenant != -1 && st->slog_cap) {
                     unsigned long long i = atomicAdd(&st->slog_count, 1ull);
                     if (i < st->slog_cap) {

@@ -90,6 +90,8 @@ struct ds_domain {
     int ring_cap = 1024;
     int lend_idle = 1;
     int lend_tenant = -1;
+    int lane_split = 0;  // 1: owned SMs run the lend tenant on lane 1; 2: and lane 0 runs the owner only;
+                         // 3, 4: as 1, 2 on every other owned SM
 
     cudaStream_t exec_stream = nullptr, copy_stream = nullptr;
     ds::DevState* d_state = nullptr;
@@ -176,6 +178,13 @@ int push_control(ds_domain* d) {
         // (a latency-critical owner would wait a whole foreign block on every
         // kernel boundary)
         if (d->lend_idle && l < 0 && o < 0 && d->lend_tenant >= 0) l = d->lend_tenant;
+        // lane split: the owner's SMs also run the lend tenant on their second lane
+        // (modes 3, 4: the same on every other owned SM only)
+        if (d->lane_split && o >= 0 && d->lend_tenant >= 0 && d->lend_tenant != o &&
+            (d->lane_split <= 2 || (s & 1))) {
+            l = d->lend_tenant;
+            o |= ds::kCtlSplit | (d->lane_split % 2 == 0 ? ds::kCtlOwnerOnly0 : 0);
+        }
         d->mb->owner[sm] = o;
         d->mb->lender[sm] = l;
     }
@@ -738,6 +747,14 @@ int ds_quota_get(ds_domain* d, int32_t* owner, int32_t* lender, int n) {
         if (lender) lender[i] = d->lender[i];
     }
     return DS_OK;
+}
+
+int ds_set_lane_split(ds_domain* d, int mode) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    if (mode < 0 || mode > 4) return fail(DS_INVALID_ARGUMENT, "lane split mode is 0..4");
+    std::lock_guard<std::mutex> g(d->mu);
+    d->lane_split = mode;
+    return d->running ? push_control(d) : DS_OK;
 }
 
 int ds_set_lend(ds_domain* d, int lend_tenant) {

@@ -15,22 +15,11 @@ import torch
 
 from paper_2603_15042_b200 import _abi
 from paper_2603_15042_b200._abi import DsError
-from paper_2603_15042_b200.runtime import Domain, Engine, solo_launch
+from paper_2603_15042_b200.runtime import Domain, Engine
 from paper_2603_15042_b200.tenants import DecodeConfig, DecodeModel
+from gpu_util import sgemm_copies as _sgemm
 
 pytestmark = pytest.mark.gpu
-
-
-def _sgemm(M=1024, N=1024, K=1024, copies=1):
-    g = torch.Generator(device="cuda").manual_seed(11)
-    A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
-    B = torch.rand(K, N, device="cuda", generator=g) * 2 - 1
-    Cs = [torch.zeros(M, N, device="cuda") for _ in range(copies + 1)]
-    args = [_abi.SgemmArgs(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, 0) for C in Cs]
-    grid = (N // 64, M // 64, 1)
-    solo_launch(0, "sgemm", _abi.BODY_SGEMM, grid, args[0])  # reference result in Cs[0]
-    torch.cuda.synchronize()
-    return (A, B, Cs), args, grid
 
 
 def test_injected_fault_mid_decode_leaves_training_bit_exact():
@@ -173,3 +162,4 @@ def test_engine_local_exception_fails_the_bound_job_only():
     ref = got[0].numpy().view(np.uint32)
     for C in got[1:]:
         assert np.array_equal(C.numpy().view(np.uint32), ref)
+
