@@ -730,7 +730,7 @@ extern "C" cudaError_t ds_dev_probe(int nblocks, uint32_t* smids, uint32_t* nsmi
 extern "C" uint32_t ds_dev_body_smem(int body) {
     switch (body) {
         case DS_BODY_REDUCE_CHUNKS: return 16384 * 4 + 1024;
-        case DS_BODY_SGEMM: return (32 * 68 + 32 * 64) * 4 + 1024;
+        case DS_BODY_SGEMM: return (64 * ds::kSgA + 32 * 64) * 4 + 1024;
         case DS_BODY_SPIN: return 1024;
         case DS_BODY_GEMM_BF16: return ds::TcSmem<ds::kGemmBN, ds::kGemmStages>::kBytes + 1024;
         case DS_BODY_GEMV_BF16: {
