@@ -31,18 +31,30 @@ for name, a in variants.items():
     gk[name] = dom.kernel("train/" + name, _abi.BODY_GEMM_BF16, _abi.gemm_grid(8192, 8192, bn), a)
 dom.start()
 n = dom.num_sms
-dom.quota_set([td if i < n // 2 else tt for i in range(n)])
+smids = dom.smids()
+order = sorted(range(n), key=lambda i: smids[i])
+low = set(order[: n // 2])  # the engine's pick_slots: lowest smids (whole TPCs) first
+layouts = {"slot_order": [td if i < n // 2 else tt for i in range(n)]}
+_unused = {
+           "low_smids": [td if i in low else tt for i in range(n)],
+           "even_smids": [td if smids[i] % 4 < 2 else tt for i in range(n)]}
+if os.environ.get("LAYOUTS"):
+    layouts = {k: v for k, v in layouts.items() if k in os.environ["LAYOUTS"].split(",")}
+only = os.environ.get("VARIANTS", "")
+if only:
+    variants = {k: v for k, v in variants.items() if k in only.split(",")}
 res = {}
-for name in variants:
+for (lname, owner), name in [(lo, v) for lo in layouts.items() for v in variants]:
+    dom.quota_set(owner)
     tseqs = []
     if name != "none":
-        tseqs = [dom.launch(tt, gk[name]) for _ in range(70)]
+        tseqs = [dom.launch(tt, gk[name]) for _ in range(int(os.environ.get("GEMMS", "70")))]
     for k in kids:
         last = dom.launch(td, k)
     dom.wait(td, last)
     dom.poll(1 << 20)
     steps = []
-    for _ in range(6):
+    for _ in range(int(os.environ.get("STEPS", "6"))):
         for k in kids:
             last = dom.launch(td, k)
         dom.wait(td, last)
@@ -53,7 +65,11 @@ for name in variants:
     if tseqs:
         dom.wait(tt, tseqs[-1], 120000)
         tc = [c for c in dom.poll(1 << 20) if c.tenant == tt]
-    res[name] = {"decode_step_ms": round(statistics.median(steps), 3)}
-    print(name, res[name], flush=True)
+    res[lname + "/" + name] = {"decode_step_ms": round(statistics.median(steps), 3),
+                               "first_last": [round(steps[0], 3), round(steps[-1], 3)]}
+    print(lname + "/" + name, res[lname + "/" + name], flush=True)
+print("smids of the first 8 slots", smids[:8])
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump(res, open("gpurun_out/interference.json", "w"), indent=1)
 dom.stop()
 dom.close()
