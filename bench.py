@@ -625,6 +625,123 @@ def cpu_baseline_leg(solo, requests, tokens, budget_s=10.0):
                       f"calibrated with measured solo durations; {ev} events in {wall:.2f} s wall"}
 
 
+def _ref_timed(sc, reps_budget_s=2.0, equivalence=False):
+    """simulate (and optionally check_immutable_equivalence) of one reference
+    scenario, repeated until ~reps_budget_s of CPU work; per-run wall time."""
+    from oracle import loader
+    text = json.dumps(sc)
+    runs, wall, out, eq = 0, 0.0, None, None
+    while runs == 0 or (wall < reps_budget_s and runs < 20):
+        out = json.loads(loader.ref_simulate(text))
+        wall += out["wall_ns"] / 1e9
+        if equivalence:
+            eq = json.loads(loader.ref_equivalence(text))
+            wall += eq["wall_ns"] / 1e9
+        runs += 1
+    return out, eq, wall / runs, runs
+
+
+def cpu_reference_configs(c1_solo_us, step_us, gemm_us, resnet_iter_us):
+    """the reference simulator (oracle/_ref, 1 host core) timed
+    on each config's scenario beside the GPU numbers.  Time unit 1 us,
+    calibrated with the measured B200 durations."""
+    import multiprocessing
+    out = {}
+    # config 1: one SGEMM kernel (256 logical blocks, a yield point per
+    # block); a soft hang at 30% is detected (3x prediction) and the kernel
+    # is quarantined 1 -> 1/4 mid-run: the reference's quota change
+    c1 = max(1, int(c1_solo_us))
+    sc1 = {"devices": [{"tiers": ["0.25", "1"]}], "policy": "slo-aware", "segments_per_kernel": 256,
+           "hang_detection": True,
+           "faults": [{"kind": "soft_hang", "pctx": 1, "time": str(int(0.3 * c1)), "stretch": "10"}],
+           "profiles": {"training": {"sgemm": {"iteration_cost": str(c1), "saturation": "1", "mem_bound": "0.1",
+                                               "grid": 256}}},
+           "workload": {"records": [{"arrival_time": "0", "job_id": "sgemm", "kind": "training", "iterations": 1,
+                                     "priority": "best_effort", "profile": "sgemm"}]}}
+    r, eq, per, runs = _ref_timed(sc1, equivalence=True)
+    out["config1"] = {"wall_us_per_run": round(per * 1e6, 1), "runs": runs, "cores": 1,
+                      "equivalent": eq["equivalent"], "kernels_completed": r["kernels_completed"],
+                      "sim_preemptions": r["preemptions"],
+                      "what": "simulate + check_immutable_equivalence (J+1 runs) of the SGEMM scenario"}
+    # config 3: periodic switching between two tenants (temporal policy with
+    # quantum = period); the model's preempt ledger beside the measured yields
+    rows = []
+    for period in (50, 200, 1000, 5000):
+        sc3 = {"devices": [{"tiers": ["0.25", "1"]}], "policy": "temporal", "policy_params": {"quantum": str(period)},
+               "segments_per_kernel": 16,
+               "profiles": {"training": {"g": {"iteration_cost": str(gemm_us), "saturation": "1", "grid": 2048}}},
+               "workload": {"records": [
+                   {"arrival_time": "0", "job_id": "a", "kind": "training", "iterations": 8, "priority": "best_effort",
+                    "profile": "g"},
+                   {"arrival_time": "0", "job_id": "b", "kind": "training", "iterations": 8, "priority": "best_effort",
+                    "profile": "g"}]}}
+        r, _, per, runs = _ref_timed(sc3, reps_budget_s=0.5)
+        ov = r["metrics"].get("overheads", {})
+        rows.append({"period_us": period, "wall_us_per_run": round(per * 1e6, 1), "runs": runs,
+                     "preemptions": ov.get("preemptions"), "preempt_total_us": ov.get("preempt_total"),
+                     "migrations": ov.get("migrations"), "ctx_switches": ov.get("ctx_switches")})
+    out["config3"] = {"cores": 1, "sweep": rows,
+                      "what": "temporal-policy scenario per period (the reference has no quota timer; its "
+                              "time-sliced owner change is the closest periodic switch). It shows 0 preemptions: "
+                              "a bound holder keeps the full tier across quanta (SURVEY 8-appendix #1)"}
+    # config 4: the ResNet-50 training stream (one kernel per iteration at the
+    # measured iteration time) beside bursty decode (same gen_burst stream)
+    from paper_2603_15042_b200 import workload as wl
+    reqs = wl.gen_burst(0.5, 4.0, 2.0, 20.0, 60.0, wl.RequestTemplate(output_tokens=4), seed=0)
+    unit = 50_000  # us per trace time unit, as the GPU leg
+    recs = [{"arrival_time": "0", "job_id": "resnet", "kind": "training",
+             "iterations": int(60 * unit / max(1, resnet_iter_us)) + 2, "priority": "best_effort",
+             "profile": "resnet"}]
+    for i, q in enumerate(reqs):
+        recs.append({"arrival_time": str(int(q.arrival_q * unit // 10**9)), "job_id": "chat", "kind": "inference",
+                     "prompt_tokens": 8, "output_tokens": 4, "priority": "latency_critical",
+                     "slo": {"ttft": "150000", "tpot": str(3 * step_us)}})
+    sc4 = {"devices": [{"tiers": ["0.25", "0.5", "0.75", "1"]}], "policy": "tpot-first", "segments_per_kernel": 16,
+           "event_budget": 100000000,
+           "profiles": {"inference": {"default": {"decode_cost": str(step_us), "prefill_cost_per_token": "1",
+                                                  "decode_saturation": "0.75", "decode_mem_bound": "0.8",
+                                                  "decode_bw_demand": "0.75", "decode_grid": 163}},
+                        "training": {"resnet": {"iteration_cost": str(resnet_iter_us), "saturation": "0.25",
+                                                "mem_bound": "0.3", "bw_demand": "0.25", "grid": 161}}},
+           "workload": {"records": recs}}
+    r, _, per, runs = _ref_timed(sc4, reps_budget_s=2.0)
+    tp = r["metrics"]["tpot"].get("p99")
+    out["config4"] = {"wall_ms_per_run": round(per * 1e3, 2), "runs": runs, "cores": 1, "requests": len(reqs),
+                      "sim_p99_tpot_ms": float(tp) / 1000 if tp is not None else None, "events": r["events"]}
+    # config 5: one 8-device engine with the 16-tenant mix, and 8 per-device
+    # engines on 8 threads (ctypes releases the GIL inside the call)
+    def mix(devs, jobs_per_dev):
+        recs = []
+        for j in range(jobs_per_dev * devs):
+            if j % 2 == 0:
+                for r_ in range(8):
+                    recs.append({"arrival_time": str(1000 + r_ * 8 * step_us * 2), "job_id": f"chat{j}",
+                                 "kind": "inference", "prompt_tokens": 8, "output_tokens": 8,
+                                 "priority": "latency_critical", "slo": {"ttft": str(8 * step_us), "tpot": str(3 * step_us)}})
+            else:
+                recs.append({"arrival_time": "0", "job_id": f"train{j}", "kind": "training", "iterations": 100,
+                             "priority": "best_effort", "profile": "gemm"})
+        recs.sort(key=lambda x: int(x["arrival_time"]))
+        return {"devices": [{"tiers": ["0.25", "0.5", "0.75", "1"]} for _ in range(devs)], "policy": "tpot-first",
+                "segments_per_kernel": 16, "event_budget": 100000000,
+                "profiles": {"inference": {"default": {"decode_cost": str(step_us), "prefill_cost_per_token": "1",
+                                                       "decode_saturation": "0.5", "decode_grid": 163}},
+                             "training": {"gemm": {"iteration_cost": str(gemm_us), "saturation": "0.5",
+                                                   "grid": 2048}}},
+                "workload": {"records": recs}}
+    r, _, per, runs = _ref_timed(mix(8, 2), reps_budget_s=2.0)
+    from concurrent.futures import ThreadPoolExecutor
+    import time as _t
+    t0 = _t.perf_counter()
+    with ThreadPoolExecutor(8) as ex:
+        list(ex.map(lambda _: _ref_timed(mix(1, 2), reps_budget_s=0.0), range(8)))
+    par = _t.perf_counter() - t0
+    out["config5"] = {"one_engine_8_devices_ms": round(per * 1e3, 2), "runs": runs, "events": r["events"],
+                      "eight_engines_on_8_threads_ms": round(par * 1e3, 2), "nproc": multiprocessing.cpu_count(),
+                      "cores": 8}
+    return out
+
+
 def config4b_leg(co, args, solo):
     """Two chat streams with prefill (256-token prompts) + the training GEMM:
     TPOT-First vs the reference default (slo-aware) vs time slicing, in P99
@@ -1171,6 +1288,21 @@ def main():
                 out["cpu_baseline"] = cpu_baseline_leg(solo, args.steps, args.tokens)
             except Exception as e:
                 out["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+            # the reference simulator on every other config's scenario
+            try:
+                c1 = out.get("config1") or {}
+                c4 = out.get("config4") or {}
+                refs = cpu_reference_configs(
+                    c1_solo_us=1000 * float(c1.get("solo_ms", 0.1)),
+                    step_us=max(1, int(1000 * solo["decode_step_ms"])), gemm_us=max(1, int(1000 * solo["gemm_ms"])),
+                    resnet_iter_us=max(1, int(1000 * float(c4.get("resnet_solo_iter_ms", 10.0)))))
+                for k, v in refs.items():
+                    if isinstance(out.get(k), dict):
+                        out[k]["cpu_reference"] = v
+                    else:
+                        out.setdefault("cpu_reference", {})[k] = v
+            except Exception as e:
+                out["cpu_reference_error"] = repr(e)
         print(json.dumps(out))
 
 
