@@ -11,6 +11,8 @@ from paper_2603_15042_b200.tenants import DecodeModel, DecodeConfig
 layers = int(os.environ.get("LAYERS", "8"))
 base = os.environ.get("BASE", "qkv:3,o:3,gu:2,down:5,lm:1")
 cands = {"qkv": [1, 2, 3, 4], "o": [1, 2, 3, 4], "gu": [1, 2, 3], "down": [2, 3, 4, 5, 7], "lm": [1, 2]}
+if os.environ.get("CANDS"):  # e.g. '{"o": [6, 8], "qkv": [6]}'
+    cands = json.loads(os.environ["CANDS"])
 only = os.environ.get("ONLY", "")
 if only:
     cands = {k: v for k, v in cands.items() if k in only.split(",")}
