@@ -163,7 +163,8 @@ class GemmArgs(ctypes.Structure):
     _fields_ = [("tmA", TmaDesc), ("tmB", TmaDesc), ("C", ctypes.c_uint64), ("M", ctypes.c_int32),
                 ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32),
                 ("splits", ctypes.c_int32), ("ws", ctypes.c_uint64), ("bk", ctypes.c_int32),
-                ("tma_store", ctypes.c_int32), ("pad2", ctypes.c_uint8 * 16), ("tmC", TmaDesc)]  # tmC: alignas(64)
+                ("tma_store", ctypes.c_int32), ("abandon", ctypes.c_int32), ("pad2", ctypes.c_uint8 * 12),
+                ("tmC", TmaDesc)]  # tmC: alignas(64)
 
 
 class SplitkReduceArgs(ctypes.Structure):
@@ -187,7 +188,8 @@ GEMM_BM, GEMM_BN = 128, 256
 
 
 def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16, bn: int = GEMM_BN,
-              splits: int = 1, ws: int = 0, bk: int = 64, tma_store: bool = True) -> "GemmArgs":
+              splits: int = 1, ws: int = 0, bk: int = 64, tma_store: bool = True,
+              abandon: bool = False) -> "GemmArgs":
     if bn not in (64, 128, 256):
         raise DsError(10, f"gemm tile width {bn} not in (64, 128, 256)")
     if M % GEMM_BM or N % bn or K % 64:
@@ -200,6 +202,7 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
     a = GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM, bk), tensor_map_bf16(B, N, K, bn, bk), C, M, N, K, group_m, bn,
                  max(1, splits), ws, bk, int(tma_store))
     a.tmC = tmC
+    a.abandon = int(abandon)
     return a
 
 
@@ -372,7 +375,7 @@ EXPORTS = [
     "ds_engine_event_log", "ds_engine_quarantines", "ds_quota_triggers_reset",
     "ds_compute_migration_set", "ds_full_eager_set", "ds_migrate_regions",
     "ds_fault_inject", "ds_tenant_fault", "ds_engine_fault_local", "ds_engine_job_status",
-    "ds_compute_metrics", "ds_set_lane_split",
+    "ds_compute_metrics", "ds_set_lane_split", "ds_tenant_abandonable",
 ]
 
 _lib = None
@@ -474,6 +477,7 @@ def lib():
         L.ds_tenant_fault.argtypes = [vp, ctypes.c_int, ctypes.POINTER(FaultInfo)]
         L.ds_engine_fault_local.argtypes = [vp, ctypes.c_int]
         L.ds_set_lane_split.argtypes = [vp, ctypes.c_int]
+        L.ds_tenant_abandonable.argtypes = [vp, ctypes.c_int, ctypes.c_int]
         L.ds_compute_metrics.argtypes = [ctypes.POINTER(RequestOutcome), ctypes.c_int64, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.POINTER(Metrics)]
         L.ds_engine_job_status.argtypes = [vp, ctypes.c_int, ip_]

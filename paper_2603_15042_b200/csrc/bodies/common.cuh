@@ -126,6 +126,26 @@ __device__ __forceinline__ void raise_fault(const BodyCtx& c, uint32_t code) {
     fault_tenant(c.st, c.tenant, code, c.seq, c.bx + c.gx * (c.by + c.gy * c.bz));
 }
 
+// ---------------------------------------------------------------------------
+// Abandonable blocks (sub-block yields): a body may give its block up when
+// this SM no longer serves its tenant; the block re-runs from scratch later
+// (same code, same inputs: bit-identical), so no partial state is kept.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool serves_tenant(unsigned long long cw, int tenant) {
+    int32_t ow = (int32_t)(uint32_t)cw;
+    if (ow >= 0) ow &= kCtlTenantMask;
+    const int32_t ln = (int32_t)(uint32_t)(cw >> 32);
+    return ow == tenant || ln == tenant;
+}
+
+__device__ __forceinline__ unsigned long long ctl_word_here(const BodyCtx& c) {
+    return ld_volatile_u64(&c.st->ctl.word[smid()]);
+}
+
+__device__ __forceinline__ bool revoked_here(const BodyCtx& c) {
+    return ld_volatile_u32(&c.st->ctl.exit) != 0u || !serves_tenant(ctl_word_here(c), c.tenant);
+}
+
 // Wait until every earlier launch of this tenant has completed (acquire).
 // Single-thread form (the caller alone polls); see wait_prev_all.  Gives up
 // if the tenant failed (its earlier launch will never complete).

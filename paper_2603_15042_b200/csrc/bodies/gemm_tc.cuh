@@ -47,11 +47,24 @@ __device__ __forceinline__ char* align1024(char* p) {
 // SWIZZLE_64B tiles (half the bytes per stage, twice the stages in the same smem)
 // BM = 128 (default) or 64: with M = 64 the accumulator's rows 16q..16q+15
 // sit in TMEM lanes 32q..32q+15 (half sub-partitions).
+// k-block at which an abandonable mainloop stopped (~0u: ran to the end), per lane
+__device__ __forceinline__ volatile uint32_t* tc_stop_word() {
+    __shared__ uint32_t stop[2];
+    return &stop[body_lane()];
+}
+
+// when the producer decided to stop (diagnostics: abandoned attempts log it)
+__device__ __forceinline__ volatile uint64_t* tc_stop_time_of(int l) {
+    __shared__ uint64_t t[2];
+    return &t[l];
+}
+__device__ __forceinline__ volatile uint64_t* tc_stop_time() { return tc_stop_time_of(body_lane()); }
+
 template <int BN, int STAGES, int BK = kTcBK, int BM = kTcBM>
 __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
                                             int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
                                             const char* a_packed = nullptr, int a_kblocks = 0,
-                                            const BodyCtx* dep = nullptr) {
+                                            const BodyCtx* dep = nullptr, const BodyCtx* yc = nullptr) {
     using L = TcSmem<BN, STAGES, BK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -64,6 +77,7 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
         }
         tc::mbar_init(tmem_full, 1);
         tc::fence_mbar_init();
+        *tc_stop_word() = ~0u;
     }
     body_sync();
     const int nkb = kb_end - kb_begin;
@@ -94,10 +108,25 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
         if (dep) wait_prev(*dep);
         if (dep && dep->dbg) dep->dbg[7] = globaltimer();
         for (int i = 0; i < pre; ++i) issue_b(i);
+        // abandonable: the SM's control word is loaded one k-block ahead of
+        // its use, so the check costs no latency on the issue path
+        unsigned long long cw = yc ? ctl_word_here(*yc) : 0ull;
         for (int i = pre; i < nkb; ++i) {
             const int s = i % STAGES;
             const uint32_t ph = (i / STAGES) & 1;
             if (i >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
+            if (yc) {
+                const bool stop = !serves_tenant(cw, yc->tenant) || ld_volatile_u32(&yc->st->ctl.exit) != 0u;
+                if (stop) {
+                    // the MMA thread is (or will be) waiting on full[s] for this
+                    // k-block: release it without data and tell it to stop here
+                    tc_stop_time()[0] = globaltimer();
+                    *tc_stop_word() = (uint32_t)i;
+                    tc::mbar_arrive(&full[s]);
+                    break;
+                }
+                cw = ctl_word_here(*yc);
+            }
             tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
             issue_a(i);
             issue_b(i);
@@ -108,6 +137,11 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             const int s = i % STAGES;
             const uint32_t ph = (i / STAGES) & 1;
             tc::mbar_wait(&full[s], ph);
+            if (yc) {
+                const uint32_t stop = *tc_stop_word();
+                if ((uint32_t)i >= stop) break;  // abandoned: no data behind this barrier
+                if (stop != ~0u) continue;       // abandoned later: drain the issued loads, skip their MMAs
+            }
             tc::tc_fence_after();
             char* sa = base + s * L::kStageBytes;
             char* sb = sa + L::kABytes;
@@ -164,6 +198,8 @@ struct GemmArgs {
     uint64_t ws;     // fp32 [tiles][S][128][BN] when S > 1
     int32_t bk;      // 0 or 64: SWIZZLE_128B K blocks of 64; 32: SWIZZLE_64B K blocks of 32 (4-stage ring)
     int32_t tma_store;  // 1: epilogue stages the bf16 tile in smem and writes it with TMA stores (tmC)
+    int32_t abandon;    // 1: give the tile up within a k-block when the SM is revoked (re-run later)
+    int32_t pad3[3];
     TmaDesc tmC;        // C [M][N] bf16, box {64, 128}, SWIZZLE_128B
 };
 static_assert(offsetof(GemmArgs, tmC) == 320 && sizeof(GemmArgs) == 448, "GemmArgs layout (mirrored in _abi.py)");
@@ -193,9 +229,14 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
     gemm_tile_coords(a, BN, tile, m_blk, n_blk);
     const int kbs = a.K / BK;
     const int kb0 = (int)((int64_t)sp * kbs / S), kb1 = (int)((int64_t)(sp + 1) * kbs / S);
-    tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb0, kb1, c.tmem_base, false);
+    const BodyCtx* yc = (a.abandon && c.st && c.abandon) ? &c : nullptr;
+    tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb0, kb1, c.tmem_base, false,
+                                nullptr, 0, nullptr, yc);
     const int warp = ltid() >> 5, lane = ltid() & 31;
-    if (warp >= 4 && S == 1 && a.tma_store) {
+    const bool gave_up = yc && *tc_stop_word() != ~0u;  // epilogue warps: ordered by tmem_full
+    if (gave_up) {
+        // nothing stored: the tile re-runs from k = 0 elsewhere
+    } else if (warp >= 4 && S == 1 && a.tma_store) {
         // bf16 tile staged in the (consumed) ring as BN/64 SWIZZLE_128B
         // [128 rows][64 cols] sub-tiles (conflict-free 16-B chunk writes),
         // then one thread issues BN/64 bulk tensor stores
@@ -263,6 +304,7 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
         }
     }
     tc_teardown<BN, STAGES, BK>(base);
+    if (yc && ltid() == 0 && *tc_stop_word() != ~0u) *c.abandon = 1u;
 }
 
 __device__ void body_gemm_bf16(const BodyCtx& c) {

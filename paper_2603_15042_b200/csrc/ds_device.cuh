@@ -35,6 +35,10 @@ constexpr int kMaxArgs = 512;
 constexpr uint32_t kLaneSmem = kLanes == 2 ? 104 * 1024 : 200 * 1024;  // dynamic smem per lane
 constexpr uint32_t kDefaultSmem = kLaneSmem * kLanes;
 constexpr int kMaxTriggers = 64;
+// Retry ring per tenant: blocks abandoned mid-way (an abandonable body whose
+// SM was revoked, or that waited on a launch with abandoned blocks) are
+// re-run from scratch by the next claimer.  Entry = ((seq + 1) << 32) | block.
+constexpr int kRetrySlots = 320;  // >= worker lanes (2 x 148): a lane holds at most one entry of its own
 
 // Named barrier ids (0 reserved).  Lane 0: body 1, full 2, empty 3, done 4,
 // epilogue 7; lane 1: body 8, full 9, empty 10, done 11, epilogue 12; 5 = exit.
@@ -64,7 +68,8 @@ struct alignas(128) DevTenant {
     uint32_t head;             // launches completed
     unsigned long long blocks; // blocks executed (stats)
     uint32_t fault;            // local-exception code, 0 = healthy (set once, never cleared)
-    uint32_t pad[25];
+    uint32_t retry_count;      // abandoned blocks waiting in the tenant's retry ring
+    uint32_t pad[24];
 };
 static_assert(sizeof(DevTenant) == 128, "tenant word owns a 128-byte line");
 
@@ -156,6 +161,8 @@ struct DevState {
     alignas(128) uint32_t trig_next;   // next armed trigger index
     uint32_t trig_count;
     ClaimTrigger* triggers;            // device array [kMaxTriggers]
+    unsigned long long* retry;         // [DS_MAX_TENANTS][kRetrySlots]
+    unsigned long long retry_mask;     // tenants that may abandon blocks (static)
     int32_t per_owner[2][DS_MAX_SMS];  // periodic program, cached from the mailbox
     int32_t per_lender[2][DS_MAX_SMS];
 };
@@ -180,6 +187,9 @@ struct BodyCtx {
     // for.  Null in solo mode.
     DevState* st;
     int32_t tenant;
+    // Abandonable bodies set *abandon = 1 when they give the block up (the
+    // scheduler then re-queues it instead of retiring it).  Null in solo mode.
+    volatile uint32_t* abandon;
 };
 
 }  // namespace ds

@@ -41,8 +41,46 @@ __device__ __forceinline__ bool early_start_body(int body) {
     return body == DS_BODY_GEMV_BF16 || body == DS_BODY_ATTN_DECODE;
 }
 
+// An abandonable GEMM block waiting for its tenant's previous launch gives
+// itself up when its SM is revoked or when abandoned blocks wait in the
+// tenant's retry ring (they may be the ones the previous launch needs: a
+// waiting block must not hold the lane they could run on).
+__device__ __forceinline__ bool wait_prev_or_abandon(const BodyCtx& c) {
+    __shared__ uint32_t give_up_l[2];
+    volatile uint32_t* give_up = &give_up_l[body_lane()];
+    if (ltid() == 0) {
+        uint32_t g = 0;
+        while (ld_acquire_u32(c.prev_head) < c.seq) {
+            if (tenant_failed(c)) break;
+            if (ld_volatile_u32(&c.st->tenants[c.tenant].retry_count) != 0u || revoked_here(c)) {
+                g = 1;
+                break;
+            }
+            __nanosleep(64);
+        }
+        *give_up = g;
+    }
+    body_sync();
+    const bool g = *give_up != 0u;
+    body_sync();
+    return !g;
+}
+
+__device__ __forceinline__ bool abandonable(int body, const BodyCtx& c) {
+    return body == DS_BODY_GEMM_BF16 && c.abandon && reinterpret_cast<const GemmArgs*>(c.args)->abandon;
+}
+
 __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
-    if (!early_start_body(body)) wait_prev_all(c);
+    if (!early_start_body(body)) {
+        if (abandonable(body, c) && c.prev_head) {
+            if (!wait_prev_or_abandon(c)) {
+                if (ltid() == 0) *c.abandon = 1u;
+                return;
+            }
+        } else {
+            wait_prev_all(c);
+        }
+    }
     switch (body) {
         case DS_BODY_REDUCE_CHUNKS: body_reduce(c); break;
         case DS_BODY_SGEMM: body_sgemm(c); break;
@@ -276,6 +314,7 @@ struct Claimed {
     uint32_t block;
     uint32_t grid;  // executed grid of the launch (known at claim: no re-read at retire)
     LaunchSlot* slot;
+    bool retry;     // re-run of an abandoned block (from the retry ring)
 };
 
 // Per-scheduler memo of the launch it claimed from last: while that launch
@@ -368,7 +407,65 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
     out.block = b2;
     out.grid = grid;
     out.slot = slot;
+    out.retry = false;
     return true;
+}
+
+// ---- retry ring (abandoned blocks) ----
+// Linear probing from the lane's home slot: concurrent pushers start apart,
+// so a push is normally one CAS.
+__device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, int home) {
+    const unsigned long long v = ((unsigned long long)(seq + 1) << 32) | block;
+    unsigned long long* ring = st->retry + (size_t)t * kRetrySlots;
+    for (;;) {
+        for (int jj = 0; jj < kRetrySlots; ++jj) {
+            const int j = (home + jj) % kRetrySlots;
+            if (atomicCAS(ring + j, 0ull, v) == 0ull) {
+                __threadfence();  // entry visible before the count says so
+                atomicAdd(&st->tenants[t].retry_count, 1u);
+                return;
+            }
+        }
+    }
+}
+
+// Oldest abandoned block first (lowest seq, then block): a later launch's
+// blocks may be waiting for it.
+__device__ bool try_retry(DevState* st, int t, Claimed& out) {
+    if (!((st->retry_mask >> t) & 1ull)) return false;
+    DevTenant* T = &st->tenants[t];
+    if (ld_volatile_u32(&T->retry_count) == 0u) return false;
+    unsigned long long* ring = st->retry + (size_t)t * kRetrySlots;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        unsigned long long best = ~0ull;
+        int bj = -1;
+        // 16-B loads, all issued before the compares consume them
+#pragma unroll 32
+        for (int j = 0; j < kRetrySlots; j += 2) {
+            unsigned long long v0, v1;
+            asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "l"(ring + j) : "memory");
+            if (v0 != 0ull && v0 < best) {
+                best = v0;
+                bj = j;
+            }
+            if (v1 != 0ull && v1 < best) {
+                best = v1;
+                bj = j + 1;
+            }
+        }
+        if (bj < 0) return false;
+        if (atomicCAS(ring + bj, best, 0ull) == best) {
+            atomicSub(&T->retry_count, 1u);
+            out.tenant = t;
+            out.seq = (uint32_t)(best >> 32) - 1u;
+            out.block = (uint32_t)best;
+            out.slot = slot_of(st, t, out.seq);
+            out.grid = ld_volatile_u32(&out.slot->grid);
+            out.retry = true;
+            return true;
+        }
+    }
+    return false;
 }
 
 __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* slot) {
@@ -411,7 +508,8 @@ __device__ void maybe_fire_trigger(DevState* st, const Claimed& w, int lane) {
     if (fire) install_ctl(st, tr->owner, tr->lender, false, 1, lane);
 }
 
-__device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, uint32_t sm, int lane_id) {
+__device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, volatile uint32_t* ab_flag,
+                               uint32_t sm, int lane_id) {
     const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
     const int lane = threadIdx.x & 31;
     int32_t last_tenant = -1;
@@ -425,7 +523,27 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
         // ---- retire the block the body just finished ----
         if (have_prev) {
             named_sync(kDone, kBodyThreads + 32);
-            if (lane == 0) {
+            const bool abandoned = *ab_flag != 0u;  // written by the body before kDone
+            if (lane == 0 && abandoned) {
+                // the block gave up (revoked SM / waiting on abandoned work):
+                // it re-runs from scratch on the next claimer, never retires here
+                *ab_flag = 0u;
+                push_retry(st, prev.tenant, prev.seq, prev.block, (int)(sm * kLanes + lane_id) % kRetrySlots);
+                if (st->blog_cap) {
+                    unsigned long long i = atomicAdd(&st->blog_count, 1ull);
+                    if (i < st->blog_cap) {
+                        ds_block_record br;
+                        br.tenant = prev.tenant;
+                        br.seq = prev.seq;
+                        br.block = prev.block;
+                        br.smid = (uint16_t)sm;
+                        br.flags = 1;  // abandoned attempt: t_start = when it decided to stop
+                        br.t_start = *tc_stop_time_of(lane_id);
+                        br.t_end = globaltimer();
+                        st->blog[i] = br;
+                    }
+                }
+            } else if (lane == 0) {
                 uint64_t t1 = globaltimer();
                 uint64_t t0 = *body_t0;
                 // release: the body's writes (ordered before this thread by the
@@ -476,8 +594,13 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                         second = -1;
                     }
                 }
-                if (first >= 0 && first < DS_MAX_TENANTS && try_claim(st, first, w, cc)) { got = true; break; }
-                if (second >= 0 && second < DS_MAX_TENANTS && second != first && try_claim(st, second, w, cc)) {
+                if (first >= 0 && first < DS_MAX_TENANTS &&
+                    (try_retry(st, first, w) || try_claim(st, first, w, cc))) {
+                    got = true;
+                    break;
+                }
+                if (second >= 0 && second < DS_MAX_TENANTS && second != first &&
+                    (try_retry(st, second, w) || try_claim(st, second, w, cc))) {
                     got = true;
                     break;
                 }
@@ -540,7 +663,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
         w.grid = __shfl_sync(0xffffffffu, w.grid, 0);
         // ---- bookkeeping while the body runs ----
         if (lane == 0) {
-            if (w.block == 0) w.slot->t_first = globaltimer();
+            if (w.block == 0 && !w.retry) w.slot->t_first = globaltimer();
             if (w.tenant != last_tenant || w.seq != last_seq) {
                 atomicAdd(&w.slot->sms, 1u);
                 if (w.tenant != last_tenant && st->slog_cap) {
@@ -572,8 +695,8 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
 // ---------------------------------------------------------------------------
 // Body warps
 // ---------------------------------------------------------------------------
-__device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, char* smem, uint32_t smem_bytes,
-                          uint32_t tmem_base, int lane_id) {
+__device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, volatile uint32_t* ab_flag,
+                          char* smem, uint32_t smem_bytes, uint32_t tmem_base, int lane_id) {
     auto prev_head_of = [&](int t) { return &st->tenants[t].head; };
     const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
     for (;;) {
@@ -598,6 +721,7 @@ __device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0
         c.dbg = nullptr;
         c.st = st;
         c.tenant = s.tenant;
+        c.abandon = ((st->retry_mask >> s.tenant) & 1ull) ? ab_flag : nullptr;
         run_body(s.body, c);
         // the scheduler's release (acq_rel retire atomic after this barrier)
         // publishes this thread's writes at gpu scope
@@ -609,6 +733,7 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
     extern __shared__ __align__(1024) char smem[];
     __shared__ Stage stage[kLanes];
     __shared__ volatile uint64_t body_t0[kLanes];
+    __shared__ volatile uint32_t ab_flag[kLanes];
     const int warp = threadIdx.x >> 5;
     const uint32_t sm = smid();
     if (warp == kLoaderWarp) {
@@ -618,16 +743,18 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
     // TMEM: one allocation for the CTA's lifetime, split between the lanes
     __shared__ uint32_t tmem_base_sh;
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, kTmemCols);
+    if (threadIdx.x < kLanes) ab_flag[threadIdx.x] = 0u;  // ordered by the barrier below
     tc::tc_fence_before();
     named_sync(kBarExit, kLanes * (kBodyThreads + 32));
     tc::tc_fence_after();
     const uint32_t lane_smem = smem_bytes / kLanes;
     if (warp >= kSchedWarp0) {
         const int l = warp - kSchedWarp0;
-        scheduler_loop(st, &stage[l], &body_t0[l], sm, l);
+        scheduler_loop(st, &stage[l], &body_t0[l], &ab_flag[l], sm, l);
     } else {
         const int l = warp >> 3;
-        body_loop(st, &stage[l], &body_t0[l], smem + l * lane_smem, lane_smem, tmem_base_sh + l * kLaneTmemCols, l);
+        body_loop(st, &stage[l], &body_t0[l], &ab_flag[l], smem + l * lane_smem, lane_smem,
+                  tmem_base_sh + l * kLaneTmemCols, l);
     }
     tc::tc_fence_before();
     named_sync(kBarExit, kLanes * (kBodyThreads + 32));
@@ -656,6 +783,7 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     c.dbg = nullptr;
     c.st = nullptr;
     c.tenant = -1;
+    c.abandon = nullptr;
     __shared__ uint32_t tmem_base_sh;
     const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16;
     if (tc_body) {

@@ -97,6 +97,8 @@ struct ds_domain {
     ds::DevState* d_state = nullptr;
     ds::LaunchSlot* d_rings = nullptr;
     ds::ClaimTrigger* d_triggers = nullptr;
+    unsigned long long* d_retry = nullptr;   // [tenant][kRetrySlots] abandoned blocks
+    unsigned long long retry_mask = 0;       // tenants whose blocks may be abandoned
     uint8_t* d_args = nullptr;
     size_t args_cap = 0, args_used = 0;
     ds_block_record* d_blog = nullptr;
@@ -353,6 +355,7 @@ int ds_domain_create(const ds_domain_config* cfg, ds_domain** out) {
     if (cudaMalloc(&d->d_state, sizeof(ds::DevState)) != cudaSuccess ||
         cudaMalloc(&d->d_rings, ring_bytes) != cudaSuccess || cudaMalloc(&d->d_args, d->args_cap) != cudaSuccess ||
         cudaMalloc(&d->d_triggers, sizeof(ds::ClaimTrigger) * ds::kMaxTriggers) != cudaSuccess ||
+        cudaMalloc(&d->d_retry, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetrySlots) != cudaSuccess ||
         cudaMalloc(&d->d_slog, sizeof(ds_switch_record) * d->slog_cap) != cudaSuccess ||
         cudaMalloc(&d->d_clog, sizeof(ds_ctl_record) * d->clog_cap) != cudaSuccess)
         return bail(fail(DS_CUDA_ERROR, "cudaMalloc"));
@@ -385,6 +388,7 @@ int ds_domain_destroy(ds_domain* d) {
     cudaFree(d->d_rings);
     cudaFree(d->d_args);
     cudaFree(d->d_triggers);
+    cudaFree(d->d_retry);
     cudaFree(d->d_slog);
     cudaFree(d->d_clog);
     if (d->d_blog) cudaFree(d->d_blog);
@@ -534,6 +538,10 @@ int ds_start(ds_domain* d) {
     h.clog_cap = d->clog_cap;
     h.num_tenants_cap = DS_MAX_TENANTS;
     h.triggers = d->d_triggers;
+    h.retry = d->d_retry;
+    h.retry_mask = d->retry_mask;
+    DS_CUDA(cudaMemsetAsync(d->d_retry, 0, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetrySlots,
+                            d->copy_stream));
     h.trig_count = 0;
     h.trig_next = 0;
     d->n_triggers = 0;
@@ -755,6 +763,16 @@ int ds_set_lane_split(ds_domain* d, int mode) {
     std::lock_guard<std::mutex> g(d->mu);
     d->lane_split = mode;
     return d->running ? push_control(d) : DS_OK;
+}
+
+int ds_tenant_abandonable(ds_domain* d, int tenant, int enable) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    std::lock_guard<std::mutex> g(d->mu);
+    if (d->running) return fail(DS_ALREADY_RUNNING, "set before ds_start");
+    if (enable) d->retry_mask |= 1ull << tenant;
+    else d->retry_mask &= ~(1ull << tenant);
+    return DS_OK;
 }
 
 int ds_set_lend(ds_domain* d, int lend_tenant) {

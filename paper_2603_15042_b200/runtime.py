@@ -164,6 +164,11 @@ class Domain:
         check(lib().ds_quota_at_claim(self.h, tenant, seq, block, self._arr(owner), self._arr(lender),
                                       self.num_sms))
 
+    def set_abandonable(self, tenant: int, enable: bool = True):
+        """Blocks of abandonable bodies (GEMM with abandon=True) yield within
+        a k-block when revoked and re-run from scratch (before start())."""
+        check(lib().ds_tenant_abandonable(self.h, tenant, int(enable)))
+
     def set_lane_split(self, mode: int):
         """0 off; 1: owned SMs run the lend tenant on lane 1 (lane 0: owner,
         then lend tenant); 2: lane 0 runs the owner only."""
