@@ -196,6 +196,11 @@ class Colocation:
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
         self.dec_kernels = self.model.register(self.dom)
         self.gemm_kernel = self.train.register(self.dom)
+        # the same GEMM with sub-block yields (tiles give up within a k-block
+        # when revoked; bit-identical results): selectable per run
+        self.dom.set_abandonable(self.t_trn)
+        self.gemm_kernel_plain = self.gemm_kernel
+        self.gemm_kernel_abandon = self.train.register(self.dom, abandon=True)
         self.resnet = None
         if self.model2 is not None:
             self.t_dec2 = self.dom.tenant("decode2", _abi.LATENCY_CRITICAL)
@@ -966,22 +971,28 @@ def config3_leg(dev):
     # logical blocks: the latency choice)
     gemm = TrainGemm(M=16384, N=16384, K=8192, device=f"cuda:{dev}", seed=5)
     narrow = _abi.gemm_args(gemm.A.data_ptr(), gemm.B.data_ptr(), gemm.C.data_ptr(), 16384, 16384, 8192, bn=64)
+    # the same 128x256 tiles with sub-block yields (abandon within ~4 k-blocks, re-run)
+    yielding = _abi.gemm_args(gemm.A.data_ptr(), gemm.B.data_ptr(), gemm.C.data_ptr(), 16384, 16384, 8192,
+                              group_m=32, abandon=True)
     torch.cuda.synchronize()
     rows = []
     with Domain(dev, tiers=[Fraction(1)], block_log_capacity=0, lend_idle_sms=False) as dom:
         t = dom.tenant("migrating", _abi.BEST_EFFORT)
+        dom.set_abandonable(t)
         nspin = int(2 * 148 * 2 * 30000 / 5 / 8)  # ~30 ms of 5-us blocks at full quota
         spin = mg.spin_kernel(dom, 5, nspin)
         gk = gemm.register(dom)
         gn = dom.kernel("train/gemm_bf16/bn64", _abi.BODY_GEMM_BF16, _abi.gemm_grid(16384, 16384, 64), narrow,
                         phase=_abi.TRAINING)
+        gy = dom.kernel("train/gemm_bf16/abandon", _abi.BODY_GEMM_BF16, gemm.grid, yielding, phase=_abi.TRAINING)
         dom.start()
         base = mg.run(dom, t, spin, 0)
         for p in (50, 200, 1000, 5000):
             rows.append(dict(unit="spin 5 us", period_us=p, **mg.summarize(mg.run(dom, t, spin, p), base["blocks_per_s"])))
         gemm_rows = {}
         for name, k, tile_flop in (("gemm tile 128x256x8192", gk, 2 * 128 * 256 * 8192),
-                                   ("gemm tile 128x64x8192", gn, 2 * 128 * 64 * 8192)):
+                                   ("gemm tile 128x64x8192", gn, 2 * 128 * 64 * 8192),
+                                   ("gemm tile 128x256x8192 abandonable", gy, 2 * 128 * 256 * 8192)):
             gbase = mg.run(dom, t, k, 0)
             gemm_rows[name] = {"unflipped_tflops": round(gbase["blocks_per_s"] * tile_flop / 1e12, 1),
                                "block_us": round(1e6 / gbase["blocks_per_s"] * 2 * 148, 1)}

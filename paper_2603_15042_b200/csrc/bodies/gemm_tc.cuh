@@ -53,6 +53,11 @@ __device__ __forceinline__ volatile uint32_t* tc_stop_word() {
     return &stop[body_lane()];
 }
 
+// An abandonable mainloop reads its SM's control word every kYieldCheckEvery
+// k-blocks (~3 us of MMA at 128x256x64): 296 lanes polling one 1.2-KB array
+// every k-block would be an L2 hot spot.
+constexpr int kYieldCheckEvery = 4;
+
 // when the producer decided to stop (diagnostics: abandoned attempts log it)
 __device__ __forceinline__ volatile uint64_t* tc_stop_time_of(int l) {
     __shared__ uint64_t t[2];
@@ -115,7 +120,7 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             const int s = i % STAGES;
             const uint32_t ph = (i / STAGES) & 1;
             if (i >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
-            if (yc) {
+            if (yc && (i & (kYieldCheckEvery - 1)) == 0) {
                 const bool stop = !serves_tenant(cw, yc->tenant) || ld_volatile_u32(&yc->st->ctl.exit) != 0u;
                 if (stop) {
                     // the MMA thread is (or will be) waiting on full[s] for this

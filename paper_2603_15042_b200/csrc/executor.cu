@@ -429,36 +429,42 @@ __device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, in
     }
 }
 
-// Oldest abandoned block first (lowest seq, then block): a later launch's
-// blocks may be waiting for it.
-__device__ bool try_retry(DevState* st, int t, Claimed& out) {
+// Oldest launch first (a later launch's blocks may be waiting for it); among
+// its entries the one nearest the popper's home slot, so the lanes regaining
+// SMs together do not all race for the same entry.
+__device__ bool try_retry(DevState* st, int t, Claimed& out, int home) {
     if (!((st->retry_mask >> t) & 1ull)) return false;
     DevTenant* T = &st->tenants[t];
     if (ld_volatile_u32(&T->retry_count) == 0u) return false;
     unsigned long long* ring = st->retry + (size_t)t * kRetrySlots;
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        unsigned long long best = ~0ull;
-        int bj = -1;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        uint32_t best_seq = ~0u;
+        int bj = -1, bd = kRetrySlots;
+        unsigned long long bv = 0ull;
         // 16-B loads, all issued before the compares consume them
 #pragma unroll 32
         for (int j = 0; j < kRetrySlots; j += 2) {
-            unsigned long long v0, v1;
-            asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "l"(ring + j) : "memory");
-            if (v0 != 0ull && v0 < best) {
-                best = v0;
-                bj = j;
-            }
-            if (v1 != 0ull && v1 < best) {
-                best = v1;
-                bj = j + 1;
+            unsigned long long v[2];
+            asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(ring + j) : "memory");
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (v[e] == 0ull) continue;
+                const uint32_t sq = (uint32_t)(v[e] >> 32);
+                const int d = (j + e - home + kRetrySlots) % kRetrySlots;
+                if (sq < best_seq || (sq == best_seq && d < bd)) {
+                    best_seq = sq;
+                    bd = d;
+                    bj = j + e;
+                    bv = v[e];
+                }
             }
         }
         if (bj < 0) return false;
-        if (atomicCAS(ring + bj, best, 0ull) == best) {
+        if (atomicCAS(ring + bj, bv, 0ull) == bv) {
             atomicSub(&T->retry_count, 1u);
             out.tenant = t;
-            out.seq = (uint32_t)(best >> 32) - 1u;
-            out.block = (uint32_t)best;
+            out.seq = (uint32_t)(bv >> 32) - 1u;
+            out.block = (uint32_t)bv;
             out.slot = slot_of(st, t, out.seq);
             out.grid = ld_volatile_u32(&out.slot->grid);
             out.retry = true;
@@ -514,6 +520,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
     const int lane = threadIdx.x & 31;
     int32_t last_tenant = -1;
     uint32_t last_seq = 0xffffffffu;
+    const int home = (int)(sm * kLanes + lane_id) % kRetrySlots;  // this lane's retry-ring slot
     bool idle_logged = false;
     uint32_t backoff = 32;
     bool have_prev = false;
@@ -528,7 +535,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                 // the block gave up (revoked SM / waiting on abandoned work):
                 // it re-runs from scratch on the next claimer, never retires here
                 *ab_flag = 0u;
-                push_retry(st, prev.tenant, prev.seq, prev.block, (int)(sm * kLanes + lane_id) % kRetrySlots);
+                push_retry(st, prev.tenant, prev.seq, prev.block, home);
                 if (st->blog_cap) {
                     unsigned long long i = atomicAdd(&st->blog_count, 1ull);
                     if (i < st->blog_cap) {
@@ -595,12 +602,12 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                     }
                 }
                 if (first >= 0 && first < DS_MAX_TENANTS &&
-                    (try_retry(st, first, w) || try_claim(st, first, w, cc))) {
+                    (try_retry(st, first, w, home) || try_claim(st, first, w, cc))) {
                     got = true;
                     break;
                 }
                 if (second >= 0 && second < DS_MAX_TENANTS && second != first &&
-                    (try_retry(st, second, w) || try_claim(st, second, w, cc))) {
+                    (try_retry(st, second, w, home) || try_claim(st, second, w, cc))) {
                     got = true;
                     break;
                 }

@@ -292,8 +292,12 @@ class TrainGemm:
         self.grid = _abi.gemm_grid(M, N)
         self.flops = 2.0 * M * N * K
 
-    def register(self, dom, phase=_abi.TRAINING) -> int:
-        return dom.kernel("train/gemm_bf16", _abi.BODY_GEMM_BF16, self.grid, self.args, phase=phase)
+    def register(self, dom, phase=_abi.TRAINING, abandon: bool = False) -> int:
+        args = self.args
+        if abandon:
+            args = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), self.M, self.N, self.K,
+                                  group_m=32, abandon=True)
+        return dom.kernel("train/gemm_bf16", _abi.BODY_GEMM_BF16, self.grid, args, phase=phase)
 
 
 # ---------------------------------------------------------------------------
