@@ -165,7 +165,7 @@ def _guarded(fn):
 # ---------------------------------------------------------------------------
 class Colocation:
     def __init__(self, device, tokens_per_req, kv_len, layers=32, decode_sat=Fraction(1, 2), slo_x=8.0,
-                 tiers=(Fraction(1, 4), Fraction(3, 4), Fraction(1)), prefill_mix=False):
+                 tiers=(Fraction(1, 4), Fraction(3, 4), Fraction(1)), prefill_mix=False, abandon=False):
         import torch
         from paper_2603_15042_b200 import _abi
         from paper_2603_15042_b200.runtime import Domain
@@ -196,11 +196,13 @@ class Colocation:
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
         self.dec_kernels = self.model.register(self.dom)
         self.gemm_kernel = self.train.register(self.dom)
-        # the same GEMM with sub-block yields (tiles give up within a k-block
-        # when revoked; bit-identical results): selectable per run
-        self.dom.set_abandonable(self.t_trn)
+        # optionally the same GEMM with sub-block yields (tiles give up within
+        # a few k-blocks when revoked; bit-identical results), per run
         self.gemm_kernel_plain = self.gemm_kernel
-        self.gemm_kernel_abandon = self.train.register(self.dom, abandon=True)
+        self.gemm_kernel_abandon = None
+        if abandon:
+            self.dom.set_abandonable(self.t_trn)
+            self.gemm_kernel_abandon = self.train.register(self.dom, abandon=True)
         self.resnet = None
         if self.model2 is not None:
             self.t_dec2 = self.dom.tenant("decode2", _abi.LATENCY_CRITICAL)

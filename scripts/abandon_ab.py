@@ -5,7 +5,7 @@ from fractions import Fraction
 import bench
 
 co = bench.Colocation(0, 8, 1024, decode_sat=Fraction(1, 2),
-                      tiers=[Fraction(1, 4), Fraction(1, 2), Fraction(3, 4), Fraction(1)])
+                      tiers=[Fraction(1, 4), Fraction(1, 2), Fraction(3, 4), Fraction(1)], abandon=True)
 solo = co.solo(steps=3)
 reqs = int(os.environ.get("REQS", "20"))
 rows = []
