@@ -56,7 +56,10 @@ __device__ __forceinline__ volatile uint32_t* tc_stop_word() {
 // An abandonable mainloop reads its SM's control word every kYieldCheckEvery
 // k-blocks (~3 us of MMA at 128x256x64): 296 lanes polling one 1.2-KB array
 // every k-block would be an L2 hot spot.
-constexpr int kYieldCheckEvery = 4;
+#ifndef DS_YIELD_CHECK_EVERY
+#define DS_YIELD_CHECK_EVERY 4
+#endif
+constexpr int kYieldCheckEvery = DS_YIELD_CHECK_EVERY;
 
 // when the producer decided to stop (diagnostics: abandoned attempts log it)
 __device__ __forceinline__ volatile uint64_t* tc_stop_time_of(int l) {
@@ -116,12 +119,13 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
         // abandonable: the SM's control word is loaded one k-block ahead of
         // its use, so the check costs no latency on the issue path
         unsigned long long cw = yc ? ctl_word_here(*yc) : 0ull;
+        uint32_t ex = yc ? ld_volatile_u32(&yc->st->ctl.exit) : 0u;
         for (int i = pre; i < nkb; ++i) {
             const int s = i % STAGES;
             const uint32_t ph = (i / STAGES) & 1;
             if (i >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
             if (yc && (i & (kYieldCheckEvery - 1)) == 0) {
-                const bool stop = !serves_tenant(cw, yc->tenant) || ld_volatile_u32(&yc->st->ctl.exit) != 0u;
+                const bool stop = !serves_tenant(cw, yc->tenant) || ex != 0u;
                 if (stop) {
                     // the MMA thread is (or will be) waiting on full[s] for this
                     // k-block: release it without data and tell it to stop here
@@ -130,7 +134,10 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
                     tc::mbar_arrive(&full[s]);
                     break;
                 }
+                // both words for the next check, issued now: their latency
+                // hides under the next k-blocks' MMAs
                 cw = ctl_word_here(*yc);
+                ex = ld_volatile_u32(&yc->st->ctl.exit);
             }
             tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
             issue_a(i);
@@ -142,11 +149,6 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             const int s = i % STAGES;
             const uint32_t ph = (i / STAGES) & 1;
             tc::mbar_wait(&full[s], ph);
-            if (yc) {
-                const uint32_t stop = *tc_stop_word();
-                if ((uint32_t)i >= stop) break;  // abandoned: no data behind this barrier
-                if (stop != ~0u) continue;       // abandoned later: drain the issued loads, skip their MMAs
-            }
             tc::tc_fence_after();
             char* sa = base + s * L::kStageBytes;
             char* sb = sa + L::kABytes;
@@ -158,6 +160,11 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
                 tc::mma_bf16(tmem_base, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
             }
             tc::mma_commit(&empty[s]);
+            // abandoned at k-block `stop`: the MMAs just issued for it read a
+            // stale stage (no load behind its barrier), harmless since the
+            // tile's result is discarded.  Checked after the issue so the
+            // shared-memory read stays off the MMA issue path.
+            if (yc && (uint32_t)i >= *tc_stop_word()) break;
         }
         tc::mma_commit(tmem_full);
     }
