@@ -39,6 +39,7 @@ constexpr int kMaxTriggers = 64;
 // SM was revoked, or that waited on a launch with abandoned blocks) are
 // re-run from scratch by the next claimer.  Entry = ((seq + 1) << 32) | block.
 constexpr int kRetrySlots = 320;  // >= worker lanes (2 x 148): a lane holds at most one entry of its own
+constexpr int kRetryStride = kRetrySlots + 8;  // per tenant: the slots, then an occupancy bitmap (5 words, a hint)
 
 // Named barrier ids (0 reserved).  Lane 0: body 1, full 2, empty 3, done 4,
 // epilogue 7; lane 1: body 8, full 9, empty 10, done 11, epilogue 12; 5 = exit.

@@ -413,15 +413,18 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
 
 // ---- retry ring (abandoned blocks) ----
 // Linear probing from the lane's home slot: concurrent pushers start apart,
-// so a push is normally one CAS.
+// so a push is normally one CAS.  The occupancy bitmap after the slots is a
+// hint for poppers (set after the entry is written, cleared after it is
+// taken); the entries themselves are the truth.
 __device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, int home) {
     const unsigned long long v = ((unsigned long long)(seq + 1) << 32) | block;
-    unsigned long long* ring = st->retry + (size_t)t * kRetrySlots;
+    unsigned long long* ring = st->retry + (size_t)t * kRetryStride;
     for (;;) {
         for (int jj = 0; jj < kRetrySlots; ++jj) {
             const int j = (home + jj) % kRetrySlots;
             if (atomicCAS(ring + j, 0ull, v) == 0ull) {
-                __threadfence();  // entry visible before the count says so
+                atomicOr(ring + kRetrySlots + (j >> 6), 1ull << (j & 63));
+                __threadfence();  // entry (and hint) visible before the count says so
                 atomicAdd(&st->tenants[t].retry_count, 1u);
                 return;
             }
@@ -429,14 +432,63 @@ __device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, in
     }
 }
 
+__device__ __forceinline__ bool take_retry(DevState* st, int t, unsigned long long* ring, int j,
+                                           unsigned long long v, Claimed& out) {
+    if (atomicCAS(ring + j, v, 0ull) != v) return false;
+    atomicAnd(ring + kRetrySlots + (j >> 6), ~(1ull << (j & 63)));
+    atomicSub(&st->tenants[t].retry_count, 1u);
+    out.tenant = t;
+    out.seq = (uint32_t)(v >> 32) - 1u;
+    out.block = (uint32_t)v;
+    out.slot = slot_of(st, t, out.seq);
+    out.grid = ld_volatile_u32(&out.slot->grid);
+    out.retry = true;
+    return true;
+}
+
 // Oldest launch first (a later launch's blocks may be waiting for it); among
 // its entries the one nearest the popper's home slot, so the lanes regaining
-// SMs together do not all race for the same entry.
+// SMs together do not all race for the same entry.  Fast path: up to 8
+// occupied slots from the bitmap hint, nearest the home slot first; full
+// scan when the hint shows none (a hint bit can lag a racing push).
 __device__ bool try_retry(DevState* st, int t, Claimed& out, int home) {
     if (!((st->retry_mask >> t) & 1ull)) return false;
     DevTenant* T = &st->tenants[t];
     if (ld_volatile_u32(&T->retry_count) == 0u) return false;
-    unsigned long long* ring = st->retry + (size_t)t * kRetrySlots;
+    unsigned long long* ring = st->retry + (size_t)t * kRetryStride;
+    constexpr int kWords = (kRetrySlots + 63) / 64;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        unsigned long long bm[kWords];
+#pragma unroll
+        for (int w = 0; w < kWords; ++w) bm[w] = ld_volatile_u64(ring + kRetrySlots + w);
+        int cand[8], nc = 0;
+        for (int ww = 0; ww <= kWords && nc < 8; ++ww) {
+            const int w = (home / 64 + ww) % kWords;
+            unsigned long long b = bm[w];
+            if (ww == 0) b &= ~0ull << (home & 63);            // from the home slot on ...
+            else if (ww == kWords) b = bm[w] & ((1ull << (home & 63)) - 1ull);  // ... wrapping to it
+            while (b && nc < 8) {
+                const int bit = __ffsll((long long)b) - 1;
+                b &= b - 1;
+                cand[nc++] = w * 64 + bit;
+            }
+        }
+        if (nc == 0) break;
+        unsigned long long v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = k < nc ? ld_volatile_u64(ring + cand[k]) : 0ull;
+        int bk = -1;
+        uint32_t best = ~0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (v[k] != 0ull && (uint32_t)(v[k] >> 32) < best) {
+                best = (uint32_t)(v[k] >> 32);
+                bk = k;
+            }
+        if (bk < 0) break;
+        if (take_retry(st, t, ring, cand[bk], v[bk], out)) return true;
+    }
+    // full scan (hint empty or stale)
     for (int attempt = 0; attempt < 8; ++attempt) {
         uint32_t best_seq = ~0u;
         int bj = -1, bd = kRetrySlots;
@@ -444,32 +496,23 @@ __device__ bool try_retry(DevState* st, int t, Claimed& out, int home) {
         // 16-B loads, all issued before the compares consume them
 #pragma unroll 32
         for (int j = 0; j < kRetrySlots; j += 2) {
-            unsigned long long v[2];
-            asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(ring + j) : "memory");
+            unsigned long long x[2];
+            asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(x[0]), "=l"(x[1]) : "l"(ring + j) : "memory");
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                if (v[e] == 0ull) continue;
-                const uint32_t sq = (uint32_t)(v[e] >> 32);
+                if (x[e] == 0ull) continue;
+                const uint32_t sq = (uint32_t)(x[e] >> 32);
                 const int d = (j + e - home + kRetrySlots) % kRetrySlots;
                 if (sq < best_seq || (sq == best_seq && d < bd)) {
                     best_seq = sq;
                     bd = d;
                     bj = j + e;
-                    bv = v[e];
+                    bv = x[e];
                 }
             }
         }
         if (bj < 0) return false;
-        if (atomicCAS(ring + bj, bv, 0ull) == bv) {
-            atomicSub(&T->retry_count, 1u);
-            out.tenant = t;
-            out.seq = (uint32_t)(bv >> 32) - 1u;
-            out.block = (uint32_t)bv;
-            out.slot = slot_of(st, t, out.seq);
-            out.grid = ld_volatile_u32(&out.slot->grid);
-            out.retry = true;
-            return true;
-        }
+        if (take_retry(st, t, ring, bj, bv, out)) return true;
     }
     return false;
 }

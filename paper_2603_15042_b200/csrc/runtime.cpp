@@ -97,7 +97,7 @@ struct ds_domain {
     ds::DevState* d_state = nullptr;
     ds::LaunchSlot* d_rings = nullptr;
     ds::ClaimTrigger* d_triggers = nullptr;
-    unsigned long long* d_retry = nullptr;   // [tenant][kRetrySlots] abandoned blocks
+    unsigned long long* d_retry = nullptr;   // [tenant][kRetryStride] abandoned blocks + occupancy hint
     unsigned long long retry_mask = 0;       // tenants whose blocks may be abandoned
     uint8_t* d_args = nullptr;
     size_t args_cap = 0, args_used = 0;
@@ -355,7 +355,7 @@ int ds_domain_create(const ds_domain_config* cfg, ds_domain** out) {
     if (cudaMalloc(&d->d_state, sizeof(ds::DevState)) != cudaSuccess ||
         cudaMalloc(&d->d_rings, ring_bytes) != cudaSuccess || cudaMalloc(&d->d_args, d->args_cap) != cudaSuccess ||
         cudaMalloc(&d->d_triggers, sizeof(ds::ClaimTrigger) * ds::kMaxTriggers) != cudaSuccess ||
-        cudaMalloc(&d->d_retry, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetrySlots) != cudaSuccess ||
+        cudaMalloc(&d->d_retry, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetryStride) != cudaSuccess ||
         cudaMalloc(&d->d_slog, sizeof(ds_switch_record) * d->slog_cap) != cudaSuccess ||
         cudaMalloc(&d->d_clog, sizeof(ds_ctl_record) * d->clog_cap) != cudaSuccess)
         return bail(fail(DS_CUDA_ERROR, "cudaMalloc"));
@@ -540,7 +540,7 @@ int ds_start(ds_domain* d) {
     h.triggers = d->d_triggers;
     h.retry = d->d_retry;
     h.retry_mask = d->retry_mask;
-    DS_CUDA(cudaMemsetAsync(d->d_retry, 0, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetrySlots,
+    DS_CUDA(cudaMemsetAsync(d->d_retry, 0, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetryStride,
                             d->copy_stream));
     h.trig_count = 0;
     h.trig_next = 0;
