@@ -58,3 +58,38 @@ def test_gemm_tiles_abandon_on_revocation_bit_exact(abandon):
         assert p50 < 12.0  # measured p50 ~8 us, p99 ~10 us, vs up to a whole ~120 us tile without
     else:
         assert gave_up == []
+
+
+def test_abandon_across_back_to_back_launches():
+    """Several launches in flight (launch s+1 opens while s still has
+    abandoned tiles): blocks waiting on s give themselves up, s's re-runs go
+    first, nothing deadlocks, every (launch, tile) retires exactly once and
+    the output stays bit-exact."""
+    A, B = _operands()
+    C_solo = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    C_co = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    a_solo = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_solo.data_ptr(), M, N, K, group_m=16)
+    a_co = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_co.data_ptr(), M, N, K, group_m=16, abandon=True)
+    grid = _abi.gemm_grid(M, N)
+    solo_launch(0, "gemm", _abi.BODY_GEMM_BF16, grid, a_solo)
+    torch.cuda.synchronize()
+    with Domain(0, tiers=[Fraction(1)], block_log_capacity=1 << 20) as dom:
+        t = dom.tenant("train", _abi.BEST_EFFORT)
+        dom.set_abandonable(t)
+        kid = dom.kernel("train/gemm", _abi.BODY_GEMM_BF16, grid, a_co)
+        dom.start()
+        n = dom.num_sms
+        full, eighth = dom.mask(t, 0, n), dom.mask(t, 0, n // 8)
+        dom.quota_set(full)
+        dom.clear_logs()
+        dom.quota_periodic(40_000, full, eighth)  # 100% <-> 1/8 every 40 us
+        seqs = [dom.launch(t, kid) for _ in range(4)]
+        dom.wait(t, seqs[-1], 120000)
+        dom.quota_periodic(0, full, full)
+        blog = [b for b in dom.block_log() if b.tenant == t]
+        got = C_co.cpu()
+    assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
+    for s in seqs:
+        done = sorted(b.block for b in blog if b.flags == 0 and b.seq == s)
+        assert done == list(range(grid[0])), s
+    assert sum(b.flags == 1 for b in blog) > 0
