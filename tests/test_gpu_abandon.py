@@ -93,3 +93,52 @@ def test_abandon_across_back_to_back_launches():
         done = sorted(b.block for b in blog if b.flags == 0 and b.seq == s)
         assert done == list(range(grid[0])), s
     assert sum(b.flags == 1 for b in blog) > 0
+
+
+def test_engine_decode_preempts_abandonable_training():
+    """TPOT-First engine: latency-critical records bind SMs that training
+    tiles hold; abandonable tiles give them up mid-tile and re-run, training
+    output stays bit-exact."""
+    from paper_2603_15042_b200.runtime import Engine
+    A, B = _operands()
+    C_solo = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    C_co = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    a_solo = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_solo.data_ptr(), M, N, K, group_m=16)
+    a_co = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_co.data_ptr(), M, N, K, group_m=16, abandon=True)
+    grid = _abi.gemm_grid(M, N)
+    solo_launch(0, "gemm", _abi.BODY_GEMM_BF16, grid, a_solo)
+    spin_out = torch.zeros(3 * 600, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    tiers = [Fraction(1, 4), Fraction(1, 2), Fraction(3, 4), Fraction(1)]
+    with Domain(0, tiers=tiers, block_log_capacity=1 << 20) as dom:
+        td = dom.tenant("decode", _abi.LATENCY_CRITICAL)
+        tt = dom.tenant("train", _abi.BEST_EFFORT)
+        dom.set_abandonable(tt)
+        kd = dom.kernel("decode/spin", _abi.BODY_SPIN, (600, 1, 1), _abi.SpinArgs(spin_out.data_ptr(), 10_000))
+        kt = dom.kernel("train/gemm", _abi.BODY_GEMM_BF16, grid, a_co)
+        dom.start()
+        eng = Engine(dom, policy="tpot-first", lend_tenant=tt)
+        jd = eng.add_job(td, _abi.LATENCY_CRITICAL)
+        jt = eng.add_job(tt, _abi.BEST_EFFORT)
+        eng.start()
+        try:
+            tr = [eng.submit(jt, [kt], "train/gemm", phase=_abi.TRAINING, grid_size=grid[0]) for _ in range(12)]
+            import time
+            dr = []
+            for i in range(6):
+                time.sleep(0.0015)
+                dr.append(eng.submit(jd, [kd] * 3, "decode/spin", phase=_abi.DECODE, grid_size=600,
+                                     saturation=Fraction(1, 2), tpot_ns=50_000_000))
+            for r in dr + tr:
+                eng.wait(r, 120000)
+        finally:
+            eng.stop()
+            eng.close()
+        blog = [b for b in dom.block_log() if b.tenant == tt]
+        got = C_co.cpu()
+    assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
+    seqs = sorted({b.seq for b in blog})
+    assert len(seqs) == 12
+    for s in seqs:
+        assert sorted(b.block for b in blog if b.flags == 0 and b.seq == s) == list(range(grid[0]))
+    print("abandoned attempts", sum(b.flags == 1 for b in blog))
