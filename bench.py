@@ -976,6 +976,8 @@ def config3_leg(dev):
     # the same 128x256 tiles with sub-block yields (abandon within ~4 k-blocks, re-run)
     yielding = _abi.gemm_args(gemm.A.data_ptr(), gemm.B.data_ptr(), gemm.C.data_ptr(), 16384, 16384, 8192,
                               group_m=32, abandon=True)
+    spilling = _abi.gemm_args(gemm.A.data_ptr(), gemm.B.data_ptr(), gemm.C.data_ptr(), 16384, 16384, 8192,
+                              group_m=32, abandon=2)
     torch.cuda.synchronize()
     rows = []
     with Domain(dev, tiers=[Fraction(1)], block_log_capacity=0, lend_idle_sms=False) as dom:
@@ -987,6 +989,7 @@ def config3_leg(dev):
         gn = dom.kernel("train/gemm_bf16/bn64", _abi.BODY_GEMM_BF16, _abi.gemm_grid(16384, 16384, 64), narrow,
                         phase=_abi.TRAINING)
         gy = dom.kernel("train/gemm_bf16/abandon", _abi.BODY_GEMM_BF16, gemm.grid, yielding, phase=_abi.TRAINING)
+        gsp = dom.kernel("train/gemm_bf16/spill", _abi.BODY_GEMM_BF16, gemm.grid, spilling, phase=_abi.TRAINING)
         dom.start()
         base = mg.run(dom, t, spin, 0)
         for p in (50, 200, 1000, 5000):
@@ -994,7 +997,8 @@ def config3_leg(dev):
         gemm_rows = {}
         for name, k, tile_flop in (("gemm tile 128x256x8192", gk, 2 * 128 * 256 * 8192),
                                    ("gemm tile 128x64x8192", gn, 2 * 128 * 64 * 8192),
-                                   ("gemm tile 128x256x8192 abandonable", gy, 2 * 128 * 256 * 8192)):
+                                   ("gemm tile 128x256x8192 abandonable (restart)", gy, 2 * 128 * 256 * 8192),
+                                   ("gemm tile 128x256x8192 abandonable (spill + resume)", gsp, 2 * 128 * 256 * 8192)):
             gbase = mg.run(dom, t, k, 0)
             gemm_rows[name] = {"unflipped_tflops": round(gbase["blocks_per_s"] * tile_flop / 1e12, 1),
                                "block_us": round(1e6 / gbase["blocks_per_s"] * 2 * 148, 1)}

@@ -218,10 +218,12 @@ int ds_bound_pctx(ds_domain* dom, int tenant, int* pctx);
 int ds_quota_set(ds_domain* dom, const int32_t* owner, const int32_t* lender, int n);
 int ds_quota_get(ds_domain* dom, int32_t* owner, int32_t* lender, int n);
 /* Sub-block yields: blocks of an abandonable body launched by this tenant
- * (DS_BODY_GEMM_BF16 with GemmArgs.abandon = 1) give their logical block up
- * within one k-block when the SM is revoked, and re-run from scratch on the
- * next claimer (same code and inputs: bit-identical; only a completed run
- * retires the block).  Call before ds_start. */
+ * (DS_BODY_GEMM_BF16 with GemmArgs.abandon != 0) give their logical block up
+ * within ~4 k-blocks when the SM is revoked.  abandon = 1: the next claimer
+ * re-runs the tile from scratch; abandon = 2: the fp32 accumulators are
+ * spilled and the next claimer resumes at the same k-block.  Either way the
+ * MMA sequence is unchanged, so results are bit-identical; only a completed
+ * run retires the block.  Call before ds_start. */
 int ds_tenant_abandonable(ds_domain* dom, int tenant, int enable);
 /* Lane split: every SM owned by a tenant also runs the lend tenant on its
  * second worker lane (mode 1: lane 0 runs the owner, then the lend tenant when

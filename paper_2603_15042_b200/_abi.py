@@ -202,7 +202,7 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
     a = GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM, bk), tensor_map_bf16(B, N, K, bn, bk), C, M, N, K, group_m, bn,
                  max(1, splits), ws, bk, int(tma_store))
     a.tmC = tmC
-    a.abandon = int(abandon)
+    a.abandon = int(abandon)  # False/0 off, True/1 restart, 2 spill + resume
     return a
 
 

@@ -72,7 +72,8 @@ template <int BN, int STAGES, int BK = kTcBK, int BM = kTcBM>
 __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
                                             int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
                                             const char* a_packed = nullptr, int a_kblocks = 0,
-                                            const BodyCtx* dep = nullptr, const BodyCtx* yc = nullptr) {
+                                            const BodyCtx* dep = nullptr, const BodyCtx* yc = nullptr,
+                                            bool acc_init = false) {
     using L = TcSmem<BN, STAGES, BK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -127,11 +128,10 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             if (yc && (i & (kYieldCheckEvery - 1)) == 0) {
                 const bool stop = !serves_tenant(cw, yc->tenant) || ex != 0u;
                 if (stop) {
-                    // the MMA thread is (or will be) waiting on full[s] for this
-                    // k-block: release it without data and tell it to stop here
+                    // k-blocks < i are issued and will be multiplied; the MMA
+                    // thread stops when it finds k-block i not loaded
                     tc_stop_time()[0] = globaltimer();
                     *tc_stop_word() = (uint32_t)i;
-                    tc::mbar_arrive(&full[s]);
                     break;
                 }
                 // both words for the next check, issued now: their latency
@@ -148,7 +148,18 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
         for (int i = 0; i < nkb; ++i) {
             const int s = i % STAGES;
             const uint32_t ph = (i / STAGES) & 1;
-            tc::mbar_wait(&full[s], ph);
+            if (yc) {
+                bool stopped = false;
+                while (!tc::mbar_try_wait(&full[s], ph)) {
+                    if ((uint32_t)i >= *tc_stop_word()) {  // never loaded: the tile stops before it
+                        stopped = true;
+                        break;
+                    }
+                }
+                if (stopped) break;
+            } else {
+                tc::mbar_wait(&full[s], ph);
+            }
             tc::tc_fence_after();
             char* sa = base + s * L::kStageBytes;
             char* sb = sa + L::kABytes;
@@ -157,14 +168,10 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
                 // +32 B per K=16 step inside the 128-B swizzle row
-                tc::mma_bf16(tmem_base, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
+                tc::mma_bf16(tmem_base, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                             acc_init || (i | k) != 0);
             }
             tc::mma_commit(&empty[s]);
-            // abandoned at k-block `stop`: the MMAs just issued for it read a
-            // stale stage (no load behind its barrier), harmless since the
-            // tile's result is discarded.  Checked after the issue so the
-            // shared-memory read stays off the MMA issue path.
-            if (yc && (uint32_t)i >= *tc_stop_word()) break;
         }
         tc::mma_commit(tmem_full);
     }
@@ -210,7 +217,8 @@ struct GemmArgs {
     uint64_t ws;     // fp32 [tiles][S][128][BN] when S > 1
     int32_t bk;      // 0 or 64: SWIZZLE_128B K blocks of 64; 32: SWIZZLE_64B K blocks of 32 (4-stage ring)
     int32_t tma_store;  // 1: epilogue stages the bf16 tile in smem and writes it with TMA stores (tmC)
-    int32_t abandon;    // 1: give the tile up within a k-block when the SM is revoked (re-run later)
+    int32_t abandon;    // give the tile up within ~4 k-blocks when the SM is revoked: 1 re-runs it from
+                        // k = 0 (fastest yield), 2 spills the accumulators and resumes at k (no lost work)
     int32_t pad3[3];
     TmaDesc tmC;        // C [M][N] bf16, box {64, 128}, SWIZZLE_128B
 };
@@ -242,12 +250,72 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
     const int kbs = a.K / BK;
     const int kb0 = (int)((int64_t)sp * kbs / S), kb1 = (int)((int64_t)(sp + 1) * kbs / S);
     const BodyCtx* yc = (a.abandon && c.st && c.abandon) ? &c : nullptr;
-    tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb0, kb1, c.tmem_base, false,
-                                nullptr, 0, nullptr, yc);
     const int warp = ltid() >> 5, lane = ltid() & 31;
+    // resume a spilled tile: its fp32 accumulators back into TMEM, continue at k
+    const uint32_t res = yc ? c.resume : 0u;
+    int kb_start = kb0;
+    if (res) {
+        const int j = (int)(res & 0xffffu) - 1;
+        kb_start = (int)(res >> 16);
+        unsigned long long* ring = c.st->retry + (size_t)c.tenant * kRetryStride;
+        if (warp >= 4) {
+            const int q = warp & 3, row = q * 32 + lane;
+            const float* src = c.st->save + ((size_t)c.st->tenants[c.tenant].save_base + j) * kSaveFloats + (size_t)row * BN;
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                const uint4* p4 = reinterpret_cast<const uint4*>(src + ch * 32);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint4 x = __ldcg(p4 + u);
+                    v[4 * u] = x.x;
+                    v[4 * u + 1] = x.y;
+                    v[4 * u + 2] = x.z;
+                    v[4 * u + 3] = x.w;
+                }
+                tc::tmem_st_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, v);
+            }
+            tc::tmem_st_wait();
+        }
+        tc::tc_fence_before();
+        body_sync();
+        tc::tc_fence_after();
+        if (ltid() == 0) atomicExch(ring + j, 0ull);  // spill consumed: the slot is free again
+    }
+    tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb_start, kb1, c.tmem_base, false,
+                                nullptr, 0, nullptr, yc, res != 0u);
     const bool gave_up = yc && *tc_stop_word() != ~0u;  // epilogue warps: ordered by tmem_full
     if (gave_up) {
-        // nothing stored: the tile re-runs from k = 0 elsewhere
+        // abandoned: spill the accumulators (when there are any) so the tile
+        // continues at k elsewhere; nothing is stored to C
+        const uint32_t k_abs = (uint32_t)kb_start + *tc_stop_word();
+        if (warp >= 4 && a.abandon == 2 && (res != 0u || k_abs > (uint32_t)kb0)) {
+            __shared__ int spill_l[2];
+            volatile int* spill = &spill_l[body_lane()];
+            const int q = warp & 3;
+            if (q == 0 && lane == 0) {
+                unsigned long long* ring = c.st->retry + (size_t)c.tenant * kRetryStride;
+                const int home = (int)((smid() * kLanes + body_lane()) % kRetrySlots);
+                int j = -1;
+                for (int jj = 0; j < 0; jj = (jj + 1) % kRetrySlots)
+                    if (atomicCAS(ring + (home + jj) % kRetrySlots, 0ull, kRetryReserved) == 0ull) j = (home + jj) % kRetrySlots;
+                *spill = j;
+            }
+            epi_sync();
+            const int j = *spill;
+            const int row = q * 32 + lane;
+            float* dst = c.st->save + ((size_t)c.st->tenants[c.tenant].save_base + j) * kSaveFloats + (size_t)row * BN;
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, v);
+                tc::tmem_ld_wait();
+                uint4* p4 = reinterpret_cast<uint4*>(dst + ch * 32);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) __stcg(p4 + u, make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
+            }
+            if (q == 0 && lane == 0) *c.ab_info = (uint32_t)(j + 1) | (k_abs << 16);
+        }
     } else if (warp >= 4 && S == 1 && a.tma_store) {
         // bf16 tile staged in the (consumed) ring as BN/64 SWIZZLE_128B
         // [128 rows][64 cols] sub-tiles (conflict-free 16-B chunk writes),

@@ -40,6 +40,12 @@ constexpr int kMaxTriggers = 64;
 // re-run from scratch by the next claimer.  Entry = ((seq + 1) << 32) | block.
 constexpr int kRetrySlots = 320;  // >= worker lanes (2 x 148): a lane holds at most one entry of its own
 constexpr int kRetryStride = kRetrySlots + 8;  // per tenant: the slots, then an occupancy bitmap (5 words, a hint)
+// Ring entry values: 0 free, kRetryReserved (a spill in progress), kRetryTaken
+// (a resumer is reading the spill), else ((seq + 1) << 32) | (k << 20) | block
+// with k the next k-block of a spilled tile (0: restart from scratch).
+constexpr unsigned long long kRetryReserved = 1ull, kRetryTaken = 2ull;
+constexpr uint32_t kRetryBlockBits = 20;
+constexpr int kSaveFloats = 128 * 256;  // one spilled 128 x 256 fp32 accumulator tile
 
 // Named barrier ids (0 reserved).  Lane 0: body 1, full 2, empty 3, done 4,
 // epilogue 7; lane 1: body 8, full 9, empty 10, done 11, epilogue 12; 5 = exit.
@@ -70,7 +76,8 @@ struct alignas(128) DevTenant {
     unsigned long long blocks; // blocks executed (stats)
     uint32_t fault;            // local-exception code, 0 = healthy (set once, never cleared)
     uint32_t retry_count;      // abandoned blocks waiting in the tenant's retry ring
-    uint32_t pad[24];
+    uint32_t save_base;        // first spill slot of this tenant in DevState::save (abandonable tenants)
+    uint32_t pad[23];
 };
 static_assert(sizeof(DevTenant) == 128, "tenant word owns a 128-byte line");
 
@@ -162,7 +169,8 @@ struct DevState {
     alignas(128) uint32_t trig_next;   // next armed trigger index
     uint32_t trig_count;
     ClaimTrigger* triggers;            // device array [kMaxTriggers]
-    unsigned long long* retry;         // [DS_MAX_TENANTS][kRetrySlots]
+    unsigned long long* retry;         // [DS_MAX_TENANTS][kRetryStride]
+    float* save;                       // [abandonable tenants][kRetrySlots][kSaveFloats] spilled accumulators
     unsigned long long retry_mask;     // tenants that may abandon blocks (static)
     int32_t per_owner[2][DS_MAX_SMS];  // periodic program, cached from the mailbox
     int32_t per_lender[2][DS_MAX_SMS];
@@ -191,6 +199,11 @@ struct BodyCtx {
     // Abandonable bodies set *abandon = 1 when they give the block up (the
     // scheduler then re-queues it instead of retiring it).  Null in solo mode.
     volatile uint32_t* abandon;
+    // Spill/resume of abandoned tiles: *ab_info = (slot + 1) | (k << 16) of
+    // the spill the body wrote (0: none); resume = the same for the spill
+    // this block continues from (0: fresh start).
+    volatile uint32_t* ab_info;
+    uint32_t resume;
 };
 
 }  // namespace ds

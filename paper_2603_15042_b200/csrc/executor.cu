@@ -74,7 +74,10 @@ __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
     if (!early_start_body(body)) {
         if (abandonable(body, c) && c.prev_head) {
             if (!wait_prev_or_abandon(c)) {
-                if (ltid() == 0) *c.abandon = 1u;
+                if (ltid() == 0) {
+                    *c.abandon = 1u;
+                    if (c.resume) *c.ab_info = c.resume;  // hand the spill on untouched
+                }
                 return;
             }
         } else {
@@ -315,6 +318,7 @@ struct Claimed {
     uint32_t grid;  // executed grid of the launch (known at claim: no re-read at retire)
     LaunchSlot* slot;
     bool retry;     // re-run of an abandoned block (from the retry ring)
+    uint32_t resume;  // (spill slot + 1) | (k << 16) when it continues a spilled tile, else 0
 };
 
 // Per-scheduler memo of the launch it claimed from last: while that launch
@@ -408,6 +412,7 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
     out.grid = grid;
     out.slot = slot;
     out.retry = false;
+    out.resume = 0u;
     return true;
 }
 
@@ -434,12 +439,15 @@ __device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, in
 
 __device__ __forceinline__ bool take_retry(DevState* st, int t, unsigned long long* ring, int j,
                                            unsigned long long v, Claimed& out) {
-    if (atomicCAS(ring + j, v, 0ull) != v) return false;
+    const uint32_t k = ((uint32_t)v) >> kRetryBlockBits;
+    // a spilled tile keeps its slot (TAKEN) until the resumer has read it back
+    if (atomicCAS(ring + j, v, k ? kRetryTaken : 0ull) != v) return false;
     atomicAnd(ring + kRetrySlots + (j >> 6), ~(1ull << (j & 63)));
     atomicSub(&st->tenants[t].retry_count, 1u);
     out.tenant = t;
     out.seq = (uint32_t)(v >> 32) - 1u;
-    out.block = (uint32_t)v;
+    out.block = (uint32_t)v & ((1u << kRetryBlockBits) - 1u);
+    out.resume = k ? ((uint32_t)(j + 1) | (k << 16)) : 0u;
     out.slot = slot_of(st, t, out.seq);
     out.grid = ld_volatile_u32(&out.slot->grid);
     out.retry = true;
@@ -481,7 +489,7 @@ __device__ bool try_retry(DevState* st, int t, Claimed& out, int home) {
         uint32_t best = ~0u;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (v[k] != 0ull && (uint32_t)(v[k] >> 32) < best) {
+            if (v[k] > kRetryTaken && (uint32_t)(v[k] >> 32) < best) {
                 best = (uint32_t)(v[k] >> 32);
                 bk = k;
             }
@@ -500,7 +508,7 @@ __device__ bool try_retry(DevState* st, int t, Claimed& out, int home) {
             asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(x[0]), "=l"(x[1]) : "l"(ring + j) : "memory");
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                if (x[e] == 0ull) continue;
+                if (x[e] <= kRetryTaken) continue;  // free, or a spill being written / read
                 const uint32_t sq = (uint32_t)(x[e] >> 32);
                 const int d = (j + e - home + kRetrySlots) % kRetrySlots;
                 if (sq < best_seq || (sq == best_seq && d < bd)) {
@@ -558,7 +566,7 @@ __device__ void maybe_fire_trigger(DevState* st, const Claimed& w, int lane) {
 }
 
 __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, volatile uint32_t* ab_flag,
-                               uint32_t sm, int lane_id) {
+                               volatile uint32_t* ab_info, uint32_t sm, int lane_id) {
     const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
     const int lane = threadIdx.x & 31;
     int32_t last_tenant = -1;
@@ -578,7 +586,23 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                 // the block gave up (revoked SM / waiting on abandoned work):
                 // it re-runs from scratch on the next claimer, never retires here
                 *ab_flag = 0u;
-                push_retry(st, prev.tenant, prev.seq, prev.block, home);
+                const uint32_t info = *ab_info;
+                *ab_info = 0u;
+                if (info) {
+                    // the body spilled its accumulators into slot j (reserved):
+                    // publish the entry there, continuing at k-block k
+                    const int j = (int)(info & 0xffffu) - 1;
+                    const uint32_t k = info >> 16;
+                    unsigned long long* ring = st->retry + (size_t)prev.tenant * kRetryStride;
+                    __threadfence();  // the spill (ordered by kDone) before the entry
+                    atomicExch(ring + j, ((unsigned long long)(prev.seq + 1) << 32) |
+                                             ((unsigned long long)k << kRetryBlockBits) | prev.block);
+                    atomicOr(ring + kRetrySlots + (j >> 6), 1ull << (j & 63));
+                    __threadfence();
+                    atomicAdd(&st->tenants[prev.tenant].retry_count, 1u);
+                } else {
+                    push_retry(st, prev.tenant, prev.seq, prev.block, home);
+                }
                 if (st->blog_cap) {
                     unsigned long long i = atomicAdd(&st->blog_count, 1ull);
                     if (i < st->blog_cap) {
@@ -691,7 +715,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                 s.gx = h0.z;
                 s.gy = h0.w;
                 s.gz = h1.x;
-                s.pad = 0;
+                s.pad = w.resume;
                 s.args = ((uint64_t)h1.w << 32) | h1.z;
                 *stage = s;
             } else {
@@ -746,7 +770,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
 // Body warps
 // ---------------------------------------------------------------------------
 __device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, volatile uint32_t* ab_flag,
-                          char* smem, uint32_t smem_bytes, uint32_t tmem_base, int lane_id) {
+                          volatile uint32_t* ab_info, char* smem, uint32_t smem_bytes, uint32_t tmem_base, int lane_id) {
     auto prev_head_of = [&](int t) { return &st->tenants[t].head; };
     const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
     for (;;) {
@@ -772,6 +796,8 @@ __device__ void body_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0
         c.st = st;
         c.tenant = s.tenant;
         c.abandon = ((st->retry_mask >> s.tenant) & 1ull) ? ab_flag : nullptr;
+        c.ab_info = ab_info;
+        c.resume = s.pad;
         run_body(s.body, c);
         // the scheduler's release (acq_rel retire atomic after this barrier)
         // publishes this thread's writes at gpu scope
@@ -784,6 +810,7 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
     __shared__ Stage stage[kLanes];
     __shared__ volatile uint64_t body_t0[kLanes];
     __shared__ volatile uint32_t ab_flag[kLanes];
+    __shared__ volatile uint32_t ab_info[kLanes];
     const int warp = threadIdx.x >> 5;
     const uint32_t sm = smid();
     if (warp == kLoaderWarp) {
@@ -793,17 +820,20 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
     // TMEM: one allocation for the CTA's lifetime, split between the lanes
     __shared__ uint32_t tmem_base_sh;
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, kTmemCols);
-    if (threadIdx.x < kLanes) ab_flag[threadIdx.x] = 0u;  // ordered by the barrier below
+    if (threadIdx.x < kLanes) {  // ordered by the barrier below
+        ab_flag[threadIdx.x] = 0u;
+        ab_info[threadIdx.x] = 0u;
+    }
     tc::tc_fence_before();
     named_sync(kBarExit, kLanes * (kBodyThreads + 32));
     tc::tc_fence_after();
     const uint32_t lane_smem = smem_bytes / kLanes;
     if (warp >= kSchedWarp0) {
         const int l = warp - kSchedWarp0;
-        scheduler_loop(st, &stage[l], &body_t0[l], &ab_flag[l], sm, l);
+        scheduler_loop(st, &stage[l], &body_t0[l], &ab_flag[l], &ab_info[l], sm, l);
     } else {
         const int l = warp >> 3;
-        body_loop(st, &stage[l], &body_t0[l], &ab_flag[l], smem + l * lane_smem, lane_smem,
+        body_loop(st, &stage[l], &body_t0[l], &ab_flag[l], &ab_info[l], smem + l * lane_smem, lane_smem,
                   tmem_base_sh + l * kLaneTmemCols, l);
     }
     tc::tc_fence_before();
@@ -834,6 +864,8 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     c.st = nullptr;
     c.tenant = -1;
     c.abandon = nullptr;
+    c.ab_info = nullptr;
+    c.resume = 0u;
     __shared__ uint32_t tmem_base_sh;
     const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16;
     if (tc_body) {

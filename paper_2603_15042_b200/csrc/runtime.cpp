@@ -99,6 +99,8 @@ struct ds_domain {
     ds::ClaimTrigger* d_triggers = nullptr;
     unsigned long long* d_retry = nullptr;   // [tenant][kRetryStride] abandoned blocks + occupancy hint
     unsigned long long retry_mask = 0;       // tenants whose blocks may be abandoned
+    float* d_save = nullptr;                 // spilled accumulators of abandoned tiles
+    int save_tenants = 0;
     uint8_t* d_args = nullptr;
     size_t args_cap = 0, args_used = 0;
     ds_block_record* d_blog = nullptr;
@@ -389,6 +391,7 @@ int ds_domain_destroy(ds_domain* d) {
     cudaFree(d->d_args);
     cudaFree(d->d_triggers);
     cudaFree(d->d_retry);
+    cudaFree(d->d_save);
     cudaFree(d->d_slog);
     cudaFree(d->d_clog);
     if (d->d_blog) cudaFree(d->d_blog);
@@ -540,6 +543,22 @@ int ds_start(ds_domain* d) {
     h.triggers = d->d_triggers;
     h.retry = d->d_retry;
     h.retry_mask = d->retry_mask;
+    {
+        const int n_ab = __builtin_popcountll(d->retry_mask);
+        if (n_ab != d->save_tenants) {
+            cudaFree(d->d_save);
+            d->d_save = nullptr;
+            d->save_tenants = 0;
+            if (n_ab) {
+                DS_CUDA(cudaMalloc(&d->d_save, sizeof(float) * (size_t)n_ab * ds::kRetrySlots * ds::kSaveFloats));
+                d->save_tenants = n_ab;
+            }
+        }
+        int rank = 0;
+        for (int t = 0; t < DS_MAX_TENANTS; ++t)
+            if ((d->retry_mask >> t) & 1ull) h.tenants[t].save_base = (uint32_t)(rank++ * ds::kRetrySlots);
+        h.save = d->d_save;
+    }
     DS_CUDA(cudaMemsetAsync(d->d_retry, 0, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetryStride,
                             d->copy_stream));
     h.trig_count = 0;
