@@ -434,6 +434,7 @@ __device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, in
                 return;
             }
         }
+        __nanosleep(256);  // ring full (more abandoned blocks than lanes): wait for a pop
     }
 }
 
