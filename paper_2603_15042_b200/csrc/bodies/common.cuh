@@ -142,6 +142,29 @@ __device__ __forceinline__ unsigned long long ctl_word_here(const BodyCtx& c) {
     return ld_volatile_u64(&c.st->ctl.word[smid()]);
 }
 
+// Claim a free retry-ring slot nearest `home` for `v` (linear probing over
+// 8-slot windows read with 16-B loads; CAS only on slots seen free).
+__device__ inline int claim_retry_slot(unsigned long long* ring, int home, unsigned long long v) {
+    for (;;) {
+        for (int w = 0; w < kRetrySlots; w += 8) {
+            const int base = ((home & ~1) + w) % kRetrySlots;  // even: 16-B aligned pairs
+            unsigned long long x[8];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const int j = (base + 2 * p) % kRetrySlots;
+                asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                             : "=l"(x[2 * p]), "=l"(x[2 * p + 1]) : "l"(ring + j) : "memory");
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int j = (base + e) % kRetrySlots;
+                if (x[e] == 0ull && atomicCAS(ring + j, 0ull, v) == 0ull) return j;
+            }
+        }
+        __nanosleep(256);  // ring full (more abandoned blocks than lanes): wait for a pop
+    }
+}
+
 __device__ __forceinline__ bool revoked_here(const BodyCtx& c) {
     return ld_volatile_u32(&c.st->ctl.exit) != 0u || !serves_tenant(ctl_word_here(c), c.tenant);
 }

@@ -296,14 +296,7 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
             if (q == 0 && lane == 0) {
                 unsigned long long* ring = c.st->retry + (size_t)c.tenant * kRetryStride;
                 const int home = (int)((smid() * kLanes + body_lane()) % kRetrySlots);
-                int j = -1;
-                for (int jj = 0; j < 0; jj = (jj + 1) % kRetrySlots) {
-                    if (atomicCAS(ring + (home + jj) % kRetrySlots, 0ull, kRetryReserved) == 0ull)
-                        j = (home + jj) % kRetrySlots;
-                    else if (jj == kRetrySlots - 1)
-                        __nanosleep(256);  // ring full: wait for a pop
-                }
-                *spill = j;
+                *spill = claim_retry_slot(ring, home, kRetryReserved);
             }
             epi_sync();
             const int j = *spill;

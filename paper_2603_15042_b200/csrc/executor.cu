@@ -424,18 +424,10 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
 __device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, int home) {
     const unsigned long long v = ((unsigned long long)(seq + 1) << 32) | block;
     unsigned long long* ring = st->retry + (size_t)t * kRetryStride;
-    for (;;) {
-        for (int jj = 0; jj < kRetrySlots; ++jj) {
-            const int j = (home + jj) % kRetrySlots;
-            if (atomicCAS(ring + j, 0ull, v) == 0ull) {
-                atomicOr(ring + kRetrySlots + (j >> 6), 1ull << (j & 63));
-                __threadfence();  // entry (and hint) visible before the count says so
-                atomicAdd(&st->tenants[t].retry_count, 1u);
-                return;
-            }
-        }
-        __nanosleep(256);  // ring full (more abandoned blocks than lanes): wait for a pop
-    }
+    const int j = claim_retry_slot(ring, home, v);
+    atomicOr(ring + kRetrySlots + (j >> 6), 1ull << (j & 63));
+    __threadfence();  // entry (and hint) visible before the count says so
+    atomicAdd(&st->tenants[t].retry_count, 1u);
 }
 
 __device__ __forceinline__ bool take_retry(DevState* st, int t, unsigned long long* ring, int j,
