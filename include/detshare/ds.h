@@ -219,7 +219,7 @@ int ds_quota_set(ds_domain* dom, const int32_t* owner, const int32_t* lender, in
 int ds_quota_get(ds_domain* dom, int32_t* owner, int32_t* lender, int n);
 /* Sub-block yields: blocks of an abandonable body launched by this tenant
  * (DS_BODY_GEMM_BF16 with GemmArgs.abandon != 0) give their logical block up
- * within ~4 k-blocks when the SM is revoked.  abandon = 1: the next claimer
+ * within ~2 k-blocks when the SM is revoked.  abandon = 1: the next claimer
  * re-runs the tile from scratch; abandon = 2: the fp32 accumulators are
  * spilled and the next claimer resumes at the same k-block.  Either way the
  * MMA sequence is unchanged, so results are bit-identical; only a completed
