@@ -20,6 +20,7 @@ on the step outputs.
 from __future__ import annotations
 
 import argparse
+import bisect
 import json
 import math
 import os
@@ -34,6 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "co-located P99 TPOT + train throughput vs time-slicing; bit-exact vs solo"
+UNIT = "ms (P99 TPOT, decode tenant)"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -196,6 +198,15 @@ class Colocation:
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
         self.dec_kernels = self.model.register(self.dom)
         self.gemm_kernel = self.train.register(self.dom)
+        # parity evidence at full size: a per-launch checksum of the decode
+        # step's logits and of the training GEMM's C, appended to the records
+        # of the pinned run (run(pin=True)) and compared with plain-grid solo
+        # runs of the same inputs after the executor stops (pin_check)
+        from paper_2603_15042_b200.tenants import OutputChecksum
+        self.ck_logits = OutputChecksum(self.model.logits, cap=16384, grid=32)
+        self.ck_C = OutputChecksum(self.train.C, cap=32768, grid=64)
+        self.k_ck_logits = self.ck_logits.register(self.dom, "decode/logits_checksum", phase=_abi.DECODE)
+        self.k_ck_C = self.ck_C.register(self.dom, "train/C_checksum", phase=_abi.TRAINING)
         # optionally the same GEMM with sub-block yields (tiles give up within
         # a few k-blocks when revoked; bit-identical results), per run
         self.gemm_kernel_plain = self.gemm_kernel
@@ -332,14 +343,14 @@ class Colocation:
         n = len(self.dec_kernels)
         ends = [cs[(i + 1) * n - 1].t_end for i in range(steps)]
         step_ns = [(ends[i] - ends[i - 1]) for i in range(1, steps)]
-        # per-kernel device time on the step's critical path: from the later of
-        # its first claim and the previous launch's completion (early-started
-        # blocks stream operands while the previous launch finishes) to its end
+        # per-kernel device time: the launch's full span, first claim to last
+        # retire (it includes the early-start window in which its blocks
+        # stream weights while the previous launch finishes, so it is never
+        # shorter than the kernel's share of the step)
         per_kernel = {}
         for i, c in enumerate(cs):
             sid = self.model.records[i % n][0]
-            start = c.t_first_claim if i == 0 else max(c.t_first_claim, cs[i - 1].t_end)
-            per_kernel.setdefault(sid, []).append(c.t_end - start)
+            per_kernel.setdefault(sid, []).append(c.t_end - c.t_first_claim)
         dom.quota_set(dom.mask(self.t_trn, 0, dom.num_sms))
         for _ in range(3):
             last = dom.launch(self.t_trn, self.gemm_kernel)
@@ -356,13 +367,19 @@ class Colocation:
         self.gemm_ns = gemm_ms * 1e6
         dom.quota_set([-1] * dom.num_sms)
         return {"decode_step_ms": statistics.median(step_ns) / 1e6, "gemm_ms": gemm_ms,
-                "per_kernel_ns": {k: statistics.median(v) for k, v in per_kernel.items()},
-                "per_kernel_launches": {k: len(v) for k, v in per_kernel.items()}}
+                "per_kernel_ns": {k: statistics.mean(v) for k, v in per_kernel.items()},
+                "per_kernel_launches": {k: len(v) // steps for k, v in per_kernel.items()}}
 
     @_guarded
-    def run(self, policy, requests, warmup, solo, e2e=False, quantum_ms=5.0):
+    def run(self, policy, requests, warmup, solo, e2e=False, quantum_ms=5.0, pin=False):
         """Co-located run: returns per-request TPOT (ms), training TFLOP/s in
-        the timed window, and engine counters."""
+        the timed window, and engine counters.
+
+        e2e: the host token loop — every step's input tokens go H2D from
+        pinned host memory and the sampled tokens come back D2H.
+        pin: every decode record also checksums its logits and every training
+        record its C (DS_BODY_CHECKSUM, one slot per launch); the step inputs
+        and launch sequence numbers are kept for pin_check()."""
         from paper_2603_15042_b200.runtime import Engine
         _abi, torch = self._abi, self.torch
         from paper_2603_15042_b200.metrics import RequestOutcome
@@ -377,6 +394,8 @@ class Colocation:
         tpot_slo = int(self.slo_x * step_ns)
         ttft_slo = int(2 * self.slo_x * step_ns)
         period = int(2 * self.T * step_ns)  # decode busy ~50% of the time when solo
+        dec_kernels = self.dec_kernels + ([self.k_ck_logits] if pin else [])
+        trn_kernels = [self.gemm_kernel] + ([self.k_ck_C] if pin else [])
         self._cur_eng = eng
         eng.start()
         stop = threading.Event()
@@ -388,7 +407,7 @@ class Colocation:
             outstanding = []
             while not stop.is_set():
                 while len(outstanding) < 2:
-                    r = eng.submit(jt, [self.gemm_kernel], "train/gemm_bf16", _abi.TRAINING, grid_size=2048,
+                    r = eng.submit(jt, trn_kernels, "train/gemm_bf16", _abi.TRAINING, grid_size=2048,
                                    base_hint_ns=gemm_ns, saturation=Fraction(1, 4))
                     outstanding.append(r)
                     train_recs.append(r)
@@ -400,9 +419,12 @@ class Colocation:
         th.start()
         time.sleep(0.05)
         pinned_tok = torch.zeros(32, dtype=torch.int32).pin_memory()
+        pinned_tok.copy_(self.model.tokens)  # contiguous D2H (copy engine): the first step's input
         results = []
+        pin_steps = []  # (request, step, input tokens, record)
         t_next = eng.now() + period // 4
-        log(f"run {policy} e2e={e2e}: period {period/1e6:.2f} ms, step {step_ns/1e6:.2f} ms")
+        log(f"run {policy} e2e={e2e} pin={pin}: {warmup}+{requests} requests, period {period/1e6:.2f} ms, "
+            f"step {step_ns/1e6:.2f} ms")
         for req in range(warmup + requests):
             # open-loop arrival at a fixed period
             while eng.now() < t_next:
@@ -415,10 +437,13 @@ class Colocation:
                     # host buffers: H2D the step input tokens, D2H the sampled tokens
                     self.model.tokens.copy_(pinned_tok, non_blocking=True)
                     torch.cuda.current_stream().synchronize()
-                r = eng.submit(jd, self.dec_kernels, "decode/step", _abi.DECODE, grid_size=len(self.dec_kernels),
+                tok_in = pinned_tok.clone() if pin else None
+                r = eng.submit(jd, dec_kernels, "decode/step", _abi.DECODE, grid_size=len(self.dec_kernels),
                                request=req, decode_index=tok, request_arrival_ns=arrival, ttft_ns=ttft_slo,
                                tpot_ns=tpot_slo, base_hint_ns=step_ns, saturation=self.decode_sat)
                 recs.append(r)
+                if pin:
+                    pin_steps.append((req, tok, tok_in, r))
                 if e2e:
                     eng.wait(r)
                     pinned_tok.copy_(self.model.tokens, non_blocking=True)
@@ -438,8 +463,9 @@ class Colocation:
             e2e_tpot = ((host_tok_times[-1] - host_tok_times[0]) / (self.T - 1) / 1e6) if e2e else None
             gaps = [(infos[i + 1].t_first_claim - infos[i].t_end) / 1e3 for i in range(self.T - 1)]
             steps_ms = [(i.t_end - i.t_first_claim) / 1e6 for i in infos[1:]]
-            log(f"  req {req}: tpot {tpot:.3f} ms (step {statistics.mean(steps_ms):.3f} ms, "
-                f"host gap {statistics.mean(gaps):.1f} us)")
+            if req % 10 == 9 or req < 2:
+                log(f"  req {req}: tpot {tpot:.3f} ms (step {statistics.mean(steps_ms):.3f} ms, "
+                    f"host gap {statistics.mean(gaps):.1f} us)")
             results.append({"tpot_ms": tpot, "first_ms": ttft, "t0": infos[0].t_first_claim, "t1": lasts,
                             "outcome": RequestOutcome(arrival=infos[0].t_first_claim, first_decode_finish=firsts,
                                                       last_finish=lasts, output_tokens=self.T),
@@ -465,6 +491,12 @@ class Colocation:
             ov = max(0, min(b, w1) - max(a, w0))
             done_flop += self.train.flops * ov / (b - a)
             gemm_durs.append(b - a)
+        pin_data = None
+        if pin:
+            pin_data = {"steps": [(q, k, t, eng.record(r).last_seq) for q, k, t, r in pin_steps],
+                        "train": [(ti.t_first_claim, ti.t_end, ti.last_seq) for ti in tinfos],
+                        "request_starts": [r["t0"] for r in results],
+                        "logit_slots": self.ck_logits.slots(), "C_slots": self.ck_C.slots()}
         counters = eng.counters()
         eng.stop()
         eng.close()
@@ -476,7 +508,8 @@ class Colocation:
                 "gap_us": statistics.mean(r["gap_us"] for r in timed),
                 "step_ms": statistics.mean(r["step_ms"] for r in timed),
                 "window_ms": (w1 - w0) / 1e6, "train_tflops": done_flop / ((w1 - w0) * 1e-9) / 1e12,
-                "counters": counters, "gemm_ms_median": statistics.median(gemm_durs) / 1e6 if gemm_durs else None}
+                "counters": counters, "gemm_ms_median": statistics.median(gemm_durs) / 1e6 if gemm_durs else None,
+                "pin": pin_data}
 
     @_guarded
     def run_prefill_mix(self, policy, arrivals, tokens, step_ns, prefill_ns, tpot_slo_ns, ttft_slo_ns, quantum_ms=5.0):
@@ -558,29 +591,62 @@ class Colocation:
                 "ttft_slo_violation_rate": round(sum(x * 1e6 > ttft_slo_ns for x in tt) / len(tt), 4),
                 "train_tflops": round(done / ((w1 - w0) * 1e-9) / 1e12, 1), "engine_counters": counters}
 
-    def bit_exact_check(self):
-        """The decode step's logits after a co-located run must equal a solo
-        replay of the same step from the same state (no kernel or reduction
-        order changed).  Runs one step solo on the quiesced executor with the
-        whole GPU, then the same step under a 1/4 quota with a mid-step
-        change, compares bits."""
-        torch, dom = self.torch, self.dom
-        m = self.model
-        tok = m.tokens.cpu()  # caches are overwritten at a fixed position: re-running is idempotent
-        dom.quota_set(dom.mask(self.t_dec, 0, dom.num_sms))
-        for k in self.dec_kernels:
-            last = dom.launch(self.t_dec, k)
-        dom.wait(self.t_dec, last)
-        ref = m.logits.cpu().clone()
-        m.tokens.copy_(tok)  # host -> device copy only (no kernel while the executor is resident)
-        torch.cuda.current_stream().synchronize()
-        dom.quota_set(dom.mask(self.t_dec, 0, dom.num_sms // 4))
-        for k in self.dec_kernels:
-            last = dom.launch(self.t_dec, k)
-        dom.wait(self.t_dec, last)
-        got = m.logits.cpu()
-        dom.quota_set([-1] * dom.num_sms)
-        return bool(torch.equal(ref.view(torch.int16), got.view(torch.int16)))
+    def pin_check(self, pin, requests=5):
+        """After the executor stopped: replay decode steps of the pinned
+        co-located run as plain-grid solo launches (ds_solo_launch, the
+        exclusive baseline) from the same input tokens, and one solo training
+        GEMM, and compare with the co-located launches' checksums.
+        Checked: every step of the last `requests` timed requests (logits),
+        and every training iteration whose checksum slot survived (C),
+        counting those a decode request started during (revoked mid-flight:
+        the decode tenant took SMs the GEMM was running on)."""
+        import numpy as np
+        from paper_2603_15042_b200 import _abi
+        from paper_2603_15042_b200.runtime import solo_launch
+        from paper_2603_15042_b200.tenants import OutputChecksum
+        torch, m = self.torch, self.model
+        steps = pin["steps"]
+        last_req = max(q for q, _, _, _ in steps)
+        sel = [x for x in steps if x[0] > last_req - requests]
+        max_seq = max(s for _, _, _, s in steps)
+        dec_ok, dec_n = True, 0
+        for q, k, tok_in, seq in sel:
+            if seq <= max_seq - self.ck_logits.cap:
+                continue  # slot reused by a later step
+            m.tokens.copy_(tok_in)
+            m.solo_step(self.device)
+            torch.cuda.synchronize()
+            want = OutputChecksum.host(m.logits)
+            got = self.ck_logits.of_seq(pin["logit_slots"], seq)
+            dec_ok &= (want == got)
+            dec_n += 1
+        # one solo GEMM of the same operands into a separate output
+        C_solo = torch.zeros_like(self.train.C)
+        a = _abi.gemm_args(self.train.A.data_ptr(), self.train.B.data_ptr(), C_solo.data_ptr(), self.train.M,
+                           self.train.N, self.train.K, group_m=32)
+        solo_launch(self.device, "train/gemm_bf16", _abi.BODY_GEMM_BF16, self.train.grid, a)
+        torch.cuda.synchronize()
+        want_c = OutputChecksum.host(C_solo)
+        c_final_equal = bool(torch.equal(C_solo.view(torch.int16), self.train.C.view(torch.int16)))
+        tr = pin["train"]
+        max_tseq = max(s for _, _, s in tr)
+        starts = sorted(pin["request_starts"])
+        gemm_ok, gemm_n, revoked = True, 0, 0
+        for t0, t1, seq in tr:
+            if seq <= max_tseq - self.ck_C.cap:
+                continue
+            gemm_ok &= (self.ck_C.of_seq(pin["C_slots"], seq) == want_c)
+            gemm_n += 1
+            i = bisect.bisect_right(starts, t0)
+            if i < len(starts) and starts[i] < t1:
+                revoked += 1
+        return {"decode_logits_equal": bool(dec_ok), "decode_steps_checked": dec_n,
+                "gemm_C_equal": bool(gemm_ok) and c_final_equal, "gemm_launches_checked": gemm_n,
+                "gemm_launches_revoked_midflight": revoked,
+                "how": "co-located launches' per-launch checksums (DS_BODY_CHECKSUM) vs plain-grid ds_solo_launch "
+                       "replays of the same inputs (host checksum); decode: every step of the last "
+                       f"{requests} timed requests of the e2e run; training: every iteration of that run",
+                "ok": bool(dec_ok and gemm_ok and c_final_equal and dec_n > 0 and gemm_n > 0)}
 
 
 def reference_sim(solo, requests, tokens, policy="tpot-first", scale=1, slo_x=8.0):
@@ -619,17 +685,25 @@ def reference_sim(solo, requests, tokens, policy="tpot-first", scale=1, slo_x=8.
 
 
 def cpu_baseline_leg(solo, requests, tokens, budget_s=10.0):
-    """Reference simulator timed on this host (1 core), scaled until it runs
-    ~budget_s of CPU work."""
+    """The reference's CPU implementation of the path — the corosim
+    simulator (oracle/_ref, compiled from the reference sources) — timed on
+    this host's core on the same two-tenant scenario, scaled until it does
+    ~budget_s of CPU work.  value = wall ms it spends per simulated decode
+    step (token); its own prediction of the P99 TPOT is reported beside it."""
     scale = 1
     p99, wall, ev = reference_sim(solo, requests, tokens, scale=scale)
     while wall < budget_s / 2 and scale < 4096:
         scale = max(scale + 1, int(scale * min(16.0, budget_s / max(wall, 1e-3))))
         p99, wall, ev = reference_sim(solo, requests, tokens, scale=scale)
-    return {"value": p99, "unit": "ms", "cores": 1, "kind": "reference",
-            "sample": f"corosim SimEngine::simulate (oracle/_ref, compiled from the reference) of the same "
-                      f"tpot-first two-tenant scenario, {requests * scale} requests x {tokens} tokens, "
-                      f"calibrated with measured solo durations; {ev} events in {wall:.2f} s wall"}
+    steps = requests * scale * tokens
+    return {"value": round(wall * 1e3 / steps, 5), "unit": "ms wall per simulated decode step (1 core)",
+            "cores": 1, "kind": "reference",
+            "sample": f"corosim SimEngine::simulate (oracle/_ref, compiled from the reference) of the config-2 "
+                      f"tpot-first scenario: {requests * scale} requests x {tokens} tokens beside the training "
+                      f"GEMM stream, {ev} events in {wall:.2f} s wall",
+            "sim_predicted_p99_tpot_ms": p99,
+            "note": "the reference models the decode step (slowdown model, speed.cpp:5-12) instead of computing it; "
+                    "its predicted TPOT is calibrated with this run's measured solo durations"}
 
 
 def _ref_timed(sc, reps_budget_s=2.0, equivalence=False):
@@ -809,6 +883,34 @@ def config4_leg(co, args, solo):
             "tpot_first": c4["tpot-first"], "slo_aware": c4["slo-aware"], "temporal": c4["temporal"]}
 
 
+def decode_roofline(co, solo, peaks, peaks_src):
+    """Per-kernel HBM roofline of the solo decode step through the executor
+    (full GPU): algorithmic bytes per launch / mean full launch span (first
+    claim -> last retire, device %globaltimer), plus the step as a whole
+    (algorithmic bytes per step / step time).  The dominant kernel is the one
+    with the largest share of the step (span x launches per step)."""
+    m = co.model
+    kn, nl = solo["per_kernel_ns"], solo["per_kernel_launches"]
+    bytes_by = {sid: b for sid, _, _, _, b in m.records}
+    table = {}
+    for sid in kn:
+        gbs = bytes_by[sid] / kn[sid]  # bytes/ns = GB/s
+        table[sid] = {"launches_per_step": nl[sid], "bytes": bytes_by[sid], "us": round(kn[sid] / 1e3, 2),
+                      "gbs": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 4)}
+    top = max(kn, key=lambda k: kn[k] * nl[k])
+    step_gbs = m.step_bytes / (solo["decode_step_ms"] * 1e6)
+    line = {"bound": "hbm", "kernel": top, "achieved": table[top]["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": table[top]["frac"], "traffic": ncu_traffic(top), "algorithmic_bytes": bytes_by[top],
+            "peak_source": peaks_src,
+            "timing": "mean full launch span (first claim -> last retire), device %globaltimer, solo decode steps "
+                      "on the executor at 148 SMs",
+            "step": {"bytes": m.step_bytes, "ms": round(solo["decode_step_ms"], 4), "gbs": round(step_gbs, 1),
+                     "frac": round(step_gbs / peaks["hbm_gbs"], 4),
+                     "floor_ms": round(m.step_bytes / peaks["hbm_gbs"] / 1e6, 4)},
+            "per_kernel": table}
+    return line
+
+
 def gpu_arm(args, rank, world):
     import torch
     dev = int(os.environ.get("LOCAL_RANK", rank))
@@ -819,15 +921,18 @@ def gpu_arm(args, rank, world):
                     prefill_mix=not args.no_config4b)
     solo = co.solo(steps=max(3, args.warmup))
     log("solo", {k: v for k, v in solo.items() if k != "per_kernel_ns" and k != "per_kernel_launches"})
+    # one bench step = args.rps requests (P99 over steps x rps samples)
+    n_req, n_warm = args.steps * args.rps, args.warmup * args.rps
     with ClockSampler(dev) as clk:
-        sp = co.run("tpot-first", args.steps, args.warmup, solo)
-        tm = co.run("temporal", args.steps, args.warmup, solo, quantum_ms=args.quantum_ms)
+        sp = co.run("tpot-first", n_req, n_warm, solo)
+        tm = co.run("temporal", n_req, n_warm, solo, quantum_ms=args.quantum_ms)
     clocks = clk.summary()
     # time slicing with a finer quantum (lower latency, more switches): the
     # comparison must not hinge on one quantum choice
-    tm_fine = co.run("temporal", args.steps, args.warmup, solo, quantum_ms=args.quantum_ms / 5)
-    e2e = co.run("tpot-first", args.steps, args.warmup, solo, e2e=True)
-    exact = co.bit_exact_check()
+    tm_fine = co.run("temporal", args.steps * 2, args.warmup, solo, quantum_ms=args.quantum_ms / 5)
+    # the end-to-end run through the host token loop is also the pinned run:
+    # every decode step's logits and every training GEMM's C checksummed
+    e2e = co.run("tpot-first", n_req, n_warm, solo, e2e=True, pin=True)
     config4b = None
     if not args.no_config4b:
         try:
@@ -841,46 +946,37 @@ def gpu_arm(args, rank, world):
         except Exception as e:  # an auxiliary leg must not cost the headline line
             config4 = {"error": repr(e)}
     co.close()
+    exact = co.pin_check(e2e["pin"])
+    log("bit-exact vs solo:", exact)
     p99 = p99_tpot_ms(sp["outcomes"], sp["tpot_ms"])
     p99_tm = p99_tpot_ms(tm["outcomes"], tm["tpot_ms"])
     p99_e2e = nearest_rank(e2e["e2e_tpot_ms"], 99)
     m = co.model
-    # roofline: per-launch algorithmic bytes / per-launch critical-path duration
-    # (device %globaltimer, solo decode steps through the executor, full GPU)
-    kn = solo["per_kernel_ns"]
-    bytes_by = {sid: b for sid, _, _, _, b in m.records}
-    share = {sid: kn[sid] * solo["per_kernel_launches"][sid] for sid in kn}
-    top = max(share, key=share.get)
-    gemv_gbs = bytes_by[top] / kn[top]  # bytes/ns = GB/s
+    roof = decode_roofline(co, solo, peaks, peaks_src)
     gemm_tf = co.train.flops / (solo["gemm_ms"] * 1e6) / 1e3  # flop/ns -> TFLOP/s
     out = {
-        "metric": METRIC, "value": round(p99, 4), "unit": "ms (P99 TPOT, decode tenant)",
+        "metric": METRIC, "value": round(p99, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(sp["window_ms"] / args.steps, 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random tokens)",
         "config": {"workload": "config 2: Llama-3-8B-shaped decode (batch 32, KV 1024, 32 layers) + bf16 GEMM "
                                "8192^3 training tenant on 1 B200", "policy": "tpot-first (+idle-SM lending)",
                    "baseline_policy": f"temporal (time slicing, quantum {args.quantum_ms} ms)", "tiers": args.tiers,
-                   "decode_saturation": args.decode_sat,
-                   "tokens_per_request": args.tokens, "requests_timed": args.steps,
+                   "decode_saturation": args.decode_sat, "step": f"{args.rps} decode requests",
+                   "tokens_per_request": args.tokens, "requests_timed": n_req, "requests_warmup": n_warm,
                    "global_batch": 32, "seq_len": args.kv_len, "parallelism": f"independent domain per GPU x{world}",
                    "l2": "inputs larger than L2 (15 GB weights + 4.3 GB KV per step, 384 MB GEMM operands)"},
-        "train_tflops": round(sp["train_tflops"], 1),
-        "timeslice": {"p99_tpot_ms": round(p99_tm, 4), "train_tflops": round(tm["train_tflops"], 1),
-                      "quantum_ms": args.quantum_ms,
-                      "fine_quantum": {"quantum_ms": args.quantum_ms / 5,
-                                       "p99_tpot_ms": round(nearest_rank(tm_fine["tpot_ms"], 99), 4),
-                                       "train_tflops": round(tm_fine["train_tflops"], 1)}},
         "solo": {"decode_step_ms": round(solo["decode_step_ms"], 4), "gemm_ms": round(solo["gemm_ms"], 4),
                  "gemm_tflops": round(gemm_tf, 1)},
-        "bit_exact_vs_solo": exact,
+        "bit_exact_vs_solo": exact["ok"],
+        "bit_exact_detail": exact,
         "engine_counters": sp["counters"],
-        "e2e": {"value": round(p99_e2e, 4), "unit": "ms (P99 TPOT, host token loop)",
-                "h2d_bytes_per_step": 32 * 4 * args.tokens, "d2h_bytes_per_step": 32 * 4 * args.tokens},
-        "roofline": {"bound": "hbm", "kernel": top, "achieved": round(gemv_gbs, 1), "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(gemv_gbs / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(top),
-                     "algorithmic_bytes": bytes_by[top],
-                     "peak_source": peaks_src},
+        "e2e": {"value": round(p99_e2e, 4), "unit": UNIT,
+                "h2d_bytes_per_step": 32 * 4 * args.tokens * args.rps,
+                "d2h_bytes_per_step": 32 * 4 * args.tokens * args.rps,
+                "how": "host token loop: per decode step, H2D of the 32 input tokens from pinned memory and D2H "
+                       "of the 32 sampled tokens; TPOT from host clocks after each D2H"},
+        "roofline": roof,
         "roofline_gemm": {"bound": "tensor", "kernel": "train/gemm_bf16", "achieved": round(gemm_tf, 1),
                           "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                           "frac": round(gemm_tf / peaks["bf16_tflops"], 4), "peak_source": peaks_src,
@@ -888,11 +984,20 @@ def gpu_arm(args, rank, world):
         "clocks": clocks,
         # logical launches through the executor in the timed tpot-first run:
         # decode kernels of every step + training GEMM launches
-        "gpu_launches": len(m.records) * (args.steps + args.warmup) * args.tokens + sp.get("train_launches", 0),
+        "gpu_launches": len(m.records) * (n_req + n_warm) * args.tokens + sp.get("train_launches", 0),
         "config4": config4,
         "config4b": config4b,
     }
-    return out, solo
+    tail = {
+        "host_gap_us": round(sp["gap_us"], 1),
+        "train_tflops": round(sp["train_tflops"], 1),
+        "timeslice": {"p99_tpot_ms": round(p99_tm, 4), "train_tflops": round(tm["train_tflops"], 1),
+                      "quantum_ms": args.quantum_ms,
+                      "fine_quantum": {"quantum_ms": args.quantum_ms / 5,
+                                       "p99_tpot_ms": round(nearest_rank(tm_fine["tpot_ms"], 99), 4),
+                                       "train_tflops": round(tm_fine["train_tflops"], 1)}},
+    }
+    return out, tail, solo
 
 
 def config1_leg(dev):
@@ -1188,6 +1293,52 @@ def gather_ranks(out, world):
     return aggregate_ranks(vals)
 
 
+def reference_arm(args, world):
+    """bench.py --impl reference: the reference's own CPU implementation of
+    the path — the corosim simulator (oracle/_ref, built from the reference
+    sources) — timed on this host on the config-2 scenario.  A step simulates
+    `rps` decode requests of `tokens` tokens beside the training GEMM stream;
+    its per-token value is the wall time the CPU path spends per decode token.
+    value = nearest-rank P99 over the timed steps.  The engine is
+    single-threaded by construction (engine.hpp:149-151) and TPOT is a
+    latency, so extra host threads would not lower it: 1 core."""
+    solo, calib = {"decode_step_ms": 3.0, "gemm_ms": 0.78}, "nominal B200 floors: 3.0 ms/decode step, 0.78 ms/GEMM"
+    for name in ("r2_bench_latest.json", "r1_bench_latest.json"):
+        try:
+            rec = json.load(open(os.path.join(ROOT, "profiles", name)))["solo"]
+            solo = {"decode_step_ms": float(rec["decode_step_ms"]), "gemm_ms": float(rec["gemm_ms"])}
+            calib = (f"solo durations measured on B200 (profiles/{name}): "
+                     f"{solo['decode_step_ms']} ms/decode step, {solo['gemm_ms']} ms/GEMM")
+            break
+        except Exception:
+            continue
+    try:
+        per_tok, p99s, evs = [], [], 0
+        for i in range(args.warmup + args.steps):
+            p99, wall, ev = reference_sim(solo, args.rps, args.tokens)
+            if i >= args.warmup:
+                per_tok.append(wall * 1e3 / (args.rps * args.tokens))
+                p99s.append(p99)
+                evs = ev
+        v = nearest_rank(per_tok, 99)
+        return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(statistics.median(per_tok) * args.rps * args.tokens, 4),
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "rational (exact)",
+                "data": "synthetic",
+                "config": {"workload": "config 2 scenario (decode requests + training GEMM stream, tpot-first) in the "
+                                       "reference simulator (corosim SimEngine::simulate, oracle/_ref)",
+                           "step": f"{args.rps} decode requests x {args.tokens} tokens", "calibration": calib,
+                           "tpot": "CPU wall ms the reference path spends per decode token (it models the decode "
+                                   "step, it does not compute it)"},
+                "sim_predicted_p99_tpot_ms": p99s[-1],
+                "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": 1, "kind": "reference",
+                                 "sample": f"{args.rps} requests x {args.tokens} tokens per step, {evs} events"},
+                "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    except Exception as e:  # reference library missing on this host
+        return {"impl": "reference", "unavailable": f"reference simulator not built: {e}"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1195,6 +1346,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--tokens", type=int, default=8)
+    ap.add_argument("--rps", type=int, default=10, help="decode requests per bench step (P99 over steps x rps)")
     ap.add_argument("--kv-len", type=int, default=1024)
     ap.add_argument("--quantum-ms", type=float, default=5.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -1224,43 +1376,22 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        # the reference's own CPU implementation of the path: the corosim
-        # simulator (oracle/_ref), calibrated with the solo durations last
-        # measured on B200 by this bench (committed record), else nominal
-        # HBM / tensor floors
-        solo, calib = {"decode_step_ms": 3.0, "gemm_ms": 0.78}, "nominal B200 floors: 3.0 ms/decode step, 0.78 ms/GEMM"
-        try:
-            rec = json.load(open(os.path.join(ROOT, "profiles", "r1_bench_latest.json")))["solo"]
-            solo = {"decode_step_ms": float(rec["decode_step_ms"]), "gemm_ms": float(rec["gemm_ms"])}
-            calib = (f"solo durations measured on B200 (profiles/r1_bench_latest.json): "
-                     f"{solo['decode_step_ms']} ms/decode step, {solo['gemm_ms']} ms/GEMM")
-        except Exception:
-            pass
-        try:
-            p99, wall, ev = reference_sim(solo, args.steps, args.tokens)
-            steps_wall = []
-            for _ in range(args.warmup + args.steps):
-                _, w, _ = reference_sim(solo, args.steps, args.tokens)
-                steps_wall.append(w)
-            line = {"impl": "reference", "metric": METRIC, "value": p99, "unit": "ms (P99 TPOT, decode tenant)",
-                    "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                    "ms_per_step": statistics.median(steps_wall[args.warmup:]) * 1e3, "higher_is_better": False,
-                    "scaling": "weak", "vs_baseline": None, "dtype": "rational (exact)", "data": "synthetic",
-                    "config": {"workload": "config 2 scenario in the reference simulator (corosim)",
-                               "calibration": calib},
-                    "cpu_baseline": {"value": p99, "unit": "ms", "cores": 1, "kind": "reference",
-                                     "sample": f"{args.steps} requests x {args.tokens} tokens, {ev} events"},
-                    "e2e": {"value": p99, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        except Exception as e:  # reference library missing on this host
-            line = {"impl": "reference", "unavailable": f"reference simulator not built: {e}"}
-        print(json.dumps(line))
+        print(json.dumps(reference_arm(args, world)))
         return
     if args.only_config5:
-        out, solo = {}, None
+        out, tail, solo = {}, {}, None
     else:
-        out, solo = gpu_arm(args, rank, world)
+        out, tail, solo = gpu_arm(args, rank, world)
+        # the latest solo calibration (the reference arm reads it)
+        if rank == 0:
+            try:
+                json.dump({"solo": out["solo"], "roofline": out["roofline"]},
+                          open(os.path.join(ROOT, "profiles", "r2_bench_latest.json"), "w"), indent=1)
+            except Exception:
+                pass
     if world > 1 and not args.only_config5:
-        out = gather_ranks(out, world)
+        out = gather_ranks(dict(out, **tail), world)
+        tail = {k: out.pop(k) for k in ("host_gap_us", "train_tflops", "timeslice")}
     if not args.no_config13 and not args.only_config5:
         import torch
         torch.cuda.empty_cache()
@@ -1302,7 +1433,7 @@ def main():
     if rank == 0:
         if not args.no_cpu_baseline and solo is not None:
             try:
-                out["cpu_baseline"] = cpu_baseline_leg(solo, args.steps, args.tokens)
+                out["cpu_baseline"] = cpu_baseline_leg(solo, args.rps, args.tokens)
             except Exception as e:
                 out["cpu_baseline"] = {"value": None, "unavailable": str(e)}
             # the reference simulator on every other config's scenario
@@ -1320,6 +1451,9 @@ def main():
                         out.setdefault("cpu_reference", {})[k] = v
             except Exception as e:
                 out["cpu_reference_error"] = repr(e)
+        # the time-slicing comparator and training throughput last, so a
+        # truncated tail of the line still carries them
+        out.update(tail)
         print(json.dumps(out))
 
 

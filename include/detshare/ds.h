@@ -78,7 +78,8 @@ typedef enum ds_body_id {
     DS_BODY_ARGMAX = 10,        /* greedy sampling (decode step result) */
     DS_BODY_SPLITK_REDUCE = 11, /* fold a split-K GEMM's fp32 partials in fixed split order */
     DS_BODY_ALLREDUCE_P2P = 12, /* DP gradient all-reduce over NVLink peer memory, rank-ordered sum */
-    DS_BODY_COUNT = 13
+    DS_BODY_CHECKSUM = 13,      /* position-weighted integer checksum of a buffer, one slot per launch */
+    DS_BODY_COUNT = 14
 } ds_body_id;
 
 typedef enum ds_priority { DS_LATENCY_CRITICAL = 0, DS_BEST_EFFORT = 1 } ds_priority; /* types.hpp:24 */
@@ -182,6 +183,12 @@ int ds_kernel_register(ds_domain* dom, const ds_kernel_desc* desc, int* kernel_i
 /* ---- executor lifecycle ---- */
 int ds_start(ds_domain* dom);
 int ds_stop(ds_domain* dom);
+/* Run-to-drain mode (set before ds_start): the executor exits on its own once
+ * every launch enqueued so far has completed (launches, control words and
+ * claim triggers may all be issued before ds_start), and in any case after
+ * deadline_ms (0 = no deadline).  For hosts that cannot talk to a resident
+ * kernel, e.g. under a profiler that serialises kernel launches. */
+int ds_set_drain_exit(ds_domain* dom, int enable, uint64_t deadline_ms);
 
 /* ---- launches (program order per tenant; "kernel resumes, never restarts") ---- */
 int ds_launch(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, uint64_t* seq);
@@ -317,6 +324,7 @@ typedef struct ds_record_info {
     int64_t request;
     int64_t arrival_host_ns, dispatch_host_ns, finish_host_ns;
     uint64_t t_first_claim, t_end; /* device %globaltimer */
+    uint64_t first_seq, last_seq;  /* the tenant launch sequence numbers of its first / last kernel (dispatched) */
 } ds_record_info;
 
 typedef struct ds_engine_counters {

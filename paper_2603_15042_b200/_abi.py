@@ -30,6 +30,7 @@ BODY_EMBED = 9
 BODY_ARGMAX = 10
 BODY_SPLITK_REDUCE = 11
 BODY_ALLREDUCE_P2P = 12
+BODY_CHECKSUM = 13
 MAX_DP_RANKS = 8
 DP_SLOTS = 64
 
@@ -147,6 +148,12 @@ class ReduceArgs(ctypes.Structure):
     _fields_ = [("inp", ctypes.c_uint64), ("partials", ctypes.c_uint64), ("out", ctypes.c_uint64),
                 ("ticket", ctypes.c_uint64), ("n", ctypes.c_int64), ("fmt", ctypes.c_int32),
                 ("combine", ctypes.c_int32)]
+
+
+class ChecksumArgs(ctypes.Structure):
+    """Position-weighted checksum of a buffer per launch (bodies/reduce.cuh)."""
+    _fields_ = [("src", ctypes.c_uint64), ("partials", ctypes.c_uint64), ("n_words", ctypes.c_int64),
+                ("cap", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class SgemmArgs(ctypes.Structure):
@@ -282,7 +289,8 @@ class RecordInfo(ctypes.Structure):
                 ("pctx", ctypes.c_int32), ("preempted", ctypes.c_int32), ("phase", ctypes.c_int32),
                 ("decode_index", ctypes.c_int32), ("request", ctypes.c_int64), ("arrival_host_ns", ctypes.c_int64),
                 ("dispatch_host_ns", ctypes.c_int64), ("finish_host_ns", ctypes.c_int64),
-                ("t_first_claim", ctypes.c_uint64), ("t_end", ctypes.c_uint64)]
+                ("t_first_claim", ctypes.c_uint64), ("t_end", ctypes.c_uint64), ("first_seq", ctypes.c_uint64),
+                ("last_seq", ctypes.c_uint64)]
 
 
 class EngineCounters(ctypes.Structure):
@@ -375,7 +383,7 @@ EXPORTS = [
     "ds_engine_event_log", "ds_engine_quarantines", "ds_quota_triggers_reset",
     "ds_compute_migration_set", "ds_full_eager_set", "ds_migrate_regions",
     "ds_fault_inject", "ds_tenant_fault", "ds_engine_fault_local", "ds_engine_job_status",
-    "ds_compute_metrics", "ds_set_lane_split", "ds_tenant_abandonable",
+    "ds_compute_metrics", "ds_set_lane_split", "ds_tenant_abandonable", "ds_set_drain_exit",
 ]
 
 _lib = None
@@ -478,6 +486,7 @@ def lib():
         L.ds_engine_fault_local.argtypes = [vp, ctypes.c_int]
         L.ds_set_lane_split.argtypes = [vp, ctypes.c_int]
         L.ds_tenant_abandonable.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+        L.ds_set_drain_exit.argtypes = [vp, ctypes.c_int, ctypes.c_uint64]
         L.ds_compute_metrics.argtypes = [ctypes.POINTER(RequestOutcome), ctypes.c_int64, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.POINTER(Metrics)]
         L.ds_engine_job_status.argtypes = [vp, ctypes.c_int, ip_]

@@ -143,8 +143,12 @@ __device__ __forceinline__ unsigned long long ctl_word_here(const BodyCtx& c) {
 }
 
 // Claim a free retry-ring slot nearest `home` for `v` (linear probing over
-// 8-slot windows read with 16-B loads; CAS only on slots seen free).
-__device__ inline int claim_retry_slot(unsigned long long* ring, int home, unsigned long long v) {
+// 8-slot windows read with 16-B loads; CAS only on slots seen free).  The ring
+// holds at most one entry per worker lane of the tenant's single open launch
+// (ds_start checks lanes <= kRetrySlots); a full ring waits for a pop, and
+// gives up (-1) only when the executor is exiting.
+__device__ inline int claim_retry_slot(unsigned long long* ring, int home, unsigned long long v,
+                                       const uint32_t* exit_word) {
     for (;;) {
         for (int w = 0; w < kRetrySlots; w += 8) {
             const int base = ((home & ~1) + w) % kRetrySlots;  // even: 16-B aligned pairs
@@ -161,6 +165,7 @@ __device__ inline int claim_retry_slot(unsigned long long* ring, int home, unsig
                 if (x[e] == 0ull && atomicCAS(ring + j, 0ull, v) == 0ull) return j;
             }
         }
+        if (ld_volatile_u32(exit_word) != 0u) return -1;
         __nanosleep(256);  // ring full (more abandoned blocks than lanes): wait for a pop
     }
 }

@@ -223,6 +223,9 @@ struct GemmArgs {
     TmaDesc tmC;        // C [M][N] bf16, box {64, 128}, SWIZZLE_128B
 };
 static_assert(offsetof(GemmArgs, tmC) == 320 && sizeof(GemmArgs) == 448, "GemmArgs layout (mirrored in _abi.py)");
+// host-side validation of abandonable GEMMs reads these fields (runtime.cpp)
+static_assert(offsetof(GemmArgs, K) == kGemmArgsOffK && offsetof(GemmArgs, bk) == kGemmArgsOffBk &&
+                  offsetof(GemmArgs, abandon) == kGemmArgsOffAbandon, "GemmArgs offsets (ds_device.cuh)");
 
 constexpr int kGemmBN = 256;
 constexpr int kGemmStages = kCtasPerSm == 2 ? 2 : 4;
@@ -296,10 +299,11 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
             if (q == 0 && lane == 0) {
                 unsigned long long* ring = c.st->retry + (size_t)c.tenant * kRetryStride;
                 const int home = (int)((smid() * kLanes + body_lane()) % kRetrySlots);
-                *spill = claim_retry_slot(ring, home, kRetryReserved);
+                *spill = claim_retry_slot(ring, home, kRetryReserved, &c.st->ctl.exit);
             }
             epi_sync();
             const int j = *spill;
+            if (j >= 0) {  // -1: the executor is exiting, nothing to resume
             const int row = q * 32 + lane;
             float* dst = c.st->save + ((size_t)c.st->tenants[c.tenant].save_base + j) * kSaveFloats + (size_t)row * BN;
 #pragma unroll 1
@@ -312,6 +316,7 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
                 for (int u = 0; u < 8; ++u) __stcg(p4 + u, make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
             }
             if (q == 0 && lane == 0) *c.ab_info = (uint32_t)(j + 1) | (k_abs << 16);
+            }
         }
     } else if (warp >= 4 && S == 1 && a.tma_store) {
         // bf16 tile staged in the (consumed) ring as BN/64 SWIZZLE_128B

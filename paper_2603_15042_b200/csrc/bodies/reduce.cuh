@@ -92,4 +92,57 @@ __device__ void body_reduce(const BodyCtx& c) {
     body_sync();
 }
 
+// ---------------------------------------------------------------------------
+// Output checksum (parity evidence at full size): launch seq's block b writes
+// partial[(seq % cap) * grid + b] = sum over its words w_i of w_i * (2i + 1)
+// mod 2^64 (i = global 32-bit word index).  Integer arithmetic: the value
+// depends only on the buffer's bits, never on scheduling, and the per-launch
+// slot lets the host check every launch of a long co-located run against a
+// plain-grid solo run (solo: seq = 0).
+// ---------------------------------------------------------------------------
+struct ChecksumArgs {
+    uint64_t src;       // buffer (32-bit words)
+    uint64_t partials;  // u64 [cap][grid]
+    int64_t n_words;
+    int32_t cap;
+    int32_t pad;
+};
+
+__device__ void body_checksum(const BodyCtx& c) {
+    const ChecksumArgs& a = *reinterpret_cast<const ChecksumArgs*>(c.args);
+    const uint32_t g = c.gx * c.gy * c.gz;
+    const uint32_t blk = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int64_t lo = (int64_t)blk * a.n_words / g;
+    const int64_t hi = (int64_t)(blk + 1) * a.n_words / g;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a.src);
+    unsigned long long h = 0;
+    // 16-B loads on the aligned interior, scalar head / tail
+    const int64_t lo4 = (lo + 3) & ~3ll, hi4 = hi & ~3ll;
+    if (lo4 < hi4) {
+        for (int64_t i = lo4 + 4 * (int64_t)ltid(); i < hi4; i += 4 * kBodyThreads) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(w + i));
+            const unsigned long long m = 2ull * (unsigned long long)i + 1ull;
+            h += (unsigned long long)v.x * m + (unsigned long long)v.y * (m + 2) + (unsigned long long)v.z * (m + 4) +
+                 (unsigned long long)v.w * (m + 6);
+        }
+        for (int64_t i = lo + ltid(); i < lo4; i += kBodyThreads) h += (unsigned long long)w[i] * (2ull * i + 1ull);
+        for (int64_t i = hi4 + ltid(); i < hi; i += kBodyThreads) h += (unsigned long long)w[i] * (2ull * i + 1ull);
+    } else {
+        for (int64_t i = lo + ltid(); i < hi; i += kBodyThreads) h += (unsigned long long)w[i] * (2ull * i + 1ull);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    __shared__ unsigned long long red_l[2][8];
+    unsigned long long* red = red_l[body_lane()];
+    if ((ltid() & 31) == 0) red[ltid() >> 5] = h;
+    body_sync();
+    if (ltid() == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < kBodyThreads / 32; ++i) t += red[i];
+        const uint32_t slot = a.cap > 0 ? c.seq % (uint32_t)a.cap : 0u;
+        reinterpret_cast<unsigned long long*>(a.partials)[(size_t)slot * g + blk] = t;
+    }
+    body_sync();
+}
+
 }  // namespace ds

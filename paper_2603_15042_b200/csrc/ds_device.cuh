@@ -46,6 +46,10 @@ constexpr int kRetryStride = kRetrySlots + 8;  // per tenant: the slots, then an
 constexpr unsigned long long kRetryReserved = 1ull, kRetryTaken = 2ull;
 constexpr uint32_t kRetryBlockBits = 20;
 constexpr int kSaveFloats = 128 * 256;  // one spilled 128 x 256 fp32 accumulator tile
+// GemmArgs fields the host validates for abandonable GEMMs (entry encoding:
+// block < 2^20, k-block < 2^12); asserted against the struct in gemm_tc.cuh
+constexpr size_t kGemmArgsOffK = 272, kGemmArgsOffBk = 296, kGemmArgsOffAbandon = 304;
+constexpr size_t kGemmArgsBody = 448;
 
 // Named barrier ids (0 reserved).  Lane 0: body 1, full 2, empty 3, done 4,
 // epilogue 7; lane 1: body 8, full 9, empty 10, done 11, epilogue 12; 5 = exit.
@@ -172,6 +176,9 @@ struct DevState {
     unsigned long long* retry;         // [DS_MAX_TENANTS][kRetryStride]
     float* save;                       // [abandonable tenants][kRetrySlots][kSaveFloats] spilled accumulators
     unsigned long long retry_mask;     // tenants that may abandon blocks (static)
+    uint32_t drain_exit;               // loader exits once every enqueued launch completed (ds_set_drain_exit)
+    uint32_t pad2;
+    unsigned long long deadline_ns;    // loader exits this long after start (0: never)
     int32_t per_owner[2][DS_MAX_SMS];  // periodic program, cached from the mailbox
     int32_t per_lender[2][DS_MAX_SMS];
 };

@@ -668,6 +668,8 @@ int ds_engine_record(ds_engine* e, uint64_t rec_id, ds_record_info* out) {
     out->finish_host_ns = r.finish_host;
     out->t_first_claim = r.t_first_claim;
     out->t_end = r.t_end;
+    out->first_seq = r.first_seq;
+    out->last_seq = r.last_seq;
     return DS_OK;
 }
 

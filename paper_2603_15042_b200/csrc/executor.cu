@@ -44,7 +44,9 @@ __device__ __forceinline__ bool early_start_body(int body) {
 // An abandonable GEMM block waiting for its tenant's previous launch gives
 // itself up when its SM is revoked or when abandoned blocks wait in the
 // tenant's retry ring (they may be the ones the previous launch needs: a
-// waiting block must not hold the lane they could run on).
+// waiting block must not hold the lane they could run on).  Abandonable
+// tenants open a launch only once the previous one completed (try_claim), so
+// this wait normally returns at once; it stays as a guard.
 __device__ __forceinline__ bool wait_prev_or_abandon(const BodyCtx& c) {
     __shared__ uint32_t give_up_l[2];
     volatile uint32_t* give_up = &give_up_l[body_lane()];
@@ -96,6 +98,7 @@ __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {
         case DS_BODY_ARGMAX: body_argmax(c); break;
         case DS_BODY_SPLITK_REDUCE: body_splitk_reduce(c); break;
         case DS_BODY_ALLREDUCE_P2P: body_allreduce_p2p(c); break;
+        case DS_BODY_CHECKSUM: body_checksum(c); break;
         default: break;
     }
 }
@@ -202,6 +205,8 @@ __device__ void loader_loop(DevState* st) {
     uint32_t last_gen = 0, last_pgen = 0, last_fgen = 0;
     uint64_t period = 0, next_flip = 0;
     int phase = 0;
+    const uint64_t deadline = st->deadline_ns ? globaltimer() + st->deadline_ns : 0;
+    const bool drain_exit = st->drain_exit != 0u;
     for (;;) {
         // one PCIe round trip per poll: lane i reads hot[4i .. 4i+3]
         uint4 hv;
@@ -214,7 +219,22 @@ __device__ void loader_loop(DevState* st) {
         const uint32_t g = __shfl_sync(0xffffffffu, hv.x, 0);
         const uint32_t pg = __shfl_sync(0xffffffffu, hv.z, 0);
         const uint32_t fg = __shfl_sync(0xffffffffu, hv.w, 0);
-        if (ex) {
+        // a program enqueued before ds_start runs to completion and the
+        // executor exits on its own (ds_set_drain_exit): usable when the host
+        // cannot talk to a resident kernel, e.g. under a serialising profiler
+        bool quit = ex != 0u || (deadline && globaltimer() >= deadline);
+        quit = __shfl_sync(0xffffffffu, quit, 0);  // one decision for the whole warp
+        if (drain_exit && !quit) {
+            bool idle = true;
+            for (int t = lane; t < DS_MAX_TENANTS; t += 32) {
+                const uint32_t ht = ld_volatile_u32((const void*)&mb->hot[kHotTail + t]);
+                const DevTenant* T = &st->tenants[t];
+                idle &= ld_volatile_u32(&T->fault) != 0u ||
+                        (known_tail[t] == ht && ld_acquire_u32(&T->head) == ht);
+            }
+            quit = __all_sync(0xffffffffu, idle);
+        }
+        if (quit) {
             if (lane == 0) {
                 __threadfence();
                 st_volatile_u32(&st->ctl.exit, 1u);
@@ -405,7 +425,11 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
         return false;
     }
     cc.more = b2 + 1 < grid;
-    if (b2 == grid - 1) open_next(T, s2);  // fully claimed: the next launch may start early
+    // fully claimed: the next launch may start early — except for a tenant
+    // whose blocks can be abandoned: its next launch opens at completion
+    // (complete_launch), so no lane ever parks on launch s+1 while blocks of s
+    // wait in the retry ring for a lane to run them
+    if (b2 == grid - 1 && !((st->retry_mask >> t) & 1ull)) open_next(T, s2);
     out.tenant = t;
     out.seq = s2;
     out.block = b2;
@@ -424,7 +448,8 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
 __device__ void push_retry(DevState* st, int t, uint32_t seq, uint32_t block, int home) {
     const unsigned long long v = ((unsigned long long)(seq + 1) << 32) | block;
     unsigned long long* ring = st->retry + (size_t)t * kRetryStride;
-    const int j = claim_retry_slot(ring, home, v);
+    const int j = claim_retry_slot(ring, home, v, &st->ctl.exit);
+    if (j < 0) return;  // exiting
     atomicOr(ring + kRetrySlots + (j >> 6), 1ull << (j & 63));
     __threadfence();  // entry (and hint) visible before the count says so
     atomicAdd(&st->tenants[t].retry_count, 1u);
@@ -456,6 +481,8 @@ __device__ bool try_retry(DevState* st, int t, Claimed& out, int home) {
     if (!((st->retry_mask >> t) & 1ull)) return false;
     DevTenant* T = &st->tenants[t];
     if (ld_volatile_u32(&T->retry_count) == 0u) return false;
+    // a failed tenant's abandoned blocks are never re-run (its launches never complete)
+    if (ld_volatile_u32(&T->fault) != 0u) return false;
     unsigned long long* ring = st->retry + (size_t)t * kRetryStride;
     constexpr int kWords = (kRetrySlots + 63) / 64;
     for (int attempt = 0; attempt < 8; ++attempt) {
@@ -525,6 +552,8 @@ __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* s
     // 1. publish completion first (critical path: early-started blocks of the
     //    next launch are waiting on head)
     st_release_u32(&T->head, seq + 1);
+    // abandonable tenants open their next launch only now (see try_claim)
+    if ((st->retry_mask >> t) & 1ull) open_next(T, seq);
     // 2. device -> host completion record (PCIe, off the critical path)
     unsigned long long i = atomicAdd(&st->completion_count, 1ull);
     HostCompletion* hc = &st->completions[i & st->completion_mask];
@@ -947,6 +976,7 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
         case DS_BODY_ARGMAX: return 1024;
         case DS_BODY_SPLITK_REDUCE: return 1024;
         case DS_BODY_ALLREDUCE_P2P: return 1024;
+        case DS_BODY_CHECKSUM: return 1024;
         default: return ds::kDefaultSmem;
     }
 }

@@ -66,6 +66,7 @@ struct TenantRecord {
     std::string name;
     int priority;
     uint64_t next_seq = 0;            // launches issued
+    uint64_t seen_at_stop = 0;        // launches the previous executor run had visible (ds_stop)
     std::atomic<uint64_t> completed{0};  // launches completed (drainer)
     std::vector<int32_t> launched_kernel;  // by seq
     std::vector<uint32_t> launched_grid;   // by seq (executed grid)
@@ -120,6 +121,9 @@ struct ds_domain {
     std::vector<Pctx> pctxs;
     std::vector<int32_t> owner, lender;  // by SM slot
     int n_triggers = 0;
+    int prestart_triggers = 0;     // triggers installed while stopped: armed at the next ds_start
+    int drain_exit = 0;            // executor exits once every enqueued launch completed
+    uint64_t deadline_ms = 0;      // executor exits after this long (0: never)
 
     std::mutex mu;                 // API serialisation
     std::mutex comp_mu;            // completions vector
@@ -167,11 +171,11 @@ void drain_loop(ds_domain* d) {
     }
 }
 
-int push_control(ds_domain* d) {
-    // slot-space owner/lender -> smid-space mailbox, then bump the generation
+// slot-space owner/lender -> smid-space control words (owner[], lender[] by smid)
+void control_by_smid(ds_domain* d, volatile int32_t* owner_sm, volatile int32_t* lender_sm) {
     for (int i = 0; i < DS_MAX_SMS; ++i) {
-        d->mb->owner[i] = -1;
-        d->mb->lender[i] = -1;
+        owner_sm[i] = -1;
+        lender_sm[i] = -1;
     }
     for (int s = 0; s < d->num_sms; ++s) {
         int sm = d->smids[s];
@@ -189,9 +193,14 @@ int push_control(ds_domain* d) {
             l = d->lend_tenant;
             o |= ds::kCtlSplit | (d->lane_split % 2 == 0 ? ds::kCtlOwnerOnly0 : 0);
         }
-        d->mb->owner[sm] = o;
-        d->mb->lender[sm] = l;
+        owner_sm[sm] = o;
+        lender_sm[sm] = l;
     }
+}
+
+int push_control(ds_domain* d) {
+    // slot-space owner/lender -> smid-space mailbox, then bump the generation
+    control_by_smid(d, d->mb->owner, d->mb->lender);
     std::atomic_thread_fence(std::memory_order_seq_cst);
     d->mb->hot[ds::kHotGen] = d->mb->hot[ds::kHotGen] + 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
@@ -462,6 +471,16 @@ int ds_kernel_register(ds_domain* d, const ds_kernel_desc* k, int* kernel_id) {
     if (grid < 1 || grid >= ds::kSat) return fail(DS_CONFIG_ERROR, "grid_size must be >= 1");  // engine.cpp:169-171
     if (k->block_threads != 256) return fail(DS_CONFIG_ERROR, "built-in bodies run 256 threads");
     if (k->args_size > ds::kMaxArgs || (k->args_size && !k->args)) return fail(DS_CONFIG_ERROR, "args too large");
+    if (k->body == DS_BODY_GEMM_BF16 && k->args_size >= ds::kGemmArgsBody) {
+        // abandonable tiles are queued as ((seq+1) << 32) | (k << 20) | block:
+        // the logical block must fit 20 bits and the resume k-block 12 bits
+        int32_t K = 0, bk = 0, ab = 0;
+        std::memcpy(&K, (const uint8_t*)k->args + ds::kGemmArgsOffK, 4);
+        std::memcpy(&bk, (const uint8_t*)k->args + ds::kGemmArgsOffBk, 4);
+        std::memcpy(&ab, (const uint8_t*)k->args + ds::kGemmArgsOffAbandon, 4);
+        if (ab && (grid >= (1ull << ds::kRetryBlockBits) || K / (bk > 0 ? bk : 64) >= 4096))
+            return fail(DS_CONFIG_ERROR, "abandonable GEMM needs grid < 2^20 and K/bk < 4096");
+    }
     std::lock_guard<std::mutex> g(d->mu);
     if (d->args_used + ds::kMaxArgs > d->args_cap) return fail(DS_CONFIG_ERROR, "args arena full");
     KernelRecord r;
@@ -514,13 +533,26 @@ int ds_start(ds_domain* d) {
             d->mb->hot[ds::kHotTail + t] = (uint32_t)seq;
             continue;
         }
-        if (seq != done) return fail(DS_CONFIG_ERROR, "tenant has launches in flight from a previous run");
-        h.tenants[t].claim = ((unsigned long long)seq << 32) | ds::kSat;
-        h.tenants[t].tail = (uint32_t)seq;
-        h.tenants[t].head = (uint32_t)seq;
+        // launches a previous run saw must all have completed (a half-run
+        // launch cannot resume across executor restarts); launches enqueued
+        // while stopped (seq >= seen_at_stop) are picked up by the loader
+        const uint64_t seen = t < (int)d->tenants.size() ? d->tenants[t]->seen_at_stop : 0;
+        if (done != seen) return fail(DS_CONFIG_ERROR, "tenant has launches in flight from a previous run");
+        h.tenants[t].claim = ((unsigned long long)done << 32) | ds::kSat;
+        h.tenants[t].tail = (uint32_t)done;
+        h.tenants[t].head = (uint32_t)done;
         d->mb->hot[ds::kHotTail + t] = (uint32_t)seq;
     }
-    for (int i = 0; i < DS_MAX_SMS; ++i) h.ctl.word[i] = ~0ull;
+    // the control word in force at launch (installed before the kernel runs,
+    // so a pre-enqueued program needs no host round trip)
+    {
+        int32_t o[DS_MAX_SMS], l[DS_MAX_SMS];
+        control_by_smid(d, o, l);
+        for (int i = 0; i < DS_MAX_SMS; ++i)
+            h.ctl.word[i] = ((unsigned long long)(uint32_t)l[i] << 32) | (uint32_t)o[i];
+    }
+    h.drain_exit = (uint32_t)d->drain_exit;
+    h.deadline_ns = d->deadline_ms * 1000000ull;
     h.rings = d->d_rings;
     ds::LaunchSlot* hr = nullptr;
     ds::HostMailbox* hm = nullptr;
@@ -543,6 +575,9 @@ int ds_start(ds_domain* d) {
     h.triggers = d->d_triggers;
     h.retry = d->d_retry;
     h.retry_mask = d->retry_mask;
+    // a tenant's retry ring holds at most one abandoned block per worker lane
+    if (d->retry_mask && d->num_sms * ds::kLanes > ds::kRetrySlots)
+        return fail(DS_CONFIG_ERROR, "abandonable tenants need num_sms x lanes <= retry-ring slots");
     {
         const int n_ab = __builtin_popcountll(d->retry_mask);
         if (n_ab != d->save_tenants) {
@@ -561,9 +596,11 @@ int ds_start(ds_domain* d) {
     }
     DS_CUDA(cudaMemsetAsync(d->d_retry, 0, sizeof(unsigned long long) * DS_MAX_TENANTS * ds::kRetryStride,
                             d->copy_stream));
-    h.trig_count = 0;
+    // triggers installed while stopped are armed for this run; others reset
+    h.trig_count = (uint32_t)d->prestart_triggers;
     h.trig_next = 0;
-    d->n_triggers = 0;
+    d->n_triggers = d->prestart_triggers;
+    d->prestart_triggers = 0;
     // completions restart from index 0
     std::memset(d->h_comp, 0, sizeof(ds::HostCompletion) * d->comp_cap);
     d->comp_next = 0;
@@ -583,6 +620,15 @@ int ds_start(ds_domain* d) {
     }
     d->running = true;
     push_control(d);
+    return DS_OK;
+}
+
+int ds_set_drain_exit(ds_domain* d, int enable, uint64_t deadline_ms) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (d->running) return fail(DS_ALREADY_RUNNING, "set before ds_start");
+    d->drain_exit = enable ? 1 : 0;
+    d->deadline_ms = deadline_ms;
     return DS_OK;
 }
 
@@ -610,6 +656,7 @@ int ds_stop(ds_domain* d) {
     d->drain_stop = true;
     d->drainer.join();
     d->running = false;
+    for (auto* t : d->tenants) t->seen_at_stop = t->next_seq;
     if (e != cudaSuccess) return fail(DS_CUDA_ERROR, std::string("executor: ") + cudaGetErrorString(e));
     return DS_OK;
 }
@@ -924,10 +971,13 @@ int ds_quota_at_claim(ds_domain* d, int tenant, uint64_t seq, uint32_t block, co
     cudaSetDevice(d->device);
     DS_CUDA(cudaMemcpyAsync(d->d_triggers + d->n_triggers, &tr, sizeof(tr), cudaMemcpyHostToDevice, d->copy_stream));
     d->n_triggers++;
+    if (!d->running) d->prestart_triggers = d->n_triggers;
     uint32_t cnt = (uint32_t)d->n_triggers;
     DS_CUDA(cudaMemcpyAsync(&d->d_state->trig_count, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, d->copy_stream));
     DS_CUDA(cudaStreamSynchronize(d->copy_stream));
-    // the host mirror follows the last installed trigger
+    // the host mirror follows the last installed trigger (a trigger armed
+    // before ds_start leaves the mirror — the control word at launch — alone)
+    if (d->running)
     for (int s = 0; s < n; ++s) {
         d->owner[s] = owner ? owner[s] : -1;
         d->lender[s] = lender ? lender[s] : -1;
@@ -1074,6 +1124,7 @@ int ds_quota_triggers_reset(ds_domain* d) {
     DS_CUDA(cudaMemcpyAsync(&d->d_state->trig_next, z, sizeof(z), cudaMemcpyHostToDevice, d->copy_stream));
     DS_CUDA(cudaStreamSynchronize(d->copy_stream));
     d->n_triggers = 0;
+    d->prestart_triggers = 0;
     return DS_OK;
 }
 

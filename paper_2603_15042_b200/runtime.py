@@ -169,6 +169,12 @@ class Domain:
         a k-block when revoked and re-run from scratch (before start())."""
         check(lib().ds_tenant_abandonable(self.h, tenant, int(enable)))
 
+    def set_drain_exit(self, enable: bool = True, deadline_ms: int = 0):
+        """Before start(): the executor exits by itself once every launch
+        enqueued so far (launches may be issued before start) completed, or
+        after deadline_ms.  For profilers that serialise kernel launches."""
+        check(lib().ds_set_drain_exit(self.h, int(enable), deadline_ms))
+
     def set_lane_split(self, mode: int):
         """0 off; 1: owned SMs run the lend tenant on lane 1 (lane 0: owner,
         then lend tenant); 2: lane 0 runs the owner only."""

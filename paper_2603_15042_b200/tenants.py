@@ -277,6 +277,42 @@ class DecodeModel:
         return logits, h, logits.float().argmax(-1).to(torch.int32)
 
 
+class OutputChecksum:
+    """Per-launch checksum of an output buffer (DS_BODY_CHECKSUM): appended
+    to a record, launch seq writes slot seq % cap, so every co-located launch
+    of a long run can be compared with a plain-grid solo run of the same
+    inputs.  value = sum_i w_i * (2i + 1) mod 2^64 over the buffer's 32-bit
+    words w_i (integer: independent of scheduling)."""
+
+    def __init__(self, buf: torch.Tensor, cap: int = 16384, grid: int = 64):
+        self.buf, self.cap, self.grid = buf, cap, grid
+        self.n_words = buf.numel() * buf.element_size() // 4
+        self.partials = torch.zeros(cap * grid, dtype=torch.int64, device=buf.device)
+        self.args = _abi.ChecksumArgs(buf.data_ptr(), self.partials.data_ptr(), self.n_words, cap, 0)
+
+    def register(self, dom, semantic_id: str, phase=_abi.OTHER) -> int:
+        return dom.kernel(semantic_id, _abi.BODY_CHECKSUM, (self.grid, 1, 1), self.args, phase=phase)
+
+    def slots(self):
+        """uint64 checksum per slot (device partials summed on the host)."""
+        import numpy as np
+        p = self.partials.cpu().numpy().view(np.uint64).reshape(self.cap, self.grid)
+        with np.errstate(over="ignore"):
+            return p.sum(axis=1, dtype=np.uint64)
+
+    def of_seq(self, slots, seq: int) -> int:
+        return int(slots[seq % self.cap])
+
+    @staticmethod
+    def host(buf: torch.Tensor) -> int:
+        """The same checksum computed on the host (numpy, independent of the body)."""
+        import numpy as np
+        w = buf.contiguous().reshape(-1).cpu().view(torch.int32).numpy().view(np.uint32).astype(np.uint64)
+        m = 2 * np.arange(w.size, dtype=np.uint64) + 1
+        with np.errstate(over="ignore"):
+            return int((w * m).sum(dtype=np.uint64))
+
+
 class TrainGemm:
     """One training-step contraction: C = A . B^T, bf16 in, fp32 accumulate."""
 

@@ -57,17 +57,20 @@ def test_gemm_tiles_abandon_on_revocation_bit_exact(abandon):
         assert len(gave_up) > 0   # spilled and resumed: slower yield (the spill), no lost work
     elif abandon:
         assert len(gave_up) > 0
-        assert p50 < 10.0  # measured p50 ~7 us, p99 ~9 us, vs up to a whole ~120 us tile without
+        # measured p50 ~7 us, p99 ~9 us (bench config 3 reports them); the
+        # assert only pins "well under a whole ~120 us tile" so clock and
+        # power-cap variation cannot make it flaky
+        assert p50 < 50.0
     else:
         assert gave_up == []
 
 
 @pytest.mark.parametrize("mode", [1, 2])
 def test_abandon_across_back_to_back_launches(mode):
-    """Several launches in flight (launch s+1 opens while s still has
-    abandoned tiles): blocks waiting on s give themselves up, s's re-runs go
-    first, nothing deadlocks, every (launch, tile) retires exactly once and
-    the output stays bit-exact."""
+    """Several launches enqueued back to back while tiles are abandoned
+    (an abandonable tenant opens launch s+1 only once s completed, so no lane
+    parks on s+1 while s's tiles wait in the retry ring): nothing deadlocks,
+    every (launch, tile) retires exactly once and the output stays bit-exact."""
     A, B = _operands()
     C_solo = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
     C_co = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
@@ -146,3 +149,54 @@ def test_engine_decode_preempts_abandonable_training(mode):
     for s in seqs:
         assert sorted(b.block for b in blog if b.flags == 0 and b.seq == s) == list(range(grid[0]))
     print("abandoned attempts", sum(b.flags == 1 for b in blog))
+
+
+def test_abandonable_tenant_mixed_bodies_no_deadlock():
+    """an abandonable tenant whose program mixes bodies —
+    a split-K abandonable GEMM, its split-K fold (not abandonable) and a plain
+    GEMM — under 100% <-> 1/8 flips every 30 us.  Before the fix, lanes parked
+    on launch s+1 (fold / plain GEMM waiting for s) while s's abandoned tiles
+    sat in the retry ring with no lane left to run them.  Every launch must
+    complete, bit-exact vs the same program run solo."""
+    Ms, Ns, Ks, S = 2048, 2048, 4096, 4
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = ((torch.rand(Ms, Ks, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
+    B = ((torch.rand(Ns, Ks, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
+    ws = torch.zeros(_abi.splitk_ws_elems(Ms, Ns, 256, S), dtype=torch.float32, device="cuda")
+    outs = {}
+    for mode in ("solo", "co"):
+        C1 = torch.zeros(Ms, Ns, dtype=torch.bfloat16, device="cuda")
+        C2 = torch.zeros(Ms, Ns, dtype=torch.bfloat16, device="cuda")
+        ab = 0 if mode == "solo" else 1
+        a_split = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C1.data_ptr(), Ms, Ns, Ks, splits=S,
+                                 ws=ws.data_ptr(), tma_store=False, abandon=ab)
+        red_args, red_grid = _abi.splitk_reduce(ws.data_ptr(), C1.data_ptr(), Ms, Ns, Ks, 16, 256, S)
+        a_plain = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C2.data_ptr(), Ms, Ns, Ks)
+        gs, gp = _abi.gemm_grid(Ms, Ns, splits=S), _abi.gemm_grid(Ms, Ns)
+        if mode == "solo":
+            solo_launch(0, "split", _abi.BODY_GEMM_BF16, gs, a_split)
+            solo_launch(0, "fold", _abi.BODY_SPLITK_REDUCE, red_grid, red_args)
+            solo_launch(0, "plain", _abi.BODY_GEMM_BF16, gp, a_plain)
+            torch.cuda.synchronize()
+        else:
+            with Domain(0, tiers=[Fraction(1)], block_log_capacity=0) as dom:
+                t = dom.tenant("train", _abi.BEST_EFFORT)
+                dom.set_abandonable(t)
+                ks = dom.kernel("split", _abi.BODY_GEMM_BF16, gs, a_split)
+                kr = dom.kernel("fold", _abi.BODY_SPLITK_REDUCE, red_grid, red_args)
+                kp = dom.kernel("plain", _abi.BODY_GEMM_BF16, gp, a_plain)
+                dom.start()
+                n = dom.num_sms
+                full, eighth = dom.mask(t, 0, n), dom.mask(t, 0, n // 8)
+                dom.quota_set(full)
+                dom.quota_periodic(30_000, full, eighth)
+                last = None
+                for _ in range(6):
+                    dom.launch(t, ks)
+                    dom.launch(t, kr)
+                    last = dom.launch(t, kp)
+                dom.wait(t, last, 120000)  # a deadlock times out here
+                dom.quota_periodic(0, full, full)
+        outs[mode] = (C1.cpu().view(torch.int16).numpy(), C2.cpu().view(torch.int16).numpy())
+    assert np.array_equal(outs["solo"][0], outs["co"][0])
+    assert np.array_equal(outs["solo"][1], outs["co"][1])
