@@ -498,11 +498,29 @@ class Colocation:
                         "request_starts": [r["t0"] for r in results],
                         "logit_slots": self.ck_logits.slots(), "C_slots": self.ck_C.slots()}
         counters = eng.counters()
+        ledger = eng.ledger()
+        # normalized throughput (add_normalization, metrics.cpp:81-102): per
+        # job, exclusive span / shared span over the timed window; exclusive
+        # spans from the measured solo durations of the same work (training:
+        # its completed GEMMs back to back; decode: the same request starts,
+        # each request T solo steps)
+        from paper_2603_15042_b200.runtime import add_normalization
+        tw = [ti for ti in tinfos if ti.t_first_claim >= w0 and ti.t_end <= w1]
+        norm = None
+        if tw:
+            t_shared = (min(t.t_first_claim for t in tw), max(t.t_end for t in tw))
+            t_solo = (0, int(len(tw) * gemm_ns))
+            starts = [r["t0"] for r in timed]
+            d_shared = (starts[0], w1)
+            d_solo = (starts[0], starts[-1] + self.T * step_ns)
+            vals, agg = add_normalization([d_shared, t_shared], [d_solo, t_solo])
+            norm = {"decode": round(float(vals[0]), 4), "train": round(float(vals[1]), 4), "aggregate": round(agg, 4)}
         eng.stop()
         eng.close()
         dom.set_lend(-1)
         dom.quota_set([-1] * dom.num_sms)
         return {"tpot_ms": [r["tpot_ms"] for r in timed], "e2e_tpot_ms": [r["e2e_tpot_ms"] for r in timed],
+                "ledger": ledger, "normalized_throughput": norm,
                 "outcomes": [r["outcome"] for r in timed],
                 "train_launches": len(train_recs),
                 "gap_us": statistics.mean(r["gap_us"] for r in timed),
@@ -590,6 +608,35 @@ class Colocation:
                 "tpot_slo_violation_rate": round(sum(x * 1e6 > tpot_slo_ns for x in tp) / len(tp), 4),
                 "ttft_slo_violation_rate": round(sum(x * 1e6 > ttft_slo_ns for x in tt) / len(tt), 4),
                 "train_tflops": round(done / ((w1 - w0) * 1e-9) / 1e12, 1), "engine_counters": counters}
+
+    def solo_kernel_times(self, steps=3):
+        """After the executor stopped: every decode kernel as a plain-grid
+        solo launch (ds_solo_launch) in step order on one stream, each
+        bracketed by CUDA events on that stream (serialised like the ncu
+        launch list; every launch streams its own layer's weights, so the L2
+        holds none of them).  Returns {sid: mean us}, and the sum per step."""
+        from paper_2603_15042_b200 import _abi
+        from paper_2603_15042_b200.runtime import solo_launch
+        torch, m = self.torch, self.model
+        stream = torch.cuda.current_stream()
+        times = {}
+        for it in range(steps + 1):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(m.records) + 1)]
+            # hold the stream while the host enqueues the step, so no event
+            # pair includes host launch latency
+            torch.cuda._sleep(100_000_000)
+            ev[0].record(stream)
+            for i, (sid, body, grid, args, _) in enumerate(m.records):
+                solo_launch(self.device, sid, body, grid, args, stream.cuda_stream)
+                ev[i + 1].record(stream)
+            torch.cuda.synchronize()
+            if it == 0:
+                continue  # warm-up
+            for i, (sid, _, _, _, _) in enumerate(m.records):
+                times.setdefault(sid, []).append(ev[i].elapsed_time(ev[i + 1]) * 1e3)
+        per = {k: statistics.mean(v) for k, v in times.items()}
+        step_us = sum(per[sid] for sid, _, _, _, _ in m.records)
+        return per, step_us
 
     def pin_check(self, pin, requests=5):
         """After the executor stopped: replay decode steps of the pinned
@@ -883,32 +930,39 @@ def config4_leg(co, args, solo):
             "tpot_first": c4["tpot-first"], "slo_aware": c4["slo-aware"], "temporal": c4["temporal"]}
 
 
-def decode_roofline(co, solo, peaks, peaks_src):
-    """Per-kernel HBM roofline of the solo decode step through the executor
-    (full GPU): algorithmic bytes per launch / mean full launch span (first
-    claim -> last retire, device %globaltimer), plus the step as a whole
-    (algorithmic bytes per step / step time).  The dominant kernel is the one
-    with the largest share of the step (span x launches per step)."""
+def decode_roofline(co, solo, solo_us, solo_step_us, peaks, peaks_src):
+    """HBM roofline of the decode tenant.
+
+    Per kernel: algorithmic bytes per launch / the kernel's mean duration as a
+    plain-grid solo launch timed with CUDA events on its stream (solo_us:
+    serialised in step order, like the ncu launch list, so shares of the step
+    agree with profiles/).  The dominant kernel (largest share of the step) is
+    the line's roofline.  Beside it: the same kernels' full spans inside the
+    executor (first claim -> last retire, %globaltimer; spans of consecutive
+    launches overlap through early start), and the whole step on the executor
+    at 148 SMs (algorithmic bytes per step / step time)."""
     m = co.model
     kn, nl = solo["per_kernel_ns"], solo["per_kernel_launches"]
     bytes_by = {sid: b for sid, _, _, _, b in m.records}
     table = {}
-    for sid in kn:
-        gbs = bytes_by[sid] / kn[sid]  # bytes/ns = GB/s
-        table[sid] = {"launches_per_step": nl[sid], "bytes": bytes_by[sid], "us": round(kn[sid] / 1e3, 2),
-                      "gbs": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 4)}
-    top = max(kn, key=lambda k: kn[k] * nl[k])
+    for sid in solo_us:
+        gbs = bytes_by[sid] / (solo_us[sid] * 1e3)  # bytes/ns = GB/s
+        table[sid] = {"launches_per_step": nl[sid], "bytes": bytes_by[sid], "solo_us": round(solo_us[sid], 2),
+                      "gbs": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 4),
+                      "share_of_solo_step": round(solo_us[sid] * nl[sid] / solo_step_us, 4),
+                      "executor_span_us": round(kn[sid] / 1e3, 2)}
+    top = max(table, key=lambda k: table[k]["share_of_solo_step"])
     step_gbs = m.step_bytes / (solo["decode_step_ms"] * 1e6)
-    line = {"bound": "hbm", "kernel": top, "achieved": table[top]["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+    return {"bound": "hbm", "kernel": top, "achieved": table[top]["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": table[top]["frac"], "traffic": ncu_traffic(top), "algorithmic_bytes": bytes_by[top],
             "peak_source": peaks_src,
-            "timing": "mean full launch span (first claim -> last retire), device %globaltimer, solo decode steps "
-                      "on the executor at 148 SMs",
-            "step": {"bytes": m.step_bytes, "ms": round(solo["decode_step_ms"], 4), "gbs": round(step_gbs, 1),
-                     "frac": round(step_gbs / peaks["hbm_gbs"], 4),
+            "timing": "mean duration of the kernel as a plain-grid solo launch, CUDA events on its stream, "
+                      "launches serialised in decode-step order (the ncu launch-list setting)",
+            "step": {"bytes": m.step_bytes, "executor_ms": round(solo["decode_step_ms"], 4),
+                     "gbs": round(step_gbs, 1), "frac": round(step_gbs / peaks["hbm_gbs"], 4),
+                     "solo_serialised_ms": round(solo_step_us / 1e3, 4),
                      "floor_ms": round(m.step_bytes / peaks["hbm_gbs"] / 1e6, 4)},
             "per_kernel": table}
-    return line
 
 
 def gpu_arm(args, rank, world):
@@ -948,11 +1002,12 @@ def gpu_arm(args, rank, world):
     co.close()
     exact = co.pin_check(e2e["pin"])
     log("bit-exact vs solo:", exact)
+    solo_us, solo_step_us = co.solo_kernel_times()
     p99 = p99_tpot_ms(sp["outcomes"], sp["tpot_ms"])
     p99_tm = p99_tpot_ms(tm["outcomes"], tm["tpot_ms"])
     p99_e2e = nearest_rank(e2e["e2e_tpot_ms"], 99)
     m = co.model
-    roof = decode_roofline(co, solo, peaks, peaks_src)
+    roof = decode_roofline(co, solo, solo_us, solo_step_us, peaks, peaks_src)
     gemm_tf = co.train.flops / (solo["gemm_ms"] * 1e6) / 1e3  # flop/ns -> TFLOP/s
     out = {
         "metric": METRIC, "value": round(p99, 4), "unit": UNIT,
@@ -971,6 +1026,13 @@ def gpu_arm(args, rank, world):
         "bit_exact_vs_solo": exact["ok"],
         "bit_exact_detail": exact,
         "engine_counters": sp["counters"],
+        "ledger": {"tpot_first": sp["ledger"], "temporal": tm["ledger"],
+                   "what": "OverheadLedger from device %globaltimer stamps summed over worker lanes (ns): "
+                           "ctx_switch = lane gap between tenants, preempt = control install -> retire of the "
+                           "block a revoked lane was running, migration = control install -> a lane's first "
+                           "block of its new tenant"},
+        "normalized_throughput": {"tpot_first": sp["normalized_throughput"],
+                                  "temporal": tm["normalized_throughput"]},
         "e2e": {"value": round(p99_e2e, 4), "unit": UNIT,
                 "h2d_bytes_per_step": 32 * 4 * args.tokens * args.rps,
                 "d2h_bytes_per_step": 32 * 4 * args.tokens * args.rps,

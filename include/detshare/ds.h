@@ -54,7 +54,8 @@ typedef enum ds_status {
     DS_RING_FULL = 104,
     DS_INVALID_ARGUMENT = 105,
     DS_ALREADY_RUNNING = 106,
-    DS_TENANT_FAILED = 107      /* the tenant raised a local exception (ds_tenant_fault) */
+    DS_TENANT_FAILED = 107,     /* the tenant raised a local exception (ds_tenant_fault) */
+    DS_RECORD_MUTATED = 108     /* an immutable kernel record changed during the run (engine.cpp:1379-1383) */
 } ds_status;
 
 /* Local-exception codes a tenant body raises (any nonzero code may be injected). */
@@ -264,6 +265,36 @@ int ds_debug_dump(ds_domain* dom, char* out, int64_t cap); /* text snapshot of d
 /* host write of the control word -> device install acknowledged in host memory, n samples (ns) */
 int ds_ctl_roundtrip(ds_domain* dom, int n, uint64_t* out_ns);
 
+/* Overhead ledger (OverheadLedger, engine.hpp:94-107) measured from device
+ * %globaltimer stamps, summed over worker lanes (ns):
+ *   ctx_switch: a lane's gap between its last block of one tenant and its first of another
+ *   preempt:    a lane leaving a tenant its SM was revoked from: control install -> retire of
+ *               the block it was running (the boundary wait; count = lane yields)
+ *   migration:  a lane's first block of a tenant after a control change, from the install
+ *   demand_fault: always 0 (one address space per GPU; cross-GPU copies: ds_migrate_regions) */
+typedef struct ds_ledger {
+    uint64_t ctx_switches, ctx_switch_total_ns;
+    uint64_t preemptions, preempt_total_ns;
+    uint64_t migrations, migration_total_ns;
+    uint64_t demand_faults, demand_fault_total_ns;
+} ds_ledger;
+int ds_ledger_get(ds_domain* dom, ds_ledger* out);
+
+/* Kernel-record immutability (Kernel::fingerprint types.cpp:39-48; checked at
+ * finalize, engine.cpp:1379-1383): every registered kernel's fingerprint over
+ * its immutable record — semantic id, logical grid, body and argument block —
+ * recomputed from the device copy of the argument block the executor reads. */
+typedef struct ds_kernel_info {
+    uint64_t fingerprint;
+    uint64_t args_device;     /* device address of the immutable argument block */
+    uint32_t args_size, grid;
+    int32_t body, phase;
+} ds_kernel_info;
+int ds_kernel_info_get(ds_domain* dom, int kernel_id, ds_kernel_info* out);
+/* DS_OK if no record changed; DS_RECORD_MUTATED with the first mutated
+ * kernel id in *first_bad otherwise (-1 if none) */
+int ds_verify_kernels(ds_domain* dom, int* first_bad);
+
 /* ---- solo baseline: the same body as a plain __global__ grid (exclusive_baseline) ---- */
 int ds_solo_launch(int device, const ds_kernel_desc* desc, void* stream);
 int ds_solo_launch_registered(ds_domain* dom, int kernel_id, void* stream);
@@ -357,7 +388,104 @@ int ds_engine_quarantines(ds_engine* eng, int32_t* jobs, int64_t* t_ns, int cap,
 int ds_engine_fault_local(ds_engine* eng, int pctx);
 /* SimulationReport.vctx_status: 0 Active, 1 Failed, 2 Stranded (types.hpp:77) */
 int ds_engine_job_status(ds_engine* eng, int job, int* status);
+/* OverheadLedger of the run: the domain's device-measured ledger since ds_engine_start */
+int ds_engine_ledger(ds_engine* eng, ds_ledger* out);
+/* SimulationReport.kernel_fingerprints: xor of the job's launch-record
+ * fingerprints at submit; ds_engine_stop re-checks them and every device
+ * kernel record (ds_verify_kernels) and returns DS_RECORD_MUTATED on change */
+int ds_engine_job_fingerprint(ds_engine* eng, int job, uint64_t* fp);
 
+
+/* ---- user policies over the C ABI (Policy, policy.hpp:97-126) ----
+ * A policy is a POD vtable of pure, synchronous hooks over a read-only
+ * snapshot (PolicyView, policy.hpp:24-69).  The engine validates every
+ * returned decision exactly as the reference's apply_decision
+ * (engine.cpp:688-754): an illegal one becomes Defer and policy_errors++. */
+#define DS_VIEW_MAX_PCTX 64
+#define DS_VIEW_MAX_VCTX 64
+#define DS_VIEW_MAX_DEVICES 8
+
+typedef struct ds_view_pctx {          /* PolicyView::PctxEntry */
+    int32_t id, device;
+    int64_t tier_num, tier_den;
+    int32_t standby, available;
+    int32_t bound;                     /* vctx id, -1 = unbound */
+    int32_t has_running;
+    uint64_t running_kernel;           /* record id */
+    const char* running_semantic_id;   /* valid during the callback */
+    int64_t running_grid;
+    int64_t running_remaining_ns;      /* predicted remaining wall time */
+    int32_t running_phase, running_priority;
+} ds_view_pctx;
+
+typedef struct ds_view_vctx {          /* PolicyView::VctxEntry */
+    int32_t id, priority, quarantined, bound;
+    int64_t pending;
+    int32_t head_phase, decoding;
+} ds_view_vctx;
+
+typedef struct ds_view {               /* PolicyView */
+    int64_t now_ns;
+    int32_t n_pctx, n_vctx;
+    ds_view_pctx pctx[DS_VIEW_MAX_PCTX];   /* pool order across devices */
+    ds_view_vctx vctx[DS_VIEW_MAX_VCTX];
+    int32_t n_devices, pad;
+    int64_t bound_tier_sum_num[DS_VIEW_MAX_DEVICES], bound_tier_sum_den[DS_VIEW_MAX_DEVICES];
+    int64_t min_tier_num[DS_VIEW_MAX_DEVICES], min_tier_den[DS_VIEW_MAX_DEVICES];
+    int64_t active_vctx_count;
+    const void* predictor;             /* for ds_predictor_predict; valid during the callback */
+} ds_view;
+
+typedef struct ds_launch_ctx {         /* LaunchContext (policy.hpp:71-78) + its Kernel record */
+    int32_t vctx;
+    int32_t has_kernel;
+    uint64_t kernel_id;                /* record id */
+    const char* semantic_id;           /* valid during the callback */
+    int64_t grid_size, base_hint_ns;
+    int64_t sat_num, sat_den;
+    int32_t phase, decode_index;
+    int64_t request, arrival_ns, request_arrival_ns;
+    int32_t has_slo, pool_exhausted;
+    int64_t ttft_ns, tpot_ns;
+} ds_launch_ctx;
+
+typedef enum ds_decision_kind {        /* PolicyDecision::Kind */
+    DS_DISPATCH_DIRECT = 0, DS_DISPATCH_REMAP = 1, DS_DISPATCH_DEFER = 2, DS_PREEMPT = 3, DS_NO_ACTION = 4
+} ds_decision_kind;
+typedef struct ds_decision { int32_t kind; int32_t target; } ds_decision;
+
+/* Hooks write their decision to *out (plain C calling convention: no
+ * struct returns, so any FFI can implement them); *out arrives as the
+ * hook's default (defer / no action).  An out-of-range kind is an illegal
+ * decision (Defer + policy_errors). */
+typedef struct ds_policy_vtable {
+    const char* name;
+    void (*on_launch)(void* user, const ds_view* view, const ds_launch_ctx* launch, ds_decision* out);  /* required */
+    void (*on_completion)(void* user, const ds_view* view, const ds_launch_ctx* next, ds_decision* out); /* NULL: no action */
+    void (*on_congestion)(void* user, const ds_view* view, const ds_launch_ctx* launch, ds_decision* out); /* NULL: defer */
+    int (*launch_order_key)(void* user, const ds_launch_ctx* launch);                              /* NULL: 0 */
+    int (*next_review_time)(void* user, const ds_view* view, int64_t* t_ns);                       /* NULL or 0: none */
+    void (*destroy)(void* user);                                                                   /* NULL: none */
+} ds_policy_vtable;
+
+/* SimEngine(Scenario, std::unique_ptr<Policy>) (engine.hpp:155): the engine
+ * owns `user` and calls vt->destroy(user) from ds_engine_destroy. */
+int ds_engine_create_with_policy(ds_domain* dom, const ds_engine_config* cfg, const ds_policy_vtable* vt, void* user,
+                                 ds_engine** out);
+/* the PolicyView the engine would hand a hook right now (ds_snapshot) */
+int ds_engine_snapshot(ds_engine* eng, ds_view* out);
+/* DurationPredictor::predict (predictor.cpp:20-38) of the view's predictor:
+ * EWMA of measured device durations, else the hint (has_hint), else the
+ * largest seen for the semantic id, else the cold-start value. */
+int ds_predictor_predict(const void* predictor, const char* semantic_id, int64_t grid, int has_hint, int64_t hint_ns,
+                         int64_t* out_ns);
+/* predict_hol_blocking (policy.hpp:92-95) of pctx in a view */
+int ds_predict_hol_blocking(const ds_view* view, int pctx, int64_t* out_ns);
+/* the built-in policies' hooks over a C view (make_policy(name)): lets a C
+ * user policy delegate, and tests pin the C path to the C++ one */
+int ds_builtin_decide(const char* policy, int hook /* 0 launch, 1 completion, 2 congestion, 3 launch_order_key
+                                                     (the key in out->target) */, const ds_view* view,
+                      const ds_launch_ctx* launch, int64_t quantum_ns, ds_decision* out);
 
 /* ---- request streams and workload expansion ----
  * gen_poisson / gen_burst       proj/src/io/trace.cpp:189-232 (RequestTemplate trace.hpp:41-53)
@@ -470,6 +598,25 @@ typedef struct ds_metrics {  /* MetricsReport metrics.hpp:22-46 (throughputs per
  * deadline; incomplete or non-inference requests count only toward training. */
 int ds_compute_metrics(const ds_request_outcome* reqs, int64_t n, int64_t makespan_ns, int64_t kernels_completed,
                        ds_metrics* out);
+
+/* add_normalization (metrics.cpp:81-102): normalized throughput of job i =
+ * exclusive span / shared span of its kernels (first arrival -> last finish;
+ * 0 if a span is missing or the shared span is empty), exact num/den, and the
+ * aggregate sum.  The exclusive spans come from each job run alone
+ * (exclusive_baseline) on the same inputs. */
+typedef struct ds_job_span {
+    int64_t first_arrival_ns, last_finish_ns;
+    int32_t valid, pad;
+} ds_job_span;
+int ds_add_normalization(const ds_job_span* shared, const ds_job_span* solo, int n, int64_t* num, int64_t* den,
+                         double* aggregate);
+
+/* ---- determinism-lab inputs (the reduction tenant's input stream) ----
+ * seeded_values (equivalence.cpp:7-17): Rng(seed).uniform(-1, 1) rounded to
+ * the format (fmt 0 fp16, 1 bf16, 2 fp32; round_to float_format.cpp:43-67:
+ * RNE, subnormals, overflow -> inf, no signed zero); raw bit patterns. */
+int ds_seeded_values(uint64_t seed, int64_t n, int fmt, uint32_t* bits);
+int ds_round_to(int fmt, double x, uint32_t* bits);
 
 typedef struct ds_region {
     int32_t id;

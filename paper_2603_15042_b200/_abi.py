@@ -42,7 +42,9 @@ STATUS = {
     5: "EventBudgetExceeded", 6: "TraceViolation", 7: "PlanMismatch", 8: "InvalidSplit",
     9: "ParseError", 10: "ConfigError", 100: "CudaError", 101: "NoDevice", 102: "NotRunning",
     103: "Timeout", 104: "RingFull", 105: "InvalidArgument", 106: "AlreadyRunning", 107: "TenantFailed",
+    108: "RecordMutated",
 }
+RECORD_MUTATED = 108
 TENANT_FAILED = 107
 FAULT_BAD_INPUT, FAULT_INJECTED = 1, 2
 ACTIVE, FAILED, STRANDED = 0, 1, 2  # VctxStatus (types.hpp:77)
@@ -366,6 +368,79 @@ class TenantDemand(ctypes.Structure):
     _fields_ = [("priority", ctypes.c_int32), ("phase", ctypes.c_int32), ("hbm_frac", ctypes.c_double),
                 ("tensor_frac", ctypes.c_double), ("mem_gb", ctypes.c_double)]
 
+# ---- user policies over the C ABI (ds_policy_vtable) ----
+VIEW_MAX_PCTX = VIEW_MAX_VCTX = 64
+VIEW_MAX_DEVICES = 8
+DISPATCH_DIRECT, DISPATCH_REMAP, DISPATCH_DEFER, PREEMPT, NO_ACTION = 0, 1, 2, 3, 4
+
+
+class ViewPctx(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int32), ("device", ctypes.c_int32), ("tier_num", ctypes.c_int64),
+                ("tier_den", ctypes.c_int64), ("standby", ctypes.c_int32), ("available", ctypes.c_int32),
+                ("bound", ctypes.c_int32), ("has_running", ctypes.c_int32), ("running_kernel", ctypes.c_uint64),
+                ("running_semantic_id", ctypes.c_char_p), ("running_grid", ctypes.c_int64),
+                ("running_remaining_ns", ctypes.c_int64), ("running_phase", ctypes.c_int32),
+                ("running_priority", ctypes.c_int32)]
+
+
+class ViewVctx(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int32), ("priority", ctypes.c_int32), ("quarantined", ctypes.c_int32),
+                ("bound", ctypes.c_int32), ("pending", ctypes.c_int64), ("head_phase", ctypes.c_int32),
+                ("decoding", ctypes.c_int32)]
+
+
+class View(ctypes.Structure):
+    _fields_ = [("now_ns", ctypes.c_int64), ("n_pctx", ctypes.c_int32), ("n_vctx", ctypes.c_int32),
+                ("pctx", ViewPctx * VIEW_MAX_PCTX), ("vctx", ViewVctx * VIEW_MAX_VCTX),
+                ("n_devices", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("bound_tier_sum_num", ctypes.c_int64 * VIEW_MAX_DEVICES),
+                ("bound_tier_sum_den", ctypes.c_int64 * VIEW_MAX_DEVICES),
+                ("min_tier_num", ctypes.c_int64 * VIEW_MAX_DEVICES), ("min_tier_den", ctypes.c_int64 * VIEW_MAX_DEVICES),
+                ("active_vctx_count", ctypes.c_int64), ("predictor", ctypes.c_void_p)]
+
+
+class LaunchCtx(ctypes.Structure):
+    _fields_ = [("vctx", ctypes.c_int32), ("has_kernel", ctypes.c_int32), ("kernel_id", ctypes.c_uint64),
+                ("semantic_id", ctypes.c_char_p), ("grid_size", ctypes.c_int64), ("base_hint_ns", ctypes.c_int64),
+                ("sat_num", ctypes.c_int64), ("sat_den", ctypes.c_int64), ("phase", ctypes.c_int32),
+                ("decode_index", ctypes.c_int32), ("request", ctypes.c_int64), ("arrival_ns", ctypes.c_int64),
+                ("request_arrival_ns", ctypes.c_int64), ("has_slo", ctypes.c_int32), ("pool_exhausted", ctypes.c_int32),
+                ("ttft_ns", ctypes.c_int64), ("tpot_ns", ctypes.c_int64)]
+
+
+class Decision(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("target", ctypes.c_int32)]
+
+
+HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.POINTER(View), ctypes.POINTER(LaunchCtx), ctypes.POINTER(Decision))
+ORDER_KEY = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(LaunchCtx))
+REVIEW = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(View), ctypes.POINTER(ctypes.c_int64))
+DESTROY = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
+
+
+class PolicyVtable(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("on_launch", HOOK), ("on_completion", HOOK), ("on_congestion", HOOK),
+                ("launch_order_key", ORDER_KEY), ("next_review_time", REVIEW), ("destroy", DESTROY)]
+
+
+class Ledger(ctypes.Structure):
+    """OverheadLedger measured on the device (ds_ledger)."""
+    _fields_ = [("ctx_switches", ctypes.c_uint64), ("ctx_switch_total_ns", ctypes.c_uint64),
+                ("preemptions", ctypes.c_uint64), ("preempt_total_ns", ctypes.c_uint64),
+                ("migrations", ctypes.c_uint64), ("migration_total_ns", ctypes.c_uint64),
+                ("demand_faults", ctypes.c_uint64), ("demand_fault_total_ns", ctypes.c_uint64)]
+
+
+class KernelInfo(ctypes.Structure):
+    _fields_ = [("fingerprint", ctypes.c_uint64), ("args_device", ctypes.c_uint64), ("args_size", ctypes.c_uint32),
+                ("grid", ctypes.c_uint32), ("body", ctypes.c_int32), ("phase", ctypes.c_int32)]
+
+
+class JobSpan(ctypes.Structure):
+    _fields_ = [("first_arrival_ns", ctypes.c_int64), ("last_finish_ns", ctypes.c_int64), ("valid", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
 # exported symbols the header declares (checked by the CPU test suite)
 EXPORTS = [
     "ds_status_name", "ds_last_error", "ds_abi_version", "ds_domain_create", "ds_domain_destroy",
@@ -384,6 +459,9 @@ EXPORTS = [
     "ds_compute_migration_set", "ds_full_eager_set", "ds_migrate_regions",
     "ds_fault_inject", "ds_tenant_fault", "ds_engine_fault_local", "ds_engine_job_status",
     "ds_compute_metrics", "ds_set_lane_split", "ds_tenant_abandonable", "ds_set_drain_exit",
+    "ds_engine_create_with_policy", "ds_engine_snapshot", "ds_predictor_predict", "ds_predict_hol_blocking",
+    "ds_builtin_decide", "ds_add_normalization", "ds_seeded_values", "ds_round_to", "ds_ledger_get",
+    "ds_kernel_info_get", "ds_verify_kernels", "ds_engine_ledger", "ds_engine_job_fingerprint",
 ]
 
 _lib = None
@@ -487,6 +565,24 @@ def lib():
         L.ds_set_lane_split.argtypes = [vp, ctypes.c_int]
         L.ds_tenant_abandonable.argtypes = [vp, ctypes.c_int, ctypes.c_int]
         L.ds_set_drain_exit.argtypes = [vp, ctypes.c_int, ctypes.c_uint64]
+        L.ds_engine_create_with_policy.argtypes = [vp, ctypes.POINTER(EngineConfig), ctypes.POINTER(PolicyVtable), vp,
+                                                   ctypes.POINTER(vp)]
+        L.ds_engine_snapshot.argtypes = [vp, ctypes.POINTER(View)]
+        L.ds_predictor_predict.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
+                                           ctypes.POINTER(ctypes.c_int64)]
+        L.ds_predict_hol_blocking.argtypes = [ctypes.POINTER(View), ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+        L.ds_builtin_decide.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(View), ctypes.POINTER(LaunchCtx),
+                                        ctypes.c_int64, ctypes.POINTER(Decision)]
+        L.ds_add_normalization.argtypes = [ctypes.POINTER(JobSpan), ctypes.POINTER(JobSpan), ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                           ctypes.POINTER(ctypes.c_double)]
+        L.ds_seeded_values.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
+        L.ds_round_to.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_uint32)]
+        L.ds_ledger_get.argtypes = [vp, ctypes.POINTER(Ledger)]
+        L.ds_kernel_info_get.argtypes = [vp, ctypes.c_int, ctypes.POINTER(KernelInfo)]
+        L.ds_verify_kernels.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+        L.ds_engine_ledger.argtypes = [vp, ctypes.POINTER(Ledger)]
+        L.ds_engine_job_fingerprint.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
         L.ds_compute_metrics.argtypes = [ctypes.POINTER(RequestOutcome), ctypes.c_int64, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.POINTER(Metrics)]
         L.ds_engine_job_status.argtypes = [vp, ctypes.c_int, ip_]

@@ -21,8 +21,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUTLASS_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/flashinfer/data/cutlass/include"
 
 CU_SOURCES = ["executor.cu"]
-CPP_SOURCES = ["runtime.cpp", "policy.cpp", "engine.cpp", "workload.cpp", "placement.cpp", "migration.cpp",
-               "metrics.cpp"]
+CPP_SOURCES = ["runtime.cpp", "policy.cpp", "policy_abi.cpp", "engine.cpp", "workload.cpp", "placement.cpp", "migration.cpp",
+               "metrics.cpp", "numlab.cpp"]
 
 
 def sources():

@@ -106,7 +106,8 @@ struct alignas(128) DevControl {
     unsigned long long word[DS_MAX_SMS];  // by physical smid: (lender << 32) | owner, -1 = none
     uint32_t gen;                // bumped on every control change (any source)
     uint32_t exit;
-    uint32_t pad[30];
+    unsigned long long t_install;  // %globaltimer when the current control word started installing
+    uint32_t pad[28];
 };
 
 struct HostCompletion {
@@ -170,6 +171,13 @@ struct DevState {
     alignas(128) unsigned long long slog_count;
     alignas(128) unsigned long long clog_count;
     alignas(128) unsigned long long blocks_executed;
+    // overhead ledger (OverheadLedger, engine.hpp:94-107) from device timestamps, per worker lane:
+    //   switch: a lane's gap between its last block of one tenant and its first of another
+    //   yield:  a lane finishing a block of a tenant its SM was revoked from, measured from
+    //           the control install to that block's retire (the boundary wait)
+    //   grant:  a lane's first block of a tenant after a control change, from the install
+    alignas(128) unsigned long long led_switches;
+    unsigned long long led_switch_ns, led_yields, led_yield_ns, led_grants, led_grant_ns;
     alignas(128) uint32_t trig_next;   // next armed trigger index
     uint32_t trig_count;
     ClaimTrigger* triggers;            // device array [kMaxTriggers]

@@ -63,6 +63,7 @@ struct ds_engine {
         bool has_last_finish = false;
         int64_t logical_progress = 0;
         std::vector<uint64_t> transcript;
+        uint64_t fingerprint = 0;      // xor of its records' fingerprints at submit (engine.cpp:183-187)
     };
 
     ds_domain* dom = nullptr;
@@ -106,6 +107,21 @@ struct ds_engine {
     };
     std::vector<Quarantine> quarantines;
     ds_engine() : predictor(0.3, 1000000000) {}
+    ds_ledger ledger0{};  // domain ledger at ds_engine_start
+
+    // Kernel::fingerprint (types.cpp:39-48) of a launch record
+    static uint64_t record_fingerprint(const LaunchRecord& r) {
+        auto mix = [](uint64_t& h, uint64_t v) { h ^= v + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2); };
+        uint64_t h = 0x811c9dc5ULL;
+        mix(h, r.signature.semantic_id.size());
+        for (unsigned char c : r.signature.semantic_id) mix(h, c);
+        mix(h, (uint64_t)r.signature.grid_size);
+        mix(h, (uint64_t)r.base_duration);
+        mix(h, (uint64_t)r.compute_saturation.num);
+        mix(h, (uint64_t)r.compute_saturation.den);
+        for (int32_t k : r.kernels) mix(h, (uint64_t)(uint32_t)k);
+        return h;
+    }
 
     // {"t","seq","kind",...} as the reference's log_event; t in engine ns
     void log(Time t, const char* kind, const std::string& fields) {
@@ -301,7 +317,8 @@ struct ds_engine {
             case K::DispatchDefer: return kDeferPolicy;
             case K::DispatchDirect: {
                 int p = bound_pctx(ji);
-                if (p < 0) return fail();
+                if (p < 0) return fail();                               // direct dispatch while unbound
+                if (pctx_unavail_until[p] > now()) return fail();       // pctx not available
                 if (jobs[ji].running >= 0 && recs[jobs[ji].running].dispatched && p >= 0 && !launchable(ji))
                     return fail();
                 dispatch(ji);
@@ -314,7 +331,13 @@ struct ds_engine {
                 Frac sum{0, 1};
                 for (size_t p = 0; p < pctx_tier.size(); ++p)
                     if (pctx_bound[p] >= 0) sum = sum + pctx_tier[p];
-                if (sum + pctx_tier[d.target] > Frac{1, 1}) return fail();
+                if (sum + pctx_tier[d.target] > Frac{1, 1}) return fail();  // spatial feasibility
+                if (jobs[ji].quarantined) {  // quarantined vctx above minimal tier (engine.cpp:726-728)
+                    Frac mn{2, 1};
+                    for (const auto& f : pctx_tier)
+                        if (f < mn) mn = f;
+                    if (pctx_tier[d.target] != mn) return fail();
+                }
                 if (do_bind(ji, d.target)) return fail();
                 dispatch(ji);
                 return kRemap;
@@ -511,17 +534,21 @@ extern "C" {
 
 const char* ds_engine_last_error(void) { return e_last_error.c_str(); }
 
-int ds_engine_create(ds_domain* dom, const ds_engine_config* cfg, ds_engine** out) {
+static int engine_create(ds_domain* dom, const ds_engine_config* cfg, const ds_policy_vtable* vt, void* user,
+                         ds_engine** out) {
     if (!dom || !cfg || !out) return efail(DS_INVALID_ARGUMENT, "null");
+    if (vt && !vt->on_launch) return efail(DS_CONFIG_ERROR, "a policy needs on_launch");
     auto* e = new ds_engine();
     e->dom = dom;
-    e->pcfg.name = cfg->policy ? cfg->policy : "slo-aware";
+    e->pcfg.name = vt ? (vt->name ? vt->name : "user") : (cfg->policy ? cfg->policy : "slo-aware");
     if (cfg->quantum_ns > 0) e->pcfg.quantum = cfg->quantum_ns;
     if (cfg->alpha > 0) e->pcfg.predictor_alpha = cfg->alpha;
     if (cfg->cold_start_ns > 0) e->pcfg.cold_start_prediction = cfg->cold_start_ns;
     for (int i = 0; i < cfg->n_assignments && i < 64; ++i) e->pcfg.assignments[cfg->assign_vctx[i]] = cfg->assign_pctx[i];
     try {
-        e->policy = make_policy(e->pcfg);
+        // SimEngine(Scenario, std::unique_ptr<Policy>) (engine.hpp:155): a
+        // user policy replaces the named one
+        e->policy = vt ? make_abi_policy(*vt, user) : make_policy(e->pcfg);
         e->predictor = DurationPredictor(e->pcfg.predictor_alpha, e->pcfg.cold_start_prediction);
     } catch (const std::exception& ex) {
         delete e;
@@ -546,11 +573,31 @@ int ds_engine_create(ds_domain* dom, const ds_engine_config* cfg, ds_engine** ou
         e->pctx_unavail_until.push_back(0);
         if (num == den) has_full = true;
     }
-    if (e->pcfg.name == "temporal" && !has_full) {  // engine.cpp:193-202
+    if (!vt && e->pcfg.name == "temporal" && !has_full) {  // engine.cpp:193-202
         delete e;
         return efail(DS_CONFIG_ERROR, "temporal baseline needs a full-tier pctx in the pool");
     }
     *out = e;
+    return DS_OK;
+}
+
+int ds_engine_create(ds_domain* dom, const ds_engine_config* cfg, ds_engine** out) {
+    return engine_create(dom, cfg, nullptr, nullptr, out);
+}
+
+int ds_engine_create_with_policy(ds_domain* dom, const ds_engine_config* cfg, const ds_policy_vtable* vt, void* user,
+                                 ds_engine** out) {
+    if (!vt) return efail(DS_INVALID_ARGUMENT, "null policy vtable");
+    return engine_create(dom, cfg, vt, user, out);
+}
+
+int ds_engine_snapshot(ds_engine* e, ds_view* out) {
+    if (!e || !out) return efail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(e->mu);
+    PolicyView v = e->build_view();
+    view_to_c(v, out);
+    out->predictor = nullptr;  // the snapshot outlives the lock: no live pointers
+    for (int i = 0; i < out->n_pctx; ++i) out->pctx[i].running_semantic_id = nullptr;
     return DS_OK;
 }
 
@@ -602,6 +649,7 @@ int ds_engine_submit(ds_engine* e, int job, const ds_record_desc* d, uint64_t* r
     if (jb.status != 0) return efail(DS_TENANT_FAILED, "job failed (local exception)");
     if (!jb.pending.empty() && e->recs[jb.pending.back()].r.arrival > r.r.arrival)
         return efail(DS_CONFIG_ERROR, "kernel arrival floors must be non-decreasing");
+    jb.fingerprint ^= ds_engine::record_fingerprint(r.r);
     e->recs.push_back(std::move(r));
     jb.pending.push_back(e->recs.back().r.id);
     *rec_id = e->recs.back().r.id;
@@ -613,6 +661,7 @@ int ds_engine_start(ds_engine* e) {
     if (!e) return efail(DS_INVALID_ARGUMENT, "null");
     if (e->running) return efail(DS_ALREADY_RUNNING, "engine running");
     if (e->lend_tenant >= 0) ds_set_lend(e->dom, e->lend_tenant);
+    ds_ledger_get(e->dom, &e->ledger0);
     e->t0 = std::chrono::steady_clock::now();
     e->stop = false;
     e->running = true;
@@ -626,6 +675,40 @@ int ds_engine_stop(ds_engine* e) {
     e->stop = true;
     e->th.join();
     e->running = false;
+    // finalize (engine.cpp:1370-1383): kernel records must be unchanged — the
+    // engine's launch records and the device kernels' argument blocks
+    std::vector<uint64_t> fp(e->jobs.size(), 0);
+    for (const auto& r : e->recs) fp[r.r.job] ^= ds_engine::record_fingerprint(r.r);
+    for (size_t j = 0; j < e->jobs.size(); ++j)
+        if (fp[j] != e->jobs[j].fingerprint)
+            return efail(DS_RECORD_MUTATED, "launch records of job " + std::to_string(j) + " mutated during the run");
+    int bad = -1;
+    if (ds_verify_kernels(e->dom, &bad) == DS_RECORD_MUTATED)
+        return efail(DS_RECORD_MUTATED, std::string("kernel records mutated during the run: ") + ds_last_error());
+    return DS_OK;
+}
+
+int ds_engine_ledger(ds_engine* e, ds_ledger* out) {
+    if (!e || !out) return efail(DS_INVALID_ARGUMENT, "null");
+    ds_ledger now{};
+    int rc = ds_ledger_get(e->dom, &now);
+    if (rc) return efail(rc, ds_last_error());
+    out->ctx_switches = now.ctx_switches - e->ledger0.ctx_switches;
+    out->ctx_switch_total_ns = now.ctx_switch_total_ns - e->ledger0.ctx_switch_total_ns;
+    out->preemptions = now.preemptions - e->ledger0.preemptions;
+    out->preempt_total_ns = now.preempt_total_ns - e->ledger0.preempt_total_ns;
+    out->migrations = now.migrations - e->ledger0.migrations;
+    out->migration_total_ns = now.migration_total_ns - e->ledger0.migration_total_ns;
+    out->demand_faults = 0;
+    out->demand_fault_total_ns = 0;
+    return DS_OK;
+}
+
+int ds_engine_job_fingerprint(ds_engine* e, int job, uint64_t* fp) {
+    if (!e || !fp) return efail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(e->mu);
+    if (job < 0 || job >= (int)e->jobs.size()) return efail(DS_INVALID_ARGUMENT, "unknown job");
+    *fp = e->jobs[job].fingerprint;
     return DS_OK;
 }
 

@@ -157,6 +157,7 @@ __device__ void install_ctl(DevState* st, const int32_t* owner, const int32_t* l
                             uint32_t source, int lane) {
     constexpr int kPer = DS_MAX_SMS / 32;
     const uint64_t t0 = globaltimer();
+    if (lane == 0) asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&st->ctl.t_install), "l"(t0) : "memory");
     int32_t o[kPer], l[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -587,6 +588,16 @@ __device__ void maybe_fire_trigger(DevState* st, const Claimed& w, int lane) {
     if (fire) install_ctl(st, tr->owner, tr->lender, false, 1, lane);
 }
 
+// A lane leaves tenant t (switch or idle): if its SM no longer serves t, the
+// control change revoked it — the block it was running when the change came
+// is the boundary wait (install -> that block's retire).
+__device__ __forceinline__ void ledger_leave(DevState* st, unsigned long long cw, int32_t t, uint64_t t_last_retire) {
+    if (serves_tenant(cw, t)) return;
+    const uint64_t t_ins = ld_volatile_u64(&st->ctl.t_install);
+    atomicAdd(&st->led_yields, 1ull);
+    if (t_last_retire > t_ins) atomicAdd(&st->led_yield_ns, (unsigned long long)(t_last_retire - t_ins));
+}
+
 __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* body_t0, volatile uint32_t* ab_flag,
                                volatile uint32_t* ab_info, uint32_t sm, int lane_id) {
     const int kFull = bar_full(lane_id), kEmpty = bar_empty(lane_id), kDone = bar_done(lane_id);
@@ -595,6 +606,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
     uint32_t last_seq = 0xffffffffu;
     const int home = (int)(sm * kLanes + lane_id) % kRetrySlots;  // this lane's retry-ring slot
     bool idle_logged = false;
+    uint64_t t_last_retire = 0, t_last_switch = 0;  // ledger (lane 0 of the warp)
     uint32_t backoff = 32;
     bool have_prev = false;
     Claimed prev{};
@@ -625,6 +637,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                 } else {
                     push_retry(st, prev.tenant, prev.seq, prev.block, home);
                 }
+                t_last_retire = globaltimer();
                 if (st->blog_cap) {
                     unsigned long long i = atomicAdd(&st->blog_count, 1ull);
                     if (i < st->blog_cap) {
@@ -641,6 +654,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                 }
             } else if (lane == 0) {
                 uint64_t t1 = globaltimer();
+                t_last_retire = t1;
                 uint64_t t0 = *body_t0;
                 // release: the body's writes (ordered before this thread by the
                 // kDone barrier, cumulativity) are published with the retire;
@@ -671,10 +685,11 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
         Claimed w{};
         bool got = false, exit_now = false;
         if (lane == 0) {
+            unsigned long long cw = ~0ull;
             for (;;) {
                 // both words requested before either is used: one L2 round trip
                 const uint32_t ex = ld_volatile_u32(&st->ctl.exit);
-                const unsigned long long cw = ld_volatile_u64(&st->ctl.word[sm]);
+                cw = ld_volatile_u64(&st->ctl.word[sm]);
                 if (ex) { exit_now = true; break; }
                 int32_t ow = (int32_t)(uint32_t)cw;
                 const int32_t ln = (int32_t)(uint32_t)(cw >> 32);
@@ -700,6 +715,7 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                     got = true;
                     break;
                 }
+                if (!idle_logged && last_tenant != -1) ledger_leave(st, cw, last_tenant, t_last_retire);
                 if (!idle_logged && last_tenant != -1 && st->slog_cap) {
                     unsigned long long i = atomicAdd(&st->slog_count, 1ull);
                     if (i < st->slog_cap) {
@@ -713,6 +729,9 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
                         st->slog[i] = r;
                     }
                     idle_logged = true;
+                }
+                if (last_tenant != -1) {
+                    idle_logged = true;
                     last_tenant = -1;
                 }
                 __nanosleep(backoff);
@@ -720,6 +739,20 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
             }
             if (got) {
                 backoff = 32;
+                if (w.tenant != last_tenant) {
+                    const uint64_t now = globaltimer();
+                    if (last_tenant >= 0) {
+                        ledger_leave(st, cw, last_tenant, t_last_retire);
+                        atomicAdd(&st->led_switches, 1ull);
+                        atomicAdd(&st->led_switch_ns, (unsigned long long)(now - t_last_retire));
+                    }
+                    const uint64_t t_ins = ld_volatile_u64(&st->ctl.t_install);
+                    if (t_ins > t_last_switch && now > t_ins) {  // moved here by a control change
+                        atomicAdd(&st->led_grants, 1ull);
+                        atomicAdd(&st->led_grant_ns, (unsigned long long)(now - t_ins));
+                    }
+                    t_last_switch = now;
+                }
                 // no fence here: bodies acquire earlier launches' results in wait_prev
                 // the slot's first 32 B (body, grid, gx, gy, gz, kernel_id, args)
                 // in two vector loads issued together: one L2 round trip

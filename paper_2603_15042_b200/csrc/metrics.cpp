@@ -96,3 +96,31 @@ extern "C" int ds_compute_metrics(const ds_request_outcome* reqs, int64_t n, int
     *out = m;
     return DS_OK;
 }
+
+extern "C" {
+
+// add_normalization (metrics.cpp:81-102): per job, normalized throughput =
+// exclusive span / shared span (first arrival -> last finish of the job's
+// kernels), 0 when either span is missing or the shared span is empty; the
+// aggregate is their sum.  Exact ratios (reduced) plus doubles.
+int ds_add_normalization(const ds_job_span* shared, const ds_job_span* solo, int n, int64_t* num, int64_t* den,
+                         double* aggregate) {
+    if ((n > 0 && (!shared || !solo || !num || !den)) || n < 0) return DS_INVALID_ARGUMENT;
+    double agg = 0.0;
+    for (int i = 0; i < n; ++i) {
+        num[i] = 0;
+        den[i] = 1;
+        if (!shared[i].valid || !solo[i].valid) continue;
+        const int64_t sh = shared[i].last_finish_ns - shared[i].first_arrival_ns;
+        const int64_t so = solo[i].last_finish_ns - solo[i].first_arrival_ns;
+        if (sh <= 0) continue;
+        Ratio r = reduce(Ratio{so, sh});
+        num[i] = r.num;
+        den[i] = r.den;
+        agg += (double)r.num / (double)r.den;
+    }
+    if (aggregate) *aggregate = agg;
+    return DS_OK;
+}
+
+}  // extern "C"

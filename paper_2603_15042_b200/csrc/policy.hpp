@@ -14,6 +14,8 @@
 #include <utility>
 #include <vector>
 
+#include "../../include/detshare/ds.h"
+
 namespace detshare {
 
 using Time = int64_t;  // ns
@@ -201,5 +203,12 @@ class StaticPartitionPolicy : public Policy {
 
 std::unique_ptr<Policy> make_policy(const PolicyConfig& config);  // throws std::invalid_argument
 const std::vector<std::string>& policy_names();
+
+// C-ABI policies (policy_abi.cpp): a ds_policy_vtable as a Policy, and the
+// PolicyView / LaunchContext <-> C snapshot conversions
+std::unique_ptr<Policy> make_abi_policy(const ds_policy_vtable& vt, void* user);
+void view_to_c(const PolicyView& v, ds_view* out);
+void view_from_c(const ds_view& c, PolicyView& out, const DurationPredictor* fallback);
+void launch_from_c(const ds_launch_ctx& c, LaunchRecord& rec_storage, LaunchContext& out);
 
 }  // namespace detshare

@@ -145,6 +145,18 @@ uint64_t fnv_mix(uint64_t h, uint64_t v) {
     return h;
 }
 
+// fingerprint over the immutable launch configuration (Kernel::fingerprint,
+// types.cpp:39-48): semantic id, logical grid, body, argument block
+uint64_t kernel_fingerprint(const KernelRecord& r, const uint8_t* args) {
+    uint64_t h = 0x811c9dc5ULL;
+    h = fnv_mix(h, r.semantic_id.size());
+    for (unsigned char c : r.semantic_id) h = fnv_mix(h, c);
+    h = fnv_mix(h, (uint64_t)r.gx * r.gy * r.gz);
+    h = fnv_mix(h, (uint64_t)r.body);
+    for (size_t i = 0; i < r.args_host.size(); ++i) h = fnv_mix(h, args[i]);
+    return h;
+}
+
 void drain_loop(ds_domain* d) {
     while (!d->drain_stop.load(std::memory_order_acquire)) {
         bool any = false;
@@ -267,6 +279,7 @@ const char* ds_status_name(int status) {
         case DS_INVALID_ARGUMENT: return "InvalidArgument";
         case DS_ALREADY_RUNNING: return "AlreadyRunning";
         case DS_TENANT_FAILED: return "TenantFailed";
+        case DS_RECORD_MUTATED: return "RecordMutated";
     }
     return "UnknownError";  // errors.cpp:19
 }
@@ -495,14 +508,7 @@ int ds_kernel_register(ds_domain* d, const ds_kernel_desc* k, int* kernel_id) {
     r.phase = k->phase;
     r.request = k->request;
     r.decode_index = k->decode_index;
-    // fingerprint over the immutable launch configuration (Kernel::fingerprint, types.cpp:39-48)
-    uint64_t h = 0x811c9dc5ULL;
-    h = fnv_mix(h, r.semantic_id.size());
-    for (unsigned char c : r.semantic_id) h = fnv_mix(h, c);
-    h = fnv_mix(h, grid);
-    h = fnv_mix(h, (uint64_t)r.body);
-    for (uint8_t b : r.args_host) h = fnv_mix(h, b);
-    r.fingerprint = h;
+    r.fingerprint = kernel_fingerprint(r, r.args_host.data());
     if (k->args_size) {
         cudaSetDevice(d->device);
         DS_CUDA(cudaMemcpyAsync((void*)r.args_dev, k->args, k->args_size, cudaMemcpyHostToDevice, d->copy_stream));
@@ -1048,6 +1054,59 @@ int ds_stats_get(ds_domain* d, ds_stats* out) {
     out->switches = v[2];
     out->block_log_entries = std::min<uint64_t>(v[3], d->blog_cap);
     out->block_log_dropped = v[3] > d->blog_cap ? v[3] - d->blog_cap : 0;
+    return DS_OK;
+}
+
+int ds_ledger_get(ds_domain* d, ds_ledger* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    std::memset(out, 0, sizeof(*out));
+    cudaSetDevice(d->device);
+    unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
+    DS_CUDA(cudaMemcpyAsync(v, &d->d_state->led_switches, sizeof(v), cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    out->ctx_switches = v[0];
+    out->ctx_switch_total_ns = v[1];
+    out->preemptions = v[2];
+    out->preempt_total_ns = v[3];
+    out->migrations = v[4];
+    out->migration_total_ns = v[5];
+    return DS_OK;
+}
+
+int ds_kernel_info_get(ds_domain* d, int kernel_id, ds_kernel_info* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    std::lock_guard<std::mutex> g(d->mu);
+    if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
+    const KernelRecord& k = d->kernels[kernel_id];
+    out->fingerprint = k.fingerprint;
+    out->args_device = k.args_dev;
+    out->args_size = (uint32_t)k.args_host.size();
+    out->grid = k.gx * k.gy * k.gz;
+    out->body = k.body;
+    out->phase = k.phase;
+    return DS_OK;
+}
+
+// Kernel records are immutable (engine.cpp:183-187, 1379-1383): recompute each
+// fingerprint from the argument block the executor actually reads (device copy).
+int ds_verify_kernels(ds_domain* d, int* first_bad) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (first_bad) *first_bad = -1;
+    if (d->args_used == 0) return DS_OK;
+    std::vector<uint8_t> arena(d->args_used);
+    cudaSetDevice(d->device);
+    DS_CUDA(cudaMemcpyAsync(arena.data(), d->d_args, d->args_used, cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    for (size_t i = 0; i < d->kernels.size(); ++i) {
+        const KernelRecord& k = d->kernels[i];
+        const uint8_t* dev = arena.data() + (k.args_dev - (uint64_t)d->d_args);
+        if (kernel_fingerprint(k, dev) != k.fingerprint) {
+            if (first_bad) *first_bad = (int)i;
+            return fail(DS_RECORD_MUTATED, "kernel record " + std::to_string(i) + " (" + k.semantic_id +
+                                               ") mutated during the run");
+        }
+    }
     return DS_OK;
 }
 

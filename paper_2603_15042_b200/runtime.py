@@ -169,6 +169,25 @@ class Domain:
         a k-block when revoked and re-run from scratch (before start())."""
         check(lib().ds_tenant_abandonable(self.h, tenant, int(enable)))
 
+    def ledger(self) -> dict:
+        """OverheadLedger measured on the device since ds_start (ns)."""
+        l = _abi.Ledger()
+        check(lib().ds_ledger_get(self.h, ctypes.byref(l)))
+        return ledger_dict(l)
+
+    def kernel_info(self, kernel: int) -> _abi.KernelInfo:
+        out = _abi.KernelInfo()
+        check(lib().ds_kernel_info_get(self.h, kernel, ctypes.byref(out)))
+        return out
+
+    def verify_kernels(self) -> int:
+        """-1 if every kernel record is intact, else the first mutated kernel id."""
+        bad = ctypes.c_int(-1)
+        rc = lib().ds_verify_kernels(self.h, ctypes.byref(bad))
+        if rc not in (0, _abi.RECORD_MUTATED):
+            check(rc)
+        return bad.value
+
     def set_drain_exit(self, enable: bool = True, deadline_ms: int = 0):
         """Before start(): the executor exits by itself once every launch
         enqueued so far (launches may be issued before start) completed, or
@@ -283,13 +302,165 @@ def _stop_live_engines():
             pass
 
 
+class UserPolicy:
+    """A Python policy handed to the engine through the C-ABI vtable
+    (ds_engine_create_with_policy; the reference's Policy virtuals,
+    policy.hpp:97-126).  Hooks get a ``PolicyView``-shaped snapshot and a
+    launch context and return ``(kind, target)`` with kind one of
+    _abi.DISPATCH_DIRECT / DISPATCH_REMAP / DISPATCH_DEFER / PREEMPT /
+    NO_ACTION.  The engine validates every decision (apply_decision,
+    engine.cpp:688-754): an illegal one becomes Defer + policy_errors."""
+
+    name = "user"
+
+    def on_launch(self, view, launch):
+        return (_abi.DISPATCH_DEFER, -1)
+
+    def on_completion(self, view, launch):
+        return (_abi.NO_ACTION, -1)
+
+    def on_congestion(self, view, launch):
+        return (_abi.DISPATCH_DEFER, -1)
+
+    def launch_order_key(self, launch) -> int:
+        return 0
+
+    def next_review_time(self, view):
+        return None
+
+
+class _NS:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    def __repr__(self):
+        return f"{type(self).__name__}({self.__dict__})"
+
+
+def view_from_c(v: _abi.View) -> _NS:
+    """ds_view -> a PolicyView-shaped object (tiers as Fractions, times in ns)."""
+    pctxs = []
+    for i in range(v.n_pctx):
+        p = v.pctx[i]
+        pctxs.append(_NS(id=p.id, device=p.device, tier=Fraction(p.tier_num, p.tier_den), standby=bool(p.standby),
+                         available=bool(p.available), bound=None if p.bound < 0 else p.bound,
+                         running_kernel=p.running_kernel if p.has_running else None,
+                         running_semantic_id=(p.running_semantic_id or b"").decode(), running_grid=p.running_grid,
+                         running_remaining=p.running_remaining_ns, running_phase=p.running_phase,
+                         running_priority=p.running_priority))
+    vctxs = [_NS(id=x.id, priority=x.priority, quarantined=bool(x.quarantined), bound=bool(x.bound), pending=x.pending,
+                 head_phase=x.head_phase, decoding=bool(x.decoding)) for x in (v.vctx[i] for i in range(v.n_vctx))]
+    return _NS(now=v.now_ns, pctxs=pctxs, vctxs=vctxs,
+               bound_tier_sums={d: Fraction(v.bound_tier_sum_num[d], v.bound_tier_sum_den[d])
+                                for d in range(v.n_devices)},
+               min_tiers={d: Fraction(v.min_tier_num[d], v.min_tier_den[d]) for d in range(v.n_devices)},
+               active_vctx_count=v.active_vctx_count, predictor=v.predictor)
+
+
+def launch_from_c(c: _abi.LaunchCtx) -> _NS:
+    return _NS(vctx=c.vctx, has_kernel=bool(c.has_kernel), kernel_id=c.kernel_id,
+               semantic_id=(c.semantic_id or b"").decode(), grid_size=c.grid_size, base_hint_ns=c.base_hint_ns,
+               saturation=Fraction(c.sat_num, c.sat_den) if c.sat_den else Fraction(1), phase=c.phase,
+               decode_index=c.decode_index, request=c.request, arrival_ns=c.arrival_ns,
+               request_arrival_ns=c.request_arrival_ns,
+               slo=(c.ttft_ns, c.tpot_ns) if c.has_slo else None, pool_exhausted=bool(c.pool_exhausted))
+
+
+def predict(predictor, semantic_id: str, grid: int, hint_ns: Optional[int] = None) -> int:
+    """DurationPredictor::predict of a view's predictor (valid inside a hook)."""
+    out = ctypes.c_int64()
+    check(lib().ds_predictor_predict(predictor, semantic_id.encode(), grid, 0 if hint_ns is None else 1,
+                                     hint_ns or 0, ctypes.byref(out)))
+    return out.value
+
+
+def _vtable_for(policy: UserPolicy):
+    """ctypes vtable whose hooks call the Python policy (kept alive by the engine object)."""
+    def wrap(fn):
+        def hook(user, view, launch, out):
+            try:
+                k, t = fn(view_from_c(view.contents), launch_from_c(launch.contents))
+                out[0] = _abi.Decision(int(k), int(t))
+            except Exception:  # no exceptions across the ABI: an illegal decision
+                out[0] = _abi.Decision(-1, -1)
+        return _abi.HOOK(hook)
+
+    def order(user, launch):
+        try:
+            return int(policy.launch_order_key(launch_from_c(launch.contents)))
+        except Exception:
+            return 0
+
+    def review(user, view, t):
+        try:
+            r = policy.next_review_time(view_from_c(view.contents))
+        except Exception:
+            r = None
+        if r is None:
+            return 0
+        t[0] = int(r)
+        return 1
+
+    vt = _abi.PolicyVtable()
+    keep = [wrap(policy.on_launch), wrap(policy.on_completion), wrap(policy.on_congestion),
+            _abi.ORDER_KEY(order), _abi.REVIEW(review), _abi.DESTROY(0)]
+    name = str(getattr(policy, "name", "user")).encode()
+    vt.name = name
+    vt.on_launch, vt.on_completion, vt.on_congestion, vt.launch_order_key, vt.next_review_time, vt.destroy = keep
+    return vt, keep + [name]
+
+
+def builtin_decide(policy: str, hook: int, view: _abi.View, launch: _abi.LaunchCtx, quantum_ns: int = 0):
+    """A built-in policy's hook over a C view (ds_builtin_decide): (kind, target)."""
+    d = _abi.Decision()
+    check(lib().ds_builtin_decide(policy.encode(), hook, ctypes.byref(view), ctypes.byref(launch), quantum_ns,
+                                  ctypes.byref(d)))
+    return d.kind, d.target
+
+
+def seeded_values(seed: int, n: int, fmt: int) -> List[int]:
+    """seeded_values (equivalence.cpp:7-17): raw bit patterns (fmt 0 fp16, 1 bf16, 2 fp32)."""
+    out = (ctypes.c_uint32 * max(1, n))()
+    check(lib().ds_seeded_values(seed, n, fmt, out))
+    return list(out[:n])
+
+
+def round_to(fmt: int, x: float) -> int:
+    out = ctypes.c_uint32()
+    check(lib().ds_round_to(fmt, x, ctypes.byref(out)))
+    return out.value
+
+
+def add_normalization(shared, solo):
+    """add_normalization (metrics.cpp:81-102) over [(first_arrival_ns, last_finish_ns) or None] per job:
+    ([Fraction per job], aggregate float)."""
+    n = len(shared)
+    a = (_abi.JobSpan * max(1, n))()
+    b = (_abi.JobSpan * max(1, n))()
+    for i in range(n):
+        for arr, x in ((a, shared[i]), (b, solo[i])):
+            if x is not None:
+                arr[i] = _abi.JobSpan(int(x[0]), int(x[1]), 1, 0)
+    num = (ctypes.c_int64 * max(1, n))()
+    den = (ctypes.c_int64 * max(1, n))()
+    agg = ctypes.c_double()
+    check(lib().ds_add_normalization(a, b, n, num, den, ctypes.byref(agg)))
+    return [Fraction(num[i], den[i]) for i in range(n)], agg.value
+
+
+def ledger_dict(l: _abi.Ledger) -> dict:
+    return {n: getattr(l, n) for n, _ in _abi.Ledger._fields_}
+
+
 class Engine:
     """SimEngine-like dispatch loop over one domain (C++ engine thread).
 
     Jobs map 1:1 to tenants; ``submit`` is the reference's kernel arrival of a
-    launch record that runs as the listed registered kernels."""
+    launch record that runs as the listed registered kernels.  ``policy`` is a
+    built-in name or a UserPolicy object (SimEngine(Scenario,
+    std::unique_ptr<Policy>), engine.hpp:155)."""
 
-    def __init__(self, dom: Domain, policy: str = "tpot-first", quantum_ns: int = 5_000_000, alpha: float = 0.3,
+    def __init__(self, dom: Domain, policy="tpot-first", quantum_ns: int = 5_000_000, alpha: float = 0.3,
                  cold_start_ns: int = 1_000_000_000, release_on_idle: bool = True, fair_handover: bool = True,
                  lend_tenant: int = -1, assignments=None, hang_detection: bool = False, hang_threshold: float = 3.0,
                  capture_log: bool = False, reset_delay_ns: int = 0):
@@ -298,7 +469,8 @@ class Engine:
         cfg.hang_detection = int(hang_detection)
         cfg.hang_threshold = hang_threshold
         cfg.capture_log = int(capture_log)
-        cfg.policy = policy.encode()
+        user = None if isinstance(policy, str) else policy
+        cfg.policy = policy.encode() if user is None else b""
         cfg.quantum_ns = quantum_ns
         cfg.alpha = alpha
         cfg.cold_start_ns = cold_start_ns
@@ -311,10 +483,16 @@ class Engine:
             cfg.assign_vctx[i] = v
             cfg.assign_pctx[i] = p
         h = ctypes.c_void_p()
-        check_engine(lib().ds_engine_create(dom.h, ctypes.byref(cfg), ctypes.byref(h)))
+        self._keep = []
+        if user is None:
+            check_engine(lib().ds_engine_create(dom.h, ctypes.byref(cfg), ctypes.byref(h)))
+        else:
+            vt, keep = _vtable_for(user)
+            self._keep += keep + [vt, user]
+            check_engine(lib().ds_engine_create_with_policy(dom.h, ctypes.byref(cfg), ctypes.byref(vt), None,
+                                                            ctypes.byref(h)))
         self.h = h
         self.dom = dom
-        self._keep = []
         _LIVE_ENGINES.add(self)
 
     def add_job(self, tenant: int, priority: int) -> int:
@@ -358,6 +536,23 @@ class Engine:
         out = _abi.RecordInfo()
         check_engine(lib().ds_engine_record(self.h, rec, ctypes.byref(out)))
         return out
+
+    def snapshot(self):
+        """ds_snapshot: the PolicyView a hook would see now."""
+        v = _abi.View()
+        check_engine(lib().ds_engine_snapshot(self.h, ctypes.byref(v)))
+        return view_from_c(v)
+
+    def ledger(self) -> dict:
+        """OverheadLedger of this engine's run (device-measured, ns)."""
+        l = _abi.Ledger()
+        check_engine(lib().ds_engine_ledger(self.h, ctypes.byref(l)))
+        return ledger_dict(l)
+
+    def job_fingerprint(self, job: int) -> int:
+        out = ctypes.c_uint64()
+        check_engine(lib().ds_engine_job_fingerprint(self.h, job, ctypes.byref(out)))
+        return out.value
 
     def counters(self) -> dict:
         c = _abi.EngineCounters()

@@ -1,6 +1,4 @@
 set -x
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-tail -5 gpurun_out/pytest_gpu.log
-timeout 1500 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
-timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
-tail -c 3000 gpurun_out/bench.json; tail -5 gpurun_out/bench.err; cat gpurun_out/bench_ref.json
+timeout 600 python -m pytest tests/test_gpu_boundary.py -q -s > gpurun_out/pytest_boundary.log 2>&1; echo boundary=$?
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -30 gpurun_out/pytest_boundary.log; tail -5 gpurun_out/pytest_gpu.log

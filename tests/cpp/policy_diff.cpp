@@ -16,6 +16,8 @@
 
 using namespace detshare;
 
+static long g_c_checked = 0, g_c_mismatch = 0;  // C-ABI path vs the C++ path
+
 static KernelSignature sig(int i) { return KernelSignature{PC_SIG_NAMES[(i / 2) % 4], (i & 1) ? 128 : 256}; }
 
 static void native_eval(const pc_case* c, pc_result* out) {
@@ -91,6 +93,48 @@ static void native_eval(const pc_case* c, pc_result* out) {
     out->has_review = r.has_value();
     out->review = r ? *r : 0;
     for (int i = 0; i < c->n_p; ++i) out->hol[i] = predict_hol_blocking(v, v.pctxs[i], pred);
+    // the same hooks through the C ABI (view_to_c -> ds_builtin_decide ->
+    // view_from_c): what a C / façade caller of the built-ins gets.  The C
+    // view has no queued entries (the engine never fills them, SURVEY
+    // appendix #3), so cases with queued entries are skipped.
+    bool queued = false;
+    for (const auto& e : v.pctxs) queued |= !e.queued.empty();
+    if (!queued) {
+        ds_view cv;
+        view_to_c(v, &cv);
+        ds_launch_ctx cl;
+        std::memset(&cl, 0, sizeof cl);
+        cl.vctx = l.vctx;
+        cl.request_arrival_ns = l.request_arrival;
+        cl.has_slo = l.slo.has_value();
+        if (l.slo) {
+            cl.ttft_ns = l.slo->ttft_deadline;
+            cl.tpot_ns = l.slo->tpot_deadline;
+        }
+        cl.has_kernel = l.kernel != nullptr;
+        cl.semantic_id = k.signature.semantic_id.c_str();
+        cl.grid_size = k.signature.grid_size;
+        cl.base_hint_ns = k.base_duration;
+        cl.sat_num = k.compute_saturation.num;
+        cl.sat_den = k.compute_saturation.den;
+        cl.phase = (int)k.phase;
+        cl.request = -1;
+        cl.decode_index = -1;
+        if (c->n_assign == 0 || c->policy != 3) {  // the C entry point has no assignment map
+            ds_decision d[4];
+            ds_builtin_decide(cfg.name.c_str(), 0, &cv, &cl, cfg.quantum, &d[0]);
+            ds_builtin_decide(cfg.name.c_str(), 1, &cv, &cl, cfg.quantum, &d[1]);
+            ds_builtin_decide(cfg.name.c_str(), 3, &cv, &cl, cfg.quantum, &d[3]);
+            cl.pool_exhausted = 1;
+            ds_builtin_decide(cfg.name.c_str(), 2, &cv, &cl, cfg.quantum, &d[2]);
+            g_c_checked++;
+            if (d[0].kind != out->launch_kind || d[0].target != out->launch_target ||
+                d[1].kind != out->completion_kind || d[1].target != out->completion_target ||
+                d[2].kind != out->congestion_kind || d[2].target != out->congestion_target ||
+                d[3].target != out->order_key)
+                g_c_mismatch++;
+        }
+    }
 }
 
 static void gen(std::mt19937_64& g, pc_case* c) {
@@ -242,5 +286,6 @@ int main(int argc, char** argv) {
         std::printf("policy %d on_launch kinds: direct %ld remap %ld defer %ld preempt %ld none %ld\n", p, kinds[p][0],
                     kinds[p][1], kinds[p][2], kinds[p][3], kinds[p][4]);
     std::printf("cases %ld mismatches %ld ref_errors %ld\n", n, mism, errors);
-    return mism == 0 && errors == 0 ? 0 : 1;
+    std::printf("c_abi checked %ld mismatches %ld\n", g_c_checked, g_c_mismatch);
+    return mism == 0 && errors == 0 && g_c_mismatch == 0 ? 0 : 1;
 }
