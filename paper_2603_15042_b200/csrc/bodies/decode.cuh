@@ -40,7 +40,8 @@ struct GemvArgs {
     uint64_t dbg;       // optional phase timestamps [grid][8] (0 = off)
     uint64_t w_packed;  // W pre-packed as SWIZZLE_128B [N/BM][K/64][BM][64] tiles (0 = use tmW)
     int32_t bm;         // slab rows: 128 (0) or 64 (not for kGemvSiluMul)
-    int32_t pad2;
+    int32_t l2_pf_kb;   // early start: KB of this block's weights past the ring prefetched into L2 before
+                        // the dependency resolves (0 = ring only)
 };
 
 constexpr int kGemvBN = 32;
@@ -75,7 +76,8 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     BodyCtx cd = c;
     cd.dbg = dbg;
     tc_mainloop<kGemvBN, STAGES, kTcBK, BM>(base, &a.tmW, &a.tmX, n_blk * BM, 0, kb0, kb1, c.tmem_base, true,
-                                             reinterpret_cast<const char*>(a.w_packed), KB, &cd);
+                                             reinterpret_cast<const char*>(a.w_packed), KB, &cd, nullptr, false,
+                                             (uint32_t)a.l2_pf_kb << 10);
     wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
     const int warp = ltid() >> 5, lane = ltid() & 31;

@@ -73,7 +73,7 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
                                             int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
                                             const char* a_packed = nullptr, int a_kblocks = 0,
                                             const BodyCtx* dep = nullptr, const BodyCtx* yc = nullptr,
-                                            bool acc_init = false) {
+                                            bool acc_init = false, uint32_t l2_pf_bytes = 0) {
     using L = TcSmem<BN, STAGES, BK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -113,6 +113,15 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
         for (int i = 0; i < pre; ++i) {
             tc::mbar_arrive_expect_tx(&full[i % STAGES], L::kStageBytes);
             issue_a(i);
+        }
+        // ... and, past the ring, up to l2_pf_bytes more of the (contiguous,
+        // pre-packed) weight range are prefetched into L2, so HBM keeps
+        // streaming while the previous launch's tail runs
+        if (dep && a_packed && l2_pf_bytes && nkb > pre) {
+            const char* g0 = a_packed + ((size_t)(a_row / BM) * a_kblocks + kb_begin + pre) * L::kABytes;
+            const uint32_t tot = min((uint32_t)(nkb - pre) * L::kABytes, l2_pf_bytes);
+            for (uint32_t off = 0; off < tot; off += L::kABytes)
+                tc::bulk_prefetch_l2(g0 + off, min(L::kABytes, tot - off));
         }
         if (dep) wait_prev(*dep);
         if (dep && dep->dbg) dep->dbg[7] = globaltimer();

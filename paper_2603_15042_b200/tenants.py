@@ -13,6 +13,7 @@ named model's.  Device memory comes from torch (plumbing only).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import List
 
@@ -71,7 +72,7 @@ class DecodeConfig:
 
 class DecodeModel:
     def __init__(self, cfg: DecodeConfig = DecodeConfig(), device="cuda", seed: int = 0, split_override: str = "",
-                 bm_override: str = ""):
+                 bm_override: str = "", pf_override: str = ""):
         assert cfg.batch == 32 and cfg.d == cfg.n_q * 128 and cfg.n_q == 4 * cfg.n_kv
         self.cfg = cfg
         c = cfg
@@ -129,6 +130,12 @@ class DecodeModel:
                 k, v = kv.split(":")
                 self.BM[k] = int(v)
         assert self.BM["gu"] == 128
+        # early start: KB of each block's weights past its smem ring that are
+        # prefetched into L2 while the previous launch finishes
+        self.PF = {"qkv": 0, "o": 0, "gu": 0, "down": 0, "lm": 0}
+        for kv in filter(None, (pf_override or os.environ.get("DS_L2PF", "")).split(",")):
+            k, v = kv.split(":")
+            self.PF[k] = int(v)
         ws_elems = max(self.S["qkv"] * self.qkv_n, self.S["o"] * c.d, self.S["gu"] * 2 * c.ffn,
                        self.S["down"] * c.d, self.S["lm"] * c.vocab) * 32
         self.ws = torch.zeros(ws_elems, device=device)
@@ -140,7 +147,8 @@ class DecodeModel:
         self._build_args()
 
     # ---- launch records ----
-    def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None, bm=128):
+    def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None, bm=128,
+              pf=0):
         Wp = pack_sw128(W, bm)
         self._packed.append(Wp)
         tmW = _abi.tensor_map_bf16(W.data_ptr(), N, K, bm)
@@ -162,6 +170,7 @@ class DecodeModel:
         a.q_dim, a.kv_dim = self.cfg.d, self.kv_dim
         a.w_packed = Wp.data_ptr()
         a.bm = bm
+        a.l2_pf_kb = pf
         return a, ((N // bm) * S, 1, 1)
 
     def _build_args(self):
@@ -176,7 +185,7 @@ class DecodeModel:
             hin, hout = self.H[l % 2], self.H[(l + 1) % 2]
             st_in, p_in = (self.st0, 1) if l == 0 else (self.st_h, c.d // self.BM["down"])
             a, g = self._gemv(self.Wqkv[l], hin, self.qkv_n, c.d, self.S["qkv"], _abi.GEMV_QKV, self.q,
-                              stats_in=st_in, P_in=p_in, l=l, bm=self.BM["qkv"])
+                              stats_in=st_in, P_in=p_in, l=l, bm=self.BM["qkv"], pf=self.PF["qkv"])
             self.records.append((f"decode/qkv", _abi.BODY_GEMV_BF16, g, a, self.qkv_n * c.d * 2))
             rows = 32 * c.n_kv * self.Lmax
             at = _abi.AttnArgs(_abi.tensor_map_kv(self.kc[l].data_ptr(), rows, ATTN_CHUNK),
@@ -186,17 +195,17 @@ class DecodeModel:
             self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,
                                  2 * 32 * c.n_kv * c.L * 128 * 2))
             a, g = self._gemv(self.Wo[l], self.attn, c.d, c.d, self.S["o"], _abi.GEMV_RESID, self.h_mid, resid=hin,
-                              stats_out=self.st_mid, bm=self.BM["o"])
+                              stats_out=self.st_mid, bm=self.BM["o"], pf=self.PF["o"])
             self.records.append(("decode/o", _abi.BODY_GEMV_BF16, g, a, c.d * c.d * 2))
             a, g = self._gemv(self.Wgu[l], self.h_mid, 2 * c.ffn, c.d, self.S["gu"], _abi.GEMV_SILU_MUL, self.act,
-                              stats_in=self.st_mid, P_in=c.d // self.BM["o"])
+                              stats_in=self.st_mid, P_in=c.d // self.BM["o"], pf=self.PF["gu"])
             self.records.append(("decode/gate_up", _abi.BODY_GEMV_BF16, g, a, 2 * c.ffn * c.d * 2))
             a, g = self._gemv(self.Wd[l], self.act, c.d, c.ffn, self.S["down"], _abi.GEMV_RESID, hout,
-                              resid=self.h_mid, stats_out=self.st_h, bm=self.BM["down"])
+                              resid=self.h_mid, stats_out=self.st_h, bm=self.BM["down"], pf=self.PF["down"])
             self.records.append(("decode/down", _abi.BODY_GEMV_BF16, g, a, c.d * c.ffn * 2))
         hfin = self.H[c.layers % 2]
         a, g = self._gemv(self.lm, hfin, c.vocab, c.d, self.S["lm"], _abi.GEMV_STORE, self.logits,
-                          stats_in=self.st_h, P_in=c.d // self.BM["down"], bm=self.BM["lm"])
+                          stats_in=self.st_h, P_in=c.d // self.BM["down"], bm=self.BM["lm"], pf=self.PF["lm"])
         self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
         chunks = max(1, min(4, c.vocab // 2048))  # 128 blocks: one wave; every block pays a claim + ticket
         am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), self.amax_ws.data_ptr(),
