@@ -253,7 +253,9 @@ ATTN_CHUNK = 64  # KV positions per attention TMA box / pipeline stage (csrc/bod
 class AttnArgs(ctypes.Structure):
     _fields_ = [("tmK", TmaDesc), ("tmV", TmaDesc), ("q", ctypes.c_uint64), ("out", ctypes.c_uint64),
                 ("ws", ctypes.c_uint64), ("counters", ctypes.c_uint64), ("L", ctypes.c_int32),
-                ("Lmax", ctypes.c_int32), ("S", ctypes.c_int32), ("scale", ctypes.c_float), ("dbg", ctypes.c_uint64)]
+                ("Lmax", ctypes.c_int32), ("S", ctypes.c_int32), ("scale", ctypes.c_float), ("dbg", ctypes.c_uint64),
+                ("kbase", ctypes.c_uint64), ("vbase", ctypes.c_uint64), ("l2_pf_kb", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
 
 
 class EmbedArgs(ctypes.Structure):

@@ -187,6 +187,37 @@ __device__ __forceinline__ void wait_prev(const BodyCtx& c) {
     }
 }
 
+// One thread of a block whose HBM streaming is done (its last operand load
+// landed): counts it towards its launch's streamed word.  The completer of
+// launch s-1 resets the word to (s << 32) before it publishes head = s, and a
+// block of launch s streams only after it observed that head, so one
+// fire-and-forget add per block suffices (no CAS round trips under contention).
+__device__ __forceinline__ void mark_streamed(const BodyCtx& c) {
+    if (!c.st) return;  // solo
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(&c.st->tenants[c.tenant].streamed) : "memory");
+}
+
+// Single thread, before wait_prev: waits until launch seq-1 has either
+// completed (false) or streamed all its blocks (true: HBM is about to idle
+// through its epilogues, so the caller's prefetch does not compete with it).
+// False at once in solo mode, for the first launch, or when the previous
+// launch's body does not mark.
+__device__ __forceinline__ bool wait_prev_streamed(const BodyCtx& c) {
+    if (!c.prev_head || !c.st || c.seq == 0) return false;
+    const uint32_t p = c.seq - 1;
+    const LaunchSlot* ps = &c.st->rings[(size_t)c.tenant * (c.st->ring_mask + 1) + (p & c.st->ring_mask)];
+    const int pb = ld_volatile_u32(reinterpret_cast<const uint32_t*>(&ps->body));
+    if (pb != DS_BODY_GEMV_BF16 && pb != DS_BODY_ATTN_DECODE) return false;
+    const unsigned long long want = ((unsigned long long)p << 32) | ld_volatile_u32(&ps->grid);
+    const unsigned long long* w = &c.st->tenants[c.tenant].streamed;
+    for (;;) {
+        if (ld_acquire_u32(c.prev_head) >= c.seq) return false;
+        if (ld_volatile_u64(w) == want) return true;
+        if (tenant_failed(c)) return false;
+        __nanosleep(32);
+    }
+}
+
 // All 256 body threads: one thread polls, the lane barrier carries its
 // acquire to the others (so ~300 lanes x 256 threads never hammer one word).
 __device__ __forceinline__ void wait_prev_all(const BodyCtx& c) {

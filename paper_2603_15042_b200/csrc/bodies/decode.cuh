@@ -78,6 +78,7 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     tc_mainloop<kGemvBN, STAGES, kTcBK, BM>(base, &a.tmW, &a.tmX, n_blk * BM, 0, kb0, kb1, c.tmem_base, true,
                                              reinterpret_cast<const char*>(a.w_packed), KB, &cd, nullptr, false,
                                              (uint32_t)a.l2_pf_kb << 10);
+    if (ltid() == 128) mark_streamed(c);  // tmem_full: every weight / X load of this block has landed
     wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
     const int warp = ltid() >> 5, lane = ltid() & 31;
@@ -336,6 +337,11 @@ struct AttnArgs {
     int32_t L, Lmax, S;
     float scale;        // 1/sqrt(128)
     uint64_t dbg;       // optional [grid][8] timestamps
+    uint64_t kbase;     // K / V cache base (the tensor maps' global address), for L2 prefetch
+    uint64_t vbase;
+    int32_t l2_pf_kb;   // early start: KB of K and of V past the ring prefetched into L2 once the previous
+                        // launch has streamed (0 = ring only)
+    int32_t pad;
 };
 
 constexpr int kAttnChunk = 64;   // KV positions per staged chunk (QK warp w: positions w*kQkPos ..)
@@ -344,8 +350,14 @@ constexpr int kQkNt = kQkPos / 8;       // mma n-tiles per QK warp per chunk
 // Separate K and V rings: K is consumed by the QK warps (which run ahead),
 // V by the PV warps; V gets the deeper ring so its refills (issued when the
 // PV side releases a slot) have the most chunks of lookahead.
-constexpr int kAttnKSlots = 2;
-constexpr int kAttnVSlots = 4;
+#ifndef DS_ATTN_KSLOTS
+#define DS_ATTN_KSLOTS 2
+#endif
+#ifndef DS_ATTN_VSLOTS
+#define DS_ATTN_VSLOTS 4
+#endif
+constexpr int kAttnKSlots = DS_ATTN_KSLOTS;
+constexpr int kAttnVSlots = DS_ATTN_VSLOTS;
 constexpr uint32_t kAttnTile = kAttnChunk * 256;                      // 64 rows x 128 dims bf16 = 16 KB
 constexpr uint32_t kAttnVOff = kAttnKSlots * kAttnTile;               // V ring after the K ring
 constexpr uint32_t kAttnBarOff = (kAttnKSlots + kAttnVSlots) * kAttnTile;  // 96 KB
@@ -449,6 +461,17 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         int pk = 0, pv = 0;
         while (pk < min(kAttnKSlots, nch) && immutable(pk)) issue_k(pk++);
         while (pv < min(kAttnVSlots, nch) && immutable(pv)) issue_v(pv++);
+        if (a.l2_pf_kb && nch > pk && wait_prev_streamed(c)) {
+            // the rest of this block's K and V rows (contiguous, 256 B per
+            // position) into L2 while the previous launch's epilogues run
+            const char* kb = reinterpret_cast<const char*>(a.kbase) + ((size_t)row0 + pk * kAttnChunk) * 256;
+            const char* vb = reinterpret_cast<const char*>(a.vbase) + ((size_t)row0 + pv * kAttnChunk) * 256;
+            const uint32_t cap = (uint32_t)a.l2_pf_kb << 10;
+            const uint32_t kby = min(cap, (uint32_t)(p1 - p0 - pk * kAttnChunk) * 256u);
+            const uint32_t vby = min(cap, (uint32_t)max(0, p1 - p0 - pv * kAttnChunk) * 256u);
+            for (uint32_t off = 0; off < kby; off += kAttnTile) tc::bulk_prefetch_l2(kb + off, min(kAttnTile, kby - off));
+            for (uint32_t off = 0; off < vby; off += kAttnTile) tc::bulk_prefetch_l2(vb + off, min(kAttnTile, vby - off));
+        }
         wait_prev(c);
         for (int i = pk; i < min(kAttnKSlots, nch); ++i) issue_k(i);
         for (int i = pv; i < min(kAttnVSlots, nch); ++i) issue_v(i);
@@ -589,6 +612,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             }
         }
     }
+    if (ltid() == 128) mark_streamed(c);  // PV warp 0: every K / V chunk of this block consumed
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
     // PV lanes with g < 4 own O[head g][32 pw + 8 nt + 2 tq, +1], nt = 0..3
     const int pw = warp - 4;

@@ -114,10 +114,10 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             tc::mbar_arrive_expect_tx(&full[i % STAGES], L::kStageBytes);
             issue_a(i);
         }
-        // ... and, past the ring, up to l2_pf_bytes more of the (contiguous,
-        // pre-packed) weight range are prefetched into L2, so HBM keeps
-        // streaming while the previous launch's tail runs
-        if (dep && a_packed && l2_pf_bytes && nkb > pre) {
+        // ... and, once the previous launch has streamed all its operands
+        // (its epilogues are running, HBM is idle), up to l2_pf_bytes more of
+        // the (contiguous, pre-packed) weight range are prefetched into L2
+        if (dep && a_packed && l2_pf_bytes && nkb > pre && wait_prev_streamed(*dep)) {
             const char* g0 = a_packed + ((size_t)(a_row / BM) * a_kblocks + kb_begin + pre) * L::kABytes;
             const uint32_t tot = min((uint32_t)(nkb - pre) * L::kABytes, l2_pf_bytes);
             for (uint32_t off = 0; off < tot; off += L::kABytes)

@@ -81,7 +81,12 @@ struct alignas(128) DevTenant {
     uint32_t fault;            // local-exception code, 0 = healthy (set once, never cleared)
     uint32_t retry_count;      // abandoned blocks waiting in the tenant's retry ring
     uint32_t save_base;        // first spill slot of this tenant in DevState::save (abandonable tenants)
-    uint32_t pad[23];
+    uint32_t pad0;
+    // (seq << 32) | blocks of launch seq whose HBM streaming is done
+    // (mark_streamed): the next launch's early-started blocks prefetch into L2
+    // once the whole launch has streamed, i.e. while its epilogues run
+    unsigned long long streamed;
+    uint32_t pad[20];
 };
 static_assert(sizeof(DevTenant) == 128, "tenant word owns a 128-byte line");
 

@@ -551,7 +551,9 @@ __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* s
     // ordered after every block's writes by the acq_rel retire atomic
     const uint64_t tend = globaltimer();
     // 1. publish completion first (critical path: early-started blocks of the
-    //    next launch are waiting on head)
+    //    next launch are waiting on head); the streamed word moves to the next
+    //    launch before, so its blocks' marks (made after they see head) count
+    *reinterpret_cast<volatile unsigned long long*>(&T->streamed) = (unsigned long long)(seq + 1) << 32;
     st_release_u32(&T->head, seq + 1);
     // abandonable tenants open their next launch only now (see try_claim)
     if ((st->retry_mask >> t) & 1ull) open_next(T, seq);

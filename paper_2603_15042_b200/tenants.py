@@ -130,9 +130,12 @@ class DecodeModel:
                 k, v = kv.split(":")
                 self.BM[k] = int(v)
         assert self.BM["gu"] == 128
-        # early start: KB of each block's weights past its smem ring that are
-        # prefetched into L2 while the previous launch finishes
-        self.PF = {"qkv": 0, "o": 0, "gu": 0, "down": 0, "lm": 0}
+        # early start: KB of each block's operands past its smem ring that are
+        # prefetched into L2 once the previous launch has streamed (its
+        # epilogues run).  Measured (scripts/pf_sweep.py,
+        # profiles/r2_l2_prefetch_sweep2.jsonl): 128 KB 4.72 vs 4.76 ms per step,
+        # deeper prefetches lose (L2 thrash)
+        self.PF = {"qkv": 128, "attn": 128, "o": 128, "gu": 128, "down": 128, "lm": 128}
         for kv in filter(None, (pf_override or os.environ.get("DS_L2PF", "")).split(",")):
             k, v = kv.split(":")
             self.PF[k] = int(v)
@@ -192,6 +195,7 @@ class DecodeModel:
                                _abi.tensor_map_kv(self.vc[l].data_ptr(), rows, ATTN_CHUNK), self.q.data_ptr(),
                                self.attn.data_ptr(), self.attn_ws.data_ptr(), self.attn_counters.data_ptr(), c.L,
                                self.Lmax, c.attn_splits, 1.0 / math.sqrt(128))
+            at.kbase, at.vbase, at.l2_pf_kb = self.kc[l].data_ptr(), self.vc[l].data_ptr(), self.PF["attn"]
             self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,
                                  2 * 32 * c.n_kv * c.L * 128 * 2))
             a, g = self._gemv(self.Wo[l], self.attn, c.d, c.d, self.S["o"], _abi.GEMV_RESID, self.h_mid, resid=hin,

@@ -11,7 +11,7 @@ from paper_2603_15042_b200.tenants import DecodeModel, DecodeConfig
 m = DecodeModel(DecodeConfig())
 tok0 = m.tokens.clone()
 torch.cuda.synchronize()
-KEYS = {"decode/qkv": "qkv", "decode/o": "o", "decode/gate_up": "gu", "decode/down": "down", "decode/lm_head": "lm"}
+KEYS = {"decode/attn": "attn", "decode/qkv": "qkv", "decode/o": "o", "decode/gate_up": "gu", "decode/down": "down", "decode/lm_head": "lm"}
 configs = [x for x in os.environ.get("PF_CONFIGS", "none;all:128;all:256;all:512;all:1024").split(";")]
 ref = None
 for cfg in configs:
