@@ -196,6 +196,28 @@ int ds_launch(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, uint64_t*
 /* negative-control mutant (engine.hpp:68-71): executed grid = max(1, floor(grid * tier)) */
 int ds_launch_atomized(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, int64_t tier_num,
                        int64_t tier_den, uint64_t* seq);
+/* A launch whose logical blocks [0, first_block) already ran elsewhere (on the
+ * device a tenant migrated from, into memory copied here with its working
+ * set): the executor hands out blocks first_block .. grid-1 only, in the same
+ * order, so the launch completes exactly as one uninterrupted run would
+ * (begin_migration / on_migration_done, engine.cpp:620-672,986-1009:
+ * "kernel resumes, never restarts").  first_block < grid. */
+int ds_launch_from(ds_domain* dom, int tenant, int kernel_id, uint64_t tag, uint32_t first_block, uint64_t* seq);
+/* Where a tenant stands on the device (read from HBM while the executor runs). */
+typedef struct ds_progress {
+    uint64_t head;          /* launches completed */
+    uint64_t tail;          /* launches the device has seen */
+    uint64_t enqueued;      /* launches enqueued by the host */
+    uint64_t claim_seq;     /* launch the claim word is on */
+    uint32_t claim_open;    /* 1: claim_seq is open for claims */
+    uint32_t claim_block;   /* next logical block it hands out (open only) */
+    uint32_t claim_grid;
+    uint32_t claim_retired; /* blocks of claim_seq retired (those before its first block included) */
+    uint32_t drained;       /* no block of the tenant is running: head == claim_seq and every
+                               claimed block of it retired */
+    uint32_t failed;
+} ds_progress;
+int ds_tenant_progress(ds_domain* dom, int tenant, ds_progress* out);
 int ds_wait_tenant(ds_domain* dom, int tenant, uint64_t seq, int timeout_ms); /* until seq completed;
                                                                                DS_TENANT_FAILED once the tenant failed */
 /* Local exception (FaultSpec::LocalException, apply_local_exception engine.cpp:1049-1083):
@@ -631,6 +653,75 @@ int ds_compute_migration_set(const ds_region* ws, int n_ws, const int32_t* touch
 int ds_full_eager_set(const ds_region* ws, int n_ws, int32_t* eager, int* n_eager, uint64_t* eager_bytes);
 int ds_migrate_regions(int src_device, int dst_device, const void* const* src_ptrs, void* const* dst_ptrs,
                        const uint64_t* bytes, int n, void* stream);
+
+/* ---- fleet: cross-device moves over per-GPU domains (§8f rows 3-4) ----
+ * Global exceptions with emergency migration to a standby device
+ * (apply_global_exception / emergency_migrate, engine.cpp:1095-1166), and
+ * working-set tracking with eager / lazy copies and demand faults for
+ * planned cross-device migrations (begin_migration, advance_lazy,
+ * service_demand_faults, engine.cpp:563-672).  A job is one tenant per device
+ * it has lived on; its regions are device buffers copied peer to peer on the
+ * copy engines; its kernels are re-registered on the destination with their
+ * pointer arguments relocated. */
+typedef struct ds_fleet ds_fleet;
+typedef struct ds_reloc {     /* an 8-byte device pointer inside a kernel's args */
+    uint32_t args_offset;
+    int32_t region;           /* working-set region it points into */
+    uint64_t region_offset;   /* pointer = region base on the running device + region_offset */
+} ds_reloc;
+typedef struct ds_place_pctx { /* a pctx of a device, as emergency_migrate sees the pools */
+    int32_t device, pctx;
+    int64_t tier_num, tier_den;
+    int32_t bound, pad;
+} ds_place_pctx;
+typedef struct ds_fleet_job_info {
+    int32_t device, tenant, pctx;
+    int32_t status;           /* VctxStatus: 0 Active, 1 Failed, 2 Stranded (types.hpp:77) */
+    uint64_t launches;
+    int32_t migrations;
+    int32_t lazy_pending;     /* background region copies still in flight */
+} ds_fleet_job_info;
+typedef struct ds_migration_info { /* MigrationRecord (migration.hpp:34-45) */
+    int32_t job, src_device, src_pctx, dst_device, dst_pctx;
+    int32_t emergency, demand_faults, pad;
+    uint64_t eager_bytes, lazy_bytes;
+    int64_t start_ns, end_ns;  /* host steady clock: start -> the job resumed on dst */
+    uint64_t resumed_launch;   /* job launch index it resumed at */
+    uint32_t resumed_block, pad2;  /* ... and that launch's first block on dst */
+} ds_migration_info;
+typedef struct ds_fleet_ledger { /* OverheadLedger migration / fault fields (engine.hpp:94-107), measured */
+    uint64_t migrations, emergency_migrations, stranded;
+    int64_t migration_total_ns;
+    uint64_t demand_faults;
+    int64_t demand_fault_total_ns;
+    uint64_t eager_bytes, lazy_bytes;
+} ds_fleet_ledger;
+const char* ds_fleet_last_error(void);
+/* emergency_migrate's target rule (engine.cpp:1128-1154) over POD pools: sets
+ * *target to an index into pctxs, or -1 (the vctx is stranded) */
+int ds_emergency_target(const int32_t* dev_failed, const int32_t* dev_standby, int n_devices,
+                        const ds_place_pctx* pctxs, int n_pctxs, int64_t cur_tier_num, int64_t cur_tier_den,
+                        int* target);
+int ds_fleet_create(ds_fleet** out);
+int ds_fleet_destroy(ds_fleet* f);   /* frees the region copies it allocated (stop the domains first) */
+int ds_fleet_add_device(ds_fleet* f, ds_domain* dom, int cuda_device, int standby, int* dev);
+int ds_fleet_add_job(ds_fleet* f, int dev, const ds_tenant_desc* desc, int* job);
+int ds_fleet_add_region(ds_fleet* f, int job, void* ptr, uint64_t bytes, int* region);
+int ds_fleet_add_kernel(ds_fleet* f, int job, const ds_kernel_desc* desc, const ds_reloc* relocs, int n_relocs,
+                        const int32_t* touched, int n_touched, int* kernel);
+int ds_fleet_kernel_id(ds_fleet* f, int job, int kernel, int dev, int* domain_kernel_id); /* -1: not there */
+int ds_fleet_bind(ds_fleet* f, int job, int pctx);
+int ds_fleet_launch(ds_fleet* f, int job, int kernel, uint64_t* launch); /* program order; demand faults first */
+int ds_fleet_wait(ds_fleet* f, int job, uint64_t launch, int timeout_ms);
+int ds_fleet_migrate(ds_fleet* f, int job, int dst_dev, int dst_pctx, int timeout_ms);
+int ds_fleet_global_exception(ds_fleet* f, int dev, int timeout_ms);
+int ds_fleet_job_get(ds_fleet* f, int job, ds_fleet_job_info* out);
+int ds_fleet_region(ds_fleet* f, int job, int region, int dev /* -1: the job's */, void** ptr, int* resident,
+                    int* dirty);
+/* copy the region's up-to-date contents (wherever they live) into host memory */
+int ds_fleet_read_region(ds_fleet* f, int job, int region, void* host, uint64_t bytes);
+int ds_fleet_migrations(ds_fleet* f, ds_migration_info* out, int cap, int* n);
+int ds_fleet_ledger_get(ds_fleet* f, ds_fleet_ledger* out);
 
 #ifdef __cplusplus
 }

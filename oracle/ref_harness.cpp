@@ -93,6 +93,33 @@ FloatFormatKind kind_of(int fmt) {
 
 }  // namespace
 
+// migrations (migration.hpp:34-45), vctx status, ledger and the event log:
+// the emergency-migration / working-set parity tests read them
+static void add_migrations(nlohmann::ordered_json& j, const SimulationReport& rep) {
+    nlohmann::ordered_json mig = nlohmann::ordered_json::array();
+    for (const auto& m : rep.migrations) {
+        mig.push_back({{"vctx", m.vctx.value},
+                       {"src", m.src.valid() ? m.src.value : -1},
+                       {"dst", m.dst.value},
+                       {"eager_bytes", m.eager_bytes},
+                       {"lazy_bytes", m.lazy_bytes},
+                       {"start", to_decimal_string(m.start)},
+                       {"end", to_decimal_string(m.end)},
+                       {"demand_faults", m.demand_faults},
+                       {"emergency", m.emergency},
+                       {"aborted", m.aborted}});
+    }
+    j["migrations"] = mig;
+    nlohmann::ordered_json vs;
+    for (const auto& [vid, stt] : rep.vctx_status) vs[std::to_string(vid.value)] = static_cast<int>(stt);
+    j["vctx_status"] = vs;
+    j["ledger"] = {{"migrations", rep.ledger.migrations},
+                   {"demand_faults", rep.ledger.demand_faults},
+                   {"migration_total", to_decimal_string(rep.ledger.migration_total)},
+                   {"demand_fault_total", to_decimal_string(rep.ledger.demand_fault_total)}};
+    j["event_log"] = rep.event_log;
+}
+
 extern "C" {
 
 // reduction_result (equivalence.cpp:19-25) as "num/den" | "inf" | "-inf" | "nan"
@@ -184,6 +211,7 @@ int ref_simulate_json(const char* scenario_json, char* out, long cap) {
         }
         j["preemptions"] = pre;
         j["policy_errors"] = rep.policy_errors;
+        add_migrations(j, rep);
         return put(j.dump(), out, cap);
     } catch (const std::exception& e) {
         put(std::string("error: ") + e.what(), out, cap);

@@ -464,6 +464,10 @@ EXPORTS = [
     "ds_engine_create_with_policy", "ds_engine_snapshot", "ds_predictor_predict", "ds_predict_hol_blocking",
     "ds_builtin_decide", "ds_add_normalization", "ds_seeded_values", "ds_round_to", "ds_ledger_get",
     "ds_kernel_info_get", "ds_verify_kernels", "ds_engine_ledger", "ds_engine_job_fingerprint",
+    "ds_launch_from", "ds_tenant_progress", "ds_emergency_target", "ds_fleet_create", "ds_fleet_destroy",
+    "ds_fleet_add_device", "ds_fleet_add_job", "ds_fleet_add_region", "ds_fleet_add_kernel", "ds_fleet_kernel_id",
+    "ds_fleet_bind", "ds_fleet_launch", "ds_fleet_wait", "ds_fleet_migrate", "ds_fleet_global_exception",
+    "ds_fleet_job_get", "ds_fleet_region", "ds_fleet_read_region", "ds_fleet_migrations", "ds_fleet_ledger_get", "ds_fleet_last_error",
 ]
 
 _lib = None

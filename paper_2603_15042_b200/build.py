@@ -22,7 +22,7 @@ CUTLASS_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/flashinfer/data/
 
 CU_SOURCES = ["executor.cu"]
 CPP_SOURCES = ["runtime.cpp", "policy.cpp", "policy_abi.cpp", "engine.cpp", "workload.cpp", "placement.cpp", "migration.cpp",
-               "metrics.cpp", "numlab.cpp"]
+               "metrics.cpp", "numlab.cpp", "fleet.cpp"]
 
 
 def sources():

@@ -121,15 +121,27 @@ struct Stage {
 // two sides are ordered by fence.sc, Dekker-style, so one of them opens it).
 // A failed tenant never reopens: the fault word is checked before, and after
 // a fence.sc past, the CAS (fault_tenant sets the word, fences, then kills).
-__device__ void try_open(DevTenant* T) {
+__device__ __forceinline__ LaunchSlot* slot_of(DevState* st, int t, uint32_t s) {
+    return &st->rings[(size_t)t * (st->ring_mask + 1) + (s & st->ring_mask)];
+}
+
+// First logical block of launch s: 0, or the resume point of a launch whose
+// lower blocks ran on another device before a migration (ds_launch_from; the
+// slot's flags word, written before the tail that publishes the slot).
+__device__ __forceinline__ uint32_t first_block(DevState* st, int t, uint32_t s) {
+    return ld_volatile_u32(&slot_of(st, t, s)->flags);
+}
+
+__device__ void try_open(DevState* st, int t) {
+    DevTenant* T = &st->tenants[t];
     for (;;) {
         if (ld_volatile_u32(&T->fault)) return;
         unsigned long long w = ld_volatile_u64(&T->claim);
         uint32_t s = (uint32_t)(w >> 32), b = (uint32_t)w;
         if (b < kSat) return;
-        uint32_t tail = ld_volatile_u32(&T->tail);
+        uint32_t tail = ld_acquire_u32(&T->tail);
         if (s >= tail) return;
-        if (atomicCAS(&T->claim, w, (unsigned long long)s << 32) == w) {
+        if (atomicCAS(&T->claim, w, ((unsigned long long)s << 32) | first_block(st, t, s)) == w) {
             __threadfence();
             if (ld_volatile_u32(&T->fault)) kill_claim(T);
             return;
@@ -276,7 +288,7 @@ __device__ void loader_loop(DevState* st) {
                     __threadfence();
                     st_release_u32(&st->tenants[tt].tail, to);
                     __threadfence();
-                    try_open(&st->tenants[tt]);
+                    try_open(st, tt);
                 }
                 __syncwarp();
                 if (lane == src) known_tail[t] = to;
@@ -356,22 +368,19 @@ struct ClaimCache {
 // completion before touching dependent data — wait_prev).  If s+1 is not
 // enqueued yet, park the word closed; the loader opens it on publish
 // (fence.sc on both sides, Dekker-style, so one of them does).
-__device__ void open_next(DevTenant* T, uint32_t s) {
+__device__ void open_next(DevState* st, int t, uint32_t s) {
+    DevTenant* T = &st->tenants[t];
     const uint32_t nxt = s + 1;
     const uint32_t tail = ld_acquire_u32(&T->tail);
     if (nxt < tail) {
-        atomicExch(&T->claim, (unsigned long long)nxt << 32);
+        atomicExch(&T->claim, ((unsigned long long)nxt << 32) | first_block(st, t, nxt));
         __threadfence();
         if (ld_volatile_u32(&T->fault)) kill_claim(T);
     } else {
         atomicExch(&T->claim, ((unsigned long long)nxt << 32) | kSat);
         __threadfence();
-        try_open(T);
+        try_open(st, t);
     }
-}
-
-__device__ __forceinline__ LaunchSlot* slot_of(DevState* st, int t, uint32_t s) {
-    return &st->rings[(size_t)t * (st->ring_mask + 1) + (s & st->ring_mask)];
 }
 
 __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
@@ -430,7 +439,7 @@ __device__ bool try_claim(DevState* st, int t, Claimed& out, ClaimCache& cc) {
     // whose blocks can be abandoned: its next launch opens at completion
     // (complete_launch), so no lane ever parks on launch s+1 while blocks of s
     // wait in the retry ring for a lane to run them
-    if (b2 == grid - 1 && !((st->retry_mask >> t) & 1ull)) open_next(T, s2);
+    if (b2 == grid - 1 && !((st->retry_mask >> t) & 1ull)) open_next(st, t, s2);
     out.tenant = t;
     out.seq = s2;
     out.block = b2;
@@ -556,7 +565,7 @@ __device__ void complete_launch(DevState* st, int t, uint32_t seq, LaunchSlot* s
     *reinterpret_cast<volatile unsigned long long*>(&T->streamed) = (unsigned long long)(seq + 1) << 32;
     st_release_u32(&T->head, seq + 1);
     // abandonable tenants open their next launch only now (see try_claim)
-    if ((st->retry_mask >> t) & 1ull) open_next(T, seq);
+    if ((st->retry_mask >> t) & 1ull) open_next(st, t, seq);
     // 2. device -> host completion record (PCIe, off the critical path)
     unsigned long long i = atomicAdd(&st->completion_count, 1ull);
     HostCompletion* hc = &st->completions[i & st->completion_mask];

@@ -668,7 +668,8 @@ int ds_stop(ds_domain* d) {
 }
 
 static int launch_impl(ds_domain* d, int tenant, int kernel_id, uint64_t tag, uint32_t exec_grid, uint32_t egx,
-                       uint32_t egy, uint32_t egz, uint64_t* seq_out) {
+                       uint32_t egy, uint32_t egz, uint64_t* seq_out, uint32_t start = 0) {
+    if (start >= exec_grid) return fail(DS_INVALID_ARGUMENT, "resume block beyond the grid");
     if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
     if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
     TenantRecord* t = d->tenants[tenant];
@@ -693,11 +694,11 @@ static int launch_impl(ds_domain* d, int tenant, int kernel_id, uint64_t tag, ui
     s.kernel_id = kernel_id;
     s.args = k.args_dev;
     s.tag = tag;
-    s.retired = 0;
+    s.retired = start;  // blocks below `start` ran before a migration: they count as retired
     s.sms = 0;
     s.t_first = 0;
     s.seq = (uint32_t)seq;
-    s.flags = 0;
+    s.flags = start;    // first logical block the executor hands out
     t->launched_kernel.push_back(kernel_id);
     t->launched_grid.push_back(exec_grid);
     t->next_seq = seq + 1;
@@ -715,6 +716,44 @@ int ds_launch(ds_domain* d, int tenant, int kernel_id, uint64_t tag, uint64_t* s
     if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
     const KernelRecord& k = d->kernels[kernel_id];
     return launch_impl(d, tenant, kernel_id, tag, k.gx * k.gy * k.gz, k.gx, k.gy, k.gz, seq);
+}
+
+int ds_launch_from(ds_domain* d, int tenant, int kernel_id, uint64_t tag, uint32_t first_block, uint64_t* seq) {
+    if (check_dom(d)) return DS_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (kernel_id < 0 || kernel_id >= (int)d->kernels.size()) return fail(DS_INVALID_ARGUMENT, "unknown kernel");
+    const KernelRecord& k = d->kernels[kernel_id];
+    return launch_impl(d, tenant, kernel_id, tag, k.gx * k.gy * k.gz, k.gx, k.gy, k.gz, seq, first_block);
+}
+
+int ds_tenant_progress(ds_domain* d, int tenant, ds_progress* out) {
+    if (check_dom(d) || !out) return fail(DS_INVALID_ARGUMENT, "null");
+    if (tenant < 0 || tenant >= (int)d->tenants.size()) return fail(DS_INVALID_ARGUMENT, "unknown tenant");
+    cudaSetDevice(d->device);
+    ds::DevTenant T;
+    DS_CUDA(cudaMemcpyAsync(&T, &d->d_state->tenants[tenant], sizeof T, cudaMemcpyDeviceToHost, d->copy_stream));
+    DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+    std::memset(out, 0, sizeof *out);
+    out->head = T.head;
+    out->tail = T.tail;
+    out->enqueued = d->tenants[tenant]->next_seq;
+    out->claim_seq = (uint32_t)(T.claim >> 32);
+    const uint32_t b = (uint32_t)T.claim;
+    out->claim_open = b < ds::kSat;
+    out->failed = (b & ds::kDead) != 0 || T.fault != 0;
+    if (out->claim_open && out->claim_seq < T.tail) {
+        ds::LaunchSlot sl;
+        const size_t idx = (size_t)tenant * d->ring_cap + (out->claim_seq & (d->ring_cap - 1));
+        DS_CUDA(cudaMemcpyAsync(&sl, d->d_rings + idx, sizeof sl, cudaMemcpyDeviceToHost, d->copy_stream));
+        DS_CUDA(cudaStreamSynchronize(d->copy_stream));
+        out->claim_block = std::min(b, sl.grid);
+        out->claim_grid = sl.grid;
+        out->claim_retired = sl.retired;
+    }
+    // quiescent: every launch before the claimed one completed and every
+    // claimed block of it retired (no block of the tenant is running)
+    out->drained = T.head == out->claim_seq && (!out->claim_open || out->claim_retired == out->claim_block);
+    return DS_OK;
 }
 
 // atomized_grid (engine.cpp:26-30): the grid is rewritten to fit the tier.
