@@ -524,6 +524,7 @@ class Colocation:
         return {"tpot_ms": [r["tpot_ms"] for r in timed], "e2e_tpot_ms": [r["e2e_tpot_ms"] for r in timed],
                 "ledger": ledger, "normalized_throughput": norm,
                 "outcomes": [r["outcome"] for r in timed],
+                "kernels_completed": len(timed) * self.T * len(self.dec_kernels) + len(tw),
                 "train_launches": len(train_recs),
                 "gap_us": statistics.mean(r["gap_us"] for r in timed),
                 "step_ms": statistics.mean(r["step_ms"] for r in timed),
@@ -966,6 +967,19 @@ def decode_roofline(co, solo, solo_us, solo_step_us, peaks, peaks_src):
             "per_kernel": table}
 
 
+def paired_report(a, b):
+    from paper_2603_15042_b200 import metrics as M
+    from paper_2603_15042_b200 import report as R
+
+    def one(run):
+        m = M.compute_metrics(run["outcomes"], makespan_ns=int(run["window_ms"] * 1e6),
+                              kernels_completed=run.get("kernels_completed", 0))
+        n = run.get("normalized_throughput")
+        return R.metrics_to_json(m, run["ledger"], {0: Fraction(str(n["decode"])), 1: Fraction(str(n["train"]))} if n else None)
+
+    return R.compare(one(a), one(b), "config2", "tpot-first", "config2", "temporal")
+
+
 def gpu_arm(args, rank, world):
     import torch
     dev = int(os.environ.get("LOCAL_RANK", rank))
@@ -1051,6 +1065,9 @@ def gpu_arm(args, rank, world):
         "gpu_launches": len(m.records) * (n_req + n_warm) * args.tokens + sp.get("train_launches", 0),
         "config4": config4,
         "config4b": config4b,
+        # corosim compare (tools/corosim.cpp:99-123) of the two timed runs, in
+        # the reference's metrics_to_json schema (times in device ns)
+        "compare": paired_report(sp, tm),
     }
     tail = {
         "host_gap_us": round(sp["gap_us"], 1),

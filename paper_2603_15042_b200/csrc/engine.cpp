@@ -133,6 +133,19 @@ struct ds_engine {
         event_log.push_back(std::move(line));
     }
     static std::string kv(const char* k, long long v) { return std::string("\"") + k + "\":" + std::to_string(v); }
+    static std::string jstr(const std::string& v) {
+        std::string o = "\"";
+        for (char c : v) {
+            if (c == '"' || c == '\\') o += '\\';
+            o += c;
+        }
+        return o + "\"";
+    }
+    // KernelStart fields as the reference logs them (engine.cpp:519-525)
+    std::string start_fields(int ji, const Rec& r, bool resumed) const {
+        return kv("vctx", ji) + "," + kv("pctx", r.pctx) + ",\"kernel\":" + jstr(r.r.signature.semantic_id) + "," +
+               kv("grid", r.r.signature.grid_size) + ",\"resumed\":" + (resumed ? "true" : "false");
+    }
 
     Time now() const {
         return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
@@ -278,8 +291,7 @@ struct ds_engine {
         if (j.running >= 0) {  // paused record resumes in place on its new binding
             Rec& pr = recs[j.running];
             pr.pctx = bound_pctx(ji);
-            log(now(), "KernelStart", kv("vctx", ji) + "," + kv("pctx", pr.pctx) + "," +
-                                          kv("kernel_id", (long long)pr.r.id) + ",\"resume\":true");
+            log(now(), "KernelStart", start_fields(ji, pr, true));
             return;
         }
         uint64_t id = j.pending.front();
@@ -300,9 +312,7 @@ struct ds_engine {
             r.hang_needed = (Time)(hang_threshold * (double)predictor.predict(r.r.signature, r.r.base_duration));
             r.hang_armed = true;
         }
-        log(r.dispatch_host, "KernelStart",
-            kv("vctx", ji) + "," + kv("pctx", r.pctx) + "," + kv("kernel_id", (long long)id) + "," +
-                kv("grid", r.r.signature.grid_size));
+        log(r.dispatch_host, "KernelStart", start_fields(ji, r, false));
     }
 
     enum Outcome { kDirect, kRemap, kDeferPolicy, kDeferError };
@@ -451,9 +461,11 @@ struct ds_engine {
         j.has_last_finish = true;
         if (r.t_end > r.t_first_claim) predictor.observe(r.r.signature, (Time)(r.t_end - r.t_first_claim));
         ctr.completed++;
+        // engine.cpp:871-877: exec = the run's executed time (device ns here)
         log(r.finish_host, "KernelFinish",
-            kv("vctx", ji) + "," + kv("pctx", r.pctx) + "," + kv("kernel_id", (long long)r.r.id) + "," +
-                kv("device_ns", (long long)(r.t_end - r.t_first_claim)));
+            kv("vctx", ji) + "," + kv("pctx", r.pctx) + ",\"kernel\":" + jstr(r.r.signature.semantic_id) + "," +
+                kv("grid", r.r.signature.grid_size) + ",\"exec\":\"" +
+                std::to_string((long long)(r.t_end - r.t_first_claim)) + "\"");
         {
             PolicyView v = build_view();
             PolicyDecision d = policy->on_completion(v, launch_context(ji));

@@ -66,9 +66,14 @@ def main():
     import test_transcript_parity as tp  # noqa: E402
     sc, _ = tp.scenario()
     out = json.loads(loader.ref_simulate(json.dumps(sc)))
+    # the event log of the same run (capture_log): per-vctx first-start /
+    # finish streams and the field names of every kind (log schema)
+    out_log = json.loads(loader.ref_simulate(json.dumps(dict(sc, capture_log=True))))
+    streams, schema = tp.log_projection(out_log["event_log"])
     with open(os.path.join(HERE, "transcript_golden.json"), "w") as f:
         json.dump({"source": out_src(out), "scenario": sc, "transcripts": out["transcripts"],
-                   "logical_progress": out["logical_progress"], "kernels_completed": out["kernels_completed"]}, f)
+                   "logical_progress": out["logical_progress"], "kernels_completed": out["kernels_completed"],
+                   "log_streams": streams, "log_schema": schema}, f)
     print("wrote transcript golden:", out["kernels_completed"], "kernels")
 
 

@@ -38,6 +38,21 @@ def scenario():
     return {"devices": [{"tiers": ["0.25", "0.5", "1"]}], "policy": "tpot-first", "workload": {"records": recs}}, reqs
 
 
+def log_projection(lines):
+    """Event log (reference schema, engine.cpp:316-329) -> per-vctx streams of
+    first starts and finishes [kind, kernel, grid] (timing-independent: the
+    transcript order), and the field names each logged kind carries."""
+    streams, schema = {}, {}
+    for line in lines:
+        e = json.loads(line) if isinstance(line, str) else line
+        k = e["kind"]
+        if k in ("KernelStart", "KernelFinish") and "kernel" in e:
+            schema.setdefault(k, sorted(e.keys()))
+            if k == "KernelFinish" or not e.get("resumed"):
+                streams.setdefault(str(e["vctx"]), []).append([k, e["kernel"], e["grid"]])
+    return streams, schema
+
+
 def expected_plan():
     """(job, semantic_id, grid) per kernel in expansion order: job 0 = train, 1 = chat."""
     _, reqs = scenario()
@@ -74,7 +89,7 @@ def test_gpu_engine_transcripts_match_reference():
             if (sid, grid) not in kid:
                 kid[(sid, grid)] = dom.kernel(sid, _abi.BODY_SPIN, (grid, 1, 1), _abi.SpinArgs(out.data_ptr(), 2000))
         dom.start()
-        eng = Engine(dom, policy="tpot-first", lend_tenant=tenants[0])
+        eng = Engine(dom, policy="tpot-first", lend_tenant=tenants[0], capture_log=True)
         jobs = [eng.add_job(tenants[0], _abi.BEST_EFFORT), eng.add_job(tenants[1], _abi.LATENCY_CRITICAL)]
         eng.start()
         try:
@@ -89,9 +104,15 @@ def test_gpu_engine_transcripts_match_reference():
                 eng.wait(r, 60000)
             got = {str(j): [sig[r] for r in eng.transcript(jobs[j])] for j in (0, 1)}
             completed = eng.counters()["completed"]
+            log = eng.event_log()
         finally:
             eng.stop()
             eng.close()
     assert got == g["transcripts"]
     assert {j: len(v) for j, v in got.items()} == g["logical_progress"]
     assert completed == g["kernels_completed"]
+    # event log: the reference's schema for every start / finish line, and the
+    # same per-vctx first-start / finish streams as the reference's own log
+    streams, schema = log_projection(log)
+    assert schema == g["log_schema"]
+    assert streams == g["log_streams"]
