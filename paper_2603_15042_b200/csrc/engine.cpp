@@ -508,6 +508,7 @@ struct ds_engine {
 
     void loop() {
         std::vector<ds_completion> buf(4096);
+        auto last_active = std::chrono::steady_clock::now();
         while (!stop.load()) {
             bool work = false;
             {
@@ -537,7 +538,17 @@ struct ds_engine {
                 for (size_t ji = 0; ji < jobs.size(); ++ji) arrivals |= launchable((int)ji);
                 if (work || review || arrivals) pump();
             }
-            if (!work) std::this_thread::sleep_for(std::chrono::microseconds(5));
+            // busy-poll (pause) while work is recent: a sleep costs the timer
+            // slack (~50 us) on every decode step's completion -> next launch
+            if (work) {
+                last_active = std::chrono::steady_clock::now();
+            } else if (std::chrono::steady_clock::now() - last_active < std::chrono::milliseconds(20)) {
+#if defined(__x86_64__) || defined(__i386__)
+                for (int i = 0; i < 32; ++i) __builtin_ia32_pause();
+#endif
+            } else {
+                std::this_thread::sleep_for(std::chrono::microseconds(5));
+            }
         }
     }
 };

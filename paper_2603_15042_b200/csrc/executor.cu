@@ -272,17 +272,34 @@ __device__ void loader_loop(DevState* st) {
                 const int tt = base + src;
                 const uint32_t from = __shfl_sync(0xffffffffu, kt, src);
                 const uint32_t to = __shfl_sync(0xffffffffu, ht, src);
-                // copy slots [from, to): 16 u32 per slot, 2 slots per warp step
-                for (uint32_t s = from; s < to; s += 2) {
-                    const uint32_t my = s + (lane >> 4);
-                    if (my < to) {
-                        const uint32_t idx = (uint32_t)tt * (st->ring_mask + 1) + (my & st->ring_mask);
-                        const uint32_t* hs = reinterpret_cast<const uint32_t*>(&st->host_rings[idx]);
-                        uint32_t* ds = reinterpret_cast<uint32_t*>(&st->rings[idx]);
-                        ds[lane & 15] = ld_volatile_u32(hs + (lane & 15));
-                        __threadfence();
+                // copy slots [from, to): lane l moves 16-B quarter (l & 3) of
+                // slots s + (l >> 2) + 8k, k < 4 — 32 slots per batch with all
+                // of a batch's PCIe reads in flight before any store (a decode
+                // step enqueues ~160 slots at once)
+                for (uint32_t s = from; s < to; s += 32) {
+                    uint4 v[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t my = s + (lane >> 2) + 8 * k;
+                        if (my < to) {
+                            const uint32_t idx = (uint32_t)tt * (st->ring_mask + 1) + (my & st->ring_mask);
+                            const uint4* hs = reinterpret_cast<const uint4*>(&st->host_rings[idx]) + (lane & 3);
+                            asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
+                                         : "l"(hs)
+                                         : "memory");
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t my = s + (lane >> 2) + 8 * k;
+                        if (my < to) {
+                            const uint32_t idx = (uint32_t)tt * (st->ring_mask + 1) + (my & st->ring_mask);
+                            reinterpret_cast<uint4*>(&st->rings[idx])[lane & 3] = v[k];
+                        }
                     }
                 }
+                __threadfence();  // every lane's slot stores before lane 0 publishes the tail
                 __syncwarp();
                 if (lane == 0) {
                     __threadfence();

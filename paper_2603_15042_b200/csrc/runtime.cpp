@@ -157,7 +157,18 @@ uint64_t kernel_fingerprint(const KernelRecord& r, const uint8_t* args) {
     return h;
 }
 
+// Host-side busy wait: the completion path is latency-critical (a decode
+// step's completion gates the next step's launches), and a sleep costs the
+// Linux timer slack (~50 us).  Poll with pause for a while after the last
+// activity, then back off to short sleeps.
+static inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+}
+
 void drain_loop(ds_domain* d) {
+    auto last_active = std::chrono::steady_clock::now();
     while (!d->drain_stop.load(std::memory_order_acquire)) {
         bool any = false;
         for (;;) {
@@ -178,8 +189,14 @@ void drain_loop(ds_domain* d) {
                 d->tenants[c.tenant]->completed.store(c.seq + 1, std::memory_order_release);
             d->completed_total.fetch_add(1, std::memory_order_relaxed);
         }
-        if (any) d->comp_cv.notify_all();
-        else std::this_thread::sleep_for(std::chrono::microseconds(2));
+        if (any) {
+            d->comp_cv.notify_all();
+            last_active = std::chrono::steady_clock::now();
+        } else if (std::chrono::steady_clock::now() - last_active < std::chrono::milliseconds(20)) {
+            for (int i = 0; i < 32; ++i) cpu_relax();
+        } else {
+            std::this_thread::sleep_for(std::chrono::microseconds(2));
+        }
     }
 }
 
