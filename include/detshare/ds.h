@@ -327,9 +327,12 @@ int ds_body_smem(int body, uint32_t* bytes);
  * matrix, SWIZZLE_128B boxes of box_rows x box_cols (box_cols*2 must be 128) */
 int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                           uint32_t box_cols);
-/* KV-cache rows of 128 bf16 as a 3-D {64, 2, rows} view: one box = box_rows
- * whole rows (contiguous), SWIZZLE_128B, smem row R = 2*row + half */
+/* KV-cache rows of 128 bf16 as a 3-D {64 dims, rows, 2 halves} view: one box
+ * = box_rows rows as two SWIZZLE_128B half-tiles (dims 0-63, then 64-127).
+ * box_rows must equal ds_attn_chunk(). */
 int ds_tensor_map_bf16_kv(void* out128, const void* base, uint64_t rows, uint32_t box_rows);
+/* KV positions per attention pipeline stage of this build (DS_BODY_ATTN_DECODE) */
+int ds_attn_chunk(void);
 
 /* ---- policy engine: the SimEngine dispatch loop over the executor ----
  * (engine.hpp:152-170; Policy hooks policy.hpp:97-126; built-ins

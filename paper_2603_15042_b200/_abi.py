@@ -187,7 +187,13 @@ def tensor_map_bf16(ptr: int, rows: int, cols: int, box_rows: int, box_cols: int
     return d
 
 
-def tensor_map_kv(ptr: int, rows: int, box_rows: int = 32) -> TmaDesc:
+def attn_chunk() -> int:
+    """KV positions per attention pipeline stage (bodies/decode.cuh kAttnChunk) of the loaded build."""
+    return int(lib().ds_attn_chunk())
+
+
+def tensor_map_kv(ptr: int, rows: int, box_rows: int = 0) -> TmaDesc:
+    box_rows = box_rows or attn_chunk()
     d = TmaDesc()
     check(lib().ds_tensor_map_bf16_kv(ctypes.byref(d), ctypes.c_void_p(ptr), rows, box_rows))
     return d
@@ -247,7 +253,6 @@ class RmsArgs(ctypes.Structure):
     _fields_ = [("x", ctypes.c_uint64), ("stats", ctypes.c_uint64), ("K", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
-ATTN_CHUNK = 64  # KV positions per attention TMA box / pipeline stage (csrc/bodies/decode.cuh kAttnChunk)
 
 
 class AttnArgs(ctypes.Structure):
@@ -452,7 +457,7 @@ EXPORTS = [
     "ds_set_lend", "ds_quota_at_claim", "ds_quota_periodic", "ds_stats_get", "ds_transcript",
     "ds_logical_progress", "ds_block_log", "ds_switch_log", "ds_ctl_log", "ds_clear_logs",
     "ds_globaltimer", "ds_debug_dump", "ds_ctl_roundtrip", "ds_solo_launch", "ds_solo_launch_registered", "ds_body_smem",
-    "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_kv", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
+    "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_kv", "ds_attn_chunk", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
     "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",

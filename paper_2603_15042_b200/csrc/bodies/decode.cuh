@@ -328,7 +328,7 @@ __device__ void body_rmsnorm(const BodyCtx& c) {
 // splits' (m, l, O) merge in order 0..S-1 in the block that retires last.
 // ---------------------------------------------------------------------------
 struct AttnArgs {
-    TmaDesc tmK;        // K cache rows as a {64, 2, rows} view, box {64, 2, 32}: 8 KB contiguous, SWIZZLE_128B
+    TmaDesc tmK;        // K cache rows [rows][128] bf16 as a 2-D view, box {64 dims, kAttnChunk rows}, SWIZZLE_128B
     TmaDesc tmV;        // V cache, same view
     uint64_t q;         // bf16 [32][32*128]
     uint64_t out;       // bf16 [32][32*128]
@@ -344,32 +344,29 @@ struct AttnArgs {
     int32_t pad;
 };
 
-constexpr int kAttnChunk = 64;   // KV positions per staged chunk (QK warp w: positions w*kQkPos ..)
-constexpr int kQkPos = kAttnChunk / 4;  // positions per QK warp per chunk
-constexpr int kQkNt = kQkPos / 8;       // mma n-tiles per QK warp per chunk
-// Separate K and V rings: K is consumed by the QK warps (which run ahead),
-// V by the PV warps; V gets the deeper ring so its refills (issued when the
-// PV side releases a slot) have the most chunks of lookahead.
-#ifndef DS_ATTN_KSLOTS
-#define DS_ATTN_KSLOTS 2
+// KV positions per pipeline stage (one TMA box height).  A stage holds the
+// chunk's K and V rows as four SWIZZLE_128B half-tiles [chunk][64 dims]
+// (K dims 0-63, K 64-127, V 0-63, V 64-127): row r of a half-tile is one
+// position, so 8 consecutive positions hit 8 distinct 16-B bank groups and
+// every ldmatrix below is conflict-free.
+#ifndef DS_ATTN_CHUNK
+#define DS_ATTN_CHUNK 64
 #endif
-#ifndef DS_ATTN_VSLOTS
-#define DS_ATTN_VSLOTS 4
-#endif
-constexpr int kAttnKSlots = DS_ATTN_KSLOTS;
-constexpr int kAttnVSlots = DS_ATTN_VSLOTS;
-constexpr uint32_t kAttnTile = kAttnChunk * 256;                      // 64 rows x 128 dims bf16 = 16 KB
-constexpr uint32_t kAttnVOff = kAttnKSlots * kAttnTile;               // V ring after the K ring
-constexpr uint32_t kAttnBarOff = (kAttnKSlots + kAttnVSlots) * kAttnTile;  // 96 KB
-constexpr uint32_t kAttnSOff = kAttnBarOff + 1024;                    // scores fp32 [2][4][64]
-constexpr uint32_t kAttnSBytes = 4 * kAttnChunk * 4;                   // one S buffer
-constexpr uint32_t kAttnSmem = kAttnSOff + 2 * kAttnSBytes + 1024;
+constexpr int kAttnChunk = DS_ATTN_CHUNK;
+constexpr int kAttnWpc = kAttnChunk / 16;                  // warps per chunk (16 positions each)
+constexpr int kAttnGroups = 8 / kAttnWpc;                  // chunk c is consumed by warp group c % groups
+constexpr uint32_t kAttnHalf = kAttnChunk * 128;           // one [chunk][64] bf16 half-tile
+constexpr uint32_t kAttnStage = 4 * kAttnHalf;             // K + V of one chunk
+constexpr int kAttnStages = (96 * 1024) / kAttnStage;      // 3 x 32 KB (chunk 64) or 6 x 16 KB (chunk 32)
+constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStage;
+constexpr uint32_t kAttnSmem = kAttnBarOff + 1024;
+static_assert(kAttnChunk == 32 || kAttnChunk == 64, "chunk of 32 or 64 positions");
+static_assert(kAttnStages >= kAttnGroups + 1, "every group needs a stage in flight beyond the others'");
 
-// byte address of (position r, dim d (multiple of 8)) in a K/V tile loaded
-// through the {64, 2, rows} view: smem 128-B row R = 2r + d/64, SWIZZLE_128B
+// byte address of (position r, dim d (multiple of 8)) of a K or V chunk
+// (tile = the chunk's K or V half-tile pair)
 __device__ __forceinline__ uint32_t kv_addr(uint32_t tile, int r, int d) {
-    const int R = 2 * r + (d >> 6);
-    return tile + R * 128 + ((((d & 63) >> 3) ^ (R & 7)) << 4);
+    return tile + (d >> 6) * kAttnHalf + r * 128 + ((((d & 63) >> 3) ^ (r & 7)) << 4);
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -379,6 +376,11 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t a) {
+    uint32_t d;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+    return d;
 }
 // D = A(16x16 bf16, row) . B(16x8 bf16, col) + D, fp32 accumulate
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -390,16 +392,19 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// GQA decode attention on tensor cores, warp-specialised.  K/V chunks of 64
-// positions arrive by TMA (SWIZZLE_128B, one contiguous 16-KB box each) into
-// separate K and V rings.
-//   warps 0-3 (QK):  S = Q.K^T for 16 positions each (M = 16 rows, the kv
-//                    group's 4 query heads real; K = 128 dims, 8 mma k-steps)
-//   warps 4-7 (PV):  softmax over the chunk (one rescale per chunk) and
-//                    O += P.V for 32 dims each (P reused from registers as A)
-// S is handed over through two smem buffers with FULL/EMPTY mbarriers, so QK
-// runs up to two chunks ahead of softmax/PV.  Deterministic: fixed chunk
-// order, fixed reduction trees.
+// GQA decode attention on tensor cores, positions split across warps.
+// Chunk c (kAttnChunk positions) lands by TMA in stage c % kAttnStages and is
+// consumed by warp group c % kAttnGroups: each warp of the group owns 16 of
+// its positions and runs, in registers,
+//   S^T[16 pos][8] = K[16 pos][128] . Q^T      (M = positions, N = the kv
+//                                               group's 4 query heads + 4 zero)
+//   online softmax per head (max over the 16 positions by shuffles)
+//   O^T[128][8]   += V^T[128][16 pos] . P^T    (P^T regrouped by movmatrix)
+// so no scores cross warps and nothing waits on another warp except the
+// stage refill.  Each warp keeps its own (m, l, O) over the positions it
+// owned; at the end the 8 warps merge in warp order.  Deterministic: the
+// position -> warp map, the chunk order and every reduction tree are fixed
+// functions of (L, S, block).
 __device__ void body_attn_decode(const BodyCtx& c) {
     const AttnArgs& a = *reinterpret_cast<const AttnArgs*>(c.args);
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
@@ -407,232 +412,257 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     const int b = bh >> 3, h = bh & 7;
     const int warp = ltid() >> 5, lane = ltid() & 31;
     const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+    const int grp = warp / kAttnWpc, sub = warp % kAttnWpc;
     const int p0 = (int)((int64_t)sp * a.L / a.S), p1 = (int)((int64_t)(sp + 1) * a.L / a.S);
     const int nch = (p1 - p0 + kAttnChunk - 1) / kAttnChunk;
     char* base = align1024(c.smem);
     const uint32_t sbase = tc::smem_u32(base);
-    uint64_t* kfull = reinterpret_cast<uint64_t*>(base + kAttnBarOff);  // [kAttnKSlots]
-    uint64_t* kempty = kfull + kAttnKSlots;
-    uint64_t* vfull = kempty + kAttnKSlots;                                // [kAttnVSlots]
-    uint64_t* vempty = vfull + kAttnVSlots;
-    const uint32_t Ssm = sbase + kAttnSOff;  // scores fp32 [2][4][kAttnChunk], double-buffered
-    // S handoff QK -> PV through two buffers: QK warps run up to two chunks
-    // ahead of the PV warps (mbarriers, 128 arrivals each)
-    uint64_t* sfull = vempty + kAttnVSlots;  // [2]
-    uint64_t* sempty = sfull + 2;            // [2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + kAttnBarOff);  // [kAttnStages]
+    // chunk each stage holds or is loading (written by the issuer before
+    // the TMA): groups run independently, so a consumer first waits for its
+    // chunk to be issued into the stage, then on the stage's full barrier
+    // with the exact phase parity (never a phase behind or two ahead)
+    volatile int* stage_chunk = reinterpret_cast<volatile int*>(base + kAttnBarOff + 256);  // [kAttnStages]
+    // warps of the consuming group done with the stage; the last one refills it
+    uint32_t* stage_done = reinterpret_cast<uint32_t*>(base + kAttnBarOff + 512);        // [kAttnStages]
     const int row0 = (b * 8 + h) * a.Lmax + p0;
+#ifdef DS_ATTN_TRACE  // diagnostic build: per-chunk timeline (dbg stride 128 per block)
+    uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 128 : nullptr;
+#else
     uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
-    if (dbg && ltid() == 128) dbg[0] = globaltimer();
-    auto issue_k = [&](int i) {
-        const int s = i % kAttnKSlots;
-        tc::mbar_arrive_expect_tx(&kfull[s], kAttnTile);
-        tc::tma_load_3d_hint(base + s * kAttnTile, &a.tmK, &kfull[s], 0, 0, row0 + i * kAttnChunk,
-                             tc::policy_evict_first());
-    };
-    auto issue_v = [&](int i) {
-        const int s = i % kAttnVSlots;
-        tc::mbar_arrive_expect_tx(&vfull[s], kAttnTile);
-        tc::tma_load_3d_hint(base + kAttnVOff + s * kAttnTile, &a.tmV, &vfull[s], 0, 0, row0 + i * kAttnChunk,
-                             tc::policy_evict_first());
+#endif
+    if (dbg && ltid() == 0) dbg[0] = globaltimer();
+    auto issue = [&](int i) {
+#ifdef DS_ATTN_TRACE
+        if (dbg && i < 64) dbg[64 + i] = globaltimer();
+#endif
+        const int s = i % kAttnStages;
+        char* st = base + s * kAttnStage;
+        const uint64_t pol = tc::policy_evict_first();
+        stage_chunk[s] = i;
+        tc::mbar_arrive_expect_tx(&full[s], kAttnStage);
+#ifdef DS_ATTN_BULK  // diagnostic build: contiguous bulk copies (layout unswizzled: timing only)
+        tc::bulk_g2s_hint(st, reinterpret_cast<const char*>(a.kbase) + (size_t)(row0 + i * kAttnChunk) * 256,
+                          2 * kAttnHalf, &full[s], pol);
+        tc::bulk_g2s_hint(st + 2 * kAttnHalf, reinterpret_cast<const char*>(a.vbase) + (size_t)(row0 + i * kAttnChunk) * 256,
+                          2 * kAttnHalf, &full[s], pol);
+        return;
+#endif
+        tc::tma_load_3d_hint(st, &a.tmK, &full[s], 0, row0 + i * kAttnChunk, 0, pol);
+        tc::tma_load_3d_hint(st + 2 * kAttnHalf, &a.tmV, &full[s], 0, row0 + i * kAttnChunk, 0, pol);
     };
     if (ltid() == 0) {
-        for (int s = 0; s < kAttnKSlots; ++s) {
-            tc::mbar_init(&kfull[s], 1);
-            tc::mbar_init(&kempty[s], 4);  // the 4 QK warps
-        }
-        for (int s = 0; s < kAttnVSlots; ++s) {
-            tc::mbar_init(&vfull[s], 1);
-            tc::mbar_init(&vempty[s], 4);  // the 4 PV warps
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&sfull[b], 128);
-            tc::mbar_init(&sempty[b], 128);
+        for (int s = 0; s < kAttnStages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            stage_chunk[s] = -1;
+            stage_done[s] = 0u;
         }
         tc::fence_mbar_init();
         tc::tma_fence_desc(&a.tmK);
         tc::tma_fence_desc(&a.tmV);
-    }
-    // Early start: the cache rows below L-1 are immutable for this step (the
-    // preceding QKV launch appends position L-1 only), so their first stages
-    // stream while that launch finishes; the chunk holding L-1 and the query
-    // rows are read only after wait_prev (launch order + acquire).
-    if (ltid() == 0) {
-        auto immutable = [&](int i) { return p0 + (i + 1) * kAttnChunk <= a.L - 1; };
-        int pk = 0, pv = 0;
-        while (pk < min(kAttnKSlots, nch) && immutable(pk)) issue_k(pk++);
-        while (pv < min(kAttnVSlots, nch) && immutable(pv)) issue_v(pv++);
+        // Early start: the cache rows below L-1 are immutable for this step
+        // (the preceding QKV launch appends position L-1 only), so their
+        // stages stream while that launch finishes; the chunk holding L-1
+        // and the query rows are read only after wait_prev (launch order +
+        // acquire).
+        const int pre = min(kAttnStages, nch);
+        int pk = 0;
+        while (pk < pre && p0 + (pk + 1) * kAttnChunk <= a.L - 1) issue(pk++);
         if (a.l2_pf_kb && nch > pk && wait_prev_streamed(c)) {
             // the rest of this block's K and V rows (contiguous, 256 B per
             // position) into L2 while the previous launch's epilogues run
             const char* kb = reinterpret_cast<const char*>(a.kbase) + ((size_t)row0 + pk * kAttnChunk) * 256;
-            const char* vb = reinterpret_cast<const char*>(a.vbase) + ((size_t)row0 + pv * kAttnChunk) * 256;
-            const uint32_t cap = (uint32_t)a.l2_pf_kb << 10;
-            const uint32_t kby = min(cap, (uint32_t)(p1 - p0 - pk * kAttnChunk) * 256u);
-            const uint32_t vby = min(cap, (uint32_t)max(0, p1 - p0 - pv * kAttnChunk) * 256u);
-            for (uint32_t off = 0; off < kby; off += kAttnTile) tc::bulk_prefetch_l2(kb + off, min(kAttnTile, kby - off));
-            for (uint32_t off = 0; off < vby; off += kAttnTile) tc::bulk_prefetch_l2(vb + off, min(kAttnTile, vby - off));
+            const char* vb = reinterpret_cast<const char*>(a.vbase) + ((size_t)row0 + pk * kAttnChunk) * 256;
+            const uint32_t by = min((uint32_t)a.l2_pf_kb << 10, (uint32_t)(p1 - p0 - pk * kAttnChunk) * 256u);
+            for (uint32_t off = 0; off < by; off += 16384) {
+                tc::bulk_prefetch_l2(kb + off, min(16384u, by - off));
+                tc::bulk_prefetch_l2(vb + off, min(16384u, by - off));
+            }
         }
         wait_prev(c);
-        for (int i = pk; i < min(kAttnKSlots, nch); ++i) issue_k(i);
-        for (int i = pv; i < min(kAttnVSlots, nch); ++i) issue_v(i);
+        for (int i = pk; i < pre; ++i) issue(i);
     }
     body_sync();  // carries thread 0's acquire (wait_prev) to the whole lane
-    const float scale = a.scale;
-    float m = kNegInf, lsum = 0.f;
-    float o[4][4];
+    if (dbg && ltid() == 0) dbg[7] = globaltimer();
+    // Q^T as the B operand of S^T = K . Q^T: B[k = dim][n = head g]; heads
+    // g >= 4 are zero padding (N = 8)
+    uint32_t qb[8][2];
+    {
+        const uint32_t* qr = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(a.q) +
+                                                                (size_t)b * 4096 + (h * 4 + (g & 3)) * 128);
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[nt][j] = 0.f;
-    if (warp < 4) {
-        // ================= QK warps =================
-        uint32_t qa[8][2];  // Q A-fragments (rows = query heads g < 4, rest zero)
-        {
-            const uint32_t* qb = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(a.q) +
-                                                                    (size_t)b * 4096 + (h * 4 + (g & 3)) * 128);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                qa[kk][0] = g < 4 ? __ldcg(qb + kk * 8 + tq) : 0u;
-                qa[kk][1] = g < 4 ? __ldcg(qb + kk * 8 + 4 + tq) : 0u;
-            }
-        }
-        const int m4 = lane >> 3;
-        for (int ci = 0; ci < nch; ++ci) {
-            const int s = ci % kAttnKSlots;
-            tc::mbar_wait(&kfull[s], (ci / kAttnKSlots) & 1);
-            const uint32_t kt = sbase + s * kAttnTile;
-            const int valid = min(kAttnChunk, p1 - (p0 + ci * kAttnChunk));
-            float sv[kQkNt][2];
-#pragma unroll
-            for (int nt = 0; nt < kQkNt; ++nt) {  // positions kQkPos*w + 8nt .. +7
-                float acc4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-                const int prow = warp * kQkPos + nt * 8 + (lane & 7);
-#pragma unroll
-                for (int kk = 0; kk < 8; kk += 2) {
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4(kv_addr(kt, prow, 16 * (kk + (m4 >> 1)) + 8 * (m4 & 1)), b0, b1, b2, b3);
-                    mma16816(acc4[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
-                    mma16816(acc4[1], qa[kk + 1][0], 0u, qa[kk + 1][1], 0u, b2, b3);
-                }
-                const int pc = warp * kQkPos + nt * 8 + 2 * tq;
-                sv[nt][0] = pc < valid ? (acc4[0][0] + acc4[1][0]) * scale : kNegInf;
-                sv[nt][1] = pc + 1 < valid ? (acc4[0][1] + acc4[1][1]) * scale : kNegInf;
-            }
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&kempty[s]);  // K of this slot consumed
-            // K refill by the QK side (warp 0 lane 0), as soon as all 4 QK warps
-            // released the slot
-            if (warp == 0 && lane == 0 && ci + kAttnKSlots < nch) {
-                tc::mbar_wait(&kempty[s], (ci / kAttnKSlots) & 1);
-                issue_k(ci + kAttnKSlots);
-            }
-            const int sb = ci & 1;
-            if (ci >= 2) tc::mbar_wait(&sempty[sb], ((ci - 2) >> 1) & 1);  // PV read chunk ci-2's S
-            if (g < 4) {
-#pragma unroll
-                for (int nt = 0; nt < kQkNt; ++nt) {
-                    const uint32_t sa = Ssm + sb * kAttnSBytes + (g * kAttnChunk + warp * kQkPos + nt * 8 + 2 * tq) * 4;
-                    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(sa), "f"(sv[nt][0]), "f"(sv[nt][1])
-                                 : "memory");
-                }
-            }
-            tc::mbar_arrive(&sfull[sb]);  // release: this thread's S stores
-        }
-    } else {
-        // ================= PV warps =================
-        const int pw = warp - 4;  // dims 32 pw .. 32 pw + 31
-        constexpr int KS = kAttnChunk / 16;
-        const int m4 = lane >> 3;
-        if (pw == 0 && lane == 0) {  // this thread issues the refills
-            tc::tma_fence_desc(&a.tmK);
-            tc::tma_fence_desc(&a.tmV);
-        }
-        for (int ci = 0; ci < nch; ++ci) {
-            const int s = ci % kAttnVSlots;
-            tc::mbar_wait(&vfull[s], (ci / kAttnVSlots) & 1);
-            const uint32_t vt = sbase + kAttnVOff + s * kAttnTile;
-            const int sb = ci & 1;
-            tc::mbar_wait(&sfull[sb], (ci >> 1) & 1);
-            float pv[KS][4];  // [k-step][a0.x, a0.y, a2.x, a2.y]
-            {
-                const uint32_t sr = Ssm + sb * kAttnSBytes + ((g & 3) * kAttnChunk + 2 * tq) * 4;
-#pragma unroll
-                for (int kk = 0; kk < KS; ++kk) {
-                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(pv[kk][0]), "=f"(pv[kk][1]) : "r"(sr + 64 * kk));
-                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(pv[kk][2]), "=f"(pv[kk][3])
-                                 : "r"(sr + 64 * kk + 32));
-                }
-            }
-            tc::mbar_arrive(&sempty[sb]);  // S copied into registers
-            float cm = kNegInf;
-#pragma unroll
-            for (int kk = 0; kk < KS; ++kk)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) cm = fmaxf(cm, pv[kk][j]);
-            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
-            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
-            const float mn = fmaxf(m, cm);
-            const float alpha = __expf(m - mn);
-            float ps = 0.f;
-#pragma unroll
-            for (int kk = 0; kk < KS; ++kk)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    pv[kk][j] = __expf(pv[kk][j] - mn);
-                    ps += pv[kk][j];
-                }
-            ps += __shfl_xor_sync(0xffffffffu, ps, 1);
-            ps += __shfl_xor_sync(0xffffffffu, ps, 2);
-            lsum = lsum * alpha + ps;
-            m = mn;
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-                o[nt][0] *= alpha;
-                o[nt][1] *= alpha;
-            }
-#pragma unroll
-            for (int kk = 0; kk < KS; ++kk) {
-                const uint32_t pa0 = g < 4 ? pack_bf16x2(pv[kk][0], pv[kk][1]) : 0u;
-                const uint32_t pa2 = g < 4 ? pack_bf16x2(pv[kk][2], pv[kk][3]) : 0u;
-                const int pos = 16 * kk + 8 * (m4 & 1) + (lane & 7);
-#pragma unroll
-                for (int np = 0; np < 2; ++np) {  // n-tile pairs (4 n-tiles of 8 dims)
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4_t(kv_addr(vt, pos, 32 * pw + 16 * np + 8 * (m4 >> 1)), b0, b1, b2, b3);
-                    mma16816(o[2 * np], pa0, 0u, pa2, 0u, b0, b1);
-                    mma16816(o[2 * np + 1], pa0, 0u, pa2, 0u, b2, b3);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&vempty[s]);  // V of this slot consumed
-            // V refill by the PV side: no QK warp ever waits for PV
-            if (pw == 0 && lane == 0 && ci + kAttnVSlots < nch) {
-                tc::mbar_wait(&vempty[s], (ci / kAttnVSlots) & 1);
-                issue_v(ci + kAttnVSlots);
-            }
+        for (int ks = 0; ks < 8; ++ks) {
+            qb[ks][0] = g < 4 ? __ldcg(qr + ks * 8 + tq) : 0u;
+            qb[ks][1] = g < 4 ? __ldcg(qr + ks * 8 + 4 + tq) : 0u;
         }
     }
-    if (ltid() == 128) mark_streamed(c);  // PV warp 0: every K / V chunk of this block consumed
-    if (dbg && ltid() == 128) dbg[1] = globaltimer();
-    // PV lanes with g < 4 own O[head g][32 pw + 8 nt + 2 tq, +1], nt = 0..3
-    const int pw = warp - 4;
-    bool write_out = true;
-    __shared__ int last_flag_l[2];
-    int& last_flag = last_flag_l[body_lane()];
-    float M = m, Ls = lsum;
-    const int hq = g & 3;
-    if (a.S > 1) {
-        float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130 + hq * 130;
-        if (warp >= 4 && g < 4) {
+    const float scale = a.scale;
+    // this thread: heads 2tq, 2tq+1 (real for tq < 2); O^T rows 16 mt + g, + 8
+    float m0 = kNegInf, m1 = kNegInf, l0 = 0.f, l1 = 0.f;
+    float o[8][4];
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-                ws[32 * pw + 8 * nt + 2 * tq] = o[nt][0];
-                ws[32 * pw + 8 * nt + 2 * tq + 1] = o[nt][1];
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[mt][j] = 0.f;
+    const int pw = 16 * sub;  // this warp's positions within a chunk
+    const int lr = lane & 7, lm = lane >> 3;
+    for (int ci = grp; ci < nch; ci += kAttnGroups) {
+        const int s = ci % kAttnStages;
+#ifdef DS_ATTN_TRACE
+        const int tj = ci / kAttnGroups;
+        const bool tr = dbg && ltid() == 0 && tj < 12;
+        if (tr) dbg[8 + 4 * tj] = globaltimer();
+#endif
+        while (stage_chunk[s] != ci) {
+        }
+#ifdef DS_ATTN_TRACE
+        if (tr) dbg[9 + 4 * tj] = globaltimer();
+#endif
+        tc::mbar_wait(&full[s], (ci / kAttnStages) & 1);
+#ifdef DS_ATTN_TRACE
+        if (tr) dbg[10 + 4 * tj] = globaltimer();
+#endif
+        const uint32_t kt = sbase + s * kAttnStage, vt = kt + 2 * kAttnHalf;
+#ifdef DS_ATTN_NOCOMPUTE  // diagnostic build: ring traffic and handoffs only
+        __syncwarp();
+        if (lane == 0 && atomicAdd(&stage_done[s], 1u) == kAttnWpc - 1) {
+            stage_done[s] = 0u;
+            if (ci + kAttnStages < nch) issue(ci + kAttnStages);
+        }
+        __syncwarp();
+        continue;
+#endif
+        // ---- S^T[16 pos][8] = K[pw..pw+15][:] . Q^T (two chains) ----
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < 8; ks += 2) {
+            uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
+            ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * ks + 8 * (lm >> 1)), a0, a1, a2, a3);
+            ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * (ks + 1) + 8 * (lm >> 1)), c0, c1, c2, c3);
+            mma16816(sa, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+            mma16816(sb2, c0, c1, c2, c3, qb[ks + 1][0], qb[ks + 1][1]);
+        }
+        // (pos g | g+8, head 2tq | 2tq+1); positions past the range masked
+        const int valid = p1 - (p0 + ci * kAttnChunk) - pw;
+        float sv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sv[j] = (sa[j] + sb2[j]) * scale;
+        if (g >= valid) sv[0] = sv[1] = kNegInf;
+        if (g + 8 >= valid) sv[2] = sv[3] = kNegInf;
+        // ---- online softmax per head over the warp's 16 positions ----
+        float c0m = fmaxf(sv[0], sv[2]), c1m = fmaxf(sv[1], sv[3]);
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+            c0m = fmaxf(c0m, __shfl_xor_sync(0xffffffffu, c0m, off));
+            c1m = fmaxf(c1m, __shfl_xor_sync(0xffffffffu, c1m, off));
+        }
+        const float n0 = fmaxf(m0, c0m), n1 = fmaxf(m1, c1m);
+        const float al0 = n0 == kNegInf ? 1.f : __expf(m0 - n0), al1 = n1 == kNegInf ? 1.f : __expf(m1 - n1);
+        const float e0 = sv[0] == kNegInf ? 0.f : __expf(sv[0] - n0);
+        const float e1 = sv[1] == kNegInf ? 0.f : __expf(sv[1] - n1);
+        const float e2 = sv[2] == kNegInf ? 0.f : __expf(sv[2] - n0);
+        const float e3 = sv[3] == kNegInf ? 0.f : __expf(sv[3] - n1);
+        m0 = n0;
+        m1 = n1;
+        // per-thread partial row sums (positions g, g+8); reduced over g at the end
+        l0 = l0 * al0 + (e0 + e2);
+        l1 = l1 * al1 + (e1 + e3);
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            o[mt][0] *= al0;
+            o[mt][1] *= al1;
+            o[mt][2] *= al0;
+            o[mt][3] *= al1;
+        }
+        // P^T as the B operand: B[k = pos 2tq..][n = head g] = transpose of
+        // the (pos g, head 2tq..) fragment, per 8x8 half
+        const uint32_t pb0 = movm_t(pack_bf16x2(e0, e1));
+        const uint32_t pb1 = movm_t(pack_bf16x2(e2, e3));
+        // ---- O^T[128][8] += V^T[:, pw..pw+15] . P^T ----
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_t(kv_addr(vt, pw + lr + 8 * (lm >> 1), 16 * mt + 8 * (lm & 1)), a0, a1, a2, a3);
+            mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
+        }
+        __syncwarp();
+#ifdef DS_ATTN_TRACE
+        if (tr) dbg[11 + 4 * tj] = globaltimer();
+#endif
+        // the group's last warp to finish the stage refills it (its reads,
+        // and through the acq_rel counter every other warp's, are complete)
+        if (lane == 0) {
+            uint32_t n;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(n) : "r"(tc::smem_u32(&stage_done[s])) : "memory");
+            if (n == kAttnWpc - 1) {
+                stage_done[s] = 0u;
+                if (ci + kAttnStages < nch) issue(ci + kAttnStages);
             }
-            if (warp == 4 && tq == 0) {
-                ws[128] = M;
-                ws[129] = Ls;
-            }
+        }
+        __syncwarp();
+    }
+#ifdef DS_ATTN_NOCOMPUTE
+    m0 = m1 = 0.f;
+    l0 = l1 = 0.125f;
+#endif
+    // l over the 8 g-rows of the warp (fixed tree)
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+    body_sync();  // every stage consumed: the ring is scratch from here on
+    if (ltid() == 0) mark_streamed(c);
+    if (dbg && ltid() == 0) dbg[1] = globaltimer();
+    // ---- merge the 8 warps in warp order ----
+    // scratch: O_w [8 warps][4 heads][128 dims] fp32, m/l [8][4]
+    float* Ow = reinterpret_cast<float*>(base);
+    float* Mw = Ow + 8 * 4 * 128;
+    float* Lw = Mw + 32;
+    if (tq < 2) {
+        float* ow = Ow + warp * 512;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            ow[(2 * tq) * 128 + 16 * mt + g] = o[mt][0];
+            ow[(2 * tq + 1) * 128 + 16 * mt + g] = o[mt][1];
+            ow[(2 * tq) * 128 + 16 * mt + g + 8] = o[mt][2];
+            ow[(2 * tq + 1) * 128 + 16 * mt + g + 8] = o[mt][3];
+        }
+        if (g == 0) {
+            Mw[warp * 4 + 2 * tq] = m0;
+            Mw[warp * 4 + 2 * tq + 1] = m1;
+            Lw[warp * 4 + 2 * tq] = l0;
+            Lw[warp * 4 + 2 * tq + 1] = l1;
+        }
+    }
+    body_sync();
+    // thread -> (head hq, dims 2j, 2j+1)
+    const int hq = ltid() >> 6, j2 = 2 * (ltid() & 63);
+    float M = kNegInf;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) M = fmaxf(M, Mw[w * 4 + hq]);
+    float Ls = 0.f, O0 = 0.f, O1 = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const float mw = Mw[w * 4 + hq];
+        const float f = mw == kNegInf ? 0.f : __expf(mw - M);
+        Ls += Lw[w * 4 + hq] * f;
+        O0 += Ow[w * 512 + hq * 128 + j2] * f;
+        O1 += Ow[w * 512 + hq * 128 + j2 + 1] * f;
+    }
+    bool write_out = true;
+    if (a.S > 1) {
+        // this split's (O, M, L) to the workspace; the split that retires
+        // last merges splits 0..S-1 in order
+        __shared__ int last_flag_l[2];
+        int& last_flag = last_flag_l[body_lane()];
+        float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130 + hq * 130;
+        ws[j2] = O0;
+        ws[j2 + 1] = O1;
+        if (j2 == 0) {
+            ws[128] = M;
+            ws[129] = Ls;
         }
         body_sync();
         if (ltid() == 0) {
@@ -643,39 +673,32 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         }
         body_sync();
         write_out = last_flag != 0;
-        if (write_out && warp >= 4 && g < 4) {
+        if (write_out) {
             __threadfence();
             const float* wsb = reinterpret_cast<const float*>(a.ws) + (size_t)bh * a.S * 4 * 130 + hq * 130;
             M = kNegInf;
             for (int s2 = 0; s2 < a.S; ++s2) M = fmaxf(M, __ldcg(wsb + s2 * 4 * 130 + 128));
-            Ls = 0.f;
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) o[nt][0] = o[nt][1] = 0.f;
+            Ls = O0 = O1 = 0.f;
             for (int s2 = 0; s2 < a.S; ++s2) {  // fixed order
                 const float* src = wsb + s2 * 4 * 130;
                 const float mw = __ldcg(src + 128);
                 const float f = (mw == kNegInf) ? 0.f : __expf(mw - M);
                 Ls += __ldcg(src + 129) * f;
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    o[nt][0] += __ldcg(src + 32 * pw + 8 * nt + 2 * tq) * f;
-                    o[nt][1] += __ldcg(src + 32 * pw + 8 * nt + 2 * tq + 1) * f;
-                }
+                O0 += __ldcg(src + j2) * f;
+                O1 += __ldcg(src + j2 + 1) * f;
             }
+            if (ltid() == 0) reinterpret_cast<uint32_t*>(a.counters)[bh] = 0;
         }
-        if (write_out && ltid() == 0) reinterpret_cast<uint32_t*>(a.counters)[bh] = 0;
     }
-    if (write_out && warp >= 4 && g < 4) {
+    if (write_out) {
         const float inv = 1.f / Ls;
         uint16_t* orow = reinterpret_cast<uint16_t*>(a.out) + (size_t)b * 4096 + (h * 4 + hq) * 128;
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-            *reinterpret_cast<uint32_t*>(orow + 32 * pw + 8 * nt + 2 * tq) = pack_bf16x2(o[nt][0] * inv, o[nt][1] * inv);
+        *reinterpret_cast<uint32_t*>(orow + j2) = pack_bf16x2(O0 * inv, O1 * inv);
     }
     body_sync();
-    if (dbg && ltid() == 128) dbg[6] = globaltimer();
+    if (dbg && ltid() == 0) dbg[6] = globaltimer();
     if (ltid() == 0)
-        for (int s = 0; s < 2 * (kAttnKSlots + kAttnVSlots) + 4; ++s) tc::mbar_inval(&kfull[s]);
+        for (int s = 0; s < kAttnStages; ++s) tc::mbar_inval(&full[s]);
 }
 
 }  // namespace ds

@@ -1042,6 +1042,8 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
     }
 }
 
+extern "C" int ds_attn_chunk(void) { return ds::kAttnChunk; }
+
 extern "C" int ds_dev_ctas_per_sm(void) { return 1; }  // one CTA per SM (kLanes worker lanes inside)
 
 extern "C" int ds_dev_exec_attrs(int* regs, int* local, int* static_smem, int* max_threads) {

@@ -1335,9 +1335,10 @@ int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_
 }
 
 // KV-cache view for the attention body: [rows][128] bf16 as a 3-D tensor
-// {64 dims, 2 halves, rows} so one box {64, 2, 32} is 32 whole rows = 8 KB
-// of contiguous memory, landing in smem as 64 SWIZZLE_128B rows
-// (smem row R = 2*row + half).
+// {64 dims, rows, 2 halves} (strides 256 B per row, 128 B per half); one box
+// {64, box_rows, 2} lands as two half-tiles [box_rows][64] (128-B rows,
+// SWIZZLE_128B), dims 0-63 then 64-127: one smem row per KV position, so the
+// body's ldmatrix reads are conflict-free, and one TMA per chunk operand.
 int ds_tensor_map_bf16_kv(void* out128, const void* base, uint64_t rows, uint32_t box_rows) {
     if (!out128 || !base) return fail(DS_INVALID_ARGUMENT, "null");
     if (((uintptr_t)base & 15)) return fail(DS_CONFIG_ERROR, "base must be 16-B aligned");
@@ -1350,9 +1351,10 @@ int ds_tensor_map_bf16_kv(void* out128, const void* base, uint64_t rows, uint32_
         fn = (EncodeTiledFn)p;
     }
     CUtensorMap m;
-    cuuint64_t dims[3] = {64, 2, rows};
-    cuuint64_t strides[2] = {128, 256};
-    cuuint32_t box[3] = {64, 2, box_rows};
+    if ((int)box_rows != ds_attn_chunk()) return fail(DS_CONFIG_ERROR, "kv box rows must equal ds_attn_chunk()");
+    cuuint64_t dims[3] = {64, rows, 2};
+    cuuint64_t strides[2] = {256, 128};
+    cuuint32_t box[3] = {64, box_rows, 2};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -22,7 +22,6 @@ import torch
 from . import _abi
 
 SMS = 148
-ATTN_CHUNK = _abi.ATTN_CHUNK  # KV positions per attention TMA box (bodies/decode.cuh kAttnChunk)
 LANES = 2
 WORKERS = SMS * LANES  # concurrent logical blocks (2 worker lanes per SM)
 
@@ -191,8 +190,8 @@ class DecodeModel:
                               stats_in=st_in, P_in=p_in, l=l, bm=self.BM["qkv"], pf=self.PF["qkv"])
             self.records.append((f"decode/qkv", _abi.BODY_GEMV_BF16, g, a, self.qkv_n * c.d * 2))
             rows = 32 * c.n_kv * self.Lmax
-            at = _abi.AttnArgs(_abi.tensor_map_kv(self.kc[l].data_ptr(), rows, ATTN_CHUNK),
-                               _abi.tensor_map_kv(self.vc[l].data_ptr(), rows, ATTN_CHUNK), self.q.data_ptr(),
+            at = _abi.AttnArgs(_abi.tensor_map_kv(self.kc[l].data_ptr(), rows),
+                               _abi.tensor_map_kv(self.vc[l].data_ptr(), rows), self.q.data_ptr(),
                                self.attn.data_ptr(), self.attn_ws.data_ptr(), self.attn_counters.data_ptr(), c.L,
                                self.Lmax, c.attn_splits, 1.0 / math.sqrt(128))
             at.kbase, at.vbase, at.l2_pf_kb = self.kc[l].data_ptr(), self.vc[l].data_ptr(), self.PF["attn"]

@@ -22,8 +22,8 @@ def test_attention_matches_fp32_reference(L, S):
     ws = torch.zeros(256 * S * 4 * 130, device="cuda")
     ctr = torch.zeros(256, device="cuda", dtype=torch.int32)
     rows = 32 * 8 * Lmax
-    a = _abi.AttnArgs(_abi.tensor_map_kv(kc.data_ptr(), rows, _abi.ATTN_CHUNK),
-                      _abi.tensor_map_kv(vc.data_ptr(), rows, _abi.ATTN_CHUNK),
+    a = _abi.AttnArgs(_abi.tensor_map_kv(kc.data_ptr(), rows),
+                      _abi.tensor_map_kv(vc.data_ptr(), rows),
                       q.data_ptr(), out.data_ptr(), ws.data_ptr(), ctr.data_ptr(), L, Lmax, S, 1.0 / math.sqrt(128), 0)
     solo_launch(0, "attn", _abi.BODY_ATTN_DECODE, (256 * S, 1, 1), a)
     torch.cuda.synchronize()
