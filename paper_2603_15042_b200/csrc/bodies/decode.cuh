@@ -359,7 +359,8 @@ constexpr uint32_t kAttnHalf = kAttnChunk * 128;           // one [chunk][64] bf
 constexpr uint32_t kAttnStage = 4 * kAttnHalf;             // K + V of one chunk
 constexpr int kAttnStages = (96 * 1024) / kAttnStage;      // 3 x 32 KB (chunk 64) or 6 x 16 KB (chunk 32)
 constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStage;
-constexpr uint32_t kAttnSmem = kAttnBarOff + 1024;
+constexpr uint32_t kAttnQOff = kAttnBarOff + 1024;           // Q^T B fragments [8 ks][2][4 heads][4 tq] u32
+constexpr uint32_t kAttnSmem = kAttnQOff + 1024;
 static_assert(kAttnChunk == 32 || kAttnChunk == 64, "chunk of 32 or 64 positions");
 static_assert(kAttnStages >= kAttnGroups + 1, "every group needs a stage in flight beyond the others'");
 
@@ -376,6 +377,11 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 __device__ __forceinline__ uint32_t movm_t(uint32_t a) {
     uint32_t d;
@@ -485,18 +491,25 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     body_sync();  // carries thread 0's acquire (wait_prev) to the whole lane
     if (dbg && ltid() == 0) dbg[7] = globaltimer();
     // Q^T as the B operand of S^T = K . Q^T: B[k = dim][n = head g]; heads
-    // g >= 4 are zero padding (N = 8)
-    uint32_t qb[8][2];
+    // g >= 4 are zero padding (N = 8).  The fragments live in smem, in
+    // fragment order (registers are the executor's scarce resource: the
+    // O^T accumulators take 32 of them), and are re-read per k-step.
+    const uint32_t qs = sbase + kAttnQOff;
     {
-        const uint32_t* qr = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(a.q) +
-                                                                (size_t)b * 4096 + (h * 4 + (g & 3)) * 128);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-            qb[ks][0] = g < 4 ? __ldcg(qr + ks * 8 + tq) : 0u;
-            qb[ks][1] = g < 4 ? __ldcg(qr + ks * 8 + 4 + tq) : 0u;
-        }
+        // thread i: head i >> 6, u32 i & 63 of that head's 128 dims -> (ks, j, tq)
+        const int hq = ltid() >> 6, w = ltid() & 63;
+        const uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(a.q) +
+                                                                    (size_t)b * 4096 + (h * 4 + hq) * 128) + w);
+        const int ks = w >> 3, j = (w >> 2) & 1, q4 = w & 3;
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(qs + (((ks * 2 + j) * 4 + hq) * 4 + q4) * 4), "r"(v) : "memory");
     }
-    const float scale = a.scale;
+    body_sync();
+    auto qfrag = [&](int ks, int j) -> uint32_t {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(qs + (((ks * 2 + j) * 4 + (g & 3)) * 4 + tq) * 4));
+        return g < 4 ? v : 0u;
+    };
+    const float scale2 = a.scale * 1.4426950408889634f;  // softmax in base 2
     // this thread: heads 2tq, 2tq+1 (real for tq < 2); O^T rows 16 mt + g, + 8
     float m0 = kNegInf, m1 = kNegInf, l0 = 0.f, l1 = 0.f;
     float o[8][4];
@@ -523,6 +536,21 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         if (tr) dbg[10 + 4 * tj] = globaltimer();
 #endif
         const uint32_t kt = sbase + s * kAttnStage, vt = kt + 2 * kAttnHalf;
+#ifdef DS_ATTN_LDSM_ONLY  // diagnostic build: the ldmatrix reads of K and V, no math
+        {
+            uint32_t x = 0;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * ks + 8 * (lm >> 1)), a0, a1, a2, a3);
+                x ^= a0 ^ a1 ^ a2 ^ a3;
+                ldsm_x4_t(kv_addr(vt, pw + lr + 8 * (lm >> 1), 16 * ks + 8 * (lm & 1)), a0, a1, a2, a3);
+                x ^= a0 ^ a1 ^ a2 ^ a3;
+            }
+            o[0][0] += __uint_as_float(x & 0x3f000000u);
+        }
+#define DS_ATTN_NOCOMPUTE
+#endif
 #ifdef DS_ATTN_NOCOMPUTE  // diagnostic build: ring traffic and handoffs only
         __syncwarp();
         if (lane == 0 && atomicAdd(&stage_done[s], 1u) == kAttnWpc - 1) {
@@ -539,16 +567,19 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
             ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * ks + 8 * (lm >> 1)), a0, a1, a2, a3);
             ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * (ks + 1) + 8 * (lm >> 1)), c0, c1, c2, c3);
-            mma16816(sa, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-            mma16816(sb2, c0, c1, c2, c3, qb[ks + 1][0], qb[ks + 1][1]);
+            mma16816(sa, a0, a1, a2, a3, qfrag(ks, 0), qfrag(ks, 1));
+            mma16816(sb2, c0, c1, c2, c3, qfrag(ks + 1, 0), qfrag(ks + 1, 1));
         }
-        // (pos g | g+8, head 2tq | 2tq+1); positions past the range masked
+        // (pos g | g+8, head 2tq | 2tq+1), in log2 units (exp(x) = 2^(x log2 e));
+        // positions past the range masked
         const int valid = p1 - (p0 + ci * kAttnChunk) - pw;
         float sv[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sv[j] = (sa[j] + sb2[j]) * scale;
-        if (g >= valid) sv[0] = sv[1] = kNegInf;
-        if (g + 8 >= valid) sv[2] = sv[3] = kNegInf;
+        for (int j = 0; j < 4; ++j) sv[j] = (sa[j] + sb2[j]) * scale2;
+        if (valid < 16) {
+            if (g >= valid) sv[0] = sv[1] = kNegInf;
+            if (g + 8 >= valid) sv[2] = sv[3] = kNegInf;
+        }
         // ---- online softmax per head over the warp's 16 positions ----
         float c0m = fmaxf(sv[0], sv[2]), c1m = fmaxf(sv[1], sv[3]);
 #pragma unroll
@@ -556,23 +587,26 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             c0m = fmaxf(c0m, __shfl_xor_sync(0xffffffffu, c0m, off));
             c1m = fmaxf(c1m, __shfl_xor_sync(0xffffffffu, c1m, off));
         }
+        // a head with no valid position yet keeps max -inf: exponents
+        // against 0 then give 2^-inf = 0 (never -inf - -inf)
         const float n0 = fmaxf(m0, c0m), n1 = fmaxf(m1, c1m);
-        const float al0 = n0 == kNegInf ? 1.f : __expf(m0 - n0), al1 = n1 == kNegInf ? 1.f : __expf(m1 - n1);
-        const float e0 = sv[0] == kNegInf ? 0.f : __expf(sv[0] - n0);
-        const float e1 = sv[1] == kNegInf ? 0.f : __expf(sv[1] - n1);
-        const float e2 = sv[2] == kNegInf ? 0.f : __expf(sv[2] - n0);
-        const float e3 = sv[3] == kNegInf ? 0.f : __expf(sv[3] - n1);
+        const float z0 = n0 == kNegInf ? 0.f : n0, z1 = n1 == kNegInf ? 0.f : n1;
+        const float al0 = ex2_ftz(m0 - z0), al1 = ex2_ftz(m1 - z1);
+        const float e0 = ex2_ftz(sv[0] - z0), e1 = ex2_ftz(sv[1] - z1);
+        const float e2 = ex2_ftz(sv[2] - z0), e3 = ex2_ftz(sv[3] - z1);
         m0 = n0;
         m1 = n1;
         // per-thread partial row sums (positions g, g+8); reduced over g at the end
         l0 = l0 * al0 + (e0 + e2);
         l1 = l1 * al1 + (e1 + e3);
+        if (!__all_sync(0xffffffffu, al0 == 1.f && al1 == 1.f)) {  // x 1.0 is exact: skipped when no max moved
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-            o[mt][0] *= al0;
-            o[mt][1] *= al1;
-            o[mt][2] *= al0;
-            o[mt][3] *= al1;
+            for (int mt = 0; mt < 8; ++mt) {
+                o[mt][0] *= al0;
+                o[mt][1] *= al1;
+                o[mt][2] *= al0;
+                o[mt][3] *= al1;
+            }
         }
         // P^T as the B operand: B[k = pos 2tq..][n = head g] = transpose of
         // the (pos g, head 2tq..) fragment, per 8x8 half
@@ -646,7 +680,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
         const float mw = Mw[w * 4 + hq];
-        const float f = mw == kNegInf ? 0.f : __expf(mw - M);
+        const float f = mw == kNegInf ? 0.f : ex2_ftz(mw - M);
         Ls += Lw[w * 4 + hq] * f;
         O0 += Ow[w * 512 + hq * 128 + j2] * f;
         O1 += Ow[w * 512 + hq * 128 + j2 + 1] * f;
@@ -682,7 +716,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
             for (int s2 = 0; s2 < a.S; ++s2) {  // fixed order
                 const float* src = wsb + s2 * 4 * 130;
                 const float mw = __ldcg(src + 128);
-                const float f = (mw == kNegInf) ? 0.f : __expf(mw - M);
+                const float f = (mw == kNegInf) ? 0.f : ex2_ftz(mw - M);
                 Ls += __ldcg(src + 129) * f;
                 O0 += __ldcg(src + j2) * f;
                 O1 += __ldcg(src + j2 + 1) * f;
