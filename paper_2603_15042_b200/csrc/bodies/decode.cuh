@@ -14,9 +14,10 @@ namespace ds {
 // ---------------------------------------------------------------------------
 // Projection: y[b][n] = sum_k W[n][k] x[b][k]  (b < 32), swap-AB on tcgen05:
 // D[128 weight rows][32 batch] with the weight slab as the M operand.
-// Logical block t -> (row slab n_blk = t % nb, K-split s = t / nb).  With
-// S > 1 each block writes fp32 partials and the block that retires last for
-// its slab (ticket) sums s = 0..S-1 in order and runs the epilogue.
+// Logical block t -> (row slab, k-range) pieces: split-K (t -> slab t % nb,
+// split t / nb) or stream-K (equal contiguous runs of (slab, k-block) units
+// over any grid size).  A slab's last contributor sums the others' fp32
+// partials in ascending k order and runs the epilogue.
 // ---------------------------------------------------------------------------
 enum GemvMode : int32_t { kGemvStore = 0, kGemvResid = 1, kGemvSiluMul = 2, kGemvQKV = 3 };
 
@@ -42,6 +43,9 @@ struct GemvArgs {
     int32_t bm;         // slab rows: 128 (0) or 64 (not for kGemvSiluMul)
     int32_t l2_pf_kb;   // early start: KB of this block's weights past the ring prefetched into L2 before
                         // the dependency resolves (0 = ring only)
+    int32_t sk;         // 1: stream-K over the logical grid (equal runs of (slab, k-block) units, <= 2 slabs
+                        // per block); 0: split-K S with grid nb * S
+    int32_t pad;
 };
 
 constexpr int kGemvBN = 32;
@@ -59,8 +63,127 @@ __device__ __forceinline__ uint16_t f_to_bf16(float f) {
 }
 
 
+// A logical block's share of one row slab: k-blocks [ka, kb) of slab n; it is
+// contributor c of the slab's nc contributors (ascending k), and the owner
+// (combiner) when it holds the slab's last k-block.
+struct GemvPiece {
+    int n, ka, kb, c, nc;
+    bool owner;
+};
+
+// Stream-K: unit u = n * KB + k (slab-major), block t covers units
+// [t U / G, (t+1) U / G); block_of(u) inverts that.
+__device__ __forceinline__ int gemv_block_of(int64_t u, int64_t U, int G) {
+    return (int)(((u + 1) * G - 1) / U);
+}
+
+// Mainloop over a block's pieces (at most 2, consecutive slabs): one smem
+// ring across both; piece p accumulates in TMEM columns [32 p, 32 p + 32).
+// The weight operand of step i is packed k-block (n*KB + k) -- in stream-K
+// order the block's whole weight range is one contiguous run of 16-KB tiles.
+template <int BM, int STAGES>
+__device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, const GemvPiece p0, const GemvPiece p1,
+                                              int np, uint32_t tmem_base, const BodyCtx& dep) {
+    using L = TcSmem<kGemvBN, STAGES, kTcBK, BM>;
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    const int warp = ltid() >> 5, lane = ltid() & 31;
+    const int KB = a.K / kTcBK;
+    const char* a_packed = reinterpret_cast<const char*>(a.w_packed);
+    if (ltid() == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tmem_full, 1);
+        tc::fence_mbar_init();
+    }
+    body_sync();
+    // pieces as scalars (a dynamically indexed array would live in local memory)
+    const int pn0 = p0.n, pka0 = p0.ka, n0 = p0.kb - p0.ka;
+    const int pn1 = np > 1 ? p1.n : pn0, pka1 = np > 1 ? p1.ka : 0;
+    const int total = n0 + (np > 1 ? p1.kb - p1.ka : 0);
+    // step i -> (slab, k-block)
+    auto piece_of = [&](int i, int& n, int& k) {
+        const bool second = i >= n0;
+        n = second ? pn1 : pn0;
+        k = second ? pka1 + (i - n0) : pka0 + i;
+    };
+    if (warp == 0 && lane == 0) {
+        if (!a_packed) tc::tma_fence_desc(&a.tmW);
+        tc::tma_fence_desc(&a.tmX);
+        const uint64_t pol = tc::policy_evict_first();
+        auto issue_a = [&](int i) {
+            int n, k;
+            piece_of(i, n, k);
+            char* sa = base + (i % STAGES) * L::kStageBytes;
+            if (a_packed)
+                tc::bulk_g2s_hint(sa, a_packed + ((size_t)n * KB + k) * L::kABytes, L::kABytes, &full[i % STAGES], pol);
+            else
+                tc::tma_load_2d_hint(sa, &a.tmW, &full[i % STAGES], k * kTcBK, n * BM, pol);
+        };
+        auto issue_b = [&](int i) {
+            int n, k;
+            piece_of(i, n, k);
+            tc::tma_load_2d(base + (i % STAGES) * L::kStageBytes + L::kABytes, &a.tmX, &full[i % STAGES], k * kTcBK, 0);
+        };
+        // the weights (immutable) stream while the previous launch finishes;
+        // X (its output) only after wait_prev
+        const int pre = min(STAGES, total);
+        for (int i = 0; i < pre; ++i) {
+            tc::mbar_arrive_expect_tx(&full[i], L::kStageBytes);
+            issue_a(i);
+        }
+        if (a_packed && a.l2_pf_kb && total > pre && wait_prev_streamed(dep)) {
+            int n, k;
+            piece_of(pre, n, k);
+            const char* g0 = a_packed + ((size_t)n * KB + k) * L::kABytes;
+            const uint32_t tot = min((uint32_t)(total - pre) * L::kABytes, (uint32_t)a.l2_pf_kb << 10);
+            for (uint32_t off = 0; off < tot; off += L::kABytes) tc::bulk_prefetch_l2(g0 + off, min(L::kABytes, tot - off));
+        }
+        wait_prev(dep);
+        if (dep.dbg) dep.dbg[7] = globaltimer();
+        for (int i = 0; i < pre; ++i) issue_b(i);
+        for (int i = pre; i < total; ++i) {
+            const int s = i % STAGES;
+            tc::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+            issue_a(i);
+            issue_b(i);
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, kGemvBN);
+        for (int i = 0; i < total; ++i) {
+            const int s = i % STAGES;
+            tc::mbar_wait(&full[s], (i / STAGES) & 1);
+            tc::tc_fence_after();
+            char* sa = base + s * L::kStageBytes;
+            const uint64_t ad = tc::smem_desc_k_sw128(sa), bd = tc::smem_desc_k_sw128(sa + L::kABytes);
+            const int p = i < n0 ? 0 : 1;
+            const bool first = i == 0 || i == n0;
+#pragma unroll
+            for (int k = 0; k < kTcBK / 16; ++k)
+                tc::mma_bf16(tmem_base + 32 * p, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, !(first && k == 0));
+            tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(tmem_full);
+    }
+    if (warp >= 4) {
+        tc::mbar_wait(tmem_full, 0);
+        tc::tc_fence_after();
+    }
+}
+
 // BM = 128 or 64 weight rows per slab (M = 64: smaller blocks for the small
 // projections; rows 16q..16q+15 sit in TMEM lanes 32q.. of epilogue warp q).
+// Block -> work: classic split-K (a.sk = 0: t -> slab t % nb, split t / nb,
+// S equal splits, split S-1 combines) or stream-K (a.sk = 1: the grid's G
+// blocks take equal contiguous runs of the nb x KB (slab, k-block) units,
+// so any grid size -- e.g. a multiple of the lanes at every quota -- is
+// balanced; a run spans at most two slabs, host-checked).  Either way a
+// slab's partials are summed in ascending k order by its last contributor:
+// the order is a function of (N, K, grid) only, never of the schedule.
 template <int BM, int STAGES>
 __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     constexpr int QR = BM / 4;            // slab rows per epilogue warp
@@ -68,16 +191,34 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     char* base = align1024(c.smem);
     const int nb = a.N / BM;
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
-    const int n_blk = t % nb, s = t / nb;
     const int KB = a.K / kTcBK;
-    const int kb0 = (int)((int64_t)s * KB / a.S), kb1 = (int)((int64_t)(s + 1) * KB / a.S);
+    // pA: the block's first piece; pB (np = 2): the head of the next slab.
+    // A run is at most KB k-blocks long (host-checked), so with two pieces pA
+    // ends its slab (owner) and pB does not (non-owner).
+    GemvPiece pA, pB{};
+    int np = 1;
+    if (a.sk) {
+        const int G = c.gx * c.gy * c.gz;
+        const int64_t U = (int64_t)nb * KB;
+        const int64_t u0 = (int64_t)t * U / G, u1 = (int64_t)(t + 1) * U / G;
+        const int n = (int)(u0 / KB), ka = (int)(u0 % KB);
+        const int kb = (int)min((int64_t)KB, ka + (u1 - u0));
+        const int first = gemv_block_of((int64_t)n * KB, U, G), last = gemv_block_of((int64_t)n * KB + KB - 1, U, G);
+        pA = GemvPiece{n, ka, kb, t - first, last - first + 1, kb == KB};
+        if (u0 + (kb - ka) < u1) {
+            const int lastB = gemv_block_of((int64_t)(n + 1) * KB + KB - 1, U, G);
+            pB = GemvPiece{n + 1, 0, (int)(u1 - (int64_t)(n + 1) * KB), 0, lastB - t + 1, false};
+            np = 2;
+        }
+    } else {
+        const int n = t % nb, s = t / nb;
+        pA = GemvPiece{n, (int)((int64_t)s * KB / a.S), (int)((int64_t)(s + 1) * KB / a.S), s, a.S, s == a.S - 1};
+    }
     uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
     if (dbg && ltid() == 0) dbg[0] = globaltimer();
     BodyCtx cd = c;
     cd.dbg = dbg;
-    tc_mainloop<kGemvBN, STAGES, kTcBK, BM>(base, &a.tmW, &a.tmX, n_blk * BM, 0, kb0, kb1, c.tmem_base, true,
-                                             reinterpret_cast<const char*>(a.w_packed), KB, &cd, nullptr, false,
-                                             (uint32_t)a.l2_pf_kb << 10);
+    gemv_mainloop<BM, STAGES>(base, a, pA, pB, np, c.tmem_base, cd);
     if (ltid() == 128) mark_streamed(c);  // tmem_full: every weight / X load of this block has landed
     wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
@@ -87,54 +228,64 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     const int q = warp & 3;
     const bool active = lane < QR;  // lanes holding a slab row (all of them at BM = 128)
     const int row = q * QR + lane;  // epilogue warps: row within the slab
-    const int n = n_blk * BM + row;
-    // Split-K: split S-1 of each slab is its combiner (claimed after every
-    // other split of every slab: claims follow the logical index, so it never
-    // waits on an unclaimed block).  The other splits store their partial and
-    // arrive (fire-and-forget release); the combiner waits for S-1 arrivals and
-    // sums s = 0..S-1 in order.
-    const bool combiner = a.S == 1 || s == a.S - 1;
-    // RMSNorm scale of the input rows (statistics of an earlier launch): load
-    // it now, its latency hides under the partial exchange
-    if (combiner && a.stats_in && warp >= 4) {
-        float* red = scratch + 128 * 33 + 64;  // [4][32]
-        const float* st = reinterpret_cast<const float*>(a.stats_in);
-        const int p0 = q * a.P_in / 4, p1 = (q + 1) * a.P_in / 4;
-        float ss = 0.f;
-#pragma unroll 8
-        for (int p = p0; p < p1; ++p) ss += __ldcg(st + p * 32 + lane);
-        red[q * 32 + lane] = ss;
-    }
-    float v[32];
-    if (warp >= 4) {
-        uint32_t raw[32];
-        tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16), raw);
-        tc::tmem_ld_wait();
+    // ---- non-owner piece (at most one): fp32 partial out, fire-and-forget
+    // arrival; before the owner piece's wait, so no block ever waits on a
+    // block that is itself waiting
+    const bool has_non = np == 2 || !pA.owner;
+    if (has_non) {
+        const GemvPiece& pn = np == 2 ? pB : pA;
+        const uint32_t col = np == 2 ? 32u : 0u;
+        if (warp >= 4) {
+            uint32_t raw[32];  // the tcgen05.ld is warp-collective; rows past BM (lanes >= QR) unused
+            tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + col, raw);
+            tc::tmem_ld_wait();
+            if (active) {
+                float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.ws) +
+                                                      ((size_t)pn.c * a.N + pn.n * BM + row) * 32);
 #pragma unroll
-        for (int b = 0; b < 32; ++b) v[b] = __uint_as_float(raw[b]);
-    }
-    const bool proceed = combiner;
-    // the combiner's own partial stays on chip: [128 rows][8 float4] in the
-    // (consumed) ring, same element order as a workspace slab
-    float4* own = reinterpret_cast<float4*>(base + kGemvOwnOff);
-    if (a.S > 1) {
-        uint32_t* ctr = reinterpret_cast<uint32_t*>(a.counters) + n_blk;
-        if (!combiner) {
-            if (warp >= 4 && active) {
-                float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.ws) + ((size_t)s * a.N + n) * 32);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                for (int j = 0; j < 8; ++j)
+                    w[j] = make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
+                                       __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3]));
             }
-            body_sync();  // orders the CTA's partial stores before thread 0's release
-            if (ltid() == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
-        } else {
-            if (warp >= 4 && active) {
+        }
+        body_sync();  // orders the CTA's partial stores before thread 0's release
+        if (ltid() == 0)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(reinterpret_cast<uint32_t*>(a.counters) + pn.n)
+                         : "memory");
+    }
+    if (pA.owner) {
+        const int n_blk = pA.n, S = pA.nc;
+        const int n = n_blk * BM + row;
+        // RMSNorm scale of the input rows (statistics of an earlier launch): load
+        // it now, its latency hides under the partial exchange
+        if (a.stats_in && warp >= 4) {
+            float* red = scratch + 128 * 33 + 64;  // [4][32]
+            const float* st = reinterpret_cast<const float*>(a.stats_in);
+            const int p0 = q * a.P_in / 4, p1 = (q + 1) * a.P_in / 4;
+            float ss = 0.f;
+#pragma unroll 8
+            for (int p = p0; p < p1; ++p) ss += __ldcg(st + p * 32 + lane);
+            red[q * 32 + lane] = ss;
+        }
+        if (S > 1) {
+            // the owner's own partial stays on chip: [128 rows][8 float4] in the
+            // (consumed) ring, same element order as a workspace slab
+            float4* own = reinterpret_cast<float4*>(base + kGemvOwnOff);
+            uint32_t* ctr = reinterpret_cast<uint32_t*>(a.counters) + n_blk;
+            if (warp >= 4) {
+                uint32_t raw[32];
+                tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16), raw);
+                tc::tmem_ld_wait();
+                if (active) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) own[row * 8 + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    for (int j = 0; j < 8; ++j)
+                        own[row * 8 + j] = make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
+                                                       __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3]));
+                }
             }
             if (ltid() == 0) {
-                while (ld_acquire_u32(ctr) != (uint32_t)(a.S - 1)) {
-                    if (tenant_failed(c)) break;  // a split that will never be claimed
+                while (ld_acquire_u32(ctr) != (uint32_t)(S - 1)) {
+                    if (tenant_failed(c)) break;  // a contributor that will never be claimed
                     __nanosleep(32);
                 }
                 *ctr = 0;  // at rest for the next launch (which only arrives after this one completes)
@@ -142,8 +293,8 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
             body_sync();
             if (dbg && ltid() == 0) dbg[2] = globaltimer() | (1ull << 63);
             // all 256 threads, coalesced: thread owns float4 f = ltid() + 256 j
-            // of the slab's [128 rows][32] block; partials summed in the fixed
-            // order s = 0..S-1
+            // of the slab's [BM rows][32] block; partials summed in the fixed
+            // order c = 0..S-1 (ascending k), the owner's own last
             const float4* wsb = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.ws) +
                                                                 (size_t)n_blk * BM * 32);
             const size_t sstride4 = (size_t)a.N * 8;
@@ -151,9 +302,9 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
 #pragma unroll
             for (int j = 0; j < FJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 3
-            for (int sp = 0; sp < a.S; ++sp) {
+            for (int sp = 0; sp < S; ++sp) {
                 float4 x[FJ];
-                if (sp < a.S - 1) {
+                if (sp < S - 1) {
 #pragma unroll
                     for (int j = 0; j < FJ; ++j) x[j] = __ldcg(wsb + sp * sstride4 + ltid() + 256 * j);
                 } else {
@@ -179,54 +330,57 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
                 dst[3] = acc[j].w;
             }
             body_sync();
-            if (warp >= 4 && active) {
-#pragma unroll
-                for (int b = 0; b < 32; ++b) v[b] = scratch[row * 33 + b];
-            }
-            body_sync();  // scratch rows are rewritten by the mode epilogues below
             if (dbg && ltid() == 0) dbg[3] = globaltimer();
-        }
-    }
-    if (warp >= 4) {
-        if (proceed) {
-            // RMSNorm of the input rows folded in as a per-row scale (sums
-            // loaded before the partial exchange)
-            if (a.stats_in) {
-                float* red = scratch + 128 * 33 + 64;  // [4][32]
-                epi_sync();
-                if (warp == 4) {
-                    const float ss = ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
-                    rvec[lane] = rsqrtf(ss / (float)a.K + a.eps);
-                }
-                epi_sync();
+        } else if (warp >= 4) {
+            uint32_t raw[32];
+            tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16), raw);
+            tc::tmem_ld_wait();
+            if (active) {
 #pragma unroll
-                for (int b = 0; b < 32; ++b) v[b] *= rvec[b];
+                for (int b = 0; b < 32; ++b) scratch[row * 33 + b] = __uint_as_float(raw[b]);
             }
+        }
+        // from here the slab's accumulators are scratch[row * 33 + b] (fp32,
+        // summed in k order); each mode reads them element by element, so no
+        // 32-register array stays live through the epilogue
+        if (warp >= 4) {
+            // RMSNorm of the input rows folded in as a per-row scale (sums
+            // loaded before the partial exchange); x 1.0 (exact) without it
+            float* red = scratch + 128 * 33 + 64;  // [4][32]
+            epi_sync();
+            if (warp == 4)
+                rvec[lane] = a.stats_in ? rsqrtf((((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane]) /
+                                                     (float)a.K + a.eps)
+                                        : 1.f;
+            epi_sync();
+            const float* acc = scratch + row * 33;
             if (dbg && ltid() == 128) dbg[4] = globaltimer();
             if (a.mode == kGemvStore) {
                 uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
                 if (active) {
-#pragma unroll
-                    for (int b = 0; b < 32; ++b) out[(size_t)b * a.N + n] = f_to_bf16(v[b]);
+#pragma unroll 8
+                    for (int b = 0; b < 32; ++b) out[(size_t)b * a.N + n] = f_to_bf16(acc[b] * rvec[b]);
                 }
             } else if (a.mode == kGemvResid) {
                 const uint16_t* __restrict__ res = reinterpret_cast<const uint16_t*>(a.resid);
                 uint16_t* __restrict__ out = reinterpret_cast<uint16_t*>(a.out);
                 if (active) {
-                    uint16_t rv[32];  // all residual loads in flight before any store
 #pragma unroll
-                    for (int b = 0; b < 32; ++b) rv[b] = __ldcg(res + (size_t)b * a.N + n);
+                    for (int h2 = 0; h2 < 32; h2 += 16) {
+                        uint16_t rv[16];  // 16 residual loads in flight before any store
 #pragma unroll
-                    for (int b = 0; b < 32; ++b) {
-                        const uint16_t hb = f_to_bf16(bf16_to_f(rv[b]) + v[b]);
-                        out[(size_t)b * a.N + n] = hb;
-                        const float hr = bf16_to_f(hb);
-                        scratch[row * 33 + b] = hr * hr;
+                        for (int b = 0; b < 16; ++b) rv[b] = __ldcg(res + (size_t)(h2 + b) * a.N + n);
+#pragma unroll
+                        for (int b = 0; b < 16; ++b) {
+                            const uint16_t hb = f_to_bf16(bf16_to_f(rv[b]) + acc[h2 + b] * rvec[h2 + b]);
+                            out[(size_t)(h2 + b) * a.N + n] = hb;
+                            const float hr = bf16_to_f(hb);
+                            scratch[row * 33 + h2 + b] = hr * hr;
+                        }
                     }
                 }
                 epi_sync();
                 {  // fixed-order sum over the slab's rows: 4 quarter sums, then in order
-                    float* red = scratch + 128 * 33 + 64;
                     float ss = 0.f;
 #pragma unroll 8
                     for (int r = q * QR; r < q * QR + QR; ++r) ss += scratch[r * 33 + lane];
@@ -238,34 +392,31 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
                 }
             } else if (a.mode == kGemvSiluMul && BM == 128) {
                 // slab rows [0,64) are gate features, [64,128) the matching up features
-#pragma unroll
-                for (int b = 0; b < 32; ++b) scratch[row * 33 + b] = v[b];
-                epi_sync();
                 if (row < 64) {
                     uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
                     const int f = n_blk * 64 + row;
                     const int F = a.N / 2;
-#pragma unroll
+#pragma unroll 8
                     for (int b = 0; b < 32; ++b) {
-                        float g = scratch[row * 33 + b], u = scratch[(row + 64) * 33 + b];
-                        float act = g / (1.f + __expf(-g)) * u;
+                        const float g = scratch[row * 33 + b] * rvec[b], u = scratch[(row + 64) * 33 + b] * rvec[b];
+                        const float act = g / (1.f + __expf(-g)) * u;
                         out[(size_t)b * F + f] = f_to_bf16(act);
                     }
                 }
             } else if (a.mode == kGemvQKV && active) {
                 if (n < a.q_dim) {
                     uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
-#pragma unroll
-                    for (int b = 0; b < 32; ++b) out[(size_t)b * a.q_dim + n] = f_to_bf16(v[b]);
+#pragma unroll 8
+                    for (int b = 0; b < 32; ++b) out[(size_t)b * a.q_dim + n] = f_to_bf16(acc[b] * rvec[b]);
                 } else {
                     const bool is_k = n < a.q_dim + a.kv_dim;
                     const int m = n - a.q_dim - (is_k ? 0 : a.kv_dim);
                     const int h = m >> 7, d = m & 127;
                     const int nkv = a.kv_dim >> 7;
                     uint16_t* cache = reinterpret_cast<uint16_t*>(is_k ? a.kcache : a.vcache);
-#pragma unroll
+#pragma unroll 8
                     for (int b = 0; b < 32; ++b)
-                        cache[(((size_t)b * nkv + h) * a.Lmax + a.pos) * 128 + d] = f_to_bf16(v[b]);
+                        cache[(((size_t)b * nkv + h) * a.Lmax + a.pos) * 128 + d] = f_to_bf16(acc[b] * rvec[b]);
                 }
             }
         }

@@ -69,9 +69,21 @@ class DecodeConfig:
     attn_splits: int = 1   # one block per (batch row, kv head): measured best (scripts/block_stats.py ASPLIT sweep)
 
 
+def sk_contributors(nb: int, kb: int, G: int) -> int:
+    """Stream-K GEMV plan (bodies/decode.cuh gemv_body, a.sk = 1): block t of
+    G takes units [t U / G, (t+1) U / G) of the U = nb * kb (slab, k-block)
+    units.  Returns the most blocks any slab is split across; a run must not
+    exceed one slab's k-blocks (the body handles two pieces per block)."""
+    U = nb * kb
+    if not (1 <= G <= U) or -(-U // G) > kb:
+        raise ValueError(f"stream-K grid {G} invalid for {nb} slabs x {kb} k-blocks")
+    block_of = lambda u: ((u + 1) * G - 1) // U
+    return max(block_of(n * kb + kb - 1) - block_of(n * kb) + 1 for n in range(nb))
+
+
 class DecodeModel:
     def __init__(self, cfg: DecodeConfig = DecodeConfig(), device="cuda", seed: int = 0, split_override: str = "",
-                 bm_override: str = "", pf_override: str = ""):
+                 bm_override: str = "", pf_override: str = "", g_override: str = ""):
         assert cfg.batch == 32 and cfg.d == cfg.n_q * 128 and cfg.n_q == 4 * cfg.n_kv
         self.cfg = cfg
         c = cfg
@@ -121,6 +133,14 @@ class DecodeModel:
             for kv in split_override.split(","):
                 k, v = kv.split(":")
                 self.S[k] = int(v)
+        # stream-K grids (bodies/decode.cuh gemv_body, a.sk): G equal runs of
+        # (slab, k-block) units instead of nb x S blocks, so the grid can be a
+        # multiple of the worker lanes at both the full GPU (296) and the
+        # decode tenant's 1/2 tier (148); 0 = split-K S
+        self.G = {"qkv": 0, "o": 0, "gu": 0, "down": 0, "lm": 0}
+        for kv in filter(None, (g_override or os.environ.get("DS_GEMV_G", "")).split(",")):
+            k, v = kv.split(":")
+            self.G[k] = int(v)
         # weight rows per slab (M of the swap-AB MMA): 128, or 64 for the small
         # projections (gate_up's SiLU pairing needs 128-row slabs)
         self.BM = {"qkv": 128, "o": 128, "gu": 128, "down": 128, "lm": 128}
@@ -138,8 +158,10 @@ class DecodeModel:
         for kv in filter(None, (pf_override or os.environ.get("DS_L2PF", "")).split(",")):
             k, v = kv.split(":")
             self.PF[k] = int(v)
-        ws_elems = max(self.S["qkv"] * self.qkv_n, self.S["o"] * c.d, self.S["gu"] * 2 * c.ffn,
-                       self.S["down"] * c.d, self.S["lm"] * c.vocab) * 32
+        shapes = {"qkv": (self.qkv_n, c.d), "o": (c.d, c.d), "gu": (2 * c.ffn, c.d), "down": (c.d, c.ffn),
+                  "lm": (c.vocab, c.d)}
+        ws_elems = max((sk_contributors(N // self.BM[k], K // 64, self.G[k]) if self.G[k] else self.S[k]) * N
+                       for k, (N, K) in shapes.items()) * 32
         self.ws = torch.zeros(ws_elems, device=device)
         self.counters = torch.zeros(max(c.vocab, 2 * c.ffn) // 128 + 1, device=device, dtype=torch.int32)
         self.attn_ws = torch.zeros(256 * c.attn_splits * 4 * 130, device=device)
@@ -150,7 +172,7 @@ class DecodeModel:
 
     # ---- launch records ----
     def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None, bm=128,
-              pf=0):
+              pf=0, G=0):
         Wp = pack_sw128(W, bm)
         self._packed.append(Wp)
         tmW = _abi.tensor_map_bf16(W.data_ptr(), N, K, bm)
@@ -173,6 +195,10 @@ class DecodeModel:
         a.w_packed = Wp.data_ptr()
         a.bm = bm
         a.l2_pf_kb = pf
+        if G:
+            sk_contributors(N // bm, K // 64, G)  # validates the plan
+            a.sk = 1
+            return a, (G, 1, 1)
         return a, ((N // bm) * S, 1, 1)
 
     def _build_args(self):
@@ -187,7 +213,8 @@ class DecodeModel:
             hin, hout = self.H[l % 2], self.H[(l + 1) % 2]
             st_in, p_in = (self.st0, 1) if l == 0 else (self.st_h, c.d // self.BM["down"])
             a, g = self._gemv(self.Wqkv[l], hin, self.qkv_n, c.d, self.S["qkv"], _abi.GEMV_QKV, self.q,
-                              stats_in=st_in, P_in=p_in, l=l, bm=self.BM["qkv"], pf=self.PF["qkv"])
+                              stats_in=st_in, P_in=p_in, l=l, bm=self.BM["qkv"], pf=self.PF["qkv"],
+                              G=self.G["qkv"])
             self.records.append((f"decode/qkv", _abi.BODY_GEMV_BF16, g, a, self.qkv_n * c.d * 2))
             rows = 32 * c.n_kv * self.Lmax
             at = _abi.AttnArgs(_abi.tensor_map_kv(self.kc[l].data_ptr(), rows),
@@ -198,17 +225,19 @@ class DecodeModel:
             self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,
                                  2 * 32 * c.n_kv * c.L * 128 * 2))
             a, g = self._gemv(self.Wo[l], self.attn, c.d, c.d, self.S["o"], _abi.GEMV_RESID, self.h_mid, resid=hin,
-                              stats_out=self.st_mid, bm=self.BM["o"], pf=self.PF["o"])
+                              stats_out=self.st_mid, bm=self.BM["o"], pf=self.PF["o"], G=self.G["o"])
             self.records.append(("decode/o", _abi.BODY_GEMV_BF16, g, a, c.d * c.d * 2))
             a, g = self._gemv(self.Wgu[l], self.h_mid, 2 * c.ffn, c.d, self.S["gu"], _abi.GEMV_SILU_MUL, self.act,
-                              stats_in=self.st_mid, P_in=c.d // self.BM["o"], pf=self.PF["gu"])
+                              stats_in=self.st_mid, P_in=c.d // self.BM["o"], pf=self.PF["gu"], G=self.G["gu"])
             self.records.append(("decode/gate_up", _abi.BODY_GEMV_BF16, g, a, 2 * c.ffn * c.d * 2))
             a, g = self._gemv(self.Wd[l], self.act, c.d, c.ffn, self.S["down"], _abi.GEMV_RESID, hout,
-                              resid=self.h_mid, stats_out=self.st_h, bm=self.BM["down"], pf=self.PF["down"])
+                              resid=self.h_mid, stats_out=self.st_h, bm=self.BM["down"], pf=self.PF["down"],
+                              G=self.G["down"])
             self.records.append(("decode/down", _abi.BODY_GEMV_BF16, g, a, c.d * c.ffn * 2))
         hfin = self.H[c.layers % 2]
         a, g = self._gemv(self.lm, hfin, c.vocab, c.d, self.S["lm"], _abi.GEMV_STORE, self.logits,
-                          stats_in=self.st_h, P_in=c.d // self.BM["down"], bm=self.BM["lm"], pf=self.PF["lm"])
+                          stats_in=self.st_h, P_in=c.d // self.BM["down"], bm=self.BM["lm"], pf=self.PF["lm"],
+                          G=self.G["lm"])
         self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
         chunks = max(1, min(4, c.vocab // 2048))  # 128 blocks: one wave; every block pays a claim + ticket
         am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), self.amax_ws.data_ptr(),

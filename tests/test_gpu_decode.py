@@ -17,12 +17,18 @@ from paper_2603_15042_b200.tenants import DecodeConfig, DecodeModel, pick_split
 pytestmark = pytest.mark.gpu
 
 
-BM_VARIANTS = ["", "qkv:64,o:64,down:64,lm:64"]
+# (row slabs, GEMV grids): split-K defaults, 64-row slabs, and stream-K
+# grids at the full GPU's and the 1/2 tier's lane counts
+BM_VARIANTS = ["", "qkv:64,o:64,down:64,lm:64", "sk296", "qkv:64,o:64,down:64,lm:64/sk148"]
+SK = {"sk296": "qkv:296,o:296,gu:296,down:296", "sk148": "qkv:148,o:148,gu:296,down:148"}
 
 
 def small_model(bms=""):
     cfg = DecodeConfig(layers=2, vocab=2048, L=96, attn_splits=2)
-    return DecodeModel(cfg, seed=5, bm_override=bms)
+    bm, _, g = bms.rpartition("/") if "/" in bms else (bms, "", "")
+    if bm.startswith("sk"):
+        bm, g = "", bm
+    return DecodeModel(cfg, seed=5, bm_override=bm, g_override=SK.get(g, ""))
 
 
 @pytest.mark.parametrize("bms", BM_VARIANTS)
