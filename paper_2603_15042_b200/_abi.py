@@ -33,6 +33,7 @@ BODY_ALLREDUCE_P2P = 12
 BODY_CHECKSUM = 13
 MAX_DP_RANKS = 8
 DP_SLOTS = 64
+DP_MAX_CHUNKS = 4096  # collective.cuh kDpMaxChunks
 
 LATENCY_CRITICAL, BEST_EFFORT = 0, 1
 PREFILL, DECODE, TRAINING, OTHER = 0, 1, 2, 3
@@ -363,6 +364,7 @@ REQ_INFERENCE, REQ_TRAINING = 0, 1
 class AllreduceArgs(ctypes.Structure):
     """csrc/bodies/collective.cuh"""
     _fields_ = [("grad", ctypes.c_uint64 * 8), ("flags", ctypes.c_uint64 * 8), ("out", ctypes.c_uint64),
+                ("outs", ctypes.c_uint64 * 8),
                 ("n", ctypes.c_int64), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("chunk", ctypes.c_int32), ("pad", ctypes.c_int32)]
 

@@ -1,6 +1,7 @@
 """Data-parallel training tenant: gradient all-reduce over NVLink peer memory
-as an executor body (csrc/bodies/collective.cuh), so the collective runs
-under the SM arbiter on the tenant's own quota.
+as an executor body (csrc/bodies/collective.cuh: reduce-scatter + all-gather
+in one launch, rank-ordered fp32 sums), so the collective runs under the SM
+arbiter on the tenant's own quota.
 
 One process per GPU: each rank allocates its gradient / output / flag
 buffers with ``ds_ipc_alloc``, the 64-byte IPC handles travel over the host
@@ -18,7 +19,7 @@ from typing import Callable, List, Sequence
 from . import _abi
 from ._abi import check, lib
 
-FLAG_BYTES = (2 * _abi.DP_SLOTS + 1) * 8  # ready, done, abort
+FLAG_BYTES = (2 * _abi.DP_SLOTS + 8 + _abi.DP_MAX_CHUNKS) * 8  # ready, done, abort (+pad), chunk epochs
 
 
 def _alloc(device: int, nbytes: int) -> int:
@@ -44,17 +45,33 @@ def peer_table(own: int, rank: int, handles: Sequence[bytes], open_fn: Callable[
     return [own if r == rank else open_fn(h) for r, h in enumerate(handles)]
 
 
-def make_args(grads: Sequence[int], flags: Sequence[int], out: int, n: int, rank: int,
+def make_args(grads: Sequence[int], flags: Sequence[int], outs: Sequence[int], n: int, rank: int,
               chunk: int = 1 << 16) -> _abi.AllreduceArgs:
+    """Rank `rank`'s arguments: every rank's gradient, flag and output
+    buffers in rank order (own entries local, peers' opened over IPC)."""
     world = len(grads)
-    if world > _abi.MAX_DP_RANKS or n % 8 or chunk % 8:
-        raise _abi.DsError(10, "DP all-reduce: <= 8 ranks, n and chunk multiples of 8")
+    if world > _abi.MAX_DP_RANKS or n % 8 or chunk % 8 or len(outs) != world or len(flags) != world:
+        raise _abi.DsError(10, "DP all-reduce: <= 8 ranks, n and chunk multiples of 8, one buffer per rank")
+    if (n + chunk - 1) // chunk > _abi.DP_MAX_CHUNKS:
+        raise _abi.DsError(10, f"DP all-reduce: more than {_abi.DP_MAX_CHUNKS} chunks")
     a = _abi.AllreduceArgs()
     for r in range(world):
         a.grad[r] = grads[r]
         a.flags[r] = flags[r]
-    a.out, a.n, a.world, a.rank, a.chunk = out, n, world, rank, chunk
+        a.outs[r] = outs[r]
+    a.out, a.n, a.world, a.rank, a.chunk = outs[rank], n, world, rank, chunk
     return a
+
+
+def shard_bounds(rank: int, G: int, world: int) -> tuple:
+    """Chunks [lo, hi) rank `rank` reduces (collective.cuh: lo(r) = r G / W)."""
+    return rank * G // world, (rank + 1) * G // world
+
+
+def block_chunk(rank: int, j: int, G: int, world: int) -> int:
+    """Chunk that logical block j of rank `rank` handles: its own shard
+    first in claim order, then the others' (collective.cuh)."""
+    return (shard_bounds(rank, G, world)[0] + j) % G
 
 
 def grid_for(n: int, chunk: int = 1 << 16):
@@ -69,11 +86,12 @@ class DpGroup:
         self.grad = _alloc(device, 2 * n)
         self.out = _alloc(device, 2 * n)
         self.flags = _alloc(device, FLAG_BYTES)
-        hs = gather_fn((ipc_handle(self.grad), ipc_handle(self.flags)))
+        hs = gather_fn((ipc_handle(self.grad), ipc_handle(self.flags), ipc_handle(self.out)))
         opener = lambda h: ipc_open(device, h)  # noqa: E731
         self.grads = peer_table(self.grad, rank, [h[0] for h in hs], opener)
         self.flag_ptrs = peer_table(self.flags, rank, [h[1] for h in hs], opener)
-        self.args = make_args(self.grads, self.flag_ptrs, self.out, n, rank, chunk)
+        self.outs = peer_table(self.out, rank, [h[2] for h in hs], opener)
+        self.args = make_args(self.grads, self.flag_ptrs, self.outs, n, rank, chunk)
 
     def abort(self):
         """Release this rank's blocks still waiting for a peer (shutdown)."""
@@ -90,5 +108,5 @@ def virtual_group(device: int, n: int, world: int, chunk: int = 1 << 16):
     grads = [_alloc(device, 2 * n) for _ in range(world)]
     outs = [_alloc(device, 2 * n) for _ in range(world)]
     flags = [_alloc(device, FLAG_BYTES) for _ in range(world)]
-    args = [make_args(grads, flags, outs[r], n, r, chunk) for r in range(world)]
+    args = [make_args(grads, flags, outs, n, r, chunk) for r in range(world)]
     return grads, outs, flags, args

@@ -7,7 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "profiles")
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r1"
 ALG = {"attn": 2 * 32 * 8 * 1024 * 128 * 2, "gate_up": 2 * 14336 * 4096 * 2, "lm_head": 128256 * 4096 * 2,
-       "qkv": 6144 * 4096 * 2, "down": 4096 * 14336 * 2, "gemm": 3 * 8192 * 8192 * 2}
+       "qkv": 6144 * 4096 * 2, "o": 4096 * 4096 * 2, "down": 4096 * 14336 * 2, "gemm": 3 * 8192 * 8192 * 2}
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",

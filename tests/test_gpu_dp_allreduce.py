@@ -1,8 +1,9 @@
-"""DP training tenant's gradient all-reduce body (csrc/bodies/collective.cuh)
-on W virtual ranks = W tenants of one domain on one B200 (the multi-GPU
-path differs only in where the peer pointers come from).  Bit-exact against
-a rank-ordered fp32 sum rounded once to bf16, identical on every rank,
-across epochs (flag-slot reuse) and with ranks arriving late."""
+"""DP training tenant's gradient all-reduce body (csrc/bodies/collective.cuh,
+reduce-scatter + all-gather) on W virtual ranks = W tenants of one domain on
+one B200 (the multi-GPU path differs only in where the peer pointers come
+from).  Bit-exact against a rank-ordered fp32 sum rounded once to bf16,
+identical on every rank, across epochs (flag-slot reuse), with ranks arriving
+late, and with fewer chunks than ranks (ranks owning no chunk)."""
 import time
 
 import numpy as np
@@ -23,7 +24,7 @@ def expected(grads):
 
 
 @pytest.mark.parametrize("world,n,chunk", [(4, 1 << 20, 1 << 16), (3, 1000000, 1 << 15), (8, 65536, 8192),
-                                           (1, 4096, 1024)])
+                                           (1, 4096, 1024), (8, 24576, 8192)])
 def test_allreduce_virtual_ranks_bit_exact(world, n, chunk):
     g = torch.Generator(device="cuda").manual_seed(world)
     flags = [torch.zeros(dp.FLAG_BYTES, dtype=torch.uint8, device="cuda") for _ in range(world)]
@@ -43,7 +44,7 @@ def test_allreduce_virtual_ranks_bit_exact(world, n, chunk):
             kids = []
             for r in range(world):
                 a = dp.make_args([x.data_ptr() for x in grads[epoch]], [f.data_ptr() for f in flags],
-                                 outs[epoch][r].data_ptr(), n, r, chunk)
+                                 [o.data_ptr() for o in outs[epoch]], n, r, chunk)
                 kids.append(dom.kernel("dp/allreduce", _abi.BODY_ALLREDUCE_P2P, dp.grid_for(n, chunk), a,
                                        phase=_abi.TRAINING))
             seqs = []
