@@ -197,6 +197,10 @@ class Colocation:
         self.t_dec = self.dom.tenant("decode", _abi.LATENCY_CRITICAL)
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
         self.dec_kernels = self.model.register(self.dom)
+        # the step as TPOT-First runs it on its 1/2 tier: gate_up as two-slab
+        # blocks, one wave on 148 worker lanes (bit-identical outputs; the
+        # full-GPU runs — solo, time slicing — keep the one-slab blocks)
+        self.dec_kernels_half = self.model.register_variant(self.dom, self.dec_kernels, "gu_pair")
         self.gemm_kernel = self.train.register(self.dom)
         # parity evidence at full size: a per-launch checksum of the decode
         # step's logits and of the training GEMM's C, appended to the records
@@ -396,7 +400,9 @@ class Colocation:
         tpot_slo = int(self.slo_x * step_ns)
         ttft_slo = int(2 * self.slo_x * step_ns)
         period = int(2 * self.T * step_ns)  # decode busy ~50% of the time when solo
-        dec_kernels = self.dec_kernels + ([self.k_ck_logits] if pin else [])
+        half = policy == "tpot-first" and self.decode_sat <= Fraction(1, 2) and os.environ.get("DS_GU_PAIR", "1") != "0"
+        base = self.dec_kernels_half if half else self.dec_kernels
+        dec_kernels = base + ([self.k_ck_logits] if pin else [])
         trn_kernels = [self.gemm_kernel] + ([self.k_ck_C] if pin else [])
         self._cur_eng = eng
         eng.start()

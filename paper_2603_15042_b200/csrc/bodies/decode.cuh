@@ -45,7 +45,9 @@ struct GemvArgs {
                         // the dependency resolves (0 = ring only)
     int32_t sk;         // 1: stream-K over the logical grid (equal runs of (slab, k-block) units, <= 2 slabs
                         // per block); 0: split-K S with grid nb * S
-    int32_t pad;
+    int32_t pair;       // kGemvSiluMul only (whose weights always interleave gate/up rows: 2i gate, 2i+1 up
+                        // of feature i): 1 = two whole slabs per block (grid nb / 2), slab 0's epilogue
+                        // overlapping slab 1's stream
 };
 
 constexpr int kGemvBN = 32;
@@ -87,7 +89,7 @@ __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, con
     using L = TcSmem<kGemvBN, STAGES, kTcBK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_full = empty + STAGES;  // [2]: per piece in pair mode, else [0] for the whole block
     const int warp = ltid() >> 5, lane = ltid() & 31;
     const int KB = a.K / kTcBK;
     const char* a_packed = reinterpret_cast<const char*>(a.w_packed);
@@ -96,7 +98,8 @@ __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, con
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
         }
-        tc::mbar_init(tmem_full, 1);
+        tc::mbar_init(&tmem_full[0], 1);
+        tc::mbar_init(&tmem_full[1], 1);
         tc::fence_mbar_init();
     }
     body_sync();
@@ -166,12 +169,45 @@ __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, con
             for (int k = 0; k < kTcBK / 16; ++k)
                 tc::mma_bf16(tmem_base + 32 * p, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, !(first && k == 0));
             tc::mma_commit(&empty[s]);
+            if (a.pair && i == n0 - 1) tc::mma_commit(&tmem_full[0]);  // slab 0's accumulator is final
         }
-        tc::mma_commit(tmem_full);
+        tc::mma_commit(&tmem_full[a.pair ? 1 : 0]);
     }
-    if (warp >= 4) {
+    if (warp >= 4 && !a.pair) {
         tc::mbar_wait(tmem_full, 0);
         tc::tc_fence_after();
+    }
+}
+
+// Pair mode (gate_up): SiLU(gate) * up of one slab straight from TMEM.
+// Interleaved rows: TMEM lane 2i holds gate feature i of the slab, 2i+1 its
+// up partner, so the pair meets by one shuffle; the even lane writes batch
+// rows 0-15, the odd lane 16-31.  rvec: the inputs' RMSNorm scales.
+__device__ __forceinline__ void gemv_silu_pair_epilogue(const BodyCtx& c, const GemvArgs& a, int slab, uint32_t col,
+                                                        const float* rvec) {
+    const int q = (ltid() >> 5) & 3, lane = ltid() & 31;
+    uint32_t raw[32];
+    tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + col, raw);
+    tc::tmem_ld_wait();
+    const bool odd = lane & 1;
+    float mine[16], other[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        // even lane keeps its b < 16 and sends b >= 16; odd lane the reverse
+        const float keep = __uint_as_float(raw[odd ? b + 16 : b]);
+        const float send = __uint_as_float(raw[odd ? b : b + 16]);
+        other[b] = __shfl_xor_sync(0xffffffffu, send, 1);
+        mine[b] = keep;
+    }
+    uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
+    const int F = a.N / 2;
+    const int f = slab * 64 + q * 16 + (lane >> 1);
+    const int b0 = odd ? 16 : 0;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        const float g = (odd ? other[b] : mine[b]) * rvec[b0 + b];
+        const float u = (odd ? mine[b] : other[b]) * rvec[b0 + b];
+        out[(size_t)(b0 + b) * F + f] = f_to_bf16(g / (1.f + __expf(-g)) * u);
     }
 }
 
@@ -210,6 +246,10 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
             pB = GemvPiece{n + 1, 0, (int)(u1 - (int64_t)(n + 1) * KB), 0, lastB - t + 1, false};
             np = 2;
         }
+    } else if (a.pair) {
+        pA = GemvPiece{2 * t, 0, KB, 0, 1, true};
+        pB = GemvPiece{2 * t + 1, 0, KB, 0, 1, true};
+        np = 2;
     } else {
         const int n = t % nb, s = t / nb;
         pA = GemvPiece{n, (int)((int64_t)s * KB / a.S), (int)((int64_t)(s + 1) * KB / a.S), s, a.S, s == a.S - 1};
@@ -219,6 +259,44 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     BodyCtx cd = c;
     cd.dbg = dbg;
     gemv_mainloop<BM, STAGES>(base, a, pA, pB, np, c.tmem_base, cd);
+    if (a.pair) {
+        // two whole slabs, no exchange: the epilogue warps finish slab 0 while
+        // the ring streams slab 1 (their scratch is the barrier block's tail,
+        // not the ring)
+        using L = TcSmem<kGemvBN, STAGES, kTcBK, BM>;
+        uint64_t* tmem_full = reinterpret_cast<uint64_t*>(base + L::kBarOff) + 2 * STAGES;
+        float* red = reinterpret_cast<float*>(base + L::kBarOff + 256);  // [4][32]
+        float* rv = red + 128;                                            // [32]
+        const int warp = ltid() >> 5, lane = ltid() & 31;
+        if (warp >= 4) {
+            const int q = warp & 3;
+            if (ltid() == 128) wait_prev(c);  // acquire for the statistics of earlier launches
+            epi_sync();
+            float ss = 0.f;
+            if (a.stats_in) {
+                const float* st = reinterpret_cast<const float*>(a.stats_in);
+#pragma unroll 8
+                for (int p = q * a.P_in / 4; p < (q + 1) * a.P_in / 4; ++p) ss += __ldcg(st + p * 32 + lane);
+            }
+            red[q * 32 + lane] = ss;
+            epi_sync();
+            if (warp == 4)
+                rv[lane] = a.stats_in ? rsqrtf((((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane]) /
+                                                   (float)a.K + a.eps)
+                                      : 1.f;
+            epi_sync();
+            tc::mbar_wait(&tmem_full[0], 0);
+            tc::tc_fence_after();
+            gemv_silu_pair_epilogue(c, a, pA.n, 0u, rv);
+            tc::mbar_wait(&tmem_full[1], 0);
+            tc::tc_fence_after();
+            if (ltid() == 128) mark_streamed(c);  // every weight / X load of this block has landed
+            gemv_silu_pair_epilogue(c, a, pB.n, 32u, rv);
+        }
+        tc_teardown<kGemvBN, STAGES, kTcBK, BM>(base);
+        if (ltid() == 0) tc::mbar_inval(tmem_full + 1);
+        return;
+    }
     if (ltid() == 128) mark_streamed(c);  // tmem_full: every weight / X load of this block has landed
     wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
@@ -391,14 +469,14 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
                             ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
                 }
             } else if (a.mode == kGemvSiluMul && BM == 128) {
-                // slab rows [0,64) are gate features, [64,128) the matching up features
-                if (row < 64) {
+                // interleaved slab rows: 2i gate feature i, 2i+1 its up partner
+                if (!(row & 1)) {
                     uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
-                    const int f = n_blk * 64 + row;
+                    const int f = n_blk * 64 + (row >> 1);
                     const int F = a.N / 2;
 #pragma unroll 8
                     for (int b = 0; b < 32; ++b) {
-                        const float g = scratch[row * 33 + b] * rvec[b], u = scratch[(row + 64) * 33 + b] * rvec[b];
+                        const float g = scratch[row * 33 + b] * rvec[b], u = scratch[(row + 1) * 33 + b] * rvec[b];
                         const float act = g / (1.f + __expf(-g)) * u;
                         out[(size_t)b * F + f] = f_to_bf16(act);
                     }
@@ -423,6 +501,7 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     }
     if (dbg && ltid() == 128) dbg[5] = globaltimer();
     tc_teardown<kGemvBN, STAGES, kTcBK, BM>(base);
+    if (ltid() == 0) tc::mbar_inval(reinterpret_cast<uint64_t*>(base + TcSmem<kGemvBN, STAGES, kTcBK, BM>::kBarOff) + 2 * STAGES + 1);
     if (dbg && ltid() == 0) dbg[6] = globaltimer();
 }
 

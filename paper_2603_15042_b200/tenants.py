@@ -173,6 +173,12 @@ class DecodeModel:
     # ---- launch records ----
     def _gemv(self, W, X, N, K, S, mode, out, resid=None, stats_in=None, P_in=0, stats_out=None, l=None, bm=128,
               pf=0, G=0):
+        if mode == _abi.GEMV_SILU_MUL:
+            # slabs [64 gate | 64 up] -> rows interleaved gate/up (2i, 2i+1):
+            # the SiLU pairing then stays inside a warp (bodies/decode.cuh)
+            assert bm == 128 and (N // bm) % 2 == 0
+            W = W.view(N // bm, 2, 64, K).transpose(1, 2).reshape(N, K)
+            self._packed.append(W)  # keeps the permuted copy (tmW's base) alive
         Wp = pack_sw128(W, bm)
         self._packed.append(Wp)
         tmW = _abi.tensor_map_bf16(W.data_ptr(), N, K, bm)
@@ -204,6 +210,8 @@ class DecodeModel:
     def _build_args(self):
         c = self.cfg
         self.records = []  # (semantic_id, body, grid, args, bytes)
+        # alternative records of the same step, by variant name: {record index: record}
+        self.variant_records = {}
         self._packed = []  # pre-packed weights (the copies the GEMV bodies stream)
         # token gather + the input rows' RMS statistics in one launch
         ea = _abi.EmbedArgs(self.embed.data_ptr(), self.tokens.data_ptr(), self.H[0].data_ptr(), c.d, c.vocab,
@@ -230,6 +238,13 @@ class DecodeModel:
             a, g = self._gemv(self.Wgu[l], self.h_mid, 2 * c.ffn, c.d, self.S["gu"], _abi.GEMV_SILU_MUL, self.act,
                               stats_in=self.st_mid, P_in=c.d // self.BM["o"], pf=self.PF["gu"], G=self.G["gu"])
             self.records.append(("decode/gate_up", _abi.BODY_GEMV_BF16, g, a, 2 * c.ffn * c.d * 2))
+            if not self.G["gu"] and self.S["gu"] == 1:
+                # the same projection as two-slab blocks (bit-identical: every
+                # slab is still one block's k-ordered accumulation)
+                ap = _abi.GemvArgs.from_buffer_copy(a)
+                ap.pair = 1
+                self.variant_records.setdefault("gu_pair", {})[len(self.records) - 1] = (
+                    "decode/gate_up", _abi.BODY_GEMV_BF16, (g[0] // 2, 1, 1), ap, 2 * c.ffn * c.d * 2)
             a, g = self._gemv(self.Wd[l], self.act, c.d, c.ffn, self.S["down"], _abi.GEMV_RESID, hout,
                               resid=self.h_mid, stats_out=self.st_h, bm=self.BM["down"], pf=self.PF["down"],
                               G=self.G["down"])
@@ -256,6 +271,17 @@ class DecodeModel:
 
     def register(self, dom, phase=_abi.DECODE) -> List[int]:
         return [dom.kernel(sid, body, grid, args, phase=phase) for sid, body, grid, args, _ in self.records]
+
+    def register_variant(self, dom, ids: List[int], name: str = "gu_pair", phase=_abi.DECODE) -> List[int]:
+        """The step's kernel ids with variant `name`'s records registered in
+        place of the base ones (other ids shared).  "gu_pair": gate_up as 112
+        two-slab blocks — one wave at the decode tenant's 1/2 tier (148
+        worker lanes) where the 224 one-slab blocks need two; outputs are
+        bit-identical to the base step."""
+        out = list(ids)
+        for i, (sid, body, grid, args, _) in self.variant_records.get(name, {}).items():
+            out[i] = dom.kernel(sid, body, grid, args, phase=phase)
+        return out
 
     def prefill_records(self, prompt_tokens: int = 256):
         """A prompt's prefill on the same weights: per layer the four

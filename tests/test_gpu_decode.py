@@ -97,8 +97,9 @@ def test_full_decode_step_matches_torch_fp32_and_coroutine_bit_exact():
     restatement with bf16 rounding points: |err| <= 0.05 (|ref| + 1), mean
     <= 5e-3 (same tolerance as the 2-layer case; bf16 storage of every
     intermediate).  Then the same step as a coroutine on a quarter of the SMs
-    with a mid-step change to all of them is bit-identical to the solo step,
-    and the device checksum body agrees with the host checksum."""
+    with a mid-step change to all of them -- its gate_up projections as the
+    two-slab-block variant -- is bit-identical to the solo step, and the
+    device checksum body agrees with the host checksum."""
     from paper_2603_15042_b200.tenants import OutputChecksum
     m = DecodeModel(DecodeConfig(), seed=7)
     tok0 = m.tokens.clone()
@@ -118,7 +119,9 @@ def test_full_decode_step_matches_torch_fp32_and_coroutine_bit_exact():
     torch.cuda.synchronize()
     with Domain(0, tiers=[Fraction(1)], block_log_capacity=0) as dom:
         t = dom.tenant("decode", _abi.LATENCY_CRITICAL)
-        kids = m.register(dom) + [ck.register(dom, "decode/logits_checksum")]
+        # the co-located variant (gate_up as two-slab blocks) against the
+        # plain split-K solo step: bit-identical by construction
+        kids = m.register_variant(dom, m.register(dom), "gu_pair") + [ck.register(dom, "decode/logits_checksum")]
         dom.start()
         dom.quota_set(dom.mask(t, 0, dom.num_sms // 4))
         dom.quota_at_claim(t, 80, 0, dom.mask(t, 0, dom.num_sms))
@@ -129,3 +132,35 @@ def test_full_decode_step_matches_torch_fp32_and_coroutine_bit_exact():
         slots = ck.slots()
     assert torch.equal(m.logits.view(torch.int16), solo_logits.view(torch.int16))
     assert ck.of_seq(slots, last) == OutputChecksum.host(solo_logits)
+
+
+def test_gate_up_pair_variant_bit_exact_vs_solo():
+    """gate_up as 112 two-slab blocks (register_variant "gu_pair") under mid-step
+    quota changes equals the 224-block solo step bit for bit."""
+    m = small_model()
+    assert "gu_pair" in m.variant_records
+    tok0 = m.tokens.clone()
+    kc0 = [k.clone() for k in m.kc]
+    vc0 = [v.clone() for v in m.vc]
+    m.solo_step()
+    torch.cuda.synchronize()
+    solo_logits, solo_act = m.logits.clone(), m.act.clone()
+    m.tokens.copy_(tok0)
+    for l in range(m.cfg.layers):
+        m.kc[l].copy_(kc0[l])
+        m.vc[l].copy_(vc0[l])
+    m.logits.zero_()
+    m.act.zero_()
+    torch.cuda.synchronize()
+    with Domain(0, tiers=[Fraction(1)], block_log_capacity=0) as dom:
+        t = dom.tenant("decode", _abi.LATENCY_CRITICAL)
+        kids = m.register_variant(dom, m.register(dom), "gu_pair")
+        dom.start()
+        dom.quota_set(dom.mask(t, 0, 74))
+        dom.quota_at_claim(t, 4, 30, dom.mask(t, 10, 50))
+        last = None
+        for k in kids:
+            last = dom.launch(t, k)
+        dom.wait(t, last)
+    assert torch.equal(m.act.view(torch.int16), solo_act.view(torch.int16))
+    assert torch.equal(m.logits.view(torch.int16), solo_logits.view(torch.int16))
