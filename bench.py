@@ -1047,6 +1047,10 @@ def gpu_arm(args, rank, world):
                  "gemm_tflops": round(gemm_tf, 1)},
         "bit_exact_vs_solo": exact["ok"],
         "bit_exact_detail": exact,
+        "tpot_distribution_ms": {name: {"p50": round(nearest_rank(v, 50), 4), "p90": round(nearest_rank(v, 90), 4),
+                                        "p99": round(nearest_rank(v, 99), 4), "mean": round(statistics.mean(v), 4),
+                                        "n": len(v)}
+                                 for name, v in (("tpot_first", sp["tpot_ms"]), ("temporal", tm["tpot_ms"]))},
         "engine_counters": sp["counters"],
         "ledger": {"tpot_first": sp["ledger"], "temporal": tm["ledger"],
                    "what": "OverheadLedger from device %globaltimer stamps summed over worker lanes (ns): "
@@ -1139,7 +1143,10 @@ def config1_leg(dev):
     exact = bool(np.array_equal(C_co.cpu().numpy().view(np.uint32), C_solo.cpu().numpy().view(np.uint32)))
     co_ms = (c.t_end - c.t_first_claim) / 1e6
     flop = 2.0 * M * N * K
-    ffma_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s, fp32 FFMA at max clock
+    try:  # measured on this device, no executor resident
+        ffma_peak, ffma_src = _abi.measure_ffma_peak(dev), "measured: ds_measure_ffma_peak (8 independent fp32 fma chains per thread, 4 x 256 threads per SM, CUDA events)"
+    except Exception as e:  # noqa: BLE001
+        ffma_peak, ffma_src = 148 * 128 * 2 * 1.965e9 / 1e12, f"nominal 148 SMs x 128 lanes x 2 x 1965 MHz ({e})"
     ach = flop / (min(solo_ms, co_ms) * 1e-3) / 1e12
     return {"workload": "config 1: SGEMM 1024^3 fp32 (64x64 logical tiles, 256 blocks) as one coroutine, quota "
                         "100% -> 25% at 30% of claimed blocks -> 100% at 60%",
@@ -1147,7 +1154,7 @@ def config1_leg(dev):
             "solo_ms": round(solo_ms, 4), "coroutine_ms": round(co_ms, 4), "ctl_switch_records": switches,
             "roofline": {"bound": "fp32 FFMA", "achieved": round(ach, 2), "peak": round(ffma_peak, 1),
                          "unit": "TFLOP/s", "frac": round(ach / ffma_peak, 4),
-                         "peak_source": "148 SMs x 128 FFMA lanes x 2 x 1965 MHz (nominal; no measured fp32 peak)"}}
+                         "peak_source": ffma_src}}
 
 
 def config3_leg(dev):

@@ -286,6 +286,9 @@ int ds_globaltimer(ds_domain* dom, uint64_t* ns); /* device %globaltimer now (pr
 int ds_debug_dump(ds_domain* dom, char* out, int64_t cap); /* text snapshot of device control state */
 /* host write of the control word -> device install acknowledged in host memory, n samples (ns) */
 int ds_ctl_roundtrip(ds_domain* dom, int n, uint64_t* out_ns);
+/* Measured fp32 FFMA throughput of the device (TFLOP/s; a plain kernel, so
+ * call it while no executor is resident): config 1's roofline denominator */
+int ds_measure_ffma_peak(int device, double* tflops);
 
 /* Overhead ledger (OverheadLedger, engine.hpp:94-107) measured from device
  * %globaltimer stamps, summed over worker lanes (ns):

@@ -1015,6 +1015,32 @@ extern "C" cudaError_t ds_dev_launch_solo(int body, const void* args, uint32_t g
     return cudaGetLastError();
 }
 
+// fp32 FFMA throughput probe (config 1's roofline denominator): 8
+// independent fma chains per thread, 4 blocks x 256 threads per SM; the
+// result is kept live so nothing is folded away
+extern "C" __global__ void __launch_bounds__(256) ds_ffma_probe_kernel(float* out, int iters, float x) {
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = x + (float)(threadIdx.x + j);
+    const float b = 1.0000001f, c = 1e-7f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = __fmaf_rn(a[j], b, c);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += a[j];
+    if (s == 12345.678f) out[blockIdx.x] = s;
+}
+
+extern "C" cudaError_t ds_dev_ffma_probe(int nblocks, int iters, float* out, cudaStream_t s) {
+    ds_ffma_probe_kernel<<<nblocks, 256, 0, s>>>(out, iters, 1.f);
+    return cudaGetLastError();
+}
+
 extern "C" cudaError_t ds_dev_probe(int nblocks, uint32_t* smids, uint32_t* nsmid, uint64_t* timer, cudaStream_t s) {
     ds::ds_probe_kernel<<<nblocks, 32, 0, s>>>(smids, nsmid, timer);
     return cudaGetLastError();

@@ -1433,6 +1433,40 @@ int ds_ipc_open(int device, const void* handle64, void** ptr) {
     return DS_OK;
 }
 
+extern "C" cudaError_t ds_dev_ffma_probe(int nblocks, int iters, float* out, cudaStream_t s);
+
+int ds_measure_ffma_peak(int device, double* tflops) {
+    if (!tflops) return fail(DS_INVALID_ARGUMENT, "null");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(DS_NO_DEVICE, "bad device ordinal");
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    float* out = nullptr;
+    DS_CUDA(cudaMalloc(&out, 4 * 4096));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = 4 * nsm, iters = 4096;
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0, 0);
+        cudaError_t e = ds_dev_ffma_probe(blocks, iters, out, 0);
+        cudaEventRecord(e1, 0);
+        if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
+            cudaFree(out);
+            return fail(DS_CUDA_ERROR, "ffma probe failed");
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double flop = 2.0 * 8 * 16 * (double)iters * 256.0 * blocks;
+        if (rep > 0 && ms > 0.f) best = std::max(best, flop / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    *tflops = best;
+    return DS_OK;
+}
+
 int ds_dp_abort(int device, void* flags) {
     if (!flags) return fail(DS_INVALID_ARGUMENT, "null");
     if (cudaSetDevice(device) != cudaSuccess) return fail(DS_NO_DEVICE, "bad device ordinal");
