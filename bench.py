@@ -912,7 +912,7 @@ def config4b_leg(co, args, solo):
             "tpot_first": res["tpot-first"], "slo_aware": res["slo-aware"], "temporal": res["temporal"]}
 
 
-def config4_leg(co, args, solo):
+def config4_leg(co, args, solo, peaks):
     """Config 4: the ResNet-50-shaped training stream co-located with bursty
     decode requests (gen_burst arrivals), TPOT-First vs time slicing."""
     from paper_2603_15042_b200 import workload as wl
@@ -935,6 +935,14 @@ def config4_leg(co, args, solo):
                         f"{args.burst_units}) x {unit_ms} ms/unit (trace.cpp:204-232), seed 0",
             "resnet_solo_iter_ms": round(res_ms, 3),
             "resnet_solo_images_per_s": round(co.resnet.batch / (res_ms * 1e-3), 1),
+            "roofline": {"bound": "tensor", "kernel": "train/resnet50 iteration (161 GEMMs + folds)",
+                         "achieved": round(co.resnet.flops / (res_ms * 1e-3) / 1e12, 1),
+                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": round(co.resnet.flops / (res_ms * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
+                         "padded_frac": round(co.resnet.padded_flops / (res_ms * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
+                         "what": "algorithmic (unpadded) conv/FC flops of one fwd+dgrad+wgrad iteration over its "
+                                 "solo time on the executor (full GPU); padded_frac counts the flops of the "
+                                 "128-row-tiled GEMMs actually issued"},
             "tpot_first": c4["tpot-first"], "slo_aware": c4["slo-aware"], "temporal": c4["temporal"]}
 
 
@@ -1017,7 +1025,7 @@ def gpu_arm(args, rank, world):
     config4 = None
     if not args.no_config4:
         try:
-            config4 = config4_leg(co, args, solo)
+            config4 = config4_leg(co, args, solo, peaks)
         except Exception as e:  # an auxiliary leg must not cost the headline line
             config4 = {"error": repr(e)}
     co.close()
@@ -1377,6 +1385,11 @@ def aggregate_ranks(vals):
     out["bit_exact_vs_solo"] = all(v["bit_exact_vs_solo"] for v in vals)
     out["gpu_launches"] = sum(v["gpu_launches"] for v in vals)
     out["n_gpus"] = len(vals)
+    # every rank's own numbers (each GPU ran its own domain: evidence that all
+    # of them were busy, and the spread behind the worst-rank value)
+    out["per_rank"] = [{"rank": i, "value": v["value"], "train_tflops": v["train_tflops"],
+                        "gpu_launches": v["gpu_launches"], "ms_per_step": v["ms_per_step"],
+                        "bit_exact_vs_solo": v["bit_exact_vs_solo"]} for i, v in enumerate(vals)]
     return out
 
 

@@ -658,7 +658,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     // the TMA): groups run independently, so a consumer first waits for its
     // chunk to be issued into the stage, then on the stage's full barrier
     // with the exact phase parity (never a phase behind or two ahead)
-    volatile int* stage_chunk = reinterpret_cast<volatile int*>(base + kAttnBarOff + 256);  // [kAttnStages]
+    int* stage_chunk = reinterpret_cast<int*>(base + kAttnBarOff + 256);  // [kAttnStages] (shared-window accesses)
     // warps of the consuming group done with the stage; the last one refills it
     uint32_t* stage_done = reinterpret_cast<uint32_t*>(base + kAttnBarOff + 512);        // [kAttnStages]
     const int row0 = (b * 8 + h) * a.Lmax + p0;
@@ -675,7 +675,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         const int s = i % kAttnStages;
         char* st = base + s * kAttnStage;
         const uint64_t pol = tc::policy_evict_first();
-        stage_chunk[s] = i;
+        asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(tc::smem_u32(&stage_chunk[s])), "r"(i) : "memory");
         tc::mbar_arrive_expect_tx(&full[s], kAttnStage);
 #ifdef DS_ATTN_BULK  // diagnostic build: contiguous bulk copies (layout unswizzled: timing only)
         tc::bulk_g2s_hint(st, reinterpret_cast<const char*>(a.kbase) + (size_t)(row0 + i * kAttnChunk) * 256,
@@ -756,7 +756,12 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         const bool tr = dbg && ltid() == 0 && tj < 12;
         if (tr) dbg[8 + 4 * tj] = globaltimer();
 #endif
-        while (stage_chunk[s] != ci) {
+        {  // shared-window spin (a generic volatile load would take the global path)
+            const uint32_t sc = tc::smem_u32(&stage_chunk[s]);
+            int cur;
+            do {
+                asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(cur) : "r"(sc) : "memory");
+            } while (cur != ci);
         }
 #ifdef DS_ATTN_TRACE
         if (tr) dbg[9 + 4 * tj] = globaltimer();
@@ -853,11 +858,12 @@ __device__ void body_attn_decode(const BodyCtx& c) {
 #ifdef DS_ATTN_TRACE
         if (tr) dbg[11 + 4 * tj] = globaltimer();
 #endif
-        // the group's last warp to finish the stage refills it (its reads,
-        // and through the acq_rel counter every other warp's, are complete)
+        // the group's last warp to finish the stage refills it.  A relaxed
+        // count suffices: a warp's ldmatrix reads of the stage returned
+        // before its MMAs could issue, i.e. before its arrival
         if (lane == 0) {
             uint32_t n;
-            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+            asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
                          : "=r"(n) : "r"(tc::smem_u32(&stage_done[s])) : "memory");
             if (n == kAttnWpc - 1) {
                 stage_done[s] = 0u;
