@@ -270,7 +270,7 @@ class AttnArgs(ctypes.Structure):
                 ("ws", ctypes.c_uint64), ("counters", ctypes.c_uint64), ("L", ctypes.c_int32),
                 ("Lmax", ctypes.c_int32), ("S", ctypes.c_int32), ("scale", ctypes.c_float), ("dbg", ctypes.c_uint64),
                 ("kbase", ctypes.c_uint64), ("vbase", ctypes.c_uint64), ("l2_pf_kb", ctypes.c_int32),
-                ("pad", ctypes.c_int32)]
+                ("tc", ctypes.c_int32)]
 
 
 class EmbedArgs(ctypes.Structure):

@@ -571,7 +571,7 @@ struct AttnArgs {
     uint64_t vbase;
     int32_t l2_pf_kb;   // early start: KB of K and of V past the ring prefetched into L2 once the previous
                         // launch has streamed (0 = ring only)
-    int32_t pad;
+    int32_t tc;         // 1: both products on tcgen05 with TMEM accumulators (body_attn_decode_tc)
 };
 
 // KV positions per pipeline stage (one TMA box height).  A stage holds the
@@ -628,6 +628,411 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// ---------------------------------------------------------------------------
+// GQA decode attention on tcgen05 (a.tc = 1).  Same blocks, chunking and
+// K/V staging as body_attn_decode (3-stage ring of 64-position chunks, one
+// smem row per position), but both products run on the 5th-gen tensor core
+// with accumulators in TMEM:
+//   S^T[64 pos][8]  = K[64 pos][128] . Q^T          M = 64, N = 8 (4 heads + 4 zero),
+//                                                    A = the K tile (K-major), B = Q^T (K-major)
+//   O_q^T[128][16] += V^T[128][16 pos] . P_q^T       M = 128, N = 16 (4 heads + 12 zero), K = 16,
+//                                                    A = the V tile read MN-major (dims contiguous),
+//                                                    B = P_q^T in smem (K-major, no swizzle)
+// Softmax stream q (epilogue warp 4+q) owns positions 16q..16q+15 of every
+// chunk: it reads its 16 S^T rows (TMEM lanes 32q..32q+15), keeps its own
+// running max / sum per head and writes P_q^T; O_q accumulates in its own 16
+// TMEM columns.  The running max is lazy: it moves (and O_q, l_q are
+// rescaled) only when a chunk's max exceeds it by more than 2^8, so P stays
+// in [0, 256] and most chunks need no rescale.  The four streams merge in
+// stream order at the end.  Every decision depends on the data alone:
+// deterministic, and bit-identical wherever the block runs.
+// Roles: warp 0 lane 0 TMA producer, warp 1 lane 0 MMA issuer, warps 4-7
+// softmax + O epilogue.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kAtQOff = kAttnStages * kAttnStage;            // Q^T [2 atoms][8 rows][128 B]
+constexpr uint32_t kAtPOff = kAtQOff + 2048;                      // P^T [2 bufs][4 streams][512 B]
+constexpr uint32_t kAtBarOff = kAtPOff + 4096;                    // barriers + exchange words
+constexpr uint32_t kAtSmem = kAtBarOff + 1024;
+constexpr float kAtLazy = 8.f;                                    // log2 of the largest unnormalised P
+static_assert(kAttnChunk == 64, "the tcgen05 attention stages 64-position chunks");
+
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // MN-major SWIZZLE_128B: 64 MN-elements per 128-B row, 8 K-rows per atom;
+    // LBO = next 64 MN-elements, SBO = next 8 K-rows (cute make_umma_desc<MN>)
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+__device__ __forceinline__ uint64_t smem_desc_k_interleave(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // K-major, no swizzle: core matrices of 8 rows x 16 B; LBO = next K
+    // core matrix, SBO = next 8 rows
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+__device__ void body_attn_decode_tc(const BodyCtx& c, const AttnArgs& a) {
+    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int bh = t % 256, sp = t / 256;
+    const int b = bh >> 3, h = bh & 7;
+    const int warp = ltid() >> 5, lane = ltid() & 31;
+    const int p0 = (int)((int64_t)sp * a.L / a.S), p1 = (int)((int64_t)(sp + 1) * a.L / a.S);
+    const int nch = (p1 - p0 + kAttnChunk - 1) / kAttnChunk;
+    char* base = align1024(c.smem);
+    const uint32_t sbase = tc::smem_u32(base);
+    // K and V of a stage recycle separately: K after its chunk's QK, V after its PV
+    uint64_t* fullK = reinterpret_cast<uint64_t*>(base + kAtBarOff);  // [3]
+    uint64_t* fullV = fullK + kAttnStages;                            // [3]
+    uint64_t* emptyK = fullV + kAttnStages;                           // [3]
+    uint64_t* emptyV = emptyK + kAttnStages;                          // [3]
+    uint64_t* s_full = emptyV + kAttnStages;                          // [2] S^T of a chunk in TMEM
+    uint64_t* s_free = s_full + 2;                                   // [2] 4 softmax warps read it
+    uint64_t* p_ready = s_free + 2;                                  // [2] P^T written, O rescaled
+    uint64_t* o_done = p_ready + 2;                                  // [2] PV of a chunk complete
+    float* xchg = reinterpret_cast<float*>(base + kAtBarOff + 256);  // [2][4 streams][8]: alpha (0 = none)
+    float* fin = xchg + 64;                                          // [4 streams][8 heads][m, l]
+    const uint32_t tS = c.tmem_base, tO = c.tmem_base + 32;          // S: 2 x 8 cols; O: 4 streams x 16 cols
+    const int row0 = (b * 8 + h) * a.Lmax + p0;
+#ifdef DS_ATTN_TRACE  // diagnostic build: per-chunk timeline (dbg stride 128 per block)
+    uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 128 : nullptr;
+#else
+    uint64_t* dbg = a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr;
+#endif
+    if (dbg && ltid() == 0) dbg[0] = globaltimer();
+    auto issue_k = [&](int i) {
+        const int s = i % kAttnStages;
+        tc::mbar_arrive_expect_tx(&fullK[s], 2 * kAttnHalf);
+        tc::tma_load_3d_hint(base + s * kAttnStage, &a.tmK, &fullK[s], 0, row0 + i * kAttnChunk, 0,
+                             tc::policy_evict_first());
+    };
+    auto issue_v = [&](int i) {
+        const int s = i % kAttnStages;
+        tc::mbar_arrive_expect_tx(&fullV[s], 2 * kAttnHalf);
+        tc::tma_load_3d_hint(base + s * kAttnStage + 2 * kAttnHalf, &a.tmV, &fullV[s], 0, row0 + i * kAttnChunk, 0,
+                             tc::policy_evict_first());
+    };
+    auto issue = [&](int i) {
+        issue_k(i);
+        issue_v(i);
+    };
+    if (ltid() == 0) {
+        for (int s = 0; s < kAttnStages; ++s) {
+            tc::mbar_init(&fullK[s], 1);
+            tc::mbar_init(&fullV[s], 1);
+            tc::mbar_init(&emptyK[s], 1);
+            tc::mbar_init(&emptyV[s], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            tc::mbar_init(&s_full[k], 1);
+            tc::mbar_init(&s_free[k], 4);
+            tc::mbar_init(&p_ready[k], 1);
+            tc::mbar_init(&o_done[k], 1);
+        }
+        tc::fence_mbar_init();
+        tc::tma_fence_desc(&a.tmK);
+        tc::tma_fence_desc(&a.tmV);
+        // early start: chunks entirely below L-1 are immutable this step
+        const int pre = min(kAttnStages, nch);
+        int pk = 0;
+        while (pk < pre && p0 + (pk + 1) * kAttnChunk <= a.L - 1) issue(pk++);
+        wait_prev(c);
+        for (int i = pk; i < pre; ++i) issue(i);
+    }
+    body_sync();  // barriers initialised; thread 0's acquire (wait_prev) for the whole lane
+    if (dbg && ltid() == 0) dbg[7] = globaltimer();
+    {  // Q^T -> smem, K-major SWIZZLE_128B: row r = head (rows 4-7 zero), 16-B chunk j of
+       // dims [64 a, 64 a + 64) at atom a, chunk j ^ r
+        const int r = ltid() >> 5, j16 = (ltid() >> 1) & 15, half = ltid() & 1;  // 8 rows x 16 chunks of 16 B, 2 threads each
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < 4 && !half) {
+            const uint4* q = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.q) + (size_t)b * 4096 +
+                                                            (h * 4 + r) * 128);
+            v = __ldcg(q + j16);
+        }
+        if (!half) {
+            const int at = j16 >> 3, jj = j16 & 7;
+            *reinterpret_cast<uint4*>(base + kAtQOff + at * 1024 + r * 128 + ((jj ^ r) << 4)) = v;
+        }
+        // P^T buffers: rows 4-15 (padding heads) stay zero
+        for (int i = ltid(); i < 4096 / 16; i += kBodyThreads)
+            reinterpret_cast<uint4*>(base + kAtPOff)[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    tc::fence_proxy_async();  // generic smem writes (Q^T, P^T zeros) -> tensor-core reads
+    body_sync();
+    if (warp == 0 && lane == 0) {
+        // ---- K producer: refill a K slot once its chunk's QK consumed it ----
+        for (int i = kAttnStages; i < nch; ++i) {
+            tc::mbar_wait(&emptyK[i % kAttnStages], ((i / kAttnStages) - 1) & 1);
+            issue_k(i);
+        }
+    } else if (warp == 2 && lane == 0) {
+        // ---- V producer: refill a V slot once its chunk's PV consumed it ----
+        for (int i = kAttnStages; i < nch; ++i) {
+            tc::mbar_wait(&emptyV[i % kAttnStages], ((i / kAttnStages) - 1) & 1);
+            issue_v(i);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer ----
+        constexpr uint32_t idS = tc::idesc_bf16_f32(64, 8);
+        constexpr uint32_t idO = tc::idesc_bf16_f32(128, 16) | (1u << 15);  // A (V^T) MN-major
+        auto qk = [&](int ci) {
+            const int s = ci % kAttnStages, sb = ci & 1;
+            tc::mbar_wait(&fullK[s], (ci / kAttnStages) & 1);
+            if (ci >= 2) tc::mbar_wait(&s_free[sb], ((ci >> 1) - 1) & 1);
+            tc::tc_fence_after();
+            const uint32_t kt = sbase + s * kAttnStage;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint64_t ad = tc::smem_desc_k_sw128(base + (kt - sbase) + (ks >> 2) * kAttnHalf) + (uint64_t)((ks & 3) * 2);
+                const uint64_t bd = tc::smem_desc_k_sw128(base + kAtQOff + (ks >> 2) * 1024) + (uint64_t)((ks & 3) * 2);
+                tc::mma_bf16(tS + 8 * sb, ad, bd, idS, ks != 0);
+            }
+            tc::mma_commit(&s_full[sb]);
+            tc::mma_commit(&emptyK[s]);  // K of the stage consumed
+#ifdef DS_ATTN_TRACE
+            if (dbg && ci < 16) dbg[80 + ci] = globaltimer();
+#endif
+        };
+        if (nch > 0) qk(0);
+        for (int ci = 0; ci < nch; ++ci) {
+            if (ci + 1 < nch) qk(ci + 1);  // S of the next chunk while softmax runs on this one
+            const int s = ci % kAttnStages, sb = ci & 1;
+            tc::mbar_wait(&p_ready[sb], (ci >> 1) & 1);
+            tc::mbar_wait(&fullV[s], (ci / kAttnStages) & 1);
+            tc::tc_fence_after();
+            const uint32_t vt = sbase + s * kAttnStage + 2 * kAttnHalf;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                // A: V^T [128 dims][16 positions 16q..], MN-major: dims 0-63 | 64-127 are the two
+                // half-tiles (LBO = one half-tile), 8 positions per 1-KB atom (SBO)
+                const uint64_t ad = smem_desc_mn_sw128(vt + q * 2048, kAttnHalf, 1024);
+                // B: P_q^T [16 rows][16 positions], no swizzle: [k half][2 row groups][8 rows][16 B]
+                const uint64_t bd = smem_desc_k_interleave(sbase + kAtPOff + sb * 2048 + q * 512, 256, 128);
+                tc::mma_bf16(tO + 16 * q, ad, bd, idO, ci != 0);
+            }
+            tc::mma_commit(&o_done[sb]);
+            tc::mma_commit(&emptyV[s]);  // V of the stage consumed
+#ifdef DS_ATTN_TRACE
+            if (dbg && ci < 16) dbg[64 + ci] = globaltimer();
+#endif
+        }
+    } else if (warp >= 4) {
+        // ---- softmax stream q: positions 16q..16q+15 of every chunk ----
+        const int q = warp - 4;
+        const float scale2 = a.scale * 1.4426950408889634f;
+        float m[4] = {kNegInf, kNegInf, kNegInf, kNegInf};  // lazy running max per head (log2 units)
+        float l[4] = {0.f, 0.f, 0.f, 0.f};                  // this lane's share of the running sums
+        for (int ci = 0; ci < nch; ++ci) {
+            const int sb = ci & 1;
+#ifdef DS_ATTN_TRACE
+            const bool tr = dbg && ltid() == 128 && ci < 14;
+            if (tr) dbg[8 + 4 * ci] = globaltimer();
+#endif
+            tc::mbar_wait(&s_full[sb], (ci >> 1) & 1);
+#ifdef DS_ATTN_TRACE
+            if (tr) dbg[9 + 4 * ci] = globaltimer();
+#endif
+            tc::tc_fence_after();
+            uint32_t raw[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(raw[0]), "=r"(raw[1]), "=r"(raw[2]), "=r"(raw[3]), "=r"(raw[4]), "=r"(raw[5]),
+                           "=r"(raw[6]), "=r"(raw[7])
+                         : "r"(tS + 8 * sb + ((uint32_t)(q * 32) << 16)));
+            tc::tmem_ld_wait();
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&s_free[sb]);
+            // lane < 16: position 16q + lane of the chunk (M = 64: rows 16q.. in lanes 32q..32q+15)
+            const int pos = ci * kAttnChunk + 16 * q + lane;
+            const bool ok = lane < 16 && p0 + pos < p1;
+            float sv[4], cm[4];
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+                sv[hh] = ok ? __uint_as_float(raw[hh]) * scale2 : kNegInf;
+                cm[hh] = sv[hh];
+            }
+#pragma unroll
+            for (int off = 1; off < 16; off <<= 1)
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) cm[hh] = fmaxf(cm[hh], __shfl_xor_sync(0xffffffffu, cm[hh], off));
+            // lazy max: move it only when the chunk exceeds it by > 2^kAtLazy
+            bool move = false;
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) move |= cm[hh] > m[hh] + kAtLazy;
+            float al[4] = {1.f, 1.f, 1.f, 1.f};
+            if (move) {
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                    const float nm = fmaxf(m[hh], cm[hh]);
+                    al[hh] = m[hh] == kNegInf ? 0.f : ex2_ftz(m[hh] - nm);
+                    m[hh] = nm;
+                    l[hh] *= al[hh];
+                }
+            }
+            // P_q^T (bf16): row = head, column = position; buffer sb was last read by PV(ci-2)
+            if (ci >= 2) tc::mbar_wait(&o_done[sb], ((ci >> 1) - 1) & 1);
+            char* pb = base + kAtPOff + sb * 2048 + q * 512;
+            if (lane < 16) {
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                    const float pv = (sv[hh] == kNegInf || m[hh] == kNegInf) ? 0.f : ex2_ftz(sv[hh] - m[hh]);
+                    l[hh] += pv;
+                    const __nv_bfloat16 pbf = __float2bfloat16_rn(pv);
+                    // [k half (lane / 8)][row group 0][row hh][16 B] + (lane % 8) * 2
+                    *reinterpret_cast<__nv_bfloat16*>(pb + (lane >> 3) * 256 + hh * 16 + (lane & 7) * 2) = pbf;
+                }
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) xchg[(sb * 4 + q) * 8 + hh] = move ? al[hh] : 1.f;
+                xchg[(sb * 4 + q) * 8 + 7] = move ? 1.f : 0.f;
+            }
+#ifdef DS_ATTN_TRACE
+            if (tr) dbg[10 + 4 * ci] = globaltimer();
+#endif
+            tc::fence_proxy_async();  // P^T (generic writes) before the tensor core reads it
+            epi_sync();               // every stream's P^T and rescale decision
+            // rescale O of the streams whose max moved (all 4 warps: O_q spans every lane)
+            bool any = false;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) any |= xchg[(sb * 4 + qq) * 8 + 7] != 0.f;
+            if (any && ci >= 1) {
+                tc::mbar_wait(&o_done[(ci - 1) & 1], ((ci - 1) >> 1) & 1);  // PV(ci-1) final
+                tc::tc_fence_after();
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    if (xchg[(sb * 4 + qq) * 8 + 7] == 0.f) continue;
+                    uint32_t o[16];
+                    const uint32_t ta = tO + 16 * qq + ((uint32_t)(q * 32) << 16);
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+                                 : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]),
+                                   "=r"(o[7]), "=r"(o[8]), "=r"(o[9]), "=r"(o[10]), "=r"(o[11]), "=r"(o[12]), "=r"(o[13]),
+                                   "=r"(o[14]), "=r"(o[15])
+                                 : "r"(ta));
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int hh = 0; hh < 4; ++hh) o[hh] = __float_as_uint(__uint_as_float(o[hh]) * xchg[(sb * 4 + qq) * 8 + hh]);
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+                                 ::"r"(ta), "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]),
+                                   "r"(o[8]), "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15])
+                                 : "memory");
+                }
+                tc::tmem_st_wait();
+            }
+            tc::tc_fence_before();
+            epi_sync();  // P^T of every stream written, every rescale stored
+            if (warp == 4 && lane == 0) tc::mbar_arrive(&p_ready[sb]);
+#ifdef DS_ATTN_TRACE
+            if (tr) dbg[11 + 4 * ci] = globaltimer();
+#endif
+        }
+        // ---- merge the four streams ----
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+#pragma unroll
+            for (int off = 1; off < 16; off <<= 1) l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], off);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+                fin[(q * 8 + hh) * 2] = m[hh];
+                fin[(q * 8 + hh) * 2 + 1] = l[hh];
+            }
+        }
+        if (nch > 0) tc::mbar_wait(&o_done[(nch - 1) & 1], ((nch - 1) >> 1) & 1);
+        tc::tc_fence_after();
+        epi_sync();
+        // thread: dim d = 32 (warp - 4) + lane, heads 0-3 (TMEM lanes are dims)
+        uint32_t o[4][4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(o[qq][0]), "=r"(o[qq][1]), "=r"(o[qq][2]), "=r"(o[qq][3])
+                         : "r"(tO + 16 * qq + ((uint32_t)(q * 32) << 16)));
+        }
+        tc::tmem_ld_wait();
+        const int d = 32 * q + lane;
+        float O[4], Ls[4], M[4];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+            M[hh] = kNegInf;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) M[hh] = fmaxf(M[hh], fin[(qq * 8 + hh) * 2]);
+            O[hh] = 0.f;
+            Ls[hh] = 0.f;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {  // stream order
+                const float mq = fin[(qq * 8 + hh) * 2];
+                const float f = mq == kNegInf ? 0.f : ex2_ftz(mq - M[hh]);
+                Ls[hh] += fin[(qq * 8 + hh) * 2 + 1] * f;
+                O[hh] += __uint_as_float(o[qq][hh]) * f;
+            }
+        }
+        bool write_out = true;
+        if (a.S > 1) {
+            __shared__ int last_flag_t[2];
+            float* ws = reinterpret_cast<float*>(a.ws) + ((size_t)bh * a.S + sp) * 4 * 130;
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+                ws[hh * 130 + d] = O[hh];
+                if (d == 0) {
+                    ws[hh * 130 + 128] = M[hh];
+                    ws[hh * 130 + 129] = Ls[hh];
+                }
+            }
+            epi_sync();
+            if (warp == 4 && lane == 0) {
+                uint32_t tk;
+                __threadfence();
+                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                             : "=r"(tk) : "l"(reinterpret_cast<uint32_t*>(a.counters) + bh) : "memory");
+                last_flag_t[body_lane()] = tk == (uint32_t)a.S - 1;
+            }
+            epi_sync();
+            write_out = last_flag_t[body_lane()] != 0;
+            if (write_out) {
+                __threadfence();
+                const float* wsb = reinterpret_cast<const float*>(a.ws) + (size_t)bh * a.S * 4 * 130;
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                    float MM = kNegInf;
+                    for (int s2 = 0; s2 < a.S; ++s2) MM = fmaxf(MM, __ldcg(wsb + s2 * 4 * 130 + hh * 130 + 128));
+                    float oo = 0.f, ll = 0.f;
+                    for (int s2 = 0; s2 < a.S; ++s2) {  // fixed order
+                        const float* src = wsb + s2 * 4 * 130 + hh * 130;
+                        const float mw = __ldcg(src + 128);
+                        const float f = mw == kNegInf ? 0.f : ex2_ftz(mw - MM);
+                        ll += __ldcg(src + 129) * f;
+                        oo += __ldcg(src + d) * f;
+                    }
+                    O[hh] = oo;
+                    Ls[hh] = ll;
+                }
+                epi_sync();
+                if (warp == 4 && lane == 0) reinterpret_cast<uint32_t*>(a.counters)[bh] = 0;
+            }
+        }
+        if (write_out) {
+            uint16_t* orow = reinterpret_cast<uint16_t*>(a.out) + (size_t)b * 4096 + (h * 4) * 128 + d;
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) orow[hh * 128] = f_to_bf16(O[hh] / Ls[hh]);
+        }
+    }
+    tc::tc_fence_before();
+    body_sync();
+    if (ltid() == 0) mark_streamed(c);
+    if (dbg && ltid() == 0) dbg[6] = globaltimer();
+    if (ltid() == 0)
+        for (int k = 0; k < 4 * kAttnStages + 8; ++k) tc::mbar_inval(&fullK[k]);
+}
+
 // GQA decode attention on tensor cores, positions split across warps.
 // Chunk c (kAttnChunk positions) lands by TMA in stage c % kAttnStages and is
 // consumed by warp group c % kAttnGroups: each warp of the group owns 16 of
@@ -643,6 +1048,10 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
 // functions of (L, S, block).
 __device__ void body_attn_decode(const BodyCtx& c) {
     const AttnArgs& a = *reinterpret_cast<const AttnArgs*>(c.args);
+    if (a.tc) {
+        body_attn_decode_tc(c, a);
+        return;
+    }
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
     const int bh = t % 256, sp = t / 256;
     const int b = bh >> 3, h = bh & 7;

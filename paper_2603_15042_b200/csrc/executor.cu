@@ -950,7 +950,7 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     c.ab_info = nullptr;
     c.resume = 0u;
     __shared__ uint32_t tmem_base_sh;
-    const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16;
+    const bool tc_body = body == DS_BODY_GEMM_BF16 || body == DS_BODY_GEMV_BF16 || body == DS_BODY_ATTN_DECODE;
     if (tc_body) {
         if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(&tmem_base_sh, kLaneTmemCols);
         tc::tc_fence_before();
@@ -1057,7 +1057,7 @@ extern "C" uint32_t ds_dev_body_smem(int body) {
             const uint32_t b = ds::TcSmem<ds::kGemvBN, ds::kGemvStages64, ds::kTcBK, 64>::kBytes;
             return (a > b ? a : b) + 1024;
         }
-        case DS_BODY_ATTN_DECODE: return ds::kAttnSmem + 1024;
+        case DS_BODY_ATTN_DECODE: return (ds::kAttnSmem > ds::kAtSmem ? ds::kAttnSmem : ds::kAtSmem) + 1024;
         case DS_BODY_RMSNORM: return 1024;
         case DS_BODY_EMBED: return 1024;
         case DS_BODY_ARGMAX: return 1024;

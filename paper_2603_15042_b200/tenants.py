@@ -141,6 +141,8 @@ class DecodeModel:
         for kv in filter(None, (g_override or os.environ.get("DS_GEMV_G", "")).split(",")):
             k, v = kv.split(":")
             self.G[k] = int(v)
+        # attention products on tcgen05 (TMEM accumulators) instead of mma.sync
+        self.attn_tc = int(os.environ.get("DS_ATTN_TC", "0"))
         # weight rows per slab (M of the swap-AB MMA): 128, or 64 for the small
         # projections (gate_up's SiLU pairing needs 128-row slabs)
         self.BM = {"qkv": 128, "o": 128, "gu": 128, "down": 128, "lm": 128}
@@ -230,6 +232,7 @@ class DecodeModel:
                                self.attn.data_ptr(), self.attn_ws.data_ptr(), self.attn_counters.data_ptr(), c.L,
                                self.Lmax, c.attn_splits, 1.0 / math.sqrt(128))
             at.kbase, at.vbase, at.l2_pf_kb = self.kc[l].data_ptr(), self.vc[l].data_ptr(), self.PF["attn"]
+            at.tc = self.attn_tc
             self.records.append(("decode/attn", _abi.BODY_ATTN_DECODE, (256 * c.attn_splits, 1, 1), at,
                                  2 * 32 * c.n_kv * c.L * 128 * 2))
             a, g = self._gemv(self.Wo[l], self.attn, c.d, c.d, self.S["o"], _abi.GEMV_RESID, self.h_mid, resid=hin,

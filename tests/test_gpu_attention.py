@@ -1,5 +1,6 @@
-"""GQA decode attention body vs a plain torch fp32 reference on the same bf16
-inputs (tolerance: bf16 output rounding, |err| <= 2^-7 |ref| + 2^-9)."""
+"""GQA decode attention body (mma.sync and tcgen05 paths) vs a plain torch
+fp32 reference on the same bf16 inputs (tolerance: bf16 output rounding,
+|err| <= 2^-7 |ref| + 2^-9)."""
 import math
 
 import pytest
@@ -11,8 +12,9 @@ from paper_2603_15042_b200.runtime import solo_launch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("L,S", [(96, 2), (1024, 2), (333, 3), (32, 1), (1000, 4)])
-def test_attention_matches_fp32_reference(L, S):
+@pytest.mark.parametrize("tc", [0, 1])
+@pytest.mark.parametrize("L,S", [(96, 2), (1024, 2), (333, 3), (32, 1), (1000, 4), (1024, 1), (70, 1)])
+def test_attention_matches_fp32_reference(L, S, tc):
     g = torch.Generator(device="cuda").manual_seed(L)
     Lmax = L + 5
     q = (torch.randn(32, 4096, device="cuda", generator=g)).to(torch.bfloat16)
@@ -25,6 +27,7 @@ def test_attention_matches_fp32_reference(L, S):
     a = _abi.AttnArgs(_abi.tensor_map_kv(kc.data_ptr(), rows),
                       _abi.tensor_map_kv(vc.data_ptr(), rows),
                       q.data_ptr(), out.data_ptr(), ws.data_ptr(), ctr.data_ptr(), L, Lmax, S, 1.0 / math.sqrt(128), 0)
+    a.tc = tc  # 1: S^T / O^T on tcgen05 with TMEM accumulators (lazy softmax rescale)
     solo_launch(0, "attn", _abi.BODY_ATTN_DECODE, (256 * S, 1, 1), a)
     torch.cuda.synchronize()
     Q = q.float().view(32, 8, 4, 128)
