@@ -1,0 +1,20 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
+for i in 1 2; do
+for lib in "" paper_2603_15042_b200/_var_prev.so; do
+  if [ -n "$lib" ]; then export DS_LIB=$lib; else unset DS_LIB; fi
+  echo "== lib=${lib:-current}"
+  timeout 300 python scripts/perf_resnet.py 2>&1 | grep -E '"iter_ms"|"tflops"'
+  for n in 74 148; do
+   NSM=$n LAYERS=8 timeout 300 python scripts/critpath.py 2>&1 | grep -v Warn | python -c "
+import sys,json
+tot=0; out=[]
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l)
+        if d['n']>1: tot+=d['incr_us']; out.append(f\"{d['k'][7:]}={d['incr_us']}\")
+print('nsm=$n', ' '.join(out), 'layer_us', round(tot,1))
+"
+  done
+done
+done
+unset DS_LIB
