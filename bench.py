@@ -1175,7 +1175,8 @@ def config3_leg(dev):
     from paper_2603_15042_b200 import _abi, migration as mg
     from paper_2603_15042_b200.runtime import Domain
     from paper_2603_15042_b200.tenants import TrainGemm
-    # 16384 x 16384 x 8192 (~4 ms): long enough for flips every 200 us .. 2 ms;
+    # 16384 x 16384 x 8192 (~4 ms at the full quota): flips every 50 us .. 5 ms
+    # (at 5 ms the launch sees at most one flip);
     # 128x256 tiles (the throughput choice) and 128x64 tiles (4x shorter
     # logical blocks: the latency choice)
     gemm = TrainGemm(M=16384, N=16384, K=8192, device=f"cuda:{dev}", seed=5)
@@ -1209,7 +1210,7 @@ def config3_leg(dev):
             gbase = mg.run(dom, t, k, 0)
             gemm_rows[name] = {"unflipped_tflops": round(gbase["blocks_per_s"] * tile_flop / 1e12, 1),
                                "block_us": round(1e6 / gbase["blocks_per_s"] * 2 * 148, 1)}
-            for p in (200, 1000):
+            for p in (50, 200, 1000, 5000):  # 50 us .. 5 ms
                 rows.append(dict(unit=name, period_us=p, **mg.summarize(mg.run(dom, t, k, p), gbase["blocks_per_s"])))
         rtt = [x / 1e3 for x in dom.ctl_roundtrip(100)]
     return {"workload": "config 3: quota flips 100% <-> 25% of the SMs by the device timer (no host round trip)",
