@@ -287,14 +287,18 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
             epi_sync();
             tc::mbar_wait(&tmem_full[0], 0);
             tc::tc_fence_after();
+            if (dbg && ltid() == 128) dbg[1] = globaltimer();
             gemv_silu_pair_epilogue(c, a, pA.n, 0u, rv);
             tc::mbar_wait(&tmem_full[1], 0);
             tc::tc_fence_after();
+            if (dbg && ltid() == 128) dbg[2] = globaltimer();
             if (ltid() == 128) mark_streamed(c);  // every weight / X load of this block has landed
             gemv_silu_pair_epilogue(c, a, pB.n, 32u, rv);
         }
+        if (dbg && ltid() == 128) dbg[5] = globaltimer();
         tc_teardown<kGemvBN, STAGES, kTcBK, BM>(base);
         if (ltid() == 0) tc::mbar_inval(tmem_full + 1);
+        if (dbg && ltid() == 0) dbg[6] = globaltimer();
         return;
     }
     if (ltid() == 128) mark_streamed(c);  // tmem_full: every weight / X load of this block has landed

@@ -8,11 +8,15 @@
 #include <vector>
 #include <algorithm>
 #include <cuda_runtime.h>
+#include <cuda.h>
 #include "bodies/tc_ptx.cuh"
 
 using namespace ds;
 
+struct alignas(64) TMap { CUtensorMap m; };
 struct P {
+    TMap xmap;          // X [32][K] bf16, box {64, 32}, SWIZZLE_128B (xtma = 1)
+    int xtma;
     const char* src;
     const char* x;
     unsigned long long* t;   // [grid*lanes][2]
@@ -26,7 +30,7 @@ __device__ __forceinline__ unsigned long long gt() {
     return v;
 }
 
-extern "C" __global__ void __launch_bounds__(128) k_stream(P p) {
+extern "C" __global__ void __launch_bounds__(128) k_stream(const __grid_constant__ P p) {
     extern __shared__ __align__(1024) char sm_raw[];
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     const int lane_id = threadIdx.x >> 6, w = (threadIdx.x >> 5) & 1, l = threadIdx.x & 31;
@@ -62,8 +66,9 @@ extern "C" __global__ void __launch_bounds__(128) k_stream(P p) {
             tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
             char* d = lb + s * stage_bytes;
             tc::bulk_g2s_hint(d, src + (size_t)i * p.wbytes, p.wbytes, &full[s], pol);
-            if (p.xbytes) tc::bulk_g2s_hint(d + p.wbytes, p.x + (size_t)(i & 63) * p.xbytes, p.xbytes, &full[s],
-                                            tc::policy_evict_last());
+            if (p.xbytes && p.xtma) tc::tma_load_2d(d + p.wbytes, &p.xmap, &full[s], (i & 63) * 64, 0);
+            else if (p.xbytes) tc::bulk_g2s_hint(d + p.wbytes, p.x + (size_t)(i & 63) * p.xbytes, p.xbytes, &full[s],
+                                                 tc::policy_evict_last());
             if (p.pf) {
                 const size_t off = (size_t)i * p.wbytes + (size_t)p.pf;
                 if (off < p.lane_bytes) tc::bulk_prefetch_l2(src + off, p.wbytes);
@@ -108,7 +113,9 @@ int main(int argc, char** argv) {
     int xkb = argc > 6 ? atoi(argv[6]) : 4;
     int lane_mb = argc > 7 ? atoi(argv[7]) : 2;
     int wkb = argc > 8 ? atoi(argv[8]) : 16;
+    int xtma = argc > 9 ? atoi(argv[9]) : 0;
     P p{};
+    p.xtma = xtma;
     p.lane_bytes = (size_t)lane_mb << 20;
     p.stages = stages;
     p.lanes = lanes;
@@ -121,11 +128,21 @@ int main(int argc, char** argv) {
     unsigned long long* t;
     cudaMalloc(&src, total + (64 << 20));
     cudaMemset(src, 0, total + (64 << 20));
-    cudaMalloc(&x, 64 * 8192);
-    cudaMemset(x, 0, 64 * 8192);
+    cudaMalloc(&x, 32 * 4096 * 2 + 64 * 8192);
+    cudaMemset(x, 0, 32 * 4096 * 2 + 64 * 8192);
     cudaMalloc(&t, nsm * lanes * 16);
     p.src = src;
     p.x = x;
+    if (xtma) {  // X [32][4096] bf16 view of the x buffer (64 k-blocks), box {64, 32}
+        cuuint64_t dims[2] = {4096, 32};
+        cuuint64_t strides[1] = {4096 * 2};
+        cuuint32_t box[2] = {64, 32};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = cuTensorMapEncodeTiled(&p.xmap.m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, strides, box, es,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
+    }
     p.t = t;
     int smem = lanes * stages * (p.wbytes + p.xbytes) + lanes * 64 * 8 + 1024;
     smem = std::max(smem, 120 << 10);  // one CTA per SM
@@ -153,8 +170,8 @@ int main(int argc, char** argv) {
             lane_rate = lr / (nsm * lanes);
         }
     }
-    printf("{\"nsm\": %d, \"lanes\": %d, \"stages\": %d, \"wkb\": %d, \"xkb\": %d, \"mma\": %d, \"pf_kb\": %d, \"GBps\": %.1f, "
+    printf("{\"nsm\": %d, \"lanes\": %d, \"stages\": %d, \"wkb\": %d, \"xkb\": %d, \"mma\": %d, \"pf_kb\": %d, \"xtma\": %d, \"GBps\": %.1f, "
            "\"per_sm_GBps\": %.1f, \"lane_GBps\": %.1f}\n",
-           nsm, lanes, stages, wkb, xkb, mma, pf_kb, best, best / nsm, lane_rate);
+           nsm, lanes, stages, wkb, xkb, mma, pf_kb, xtma, best, best / nsm, lane_rate);
     return 0;
 }
