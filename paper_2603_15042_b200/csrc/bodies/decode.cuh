@@ -114,8 +114,10 @@ __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, con
         k = second ? pka1 + (i - n0) : pka0 + i;
     };
     if (warp == 0 && lane == 0) {
-        if (!a_packed) tc::tma_fence_desc(&a.tmW);
-        tc::tma_fence_desc(&a.tmX);
+        if (desc_fence_needed(dep.st ? &a : nullptr)) {
+            if (!a_packed) tc::tma_fence_desc(&a.tmW);
+            tc::tma_fence_desc(&a.tmX);
+        }
         const uint64_t pol = tc::policy_evict_first();
         auto issue_a = [&](int i) {
             int n, k;

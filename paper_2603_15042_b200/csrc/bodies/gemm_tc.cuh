@@ -68,12 +68,26 @@ __device__ __forceinline__ volatile uint64_t* tc_stop_time_of(int l) {
 }
 __device__ __forceinline__ volatile uint64_t* tc_stop_time() { return tc_stop_time_of(body_lane()); }
 
+// Descriptor fences: a launch record's tensor maps are immutable once
+// registered, so a lane fences them (generic -> tensormap proxy) on its first
+// block of a record and skips the fence on the record's later blocks.  Keyed
+// by the record's args pointer; nullptr (solo grids) always fences.
+__shared__ const void* g_desc_fenced[2];
+
+__device__ __forceinline__ bool desc_fence_needed(const void* key) {
+    if (!key) return true;
+    if (g_desc_fenced[body_lane()] == key) return false;
+    g_desc_fenced[body_lane()] = key;
+    return true;
+}
+
 template <int BN, int STAGES, int BK = kTcBK, int BM = kTcBM>
 __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, const TmaDesc* tmB, int a_row, int b_row,
                                             int kb_begin, int kb_end, uint32_t tmem_base, bool a_evict_first,
                                             const char* a_packed = nullptr, int a_kblocks = 0,
                                             const BodyCtx* dep = nullptr, const BodyCtx* yc = nullptr,
-                                            bool acc_init = false, uint32_t l2_pf_bytes = 0) {
+                                            bool acc_init = false, uint32_t l2_pf_bytes = 0,
+                                            const void* fence_key = nullptr) {
     using L = TcSmem<BN, STAGES, BK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -91,8 +105,10 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
     body_sync();
     const int nkb = kb_end - kb_begin;
     if (warp == 0 && lane == 0) {
-        if (!a_packed) tc::tma_fence_desc(tmA);
-        tc::tma_fence_desc(tmB);
+        if (desc_fence_needed(fence_key)) {
+            if (!a_packed) tc::tma_fence_desc(tmA);
+            tc::tma_fence_desc(tmB);
+        }
         const uint64_t pol = a_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
         auto issue_a = [&](int i) {
             const int s = i % STAGES;
@@ -295,7 +311,7 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
         if (ltid() == 0) atomicExch(ring + j, 0ull);  // spill consumed: the slot is free again
     }
     tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb_start, kb1, c.tmem_base, false,
-                                nullptr, 0, nullptr, yc, res != 0u);
+                                nullptr, 0, nullptr, yc, res != 0u, 0, c.st ? c.args : nullptr);
     const bool gave_up = yc && *tc_stop_word() != ~0u;  // epilogue warps: ordered by tmem_full
     if (gave_up) {
         // abandoned: spill the accumulators (when there are any) so the tile

@@ -906,6 +906,7 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
     if (threadIdx.x < kLanes) {  // ordered by the barrier below
         ab_flag[threadIdx.x] = 0u;
         ab_info[threadIdx.x] = 0u;
+        g_desc_fenced[threadIdx.x] = nullptr;
     }
     tc::tc_fence_before();
     named_sync(kBarExit, kLanes * (kBodyThreads + 32));
