@@ -1092,13 +1092,6 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         const uint64_t pol = tc::policy_evict_first();
         asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(tc::smem_u32(&stage_chunk[s])), "r"(i) : "memory");
         tc::mbar_arrive_expect_tx(&full[s], kAttnStage);
-#ifdef DS_ATTN_BULK  // diagnostic build: contiguous bulk copies (layout unswizzled: timing only)
-        tc::bulk_g2s_hint(st, reinterpret_cast<const char*>(a.kbase) + (size_t)(row0 + i * kAttnChunk) * 256,
-                          2 * kAttnHalf, &full[s], pol);
-        tc::bulk_g2s_hint(st + 2 * kAttnHalf, reinterpret_cast<const char*>(a.vbase) + (size_t)(row0 + i * kAttnChunk) * 256,
-                          2 * kAttnHalf, &full[s], pol);
-        return;
-#endif
         tc::tma_load_3d_hint(st, &a.tmK, &full[s], 0, row0 + i * kAttnChunk, 0, pol);
         tc::tma_load_3d_hint(st + 2 * kAttnHalf, &a.tmV, &full[s], 0, row0 + i * kAttnChunk, 0, pol);
     };
@@ -1186,30 +1179,6 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         if (tr) dbg[10 + 4 * tj] = globaltimer();
 #endif
         const uint32_t kt = sbase + s * kAttnStage, vt = kt + 2 * kAttnHalf;
-#ifdef DS_ATTN_LDSM_ONLY  // diagnostic build: the ldmatrix reads of K and V, no math
-        {
-            uint32_t x = 0;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * ks + 8 * (lm >> 1)), a0, a1, a2, a3);
-                x ^= a0 ^ a1 ^ a2 ^ a3;
-                ldsm_x4_t(kv_addr(vt, pw + lr + 8 * (lm >> 1), 16 * ks + 8 * (lm & 1)), a0, a1, a2, a3);
-                x ^= a0 ^ a1 ^ a2 ^ a3;
-            }
-            o[0][0] += __uint_as_float(x & 0x3f000000u);
-        }
-#define DS_ATTN_NOCOMPUTE
-#endif
-#ifdef DS_ATTN_NOCOMPUTE  // diagnostic build: ring traffic and handoffs only
-        __syncwarp();
-        if (lane == 0 && atomicAdd(&stage_done[s], 1u) == kAttnWpc - 1) {
-            stage_done[s] = 0u;
-            if (ci + kAttnStages < nch) issue(ci + kAttnStages);
-        }
-        __syncwarp();
-        continue;
-#endif
         // ---- S^T[16 pos][8] = K[pw..pw+15][:] . Q^T (two chains) ----
         float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1287,10 +1256,6 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         }
         __syncwarp();
     }
-#ifdef DS_ATTN_NOCOMPUTE
-    m0 = m1 = 0.f;
-    l0 = l1 = 0.125f;
-#endif
     // l over the 8 g-rows of the warp (fixed tree)
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
