@@ -61,6 +61,28 @@ if os.path.exists(lpath):
             ns = v * {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(unit, 1)
             f.write(f'{r["ID"]},{r["Kernel Name"][:80].replace(",", ";")},{int(ns)}\n')
     summary["launch_list"] = {"file": f"{TAG}_launches_decode_step.csv", "solo_body_launches": len(solo)}
+    # label the solo launches by decode-step order (profile_solo.py decode: 2 steps of
+    # embed, 32 x (qkv, attn, o, gate_up, down), lm_head, argmax) and average per kernel:
+    # the serialised cold-cache counterpart of the bench's per-kernel CUDA-event times
+    order = ["embed"] + ["qkv", "attn", "o", "gate_up", "down"] * 32 + ["lm_head", "argmax"]
+    def ns_of(r):
+        v = float(r["Metric Value"].replace(",", ""))
+        return v * {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(r.get("Metric Unit", "ns"), 1)
+    if len(solo) % len(order) == 0:
+        per = collections.defaultdict(list)
+        for i, r in enumerate(solo):
+            per[order[i % len(order)]].append(ns_of(r))
+        step_ns = sum(ns_of(r) for r in solo) / (len(solo) // len(order))
+        byts = {"qkv": 6144 * 4096 * 2, "attn": 2 * 32 * 8 * 1024 * 128 * 2, "o": 4096 * 4096 * 2,
+                "gate_up": 2 * 14336 * 4096 * 2, "down": 4096 * 14336 * 2, "lm_head": 128256 * 4096 * 2}
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.6
+        summary["launch_list"]["per_kernel_us"] = {
+            k: {"mean_us": round(sum(v) / len(v) / 1e3, 2), "launches_per_step": len(v) * len(order) // len(solo),
+                "share_of_step": round(sum(v) / (len(solo) // len(order)) / step_ns, 4),
+                **({"hbm_frac": round(byts[k] / (sum(v) / len(v)) / hbm, 4)} if k in byts else {})}
+            for k, v in per.items()}
+        summary["launch_list"]["step_ms_serialised"] = round(step_ns / 1e6, 4)
 json.dump(summary, open(os.path.join(OUT, f"{TAG}_ncu_summary.json"), "w"), indent=1)
 for k, d in summary["kernels"].items():
     print(k, round(d["duration_s"] * 1e6, 1), "us", d["achieved_GBps_algorithmic"], "GB/s alg", "traffic/alg",
