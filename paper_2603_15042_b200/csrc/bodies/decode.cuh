@@ -595,8 +595,8 @@ constexpr uint32_t kAttnHalf = kAttnChunk * 128;           // one [chunk][64] bf
 constexpr uint32_t kAttnStage = 4 * kAttnHalf;             // K + V of one chunk
 constexpr int kAttnStages = (96 * 1024) / kAttnStage;      // 3 x 32 KB (chunk 64) or 6 x 16 KB (chunk 32)
 constexpr uint32_t kAttnBarOff = kAttnStages * kAttnStage;
-constexpr uint32_t kAttnQOff = kAttnBarOff + 1024;           // Q^T B fragments [8 ks][2][4 heads][4 tq] u32
-constexpr uint32_t kAttnSmem = kAttnQOff + 1024;
+constexpr uint32_t kAttnQOff = kAttnBarOff + 1024;           // Q^T B fragments [8 ks][2][8 heads][4 tq] u32 (4-7 zero)
+constexpr uint32_t kAttnSmem = kAttnQOff + 2048;
 static_assert(kAttnChunk == 32 || kAttnChunk == 64, "chunk of 32 or 64 positions");
 static_assert(kAttnStages >= kAttnGroups + 1, "every group needs a stage in flight beyond the others'");
 
@@ -1134,18 +1134,21 @@ __device__ void body_attn_decode(const BodyCtx& c) {
     // O^T accumulators take 32 of them), and are re-read per k-step.
     const uint32_t qs = sbase + kAttnQOff;
     {
-        // thread i: head i >> 6, u32 i & 63 of that head's 128 dims -> (ks, j, tq)
+        // thread i: head i >> 6, u32 i & 63 of that head's 128 dims -> (ks, j, tq);
+        // rows of the padding heads 4-7 are zero, so a fragment is one plain load
         const int hq = ltid() >> 6, w = ltid() & 63;
         const uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(a.q) +
                                                                     (size_t)b * 4096 + (h * 4 + hq) * 128) + w);
         const int ks = w >> 3, j = (w >> 2) & 1, q4 = w & 3;
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(qs + (((ks * 2 + j) * 4 + hq) * 4 + q4) * 4), "r"(v) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(qs + (((ks * 2 + j) * 8 + hq) * 4 + q4) * 4), "r"(v) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(qs + (((ks * 2 + j) * 8 + 4 + hq) * 4 + q4) * 4), "r"(0u) : "memory");
     }
     body_sync();
+    const uint32_t qfb = qs + (g * 4 + tq) * 4;
     auto qfrag = [&](int ks, int j) -> uint32_t {
         uint32_t v;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(qs + (((ks * 2 + j) * 4 + (g & 3)) * 4 + tq) * 4));
-        return g < 4 ? v : 0u;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(qfb + (ks * 2 + j) * 128));
+        return v;
     };
     const float scale2 = a.scale * 1.4426950408889634f;  // softmax in base 2
     // this thread: heads 2tq, 2tq+1 (real for tq < 2); O^T rows 16 mt + g, + 8
@@ -1157,6 +1160,11 @@ __device__ void body_attn_decode(const BodyCtx& c) {
         for (int j = 0; j < 4; ++j) o[mt][j] = 0.f;
     const int pw = 16 * sub;  // this warp's positions within a chunk
     const int lr = lane & 7, lm = lane >> 3;
+    // per-thread parts of the ldmatrix addresses (kv_addr with the k-step
+    // folded in at compile time): row offset, and the swizzle term XORed
+    // into the 16-B chunk index (row % 8 == lr since pw % 16 == 0)
+    const uint32_t qk_row = (uint32_t)(pw + lr + 8 * (lm & 1)) * 128u, qk_y = (uint32_t)(((lm >> 1) ^ lr) & 7) << 4;
+    const uint32_t pv_row = (uint32_t)(pw + lr + 8 * (lm >> 1)) * 128u, pv_y = (uint32_t)(((lm & 1) ^ lr) & 7) << 4;
     for (int ci = grp; ci < nch; ci += kAttnGroups) {
         const int s = ci % kAttnStages;
 #ifdef DS_ATTN_TRACE
@@ -1184,8 +1192,8 @@ __device__ void body_attn_decode(const BodyCtx& c) {
 #pragma unroll
         for (int ks = 0; ks < 8; ks += 2) {
             uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
-            ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * ks + 8 * (lm >> 1)), a0, a1, a2, a3);
-            ldsm_x4(kv_addr(kt, pw + lr + 8 * (lm & 1), 16 * (ks + 1) + 8 * (lm >> 1)), c0, c1, c2, c3);
+            ldsm_x4(kt + (ks >> 2) * kAttnHalf + qk_row + ((((2 * ks) & 7) << 4) ^ qk_y), a0, a1, a2, a3);
+            ldsm_x4(kt + ((ks + 1) >> 2) * kAttnHalf + qk_row + ((((2 * ks + 2) & 7) << 4) ^ qk_y), c0, c1, c2, c3);
             mma16816(sa, a0, a1, a2, a3, qfrag(ks, 0), qfrag(ks, 1));
             mma16816(sb2, c0, c1, c2, c3, qfrag(ks + 1, 0), qfrag(ks + 1, 1));
         }
@@ -1235,7 +1243,7 @@ __device__ void body_attn_decode(const BodyCtx& c) {
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
             uint32_t a0, a1, a2, a3;
-            ldsm_x4_t(kv_addr(vt, pw + lr + 8 * (lm >> 1), 16 * mt + 8 * (lm & 1)), a0, a1, a2, a3);
+            ldsm_x4_t(vt + (mt >> 2) * kAttnHalf + pv_row + ((((2 * mt) & 7) << 4) ^ pv_y), a0, a1, a2, a3);
             mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
         }
         __syncwarp();
