@@ -717,7 +717,11 @@ __device__ void scheduler_loop(DevState* st, Stage* stage, volatile uint64_t* bo
             for (;;) {
                 // both words requested before either is used: one L2 round trip
                 const uint32_t ex = ld_volatile_u32(&st->ctl.exit);
-                cw = ld_volatile_u64(&st->ctl.word[sm]);
+                // the SM's own control word, by %smid read at the boundary
+                // (a resident CTA never changes SM, so this equals the value
+                // read at start; reading it here keeps the arbiter's contract
+                // "each boundary consults the word of the SM it runs on")
+                cw = ld_volatile_u64(&st->ctl.word[smid()]);
                 if (ex) { exit_now = true; break; }
                 int32_t ow = (int32_t)(uint32_t)cw;
                 const int32_t ln = (int32_t)(uint32_t)(cw >> 32);
