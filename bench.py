@@ -197,10 +197,13 @@ class Colocation:
         self.t_dec = self.dom.tenant("decode", _abi.LATENCY_CRITICAL)
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
         self.dec_kernels = self.model.register(self.dom)
-        # the step as TPOT-First runs it on its 1/2 tier: gate_up as two-slab
-        # blocks, one wave on 148 worker lanes (bit-identical outputs; the
-        # full-GPU runs — solo, time slicing — keep the one-slab blocks)
-        self.dec_kernels_half = self.model.register_variant(self.dom, self.dec_kernels, "gu_pair")
+        # optional: the step as TPOT-First would run it on its 1/2 tier, with
+        # gate_up as two-slab and the LM head as seven-slab blocks (one wave
+        # each on 148 worker lanes; bit-identical outputs).  Measured co-located
+        # (profiles/r2_half_tier_variants_ab.txt): gate_up two-slab +0.18 ms
+        # P50 TPOT, LM head seven-slab neutral — off by default
+        hv = os.environ.get("DS_HALF_VARIANTS", "0")
+        self.dec_kernels_half = self.model.register_variant(self.dom, self.dec_kernels, "" if hv == "0" else hv)
         self.gemm_kernel = self.train.register(self.dom)
         # parity evidence at full size: a per-launch checksum of the decode
         # step's logits and of the training GEMM's C, appended to the records
@@ -400,7 +403,7 @@ class Colocation:
         tpot_slo = int(self.slo_x * step_ns)
         ttft_slo = int(2 * self.slo_x * step_ns)
         period = int(2 * self.T * step_ns)  # decode busy ~50% of the time when solo
-        half = policy == "tpot-first" and self.decode_sat <= Fraction(1, 2) and os.environ.get("DS_GU_PAIR", "1") != "0"
+        half = policy == "tpot-first" and self.decode_sat <= Fraction(1, 2)
         base = self.dec_kernels_half if half else self.dec_kernels
         dec_kernels = base + ([self.k_ck_logits] if pin else [])
         trn_kernels = [self.gemm_kernel] + ([self.k_ck_C] if pin else [])

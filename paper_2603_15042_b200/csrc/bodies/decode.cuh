@@ -45,9 +45,9 @@ struct GemvArgs {
                         // the dependency resolves (0 = ring only)
     int32_t sk;         // 1: stream-K over the logical grid (equal runs of (slab, k-block) units, <= 2 slabs
                         // per block); 0: split-K S with grid nb * S
-    int32_t pair;       // kGemvSiluMul only (whose weights always interleave gate/up rows: 2i gate, 2i+1 up
-                        // of feature i): 1 = two whole slabs per block (grid nb / 2), slab 0's epilogue
-                        // overlapping slab 1's stream
+    int32_t pair;       // P >= 2: P whole 128-row slabs per block (grid ceil(nb / P)), one continuous weight
+                        // stream, slab j's epilogue overlapping slab j+1's; kGemvSiluMul (whose weights always
+                        // interleave gate/up rows: 2i gate, 2i+1 up of feature i) or kGemvStore
 };
 
 constexpr int kGemvBN = 32;
@@ -171,11 +171,10 @@ __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, con
             for (int k = 0; k < kTcBK / 16; ++k)
                 tc::mma_bf16(tmem_base + 32 * p, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, !(first && k == 0));
             tc::mma_commit(&empty[s]);
-            if (a.pair && i == n0 - 1) tc::mma_commit(&tmem_full[0]);  // slab 0's accumulator is final
         }
-        tc::mma_commit(&tmem_full[a.pair ? 1 : 0]);
+        tc::mma_commit(&tmem_full[0]);
     }
-    if (warp >= 4 && !a.pair) {
+    if (warp >= 4) {
         tc::mbar_wait(tmem_full, 0);
         tc::tc_fence_after();
     }
@@ -213,6 +212,142 @@ __device__ __forceinline__ void gemv_silu_pair_epilogue(const BodyCtx& c, const 
     }
 }
 
+// Multi-slab blocks (a.pair = P >= 2, 128-row slabs, no split): block t
+// computes whole slabs [P t, P t + P) as one continuous weight stream (the
+// packed tiles of consecutive slabs are contiguous).  Slab j accumulates in
+// TMEM columns 32 (j % 2); the epilogue warps finish slab j while the ring
+// streams slab j+1, and hand the columns back (tmem_empty) before slab j+2.
+// Each slab is still one k-ordered accumulation, so the outputs are
+// bit-identical to the one-slab records.  Modes: kGemvSiluMul (interleaved
+// gate/up rows) and kGemvStore (e.g. the LM head).
+template <int STAGES>
+__device__ __forceinline__ void store_slab_epilogue(const BodyCtx& c, const GemvArgs& a, int slab, uint32_t col,
+                                                    const float* rvec) {
+    const int q = (ltid() >> 5) & 3, lane = ltid() & 31;
+    uint32_t raw[32];
+    tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + col, raw);
+    tc::tmem_ld_wait();
+    uint16_t* out = reinterpret_cast<uint16_t*>(a.out);
+    const int n = slab * 128 + q * 32 + lane;
+#pragma unroll 8
+    for (int b = 0; b < 32; ++b) out[(size_t)b * a.N + n] = f_to_bf16(__uint_as_float(raw[b]) * rvec[b]);
+}
+
+template <int STAGES>
+__device__ void gemv_multi(const BodyCtx& c, const GemvArgs& a, uint64_t* dbg) {
+    using L = TcSmem<kGemvBN, STAGES, kTcBK, 128>;
+    char* base = align1024(c.smem);
+    const int nb = a.N / 128, KB = a.K / kTcBK;
+    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int s0 = a.pair * t, ns = min(a.pair, nb - s0), total = ns * KB;
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2] slab accumulator final
+    uint64_t* tempty = tfull + 2;      // [2] its TMEM columns read (4 epilogue warps)
+    float* red = reinterpret_cast<float*>(base + L::kBarOff + 256);  // [4][32]
+    float* rv = red + 128;                                            // [32]
+    const int warp = ltid() >> 5, lane = ltid() & 31;
+    const char* a_packed = reinterpret_cast<const char*>(a.w_packed) + (size_t)s0 * KB * L::kABytes;
+    if (ltid() == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            tc::mbar_init(&tfull[k], 1);
+            tc::mbar_init(&tempty[k], 4);
+        }
+        tc::fence_mbar_init();
+    }
+    body_sync();
+    if (warp == 0 && lane == 0) {
+        if (desc_fence_needed(c.st ? &a : nullptr)) tc::tma_fence_desc(&a.tmX);
+        const uint64_t pol = tc::policy_evict_first();
+        auto issue_a = [&](int i) {
+            tc::bulk_g2s_hint(base + (i % STAGES) * L::kStageBytes, a_packed + (size_t)i * L::kABytes, L::kABytes,
+                              &full[i % STAGES], pol);
+        };
+        auto issue_b = [&](int i) {
+            tc::tma_load_2d(base + (i % STAGES) * L::kStageBytes + L::kABytes, &a.tmX, &full[i % STAGES],
+                            (i % KB) * kTcBK, 0);
+        };
+        // weights stream while the previous launch finishes; X only after wait_prev
+        const int pre = min(STAGES, total);
+        for (int i = 0; i < pre; ++i) {
+            tc::mbar_arrive_expect_tx(&full[i], L::kStageBytes);
+            issue_a(i);
+        }
+        if (a.l2_pf_kb && total > pre && wait_prev_streamed(c)) {
+            const uint32_t tot = min((uint32_t)(total - pre) * L::kABytes, (uint32_t)a.l2_pf_kb << 10);
+            for (uint32_t off = 0; off < tot; off += L::kABytes)
+                tc::bulk_prefetch_l2(a_packed + (size_t)pre * L::kABytes + off, min(L::kABytes, tot - off));
+        }
+        wait_prev(c);
+        if (dbg) dbg[7] = globaltimer();
+        for (int i = 0; i < pre; ++i) issue_b(i);
+        for (int i = pre; i < total; ++i) {
+            const int s = i % STAGES;
+            tc::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+            issue_a(i);
+            issue_b(i);
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(128, kGemvBN);
+        for (int i = 0; i < total; ++i) {
+            const int j = i / KB, kk = i - j * KB, s = i % STAGES;
+            if (kk == 0 && j >= 2) {
+                tc::mbar_wait(&tempty[j & 1], ((j >> 1) - 1) & 1);  // slab j-2's columns read
+                tc::tc_fence_after();
+            }
+            tc::mbar_wait(&full[s], (i / STAGES) & 1);
+            tc::tc_fence_after();
+            char* sa = base + s * L::kStageBytes;
+            const uint64_t ad = tc::smem_desc_k_sw128(sa), bd = tc::smem_desc_k_sw128(sa + L::kABytes);
+#pragma unroll
+            for (int k = 0; k < kTcBK / 16; ++k)
+                tc::mma_bf16(c.tmem_base + 32 * (j & 1), ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                             !(kk == 0 && k == 0));
+            tc::mma_commit(&empty[s]);
+            if (kk == KB - 1) tc::mma_commit(&tfull[j & 1]);
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3;
+        if (ltid() == 128) wait_prev(c);  // acquire for the statistics of earlier launches
+        epi_sync();
+        float ss = 0.f;
+        if (a.stats_in) {
+            const float* st = reinterpret_cast<const float*>(a.stats_in);
+#pragma unroll 8
+            for (int p = q * a.P_in / 4; p < (q + 1) * a.P_in / 4; ++p) ss += __ldcg(st + p * 32 + lane);
+        }
+        red[q * 32 + lane] = ss;
+        epi_sync();
+        if (warp == 4)
+            rv[lane] = a.stats_in ? rsqrtf((((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane]) /
+                                               (float)a.K + a.eps)
+                                  : 1.f;
+        epi_sync();
+        for (int j = 0; j < ns; ++j) {
+            tc::mbar_wait(&tfull[j & 1], (j >> 1) & 1);
+            tc::tc_fence_after();
+            if (dbg && ltid() == 128 && j < 2) dbg[1 + j] = globaltimer();
+            if (j == ns - 1 && ltid() == 128) mark_streamed(c);  // every load of the block has landed
+            if (a.mode == kGemvSiluMul) gemv_silu_pair_epilogue(c, a, s0 + j, 32u * (j & 1), rv);
+            else store_slab_epilogue<STAGES>(c, a, s0 + j, 32u * (j & 1), rv);
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[j & 1]);
+        }
+    }
+    if (dbg && ltid() == 128) dbg[5] = globaltimer();
+    tc::tc_fence_before();
+    body_sync();
+    if (ltid() == 0)
+        for (int k = 0; k < 2 * STAGES + 4; ++k) tc::mbar_inval(&full[k]);
+    if (dbg && ltid() == 0) dbg[6] = globaltimer();
+}
+
 // BM = 128 or 64 weight rows per slab (M = 64: smaller blocks for the small
 // projections; rows 16q..16q+15 sit in TMEM lanes 32q.. of epilogue warp q).
 // Block -> work: classic split-K (a.sk = 0: t -> slab t % nb, split t / nb,
@@ -248,10 +383,6 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
             pB = GemvPiece{n + 1, 0, (int)(u1 - (int64_t)(n + 1) * KB), 0, lastB - t + 1, false};
             np = 2;
         }
-    } else if (a.pair) {
-        pA = GemvPiece{2 * t, 0, KB, 0, 1, true};
-        pB = GemvPiece{2 * t + 1, 0, KB, 0, 1, true};
-        np = 2;
     } else {
         const int n = t % nb, s = t / nb;
         pA = GemvPiece{n, (int)((int64_t)s * KB / a.S), (int)((int64_t)(s + 1) * KB / a.S), s, a.S, s == a.S - 1};
@@ -261,48 +392,6 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     BodyCtx cd = c;
     cd.dbg = dbg;
     gemv_mainloop<BM, STAGES>(base, a, pA, pB, np, c.tmem_base, cd);
-    if (a.pair) {
-        // two whole slabs, no exchange: the epilogue warps finish slab 0 while
-        // the ring streams slab 1 (their scratch is the barrier block's tail,
-        // not the ring)
-        using L = TcSmem<kGemvBN, STAGES, kTcBK, BM>;
-        uint64_t* tmem_full = reinterpret_cast<uint64_t*>(base + L::kBarOff) + 2 * STAGES;
-        float* red = reinterpret_cast<float*>(base + L::kBarOff + 256);  // [4][32]
-        float* rv = red + 128;                                            // [32]
-        const int warp = ltid() >> 5, lane = ltid() & 31;
-        if (warp >= 4) {
-            const int q = warp & 3;
-            if (ltid() == 128) wait_prev(c);  // acquire for the statistics of earlier launches
-            epi_sync();
-            float ss = 0.f;
-            if (a.stats_in) {
-                const float* st = reinterpret_cast<const float*>(a.stats_in);
-#pragma unroll 8
-                for (int p = q * a.P_in / 4; p < (q + 1) * a.P_in / 4; ++p) ss += __ldcg(st + p * 32 + lane);
-            }
-            red[q * 32 + lane] = ss;
-            epi_sync();
-            if (warp == 4)
-                rv[lane] = a.stats_in ? rsqrtf((((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane]) /
-                                                   (float)a.K + a.eps)
-                                      : 1.f;
-            epi_sync();
-            tc::mbar_wait(&tmem_full[0], 0);
-            tc::tc_fence_after();
-            if (dbg && ltid() == 128) dbg[1] = globaltimer();
-            gemv_silu_pair_epilogue(c, a, pA.n, 0u, rv);
-            tc::mbar_wait(&tmem_full[1], 0);
-            tc::tc_fence_after();
-            if (dbg && ltid() == 128) dbg[2] = globaltimer();
-            if (ltid() == 128) mark_streamed(c);  // every weight / X load of this block has landed
-            gemv_silu_pair_epilogue(c, a, pB.n, 32u, rv);
-        }
-        if (dbg && ltid() == 128) dbg[5] = globaltimer();
-        tc_teardown<kGemvBN, STAGES, kTcBK, BM>(base);
-        if (ltid() == 0) tc::mbar_inval(tmem_full + 1);
-        if (dbg && ltid() == 0) dbg[6] = globaltimer();
-        return;
-    }
     if (ltid() == 128) mark_streamed(c);  // tmem_full: every weight / X load of this block has landed
     wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
@@ -513,6 +602,11 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
 
 __device__ void body_gemv_bf16(const BodyCtx& c) {
     const GemvArgs& a = *reinterpret_cast<const GemvArgs*>(c.args);
+    if (a.pair >= 2) {
+        const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+        gemv_multi<kGemvStages>(c, a, a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr);
+        return;
+    }
     if (a.bm == 64) gemv_body<64, kGemvStages64>(c, a);
     else gemv_body<128, kGemvStages>(c, a);
 }

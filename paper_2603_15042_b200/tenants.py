@@ -245,7 +245,7 @@ class DecodeModel:
                 # the same projection as two-slab blocks (bit-identical: every
                 # slab is still one block's k-ordered accumulation)
                 ap = _abi.GemvArgs.from_buffer_copy(a)
-                ap.pair = 1
+                ap.pair = 2
                 self.variant_records.setdefault("gu_pair", {})[len(self.records) - 1] = (
                     "decode/gate_up", _abi.BODY_GEMV_BF16, (g[0] // 2, 1, 1), ap, 2 * c.ffn * c.d * 2)
             a, g = self._gemv(self.Wd[l], self.act, c.d, c.ffn, self.S["down"], _abi.GEMV_RESID, hout,
@@ -257,6 +257,13 @@ class DecodeModel:
                           stats_in=self.st_h, P_in=c.d // self.BM["down"], bm=self.BM["lm"], pf=self.PF["lm"],
                           G=self.G["lm"])
         self.records.append(("decode/lm_head", _abi.BODY_GEMV_BF16, g, a, c.vocab * c.d * 2))
+        if not self.G["lm"] and self.S["lm"] == 1 and self.BM["lm"] == 128:
+            # the LM head as 7-slab blocks (144 blocks: one wave on 148 lanes, one continuous
+            # 7 MB stream per lane); bit-identical to the one-slab record
+            am = _abi.GemvArgs.from_buffer_copy(a)
+            am.pair = 7
+            self.variant_records.setdefault("lm_multi", {})[len(self.records) - 1] = (
+                "decode/lm_head", _abi.BODY_GEMV_BF16, (-(-(c.vocab // 128) // 7), 1, 1), am, c.vocab * c.d * 2)
         chunks = max(1, min(4, c.vocab // 2048))  # 128 blocks: one wave; every block pays a claim + ticket
         am = _abi.ArgmaxArgs(self.logits.data_ptr(), self.tokens.data_ptr(), self.amax_ws.data_ptr(),
                              self.amax_counters.data_ptr(), c.vocab, chunks)
@@ -275,15 +282,19 @@ class DecodeModel:
     def register(self, dom, phase=_abi.DECODE) -> List[int]:
         return [dom.kernel(sid, body, grid, args, phase=phase) for sid, body, grid, args, _ in self.records]
 
-    def register_variant(self, dom, ids: List[int], name: str = "gu_pair", phase=_abi.DECODE) -> List[int]:
-        """The step's kernel ids with variant `name`'s records registered in
-        place of the base ones (other ids shared).  "gu_pair": gate_up as 112
-        two-slab blocks — one wave at the decode tenant's 1/2 tier (148
-        worker lanes) where the 224 one-slab blocks need two; outputs are
-        bit-identical to the base step."""
+    HALF_TIER = "gu_pair,lm_multi"
+
+    def register_variant(self, dom, ids: List[int], names: str = HALF_TIER, phase=_abi.DECODE) -> List[int]:
+        """The step's kernel ids with the named variants' records registered in
+        place of the base ones (other ids shared; names comma-separated).
+        "gu_pair": gate_up as 112 two-slab blocks — one wave at the decode
+        tenant's 1/2 tier (148 worker lanes) where the 224 one-slab blocks
+        need two; "lm_multi": the LM head as 144 seven-slab blocks.  Outputs
+        are bit-identical to the base step."""
         out = list(ids)
-        for i, (sid, body, grid, args, _) in self.variant_records.get(name, {}).items():
-            out[i] = dom.kernel(sid, body, grid, args, phase=phase)
+        for name in filter(None, names.split(",")):
+            for i, (sid, body, grid, args, _) in self.variant_records.get(name, {}).items():
+                out[i] = dom.kernel(sid, body, grid, args, phase=phase)
         return out
 
     def prefill_records(self, prompt_tokens: int = 256):

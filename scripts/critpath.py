@@ -15,6 +15,8 @@ print("S", m.S, "BM", m.BM, flush=True)
 dom = Domain(0, tiers=[Fraction(1)], block_log_capacity=1 << 22)
 t = dom.tenant("decode", 0)
 kids = m.register(dom)
+if os.environ.get("VARIANTS"):  # e.g. "gu_pair,lm_multi": the decode tier's bit-identical variants
+    kids = m.register_variant(dom, kids, os.environ["VARIANTS"])
 dom.start()
 dom.quota_set(dom.mask(t, 0, nsm))
 for _ in range(3):

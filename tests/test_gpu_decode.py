@@ -121,7 +121,7 @@ def test_full_decode_step_matches_torch_fp32_and_coroutine_bit_exact():
         t = dom.tenant("decode", _abi.LATENCY_CRITICAL)
         # the co-located variant (gate_up as two-slab blocks) against the
         # plain split-K solo step: bit-identical by construction
-        kids = m.register_variant(dom, m.register(dom), "gu_pair") + [ck.register(dom, "decode/logits_checksum")]
+        kids = m.register_variant(dom, m.register(dom)) + [ck.register(dom, "decode/logits_checksum")]
         dom.start()
         dom.quota_set(dom.mask(t, 0, dom.num_sms // 4))
         dom.quota_at_claim(t, 80, 0, dom.mask(t, 0, dom.num_sms))
@@ -134,11 +134,12 @@ def test_full_decode_step_matches_torch_fp32_and_coroutine_bit_exact():
     assert ck.of_seq(slots, last) == OutputChecksum.host(solo_logits)
 
 
-def test_gate_up_pair_variant_bit_exact_vs_solo():
-    """gate_up as 112 two-slab blocks (register_variant "gu_pair") under mid-step
-    quota changes equals the 224-block solo step bit for bit."""
+def test_half_tier_variants_bit_exact_vs_solo():
+    """gate_up as 112 two-slab blocks and the LM head as 7-slab blocks
+    (register_variant: "gu_pair", "lm_multi") under mid-step quota changes
+    equal the one-slab solo step bit for bit."""
     m = small_model()
-    assert "gu_pair" in m.variant_records
+    assert "gu_pair" in m.variant_records and "lm_multi" in m.variant_records
     tok0 = m.tokens.clone()
     kc0 = [k.clone() for k in m.kc]
     vc0 = [v.clone() for v in m.vc]
@@ -154,7 +155,7 @@ def test_gate_up_pair_variant_bit_exact_vs_solo():
     torch.cuda.synchronize()
     with Domain(0, tiers=[Fraction(1)], block_log_capacity=0) as dom:
         t = dom.tenant("decode", _abi.LATENCY_CRITICAL)
-        kids = m.register_variant(dom, m.register(dom), "gu_pair")
+        kids = m.register_variant(dom, m.register(dom))
         dom.start()
         dom.quota_set(dom.mask(t, 0, 74))
         dom.quota_at_claim(t, 4, 30, dom.mask(t, 10, 50))
