@@ -603,6 +603,13 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
 __device__ void body_gemv_bf16(const BodyCtx& c) {
     const GemvArgs& a = *reinterpret_cast<const GemvArgs*>(c.args);
     if (a.pair >= 2) {
+        // multi-slab records need 128-row packed slabs and a per-slab epilogue
+        // (SiLU pairing or plain store); anything else is a malformed record:
+        // the tenant fails alone instead of writing wrong outputs
+        if ((a.mode != kGemvSiluMul && a.mode != kGemvStore) || a.bm == 64 || !a.w_packed || a.sk) {
+            if (ltid() == 0) raise_fault(c, DS_FAULT_BAD_INPUT);
+            return;
+        }
         const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
         gemv_multi<kGemvStages>(c, a, a.dbg ? reinterpret_cast<uint64_t*>(a.dbg) + (size_t)t * 8 : nullptr);
         return;

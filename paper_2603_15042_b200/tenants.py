@@ -129,6 +129,7 @@ class DecodeModel:
         # epilogue around its weight stream, so the fewest splits that still
         # fill the lanes win — no split at all for gate_up and the LM head
         self.S.update({"qkv": 3, "o": 4, "gu": 1, "down": 4, "lm": 1})
+        split_override = split_override or os.environ.get("DS_SPLITS", "")
         if split_override:  # e.g. "o:4,down:5"
             for kv in split_override.split(","):
                 k, v = kv.split(":")
