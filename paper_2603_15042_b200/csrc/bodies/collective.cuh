@@ -50,6 +50,10 @@ struct AllreduceArgs {
     int32_t chunk;                // elements per logical block (multiple of 8)
     int32_t pad;
 };
+static_assert(offsetof(AllreduceArgs, out) == 128 && offsetof(AllreduceArgs, outs) == 136 &&
+                  offsetof(AllreduceArgs, n) == 200 && offsetof(AllreduceArgs, rank) == 212 &&
+                  offsetof(AllreduceArgs, chunk) == 216,
+              "AllreduceArgs layout (mirrored in _abi.py)");
 
 __device__ __forceinline__ uint64_t ld_acquire_sys_u64_(const void* p) {
     uint64_t v;

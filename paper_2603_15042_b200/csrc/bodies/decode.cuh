@@ -50,6 +50,12 @@ struct GemvArgs {
                         // interleave gate/up rows: 2i gate, 2i+1 up of feature i) or kGemvStore
 };
 
+// the host builds these records with ctypes mirrors (_abi.py): pinned offsets
+static_assert(offsetof(GemvArgs, out) == 256 && offsetof(GemvArgs, N) == 320 && offsetof(GemvArgs, dbg) == 360 &&
+                  offsetof(GemvArgs, w_packed) == 368 && offsetof(GemvArgs, bm) == 376 &&
+                  offsetof(GemvArgs, sk) == 384 && offsetof(GemvArgs, pair) == 388,
+              "GemvArgs layout (mirrored in _abi.py)");
+
 constexpr int kGemvBN = 32;
 constexpr int kGemvStages = kCtasPerSm == 2 ? 5 : 8;     // 20-KB stages (128-row W tile + X)
 constexpr int kGemvStages64 = kCtasPerSm == 2 ? 8 : 12;  // 12-KB stages (64-row W tile + X)
@@ -680,6 +686,11 @@ struct AttnArgs {
                         // launch has streamed (0 = ring only)
     int32_t tc;         // 1: both products on tcgen05 with TMEM accumulators (body_attn_decode_tc)
 };
+
+static_assert(offsetof(AttnArgs, q) == 256 && offsetof(AttnArgs, L) == 288 && offsetof(AttnArgs, scale) == 300 &&
+                  offsetof(AttnArgs, dbg) == 304 && offsetof(AttnArgs, kbase) == 312 &&
+                  offsetof(AttnArgs, l2_pf_kb) == 328 && offsetof(AttnArgs, tc) == 332,
+              "AttnArgs layout (mirrored in _abi.py)");
 
 // KV positions per pipeline stage (one TMA box height).  A stage holds the
 // chunk's K and V rows as four SWIZZLE_128B half-tiles [chunk][64 dims]

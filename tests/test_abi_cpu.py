@@ -43,6 +43,13 @@ def test_args_struct_layout():
     assert ctypes.sizeof(_abi.SgemmArgs) == 40
     assert ctypes.sizeof(_abi.Completion) == 48
     assert ctypes.sizeof(_abi.BlockRecord) == 32
+    # field offsets pinned by static_asserts in bodies/decode.cuh and collective.cuh
+    want = {_abi.GemvArgs: {"out": 256, "N": 320, "dbg": 360, "w_packed": 368, "bm": 376, "sk": 384, "pair": 388},
+            _abi.AttnArgs: {"q": 256, "L": 288, "scale": 300, "dbg": 304, "kbase": 312, "l2_pf_kb": 328, "tc": 332},
+            _abi.AllreduceArgs: {"out": 128, "outs": 136, "n": 200, "rank": 212, "chunk": 216}}
+    for S, fields in want.items():
+        for name, off in fields.items():
+            assert getattr(S, name).offset == off, (S.__name__, name)
 
 
 def test_domain_create_fails_loudly_without_gpu():
