@@ -1218,7 +1218,14 @@ def config3_leg(dev):
         rtt = [x / 1e3 for x in dom.ctl_roundtrip(100)]
     return {"workload": "config 3: quota flips 100% <-> 25% of the SMs by the device timer (no host round trip)",
             "sweep": rows, "gemm_tiles": gemm_rows,
-            "host_device_ctl_roundtrip_us": {"p50": round(mg.pct(rtt, .5), 2), "p99": round(mg.pct(rtt, .99), 2)}}
+            "host_device_ctl_roundtrip_us": {"p50": round(mg.pct(rtt, .5), 2), "p99": round(mg.pct(rtt, .99), 2)},
+            # a host (policy) driven quota change: half the measured round trip
+            # (host write -> device install; the ack returns the other half)
+            # plus the device-measured grant (install -> the new owner's first
+            # block on a granted SM, 5-us blocks)
+            "host_driven_migration_us": {
+                "p50": round(mg.pct(rtt, .5) / 2 + rows[0]["grant_us_p50"], 2),
+                "what": "ctl round trip p50 / 2 (one way, upper bound) + device grant p50 of the 50-us-period row"}}
 
 
 def config5_leg(args, rank, world, dev, gather_fn):

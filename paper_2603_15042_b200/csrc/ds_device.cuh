@@ -138,8 +138,16 @@ static_assert(sizeof(HostFault) == 32, "fault record");
 // "hot" block read with a single warp-wide 16-B/lane load per poll:
 //   hot[0] control generation, hot[1] exit, hot[2] periodic-program generation,
 //   hot[3] fault-request generation, hot[64 + t] launch tail of tenant t.
+// Compact control image, polled in the same PCIe round trip as hot[]: one
+// 32-bit entry per smid = owner (7 bits, 0x7f none) | lender << 7 (7 bits)
+// | split << 14 | owner-only-lane-0 << 15 | generation tag << 16.  The
+// loader installs it from the poll that announced the generation when every
+// entry carries that generation's tag (32-bit host stores are atomic), so a
+// control change costs no second round trip; a torn read waits one poll.
+constexpr uint32_t kImgNone = 0x7fu;
 struct HostMailbox {
     volatile uint32_t hot[128];
+    volatile uint32_t ctl_img[DS_MAX_SMS];
     volatile unsigned long long periodic_ns;
     volatile int32_t owner[DS_MAX_SMS];   // by smid
     volatile int32_t lender[DS_MAX_SMS];

@@ -182,7 +182,9 @@ __device__ void install_ctl(DevState* st, const int32_t* owner, const int32_t* l
             l[j] = lender[i];
         }
     }
-    if (volatile_src) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    // (host-image loads are ordered after the generation that announced
+    // them by the loader's poll fence; the stores below depend on their
+    // values, so no further system fence is needed here)
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
         const unsigned long long w = ((unsigned long long)(uint32_t)l[j] << 32) | (uint32_t)o[j];
@@ -227,11 +229,35 @@ __device__ void loader_loop(DevState* st) {
                      : "=r"(hv.x), "=r"(hv.y), "=r"(hv.z), "=r"(hv.w)
                      : "l"(&mb->hot[4 * lane])
                      : "memory");
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        // the compact control image (8 smids per lane), same round trip
+        uint4 iv0, iv1;
+        asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(iv0.x), "=r"(iv0.y), "=r"(iv0.z), "=r"(iv0.w)
+                     : "l"(&mb->ctl_img[8 * lane])
+                     : "memory");
+        asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(iv1.x), "=r"(iv1.y), "=r"(iv1.z), "=r"(iv1.w)
+                     : "l"(&mb->ctl_img[8 * lane + 4])
+                     : "memory");
         const uint32_t ex = __shfl_sync(0xffffffffu, hv.y, 0);
         const uint32_t g = __shfl_sync(0xffffffffu, hv.x, 0);
         const uint32_t pg = __shfl_sync(0xffffffffu, hv.z, 0);
         const uint32_t fg = __shfl_sync(0xffffffffu, hv.w, 0);
+        // acquire (system scope) only when the host published something: the
+        // reads that follow (launch slots, control image, fault codes) must
+        // not pass the poll; an idle poll skips the fence and comes round
+        // sooner
+        {
+            bool tail_moved = false;
+            if (lane >= kHotTail / 4 && lane < (kHotTail + DS_MAX_TENANTS) / 4) {
+                const int t0 = 4 * lane - kHotTail;
+                tail_moved = hv.x != known_tail[t0] || hv.y != known_tail[t0 + 1] || hv.z != known_tail[t0 + 2] ||
+                             hv.w != known_tail[t0 + 3];
+            }
+            const bool changed = __any_sync(0xffffffffu, tail_moved) || g != last_gen || pg != last_pgen ||
+                                 fg != last_fgen || ex != 0u;
+            if (changed) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        }
         // a program enqueued before ds_start runs to completion and the
         // executor exits on its own (ds_set_drain_exit): usable when the host
         // cannot talk to a resident kernel, e.g. under a serialising profiler
@@ -325,14 +351,48 @@ __device__ void loader_loop(DevState* st) {
             }
             __syncwarp();
         }
-        // control word
+        // control word: from the image read in this poll when every entry
+        // carries the new generation's tag, else from the full arrays
         if (g != last_gen) {
-            install_ctl(st, (const int32_t*)mb->owner, (const int32_t*)mb->lender, true, 0, lane);
-            last_gen = g;
-            if (lane == 0) {
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&mb->ack_gen), "r"(g) : "memory");
+            const uint32_t tag = g & 0xffffu;
+            const uint32_t im[8] = {iv0.x, iv0.y, iv0.z, iv0.w, iv1.x, iv1.y, iv1.z, iv1.w};
+            bool fresh = true;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) fresh &= (im[k] >> 16) == tag;
+            if (__all_sync(0xffffffffu, fresh)) {
+                const uint64_t t0 = globaltimer();
+                if (lane == 0) asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&st->ctl.t_install), "l"(t0) : "memory");
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t e = im[k], ot = e & 0x7fu, lt = (e >> 7) & 0x7fu;
+                    int32_t o = ot == kImgNone ? -1 : (int32_t)ot;
+                    if (o >= 0) o |= ((e >> 14) & 1u ? kCtlSplit : 0) | ((e >> 15) & 1u ? kCtlOwnerOnly0 : 0);
+                    const int32_t l = lt == kImgNone ? -1 : (int32_t)lt;
+                    const unsigned long long w = ((unsigned long long)(uint32_t)l << 32) | (uint32_t)o;
+                    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&st->ctl.word[8 * lane + k]), "l"(w) : "memory");
+                }
+                __syncwarp();
+                __threadfence();
+                if (lane == 0) {
+                    const uint32_t gg = atomicAdd(&st->ctl.gen, 1u) + 1u;
+                    if (st->clog_cap) {
+                        const unsigned long long i = atomicAdd(&st->clog_count, 1ull);
+                        if (i < st->clog_cap) {
+                            ds_ctl_record r;
+                            r.ctl_gen = gg;
+                            r.source = 0;
+                            r.t = t0;
+                            st->clog[i] = r;
+                        }
+                    }
+                }
+                __syncwarp();
+            } else {
+                install_ctl(st, (const int32_t*)mb->owner, (const int32_t*)mb->lender, true, 0, lane);
             }
+            last_gen = g;
+            // release (system scope): the installed words before the host sees the ack
+            if (lane == 0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&mb->ack_gen), "r"(g) : "memory");
         }
         // periodic device-timer program (config 3 migration sweep): both
         // control words are copied into HBM once per program change, so a flip

@@ -228,10 +228,21 @@ void control_by_smid(ds_domain* d, volatile int32_t* owner_sm, volatile int32_t*
 }
 
 int push_control(ds_domain* d) {
-    // slot-space owner/lender -> smid-space mailbox, then bump the generation
+    // slot-space owner/lender -> smid-space mailbox (full arrays and the
+    // compact tagged image the loader installs from its poll), then bump the
+    // generation
     control_by_smid(d, d->mb->owner, d->mb->lender);
+    const uint32_t gen = d->mb->hot[ds::kHotGen] + 1;
+    const uint32_t tag = (gen & 0xffffu) << 16;
+    for (int i = 0; i < DS_MAX_SMS; ++i) {
+        const int32_t o = d->mb->owner[i], l = d->mb->lender[i];
+        const uint32_t ot = o < 0 ? ds::kImgNone : (uint32_t)(o & ds::kCtlTenantMask) & 0x3fu;
+        const uint32_t lt = l < 0 ? ds::kImgNone : (uint32_t)l & 0x3fu;
+        const uint32_t fl = o < 0 ? 0u : (((o & ds::kCtlSplit) ? 1u : 0u) << 14) | (((o & ds::kCtlOwnerOnly0) ? 1u : 0u) << 15);
+        d->mb->ctl_img[i] = tag | fl | (lt << 7) | ot;
+    }
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    d->mb->hot[ds::kHotGen] = d->mb->hot[ds::kHotGen] + 1;
+    d->mb->hot[ds::kHotGen] = gen;
     std::atomic_thread_fence(std::memory_order_seq_cst);
     return DS_OK;
 }
