@@ -591,12 +591,19 @@ class Colocation:
                                decode_index=k, request_arrival_ns=arr, ttft_ns=ttft_slo_ns, tpot_ns=tpot_slo_ns,
                                base_hint_ns=step_ns, saturation=self.decode_sat) for k in range(tokens)]
             reqs.append((arr, pf, recs))
-        for _, _, recs in reqs:
-            eng.wait(recs[-1], timeout_ms=120000)
-        stop.set()
-        th.join()
-        for r in train_recs:
-            eng.wait(r)
+        try:
+            for _, _, recs in reqs:
+                eng.wait(recs[-1], timeout_ms=120000)
+            stop.set()
+            th.join()
+            for r in train_recs:
+                eng.wait(r, timeout_ms=120000)
+        except Exception:
+            log("TIMEOUT prefill mix", policy, eng.counters(),
+                [(eng.record(pf).state, [eng.record(r).state for r in recs]) for _, pf, recs in reqs],
+                [eng.record(r).state for r in train_recs])
+            log(dom.debug())
+            raise
         out = []
         for arr, pf, recs in reqs:
             inf = [eng.record(r) for r in recs]
@@ -1007,6 +1014,14 @@ def gpu_arm(args, rank, world):
                     prefill_mix=not args.no_config4b)
     solo = co.solo(steps=max(3, args.warmup))
     log("solo", {k: v for k, v in solo.items() if k != "per_kernel_ns" and k != "per_kernel_launches"})
+    if args.only_config4b:
+        try:
+            r = config4b_leg(co, args, solo)
+        except Exception as e:
+            r = {"error": repr(e)}
+        co.close()
+        print(json.dumps({"config4b": r}))
+        sys.exit(0)
     # one bench step = args.rps requests (P99 over steps x rps samples)
     n_req, n_warm = args.steps * args.rps, args.warmup * args.rps
     with ClockSampler(dev) as clk:
@@ -1478,6 +1493,7 @@ def main():
     ap.add_argument("--c5-drain-s", type=float, default=30.0, help="config 5 drain deadline")
     ap.add_argument("--only-config5", action="store_true", help="run the config 5 leg alone (debug)")
     ap.add_argument("--no-config4b", action="store_true", help="skip the two-stream prefill mix leg")
+    ap.add_argument("--only-config4b", action="store_true", help="run the two-stream prefill mix leg alone (debug)")
     ap.add_argument("--no-config4", action="store_true", help="skip the config 4 (ResNet + bursty decode) leg")
     ap.add_argument("--burst-units", type=float, default=60.0, help="config 4 trace duration (units of 50 ms)")
     ap.add_argument("--tiers", default="1/4,1/2,3/4,1", help="pctx pool tiers (create_pool; SPEC.md:65 pool)")

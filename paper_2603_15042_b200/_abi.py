@@ -173,7 +173,8 @@ class GemmArgs(ctypes.Structure):
     _fields_ = [("tmA", TmaDesc), ("tmB", TmaDesc), ("C", ctypes.c_uint64), ("M", ctypes.c_int32),
                 ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32),
                 ("splits", ctypes.c_int32), ("ws", ctypes.c_uint64), ("bk", ctypes.c_int32),
-                ("tma_store", ctypes.c_int32), ("abandon", ctypes.c_int32), ("pad2", ctypes.c_uint8 * 12),
+                ("tma_store", ctypes.c_int32), ("abandon", ctypes.c_int32), ("l2_hint", ctypes.c_int32),
+                ("pad2", ctypes.c_uint8 * 8),
                 ("tmC", TmaDesc)]  # tmC: alignas(64)
 
 
@@ -213,7 +214,7 @@ GEMM_BM, GEMM_BN = 128, 256
 
 def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16, bn: int = GEMM_BN,
               splits: int = 1, ws: int = 0, bk: int = 64, tma_store: bool = True,
-              abandon: bool = False) -> "GemmArgs":
+              abandon: bool = False, l2_hint: int = 0) -> "GemmArgs":
     if bn not in (64, 128, 256):
         raise DsError(10, f"gemm tile width {bn} not in (64, 128, 256)")
     if M % GEMM_BM or N % bn or K % 64:
@@ -227,6 +228,9 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
                  max(1, splits), ws, bk, int(tma_store))
     a.tmC = tmC
     a.abandon = int(abandon)  # False/0 off, True/1 restart, 2 spill + resume
+    # L2 policy of the operand loads: bits [1:0] A, [3:2] B; 0 default (A evict_last, B none),
+    # 1 evict_first, 2 evict_last, 3 evict_normal
+    a.l2_hint = int(l2_hint)
     return a
 
 

@@ -87,7 +87,7 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
                                             const char* a_packed = nullptr, int a_kblocks = 0,
                                             const BodyCtx* dep = nullptr, const BodyCtx* yc = nullptr,
                                             bool acc_init = false, uint32_t l2_pf_bytes = 0,
-                                            const void* fence_key = nullptr) {
+                                            const void* fence_key = nullptr, uint32_t l2_hint = 0) {
     using L = TcSmem<BN, STAGES, BK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -109,7 +109,14 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
             if (!a_packed) tc::tma_fence_desc(tmA);
             tc::tma_fence_desc(tmB);
         }
-        const uint64_t pol = a_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
+        // l2_hint bits [1:0] A, [3:2] B: 0 default (A: a_evict_first ? first : last; B: none),
+        // 1 evict_first, 2 evict_last, 3 evict_normal
+        auto pick = [](uint32_t h, uint64_t dflt) {
+            return h == 1 ? tc::policy_evict_first() : h == 2 ? tc::policy_evict_last() : h == 3 ? tc::policy_evict_normal() : dflt;
+        };
+        const uint64_t pol = pick(l2_hint & 3u, a_evict_first ? tc::policy_evict_first() : tc::policy_evict_last());
+        const uint32_t hb = (l2_hint >> 2) & 3u;
+        const uint64_t pol_b = hb ? pick(hb, 0ull) : 0ull;
         auto issue_a = [&](int i) {
             const int s = i % STAGES;
             char* sa = base + s * L::kStageBytes;
@@ -121,7 +128,10 @@ __device__ __forceinline__ void tc_mainloop(char* base, const TmaDesc* tmA, cons
         };
         auto issue_b = [&](int i) {
             const int s = i % STAGES;
-            tc::tma_load_2d(base + s * L::kStageBytes + L::kABytes, tmB, &full[s], (kb_begin + i) * BK, b_row);
+            if (hb)
+                tc::tma_load_2d_hint(base + s * L::kStageBytes + L::kABytes, tmB, &full[s], (kb_begin + i) * BK, b_row, pol_b);
+            else
+                tc::tma_load_2d(base + s * L::kStageBytes + L::kABytes, tmB, &full[s], (kb_begin + i) * BK, b_row);
         };
         // With a dependency, the A operand (weights, immutable) streams while
         // the previous launch finishes; B (its output) only after wait_prev.
@@ -244,7 +254,8 @@ struct GemmArgs {
     int32_t tma_store;  // 1: epilogue stages the bf16 tile in smem and writes it with TMA stores (tmC)
     int32_t abandon;    // give the tile up within ~2 k-blocks when the SM is revoked: 1 re-runs it from
                         // k = 0 (fastest yield), 2 spills the accumulators and resumes at k (no lost work)
-    int32_t pad3[3];
+    int32_t l2_hint;    // L2 policy of the A / B operand loads (tc_mainloop's l2_hint; 0 = A evict_last, B none)
+    int32_t pad3[2];
     TmaDesc tmC;        // C [M][N] bf16, box {64, 128}, SWIZZLE_128B
 };
 static_assert(offsetof(GemmArgs, tmC) == 320 && sizeof(GemmArgs) == 448, "GemmArgs layout (mirrored in _abi.py)");
@@ -311,7 +322,8 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
         if (ltid() == 0) atomicExch(ring + j, 0ull);  // spill consumed: the slot is free again
     }
     tc_mainloop<BN, STAGES, BK>(base, &a.tmA, &a.tmB, m_blk * kTcBM, n_blk * BN, kb_start, kb1, c.tmem_base, false,
-                                nullptr, 0, nullptr, yc, res != 0u, 0, c.st ? c.args : nullptr);
+                                nullptr, 0, nullptr, yc, res != 0u, 0, c.st ? c.args : nullptr,
+                                (uint32_t)a.l2_hint);
     const bool gave_up = yc && *tc_stop_word() != ~0u;  // epilogue warps: ordered by tmem_full
     if (gave_up) {
         // abandoned: spill the accumulators (when there are any) so the tile
