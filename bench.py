@@ -950,9 +950,13 @@ def config4_leg(co, args, solo, peaks):
                          "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                          "frac": round(co.resnet.flops / (res_ms * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
                          "padded_frac": round(co.resnet.padded_flops / (res_ms * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
+                         "stream_bound_ms": round(co.resnet.bound_s(peaks["bf16_tflops"], peaks["hbm_gbs"]) * 1e3, 3),
+                         "frac_of_stream_bound": round(co.resnet.bound_s(peaks["bf16_tflops"], peaks["hbm_gbs"]) * 1e3
+                                                       / res_ms, 4),
                          "what": "algorithmic (unpadded) conv/FC flops of one fwd+dgrad+wgrad iteration over its "
                                  "solo time on the executor (full GPU); padded_frac counts the flops of the "
-                                 "128-row-tiled GEMMs actually issued"},
+                                 "128-row-tiled GEMMs actually issued; stream_bound_ms sums per GEMM "
+                                 "max(flops / bf16 peak, bytes / HBM peak) (most of the stream is HBM-bound)"},
             "tpot_first": c4["tpot-first"], "slo_aware": c4["slo-aware"], "temporal": c4["temporal"]}
 
 

@@ -174,7 +174,7 @@ class GemmArgs(ctypes.Structure):
                 ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32),
                 ("splits", ctypes.c_int32), ("ws", ctypes.c_uint64), ("bk", ctypes.c_int32),
                 ("tma_store", ctypes.c_int32), ("abandon", ctypes.c_int32), ("l2_hint", ctypes.c_int32),
-                ("pad2", ctypes.c_uint8 * 8),
+                ("tiles", ctypes.c_int32), ("pad2", ctypes.c_uint8 * 4),
                 ("tmC", TmaDesc)]  # tmC: alignas(64)
 
 
@@ -214,7 +214,7 @@ GEMM_BM, GEMM_BN = 128, 256
 
 def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16, bn: int = GEMM_BN,
               splits: int = 1, ws: int = 0, bk: int = 64, tma_store: bool = True,
-              abandon: bool = False, l2_hint: int = 0) -> "GemmArgs":
+              abandon: bool = False, l2_hint: int = 0, tiles: int = 1) -> "GemmArgs":
     if bn not in (64, 128, 256):
         raise DsError(10, f"gemm tile width {bn} not in (64, 128, 256)")
     if M % GEMM_BM or N % bn or K % 64:
@@ -223,6 +223,8 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
         raise DsError(10, "split-K needs a workspace and <= K/64 splits")
     if bk not in (64, 32) or (bk == 32 and bn != 256):
         raise DsError(10, "bk 32 (SWIZZLE_64B, 4 stages) is built for 128x256 tiles only")
+    if tiles > 1 and (bn not in (64, 128) or splits > 1 or bk != 64 or not tma_store or abandon):
+        raise DsError(10, "multi-tile GEMM blocks need bn 64/128, no split-K, bk 64, TMA stores, no abandon")
     tmC = tensor_map_bf16(C, M, N, GEMM_BM, 64) if tma_store else TmaDesc()
     a = GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM, bk), tensor_map_bf16(B, N, K, bn, bk), C, M, N, K, group_m, bn,
                  max(1, splits), ws, bk, int(tma_store))
@@ -231,11 +233,15 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
     # L2 policy of the operand loads: bits [1:0] A, [3:2] B; 0 default (A evict_last, B none),
     # 1 evict_first, 2 evict_last, 3 evict_normal
     a.l2_hint = int(l2_hint)
+    a.tiles = max(1, int(tiles))  # T consecutive raster tiles per logical block (gemm_multi)
     return a
 
 
-def gemm_grid(M: int, N: int, bn: int = GEMM_BN, splits: int = 1):
-    return ((M // GEMM_BM) * (N // bn) * max(1, splits), 1, 1)
+def gemm_grid(M: int, N: int, bn: int = GEMM_BN, splits: int = 1, tiles: int = 1):
+    n = (M // GEMM_BM) * (N // bn)
+    if tiles > 1:
+        return ((n + tiles - 1) // tiles, 1, 1)
+    return (n * max(1, splits), 1, 1)
 
 
 def splitk_ws_elems(M: int, N: int, bn: int, splits: int) -> int:

@@ -255,11 +255,14 @@ struct GemmArgs {
     int32_t abandon;    // give the tile up within ~2 k-blocks when the SM is revoked: 1 re-runs it from
                         // k = 0 (fastest yield), 2 spills the accumulators and resumes at k (no lost work)
     int32_t l2_hint;    // L2 policy of the A / B operand loads (tc_mainloop's l2_hint; 0 = A evict_last, B none)
-    int32_t pad3[2];
+    int32_t tiles;      // 0/1: one output tile per logical block; T >= 2: T consecutive raster tiles per block
+                        // (gemm_multi: BN 64 / 128, no split-K, not abandonable; same bits per tile)
+    int32_t pad3;
     TmaDesc tmC;        // C [M][N] bf16, box {64, 128}, SWIZZLE_128B
 };
 static_assert(offsetof(GemmArgs, tmC) == 320 && sizeof(GemmArgs) == 448, "GemmArgs layout (mirrored in _abi.py)");
 // host-side validation of abandonable GEMMs reads these fields (runtime.cpp)
+static_assert(offsetof(GemmArgs, l2_hint) == 308 && offsetof(GemmArgs, tiles) == 312, "GemmArgs tail (mirrored in _abi.py)");
 static_assert(offsetof(GemmArgs, K) == kGemmArgsOffK && offsetof(GemmArgs, bk) == kGemmArgsOffBk &&
                   offsetof(GemmArgs, abandon) == kGemmArgsOffAbandon, "GemmArgs offsets (ds_device.cuh)");
 
@@ -426,8 +429,140 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
     if (yc && ltid() == 0 && *tc_stop_word() != ~0u) *c.abandon = 1u;
 }
 
+// ---------------------------------------------------------------------------
+// Multi-tile blocks (GemmArgs.tiles = T >= 2; BN 64 or 128, S = 1): logical
+// block t computes raster tiles [T t, T t + T) as one continuous operand
+// stream through the lane's ring.  Tile j accumulates in TMEM columns
+// BN (j % 2); the epilogue warps drain tile j into a bf16 staging image and
+// TMA-store it while the ring streams and the MMA issuer multiplies tile j+1,
+// then hand the columns back (tempty) before tile j+2.  For the tall, short-K
+// GEMMs of a convolution stream (K = 64 .. 576: one to nine k-blocks per tile)
+// this removes the per-tile block overhead (claim, barrier set-up, pipeline
+// fill, store drain) that otherwise costs more than the tile's bytes.  Every
+// tile is the same k-ordered tcgen05 chain (same instruction descriptor, same
+// smem descriptors, same k steps) as in gemm_body_bn, so C is bit-identical
+// to the one-tile records wherever the blocks run.
+// ---------------------------------------------------------------------------
+template <int BN, int STAGES>
+__device__ void gemm_multi(const BodyCtx& c, const GemmArgs& a) {
+    using L = TcSmem<BN, STAGES>;
+    static_assert(2 * BN <= 256, "two TMEM accumulators per lane");
+    static_assert(L::kBytes + BN * 256 + 1024 <= kLaneSmem, "ring + staging fit the lane");
+    char* base = align1024(c.smem);
+    char* stage_c = base + L::kBytes;  // BN/64 SWIZZLE_128B [128][64] bf16 images (1024-aligned)
+    const int tiles_total = (a.M / kTcBM) * (a.N / BN);
+    const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
+    const int j0 = a.tiles * t, nt = min(a.tiles, tiles_total - j0);
+    const int nkb = a.K / kTcBK, total = nt * nkb;
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2] tile accumulator final
+    uint64_t* tempty = tfull + 2;      // [2] its TMEM columns read (4 epilogue warps)
+    const int warp = ltid() >> 5, lane = ltid() & 31;
+    if (ltid() == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            tc::mbar_init(&tfull[k], 1);
+            tc::mbar_init(&tempty[k], 4);
+        }
+        tc::fence_mbar_init();
+    }
+    body_sync();
+    if (warp == 0 && lane == 0) {
+        if (desc_fence_needed(c.st ? c.args : nullptr)) {
+            tc::tma_fence_desc(&a.tmA);
+            tc::tma_fence_desc(&a.tmB);
+        }
+        const uint64_t pol = tc::policy_evict_last();
+        int m_blk = 0, n_blk = 0;
+        for (int i = 0; i < total; ++i) {
+            const int j = i / nkb, kk = i - j * nkb, s = i % STAGES;
+            if (kk == 0) gemm_tile_coords(a, BN, j0 + j, m_blk, n_blk);
+            if (i >= STAGES) tc::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            char* sa = base + s * L::kStageBytes;
+            tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+            tc::tma_load_2d_hint(sa, &a.tmA, &full[s], kk * kTcBK, m_blk * kTcBM, pol);
+            tc::tma_load_2d(sa + L::kABytes, &a.tmB, &full[s], kk * kTcBK, n_blk * BN);
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(kTcBM, BN);
+        for (int i = 0; i < total; ++i) {
+            const int j = i / nkb, kk = i - j * nkb, s = i % STAGES;
+            if (kk == 0 && j >= 2) {
+                tc::mbar_wait(&tempty[j & 1], ((j >> 1) - 1) & 1);  // tile j-2's columns read
+                tc::tc_fence_after();
+            }
+            tc::mbar_wait(&full[s], (i / STAGES) & 1);
+            tc::tc_fence_after();
+            char* sa = base + s * L::kStageBytes;
+            const uint64_t ad = tc::smem_desc_k_sw128(sa), bd = tc::smem_desc_k_sw128(sa + L::kABytes);
+#pragma unroll
+            for (int k = 0; k < kTcBK / 16; ++k)
+                tc::mma_bf16(c.tmem_base + BN * (j & 1), ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                             (kk | k) != 0);
+            tc::mma_commit(&empty[s]);
+            if (kk == nkb - 1) tc::mma_commit(&tfull[j & 1]);
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3, r = q * 32 + lane;
+        for (int j = 0; j < nt; ++j) {
+            int m_blk, n_blk;
+            gemm_tile_coords(a, BN, j0 + j, m_blk, n_blk);
+            if (j > 0) {
+                if (q == 0 && lane == 0) tc::bulk_wait_read_all();  // tile j-1's stores have read the staging image
+                epi_sync();
+            }
+            tc::mbar_wait(&tfull[j & 1], (j >> 1) & 1);
+            tc::tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                tc::tmem_ld_32x32b_x32(c.tmem_base + ((uint32_t)(q * 32) << 16) + BN * (j & 1) + ch * 32, v);
+                tc::tmem_ld_wait();
+                char* sub = stage_c + (ch >> 1) * 16384 + r * 128;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint4 o;
+                    o.x = pack_bf16x2(__uint_as_float(v[8 * u + 0]), __uint_as_float(v[8 * u + 1]));
+                    o.y = pack_bf16x2(__uint_as_float(v[8 * u + 2]), __uint_as_float(v[8 * u + 3]));
+                    o.z = pack_bf16x2(__uint_as_float(v[8 * u + 4]), __uint_as_float(v[8 * u + 5]));
+                    o.w = pack_bf16x2(__uint_as_float(v[8 * u + 6]), __uint_as_float(v[8 * u + 7]));
+                    const int chunk = (ch & 1) * 4 + u;
+                    *reinterpret_cast<uint4*>(sub + ((chunk ^ (r & 7)) << 4)) = o;
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[j & 1]);
+            tc::fence_proxy_async();  // generic smem writes -> async proxy
+            epi_sync();
+            if (q == 0 && lane == 0) {
+                for (int sub = 0; sub < BN / 64; ++sub)
+                    tc::tma_store_2d(&a.tmC, stage_c + sub * 16384, n_blk * BN + sub * 64, m_blk * kTcBM);
+                tc::bulk_commit();
+            }
+        }
+        if (q == 0 && lane == 0) {
+            tc::bulk_wait_all();  // global writes complete before the block retires
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+    }
+    tc::tc_fence_before();
+    body_sync();
+    if (ltid() == 0)
+        for (int k = 0; k < 2 * STAGES + 4; ++k) tc::mbar_inval(&full[k]);
+}
+
 __device__ void body_gemm_bf16(const BodyCtx& c) {
     const GemmArgs& a = *reinterpret_cast<const GemmArgs*>(c.args);
+    if (a.tiles > 1) {  // host-validated: bn 64 / 128, splits 1, bk 64, TMA store, not abandonable
+        if (a.bn == 64) gemm_multi<64, kCtasPerSm == 2 ? 3 : 6>(c, a);
+        else gemm_multi<128, kCtasPerSm == 2 ? 2 : 4>(c, a);
+        return;
+    }
     if (a.bk == 32 && (a.bn == 0 || a.bn == 256)) {  // 4 x 24 KB stages per lane
         gemm_body_bn<kGemmBN, kCtasPerSm == 2 ? 4 : 8, 32>(c, a);
         return;

@@ -69,7 +69,8 @@ __device__ __forceinline__ bool wait_prev_or_abandon(const BodyCtx& c) {
 }
 
 __device__ __forceinline__ bool abandonable(int body, const BodyCtx& c) {
-    return body == DS_BODY_GEMM_BF16 && c.abandon && reinterpret_cast<const GemmArgs*>(c.args)->abandon;
+    return body == DS_BODY_GEMM_BF16 && c.abandon && reinterpret_cast<const GemmArgs*>(c.args)->abandon &&
+           reinterpret_cast<const GemmArgs*>(c.args)->tiles <= 1;
 }
 
 __device__ __forceinline__ void run_body(int body, const BodyCtx& c) {

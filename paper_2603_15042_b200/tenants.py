@@ -467,19 +467,43 @@ def resnet50_gemms(batch: int = 128, image: int = 224):
     return fwd + bwd
 
 
-def plan_gemm(M: int, N: int, K: int, workers: int = WORKERS):
+def plan_gemm(M: int, N: int, K: int, workers: int = WORKERS, wide: bool = None):
     """Tile width and split-K for a padded GEMM: the widest tile giving >= one
-    wave of logical blocks, else the narrowest that divides N; split K while
-    the grid is short of a wave and every split keeps >= 8 k-blocks."""
+    wave of logical blocks; else (wide) the widest tile whose split-K still
+    fills a wave with >= 8 k-blocks per split -- wider tiles re-read the A
+    panel from L2 fewer times -- or the narrowest that divides N; split K
+    while the grid is short of a wave and every split keeps >= 8 k-blocks."""
+    if wide is None:
+        wide = os.environ.get("DS_RESNET_WIDE", "0") != "0"
     Mp, Kp = _round(M, 128), _round(K, 64)
     Np = _round(N, 64)
     choices = [bn for bn in (256, 128, 64) if Np % bn == 0]
-    bn = next((b for b in choices if (Mp // 128) * (Np // b) >= workers), choices[-1])
+    full = [b for b in choices if (Mp // 128) * (Np // b) >= workers]
+    fill = [b for b in choices if (Mp // 128) * (Np // b) * ((Kp // 64) // 8) >= workers]
+    bn = full[0] if full else (fill[0] if wide and fill else choices[-1])
     tiles = (Mp // 128) * (Np // bn)
     splits = 1
     if tiles < workers:
         splits = max(1, min(256, -(-workers // tiles), (Kp // 64) // 8))
     return Mp, Np, Kp, bn, splits
+
+
+def plan_tiles(Mp: int, Np: int, Kp: int, bn: int, splits: int, workers: int = WORKERS, max_tiles: int = 8):
+    """Multi-tile blocks for the tall, short-K GEMMs of the stream (gemm_multi):
+    with no split-K, K <= 1152 (at most 18 k-blocks per tile, where the
+    per-block overhead rivals the tile's bytes) and at least two waves of
+    tiles, T consecutive raster tiles per block with T chosen to leave >= 2
+    blocks per worker lane (load balance), capped at max_tiles.  The tile
+    narrows to 128 columns (two TMEM accumulators per lane).  Returns
+    (bn, T); T = 1 keeps the one-tile record."""
+    if splits > 1 or Kp > 1152 or max_tiles < 2:
+        return bn, 1
+    bn2 = min(bn, 128)
+    if Np % bn2:
+        return bn, 1
+    tiles = (Mp // 128) * (Np // bn2)
+    T = min(max_tiles, tiles // (2 * workers))
+    return (bn2, T) if T >= 2 else (bn, 1)
 
 
 class ResNetStream:
@@ -488,7 +512,7 @@ class ResNetStream:
     padded to tile multiples and share three arenas (contents are synthetic;
     shapes, flops and launch order are ResNet-50's)."""
 
-    def __init__(self, batch: int = 128, image: int = 224, device="cuda", seed: int = 2):
+    def __init__(self, batch: int = 128, image: int = 224, device="cuda", seed: int = 2, max_tiles=None):
         self.gemms = resnet50_gemms(batch, image)
         self.batch = batch
         self.flops = sum(2.0 * M * N * K for _, M, N, K in self.gemms)  # algorithmic (unpadded)
@@ -511,10 +535,16 @@ class ResNetStream:
         self.C = torch.zeros(c_el, device=device, dtype=torch.bfloat16)
         self.ws = torch.zeros(max(1, ws_el), device=device, dtype=torch.float32)
         self.records = []  # (semantic_id, body, grid, args, flops)
+        # multi-tile blocks for the tall short-K GEMMs (max tiles per block;
+        # DS_RESNET_TILES=1 keeps every GEMM on one-tile blocks)
+        max_t = int(os.environ.get("DS_RESNET_TILES", "4")) if max_tiles is None else max_tiles
+        self.tiles = []
         for (name, M, N, K), (Mp, Np, Kp, bn, s) in zip(self.gemms, plans):
+            bn, T = plan_tiles(Mp, Np, Kp, bn, s, max_tiles=max_t)
+            self.tiles.append((bn, T))
             ga = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, bn=bn,
-                                splits=s, ws=self.ws.data_ptr() if s > 1 else 0)
-            self.records.append((f"resnet/{name}", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, s), ga,
+                                splits=s, ws=self.ws.data_ptr() if s > 1 else 0, tiles=T)
+            self.records.append((f"resnet/{name}", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, s, T), ga,
                                  2.0 * M * N * K))
             if s > 1:
                 ra, rg = _abi.splitk_reduce(self.ws.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, 16, bn, s)
@@ -523,3 +553,11 @@ class ResNetStream:
 
     def register(self, dom, phase=_abi.TRAINING) -> List[int]:
         return [dom.kernel(sid, body, grid, args, phase=phase) for sid, body, grid, args, _ in self.records]
+
+    def bound_s(self, tflops: float, hbm_gbs: float) -> float:
+        """Roofline lower bound of one iteration: per GEMM (true sizes) the
+        larger of flops / bf16 peak and (A + B + C) bytes / HBM peak, summed.
+        Most of the stream's GEMMs are HBM-bound at batch 128 (K = 64..576
+        against M = 100k..1.6M rows), so this is the honest denominator."""
+        return sum(max(2.0 * M * N * K / (tflops * 1e12), 2.0 * (M * K + N * K + M * N) / (hbm_gbs * 1e9))
+                   for _, M, N, K in self.gemms)

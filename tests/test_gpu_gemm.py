@@ -171,3 +171,49 @@ def test_gemm_8192_coroutine_bit_exact_vs_solo_and_fp32():
     assert r["flips"] >= 4
     assert sorted(b.block for b in blog if b.flags == 0) == list(range(grid[0]))
     assert torch.equal(C_co.view(torch.int16), C_solo.view(torch.int16))
+
+
+@pytest.mark.parametrize("shape", [(12800, 256, 64, 128, 5), (25600, 64, 576, 64, 8), (3200, 128, 1152, 128, 3),
+                                   (1280, 128, 192, 64, 7)])
+def test_gemm_multi_tile_blocks_bit_exact_vs_one_tile(shape):
+    """Multi-tile blocks (GemmArgs.tiles = T: T consecutive raster tiles per
+    logical block, TMEM double-buffered, epilogue + TMA store overlapping the
+    next tile's stream; ragged last block included) give C bit-identical to
+    the one-tile records of the same tile width, solo and as a coroutine under
+    mid-kernel quota changes, and within the bf16 tolerance of fp32."""
+    M, N, K, bn, T = shape
+    A, B, C_one = make(M, N, K, seed=5)
+    C_multi, C_co = torch.zeros_like(C_one), torch.zeros_like(C_one)
+    solo_launch(0, "gemm1", _abi.BODY_GEMM_BF16, _abi.gemm_grid(M, N, bn),
+                _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_one.data_ptr(), M, N, K, bn=bn))
+    grid = _abi.gemm_grid(M, N, bn, tiles=T)
+    assert grid[0] == -(-(M // 128) * (N // bn) // T)
+    solo_launch(0, "gemmT", _abi.BODY_GEMM_BF16, grid,
+                _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_multi.data_ptr(), M, N, K, bn=bn, tiles=T))
+    torch.cuda.synchronize()
+    assert torch.equal(C_multi.view(torch.int16), C_one.view(torch.int16))
+    rows = torch.arange(0, M, max(1, M // 256), device="cuda")
+    ref = A[rows].float() @ B.float().t()
+    err = (C_multi[rows].float() - ref).abs()
+    assert bool((err <= ref.abs() * 2 ** -7 + 2 ** -6).all())
+    a_co = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_co.data_ptr(), M, N, K, bn=bn, tiles=T)
+    with Domain(0, block_log_capacity=1 << 16) as dom:
+        dom.start()
+        t = dom.tenant("train", _abi.BEST_EFFORT)
+        dom.quota_set(dom.mask(t, 0, dom.num_sms))
+        kid = dom.kernel("gemmT", _abi.BODY_GEMM_BF16, grid, a_co, phase=_abi.TRAINING)
+        nblk = grid[0]
+        dom.quota_at_claim(t, 0, nblk // 3, dom.mask(t, 10, 20))
+        dom.quota_at_claim(t, 0, 2 * nblk // 3, dom.mask(t, 0, dom.num_sms))
+        s = dom.launch(t, kid)
+        dom.wait(t, s)
+        log = [b for b in dom.block_log() if b.tenant == t]
+    assert sorted(b.block for b in log) == list(range(nblk))
+    assert torch.equal(C_co.view(torch.int16), C_one.view(torch.int16))
+
+
+def test_gemm_multi_tile_rejects_unsupported():
+    from paper_2603_15042_b200._abi import DsError
+    for kw in (dict(bn=256), dict(bn=128, splits=2, ws=1), dict(bn=128, abandon=True)):
+        with pytest.raises(DsError):
+            _abi.gemm_args(1, 1, 1, 1024, 1024, 1024, tiles=4, **kw)

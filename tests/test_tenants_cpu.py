@@ -42,3 +42,23 @@ def test_resnet_stream_plan_covers_resnet50():
         Mp, Np, Kp, bn, s = plan_gemm(M, N, K)
         assert Mp % 128 == 0 and Np % bn == 0 and Kp % 64 == 0 and Mp >= M and Np >= N and Kp >= K
         assert 1 <= s <= Kp // 64
+
+
+def test_resnet_multi_tile_plan():
+    """plan_tiles: only un-split, short-K (<= 1152) GEMMs with >= 2 waves of
+    tiles get multi-tile blocks (tile narrowed to <= 128 columns, >= 2 blocks
+    per worker lane, <= 8 tiles per block)."""
+    from paper_2603_15042_b200.tenants import plan_gemm, plan_tiles, resnet50_gemms, WORKERS
+    n_multi = 0
+    for name, M, N, K in resnet50_gemms():
+        Mp, Np, Kp, bn, s = plan_gemm(M, N, K)
+        bn2, T = plan_tiles(Mp, Np, Kp, bn, s)
+        if T == 1:
+            assert bn2 == bn
+            continue
+        n_multi += 1
+        assert s == 1 and Kp <= 1152 and bn2 in (64, 128) and Np % bn2 == 0 and 2 <= T <= 8
+        assert -(-(Mp // 128) * (Np // bn2) // T) >= 2 * WORKERS
+    assert n_multi > 0
+    assert plan_tiles(8192, 8192, 8192, 256, 1) == (256, 1)   # long K: one tile per block
+    assert plan_tiles(401408, 64, 64, 64, 1, max_tiles=1) == (64, 1)
