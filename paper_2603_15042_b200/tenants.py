@@ -494,9 +494,13 @@ def plan_tiles(Mp: int, Np: int, Kp: int, bn: int, splits: int, workers: int = W
     per-block overhead rivals the tile's bytes) and at least two waves of
     tiles, T consecutive raster tiles per block with T chosen to leave >= 2
     blocks per worker lane (load balance), capped at max_tiles.  The tile
-    narrows to 128 columns (two TMEM accumulators per lane).  Returns
+    narrows to 128 columns (two TMEM accumulators per lane), only for
+    K <= 256 (profiles/r2_resnet_multi_tile_ab.txt: past that the second
+    read of each A panel costs more than the block overhead saved).  Returns
     (bn, T); T = 1 keeps the one-tile record."""
     if splits > 1 or Kp > 1152 or max_tiles < 2:
+        return bn, 1
+    if bn > 128 and Kp > 256:  # narrowing re-reads A from L2 twice; measured slower past K = 256
         return bn, 1
     bn2 = min(bn, 128)
     if Np % bn2:
