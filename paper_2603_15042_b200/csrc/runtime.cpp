@@ -185,8 +185,13 @@ void drain_loop(ds_domain* d) {
                 if (c.tenant >= 0 && c.tenant < (int)d->per_tenant_done.size())
                     d->per_tenant_done[c.tenant].push_back(c);
             }
-            if (c.tenant >= 0 && c.tenant < (int)d->tenants.size())
-                d->tenants[c.tenant]->completed.store(c.seq + 1, std::memory_order_release);
+            // monotonic: launch s+1's completion record can be written before
+            // s's (s publishes head, then appends its record; a short s+1 may
+            // retire in between), and s+1 done implies s done on the device
+            if (c.tenant >= 0 && c.tenant < (int)d->tenants.size()) {
+                auto& done = d->tenants[c.tenant]->completed;
+                if (c.seq + 1 > done.load(std::memory_order_relaxed)) done.store(c.seq + 1, std::memory_order_release);
+            }
             d->completed_total.fetch_add(1, std::memory_order_relaxed);
         }
         if (any) {
