@@ -180,7 +180,8 @@ class GemmArgs(ctypes.Structure):
 
 class SplitkReduceArgs(ctypes.Structure):
     _fields_ = [("ws", ctypes.c_uint64), ("C", ctypes.c_uint64), ("M", ctypes.c_int32), ("N", ctypes.c_int32),
-                ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32), ("splits", ctypes.c_int32)]
+                ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32), ("splits", ctypes.c_int32),
+                ("rows", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 def tensor_map_bf16(ptr: int, rows: int, cols: int, box_rows: int, box_cols: int = 64) -> TmaDesc:
@@ -249,9 +250,23 @@ def splitk_ws_elems(M: int, N: int, bn: int, splits: int) -> int:
     return (M // GEMM_BM) * (N // bn) * splits * GEMM_BM * bn
 
 
-def splitk_reduce(ws: int, C: int, M: int, N: int, K: int, group_m: int, bn: int, splits: int):
-    """(args, grid) of the split-K fold launch that follows a split GEMM."""
-    return (SplitkReduceArgs(ws, C, M, N, K, group_m, bn, splits), ((M // GEMM_BM) * (N // bn) * 8, 1, 1))
+def splitk_reduce(ws: int, C: int, M: int, N: int, K: int, group_m: int, bn: int, splits: int, rows: int = 16):
+    """(args, grid) of the split-K fold launch that follows a split GEMM:
+    one block per (tile, group of `rows` rows), rows in (16, 32, 64, 128)."""
+    if rows not in (16, 32, 64, 128):
+        raise DsError(10, f"split-K fold rows per block {rows} not in (16, 32, 64, 128)")
+    return (SplitkReduceArgs(ws, C, M, N, K, group_m, bn, splits, rows),
+            ((M // GEMM_BM) * (N // bn) * (GEMM_BM // rows), 1, 1))
+
+
+def fold_rows(M: int, N: int, bn: int, workers: int) -> int:
+    """Widest row group (fewest, largest fold blocks) that still gives every
+    worker lane a block: per-block overhead dominates 16-row groups."""
+    tiles = (M // GEMM_BM) * (N // bn)
+    for rows in (128, 64, 32):
+        if tiles * (GEMM_BM // rows) >= workers:
+            return rows
+    return 16
 
 
 class GemvArgs(ctypes.Structure):

@@ -574,8 +574,11 @@ __device__ void body_gemm_bf16(const BodyCtx& c) {
     }
 }
 
-// Split-K fold: block (tile, 16-row group) sums the S fp32 partials of its
-// rows in split order 0..S-1 and stores bf16.  grid = tiles * 8.
+// Split-K fold: block (tile, row group) sums the S fp32 partials of its rows
+// in split order 0..S-1 and stores bf16.  rows = 16 (0: legacy) .. 128 rows
+// per block, grid = tiles * 128 / rows: every element is the same s-ordered
+// sum whatever the row grouping, so the grouping is a pure launch-shape choice
+// (wider groups: fewer, larger blocks, less per-block overhead).
 struct SplitkReduceArgs {
     uint64_t ws;  // fp32 [tiles][S][128][BN]
     uint64_t C;   // bf16 [M][N]
@@ -583,12 +586,16 @@ struct SplitkReduceArgs {
     int32_t group_m;
     int32_t bn;
     int32_t splits;
+    int32_t rows;  // rows per block: 0 (= 16), 16, 32, 64 or 128
+    int32_t pad;
 };
+static_assert(sizeof(SplitkReduceArgs) == 48, "SplitkReduceArgs layout (mirrored in _abi.py)");
 
 __device__ void body_splitk_reduce(const BodyCtx& c) {
     const SplitkReduceArgs& r = *reinterpret_cast<const SplitkReduceArgs*>(c.args);
     const int t = c.bx + c.gx * (c.by + c.gy * c.bz);
-    const int tile = t >> 3, rg = t & 7;
+    const int R = r.rows > 0 ? r.rows : 16, groups = kTcBM / R;
+    const int tile = t / groups, rg = t - tile * groups;
     GemmArgs g;
     g.M = r.M;
     g.N = r.N;
@@ -598,8 +605,8 @@ __device__ void body_splitk_reduce(const BodyCtx& c) {
     const int S = r.splits, BN = r.bn;
     const float* ws = reinterpret_cast<const float*>(r.ws) + (size_t)tile * S * kTcBM * BN;
     __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(r.C);
-    for (int idx = 4 * (int)ltid(); idx < 16 * BN; idx += 4 * kBodyThreads) {
-        const int row = rg * 16 + idx / BN, col = idx % BN;
+    for (int idx = 4 * (int)ltid(); idx < R * BN; idx += 4 * kBodyThreads) {
+        const int row = rg * R + idx / BN, col = idx % BN;
         float4 acc = __ldcg(reinterpret_cast<const float4*>(ws + (size_t)row * BN + col));
         for (int s = 1; s < S; ++s) {
             const float4 p = __ldcg(reinterpret_cast<const float4*>(ws + ((size_t)s * kTcBM + row) * BN + col));

@@ -542,6 +542,7 @@ class ResNetStream:
         # multi-tile blocks for the tall short-K GEMMs (max tiles per block;
         # DS_RESNET_TILES=1 keeps every GEMM on one-tile blocks)
         max_t = int(os.environ.get("DS_RESNET_TILES", "4")) if max_tiles is None else max_tiles
+        fold_wide = os.environ.get("DS_RESNET_FOLD_WIDE", "1") != "0"
         self.tiles = []
         for (name, M, N, K), (Mp, Np, Kp, bn, s) in zip(self.gemms, plans):
             bn, T = plan_tiles(Mp, Np, Kp, bn, s, max_tiles=max_t)
@@ -551,7 +552,8 @@ class ResNetStream:
             self.records.append((f"resnet/{name}", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, s, T), ga,
                                  2.0 * M * N * K))
             if s > 1:
-                ra, rg = _abi.splitk_reduce(self.ws.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, 16, bn, s)
+                rows = _abi.fold_rows(Mp, Np, bn, WORKERS) if fold_wide else 16
+                ra, rg = _abi.splitk_reduce(self.ws.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, 16, bn, s, rows)
                 self.records.append((f"resnet/{name}/fold", _abi.BODY_SPLITK_REDUCE, rg, ra, 0.0))
         self.plans = plans
 

@@ -57,13 +57,13 @@ def test_gemm_coroutine_bit_exact_vs_solo():
     assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
 
 
-def run_split(A, B, C, M, N, K, bn, S, ws, dom=None, t=None):
+def run_split(A, B, C, M, N, K, bn, S, ws, dom=None, t=None, rows=16):
     args = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, bn=bn, splits=S,
                           ws=ws.data_ptr() if S > 1 else 0)
     grid = _abi.gemm_grid(M, N, bn, S)
     launches = [("gemm", _abi.BODY_GEMM_BF16, grid, args)]
     if S > 1:
-        ra, rg = _abi.splitk_reduce(ws.data_ptr(), C.data_ptr(), M, N, K, 16, bn, S)
+        ra, rg = _abi.splitk_reduce(ws.data_ptr(), C.data_ptr(), M, N, K, 16, bn, S, rows)
         launches.append(("fold", _abi.BODY_SPLITK_REDUCE, rg, ra))
     if dom is None:
         for sid, body, g, a in launches:
@@ -107,6 +107,28 @@ def test_splitk_coroutine_bit_exact_vs_solo():
         got = C_co.cpu()
     assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
 
+
+def test_splitk_fold_row_groups_bit_identical():
+    """The fold's row grouping (16 / 32 / 64 / 128 rows per block) is a launch
+    shape only: every grouping gives the same bits, solo and as a coroutine."""
+    M, N, K, bn, S = 512, 256, 4096, 128, 5
+    A, B, C16 = make(M, N, K, seed=8)
+    ws = torch.zeros(_abi.splitk_ws_elems(M, N, bn, S), device="cuda")
+    run_split(A, B, C16, M, N, K, bn, S, ws, rows=16)
+    for rows in (32, 64, 128):
+        C = torch.zeros_like(C16)
+        run_split(A, B, C, M, N, K, bn, S, ws, rows=rows)
+        assert torch.equal(C.view(torch.int16), C16.view(torch.int16)), rows
+    C_co = torch.zeros_like(C16)
+    with Domain(0, block_log_capacity=0) as dom:
+        dom.start()
+        t = dom.tenant("train", _abi.BEST_EFFORT)
+        dom.quota_set(dom.mask(t, 0, 24))
+        seqs, _ = run_split(A, B, C_co, M, N, K, bn, S, ws, dom, t, rows=128)
+        dom.wait(t, seqs[-1])
+    assert torch.equal(C_co.view(torch.int16), C16.view(torch.int16))
+    with pytest.raises(_abi.DsError):
+        _abi.splitk_reduce(0, 0, M, N, K, 16, bn, S, rows=48)
 
 
 @pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 1024), (384, 768, 4096)])
