@@ -607,9 +607,26 @@ __device__ void body_splitk_reduce(const BodyCtx& c) {
     __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(r.C);
     for (int idx = 4 * (int)ltid(); idx < R * BN; idx += 4 * kBodyThreads) {
         const int row = rg * R + idx / BN, col = idx % BN;
-        float4 acc = __ldcg(reinterpret_cast<const float4*>(ws + (size_t)row * BN + col));
-        for (int s = 1; s < S; ++s) {
-            const float4 p = __ldcg(reinterpret_cast<const float4*>(ws + ((size_t)s * kTcBM + row) * BN + col));
+        const float* src = ws + (size_t)row * BN + col;
+        const size_t stride = (size_t)kTcBM * BN;  // one split's partial
+        float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+        int s = 1;
+        // 8 partials in flight per thread, then added in split order (the
+        // same fp32 add sequence as one at a time)
+        for (; s + 8 <= S; s += 8) {
+            float4 p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] = __ldcg(reinterpret_cast<const float4*>(src + (s + u) * stride));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                acc.x += p[u].x;
+                acc.y += p[u].y;
+                acc.z += p[u].z;
+                acc.w += p[u].w;
+            }
+        }
+        for (; s < S; ++s) {
+            const float4 p = __ldcg(reinterpret_cast<const float4*>(src + s * stride));
             acc.x += p.x;
             acc.y += p.y;
             acc.z += p.z;

@@ -108,10 +108,12 @@ def test_splitk_coroutine_bit_exact_vs_solo():
     assert np.array_equal(got.view(torch.int16).numpy(), C_solo.cpu().view(torch.int16).numpy())
 
 
-def test_splitk_fold_row_groups_bit_identical():
+@pytest.mark.parametrize("S", [5, 21])
+def test_splitk_fold_row_groups_bit_identical(S):
     """The fold's row grouping (16 / 32 / 64 / 128 rows per block) is a launch
-    shape only: every grouping gives the same bits, solo and as a coroutine."""
-    M, N, K, bn, S = 512, 256, 4096, 128, 5
+    shape only: every grouping gives the same bits, solo and as a coroutine;
+    S = 21 covers the 8-partials-in-flight path and its remainder."""
+    M, N, K, bn = 512, 256, 4096 if S == 5 else 21 * 512, 128
     A, B, C16 = make(M, N, K, seed=8)
     ws = torch.zeros(_abi.splitk_ws_elems(M, N, bn, S), device="cuda")
     run_split(A, B, C16, M, N, K, bn, S, ws, rows=16)
