@@ -193,7 +193,8 @@ class Colocation:
         # SLO-aware rule can defer a bound decode forever once it predicts a
         # TPOT miss: upgrades count the vctx's own tier — SURVEY 8-appendix #2.)
         self.tiers = [Fraction(t) for t in tiers]
-        self.dom = Domain(device, tiers=self.tiers, block_log_capacity=0, lend_idle_sms=True)
+        self.dom = Domain(device, tiers=self.tiers, block_log_capacity=int(os.environ.get("DS_BENCH_BLOG", "0")),
+                          lend_idle_sms=True)
         self.t_dec = self.dom.tenant("decode", _abi.LATENCY_CRITICAL)
         self.t_trn = self.dom.tenant("train", _abi.BEST_EFFORT)
         self.dec_kernels = self.model.register(self.dom)
@@ -393,7 +394,7 @@ class Colocation:
         _abi, torch = self._abi, self.torch
         from paper_2603_15042_b200.metrics import RequestOutcome
         dom = self.dom
-        lend = self.t_trn if policy != "temporal" else -1
+        lend = self.t_trn if policy != "temporal" and os.environ.get("DS_BENCH_LEND", "1") != "0" else -1
         eng = Engine(dom, policy=policy, quantum_ns=int(quantum_ms * 1e6), lend_tenant=lend, fair_handover=True)
         jd = eng.add_job(self.t_dec, _abi.LATENCY_CRITICAL)
         jt = eng.add_job(self.t_trn, _abi.BEST_EFFORT)

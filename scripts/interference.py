@@ -34,7 +34,8 @@ n = dom.num_sms
 smids = dom.smids()
 order = sorted(range(n), key=lambda i: smids[i])
 low = set(order[: n // 2])  # the engine's pick_slots: lowest smids (whole TPCs) first
-layouts = {"slot_order": [td if i < n // 2 else tt for i in range(n)]}
+dn = int(os.environ.get("DEC_SMS", n // 2))  # decode's SM count (slot order)
+layouts = {f"slot_order_{dn}": [td if i < dn else tt for i in range(n)]}
 _unused = {
            "low_smids": [td if i in low else tt for i in range(n)],
            "even_smids": [td if smids[i] % 4 < 2 else tt for i in range(n)]}
