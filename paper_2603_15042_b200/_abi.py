@@ -278,7 +278,8 @@ class GemvArgs(ctypes.Structure):
                 ("P_in", ctypes.c_int32), ("eps", ctypes.c_float), ("pos", ctypes.c_int32), ("Lmax", ctypes.c_int32),
                 ("q_dim", ctypes.c_int32), ("kv_dim", ctypes.c_int32), ("dbg", ctypes.c_uint64),
                 ("w_packed", ctypes.c_uint64), ("bm", ctypes.c_int32), ("l2_pf_kb", ctypes.c_int32),
-                ("sk", ctypes.c_int32), ("pair", ctypes.c_int32)]
+                ("sk", ctypes.c_int32), ("pair", ctypes.c_int32), ("pf_ahead", ctypes.c_int32),
+                ("pad_pf", ctypes.c_int32)]
 
 
 GEMV_STORE, GEMV_RESID, GEMV_SILU_MUL, GEMV_QKV = 0, 1, 2, 3

@@ -48,12 +48,16 @@ struct GemvArgs {
     int32_t pair;       // P >= 2: P whole 128-row slabs per block (grid ceil(nb / P)), one continuous weight
                         // stream, slab j's epilogue overlapping slab j+1's; kGemvSiluMul (whose weights always
                         // interleave gate/up rows: 2i gate, 2i+1 up of feature i) or kGemvStore
+    int32_t pf_ahead;   // D > 0: every ring issue also prefetches the weight tile D k-blocks ahead into L2
+                        // (a sliding window: D x 16 KB more in flight per lane than the smem ring holds)
+    int32_t pad_pf;
 };
 
 // the host builds these records with ctypes mirrors (_abi.py): pinned offsets
 static_assert(offsetof(GemvArgs, out) == 256 && offsetof(GemvArgs, N) == 320 && offsetof(GemvArgs, dbg) == 360 &&
                   offsetof(GemvArgs, w_packed) == 368 && offsetof(GemvArgs, bm) == 376 &&
-                  offsetof(GemvArgs, sk) == 384 && offsetof(GemvArgs, pair) == 388,
+                  offsetof(GemvArgs, sk) == 384 && offsetof(GemvArgs, pair) == 388 &&
+                  offsetof(GemvArgs, pf_ahead) == 392,
               "GemvArgs layout (mirrored in _abi.py)");
 
 constexpr int kGemvBN = 32;
@@ -153,11 +157,21 @@ __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, con
             const uint32_t tot = min((uint32_t)(total - pre) * L::kABytes, (uint32_t)a.l2_pf_kb << 10);
             for (uint32_t off = 0; off < tot; off += L::kABytes) tc::bulk_prefetch_l2(g0 + off, min(L::kABytes, tot - off));
         }
+        // sliding L2 prefetch D tiles ahead of the ring (weights are immutable,
+        // so the first window may go out before the dependency resolves)
+        const int D = a_packed ? a.pf_ahead : 0;
+        auto prefetch = [&](int j) {
+            int n, k;
+            piece_of(j, n, k);
+            tc::bulk_prefetch_l2(a_packed + ((size_t)n * KB + k) * L::kABytes, L::kABytes);
+        };
+        for (int j = pre; j < min(total, pre + D); ++j) prefetch(j);
         wait_prev(dep);
         if (dep.dbg) dep.dbg[7] = globaltimer();
         for (int i = 0; i < pre; ++i) issue_b(i);
         for (int i = pre; i < total; ++i) {
             const int s = i % STAGES;
+            if (D > 0 && i + D < total) prefetch(i + D);
             tc::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
             tc::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
             issue_a(i);

@@ -204,6 +204,8 @@ class DecodeModel:
         a.w_packed = Wp.data_ptr()
         a.bm = bm
         a.l2_pf_kb = pf
+        # sliding L2 prefetch distance (k-blocks) ahead of the ring: DS_GEMV_PF_AHEAD (0 = off)
+        a.pf_ahead = int(os.environ.get("DS_GEMV_PF_AHEAD", "0"))
         if G:
             sk_contributors(N // bm, K // 64, G)  # validates the plan
             a.sk = 1
