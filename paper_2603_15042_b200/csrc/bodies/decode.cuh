@@ -67,6 +67,7 @@ constexpr int kGemvStages64 = kCtasPerSm == 2 ? 8 : 12;  // 12-KB stages (64-row
 // stage has been consumed once the accumulator is complete
 constexpr uint32_t kGemvScratch = 0;
 constexpr uint32_t kGemvOwnOff = 32768;  // combiner's own partial (16 KB), clear of the scratch
+constexpr uint32_t kGemvResOff = 49152;  // kGemvResid owner: the slab's residual inputs [32 b][BM rows] bf16 (8 KB)
 
 __device__ __forceinline__ float bf16_to_f(uint16_t v) { return __uint_as_float((uint32_t)v << 16); }
 __device__ __forceinline__ uint16_t f_to_bf16(float f) {
@@ -386,6 +387,8 @@ __device__ void gemv_multi(const BodyCtx& c, const GemvArgs& a, uint64_t* dbg) {
 // the order is a function of (N, K, grid) only, never of the schedule.
 template <int BM, int STAGES>
 __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
+    static_assert(TcSmem<kGemvBN, STAGES, kTcBK, BM>::kBarOff >= kGemvResOff + 32 * BM * 2,
+                  "the staged residual inputs fit the consumed ring");
     constexpr int QR = BM / 4;            // slab rows per epilogue warp
     constexpr int FJ = BM * 8 / kBodyThreads;  // float4 per thread over a [BM][32] block
     char* base = align1024(c.smem);
@@ -456,6 +459,22 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     if (pA.owner) {
         const int n_blk = pA.n, S = pA.nc;
         const int n = n_blk * BM + row;
+        // kGemvResid: the residual inputs (an earlier launch's output, ordered
+        // by the wait_prev before the X loads) are fetched now into the
+        // consumed ring, so their latency hides under the partial exchange;
+        // each thread later reads back exactly the values it loaded
+        uint16_t* resb = reinterpret_cast<uint16_t*>(base + kGemvResOff);
+        if (a.mode == kGemvResid && warp >= 4 && active) {
+            const uint16_t* __restrict__ res = reinterpret_cast<const uint16_t*>(a.resid);
+#pragma unroll
+            for (int h2 = 0; h2 < 32; h2 += 16) {
+                uint16_t rv[16];
+#pragma unroll
+                for (int b = 0; b < 16; ++b) rv[b] = __ldcg(res + (size_t)(h2 + b) * a.N + n);
+#pragma unroll
+                for (int b = 0; b < 16; ++b) resb[(h2 + b) * BM + row] = rv[b];
+            }
+        }
         // RMSNorm scale of the input rows (statistics of an earlier launch): load
         // it now, its latency hides under the partial exchange
         if (a.stats_in && warp >= 4) {
@@ -562,14 +581,13 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
                     for (int b = 0; b < 32; ++b) out[(size_t)b * a.N + n] = f_to_bf16(acc[b] * rvec[b]);
                 }
             } else if (a.mode == kGemvResid) {
-                const uint16_t* __restrict__ res = reinterpret_cast<const uint16_t*>(a.resid);
                 uint16_t* __restrict__ out = reinterpret_cast<uint16_t*>(a.out);
                 if (active) {
 #pragma unroll
                     for (int h2 = 0; h2 < 32; h2 += 16) {
-                        uint16_t rv[16];  // 16 residual loads in flight before any store
+                        uint16_t rv[16];  // residual inputs staged before the exchange
 #pragma unroll
-                        for (int b = 0; b < 16; ++b) rv[b] = __ldcg(res + (size_t)(h2 + b) * a.N + n);
+                        for (int b = 0; b < 16; ++b) rv[b] = resb[(h2 + b) * BM + row];
 #pragma unroll
                         for (int b = 0; b < 16; ++b) {
                             const uint16_t hb = f_to_bf16(bf16_to_f(rv[b]) + acc[h2 + b] * rvec[h2 + b]);

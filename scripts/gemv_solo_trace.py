@@ -36,4 +36,14 @@ for kname in os.environ.get("KERNELS", "gate_up,down,qkv,o").split(","):
                   "teardown_us_med": round(float(statistics.median(rel[:, 6] - rel[:, 5])), 2),
                   "accum_final_us": [round(float(v), 2) for v in (rel[:, 1].min(), statistics.median(rel[:, 1]), rel[:, 1].max())],
                   "end_us": [round(float(v), 2) for v in (rel[:, 6].min(), statistics.median(rel[:, 6]), rel[:, 6].max())]}
+    own = x[:, 2] > 0  # combiners (split-K owners) stamp the partials-arrived time
+    if own.any():
+        r = rel[own]
+        out[kname]["owners"] = {
+            "n": int(own.sum()),
+            "wait_partials_us_med": round(float(statistics.median(((x[own, 2] - t0) / 1e3) - r[:, 1])), 2),
+            "sum_us_med": round(float(statistics.median(r[:, 3] - (x[own, 2] - t0) / 1e3)), 2),
+            "scale_us_med": round(float(statistics.median(r[:, 4] - r[:, 3])), 2),
+            "mode_us_med": round(float(statistics.median(r[:, 5] - r[:, 4])), 2),
+            "end_us_max": round(float(r[:, 6].max()), 2)}
     print(kname, json.dumps(out[kname]), flush=True)
