@@ -96,7 +96,7 @@ __device__ __forceinline__ int gemv_block_of(int64_t u, int64_t U, int G) {
 // order the block's whole weight range is one contiguous run of 16-KB tiles.
 template <int BM, int STAGES>
 __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, const GemvPiece p0, const GemvPiece p1,
-                                              int np, uint32_t tmem_base, const BodyCtx& dep) {
+                                              int np, uint32_t tmem_base, const BodyCtx& dep, float* rv_out = nullptr) {
     using L = TcSmem<kGemvBN, STAGES, kTcBK, BM>;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + L::kBarOff);
     uint64_t* empty = full + STAGES;
@@ -196,6 +196,29 @@ __device__ __forceinline__ void gemv_mainloop(char* base, const GemvArgs& a, con
         tc::mma_commit(&tmem_full[0]);
     }
     if (warp >= 4) {
+        // rv_out: the epilogue warps, idle while the ring streams, fold the
+        // inputs' RMSNorm statistics (an earlier launch's output: acquired by
+        // thread 128's own wait_prev) into the per-row scale now, off the
+        // critical path; x 1.0 (exact) without statistics
+        if (rv_out) {
+            float* red = rv_out + 32;  // [4][32] quarter sums
+            const int q = warp & 3;
+            if (ltid() == 128) wait_prev(dep);
+            epi_sync();
+            float ss = 0.f;
+            if (a.stats_in) {
+                const float* st = reinterpret_cast<const float*>(a.stats_in);
+                const int pa = q * a.P_in / 4, pb = (q + 1) * a.P_in / 4;
+#pragma unroll 8
+                for (int p = pa; p < pb; ++p) ss += __ldcg(st + p * 32 + lane);
+            }
+            red[q * 32 + lane] = ss;
+            epi_sync();
+            if (warp == 4)
+                rv_out[lane] = a.stats_in ? rsqrtf((((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane]) /
+                                                   (float)a.K + a.eps)
+                                          : 1.f;
+        }
         tc::mbar_wait(tmem_full, 0);
         tc::tc_fence_after();
     }
@@ -421,13 +444,15 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
     if (dbg && ltid() == 0) dbg[0] = globaltimer();
     BodyCtx cd = c;
     cd.dbg = dbg;
-    gemv_mainloop<BM, STAGES>(base, a, pA, pB, np, c.tmem_base, cd);
+    // the owner's per-row RMSNorm scale, computed during the mainloop, lives
+    // past the barriers (the ring is busy until the accumulators are final)
+    float* rv_pre = reinterpret_cast<float*>(base + TcSmem<kGemvBN, STAGES, kTcBK, BM>::kBarOff + 256);
+    gemv_mainloop<BM, STAGES>(base, a, pA, pB, np, c.tmem_base, cd, pA.owner ? rv_pre : nullptr);
     if (ltid() == 128) mark_streamed(c);  // tmem_full: every weight / X load of this block has landed
     wait_prev_all(c);  // the epilogue reads residual / norm statistics of earlier launches
     if (dbg && ltid() == 128) dbg[1] = globaltimer();
     const int warp = ltid() >> 5, lane = ltid() & 31;
-    float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + rvec[32] + flag
-    float* rvec = scratch + 128 * 33;
+    float* scratch = reinterpret_cast<float*>(base + kGemvScratch);  // [128][33] + row sums [4][32]
     const int q = warp & 3;
     const bool active = lane < QR;  // lanes holding a slab row (all of them at BM = 128)
     const int row = q * QR + lane;  // epilogue warps: row within the slab
@@ -474,17 +499,6 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
 #pragma unroll
                 for (int b = 0; b < 16; ++b) resb[(h2 + b) * BM + row] = rv[b];
             }
-        }
-        // RMSNorm scale of the input rows (statistics of an earlier launch): load
-        // it now, its latency hides under the partial exchange
-        if (a.stats_in && warp >= 4) {
-            float* red = scratch + 128 * 33 + 64;  // [4][32]
-            const float* st = reinterpret_cast<const float*>(a.stats_in);
-            const int p0 = q * a.P_in / 4, p1 = (q + 1) * a.P_in / 4;
-            float ss = 0.f;
-#pragma unroll 8
-            for (int p = p0; p < p1; ++p) ss += __ldcg(st + p * 32 + lane);
-            red[q * 32 + lane] = ss;
         }
         if (S > 1) {
             // the owner's own partial stays on chip: [128 rows][8 float4] in the
@@ -563,15 +577,11 @@ __device__ __forceinline__ void gemv_body(const BodyCtx& c, const GemvArgs& a) {
         // summed in k order); each mode reads them element by element, so no
         // 32-register array stays live through the epilogue
         if (warp >= 4) {
-            // RMSNorm of the input rows folded in as a per-row scale (sums
-            // loaded before the partial exchange); x 1.0 (exact) without it
-            float* red = scratch + 128 * 33 + 64;  // [4][32]
-            epi_sync();
-            if (warp == 4)
-                rvec[lane] = a.stats_in ? rsqrtf((((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane]) /
-                                                     (float)a.K + a.eps)
-                                        : 1.f;
-            epi_sync();
+            // RMSNorm of the input rows folded in as a per-row scale (rv_pre,
+            // computed during the mainloop); x 1.0 (exact) without it
+            float* red = scratch + 128 * 33 + 64;  // [4][32] (kGemvResid row sums)
+            const float* rvec = rv_pre;
+            epi_sync();  // every row's accumulators in scratch (pair modes read the neighbour row)
             const float* acc = scratch + row * 33;
             if (dbg && ltid() == 128) dbg[4] = globaltimer();
             if (a.mode == kGemvStore) {
