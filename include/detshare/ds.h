@@ -323,6 +323,10 @@ int ds_verify_kernels(ds_domain* dom, int* first_bad);
 /* ---- solo baseline: the same body as a plain __global__ grid (exclusive_baseline) ---- */
 int ds_solo_launch(int device, const ds_kernel_desc* desc, void* stream);
 int ds_solo_launch_registered(ds_domain* dom, int kernel_id, void* stream);
+/* diagnostics: per-CTA globaltimer stamps of later solo launches on `device`
+ * into dev_buf (uint64 [grid][4]: entry, TMEM allocated, body returned,
+ * exit); NULL turns them off */
+int ds_solo_trace(int device, void* dev_buf);
 int ds_body_smem(int body, uint32_t* bytes);
 
 /* ---- body argument helpers ---- */

@@ -493,7 +493,7 @@ EXPORTS = [
     "ds_unbind", "ds_migrate", "ds_preempt", "ds_bound_pctx", "ds_quota_set", "ds_quota_get",
     "ds_set_lend", "ds_quota_at_claim", "ds_quota_periodic", "ds_stats_get", "ds_transcript",
     "ds_logical_progress", "ds_block_log", "ds_switch_log", "ds_ctl_log", "ds_clear_logs",
-    "ds_globaltimer", "ds_debug_dump", "ds_ctl_roundtrip", "ds_measure_ffma_peak", "ds_solo_launch", "ds_solo_launch_registered", "ds_body_smem",
+    "ds_globaltimer", "ds_debug_dump", "ds_ctl_roundtrip", "ds_measure_ffma_peak", "ds_solo_launch", "ds_solo_launch_registered", "ds_solo_trace", "ds_body_smem",
     "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_kv", "ds_attn_chunk", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",

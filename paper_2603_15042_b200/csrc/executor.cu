@@ -993,10 +993,17 @@ extern "C" __global__ void __launch_bounds__(kExecThreads, 1) ds_executor_kernel
 
 // Solo baseline: the same body as a plain grid (exclusive_baseline,
 // src/engine/engine.cpp:1400-1417).  256 threads, blockIdx = logical block.
+// optional per-CTA stamps of the solo wrapper (ds_solo_trace): entry, TMEM
+// allocated, body returned, exit -- where a plain-grid launch spends time
+// outside the body
+__device__ unsigned long long* g_solo_trace = nullptr;
+
 extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     ds_solo_kernel(int body, const void* args, uint32_t gx, uint32_t gy, uint32_t gz, uint32_t smem_bytes) {
     extern __shared__ __align__(1024) char smem[];
     uint32_t b = blockIdx.x;
+    unsigned long long* const tr = g_solo_trace;
+    if (tr && threadIdx.x == 0) tr[(size_t)b * 4] = globaltimer();
     BodyCtx c;
     c.gx = gx;
     c.gy = gy;
@@ -1026,13 +1033,16 @@ extern "C" __global__ void __launch_bounds__(kBodyThreads, 1)
     } else {
         c.tmem_base = 0;
     }
+    if (tr && threadIdx.x == 0) tr[(size_t)b * 4 + 1] = globaltimer();
     run_body(body, c);
+    if (tr && threadIdx.x == 0) tr[(size_t)b * 4 + 2] = globaltimer();
     if (tc_body) {
         tc::tc_fence_before();
         __syncthreads();
         tc::tc_fence_after();
         if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(c.tmem_base, kLaneTmemCols);
     }
+    if (tr && threadIdx.x == 0) tr[(size_t)b * 4 + 3] = globaltimer();
 }
 
 extern "C" __global__ void ds_probe_kernel(uint32_t* smids, uint32_t* nsmid, uint64_t* timer) {
@@ -1071,6 +1081,11 @@ extern "C" cudaError_t ds_dev_executor_occupancy(uint32_t smem, int* blocks_per_
     cudaError_t e = exec_attrs(smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, ds::ds_executor_kernel, ds::kExecThreads, smem);
+}
+
+extern "C" cudaError_t ds_dev_solo_trace(void* buf) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+    return cudaMemcpyToSymbol(ds::g_solo_trace, &p, sizeof(p));
 }
 
 extern "C" cudaError_t ds_dev_launch_solo(int body, const void* args, uint32_t gx, uint32_t gy, uint32_t gz,

@@ -1381,6 +1381,16 @@ int ds_tensor_map_bf16_kv(void* out128, const void* base, uint64_t rows, uint32_
     return DS_OK;
 }
 
+extern "C" cudaError_t ds_dev_solo_trace(void* buf);
+// per-CTA stamps of plain-grid solo launches into dev_buf (u64 [grid][4]:
+// entry, TMEM allocated, body returned, exit); nullptr turns them off
+int ds_solo_trace(int device, void* dev_buf) {
+    if (cudaSetDevice(device) != cudaSuccess) return fail(DS_CUDA_ERROR, "cudaSetDevice");
+    cudaError_t e = ds_dev_solo_trace(dev_buf);
+    if (e != cudaSuccess) return fail(DS_CUDA_ERROR, cudaGetErrorString(e));
+    return DS_OK;
+}
+
 int ds_solo_launch(int device, const ds_kernel_desc* k, void* stream) {
     if (!k) return fail(DS_INVALID_ARGUMENT, "null desc");
     if (k->body <= DS_BODY_NONE || k->body >= DS_BODY_COUNT) return fail(DS_CONFIG_ERROR, "unknown body");
