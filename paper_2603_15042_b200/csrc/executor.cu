@@ -1090,8 +1090,19 @@ extern "C" cudaError_t ds_dev_solo_trace(void* buf) {
 
 extern "C" cudaError_t ds_dev_launch_solo(int body, const void* args, uint32_t gx, uint32_t gy, uint32_t gz,
                                           uint32_t smem, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(ds::ds_solo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    // attributes set once per size (and the carveout pinned to max shared, the
+    // configuration every tensor-core body needs), not per launch
+    static int cur_smem[64] = {0};  // per device: function attributes are per device context
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0, cur_smem[0] = 0;
+    if ((int)smem > cur_smem[dev] || cur_smem[dev] == 0) {
+        cudaError_t e = cudaFuncSetAttribute(ds::ds_solo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(ds::ds_solo_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        cur_smem[dev] = (int)smem;
+    }
     ds::ds_solo_kernel<<<dim3(gx * gy * gz), dim3(ds::kBodyThreads), smem, s>>>(body, args, gx, gy, gz, smem);
     return cudaGetLastError();
 }
