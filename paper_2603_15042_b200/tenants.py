@@ -530,6 +530,17 @@ class ResNetStream:
             return (N, M) if pad(N, M) < pad(M, N) else (M, N)
         self.gemms = [(name,) + orient(M, N) + (K,) for name, M, N, K in self.gemms]
         plans = [plan_gemm(M, N, K) for _, M, N, K in self.gemms]
+        # measured per-GEMM (tile width, split-K) for the split-K GEMMs
+        # (scripts/autotune_resnet.py -> resnet_plan.json); DS_RESNET_TUNED=0 ignores it
+        tuned_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "resnet_plan.json")
+        if os.environ.get("DS_RESNET_TUNED", "1") != "0" and os.path.exists(tuned_path):
+            import json
+            tuned = json.load(open(tuned_path))
+            for i, (name, M, N, K) in enumerate(self.gemms):
+                t = tuned.get(name)
+                Mp, Np, Kp, bn, sp = plans[i]
+                if t and sp > 1 and Np % t["bn"] == 0 and t["splits"] >= 2 and (Kp // 64) // t["splits"] >= 1:
+                    plans[i] = (Mp, Np, Kp, int(t["bn"]), int(t["splits"]))
         self.padded_flops = sum(2.0 * Mp * Np * Kp for Mp, Np, Kp, _, _ in plans)
         a_el = max(Mp * Kp for Mp, Np, Kp, _, _ in plans)
         b_el = max(Np * Kp for Mp, Np, Kp, _, _ in plans)

@@ -62,3 +62,25 @@ def test_resnet_multi_tile_plan():
     assert n_multi > 0
     assert plan_tiles(8192, 8192, 8192, 256, 1) == (256, 1)   # long K: one tile per block
     assert plan_tiles(401408, 64, 64, 64, 1, max_tiles=1) == (64, 1)
+
+
+def test_resnet_tuned_plan_table_is_valid():
+    """resnet_plan.json (scripts/autotune_resnet.py): measured (tile width,
+    split-K) per split-K GEMM of the stream; every entry names a GEMM of the
+    stream whose plan splits K, its tile divides the padded N, and every split
+    keeps >= 8 k-blocks (the search's own bound)."""
+    import json, os
+    from paper_2603_15042_b200.tenants import plan_gemm, resnet50_gemms
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "paper_2603_15042_b200", "resnet_plan.json")
+    table = json.load(open(path))
+    shapes = {}
+    for name, M, N, K in resnet50_gemms():
+        pad = lambda m, n: ((m + 127) // 128 * 128) * ((n + 63) // 64 * 64)  # noqa: E731
+        shapes[name] = (N, M, K) if pad(N, M) < pad(M, N) else (M, N, K)  # ResNetStream's orientation
+    assert table
+    for name, t in table.items():
+        Mp, Np, Kp, bn, s = plan_gemm(*shapes[name])
+        assert s > 1, name
+        assert t["bn"] in (64, 128, 256) and Np % t["bn"] == 0, name
+        assert t["splits"] >= 2 and (Kp // 64) // t["splits"] >= 8, name
