@@ -533,14 +533,16 @@ class ResNetStream:
         # measured per-GEMM (tile width, split-K) for the split-K GEMMs
         # (scripts/autotune_resnet.py -> resnet_plan.json); DS_RESNET_TUNED=0 ignores it
         tuned_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "resnet_plan.json")
+        self._tuned_tiles = {}
         if os.environ.get("DS_RESNET_TUNED", "1") != "0" and os.path.exists(tuned_path):
             import json
             tuned = json.load(open(tuned_path))
             for i, (name, M, N, K) in enumerate(self.gemms):
                 t = tuned.get(name)
                 Mp, Np, Kp, bn, sp = plans[i]
-                if t and sp > 1 and Np % t["bn"] == 0 and t["splits"] >= 2 and (Kp // 64) // t["splits"] >= 1:
+                if t and Np % t["bn"] == 0 and (t["splits"] == 1 or (Kp // 64) // t["splits"] >= 1):
                     plans[i] = (Mp, Np, Kp, int(t["bn"]), int(t["splits"]))
+                    self._tuned_tiles[name] = int(t.get("tiles", 0))
         self.padded_flops = sum(2.0 * Mp * Np * Kp for Mp, Np, Kp, _, _ in plans)
         a_el = max(Mp * Kp for Mp, Np, Kp, _, _ in plans)
         b_el = max(Np * Kp for Mp, Np, Kp, _, _ in plans)
@@ -558,7 +560,8 @@ class ResNetStream:
         fold_wide = os.environ.get("DS_RESNET_FOLD_WIDE", "1") != "0"
         self.tiles = []
         for (name, M, N, K), (Mp, Np, Kp, bn, s) in zip(self.gemms, plans):
-            bn, T = plan_tiles(Mp, Np, Kp, bn, s, max_tiles=max_t)
+            tt = self._tuned_tiles.get(name, 0)
+            bn, T = (bn, tt) if tt else plan_tiles(Mp, Np, Kp, bn, s, max_tiles=max_t)
             self.tiles.append((bn, T))
             ga = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, bn=bn,
                                 splits=s, ws=self.ws.data_ptr() if s > 1 else 0, tiles=T)

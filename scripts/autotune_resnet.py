@@ -1,5 +1,5 @@
-"""Per-GEMM (tile width, split-K) search for the ResNet stream's split-K
-GEMMs (weight gradients): each candidate runs as its GEMM + fold launch pair
+"""Per-GEMM (tile width, split-K, tiles per block) search for every GEMM of
+the ResNet stream: each candidate runs as its GEMM (+ fold) launch pair
 on the full-GPU executor (5 timed pairs, median of first-claim -> fold end);
 the fastest is written to paper_2603_15042_b200/resnet_plan.json, which
 ResNetStream applies (DS_RESNET_TUNED=0 ignores it).  Reduction order is a
@@ -21,10 +21,10 @@ dom.start()
 dom.quota_set(dom.mask(t, 0, dom.num_sms))
 
 
-def time_pair(Mp, Np, Kp, bn, S):
+def time_pair(Mp, Np, Kp, bn, S, T=1):
     ga = _abi.gemm_args(rs.A.data_ptr(), rs.B.data_ptr(), rs.C.data_ptr(), Mp, Np, Kp, bn=bn, splits=S,
-                        ws=WS.data_ptr() if S > 1 else 0)
-    ks = [dom.kernel("tune/gemm", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, S), ga)]
+                        ws=WS.data_ptr() if S > 1 else 0, tiles=T)
+    ks = [dom.kernel("tune/gemm", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, S, T), ga)]
     if S > 1:
         ra, rg = _abi.splitk_reduce(WS.data_ptr(), rs.C.data_ptr(), Mp, Np, Kp, 16, bn, S,
                                     _abi.fold_rows(Mp, Np, bn, WORKERS))
@@ -41,24 +41,31 @@ def time_pair(Mp, Np, Kp, bn, S):
     return statistics.median(ts)
 
 
+from paper_2603_15042_b200.tenants import plan_tiles
 table = {}
 for name, M, N, K in rs.gemms:
     Mp, Np, Kp, bn0, S0 = plan_gemm(M, N, K)
-    if S0 <= 1:
-        continue
-    cands = set()
+    bnT, T0 = plan_tiles(Mp, Np, Kp, bn0, S0, max_tiles=4)
+    base = (bnT, S0, T0)  # the heuristic plan as the stream builds it
+    cands = {base}
     for bn in (64, 128, 256):
         if Np % bn:
             continue
         tiles = (Mp // 128) * (Np // bn)
-        for S in {max(2, S0 // 2), S0, 2 * S0, -(-WORKERS // tiles), -(-2 * WORKERS // tiles)}:
-            if S < 2 or (Kp // 64) // S < 8 or _abi.splitk_ws_elems(Mp, Np, bn, S) > WS.numel():
+        for S in {1, max(2, S0 // 2), S0, 2 * S0, -(-WORKERS // tiles), -(-2 * WORKERS // tiles)}:
+            if S > 1 and ((Kp // 64) // S < 8 or _abi.splitk_ws_elems(Mp, Np, bn, S) > WS.numel()):
                 continue
-            cands.add((bn, S))
+            if S == 1 and tiles < WORKERS // 2:
+                continue  # far below a wave: not a candidate
+            cands.add((bn, S, 1))
+            if S == 1 and bn <= 128 and Kp <= 1152:
+                for T in (2, 4, 8):
+                    if tiles // T >= WORKERS:
+                        cands.add((bn, 1, T))
     res = {c: time_pair(Mp, Np, Kp, *c) for c in sorted(cands)}
     best = min(res, key=res.get)
-    table[name] = {"bn": best[0], "splits": best[1], "us": round(res[best], 1),
-                   "plan": [bn0, S0], "plan_us": round(res.get((bn0, S0), float("nan")), 1)}
+    table[name] = {"bn": best[0], "splits": best[1], "tiles": best[2], "us": round(res[best], 1),
+                   "plan": list(base), "plan_us": round(res[base], 1)}
     print(name, table[name], flush=True)
 dom.stop(); dom.close()
 out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2603_15042_b200", "resnet_plan.json")
