@@ -334,6 +334,11 @@ int ds_body_smem(int body, uint32_t* bytes);
  * matrix, SWIZZLE_128B boxes of box_rows x box_cols (box_cols*2 must be 128) */
 int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                           uint32_t box_cols);
+/* the same over a pitched array: rows x cols valid elements, rows `pitch`
+ * elements apart (cols <= pitch); loads past the valid extent read zeros
+ * without touching memory, stores past it are dropped */
+int ds_tensor_map_bf16_2d_pitched(void* out128, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch,
+                                  uint32_t box_rows, uint32_t box_cols);
 /* KV-cache rows of 128 bf16 as a 3-D {64 dims, rows, 2 halves} view: one box
  * = box_rows rows as two SWIZZLE_128B half-tiles (dims 0-63, then 64-127).
  * box_rows must equal ds_attn_chunk(). */

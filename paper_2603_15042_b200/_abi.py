@@ -184,9 +184,18 @@ class SplitkReduceArgs(ctypes.Structure):
                 ("rows", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
-def tensor_map_bf16(ptr: int, rows: int, cols: int, box_rows: int, box_cols: int = 64) -> TmaDesc:
+def tensor_map_bf16(ptr: int, rows: int, cols: int, box_rows: int, box_cols: int = 64, pitch: int = 0) -> TmaDesc:
+    """rows x cols bf16 (row pitch `pitch` elements, default cols): TMA boxes
+    past the valid extent load zeros without reading memory; stores clip."""
     d = TmaDesc()
-    check(lib().ds_tensor_map_bf16_2d(ctypes.byref(d), ctypes.c_void_p(ptr), rows, cols, box_rows, box_cols))
+    if pitch and pitch != cols:
+        L = lib()
+        L.ds_tensor_map_bf16_2d_pitched.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                                    ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
+        check(L.ds_tensor_map_bf16_2d_pitched(ctypes.byref(d), ctypes.c_void_p(ptr), rows, cols, pitch, box_rows,
+                                              box_cols))
+    else:
+        check(lib().ds_tensor_map_bf16_2d(ctypes.byref(d), ctypes.c_void_p(ptr), rows, cols, box_rows, box_cols))
     return d
 
 
@@ -215,7 +224,12 @@ GEMM_BM, GEMM_BN = 128, 256
 
 def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16, bn: int = GEMM_BN,
               splits: int = 1, ws: int = 0, bk: int = 64, tma_store: bool = True,
-              abandon: bool = False, l2_hint: int = 0, tiles: int = 1) -> "GemmArgs":
+              abandon: bool = False, l2_hint: int = 0, tiles: int = 1, valid=None) -> "GemmArgs":
+    """C[M,N] = A[M,K] . B[N,K]^T over tile-padded arrays.  valid = (m, n, k):
+    the true extents inside them (<= M, N, K): the operand loads stop there
+    (TMA zero fill, padding never read) and the TMA stores clip at (m, n
+    rounded up to 8: the store unit is 16 bytes; those columns get zeros);
+    None = the padded arrays are the operands."""
     if bn not in (64, 128, 256):
         raise DsError(10, f"gemm tile width {bn} not in (64, 128, 256)")
     if M % GEMM_BM or N % bn or K % 64:
@@ -226,9 +240,16 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
         raise DsError(10, "bk 32 (SWIZZLE_64B, 4 stages) is built for 128x256 tiles only")
     if tiles > 1 and (bn not in (64, 128) or splits > 1 or bk != 64 or not tma_store or abandon):
         raise DsError(10, "multi-tile GEMM blocks need bn 64/128, no split-K, bk 64, TMA stores, no abandon")
-    tmC = tensor_map_bf16(C, M, N, GEMM_BM, 64) if tma_store else TmaDesc()
-    a = GemmArgs(tensor_map_bf16(A, M, K, GEMM_BM, bk), tensor_map_bf16(B, N, K, bn, bk), C, M, N, K, group_m, bn,
-                 max(1, splits), ws, bk, int(tma_store))
+    m, n, k = valid if valid is not None else (M, N, K)
+    if not (0 < m <= M and 0 < n <= N and 0 < k <= K):
+        raise DsError(10, f"valid extents {valid} outside the {M}x{N}x{K} arrays")
+    if valid is not None and splits <= 1 and not tma_store:
+        raise DsError(10, "valid extents need TMA stores (or split-K) to keep C's padding unwritten")
+    # TMA stores clip at 16-byte granularity: columns up to the next multiple
+    # of 8 past n are written (zeros: B's rows >= n load as zeros)
+    tmC = tensor_map_bf16(C, m, min(N, -(-n // 8) * 8), GEMM_BM, 64, pitch=N) if tma_store else TmaDesc()
+    a = GemmArgs(tensor_map_bf16(A, m, k, GEMM_BM, bk, pitch=K), tensor_map_bf16(B, n, k, bn, bk, pitch=K), C, M, N,
+                 K, group_m, bn, max(1, splits), ws, bk, int(tma_store))
     a.tmC = tmC
     a.abandon = int(abandon)  # False/0 off, True/1 restart, 2 spill + resume
     # L2 policy of the operand loads: bits [1:0] A, [3:2] B; 0 default (A evict_last, B none),
@@ -494,7 +515,7 @@ EXPORTS = [
     "ds_set_lend", "ds_quota_at_claim", "ds_quota_periodic", "ds_stats_get", "ds_transcript",
     "ds_logical_progress", "ds_block_log", "ds_switch_log", "ds_ctl_log", "ds_clear_logs",
     "ds_globaltimer", "ds_debug_dump", "ds_ctl_roundtrip", "ds_measure_ffma_peak", "ds_solo_launch", "ds_solo_launch_registered", "ds_solo_trace", "ds_body_smem",
-    "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_kv", "ds_attn_chunk", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
+    "ds_tensor_map_bf16_2d", "ds_tensor_map_bf16_2d_pitched", "ds_tensor_map_bf16_kv", "ds_attn_chunk", "ds_engine_last_error", "ds_engine_create", "ds_engine_destroy",
     "ds_engine_add_job", "ds_engine_submit", "ds_engine_start", "ds_engine_stop", "ds_engine_now", "ds_engine_wait",
     "ds_engine_record", "ds_engine_counters_get", "ds_engine_transcript", "ds_engine_predict", "ds_policy_names",
     "ds_gen_poisson", "ds_gen_burst", "ds_expand_workload", "ds_place_tenants",

@@ -1324,10 +1324,20 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                           uint32_t box_cols) {
+    return ds_tensor_map_bf16_2d_pitched(out128, base, rows, cols, cols, box_rows, box_cols);
+}
+
+// rows x cols valid elements of a row-major bf16 array whose rows are `pitch`
+// elements apart (cols <= pitch): boxes reaching past the valid extent are
+// zero-filled by the TMA unit and never read from memory; stores past it are
+// clipped (the GEMM tenant on unpadded shapes, e.g. conv1's K = 147)
+int ds_tensor_map_bf16_2d_pitched(void* out128, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch,
+                                  uint32_t box_rows, uint32_t box_cols) {
     if (!out128 || !base) return fail(DS_INVALID_ARGUMENT, "null");
+    if (cols == 0 || rows == 0 || cols > pitch) return fail(DS_INVALID_ARGUMENT, "need 0 < cols <= pitch, rows > 0");
     if (box_cols * 2 != 128 && box_cols * 2 != 64)
         return fail(DS_CONFIG_ERROR, "box inner extent must be 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B)");
-    if ((cols * 2) % 16 != 0 || ((uintptr_t)base & 15)) return fail(DS_CONFIG_ERROR, "row pitch / base must be 16-B aligned");
+    if ((pitch * 2) % 16 != 0 || ((uintptr_t)base & 15)) return fail(DS_CONFIG_ERROR, "row pitch / base must be 16-B aligned");
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         void* p = nullptr;
@@ -1338,7 +1348,7 @@ int ds_tensor_map_bf16_2d(void* out128, const void* base, uint64_t rows, uint64_
     }
     CUtensorMap m;
     cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols * 2};
+    cuuint64_t strides[1] = {pitch * 2};
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,

@@ -563,8 +563,11 @@ class ResNetStream:
             tt = self._tuned_tiles.get(name, 0)
             bn, T = (bn, tt) if tt else plan_tiles(Mp, Np, Kp, bn, s, max_tiles=max_t)
             self.tiles.append((bn, T))
+            # true extents: the TMA loads never read the tile padding (conv1's
+            # K = 147 of 192, its 147 weight-gradient rows of 256, FC's 1000)
             ga = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, bn=bn,
-                                splits=s, ws=self.ws.data_ptr() if s > 1 else 0, tiles=T)
+                                splits=s, ws=self.ws.data_ptr() if s > 1 else 0, tiles=T,
+                                valid=None if os.environ.get("DS_RESNET_PADDED") else (M, N, K))
             self.records.append((f"resnet/{name}", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, s, T), ga,
                                  2.0 * M * N * K))
             if s > 1:

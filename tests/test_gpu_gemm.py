@@ -241,3 +241,29 @@ def test_gemm_multi_tile_rejects_unsupported():
     for kw in (dict(bn=256), dict(bn=128, splits=2, ws=1), dict(bn=128, abandon=True)):
         with pytest.raises(DsError):
             _abi.gemm_args(1, 1, 1, 1024, 1024, 1024, tiles=4, **kw)
+
+
+@pytest.mark.parametrize("valid,bn,T", [((300, 200, 147), 64, 1), ((1000, 100, 100), 64, 2), ((147, 64, 5000), 64, 1)])
+def test_gemm_valid_extents_read_no_padding(valid, bn, T):
+    """Unpadded shapes inside tile-padded arrays (GemmArgs via valid=):
+    the TMA loads zero-fill past (m, k) / (n, k), so garbage in the padding
+    never reaches C, and the stores clip at (m, n), so C's padding keeps its
+    contents (past n rounded up to 8: the 16-byte store unit writes zeros up
+    to there); the valid block matches fp32 within the bf16 tolerance."""
+    m, n, k = valid
+    M, N, K = -(-m // 128) * 128, -(-n // bn) * bn, -(-k // 64) * 64
+    A, B, _ = make(M, N, K, seed=9)
+    A[m:, :] = float("nan")
+    A[:, k:] = float("nan")
+    B[n:, :] = float("nan")
+    B[:, k:] = float("nan")
+    C = torch.full((M, N), 7.0, device="cuda", dtype=torch.bfloat16)
+    args = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, bn=bn, tiles=T, valid=(m, n, k))
+    solo_launch(0, "gemm", _abi.BODY_GEMM_BF16, _abi.gemm_grid(M, N, bn, tiles=T), args)
+    torch.cuda.synchronize()
+    ref = A[:m, :k].float() @ B[:n, :k].float().t()
+    got = C[:m, :n].float()
+    assert bool(((got - ref).abs() <= ref.abs() * 2 ** -7 + 2 ** -6).all())
+    n8 = -(-n // 8) * 8  # TMA stores clip at 16-byte granularity
+    assert bool((C[m:, :] == 7.0).all()) and bool((C[:, n8:] == 7.0).all())
+    assert bool((C[:m, n:n8] == 0.0).all())
