@@ -174,7 +174,7 @@ class GemmArgs(ctypes.Structure):
                 ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_m", ctypes.c_int32), ("bn", ctypes.c_int32),
                 ("splits", ctypes.c_int32), ("ws", ctypes.c_uint64), ("bk", ctypes.c_int32),
                 ("tma_store", ctypes.c_int32), ("abandon", ctypes.c_int32), ("l2_hint", ctypes.c_int32),
-                ("tiles", ctypes.c_int32), ("pad2", ctypes.c_uint8 * 4),
+                ("tiles", ctypes.c_int32), ("fuse_fold", ctypes.c_int32),
                 ("tmC", TmaDesc)]  # tmC: alignas(64)
 
 
@@ -224,7 +224,8 @@ GEMM_BM, GEMM_BN = 128, 256
 
 def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16, bn: int = GEMM_BN,
               splits: int = 1, ws: int = 0, bk: int = 64, tma_store: bool = True,
-              abandon: bool = False, l2_hint: int = 0, tiles: int = 1, valid=None) -> "GemmArgs":
+              abandon: bool = False, l2_hint: int = 0, tiles: int = 1, valid=None,
+              fuse_fold: bool = False) -> "GemmArgs":
     """C[M,N] = A[M,K] . B[N,K]^T over tile-padded arrays.  valid = (m, n, k):
     the true extents inside them (<= M, N, K): the operand loads stop there
     (TMA zero fill, padding never read) and the TMA stores clip at (m, n
@@ -256,6 +257,11 @@ def gemm_args(A: int, B: int, C: int, M: int, N: int, K: int, group_m: int = 16,
     # 1 evict_first, 2 evict_last, 3 evict_normal
     a.l2_hint = int(l2_hint)
     a.tiles = max(1, int(tiles))  # T consecutive raster tiles per logical block (gemm_multi)
+    if fuse_fold and (splits <= 1 or abandon):
+        raise DsError(10, "fuse_fold needs split-K (splits > 1) and no abandon")
+    # split-K with the fold inside: the last split of each tile folds it; the
+    # workspace needs splitk_ws_elems + fold_tickets (zeroed) elements
+    a.fuse_fold = int(bool(fuse_fold))
     return a
 
 
@@ -264,6 +270,12 @@ def gemm_grid(M: int, N: int, bn: int = GEMM_BN, splits: int = 1, tiles: int = 1
     if tiles > 1:
         return ((n + tiles - 1) // tiles, 1, 1)
     return (n * max(1, splits), 1, 1)
+
+
+def fold_tickets(M: int, N: int, bn: int) -> int:
+    """Workspace elements (after splitk_ws_elems) holding a fused-fold GEMM's
+    per-tile tickets; zero them once, the last arriver resets its own."""
+    return (M // GEMM_BM) * (N // bn)
 
 
 def splitk_ws_elems(M: int, N: int, bn: int, splits: int) -> int:

@@ -257,7 +257,8 @@ struct GemmArgs {
     int32_t l2_hint;    // L2 policy of the A / B operand loads (tc_mainloop's l2_hint; 0 = A evict_last, B none)
     int32_t tiles;      // 0/1: one output tile per logical block; T >= 2: T consecutive raster tiles per block
                         // (gemm_multi: BN 64 / 128, no split-K, not abandonable; same bits per tile)
-    int32_t pad3;
+    int32_t fuse_fold;  // S > 1: the last-arriving split of each tile folds the S partials in split order and
+                        // stores bf16 C itself (no SPLITK_REDUCE launch); per-tile tickets follow the workspace
     TmaDesc tmC;        // C [M][N] bf16, box {64, 128}, SWIZZLE_128B
 };
 static_assert(offsetof(GemmArgs, tmC) == 320 && sizeof(GemmArgs) == 448, "GemmArgs layout (mirrored in _abi.py)");
@@ -422,6 +423,48 @@ __device__ __forceinline__ void gemm_body_bn(const BodyCtx& c, const GemmArgs& a
                 tc::tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < 8; ++j) dst[ch * 8 + j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+            if (a.fuse_fold) {
+                // ticket: the split that arrives last folds the tile (release:
+                // this split's partial stores, fenced before the add; acquire:
+                // the others', fenced after it), in split order 0..S-1 per
+                // element -- the SPLITK_REDUCE body's order, so the same bits
+                __shared__ int last_l[2];
+                volatile int* last = &last_l[body_lane()];
+                uint32_t* tickets = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(a.ws) +
+                                                                (size_t)(a.M / kTcBM) * (a.N / BN) * S * kTcBM * BN);
+                epi_sync();
+                if (q == 0 && lane == 0) {
+                    __threadfence();
+                    const uint32_t old = atomicAdd(tickets + tile, 1u);
+                    *last = old == (uint32_t)(S - 1);
+                    if (old == (uint32_t)(S - 1)) {
+                        __threadfence();
+                        tickets[tile] = 0u;  // at rest for the record's next launch
+                    }
+                }
+                epi_sync();
+                if (*last) {
+                    const int row = q * 32 + lane;
+                    const float* src = reinterpret_cast<const float*>(a.ws) + ((size_t)tile * S * kTcBM + row) * BN;
+                    __nv_bfloat16* Cr = reinterpret_cast<__nv_bfloat16*>(a.C) + (size_t)(m_blk * kTcBM + row) * a.N +
+                                        n_blk * BN;
+#pragma unroll 1
+                    for (int col = 0; col < BN; col += 4) {
+                        float4 acc = __ldcg(reinterpret_cast<const float4*>(src + col));
+                        for (int s2 = 1; s2 < S; ++s2) {
+                            const float4 p = __ldcg(reinterpret_cast<const float4*>(src + (size_t)s2 * kTcBM * BN + col));
+                            acc.x += p.x;
+                            acc.y += p.y;
+                            acc.z += p.z;
+                            acc.w += p.w;
+                        }
+                        uint2 o;
+                        o.x = pack_bf16x2(acc.x, acc.y);
+                        o.y = pack_bf16x2(acc.z, acc.w);
+                        *reinterpret_cast<uint2*>(Cr + col) = o;
+                    }
+                }
             }
         }
     }

@@ -558,6 +558,11 @@ class ResNetStream:
         # DS_RESNET_TILES=1 keeps every GEMM on one-tile blocks)
         max_t = int(os.environ.get("DS_RESNET_TILES", "4")) if max_tiles is None else max_tiles
         fold_wide = os.environ.get("DS_RESNET_FOLD_WIDE", "1") != "0"
+        # split-K GEMMs with at most fuse_max splits fold inside the GEMM (the
+        # last-arriving split of each tile), each with a private workspace so
+        # its at-rest tickets are never overwritten by another GEMM's partials
+        fuse_max = int(os.environ.get("DS_RESNET_FUSE_FOLD", "0"))
+        self._fold_ws = []
         self.tiles = []
         for (name, M, N, K), (Mp, Np, Kp, bn, s) in zip(self.gemms, plans):
             tt = self._tuned_tiles.get(name, 0)
@@ -565,12 +570,18 @@ class ResNetStream:
             self.tiles.append((bn, T))
             # true extents: the TMA loads never read the tile padding (conv1's
             # K = 147 of 192, its 147 weight-gradient rows of 256, FC's 1000)
+            fuse = 1 < s <= fuse_max
+            ws_ptr = self.ws.data_ptr() if s > 1 else 0
+            if fuse:
+                w = torch.zeros(_abi.splitk_ws_elems(Mp, Np, bn, s) + _abi.fold_tickets(Mp, Np, bn), device=device)
+                self._fold_ws.append(w)
+                ws_ptr = w.data_ptr()
             ga = _abi.gemm_args(self.A.data_ptr(), self.B.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, bn=bn,
-                                splits=s, ws=self.ws.data_ptr() if s > 1 else 0, tiles=T,
+                                splits=s, ws=ws_ptr, tiles=T, fuse_fold=fuse,
                                 valid=None if os.environ.get("DS_RESNET_PADDED") else (M, N, K))
             self.records.append((f"resnet/{name}", _abi.BODY_GEMM_BF16, _abi.gemm_grid(Mp, Np, bn, s, T), ga,
                                  2.0 * M * N * K))
-            if s > 1:
+            if s > 1 and not fuse:
                 rows = _abi.fold_rows(Mp, Np, bn, WORKERS) if fold_wide else 16
                 ra, rg = _abi.splitk_reduce(self.ws.data_ptr(), self.C.data_ptr(), Mp, Np, Kp, 16, bn, s, rows)
                 self.records.append((f"resnet/{name}/fold", _abi.BODY_SPLITK_REDUCE, rg, ra, 0.0))

@@ -47,7 +47,7 @@ def test_args_struct_layout():
     assert ctypes.sizeof(_abi.SplitkReduceArgs) == 48
     # field offsets pinned by static_asserts in bodies/decode.cuh, gemm_tc.cuh and collective.cuh
     assert ctypes.sizeof(_abi.GemvArgs) == 400
-    want = {_abi.GemmArgs: {"K": 272, "bk": 296, "abandon": 304, "l2_hint": 308, "tiles": 312, "tmC": 320},
+    want = {_abi.GemmArgs: {"K": 272, "bk": 296, "abandon": 304, "l2_hint": 308, "tiles": 312, "fuse_fold": 316, "tmC": 320},
             _abi.SplitkReduceArgs: {"splits": 36, "rows": 40},
             _abi.GemvArgs: {"out": 256, "N": 320, "dbg": 360, "w_packed": 368, "bm": 376, "sk": 384, "pair": 388, "pf_ahead": 392},
             _abi.AttnArgs: {"q": 256, "L": 288, "scale": 300, "dbg": 304, "kbase": 312, "l2_pf_kb": 328, "tc": 332},

@@ -267,3 +267,41 @@ def test_gemm_valid_extents_read_no_padding(valid, bn, T):
     n8 = -(-n // 8) * 8  # TMA stores clip at 16-byte granularity
     assert bool((C[m:, :] == 7.0).all()) and bool((C[:, n8:] == 7.0).all())
     assert bool((C[:m, n:n8] == 0.0).all())
+
+
+@pytest.mark.parametrize("S", [2, 5, 8])
+def test_splitk_fused_fold_bit_identical_to_fold_launch(S):
+    """fuse_fold: the last-arriving split of each tile folds the S partials
+    in split order inside the GEMM launch -- the same bits as the separate
+    SPLITK_REDUCE launch, solo and as a coroutine under quota changes, and
+    repeatable (the tickets come back to rest)."""
+    M, N, K, bn = 512, 384, 64 * 8 * S, 128
+    A, B, C_ref = make(M, N, K, seed=11)
+    ws = torch.zeros(_abi.splitk_ws_elems(M, N, bn, S), device="cuda")
+    run_split(A, B, C_ref, M, N, K, bn, S, ws, rows=64)
+    wsf = torch.zeros(_abi.splitk_ws_elems(M, N, bn, S) + _abi.fold_tickets(M, N, bn), device="cuda")
+    grid = _abi.gemm_grid(M, N, bn, S)
+    for rep in range(2):
+        C = torch.zeros_like(C_ref)
+        args = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, bn=bn, splits=S, ws=wsf.data_ptr(),
+                              fuse_fold=True)
+        solo_launch(0, "gemm_ff", _abi.BODY_GEMM_BF16, grid, args)
+        torch.cuda.synchronize()
+        assert torch.equal(C.view(torch.int16), C_ref.view(torch.int16)), rep
+    C_co = torch.zeros_like(C_ref)
+    a_co = _abi.gemm_args(A.data_ptr(), B.data_ptr(), C_co.data_ptr(), M, N, K, bn=bn, splits=S, ws=wsf.data_ptr(),
+                          fuse_fold=True)
+    with Domain(0, block_log_capacity=0) as dom:
+        dom.start()
+        t = dom.tenant("train", _abi.BEST_EFFORT)
+        dom.quota_set(dom.mask(t, 0, dom.num_sms))
+        kid = dom.kernel("gemm_ff", _abi.BODY_GEMM_BF16, grid, a_co, phase=_abi.TRAINING)
+        dom.quota_at_claim(t, 0, grid[0] // 3, dom.mask(t, 8, 30))
+        dom.quota_at_claim(t, 0, 2 * grid[0] // 3, dom.mask(t, 0, dom.num_sms))
+        for _ in range(3):
+            s_last = dom.launch(t, kid)
+        dom.wait(t, s_last)
+    assert torch.equal(C_co.view(torch.int16), C_ref.view(torch.int16))
+    assert int(wsf[-_abi.fold_tickets(M, N, bn):].view(torch.int32).abs().sum()) == 0
+    with pytest.raises(_abi.DsError):
+        _abi.gemm_args(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, bn=bn, fuse_fold=True)

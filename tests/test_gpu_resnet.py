@@ -33,7 +33,7 @@ def _pick(rs):
             continue
         kinds.add(kind)
         group = [recs[i]]
-        if args.splits > 1:
+        if args.splits > 1 and not args.fuse_fold:
             group.append(recs[i + 1])
             assert recs[i + 1][1] == _abi.BODY_SPLITK_REDUCE
         out.append((kind, group))
