@@ -19,6 +19,8 @@
 //              launch slots into HBM rings, mirrors the control word.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "bodies/common.cuh"
 #include "bodies/reduce.cuh"
 #include "bodies/sgemm.cuh"
@@ -1092,16 +1094,22 @@ extern "C" cudaError_t ds_dev_launch_solo(int body, const void* args, uint32_t g
                                           uint32_t smem, cudaStream_t s) {
     // attributes set once per size (and the carveout pinned to max shared, the
     // configuration every tensor-core body needs), not per launch
-    static int cur_smem[64] = {0};  // per device: function attributes are per device context
+    // per device (function attributes are per device context); concurrent
+    // launchers at worst both set the same attributes
+    static std::atomic<int> cur_smem[64];
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0, cur_smem[0] = 0;
-    if ((int)smem > cur_smem[dev] || cur_smem[dev] == 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        dev = 0;
+        cur_smem[0].store(0);
+    }
+    const int have = cur_smem[dev].load(std::memory_order_relaxed);
+    if ((int)smem > have || have == 0) {
         cudaError_t e = cudaFuncSetAttribute(ds::ds_solo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(ds::ds_solo_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
-        cur_smem[dev] = (int)smem;
+        cur_smem[dev].store((int)smem, std::memory_order_relaxed);
     }
     ds::ds_solo_kernel<<<dim3(gx * gy * gz), dim3(ds::kBodyThreads), smem, s>>>(body, args, gx, gy, gz, smem);
     return cudaGetLastError();
